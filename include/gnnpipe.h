@@ -1,0 +1,249 @@
+/*
+ * gnnpipe.h — C-ABI of the B200 chunk-pipelined GNN training engine.
+ *
+ * Two layers, both plain C (extern "C", PODs, pointers + sizes, status codes):
+ *
+ *   gp_*  DEVICE ENGINE (libgpcuda.so, sm_100a). One gp_ctx per pipeline stage.
+ *         It replaces the per-worker body of the reference trainer
+ *         (proj/src/engines_impl.hpp:564-898) — the chunk loop, the per-row
+ *         kernels it calls (proj/include/gnnsim/nn.hpp:140-293, matrix.hpp:63-86),
+ *         the historical-embedding store (engines_impl.hpp:580-617, :671-679,
+ *         :735-782), the optimizer step (nn.hpp:456-490) and the stage messages
+ *         (engines_impl.hpp:690-724 -> fabric.cpp:288-359).
+ *
+ *   gs_*  HOST API (libgnnsim_b200.so, C++). Flat C wrappers over the C++ mirror
+ *         of the reference API (namespace gnnsim, csrc/include/gnnsim_b200.hpp):
+ *         build_graph, normalize_adjacency, generate_er, load/save_dataset,
+ *         make_chunks, partition_vertices, shuffle_chunk_order,
+ *         make_stage_assignment, build_layer_specs, init_params, and
+ *         train_pipeline / train_sequential. The C++ trainers call the gp_* ABI.
+ *
+ * Status codes map the reference's exception classes
+ * (std::invalid_argument, NumericError engines.hpp:48-51, FabricError
+ * fabric.hpp:139-142); gp_last_error()/gs_last_error() return the message.
+ * There is no CPU fallback: without a CUDA device gp_create fails with
+ * GP_ECUDA.
+ */
+#ifndef GNNPIPE_H
+#define GNNPIPE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GP_ABI_VERSION 1u
+
+typedef enum {
+    GP_OK = 0,
+    GP_EINVAL = 1,    /* std::invalid_argument in the reference            */
+    GP_ENUMERIC = 2,  /* gnnsim::NumericError (non-finite loss)            */
+    GP_EFABRIC = 3,   /* gnnsim::FabricError (transport / watchdog)        */
+    GP_ECUDA = 4,     /* CUDA or NCCL failure, or no device                */
+    GP_ERUNTIME = 5   /* anything else (std::runtime_error)                */
+} gp_status;
+
+/* Mirrors LayerKind (nn.hpp:16). SageConv is outside the hot-path scope
+ * and is rejected with GP_EINVAL. */
+typedef enum { GP_DENSE = 0, GP_GCNCONV = 1, GP_SAGECONV = 2, GP_GCN2CONV = 3 } gp_layer_kind;
+
+/* Mirrors LayerSpec (nn.hpp:32-44). */
+typedef struct {
+    uint32_t kind;    /* gp_layer_kind */
+    uint32_t in_dim;
+    uint32_t out_dim;
+    uint32_t relu;
+    double alpha;     /* Gcn2Conv only */
+    double beta;      /* Gcn2Conv only */
+} gp_layer_spec;
+
+/* What one stage worker of train_hybrid needs (engines_impl.hpp:564-617). */
+typedef struct {
+    int32_t device;              /* CUDA ordinal */
+    uint32_t num_vertices;       /* N (< 2^26)                                  */
+    uint32_t num_chunks;         /* K (1..64)                                   */
+    uint32_t num_stages;         /* S                                           */
+    uint32_t stage;              /* s                                           */
+    uint32_t layer_begin;        /* [lb, le) global layers owned by s           */
+    uint32_t layer_end;
+    uint32_t num_layers;         /* L                                           */
+    const gp_layer_spec* specs;  /* all L specs (copied)                        */
+    uint32_t hidden;             /* H = width of h0 (GCNII)                     */
+    uint32_t num_classes;        /* C                                           */
+    double dropout;              /* ModelConfig::dropout (nn.hpp:26)            */
+    uint64_t seed;               /* TrainOptions::seed                          */
+    uint32_t optimizer;          /* 0 Adam, 1 SGD (OptimizerKind nn.hpp:17)    */
+    double lr, beta1, beta2, eps;/* OptimizerConfig (nn.hpp:432-438)            */
+    uint32_t fix_alpha;          /* StalenessConfig (engines.hpp:28-33)         */
+    uint32_t historical_gradients;
+    uint32_t synchronous_mode;
+} gp_stage_config;
+
+typedef struct gp_ctx gp_ctx;
+
+/* Per-epoch results of one stage (gp_run_epoch). Quality fields are valid on
+ * the last stage only (SplitStats, engines_impl.hpp:29-37, :816-825). */
+typedef struct {
+    uint32_t epoch;
+    uint32_t has_quality;
+    double loss_sum;             /* sum of train-row xent in double            */
+    uint64_t correct[3];         /* train / val / test correct counts          */
+    uint64_t bytes_sent[6];      /* by MsgTag (fabric.hpp:14-21), 4 B/value    */
+    uint64_t msgs_sent[6];
+    float epoch_ms;              /* CUDA events on the stage compute stream    */
+    float busy_ms;               /* sum of this stage's kernel times (profiling) */
+    uint64_t kernel_launches;    /* kernels this stage launched in the epoch   */
+} gp_epoch_stats;
+
+/* Per-kernel-class device time (profiling mode), summed since last reset. */
+enum {
+    GP_K_REMASK = 0, GP_K_FWD_AGG = 1, GP_K_FWD_DENSE = 2, GP_K_BWD_AGG = 3,
+    GP_K_BWD_DENSE = 4, GP_K_XENT = 5, GP_K_PGRAD = 6, GP_K_OPTIM = 7,
+    GP_K_XFER = 8, GP_K_NUM = 9
+};
+typedef struct {
+    double ms[GP_K_NUM];         /* summed kernel durations (CUDA events)      */
+    uint64_t launches[GP_K_NUM];
+    double alg_bytes[GP_K_NUM];  /* algorithmic HBM bytes       */
+    double flops[GP_K_NUM];
+    double gather_bytes[GP_K_NUM]; /* bytes gathered through L2 by SpMMs        */
+} gp_profile;
+
+/* Buffers readable through gp_download (parity tests; original vertex order). */
+enum {
+    GP_BUF_H = 0,        /* h_cur[i]   layer output                 (N x out) */
+    GP_BUF_PRE = 1,      /* pre[i]     pre-transform rows           (N x k_in)*/
+    GP_BUF_DZ = 2,       /* dz[i]                                   (N x out) */
+    GP_BUF_DAGG = 3,     /* dagg[i] (unscaled)                      (N x k_in)*/
+    GP_BUF_DH0 = 4,      /* dh0_run                                 (N x H)   */
+    GP_BUF_HSNAP = 5,    /* h_snap[i]                               (N x out) */
+    GP_BUF_IN = 6,       /* in_cur (stage input)                    (N x in0) */
+    GP_BUF_DH_IN = 7,    /* dh_in  (gradient sent upstream)         (N x in0) */
+    GP_BUF_GATHER = 8    /* masked gather source of layer i         (N x in)  */
+};
+
+/* ---- lifecycle ---------------------------------------------------------- */
+uint32_t gp_abi_version(void);
+gp_status gp_create(const gp_stage_config* cfg, gp_ctx** out);
+void gp_destroy(gp_ctx* ctx);
+const char* gp_last_error(const gp_ctx* ctx); /* ctx may be NULL: thread-local */
+gp_status gp_device_count(int* out);
+
+/* ---- data (caller-owned host buffers, copied) ---------------------------- */
+/* Normalised adjacency (CsrMatrix<float>, graph.hpp:37-45 as produced by
+ * normalize_adjacency graph.cpp:68-98) and the chunk plan (ChunkPlan::chunk_of,
+ * partition.hpp:39-44). The engine renumbers vertices chunk-contiguously on
+ * device; neighbour order inside each row is preserved. */
+gp_status gp_upload_graph(gp_ctx* ctx, const uint64_t* offsets, const uint32_t* cols,
+                          const float* vals, uint64_t nnz, const uint32_t* chunk_of);
+/* Reuse another stage's device graph (same device) instead of a second copy. */
+gp_status gp_share_graph(gp_ctx* ctx, const gp_ctx* owner);
+/* Dataset::features (dataset.hpp:17) N x F row-major; stage 0 only. */
+gp_status gp_upload_features(gp_ctx* ctx, const float* x, uint32_t num_features);
+/* Dataset::labels / split (dataset.hpp:18-20); last stage only. */
+gp_status gp_upload_labels(gp_ctx* ctx, const uint32_t* labels, const uint8_t* split);
+/* LayerParams (nn.hpp:54-58): W k_in x out row-major, b out (NULL if none). */
+gp_status gp_set_layer_params(gp_ctx* ctx, uint32_t layer, const float* W, const float* b);
+gp_status gp_get_layer_params(gp_ctx* ctx, uint32_t layer, float* W, float* b);
+
+/* ---- transport (stage boundaries, engines_impl.hpp:690-724) -------------- */
+/* Same process: upstream stage s and downstream stage s+1 exchange chunk rows
+ * with device-to-device copies ordered by CUDA events (one host thread per
+ * stage, like Fabric::Mode::Concurrent fabric.cpp:401-422). */
+gp_status gp_link_local(gp_ctx* upstream, gp_ctx* downstream);
+/* One process per GPU: NCCL send/recv over NVLink. Each stage boundary is a
+ * 2-rank communicator (rank 0 = upstream stage). Pass NULL for a missing side. */
+gp_status gp_nccl_unique_id(uint8_t out[128]);
+gp_status gp_link_nccl(gp_ctx* ctx, const uint8_t* up_id, const uint8_t* down_id);
+/* Abort a blocked local transport (error propagation across stage threads). */
+void gp_abort(gp_ctx* ctx);
+
+/* ---- epochs -------------------------------------------------------------- */
+/* One epoch t (1-based) with the host-computed chunk order (shuffle_chunk_order
+ * partition.cpp:239-248, so schedule order stays bit-exact). Blocks until the
+ * stage's work for the epoch is complete. */
+gp_status gp_run_epoch(gp_ctx* ctx, uint32_t t, const uint32_t* order, gp_epoch_stats* out);
+
+/* ---- introspection / profiling ------------------------------------------ */
+gp_status gp_download(gp_ctx* ctx, uint32_t which, uint32_t local_layer, float* out,
+                      uint64_t count);
+gp_status gp_set_profiling(gp_ctx* ctx, int enable);
+gp_status gp_get_profile(gp_ctx* ctx, gp_profile* out);
+gp_status gp_reset_profile(gp_ctx* ctx);
+gp_status gp_device_bytes(gp_ctx* ctx, uint64_t* out); /* stash footprint */
+
+/* ====================== host API (libgnnsim_b200.so) ===================== */
+
+typedef struct gs_dataset gs_dataset;
+typedef struct gs_result gs_result;
+
+typedef struct {
+    uint32_t kind;        /* 0 gcn, 1 sage (rejected), 2 gcnii (ModelKind nn.hpp:15) */
+    uint32_t layers;
+    uint32_t hidden;
+    double dropout;
+    double gcnii_alpha;
+    double gcnii_lambda;
+    uint32_t self_loops;
+} gs_model_config;        /* ModelConfig nn.hpp:22-30 */
+
+typedef struct {
+    gs_model_config model;
+    uint32_t optimizer;   /* 0 Adam, 1 SGD */
+    double lr, beta1, beta2, eps;
+    uint32_t epochs;
+    uint64_t seed;
+    uint32_t shuffle_chunks, fix_alpha, historical_gradients, synchronous_mode;
+    int32_t device;       /* first CUDA device; stages are placed round-robin */
+    uint32_t profile;     /* collect per-kernel device times                  */
+} gs_train_options;       /* TrainOptions engines.hpp:69-77 */
+
+const char* gs_last_error(void);
+
+/* Graph / dataset (graph.cpp:33-66, :119-156; dataset.cpp:64-145). */
+int gs_dataset_from_edges(uint32_t n, const uint32_t* uv, uint64_t m, const float* x,
+                          uint32_t F, const uint32_t* labels, uint32_t C, const uint8_t* split,
+                          gs_dataset** out);
+int gs_dataset_synthetic_er(uint32_t n, double p, uint64_t graph_seed, uint32_t F, uint32_t C,
+                            uint64_t feature_seed, gs_dataset** out);
+int gs_dataset_load(const char* dir, gs_dataset** out);
+int gs_dataset_save(const gs_dataset* d, const char* dir);
+void gs_dataset_free(gs_dataset* d);
+int gs_dataset_shape(const gs_dataset* d, uint32_t* n, uint64_t* m, uint32_t* F, uint32_t* C);
+int gs_dataset_graph(const gs_dataset* d, uint64_t* offsets, uint32_t* neighbors,
+                     uint32_t* degrees);
+int gs_dataset_arrays(const gs_dataset* d, float* x, uint32_t* labels, uint8_t* split);
+int gs_normalize_adjacency(const gs_dataset* d, int self_loops, uint64_t* offsets,
+                           uint32_t* cols, float* vals);
+
+/* Partitioning and schedule (partition.cpp, engines.cpp:8-21). */
+int gs_make_chunks(const gs_dataset* d, uint32_t K, uint64_t seed, uint32_t* chunk_of);
+int gs_partition_vertices(const gs_dataset* d, uint32_t parts, uint64_t seed,
+                          uint32_t* assignment, uint64_t* edge_cut, uint64_t* boundary_total);
+int gs_shuffle_chunk_order(uint32_t K, uint64_t epoch, uint64_t seed, uint32_t* order);
+int gs_make_stage_assignment(uint32_t layers, uint32_t stages, uint32_t* ranges /* 2*S */);
+
+/* Model (nn.cpp:28-71, nn.hpp:60-72). */
+int gs_num_layers(const gs_model_config* m, uint32_t* L);
+int gs_build_layer_specs(const gs_model_config* m, uint32_t F, uint32_t C, gp_layer_spec* out);
+int gs_init_params(const gs_model_config* m, uint32_t F, uint32_t C, uint64_t seed,
+                   float* flat /* concat of W_l then b_l per layer */);
+
+/* Trainers (engines.hpp:79-99): run on the GPU through gp_*. */
+int gs_train_pipeline(const gs_dataset* d, const uint32_t* chunk_of, uint32_t K, uint32_t S,
+                      const gs_train_options* opt, gs_result** out);
+int gs_train_sequential(const gs_dataset* d, const gs_train_options* opt, gs_result** out);
+/* T x {epoch, train_loss, train_acc, val_acc, test_acc, wall_time_s, bubble_fraction} */
+int gs_result_metrics(const gs_result* r, uint32_t* epochs, double* metrics,
+                      uint64_t* comm /* T x {graph, pipeline, weightsync} */);
+int gs_result_params(const gs_result* r, float* flat);
+int gs_result_profile(const gs_result* r, gp_profile* out);
+int gs_result_peak_bytes(const gs_result* r, uint64_t* out);
+void gs_result_free(gs_result* r);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GNNPIPE_H */

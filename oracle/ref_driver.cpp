@@ -1,0 +1,479 @@
+// ref_driver — runs the UNMODIFIED reference (gnnsim, compiled from
+// /root/reference/proj/src by oracle/Makefile into oracle/_ref/) and dumps its
+// outputs as "blob" files (named, typed arrays) that the parity tests and the
+// golden-fixture generator read. TEST INFRASTRUCTURE ONLY: nothing in the
+// product imports, links or executes this.
+//
+// Sub-commands (key=value arguments):
+//   graph   spec=... out=...                 CSR, normalised adjacency, dataset arrays
+//   chunks  spec=... K=.. seed=.. out=...    make_chunks + partition_vertices(K)
+//   shuffle K=.. seed=.. epochs=.. out=...   shuffle_chunk_order for epochs 1..T
+//   forward spec=... model=.. layers=.. hidden=.. seed=.. epoch=.. out=...
+//                                            whole-graph forward+backward at one epoch
+//                                            with init params (layer_forward/backward)
+//   train   spec=... model=.. layers=.. hidden=.. S=.. K=.. chunk_seed=.. epochs=..
+//           seed=.. dropout=.. fix_alpha=.. shuffle=.. sync=.. hist=.. mode=seq|pipe
+//           out=...                           metrics + final params
+//   save    spec=... dir=...                 save_dataset (reference writer)
+//   bench   spec=... ...                     CPU baseline sample (see run_bench)
+//
+// Dataset spec strings:
+//   er:N:P:GSEED:F:C:FSEED   generate_er (graph.cpp:119-156) + hashed features
+//   sbm:B:BS:PIN:POUT:SEED   generate_sbm (dataset.cpp:147-191)
+//   g8:F:C                   the test_helpers.hpp:28-50 toy graph
+//   dir:PATH                 load_dataset (dataset.cpp:64-119)
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <map>
+#include <random>
+#include <sstream>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "gnnsim/engines.hpp"
+#include "gnnsim/partition.hpp"
+
+using namespace gnnsim;
+
+namespace {
+
+// ---- blob writer: [u32 nlen][name][u8 dtype][u8 ndim][u64 dims...][raw] ----
+struct Blob {
+    std::ofstream out;
+    explicit Blob(const std::string& path) : out(path, std::ios::binary | std::ios::trunc) {
+        if (!out) throw std::runtime_error("cannot write " + path);
+        out.write("GPBLOB01", 8);
+    }
+    void put(const std::string& name, uint8_t dtype, const std::vector<uint64_t>& dims,
+             const void* data, size_t bytes) {
+        uint32_t n = uint32_t(name.size());
+        out.write(reinterpret_cast<const char*>(&n), 4);
+        out.write(name.data(), n);
+        uint8_t nd = uint8_t(dims.size());
+        out.write(reinterpret_cast<const char*>(&dtype), 1);
+        out.write(reinterpret_cast<const char*>(&nd), 1);
+        for (uint64_t d : dims) out.write(reinterpret_cast<const char*>(&d), 8);
+        out.write(static_cast<const char*>(data), std::streamsize(bytes));
+    }
+    // dtype codes: 1=u8 2=u32 3=u64 4=f32 5=f64 6=i64
+    void u8(const std::string& n, const std::vector<uint8_t>& v) { put(n, 1, {v.size()}, v.data(), v.size()); }
+    void u32(const std::string& n, const std::vector<uint32_t>& v) { put(n, 2, {v.size()}, v.data(), v.size() * 4); }
+    void u64(const std::string& n, const std::vector<uint64_t>& v) { put(n, 3, {v.size()}, v.data(), v.size() * 8); }
+    void f32(const std::string& n, const std::vector<float>& v) { put(n, 4, {v.size()}, v.data(), v.size() * 4); }
+    void f64(const std::string& n, const std::vector<double>& v) { put(n, 5, {v.size()}, v.data(), v.size() * 8); }
+    void mat(const std::string& n, const MatF& m) {
+        put(n, 4, {m.rows(), m.cols()}, m.data(), m.size() * 4);
+    }
+};
+
+using Args = std::map<std::string, std::string>;
+
+std::string arg(const Args& a, const std::string& k, const std::string& def = "") {
+    auto it = a.find(k);
+    if (it == a.end()) {
+        if (def.empty()) throw std::invalid_argument("missing argument " + k);
+        return def;
+    }
+    return it->second;
+}
+uint64_t argu(const Args& a, const std::string& k, const std::string& def = "") {
+    return std::stoull(arg(a, k, def));
+}
+double argd(const Args& a, const std::string& k, const std::string& def = "") {
+    return std::stod(arg(a, k, def));
+}
+
+std::vector<std::string> split(const std::string& s, char c) {
+    std::vector<std::string> out;
+    std::stringstream ss(s);
+    std::string t;
+    while (std::getline(ss, t, c)) out.push_back(t);
+    return out;
+}
+
+// Synthetic node features / labels / split for generated graphs. The reference
+// has no generator at these shapes; this definition is shared
+// verbatim by the product (csrc/host/dataset.cpp) and the C oracle.
+void fill_hashed_features(Dataset& d, uint32_t F, uint32_t C, uint64_t fseed) {
+    const VertexId n = d.graph.num_vertices;
+    d.features = MatF(n, F);
+    for (uint64_t v = 0; v < n; ++v)
+        for (uint64_t j = 0; j < F; ++j)
+            d.features.at(v, j) = float(hash_unit(mix64(fseed, v * F + j)) * 2.0 - 1.0);
+    d.num_classes = C;
+    d.labels.resize(n);
+    d.split.resize(n);
+    for (uint64_t v = 0; v < n; ++v) {
+        d.labels[v] = uint32_t(mix64(fseed, 0x4C42ull, v) % C);
+        const uint64_t r = mix64(fseed, 0x5350ull, v) % 10;
+        d.split[v] = r < 6 ? 1 : (r < 8 ? 2 : 3);
+    }
+}
+
+Dataset make_dataset(const std::string& spec) {
+    auto p = split(spec, ':');
+    if (p.empty()) throw std::invalid_argument("empty spec");
+    if (p[0] == "er") {
+        if (p.size() != 7) throw std::invalid_argument("er:N:P:GSEED:F:C:FSEED");
+        Dataset d;
+        d.graph = generate_er(VertexId(std::stoul(p[1])), std::stod(p[2]), std::stoull(p[3]));
+        fill_hashed_features(d, uint32_t(std::stoul(p[4])), uint32_t(std::stoul(p[5])),
+                             std::stoull(p[6]));
+        d.validate();
+        return d;
+    }
+    if (p[0] == "sbm") {
+        if (p.size() != 6) throw std::invalid_argument("sbm:B:BS:PIN:POUT:SEED");
+        return generate_sbm(uint32_t(std::stoul(p[1])), uint32_t(std::stoul(p[2])),
+                            std::stod(p[3]), std::stod(p[4]), std::stoull(p[5]));
+    }
+    if (p[0] == "g8") {
+        // test_helpers.hpp:28-50
+        const uint32_t F = p.size() > 1 ? uint32_t(std::stoul(p[1])) : 2;
+        const uint32_t C = p.size() > 2 ? uint32_t(std::stoul(p[2])) : 2;
+        Dataset d;
+        d.graph = build_graph(8, {{0, 1}, {1, 2}, {2, 3}, {3, 4}, {4, 5}, {5, 6}, {6, 7}, {2, 5}});
+        d.features = MatF(8, F);
+        std::mt19937_64 eng(7);
+        std::uniform_real_distribution<float> u(-1.f, 1.f);
+        for (size_t i = 0; i < d.features.size(); ++i) d.features.data()[i] = u(eng);
+        d.num_classes = C;
+        d.labels.resize(8);
+        for (int v = 0; v < 8; ++v) d.labels[v] = uint32_t(v) % C;
+        d.split.assign(8, 1);
+        d.split[6] = 2;
+        d.split[7] = 3;
+        return d;
+    }
+    if (p[0] == "dir") return load_dataset(spec.substr(4));
+    throw std::invalid_argument("unknown spec kind " + p[0]);
+}
+
+ModelConfig model_from(const Args& a) {
+    ModelConfig m;
+    m.kind = parse_model_kind(arg(a, "model", "gcn"));
+    m.layers = uint32_t(argu(a, "layers", "2"));
+    m.hidden = uint32_t(argu(a, "hidden", "16"));
+    m.dropout = argd(a, "dropout", "0.5");
+    m.gcnii_alpha = argd(a, "alpha", "0.1");
+    m.gcnii_lambda = argd(a, "lambda", "0.5");
+    m.self_loops = argu(a, "self_loops", "1") != 0;
+    return m;
+}
+
+void dump_params(Blob& b, const std::string& prefix, const std::vector<LayerParams<float>>& ps) {
+    for (size_t l = 0; l < ps.size(); ++l) {
+        b.mat(prefix + "W" + std::to_string(l), ps[l].weight);
+        b.f32(prefix + "b" + std::to_string(l), ps[l].bias);
+    }
+}
+
+void cmd_graph(const Args& a) {
+    Dataset d = make_dataset(arg(a, "spec"));
+    Blob b(arg(a, "out"));
+    b.u64("csr_offsets", d.graph.csr_offsets);
+    b.u32("csr_neighbors", d.graph.csr_neighbors);
+    b.u32("degrees", d.graph.degrees);
+    b.u64("num_edges", {d.graph.num_edges});
+    auto m = normalize_adjacency<float>(d.graph, argu(a, "self_loops", "1") != 0);
+    b.u64("norm_offsets", m.offsets);
+    b.u32("norm_cols", m.cols);
+    b.f32("norm_vals", m.vals);
+    b.mat("features", d.features);
+    b.u32("labels", d.labels);
+    b.u8("split", d.split);
+    b.u32("num_classes", {d.num_classes});
+}
+
+void cmd_chunks(const Args& a) {
+    Dataset d = make_dataset(arg(a, "spec"));
+    const uint32_t K = uint32_t(argu(a, "K"));
+    const uint64_t seed = argu(a, "seed");
+    Blob b(arg(a, "out"));
+    ChunkPlan plan = make_chunks(d.graph, K, seed);
+    b.u32("chunk_of", plan.chunk_of);
+    Partition part = partition_vertices(d.graph, K, seed);
+    b.u32("assignment", part.assignment);
+    std::vector<uint64_t> bsizes;
+    std::vector<uint32_t> bflat;
+    for (const auto& bs : part.boundary_sets) {
+        bsizes.push_back(bs.size());
+        bflat.insert(bflat.end(), bs.begin(), bs.end());
+    }
+    b.u64("boundary_sizes", bsizes);
+    b.u32("boundary_flat", bflat);
+    b.u64("edge_cut", {part.edge_cut(d.graph)});
+}
+
+void cmd_shuffle(const Args& a) {
+    ChunkPlan plan;
+    plan.num_chunks = uint32_t(argu(a, "K"));
+    const uint64_t seed = argu(a, "seed");
+    const uint32_t T = uint32_t(argu(a, "epochs"));
+    std::vector<uint32_t> all;
+    for (uint32_t t = 1; t <= T; ++t) {
+        auto o = shuffle_chunk_order(plan, t, seed);
+        all.insert(all.end(), o.begin(), o.end());
+    }
+    Blob b(arg(a, "out"));
+    b.u32("orders", all);
+    std::vector<uint32_t> ranges;
+    for (uint32_t L : {1u, 3u, 8u, 16u, 64u})
+        for (uint32_t S = 1; S <= std::min(L, 8u); ++S) {
+            auto sa = make_stage_assignment(L, S);
+            for (auto [lo, hi] : sa.ranges) {
+                ranges.push_back(L);
+                ranges.push_back(S);
+                ranges.push_back(lo);
+                ranges.push_back(hi);
+            }
+        }
+    b.u32("stage_ranges", ranges);
+}
+
+// Whole-graph forward + backward at epoch `epoch` with freshly initialised
+// parameters, using the reference's whole-matrix ops (nn.hpp:297-361). This is
+// exactly train_sequential's first epoch (engines_impl.hpp:226-283) with the
+// per-layer activations exposed.
+void cmd_forward(const Args& a) {
+    Dataset d = make_dataset(arg(a, "spec"));
+    ModelConfig mc = model_from(a);
+    const uint64_t seed = argu(a, "seed", "1");
+    const uint64_t epoch = argu(a, "epoch", "1");
+    auto specs = build_layer_specs(mc, d.num_features(), d.num_classes);
+    auto params = init_params<float>(specs, seed);
+    auto adj = build_adj_bundle<float>(d.graph, mc.self_loops);
+    const uint32_t L = uint32_t(specs.size());
+    const VertexId n = d.num_vertices();
+    const bool needs_h0 = model_needs_h0(specs);
+    Blob b(arg(a, "out"));
+    dump_params(b, "init_", params);
+    std::vector<ForwardCache<float>> caches;
+    std::vector<DropMask<float>> masks;
+    for (uint32_t l = 0; l < L; ++l) {
+        masks.push_back(DropMask<float>::make(mc.dropout, seed, epoch, l, n, specs[l].in_dim));
+        const MatF& src = l == 0 ? d.features : caches[l - 1].out;
+        const MatF* h0 = needs_h0 && l > 0 ? &caches[0].out : nullptr;
+        caches.push_back(layer_forward(specs[l], params[l], adj, src, h0, masks[l]));
+        b.mat("pre" + std::to_string(l), caches[l].pre);
+        b.mat("h" + std::to_string(l), caches[l].out);
+    }
+    // Loss head on the training rows, as train_sequential does.
+    std::vector<uint8_t> train_mask = d.mask(Split::Train);
+    auto loss = softmax_xent(caches[L - 1].out, d.labels, train_mask);
+    b.f64("loss", {loss.loss});
+    b.mat("grad_logits", loss.grad_logits);
+    // Backward: reproduce train_sequential's loop (engines_impl.hpp:250-277),
+    // dumping dz/dagg/grad_in per layer and param grads.
+    std::vector<MatF> dz(L), dagg(L), dh(L);
+    for (uint32_t l = 0; l < L; ++l) {
+        dz[l] = MatF(n, specs[l].out_dim);
+        dagg[l] = MatF(n, specs[l].k_in());
+        dh[l] = MatF(n, specs[l].out_dim);
+    }
+    MatF dh0;
+    if (needs_h0) dh0 = MatF(n, mc.hidden);
+    dh[L - 1] = loss.grad_logits;
+    for (int l = int(L) - 1; l >= 0; --l) {
+        const auto& spec = specs[l];
+        if (l == 0 && needs_h0)
+            for (VertexId v = 0; v < n; ++v)
+                for (uint32_t j = 0; j < mc.hidden; ++j) dh[0].at(v, j) += dh0.at(v, j);
+        for (VertexId v = 0; v < n; ++v)
+            kernel::backward_out_row(spec, params[l], dh[l].row(v), caches[l].out.row(v),
+                                     dz[l].row(v), dagg[l].row(v),
+                                     needs_h0 && spec.kind == LayerKind::Gcn2Conv ? dh0.row(v)
+                                                                                  : nullptr);
+        if (l > 0)
+            for (VertexId u = 0; u < n; ++u)
+                kernel::backward_prev_row(spec, adj, u,
+                                          [&](VertexId v2) { return dagg[l].row(v2); },
+                                          dagg[l].row(u), masks[l], dh[l - 1].row(u));
+    }
+    auto rows = std::vector<VertexId>(n);
+    for (VertexId v = 0; v < n; ++v) rows[v] = v;
+    for (uint32_t l = 0; l < L; ++l) {
+        b.mat("dz" + std::to_string(l), dz[l]);
+        if (l > 0) b.mat("dagg" + std::to_string(l), dagg[l]);
+        b.mat("dh" + std::to_string(l), dh[l]);
+        auto g = param_grads_for_rows(specs[l], rows, caches[l].pre, dz[l]);
+        b.mat("gW" + std::to_string(l), g.weight);
+        b.f32("gb" + std::to_string(l), g.bias);
+    }
+    if (needs_h0) b.mat("dh0", dh0);
+}
+
+void cmd_train(const Args& a) {
+    Dataset d = make_dataset(arg(a, "spec"));
+    TrainOptions<float> opt;
+    opt.model = model_from(a);
+    opt.epochs = uint32_t(argu(a, "epochs", "1"));
+    opt.seed = argu(a, "seed", "1");
+    opt.optimizer.kind = arg(a, "optimizer", "adam") == "sgd" ? OptimizerKind::Sgd : OptimizerKind::Adam;
+    opt.optimizer.lr = argd(a, "lr", "0.001");
+    opt.staleness.shuffle_chunks = argu(a, "shuffle", "1") != 0;
+    opt.staleness.fix_alpha = uint32_t(argu(a, "fix_alpha", "10"));
+    opt.staleness.historical_gradients = argu(a, "hist", "0") != 0;
+    opt.staleness.synchronous_mode = argu(a, "sync", "0") != 0;
+    opt.fabric.mode = arg(a, "fabric", "det") == "conc" ? Fabric::Mode::Concurrent
+                                                        : Fabric::Mode::Deterministic;
+    const std::string mode = arg(a, "mode", "pipe");
+    TrainResult<float> res;
+    std::vector<uint32_t> chunk_of;
+    const auto t0 = std::chrono::steady_clock::now();
+    if (mode == "seq") {
+        res = train_sequential(d, opt);
+    } else {
+        const uint32_t S = uint32_t(argu(a, "S", "1"));
+        const uint32_t K = uint32_t(argu(a, "K", "1"));
+        const uint32_t G = uint32_t(argu(a, "G", "1"));
+        ChunkPlan plan = K == 1 ? chunk_plan_from_assignment(d.num_vertices(),
+                                                             std::vector<uint32_t>(d.num_vertices(), 0))
+                                : make_chunks(d.graph, K, argu(a, "chunk_seed", "1"));
+        chunk_of = plan.chunk_of;
+        const uint32_t L = uint32_t(build_layer_specs(opt.model, d.num_features(), d.num_classes).size());
+        auto sa = make_stage_assignment(L, S);
+        if (G == 1) {
+            res = train_pipeline(d, plan, sa, opt);
+        } else {
+            Partition part = partition_vertices(d.graph, G, argu(a, "part_seed", "1"));
+            GroupMap gmap = assign_groups(S * G, 4, S, G);
+            res = train_hybrid(d, part, plan, sa, gmap, opt);
+        }
+    }
+    const double secs =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    Blob b(arg(a, "out"));
+    std::vector<double> mt;
+    std::vector<uint64_t> comm;
+    for (const auto& m : res.metrics) {
+        mt.insert(mt.end(), {double(m.epoch), m.train_loss, m.train_acc, m.val_acc, m.test_acc});
+        comm.insert(comm.end(), {m.comm_bytes_graph, m.comm_bytes_pipeline, m.comm_bytes_weightsync});
+    }
+    b.f64("metrics", mt);
+    b.u64("comm", comm);
+    b.u32("chunk_of", chunk_of);
+    b.f64("seconds", {secs});
+    b.u64("peak_buffer_bytes", {res.peak_buffer_bytes});
+    dump_params(b, "", res.params);
+}
+
+void cmd_save(const Args& a) {
+    Dataset d = make_dataset(arg(a, "spec"));
+    save_dataset(d, arg(a, "dir"));
+}
+
+// CPU baseline sample (bench.py --impl reference / cpu_baseline). Times the
+// reference's own per-row kernels (nn.hpp:159-257, param_grads nn.hpp:269-293)
+// for one Gcn2Conv/GcnConv layer over a bounded row sample, split across T
+// threads (rows are independent: nn.hpp kernels are pure per row), and
+// extrapolates to a full epoch: per-row cost x N x aggregating layers plus the
+// measured dense layers. Reports seconds per epoch.
+void cmd_bench(const Args& a) {
+    Dataset d = make_dataset(arg(a, "spec"));
+    ModelConfig mc = model_from(a);
+    const uint32_t threads = uint32_t(argu(a, "threads", "1"));
+    const uint32_t sample = uint32_t(argu(a, "rows", "2000"));
+    const uint32_t steps = uint32_t(argu(a, "steps", "1"));
+    auto specs = build_layer_specs(mc, d.num_features(), d.num_classes);
+    auto params = init_params<float>(specs, 1);
+    auto adj = build_adj_bundle<float>(d.graph, mc.self_loops);
+    const VertexId n = d.num_vertices();
+    const uint32_t L = uint32_t(specs.size());
+    // pick the representative aggregating layer (index 1 for GCNII, 1 for GCN)
+    const uint32_t li = L > 1 ? 1 : 0;
+    const auto& sp = specs[li];
+    MatF h_prev(n, sp.in_dim), h0(n, mc.hidden), pre(n, sp.k_in()), out(n, sp.out_dim);
+    for (size_t i = 0; i < h_prev.size(); ++i) h_prev.data()[i] = float(hash_unit(mix64(3, i)) - 0.5);
+    for (size_t i = 0; i < h0.size(); ++i) h0.data()[i] = float(hash_unit(mix64(4, i)) - 0.5);
+    MatF dz(n, sp.out_dim), dagg(n, sp.k_in()), dprev(n, sp.in_dim), dh0(n, mc.hidden), dout(n, sp.out_dim);
+    for (size_t i = 0; i < dout.size(); ++i) dout.data()[i] = float(hash_unit(mix64(5, i)) - 0.5);
+    auto mask = DropMask<float>::make(mc.dropout, 1, 1, li, n, sp.in_dim);
+    // dense layers: first and last, timed the same way
+    std::vector<double> per_step;
+    const uint32_t stride = std::max<uint32_t>(1, n / sample);
+    std::vector<VertexId> rows;
+    for (VertexId v = 0; v < n && rows.size() < sample; v += stride) rows.push_back(v);
+    for (uint32_t s = 0; s < steps; ++s) {
+        const auto t0 = std::chrono::steady_clock::now();
+        std::vector<std::thread> pool;
+        for (uint32_t t = 0; t < threads; ++t)
+            pool.emplace_back([&, t]() {
+                for (size_t r = t; r < rows.size(); r += threads) {
+                    const VertexId v = rows[r];
+                    kernel::forward_row(sp, params[li], adj, v,
+                                        [&](VertexId u) { return h_prev.row(u); }, mask,
+                                        h0.row(v), pre.row(v), out.row(v));
+                    kernel::backward_out_row(sp, params[li], dout.row(v), out.row(v), dz.row(v),
+                                             dagg.row(v), sp.kind == LayerKind::Gcn2Conv ? dh0.row(v) : nullptr);
+                    kernel::backward_prev_row(sp, adj, v, [&](VertexId u) { return dagg.row(u); },
+                                              dagg.row(v), mask, dprev.row(v));
+                }
+            });
+        for (auto& th : pool) th.join();
+        // param grads over the sampled rows (the reference sums over all N at epoch end)
+        auto g = param_grads_for_rows(sp, rows, pre, dz);
+        (void)g;
+        const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        const double per_row = secs / double(rows.size());
+        uint32_t agg_layers = 0;
+        for (const auto& s2 : specs) agg_layers += s2.aggregates();
+        // dense layers cost (GCNII first/last) approximated by GEMV cost ratio
+        double dense_rel = 0;
+        for (const auto& s2 : specs)
+            if (!s2.aggregates())
+                dense_rel += double(s2.in_dim) * s2.out_dim * 3.0 /
+                             (double(sp.in_dim) * sp.out_dim * 3.0 + 2.0 * double(adj.norm.cols.size()) / n * sp.in_dim);
+        per_step.push_back(per_row * double(n) * (double(agg_layers) + dense_rel));
+    }
+    Blob b(arg(a, "out"));
+    b.f64("epoch_seconds", per_step);
+    b.u64("rows_sampled", {rows.size()});
+    b.u64("threads", {threads});
+    b.u64("nnz", {adj.norm.cols.size()});
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+    if (argc < 2) {
+        std::fprintf(stderr, "usage: ref_driver <cmd> key=value...\n");
+        return 2;
+    }
+    Args a;
+    for (int i = 2; i < argc; ++i) {
+        std::string s = argv[i];
+        auto eq = s.find('=');
+        if (eq == std::string::npos) {
+            std::fprintf(stderr, "bad argument %s\n", argv[i]);
+            return 2;
+        }
+        a[s.substr(0, eq)] = s.substr(eq + 1);
+    }
+    const std::string cmd = argv[1];
+    try {
+        if (cmd == "graph") cmd_graph(a);
+        else if (cmd == "chunks") cmd_chunks(a);
+        else if (cmd == "shuffle") cmd_shuffle(a);
+        else if (cmd == "forward") cmd_forward(a);
+        else if (cmd == "train") cmd_train(a);
+        else if (cmd == "save") cmd_save(a);
+        else if (cmd == "bench") cmd_bench(a);
+        else {
+            std::fprintf(stderr, "unknown command %s\n", cmd.c_str());
+            return 2;
+        }
+    } catch (const std::invalid_argument& e) {
+        std::fprintf(stderr, "invalid argument: %s\n", e.what());
+        return 2;
+    } catch (const std::exception& e) {
+        std::fprintf(stderr, "error: %s\n", e.what());
+        return 3;
+    }
+    return 0;
+}

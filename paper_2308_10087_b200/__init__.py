@@ -1,0 +1,593 @@
+"""B200-native chunk-pipelined full-graph GCN/GCNII training (GNNPipe, arXiv 2308.10087).
+
+Python mirror of the reference's public API for the hot path (proj/include/gnnsim/*.hpp),
+implemented over the in-tree C-ABI libraries:
+
+* ``lib/libgnnsim_b200.so`` — host C++ (bit-exact CSR / chunking / schedule / init) and
+  the trainers, exported as ``gs_*``;
+* ``lib/libgpcuda.so`` — the sm_100a stage engine, exported as ``gp_*``.
+
+Nothing here computes on the CPU: training goes through the CUDA engine and fails loudly
+(``GpuEngineError``) when the extension or a device is missing.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+__all__ = [
+    "GP_OK", "GP_EINVAL", "GP_ENUMERIC", "GP_EFABRIC", "GP_ECUDA", "GP_ERUNTIME",
+    "GnnsimError", "InvalidArgument", "NumericError", "FabricError", "GpuEngineError",
+    "LayerKind", "ModelKind", "ModelConfig", "TrainOptions", "TrainResult", "LayerSpec",
+    "Dataset", "make_chunks", "partition_vertices", "shuffle_chunk_order", "make_stage_assignment",
+    "build_layer_specs", "init_params", "train_pipeline", "train_sequential", "StageEngine",
+    "nccl_unique_id", "device_count", "lib_paths", "PROFILE_CLASSES",
+]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIBDIR = os.path.join(_HERE, "lib")
+
+GP_OK, GP_EINVAL, GP_ENUMERIC, GP_EFABRIC, GP_ECUDA, GP_ERUNTIME = 0, 1, 2, 3, 4, 5
+PROFILE_CLASSES = ["remask", "fwd_agg", "fwd_dense", "bwd_agg", "bwd_dense", "xent", "pgrad", "optim", "xfer"]
+GP_BUF = {"h": 0, "pre": 1, "dz": 2, "dagg": 3, "dh0": 4, "hsnap": 5, "in": 6, "dh_in": 7, "gather": 8}
+
+
+class GnnsimError(RuntimeError):
+    """Base error (std::runtime_error in the reference)."""
+
+
+class InvalidArgument(GnnsimError, ValueError):
+    """std::invalid_argument."""
+
+
+class NumericError(GnnsimError):
+    """gnnsim::NumericError (engines.hpp:48-51)."""
+
+
+class FabricError(GnnsimError):
+    """gnnsim::FabricError (fabric.hpp:139-142)."""
+
+
+class GpuEngineError(GnnsimError):
+    """CUDA / NCCL failure or missing device / extension."""
+
+
+_ERR = {GP_EINVAL: InvalidArgument, GP_ENUMERIC: NumericError, GP_EFABRIC: FabricError, GP_ECUDA: GpuEngineError}
+
+
+class LayerKind:
+    DENSE, GCNCONV, SAGECONV, GCN2CONV = 0, 1, 2, 3
+
+
+class ModelKind:
+    GCN, SAGE, GCNII = 0, 1, 2
+
+
+# ----------------------------------------------------------------------------- ctypes
+class gp_layer_spec(C.Structure):
+    _fields_ = [("kind", C.c_uint32), ("in_dim", C.c_uint32), ("out_dim", C.c_uint32), ("relu", C.c_uint32),
+                ("alpha", C.c_double), ("beta", C.c_double)]
+
+
+class gp_stage_config(C.Structure):
+    _fields_ = [("device", C.c_int32), ("num_vertices", C.c_uint32), ("num_chunks", C.c_uint32),
+                ("num_stages", C.c_uint32), ("stage", C.c_uint32), ("layer_begin", C.c_uint32),
+                ("layer_end", C.c_uint32), ("num_layers", C.c_uint32), ("specs", C.POINTER(gp_layer_spec)),
+                ("hidden", C.c_uint32), ("num_classes", C.c_uint32), ("dropout", C.c_double),
+                ("seed", C.c_uint64), ("optimizer", C.c_uint32), ("lr", C.c_double), ("beta1", C.c_double),
+                ("beta2", C.c_double), ("eps", C.c_double), ("fix_alpha", C.c_uint32),
+                ("historical_gradients", C.c_uint32), ("synchronous_mode", C.c_uint32)]
+
+
+class gp_epoch_stats(C.Structure):
+    _fields_ = [("epoch", C.c_uint32), ("has_quality", C.c_uint32), ("loss_sum", C.c_double),
+                ("correct", C.c_uint64 * 3), ("bytes_sent", C.c_uint64 * 6), ("msgs_sent", C.c_uint64 * 6),
+                ("epoch_ms", C.c_float), ("busy_ms", C.c_float), ("kernel_launches", C.c_uint64)]
+
+
+class gp_profile(C.Structure):
+    _fields_ = [("ms", C.c_double * 9), ("launches", C.c_uint64 * 9), ("alg_bytes", C.c_double * 9),
+                ("flops", C.c_double * 9), ("gather_bytes", C.c_double * 9)]
+
+
+class gs_model_config(C.Structure):
+    _fields_ = [("kind", C.c_uint32), ("layers", C.c_uint32), ("hidden", C.c_uint32), ("dropout", C.c_double),
+                ("gcnii_alpha", C.c_double), ("gcnii_lambda", C.c_double), ("self_loops", C.c_uint32)]
+
+
+class gs_train_options(C.Structure):
+    _fields_ = [("model", gs_model_config), ("optimizer", C.c_uint32), ("lr", C.c_double),
+                ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double), ("epochs", C.c_uint32),
+                ("seed", C.c_uint64), ("shuffle_chunks", C.c_uint32), ("fix_alpha", C.c_uint32),
+                ("historical_gradients", C.c_uint32), ("synchronous_mode", C.c_uint32), ("device", C.c_int32),
+                ("profile", C.c_uint32)]
+
+
+_lib = None
+
+
+def lib_paths() -> List[str]:
+    return [os.path.join(_LIBDIR, "libgnnsim_b200.so"), os.path.join(_LIBDIR, "libgpcuda.so")]
+
+
+def _L():
+    """Load the in-tree libraries (fails loudly: there is no CPU fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = lib_paths()[0]
+    if not os.path.exists(path):
+        raise GpuEngineError(f"{path} is missing: run __graft_entry__.build() (make -C paper_2308_10087_b200/csrc)")
+    lib = C.CDLL(path, mode=C.RTLD_GLOBAL)
+    P = C.POINTER
+    u32p, u64p, f32p, u8p, f64p = P(C.c_uint32), P(C.c_uint64), P(C.c_float), P(C.c_uint8), P(C.c_double)
+    vp = C.c_void_p
+    sig = {
+        "gs_last_error": (C.c_char_p, []),
+        "gs_dataset_from_edges": (C.c_int, [C.c_uint32, u32p, C.c_uint64, f32p, C.c_uint32, u32p, C.c_uint32, u8p, P(vp)]),
+        "gs_dataset_synthetic_er": (C.c_int, [C.c_uint32, C.c_double, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint64, P(vp)]),
+        "gs_dataset_load": (C.c_int, [C.c_char_p, P(vp)]),
+        "gs_dataset_save": (C.c_int, [vp, C.c_char_p]),
+        "gs_dataset_free": (None, [vp]),
+        "gs_dataset_shape": (C.c_int, [vp, u32p, u64p, u32p, u32p]),
+        "gs_dataset_graph": (C.c_int, [vp, u64p, u32p, u32p]),
+        "gs_dataset_arrays": (C.c_int, [vp, f32p, u32p, u8p]),
+        "gs_normalize_adjacency": (C.c_int, [vp, C.c_int, u64p, u32p, f32p]),
+        "gs_make_chunks": (C.c_int, [vp, C.c_uint32, C.c_uint64, u32p]),
+        "gs_partition_vertices": (C.c_int, [vp, C.c_uint32, C.c_uint64, u32p, u64p, u64p]),
+        "gs_shuffle_chunk_order": (C.c_int, [C.c_uint32, C.c_uint64, C.c_uint64, u32p]),
+        "gs_make_stage_assignment": (C.c_int, [C.c_uint32, C.c_uint32, u32p]),
+        "gs_num_layers": (C.c_int, [P(gs_model_config), u32p]),
+        "gs_build_layer_specs": (C.c_int, [P(gs_model_config), C.c_uint32, C.c_uint32, P(gp_layer_spec)]),
+        "gs_init_params": (C.c_int, [P(gs_model_config), C.c_uint32, C.c_uint32, C.c_uint64, f32p]),
+        "gs_train_pipeline": (C.c_int, [vp, u32p, C.c_uint32, C.c_uint32, P(gs_train_options), P(vp)]),
+        "gs_train_sequential": (C.c_int, [vp, P(gs_train_options), P(vp)]),
+        "gs_result_metrics": (C.c_int, [vp, u32p, f64p, u64p]),
+        "gs_result_params": (C.c_int, [vp, f32p]),
+        "gs_result_profile": (C.c_int, [vp, P(gp_profile)]),
+        "gs_result_peak_bytes": (C.c_int, [vp, u64p]),
+        "gs_result_free": (None, [vp]),
+        "gp_abi_version": (C.c_uint32, []),
+        "gp_device_count": (C.c_int, [P(C.c_int)]),
+        "gp_create": (C.c_int, [P(gp_stage_config), P(vp)]),
+        "gp_destroy": (None, [vp]),
+        "gp_last_error": (C.c_char_p, [vp]),
+        "gp_upload_graph": (C.c_int, [vp, u64p, u32p, f32p, C.c_uint64, u32p]),
+        "gp_share_graph": (C.c_int, [vp, vp]),
+        "gp_upload_features": (C.c_int, [vp, f32p, C.c_uint32]),
+        "gp_upload_labels": (C.c_int, [vp, u32p, u8p]),
+        "gp_set_layer_params": (C.c_int, [vp, C.c_uint32, f32p, f32p]),
+        "gp_get_layer_params": (C.c_int, [vp, C.c_uint32, f32p, f32p]),
+        "gp_link_local": (C.c_int, [vp, vp]),
+        "gp_nccl_unique_id": (C.c_int, [P(C.c_uint8)]),
+        "gp_link_nccl": (C.c_int, [vp, P(C.c_uint8), P(C.c_uint8)]),
+        "gp_abort": (None, [vp]),
+        "gp_run_epoch": (C.c_int, [vp, C.c_uint32, u32p, P(gp_epoch_stats)]),
+        "gp_download": (C.c_int, [vp, C.c_uint32, C.c_uint32, f32p, C.c_uint64]),
+        "gp_set_profiling": (C.c_int, [vp, C.c_int]),
+        "gp_get_profile": (C.c_int, [vp, P(gp_profile)]),
+        "gp_reset_profile": (C.c_int, [vp]),
+        "gp_device_bytes": (C.c_int, [vp, u64p]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def _ptr(a: np.ndarray, ct):
+    return a.ctypes.data_as(C.POINTER(ct))
+
+
+def _gs(rc: int) -> None:
+    if rc != GP_OK:
+        msg = (_L().gs_last_error() or b"").decode()
+        raise _ERR.get(rc, GnnsimError)(msg)
+
+
+def _gp(rc: int, ctx=None) -> None:
+    if rc != GP_OK:
+        msg = (_L().gp_last_error(ctx) or b"").decode()
+        raise _ERR.get(rc, GnnsimError)(msg)
+
+
+def device_count() -> int:
+    n = C.c_int(0)
+    _L().gp_device_count(C.byref(n))
+    return n.value
+
+
+# ----------------------------------------------------------------------------- model
+@dataclass
+class ModelConfig:
+    """ModelConfig (nn.hpp:22-30)."""
+    kind: int = ModelKind.GCN
+    layers: int = 2
+    hidden: int = 16
+    dropout: float = 0.5
+    gcnii_alpha: float = 0.1
+    gcnii_lambda: float = 0.5
+    self_loops: bool = True
+
+    def c(self) -> gs_model_config:
+        return gs_model_config(self.kind, self.layers, self.hidden, self.dropout, self.gcnii_alpha,
+                               self.gcnii_lambda, int(self.self_loops))
+
+
+@dataclass
+class TrainOptions:
+    """TrainOptions (engines.hpp:69-77) + StalenessConfig (:28-33) + OptimizerConfig (nn.hpp:432-438)."""
+    model: ModelConfig = field(default_factory=ModelConfig)
+    optimizer: str = "adam"
+    lr: float = 1e-3
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
+    epochs: int = 1
+    seed: int = 1
+    shuffle_chunks: bool = True
+    fix_alpha: int = 10
+    historical_gradients: bool = False
+    synchronous_mode: bool = False
+    device: int = 0
+    profile: bool = False
+
+    def c(self) -> gs_train_options:
+        return gs_train_options(self.model.c(), 1 if self.optimizer == "sgd" else 0, self.lr, self.beta1,
+                                self.beta2, self.eps, self.epochs, self.seed, int(self.shuffle_chunks),
+                                self.fix_alpha, int(self.historical_gradients), int(self.synchronous_mode),
+                                self.device, int(self.profile))
+
+
+@dataclass
+class LayerSpec:
+    kind: int
+    in_dim: int
+    out_dim: int
+    relu: bool
+    alpha: float
+    beta: float
+
+    @property
+    def has_bias(self) -> bool:
+        return self.kind != LayerKind.GCN2CONV
+
+    @property
+    def aggregates(self) -> bool:
+        return self.kind != LayerKind.DENSE
+
+
+def build_layer_specs(model: ModelConfig, in_features: int, num_classes: int) -> List[LayerSpec]:
+    """build_layer_specs (nn.cpp:28-64)."""
+    L = C.c_uint32()
+    _gs(_L().gs_num_layers(C.byref(model.c()), C.byref(L)))
+    arr = (gp_layer_spec * L.value)()
+    _gs(_L().gs_build_layer_specs(C.byref(model.c()), in_features, num_classes, arr))
+    return [LayerSpec(s.kind, s.in_dim, s.out_dim, bool(s.relu), s.alpha, s.beta) for s in arr]
+
+
+def _split_params(specs: Sequence[LayerSpec], flat: np.ndarray):
+    out, at = [], 0
+    for s in specs:
+        w = flat[at:at + s.in_dim * s.out_dim].reshape(s.in_dim, s.out_dim).copy()
+        at += s.in_dim * s.out_dim
+        b = flat[at:at + s.out_dim].copy() if s.has_bias else np.zeros(0, np.float32)
+        at += s.out_dim if s.has_bias else 0
+        out.append((w, b))
+    return out
+
+
+def _param_count(specs) -> int:
+    return sum(s.in_dim * s.out_dim + (s.out_dim if s.has_bias else 0) for s in specs)
+
+
+def init_params(model: ModelConfig, in_features: int, num_classes: int, seed: int):
+    """init_params (nn.hpp:60-72): list of (W [k_in x out], b) float32, bit-exact Glorot."""
+    specs = build_layer_specs(model, in_features, num_classes)
+    flat = np.zeros(_param_count(specs), np.float32)
+    _gs(_L().gs_init_params(C.byref(model.c()), in_features, num_classes, seed, _ptr(flat, C.c_float)))
+    return _split_params(specs, flat)
+
+
+# ----------------------------------------------------------------------------- dataset
+class Dataset:
+    """Dataset (dataset.hpp:15-29) held by the host library."""
+
+    def __init__(self, handle):
+        self._h = handle
+        n, m, F, Cc = C.c_uint32(), C.c_uint64(), C.c_uint32(), C.c_uint32()
+        _gs(_L().gs_dataset_shape(handle, C.byref(n), C.byref(m), C.byref(F), C.byref(Cc)))
+        self.num_vertices, self.num_edges, self.num_features, self.num_classes = n.value, m.value, F.value, Cc.value
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.gs_dataset_free(self._h)
+            self._h = None
+
+    @staticmethod
+    def from_edges(n: int, edges: np.ndarray, features: np.ndarray, labels: np.ndarray, num_classes: int,
+                   split: np.ndarray) -> "Dataset":
+        """build_graph (graph.cpp:33-66) over an arbitrary edge list + node data."""
+        e = np.ascontiguousarray(np.asarray(edges, np.uint32).reshape(-1, 2))
+        x = np.ascontiguousarray(features, np.float32).reshape(n, -1)
+        lab = np.ascontiguousarray(labels, np.uint32)
+        sp = np.ascontiguousarray(split, np.uint8)
+        h = C.c_void_p()
+        _gs(_L().gs_dataset_from_edges(n, _ptr(e, C.c_uint32), e.shape[0], _ptr(x, C.c_float), x.shape[1],
+                                       _ptr(lab, C.c_uint32), num_classes, _ptr(sp, C.c_uint8), C.byref(h)))
+        return Dataset(h)
+
+    @staticmethod
+    def synthetic_er(n: int, p: float, graph_seed: int, num_features: int, num_classes: int,
+                     feature_seed: int) -> "Dataset":
+        """generate_er (graph.cpp:119-156) + hashed features."""
+        h = C.c_void_p()
+        _gs(_L().gs_dataset_synthetic_er(n, p, graph_seed, num_features, num_classes, feature_seed, C.byref(h)))
+        return Dataset(h)
+
+    @staticmethod
+    def load(path: str) -> "Dataset":
+        """load_dataset (dataset.cpp:64-119)."""
+        h = C.c_void_p()
+        _gs(_L().gs_dataset_load(str(path).encode(), C.byref(h)))
+        return Dataset(h)
+
+    def save(self, path: str) -> None:
+        """save_dataset (dataset.cpp:121-145)."""
+        _gs(_L().gs_dataset_save(self._h, str(path).encode()))
+
+    def graph(self):
+        """(csr_offsets u64[N+1], csr_neighbors u32[2E], degrees u32[N])."""
+        off = np.zeros(self.num_vertices + 1, np.uint64)
+        nb = np.zeros(2 * self.num_edges, np.uint32)
+        dg = np.zeros(self.num_vertices, np.uint32)
+        _gs(_L().gs_dataset_graph(self._h, _ptr(off, C.c_uint64), _ptr(nb, C.c_uint32), _ptr(dg, C.c_uint32)))
+        return off, nb, dg
+
+    def arrays(self):
+        """(features f32[N,F], labels u32[N], split u8[N])."""
+        x = np.zeros((self.num_vertices, self.num_features), np.float32)
+        lab = np.zeros(self.num_vertices, np.uint32)
+        sp = np.zeros(self.num_vertices, np.uint8)
+        _gs(_L().gs_dataset_arrays(self._h, _ptr(x, C.c_float), _ptr(lab, C.c_uint32), _ptr(sp, C.c_uint8)))
+        return x, lab, sp
+
+    def normalize_adjacency(self, self_loops: bool = True):
+        """normalize_adjacency<float> (graph.cpp:68-98): (offsets u64, cols u32, vals f32)."""
+        nnz = 2 * self.num_edges + (self.num_vertices if self_loops else 0)
+        off = np.zeros(self.num_vertices + 1, np.uint64)
+        cols = np.zeros(nnz, np.uint32)
+        vals = np.zeros(nnz, np.float32)
+        _gs(_L().gs_normalize_adjacency(self._h, int(self_loops), _ptr(off, C.c_uint64), _ptr(cols, C.c_uint32),
+                                        _ptr(vals, C.c_float)))
+        return off, cols, vals
+
+
+def make_chunks(ds: Dataset, num_chunks: int, seed: int) -> np.ndarray:
+    """make_chunks (partition.cpp:213-224): chunk_of u32[N]."""
+    out = np.zeros(ds.num_vertices, np.uint32)
+    _gs(_L().gs_make_chunks(ds._h, num_chunks, seed, _ptr(out, C.c_uint32)))
+    return out
+
+
+def partition_vertices(ds: Dataset, num_parts: int, seed: int):
+    """partition_vertices (partition.cpp:191-198): (assignment, edge_cut, boundary_total)."""
+    out = np.zeros(ds.num_vertices, np.uint32)
+    cut, bt = C.c_uint64(), C.c_uint64()
+    _gs(_L().gs_partition_vertices(ds._h, num_parts, seed, _ptr(out, C.c_uint32), C.byref(cut), C.byref(bt)))
+    return out, cut.value, bt.value
+
+
+def shuffle_chunk_order(num_chunks: int, epoch: int, seed: int) -> np.ndarray:
+    """shuffle_chunk_order (partition.cpp:239-248)."""
+    out = np.zeros(num_chunks, np.uint32)
+    _gs(_L().gs_shuffle_chunk_order(num_chunks, epoch, seed, _ptr(out, C.c_uint32)))
+    return out
+
+
+def make_stage_assignment(layers: int, stages: int):
+    """make_stage_assignment (engines.cpp:8-21): list of [begin, end)."""
+    out = np.zeros(2 * stages, np.uint32)
+    _gs(_L().gs_make_stage_assignment(layers, stages, _ptr(out, C.c_uint32)))
+    return [(int(out[2 * s]), int(out[2 * s + 1])) for s in range(stages)]
+
+
+# ----------------------------------------------------------------------------- trainers
+@dataclass
+class TrainResult:
+    """TrainResult (engines.hpp:59-67)."""
+    metrics: np.ndarray          # T x [epoch, train_loss, train_acc, val_acc, test_acc, wall_time_s, bubble]
+    comm: np.ndarray             # T x [graph, pipeline, weightsync] bytes
+    params: list                 # [(W, b)]
+    profile: dict
+    peak_buffer_bytes: int
+
+    @property
+    def train_loss(self) -> np.ndarray:
+        return self.metrics[:, 1]
+
+
+def _result(h, specs) -> TrainResult:
+    lib = _L()
+    try:
+        T = C.c_uint32()
+        _gs(lib.gs_result_metrics(h, C.byref(T), None, None))
+        met = np.zeros((T.value, 7), np.float64)
+        comm = np.zeros((T.value, 3), np.uint64)
+        _gs(lib.gs_result_metrics(h, C.byref(T), _ptr(met, C.c_double), _ptr(comm, C.c_uint64)))
+        flat = np.zeros(_param_count(specs), np.float32)
+        _gs(lib.gs_result_params(h, _ptr(flat, C.c_float)))
+        pr = gp_profile()
+        _gs(lib.gs_result_profile(h, C.byref(pr)))
+        peak = C.c_uint64()
+        _gs(lib.gs_result_peak_bytes(h, C.byref(peak)))
+        prof = {name: {"ms": pr.ms[i], "launches": pr.launches[i], "alg_bytes": pr.alg_bytes[i],
+                       "flops": pr.flops[i], "gather_bytes": pr.gather_bytes[i]}
+                for i, name in enumerate(PROFILE_CLASSES)}
+        return TrainResult(met, comm, _split_params(specs, flat), prof, peak.value)
+    finally:
+        lib.gs_result_free(h)
+
+
+def train_pipeline(ds: Dataset, chunk_of: np.ndarray, num_stages: int, opt: TrainOptions) -> TrainResult:
+    """train_pipeline<float> (engines.hpp:89-92) on the GPU engine."""
+    co = np.ascontiguousarray(chunk_of, np.uint32)
+    K = int(co.max()) + 1 if co.size else 0
+    h = C.c_void_p()
+    _gs(_L().gs_train_pipeline(ds._h, _ptr(co, C.c_uint32), K, num_stages, C.byref(opt.c()), C.byref(h)))
+    return _result(h, build_layer_specs(opt.model, ds.num_features, ds.num_classes))
+
+
+def train_sequential(ds: Dataset, opt: TrainOptions) -> TrainResult:
+    """train_sequential<float> (engines.hpp:79-81): the S=1, K=1 pipeline on the GPU."""
+    h = C.c_void_p()
+    _gs(_L().gs_train_sequential(ds._h, C.byref(opt.c()), C.byref(h)))
+    return _result(h, build_layer_specs(opt.model, ds.num_features, ds.num_classes))
+
+
+# ----------------------------------------------------------------------------- stage engine
+def nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    _gp(_L().gp_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+class StageEngine:
+    """One pipeline stage on one GPU, driven directly through the gp_* C-ABI."""
+
+    def __init__(self, *, num_vertices: int, num_chunks: int, specs: Sequence[LayerSpec], stage: int,
+                 num_stages: int, layer_range, hidden: int, num_classes: int, dropout: float, seed: int,
+                 lr: float = 1e-3, optimizer: str = "adam", fix_alpha: int = 10,
+                 historical_gradients: bool = False, synchronous_mode: bool = False, device: int = 0,
+                 beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8):
+        self.specs = list(specs)
+        self._specs_c = (gp_layer_spec * len(specs))(*[
+            gp_layer_spec(s.kind, s.in_dim, s.out_dim, int(s.relu), s.alpha, s.beta) for s in specs])
+        cfg = gp_stage_config()
+        cfg.device = device
+        cfg.num_vertices = num_vertices
+        cfg.num_chunks = num_chunks
+        cfg.num_stages = num_stages
+        cfg.stage = stage
+        cfg.layer_begin, cfg.layer_end = layer_range
+        cfg.num_layers = len(specs)
+        cfg.specs = self._specs_c
+        cfg.hidden = hidden
+        cfg.num_classes = num_classes
+        cfg.dropout = dropout
+        cfg.seed = seed
+        cfg.optimizer = 1 if optimizer == "sgd" else 0
+        cfg.lr, cfg.beta1, cfg.beta2, cfg.eps = lr, beta1, beta2, eps
+        cfg.fix_alpha = fix_alpha
+        cfg.historical_gradients = int(historical_gradients)
+        cfg.synchronous_mode = int(synchronous_mode)
+        self.n, self.K, self.stage, self.S = num_vertices, num_chunks, stage, num_stages
+        self.layer_range = tuple(layer_range)
+        self.hidden = hidden
+        h = C.c_void_p()
+        rc = _L().gp_create(C.byref(cfg), C.byref(h))
+        if rc != GP_OK:
+            raise _ERR.get(rc, GnnsimError)((_L().gp_last_error(None) or b"").decode())
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _L().gp_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def upload_graph(self, offsets, cols, vals, chunk_of):
+        off = np.ascontiguousarray(offsets, np.uint64)
+        c = np.ascontiguousarray(cols, np.uint32)
+        v = np.ascontiguousarray(vals, np.float32)
+        co = np.ascontiguousarray(chunk_of, np.uint32)
+        _gp(_L().gp_upload_graph(self._h, _ptr(off, C.c_uint64), _ptr(c, C.c_uint32), _ptr(v, C.c_float),
+                                 c.size, _ptr(co, C.c_uint32)), self._h)
+
+    def share_graph(self, owner: "StageEngine"):
+        _gp(_L().gp_share_graph(self._h, owner._h), self._h)
+
+    def upload_features(self, x):
+        x = np.ascontiguousarray(x, np.float32)
+        _gp(_L().gp_upload_features(self._h, _ptr(x, C.c_float), x.shape[1]), self._h)
+
+    def upload_labels(self, labels, split):
+        lab = np.ascontiguousarray(labels, np.uint32)
+        sp = np.ascontiguousarray(split, np.uint8)
+        _gp(_L().gp_upload_labels(self._h, _ptr(lab, C.c_uint32), _ptr(sp, C.c_uint8)), self._h)
+
+    def set_params(self, layer: int, W, b=None):
+        W = np.ascontiguousarray(W, np.float32)
+        bp = None
+        if b is not None and np.size(b):
+            b = np.ascontiguousarray(b, np.float32)
+            bp = _ptr(b, C.c_float)
+        _gp(_L().gp_set_layer_params(self._h, layer, _ptr(W, C.c_float), bp), self._h)
+
+    def get_params(self, layer: int):
+        s = self.specs[layer]
+        W = np.zeros((s.in_dim, s.out_dim), np.float32)
+        b = np.zeros(s.out_dim if s.has_bias else 0, np.float32)
+        _gp(_L().gp_get_layer_params(self._h, layer, _ptr(W, C.c_float), _ptr(b, C.c_float) if b.size else None),
+            self._h)
+        return W, b
+
+    def link_local(self, downstream: "StageEngine"):
+        _gp(_L().gp_link_local(self._h, downstream._h), downstream._h)
+
+    def link_nccl(self, up_id: Optional[bytes], down_id: Optional[bytes]):
+        up = (C.c_uint8 * 128).from_buffer_copy(up_id) if up_id else None
+        down = (C.c_uint8 * 128).from_buffer_copy(down_id) if down_id else None
+        _gp(_L().gp_link_nccl(self._h, up, down), self._h)
+
+    def abort(self):
+        _L().gp_abort(self._h)
+
+    def run_epoch(self, t: int, order) -> gp_epoch_stats:
+        o = np.ascontiguousarray(order, np.uint32)
+        st = gp_epoch_stats()
+        _gp(_L().gp_run_epoch(self._h, t, _ptr(o, C.c_uint32), C.byref(st)), self._h)
+        return st
+
+    def download(self, which: str, local_layer: int = 0) -> np.ndarray:
+        lo, hi = self.layer_range
+        if which in ("h", "dz", "hsnap"):
+            width = self.specs[lo + local_layer].out_dim
+        elif which in ("pre", "dagg", "gather"):
+            width = self.specs[lo + local_layer].in_dim
+        elif which == "dh0":
+            width = self.hidden
+        else:
+            width = self.specs[lo].in_dim
+        out = np.zeros((self.n, width), np.float32)
+        _gp(_L().gp_download(self._h, GP_BUF[which], local_layer, _ptr(out, C.c_float), out.size), self._h)
+        return out
+
+    def set_profiling(self, on: bool = True):
+        _L().gp_set_profiling(self._h, int(on))
+
+    def reset_profile(self):
+        _L().gp_reset_profile(self._h)
+
+    def profile(self) -> dict:
+        pr = gp_profile()
+        _L().gp_get_profile(self._h, C.byref(pr))
+        return {name: {"ms": pr.ms[i], "launches": pr.launches[i], "alg_bytes": pr.alg_bytes[i],
+                       "flops": pr.flops[i], "gather_bytes": pr.gather_bytes[i]}
+                for i, name in enumerate(PROFILE_CLASSES)}
+
+    def device_bytes(self) -> int:
+        v = C.c_uint64()
+        _L().gp_device_bytes(self._h, C.byref(v))
+        return v.value

@@ -1,0 +1,1360 @@
+// Stage engine: the device-resident state and epoch schedule of one pipeline
+// stage, exported through the gp_* C-ABI (include/gnnpipe.h).
+//
+// Reference mapping (proj/src/engines_impl.hpp, train_hybrid's worker body):
+//   stash allocation  :580-612  -> Stage::alloc()
+//   snapshot          :671-679  -> pointer swaps in run_epoch()
+//   dropout masks     :681-683  -> DropKey per (t, l), hashed on device
+//   forward chunk loop:784-814  -> run_epoch() forward section
+//   metrics           :816-825  -> k_xent_stats / k_xent_fold
+//   backward loop     :827-870  -> run_epoch() backward section
+//   param grads + step:872-878  -> k_pgrad_* + k_adam
+//   stage messages    :690-724  -> Transport (local D2D or NCCL)
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <condition_variable>
+#include <cstring>
+#include <deque>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../../include/gnnpipe.h"
+#include "kernels.cuh"
+
+namespace gp {
+namespace {
+
+thread_local std::string g_tls_error;
+
+struct Error : std::runtime_error {
+    gp_status code;
+    Error(gp_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define GP_CUDA(expr)                                                                       \
+    do {                                                                                    \
+        cudaError_t _e = (expr);                                                            \
+        if (_e != cudaSuccess)                                                              \
+            throw ::gp::Error(GP_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));      \
+    } while (0)
+
+inline uint32_t pad8(uint32_t d) { return (d + 7u) & ~7u; }
+
+// ------------------------------------------------------------------ NCCL (dlopen)
+// NCCL is resolved at run time so single-GPU use never depends on it and the
+// process shares whichever libnccl.so.2 torch may already have loaded.
+struct NcclApi {
+    typedef int (*GetUniqueId)(void*);
+    typedef int (*CommInitRank)(void**, int, const void*, int);  // id passed by value (128 B)
+    typedef int (*CommDestroy)(void*);
+    typedef int (*SendRecv)(const void*, size_t, int, int, void*, cudaStream_t);
+    typedef int (*Group)();
+    typedef const char* (*ErrStr)(int);
+    void* h = nullptr;
+    GetUniqueId get_unique_id = nullptr;
+    void* comm_init_rank = nullptr;
+    CommDestroy comm_destroy = nullptr;
+    SendRecv send = nullptr;
+    void* recv = nullptr;
+    Group group_start = nullptr, group_end = nullptr;
+    ErrStr err = nullptr;
+    bool load() {
+        if (h) return true;
+        h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) return false;
+        get_unique_id = (GetUniqueId)dlsym(h, "ncclGetUniqueId");
+        comm_init_rank = dlsym(h, "ncclCommInitRank");
+        comm_destroy = (CommDestroy)dlsym(h, "ncclCommDestroy");
+        send = (SendRecv)dlsym(h, "ncclSend");
+        recv = dlsym(h, "ncclRecv");
+        group_start = (Group)dlsym(h, "ncclGroupStart");
+        group_end = (Group)dlsym(h, "ncclGroupEnd");
+        err = (ErrStr)dlsym(h, "ncclGetErrorString");
+        return get_unique_id && comm_init_rank && comm_destroy && send && recv && group_start &&
+               group_end;
+    }
+};
+NcclApi g_nccl;
+
+struct NcclId {
+    char b[128];
+};
+typedef int (*NcclInitFn)(void**, int, NcclId, int);
+typedef int (*NcclRecvFn)(void*, size_t, int, int, void*, cudaStream_t);
+constexpr int kNcclFloat = 7;  // ncclFloat32
+
+void nccl_check(int r, const char* what) {
+    if (r != 0)
+        throw Error(GP_ECUDA, std::string(what) + ": " + (g_nccl.err ? g_nccl.err(r) : "nccl error"));
+}
+
+// ------------------------------------------------------------------ transport
+struct Piece {
+    float* ptr;
+    size_t floats;
+};
+
+struct Stage;
+
+// One direction of one stage boundary inside a process: FIFO of posted chunk
+// sends (the reference channel (src,dst,tag) is a FIFO deque, fabric.cpp:190).
+struct LocalQueue {
+    struct Msg {
+        uint32_t chunk;
+        cudaEvent_t ready;
+        std::vector<Piece> src;
+        int device;
+    };
+    std::mutex mu;
+    std::condition_variable cv;
+    std::deque<Msg> q;
+    bool aborted = false;
+};
+
+struct LocalLink {
+    LocalQueue fwd, bwd;
+};
+
+struct Transport {
+    // Forward: upstream stage sends chunk rows of its last layer (+h0).
+    std::shared_ptr<LocalLink> up_local, down_local;  // links to s-1 and s+1
+    void* up_comm = nullptr;                          // NCCL 2-rank comms
+    void* down_comm = nullptr;
+    cudaStream_t up_stream = nullptr, down_stream = nullptr;
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_next = 0;
+};
+
+// ------------------------------------------------------------------ stage
+struct LayerDev {
+    gp_layer_spec spec;
+    uint32_t l;          // global layer id
+    uint32_t din, dout;  // in_dim, out_dim (k_in == in_dim: no SageConv)
+    uint32_t sin, sout;  // padded strides
+    bool agg;
+    float *W = nullptr, *b = nullptr, *gW = nullptr, *gb = nullptr;
+    float *mW = nullptr, *vW = nullptr, *mb = nullptr, *vb = nullptr;
+    float *h = nullptr, *hs = nullptr;   // h_cur / h_snap
+    float *pre = nullptr, *dz = nullptr;
+    float *G = nullptr;                  // masked gather source (input of this layer)
+    float *bg = nullptr, *bgs = nullptr; // backward gather source (+ snapshot, hist mode)
+};
+
+struct Stage {
+    gp_stage_config cfg{};
+    std::vector<gp_layer_spec> specs;
+    uint32_t n = 0, K = 0, S = 1, s = 0, lb = 0, le = 0, len = 0, H = 0, C = 0;
+    bool first = true, last = true, needs_h0 = false, sync = false, hist = false;
+    int device = 0;
+    std::string err;
+    cudaStream_t cs = nullptr;
+    std::vector<LayerDev> L;
+
+    // graph (renumbered chunk-contiguous)
+    std::shared_ptr<void> graph_owner;
+    uint64_t* rowptr = nullptr;
+    uint2* edges = nullptr;
+    uint32_t* orig = nullptr;          // new -> original id (device)
+    std::vector<uint32_t> perm;        // original -> new (host)
+    std::vector<uint32_t> inv;         // new -> original (host)
+    std::vector<uint32_t> cstart;      // chunk row ranges (host), K+1
+    uint64_t nnz = 0;
+    bool graph_ready = false;
+
+    // stage-level buffers
+    float* x0 = nullptr;               // features (stage 0)
+    uint32_t F = 0, sx = 0;
+    float *in_cur = nullptr, *in_snap = nullptr;  // stage input (s > 0)
+    uint32_t in0 = 0, sin0 = 0;
+    float* h0 = nullptr;               // received h0 (s > 0, GCNII)
+    float* dh0 = nullptr;              // dh0_run (GCNII)
+    float* dtop = nullptr;             // incoming gradient of the last local layer
+    float* dh_in = nullptr;            // gradient sent upstream (s > 0)
+    uint32_t* labels = nullptr;
+    uint8_t* split = nullptr;
+    float inv_train = 0.f;
+    bool labels_ready = false, x_ready = false;
+    float* ws = nullptr;               // pgrad workspace
+    float* wsb = nullptr;
+    uint32_t splits = 1;
+    double* part_loss = nullptr;
+    unsigned long long* part_correct = nullptr;
+    double* red_loss = nullptr;
+    unsigned long long* red_correct = nullptr;
+    uint32_t xent_blocks = 0;
+    uint64_t step = 0;
+    uint32_t last_epoch = 0;
+    uint64_t dev_bytes = 0;
+    std::vector<void*> allocs;
+
+    Transport tr;
+    // profiling
+    bool profiling = false;
+    gp_profile prof{};
+    struct Timed {
+        int cls;
+        cudaEvent_t a, b;
+        double bytes, flops, gather;
+    };
+    std::vector<Timed> timed;
+    std::vector<cudaEvent_t> ev_free;
+    uint64_t launches = 0;
+    cudaEvent_t ev_start = nullptr, ev_end = nullptr;
+    int num_sms = 148;
+    int occ_fwd = 4, occ_bwd = 4, occ_row = 8;
+    std::atomic<bool> aborted{false};
+
+    // ---- memory -----------------------------------------------------------
+    template <typename T>
+    T* dalloc(size_t count, bool zero = true) {
+        void* p = nullptr;
+        const size_t bytes = std::max<size_t>(count * sizeof(T), 16);
+        GP_CUDA(cudaMalloc(&p, bytes));
+        if (zero) GP_CUDA(cudaMemset(p, 0, bytes));
+        allocs.push_back(p);
+        dev_bytes += bytes;
+        return static_cast<T*>(p);
+    }
+
+    ~Stage() {
+        if (device >= 0) cudaSetDevice(device);
+        if (cs) cudaStreamSynchronize(cs);
+        for (void* p : allocs) cudaFree(p);
+        for (auto& t : timed) {
+            cudaEventDestroy(t.a);
+            cudaEventDestroy(t.b);
+        }
+        for (auto e : ev_free) cudaEventDestroy(e);
+        for (auto e : tr.ev_pool) cudaEventDestroy(e);
+        if (ev_start) cudaEventDestroy(ev_start);
+        if (ev_end) cudaEventDestroy(ev_end);
+        if (tr.up_comm) g_nccl.comm_destroy(tr.up_comm);
+        if (tr.down_comm) g_nccl.comm_destroy(tr.down_comm);
+        if (tr.up_stream) cudaStreamDestroy(tr.up_stream);
+        if (tr.down_stream) cudaStreamDestroy(tr.down_stream);
+        if (cs) cudaStreamDestroy(cs);
+    }
+
+    // ---- configuration ------------------------------------------------------
+    void init(const gp_stage_config& c) {
+        cfg = c;
+        if (!c.specs || c.num_layers == 0) throw Error(GP_EINVAL, "gp_create: no layer specs");
+        specs.assign(c.specs, c.specs + c.num_layers);
+        cfg.specs = nullptr;
+        n = c.num_vertices;
+        K = c.num_chunks;
+        S = c.num_stages;
+        s = c.stage;
+        lb = c.layer_begin;
+        le = c.layer_end;
+        H = c.hidden;
+        C = c.num_classes;
+        if (n == 0 || n > kColMask) throw Error(GP_EINVAL, "num_vertices must be in [1, 2^26)");
+        if (K == 0 || K > kMaxChunks || K > n)
+            throw Error(GP_EINVAL, "num_chunks must be in [1, min(64, N)]");
+        if (S == 0 || s >= S) throw Error(GP_EINVAL, "bad stage index");
+        if (lb >= le || le > c.num_layers) throw Error(GP_EINVAL, "bad layer range");
+        if (c.dropout >= 1.0) throw Error(GP_EINVAL, "dropout rate must be < 1");
+        len = le - lb;
+        first = s == 0;
+        last = s + 1 == S;
+        sync = c.synchronous_mode != 0;
+        hist = c.historical_gradients != 0 && !sync;
+        needs_h0 = false;
+        for (const auto& sp : specs) {
+            if (sp.kind == GP_SAGECONV)
+                throw Error(GP_EINVAL, "SageConv is not supported by the GPU engine");
+            if (sp.kind > GP_GCN2CONV) throw Error(GP_EINVAL, "unknown layer kind");
+            if (sp.kind == GP_GCN2CONV) needs_h0 = true;
+        }
+        if (first != (lb == 0)) throw Error(GP_EINVAL, "stage 0 must own layer 0");
+        if (last != (le == c.num_layers)) throw Error(GP_EINVAL, "last stage must own layer L-1");
+        for (uint32_t l = lb; l < le; ++l) {
+            const auto& sp = specs[l];
+            if (sp.out_dim == 0 || sp.out_dim > kMaxWidth)
+                throw Error(GP_EINVAL, "layer output width must be in [1, 128]");
+            if (l > 0 && sp.in_dim > kMaxWidth)
+                throw Error(GP_EINVAL, "hidden width must be <= 128");
+            if (sp.kind == GP_GCN2CONV && sp.in_dim != sp.out_dim)
+                throw Error(GP_EINVAL, "Gcn2Conv needs in_dim == out_dim");
+        }
+        if (needs_h0 && (H == 0 || H > kMaxWidth)) throw Error(GP_EINVAL, "bad hidden width");
+        device = c.device;
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+            throw Error(GP_ECUDA, "no CUDA device (the GPU engine has no CPU fallback)");
+        if (device < 0 || device >= ndev) throw Error(GP_EINVAL, "bad device ordinal");
+        GP_CUDA(cudaSetDevice(device));
+        GP_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, device));
+        GP_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        GP_CUDA(cudaEventCreate(&ev_start));
+        GP_CUDA(cudaEventCreate(&ev_end));
+        alloc();
+        setup_kernels();
+    }
+
+    void alloc() {
+        in0 = specs[lb].in_dim;
+        sin0 = pad8(in0);
+        L.resize(len);
+        for (uint32_t i = 0; i < len; ++i) {
+            auto& d = L[i];
+            d.spec = specs[lb + i];
+            d.l = lb + i;
+            d.din = d.spec.in_dim;
+            d.dout = d.spec.out_dim;
+            d.sin = pad8(d.din);
+            d.sout = pad8(d.dout);
+            d.agg = d.spec.kind != GP_DENSE;
+            const bool bias = d.spec.kind != GP_GCN2CONV;
+            const size_t wn = size_t(d.din) * d.dout;
+            d.W = dalloc<float>(wn);
+            d.gW = dalloc<float>(wn);
+            d.mW = dalloc<float>(wn);
+            d.vW = dalloc<float>(wn);
+            if (bias) {
+                d.b = dalloc<float>(d.dout);
+                d.gb = dalloc<float>(d.dout);
+                d.mb = dalloc<float>(d.dout);
+                d.vb = dalloc<float>(d.dout);
+            }
+            d.h = dalloc<float>(size_t(n) * d.sout);
+            d.pre = dalloc<float>(size_t(n) * d.sin);
+            d.dz = dalloc<float>(size_t(n) * d.sout);
+            if (d.agg) d.G = dalloc<float>(size_t(n) * d.sin);
+            if (!sync && i + 1 < len && specs[lb + i + 1].kind != GP_DENSE)
+                d.hs = dalloc<float>(size_t(n) * d.sout);
+            if (d.l > 0) {
+                d.bg = dalloc<float>(size_t(n) * d.sin);
+                if (hist && d.agg) d.bgs = dalloc<float>(size_t(n) * d.sin);
+            }
+        }
+        if (!first) {
+            in_cur = dalloc<float>(size_t(n) * sin0);
+            if (!sync && L[0].agg) in_snap = dalloc<float>(size_t(n) * sin0);
+            dh_in = dalloc<float>(size_t(n) * sin0);
+            if (needs_h0) h0 = dalloc<float>(size_t(n) * pad8(H));
+        }
+        if (needs_h0) dh0 = dalloc<float>(size_t(n) * pad8(H));
+        dtop = dalloc<float>(size_t(n) * L[len - 1].sout);
+        // pgrad workspace: ~2 waves of CTAs
+        uint32_t max_tiles = 1;
+        for (auto& d : L) max_tiles = std::max(max_tiles, ((d.din + 63) / 64) * ((d.dout + 63) / 64));
+        splits = std::max<uint32_t>(1, std::min<uint32_t>((2 * num_sms + max_tiles - 1) / max_tiles,
+                                                          (n + 255) / 256));
+        size_t wmax = 1;
+        for (auto& d : L) wmax = std::max(wmax, size_t(d.din) * d.dout);
+        ws = dalloc<float>(size_t(splits) * wmax, false);
+        wsb = dalloc<float>(size_t(splits) * kMaxWidth, false);
+        xent_blocks = uint32_t(std::min<uint64_t>(2ull * num_sms, (n + kWarpsPerBlock - 1) / kWarpsPerBlock));
+        part_loss = dalloc<double>(xent_blocks);
+        part_correct = dalloc<unsigned long long>(3ull * xent_blocks);
+        red_loss = dalloc<double>(1);
+        red_correct = dalloc<unsigned long long>(3);
+        GP_CUDA(cudaDeviceSynchronize());
+    }
+
+    void setup_kernels() {
+        const int smem_max = 64 * 1024 + 1024;
+        GP_CUDA(cudaFuncSetAttribute(k_fwd_fused<FWD_DENSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
+        GP_CUDA(cudaFuncSetAttribute(k_fwd_fused<FWD_GCN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
+        GP_CUDA(cudaFuncSetAttribute(k_fwd_fused<FWD_GCN2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
+#define SETB(P, O) \
+    GP_CUDA(cudaFuncSetAttribute(k_bwd<P, O>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
+        SETB(PREV_TOP, OUT_LAYER) SETB(PREV_AGG, OUT_LAYER) SETB(PREV_AGG_HIST, OUT_LAYER)
+        SETB(PREV_OWN, OUT_LAYER) SETB(PREV_AGG, OUT_DHIN) SETB(PREV_AGG_HIST, OUT_DHIN)
+        SETB(PREV_OWN, OUT_DHIN)
+#undef SETB
+    }
+
+    // ---- graph --------------------------------------------------------------
+    void upload_graph(const uint64_t* off, const uint32_t* cols, const float* vals, uint64_t nz,
+                      const uint32_t* chunk_of) {
+        GP_CUDA(cudaSetDevice(device));
+        if (!off || !cols || !vals || !chunk_of) throw Error(GP_EINVAL, "null graph array");
+        if (off[0] != 0 || off[n] != nz) throw Error(GP_EINVAL, "CSR offsets inconsistent with nnz");
+        // chunk-contiguous renumbering: chunk-major, ascending original id inside
+        std::vector<uint32_t> count(K + 1, 0);
+        for (uint32_t v = 0; v < n; ++v) {
+            if (chunk_of[v] >= K) throw Error(GP_EINVAL, "chunk id out of range");
+            ++count[chunk_of[v] + 1];
+        }
+        cstart.assign(K + 1, 0);
+        for (uint32_t k = 0; k < K; ++k) cstart[k + 1] = cstart[k] + count[k + 1];
+        perm.assign(n, 0);
+        inv.assign(n, 0);
+        std::vector<uint32_t> cur(cstart.begin(), cstart.end() - 1);
+        for (uint32_t v = 0; v < n; ++v) {
+            const uint32_t r = cur[chunk_of[v]]++;
+            perm[v] = r;
+            inv[r] = v;
+        }
+        std::vector<uint64_t> rp(size_t(n) + 1, 0);
+        for (uint32_t r = 0; r < n; ++r) {
+            const uint32_t v = inv[r];
+            if (off[v + 1] < off[v]) throw Error(GP_EINVAL, "CSR offsets not monotone");
+            rp[r + 1] = rp[r] + (off[v + 1] - off[v]);
+        }
+        std::vector<uint2> e(nz);
+        const unsigned nth = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+        std::vector<std::thread> pool;
+        std::atomic<bool> bad{false};
+        for (unsigned t = 0; t < nth; ++t)
+            pool.emplace_back([&, t]() {
+                for (uint32_t r = t; r < n; r += nth) {
+                    const uint32_t v = inv[r];
+                    uint64_t w = rp[r];
+                    for (uint64_t i = off[v]; i < off[v + 1]; ++i, ++w) {
+                        const uint32_t u = cols[i];
+                        if (u >= n) {
+                            bad = true;
+                            return;
+                        }
+                        uint32_t bits;
+                        std::memcpy(&bits, &vals[i], 4);
+                        e[w] = make_uint2(perm[u] | (chunk_of[u] << kColBits), bits);
+                    }
+                }
+            });
+        for (auto& th : pool) th.join();
+        if (bad) throw Error(GP_EINVAL, "CSR column out of range");
+        nnz = nz;
+        rowptr = dalloc<uint64_t>(size_t(n) + 1, false);
+        edges = dalloc<uint2>(std::max<uint64_t>(nz, 1), false);
+        orig = dalloc<uint32_t>(n, false);
+        GP_CUDA(cudaMemcpy(rowptr, rp.data(), rp.size() * 8, cudaMemcpyHostToDevice));
+        if (nz) GP_CUDA(cudaMemcpy(edges, e.data(), nz * 8, cudaMemcpyHostToDevice));
+        GP_CUDA(cudaMemcpy(orig, inv.data(), size_t(n) * 4, cudaMemcpyHostToDevice));
+        graph_ready = true;
+    }
+
+    void share_graph(const Stage& o) {
+        if (!o.graph_ready) throw Error(GP_EINVAL, "owner stage has no graph");
+        if (o.n != n || o.K != K || o.device != device)
+            throw Error(GP_EINVAL, "graph sharing needs the same N, K and device");
+        rowptr = o.rowptr;
+        edges = o.edges;
+        orig = o.orig;
+        perm = o.perm;
+        inv = o.inv;
+        cstart = o.cstart;
+        nnz = o.nnz;
+        graph_ready = true;
+    }
+
+    void upload_features(const float* x, uint32_t f) {
+        GP_CUDA(cudaSetDevice(device));
+        if (!first) throw Error(GP_EINVAL, "features belong to stage 0");
+        if (!graph_ready) throw Error(GP_EINVAL, "upload the graph first");
+        if (f != specs[0].in_dim) throw Error(GP_EINVAL, "feature width != layer 0 in_dim");
+        F = f;
+        sx = pad8(f);
+        std::vector<float> hx(size_t(n) * sx, 0.f);
+        for (uint32_t r = 0; r < n; ++r)
+            std::memcpy(&hx[size_t(r) * sx], x + size_t(inv[r]) * f, size_t(f) * 4);
+        if (!x0) x0 = dalloc<float>(hx.size(), false);
+        GP_CUDA(cudaMemcpy(x0, hx.data(), hx.size() * 4, cudaMemcpyHostToDevice));
+        x_ready = true;
+    }
+
+    void upload_labels(const uint32_t* lab, const uint8_t* sp) {
+        GP_CUDA(cudaSetDevice(device));
+        if (!last) throw Error(GP_EINVAL, "labels belong to the last stage");
+        if (!graph_ready) throw Error(GP_EINVAL, "upload the graph first");
+        std::vector<uint32_t> hl(n);
+        std::vector<uint8_t> hs(n);
+        uint64_t ntrain = 0;
+        for (uint32_t r = 0; r < n; ++r) {
+            hl[r] = lab[inv[r]];
+            hs[r] = sp[inv[r]];
+            if (hl[r] >= C) throw Error(GP_EINVAL, "label >= num_classes");
+            ntrain += hs[r] == 1;
+        }
+        if (ntrain == 0) throw Error(GP_EINVAL, "train_hybrid: empty train mask");
+        inv_train = float(1.0 / double(ntrain));  // engines_impl.hpp:548
+        if (!labels) labels = dalloc<uint32_t>(n, false);
+        if (!split) split = dalloc<uint8_t>(n, false);
+        GP_CUDA(cudaMemcpy(labels, hl.data(), size_t(n) * 4, cudaMemcpyHostToDevice));
+        GP_CUDA(cudaMemcpy(split, hs.data(), n, cudaMemcpyHostToDevice));
+        labels_ready = true;
+    }
+
+    LayerDev& layer(uint32_t l) {
+        if (l < lb || l >= le) throw Error(GP_EINVAL, "layer not owned by this stage");
+        return L[l - lb];
+    }
+
+    void set_params(uint32_t l, const float* W, const float* b) {
+        GP_CUDA(cudaSetDevice(device));
+        auto& d = layer(l);
+        GP_CUDA(cudaMemcpy(d.W, W, size_t(d.din) * d.dout * 4, cudaMemcpyHostToDevice));
+        if (d.b) {
+            if (!b) throw Error(GP_EINVAL, "layer has a bias");
+            GP_CUDA(cudaMemcpy(d.b, b, size_t(d.dout) * 4, cudaMemcpyHostToDevice));
+        }
+    }
+
+    void get_params(uint32_t l, float* W, float* b) {
+        GP_CUDA(cudaSetDevice(device));
+        GP_CUDA(cudaStreamSynchronize(cs));
+        auto& d = layer(l);
+        if (W) GP_CUDA(cudaMemcpy(W, d.W, size_t(d.din) * d.dout * 4, cudaMemcpyDeviceToHost));
+        if (d.b && b) GP_CUDA(cudaMemcpy(b, d.b, size_t(d.dout) * 4, cudaMemcpyDeviceToHost));
+    }
+
+    // ---- launch helpers -------------------------------------------------------
+    cudaEvent_t take_event() {
+        if (!ev_free.empty()) {
+            auto e = ev_free.back();
+            ev_free.pop_back();
+            return e;
+        }
+        cudaEvent_t e;
+        GP_CUDA(cudaEventCreate(&e));
+        return e;
+    }
+
+    template <typename F>
+    void launch(int cls, double bytes, double flops, double gather, F&& fn) {
+        ++launches;
+        if (!profiling) {
+            fn();
+            GP_CUDA(cudaGetLastError());
+            return;
+        }
+        Timed t{cls, take_event(), take_event(), bytes, flops, gather};
+        GP_CUDA(cudaEventRecord(t.a, cs));
+        fn();
+        GP_CUDA(cudaGetLastError());
+        GP_CUDA(cudaEventRecord(t.b, cs));
+        timed.push_back(t);
+    }
+
+    uint32_t row_grid(uint32_t rows, int occ) const {
+        const uint64_t want = (uint64_t(rows) + kWarpsPerBlock - 1) / kWarpsPerBlock;
+        const uint64_t cap = uint64_t(num_sms) * std::max(occ, 1);
+        return uint32_t(std::max<uint64_t>(1, std::min(want, cap)));
+    }
+
+    DropKey drop_key(uint32_t t, uint32_t l, uint32_t cols) const {
+        DropKey k;
+        if (cfg.dropout <= 0.0) return k;  // DropMask::off (nn.hpp:115)
+        const double keep = 1.0 - cfg.dropout;
+        k.enabled = 1;
+        k.cols = cols;
+        k.scale = float(1.0 / keep);
+        k.k2 = mix64(mix64(cfg.seed, t, l));
+        k.thr = uint64_t(std::ceil(std::ldexp(keep, 53)));
+        return k;
+    }
+
+    // Source rows of layer i's input for stale reads: the snapshot.
+    const float* snap_src(uint32_t i) const {
+        if (i == 0) return first ? x0 : in_snap;
+        return L[i - 1].hs;
+    }
+    uint32_t src_stride(uint32_t i) const { return i == 0 ? (first ? sx : sin0) : L[i - 1].sout; }
+    const float* cur_src(uint32_t i) const {
+        if (i == 0) return first ? x0 : in_cur;
+        return L[i - 1].h;
+    }
+
+    void remask(uint32_t i, const float* src, uint32_t r0, uint32_t r1, const DropKey& key) {
+        auto& d = L[i];
+        RemaskParams p{r0, r1, d.din, src, src_stride(i), d.G, d.sin, orig, key};
+        const uint32_t rows = r1 - r0;
+        launch(GP_K_REMASK, double(rows) * d.din * 8.0, 0, 0,
+               [&]() { k_remask<<<row_grid(rows, occ_row), kBlock, 0, cs>>>(p); });
+    }
+
+    void forward_layer(uint32_t i, uint32_t r0, uint32_t r1, uint32_t t) {
+        auto& d = L[i];
+        const uint32_t rows = r1 - r0;
+        if (rows == 0) return;
+        const float* h0src = needs_h0 ? (first ? L[0].h : h0) : nullptr;
+        const uint32_t h0stride = pad8(H);
+        float* gnext = nullptr;
+        uint32_t gnstride = 0;
+        DropKey nk;
+        if (i + 1 < len && L[i + 1].agg) {
+            gnext = L[i + 1].G;
+            gnstride = L[i + 1].sin;
+            nk = drop_key(t, d.l + 1, L[i + 1].din);
+        }
+        const float alpha = float(d.spec.alpha), beta = float(d.spec.beta);
+        if (d.din <= kMaxWidth) {
+            FwdParams p{};
+            p.r0 = r0;
+            p.r1 = r1;
+            p.rowptr = rowptr;
+            p.edges = edges;
+            p.gsrc = d.G;
+            p.gstride = d.sin;
+            p.xsrc = cur_src(i);
+            p.xstride = src_stride(i);
+            p.in_mask = drop_key(t, d.l, d.din);
+            p.orig = orig;
+            p.h0 = h0src;
+            p.h0stride = h0stride;
+            p.alpha = alpha;
+            p.oma = 1.f - alpha;  // (T{1} - a) in float, nn.hpp:184-187
+            p.beta = beta;
+            p.omb = 1.f - beta;
+            p.W = d.W;
+            p.bias = d.b;
+            p.din = d.din;
+            p.dout = d.dout;
+            p.relu = d.spec.relu;
+            p.pre = d.pre;
+            p.prestride = d.sin;
+            p.out = d.h;
+            p.outstride = d.sout;
+            p.gnext = gnext;
+            p.gnstride = gnstride;
+            p.next_mask = nk;
+            const size_t smem = (size_t(d.din) + 1) * ((d.dout + 3) / 4) * 16;
+            const uint32_t grid = row_grid(rows, occ_fwd);
+            const double e = d.agg ? double(rowptr_nnz(r0, r1)) : 0.0;
+            const double bytes = (d.agg ? e * 8.0 + double(rows + 1) * 8.0 + double(n) * d.din * 4.0
+                                        : double(rows) * d.din * 4.0) +
+                                 double(rows) * (d.din + d.dout) * 4.0 +
+                                 (d.spec.kind == GP_GCN2CONV ? double(rows) * d.din * 4.0 : 0.0) +
+                                 (gnext ? double(rows) * d.dout * 4.0 : 0.0);
+            const double flops = 2.0 * e * d.din + 2.0 * double(rows) * d.din * d.dout;
+            const double gather = e * double(d.sin) * 4.0;
+            const int cls = d.agg ? GP_K_FWD_AGG : GP_K_FWD_DENSE;
+            if (d.spec.kind == GP_DENSE)
+                launch(cls, bytes, flops, 0, [&]() { k_fwd_fused<FWD_DENSE><<<grid, kBlock, smem, cs>>>(p); });
+            else if (d.spec.kind == GP_GCNCONV)
+                launch(cls, bytes, flops, gather, [&]() { k_fwd_fused<FWD_GCN><<<grid, kBlock, smem, cs>>>(p); });
+            else
+                launch(cls, bytes, flops, gather, [&]() { k_fwd_fused<FWD_GCN2><<<grid, kBlock, smem, cs>>>(p); });
+            return;
+        }
+        // wide input (layer 0 with F > 128): pre first, then the tiled transform
+        if (d.spec.kind == GP_GCN2CONV) throw Error(GP_EINVAL, "Gcn2Conv wider than 128");
+        if (d.agg) {
+            SpmmParams sp{r0, r1, d.din, rowptr, edges, d.G, d.sin, d.pre, d.sin};
+            const double e = double(rowptr_nnz(r0, r1));
+            launch(GP_K_FWD_AGG, e * 8.0 + double(n) * d.din * 4.0 + double(rows) * d.din * 4.0,
+                   2.0 * e * d.din, e * d.sin * 4.0,
+                   [&]() { k_spmm_pre<<<row_grid(rows, occ_row), kBlock, 0, cs>>>(sp); });
+        } else {
+            RemaskParams rp{r0, r1, d.din, cur_src(i), src_stride(i), d.pre, d.sin, orig,
+                            drop_key(t, d.l, d.din)};
+            launch(GP_K_FWD_DENSE, double(rows) * d.din * 8.0, 0, 0,
+                   [&]() { k_remask<<<row_grid(rows, occ_row), kBlock, 0, cs>>>(rp); });
+        }
+        GemmParams g{};
+        g.r0 = r0;
+        g.r1 = r1;
+        g.A = d.pre;
+        g.astride = d.sin;
+        g.W = d.W;
+        g.bias = d.b;
+        g.din = d.din;
+        g.dout = d.dout;
+        g.relu = d.spec.relu;
+        g.out = d.h;
+        g.outstride = d.sout;
+        g.gnext = gnext;
+        g.gnstride = gnstride;
+        g.next_mask = nk;
+        g.orig = orig;
+        launch(GP_K_FWD_DENSE,
+               double(rows) * (d.din + d.dout + (gnext ? d.dout : 0)) * 4.0 + double(d.din) * d.dout * 4.0,
+               2.0 * double(rows) * d.din * d.dout, 0,
+               [&]() { k_dense_gemm<<<(rows + 63) / 64, kBlock, 0, cs>>>(g); });
+    }
+
+    std::vector<uint64_t> h_rowptr;  // host copy for byte accounting
+    uint64_t rowptr_nnz(uint32_t r0, uint32_t r1) {
+        if (h_rowptr.empty()) {
+            h_rowptr.resize(size_t(n) + 1);
+            GP_CUDA(cudaMemcpy(h_rowptr.data(), rowptr, h_rowptr.size() * 8, cudaMemcpyDeviceToHost));
+        }
+        return h_rowptr[r1] - h_rowptr[r0];
+    }
+
+    // backward kernel for local layer i over rows [r0, r1)
+    void backward_layer(uint32_t i, uint32_t r0, uint32_t r1, uint32_t t, uint64_t done) {
+        auto& d = L[i];
+        const uint32_t rows = r1 - r0;
+        if (rows == 0) return;
+        BwdParams p{};
+        p.r0 = r0;
+        p.r1 = r1;
+        p.rowptr = rowptr;
+        p.edges = edges;
+        p.done = done;
+        p.orig = orig;
+        p.dh_width = d.dout;
+        int prev = PREV_TOP;
+        double e = 0;
+        if (i + 1 == len) {
+            p.dtop = dtop;
+            p.dtopstride = d.sout;
+        } else {
+            auto& nx = L[i + 1];
+            p.bgn = nx.bg;
+            p.bgn_snap = nx.bgs;
+            p.bgnstride = nx.sin;
+            p.prev_mask = drop_key(t, nx.l, nx.din);
+            if (nx.agg) {
+                prev = hist ? PREV_AGG_HIST : PREV_AGG;
+                e = double(rowptr_nnz(r0, r1));
+            } else {
+                prev = PREV_OWN;
+            }
+        }
+        if (d.l == 0 && needs_h0) {
+            p.dh0_add = dh0;
+            p.dh0stride = pad8(H);
+        }
+        p.h = d.h;
+        p.hstride = d.sout;
+        p.relu = d.spec.relu;
+        p.dz = d.dz;
+        p.dzstride = d.sout;
+        p.W = d.W;
+        p.din = d.din;
+        p.dout = d.dout;
+        p.need_dagg = d.l > 0;
+        p.gcn2 = d.spec.kind == GP_GCN2CONV;
+        const float alpha = float(d.spec.alpha), beta = float(d.spec.beta);
+        p.alpha = alpha;
+        p.oma = 1.f - alpha;
+        p.beta = beta;
+        p.omb = 1.f - beta;
+        p.dh0 = dh0;
+        p.bg = d.bg;
+        p.bgstride = d.sin;
+        const size_t smem = p.need_dagg ? size_t(d.dout) * ((d.din + 3) / 4) * 16 : 0;
+        const uint32_t grid = row_grid(rows, occ_bwd);
+        const double bytes = e * 8.0 + (e > 0 ? double(n) * d.dout * 4.0 : double(rows) * d.dout * 4.0) +
+                             double(rows) * d.dout * 8.0 + (p.need_dagg ? double(rows) * d.din * 4.0 : 0.0) +
+                             (p.gcn2 ? double(rows) * d.din * 8.0 : 0.0);
+        const double flops = 2.0 * e * d.dout + (p.need_dagg ? 2.0 * double(rows) * d.din * d.dout : 0.0);
+        const double gather = e * double(pad8(d.dout)) * 4.0;
+        const int cls = prev == PREV_AGG || prev == PREV_AGG_HIST ? GP_K_BWD_AGG : GP_K_BWD_DENSE;
+        switch (prev) {
+            case PREV_TOP:
+                launch(cls, bytes, flops, 0, [&]() { k_bwd<PREV_TOP, OUT_LAYER><<<grid, kBlock, smem, cs>>>(p); });
+                break;
+            case PREV_AGG:
+                launch(cls, bytes, flops, gather, [&]() { k_bwd<PREV_AGG, OUT_LAYER><<<grid, kBlock, smem, cs>>>(p); });
+                break;
+            case PREV_AGG_HIST:
+                launch(cls, bytes, flops, gather,
+                       [&]() { k_bwd<PREV_AGG_HIST, OUT_LAYER><<<grid, kBlock, smem, cs>>>(p); });
+                break;
+            default:
+                launch(cls, bytes, flops, 0, [&]() { k_bwd<PREV_OWN, OUT_LAYER><<<grid, kBlock, smem, cs>>>(p); });
+        }
+    }
+
+    // backward_prev of local layer 0 on a non-first stage -> dh_in
+    void backward_dhin(uint32_t r0, uint32_t r1, uint32_t t, uint64_t done) {
+        auto& d = L[0];
+        const uint32_t rows = r1 - r0;
+        if (rows == 0) return;
+        BwdParams p{};
+        p.r0 = r0;
+        p.r1 = r1;
+        p.rowptr = rowptr;
+        p.edges = edges;
+        p.done = done;
+        p.orig = orig;
+        p.dh_width = d.din;
+        p.bgn = d.bg;
+        p.bgn_snap = d.bgs;
+        p.bgnstride = d.sin;
+        p.prev_mask = drop_key(t, d.l, d.din);
+        p.dh_in = dh_in;
+        p.dhinstride = sin0;
+        const uint32_t grid = row_grid(rows, occ_bwd);
+        const double e = d.agg ? double(rowptr_nnz(r0, r1)) : 0.0;
+        const double bytes = e * 8.0 + (d.agg ? double(n) : double(rows)) * d.din * 4.0 + double(rows) * d.din * 4.0;
+        if (!d.agg)
+            launch(GP_K_BWD_DENSE, bytes, 0, 0, [&]() { k_bwd<PREV_OWN, OUT_DHIN><<<grid, kBlock, 0, cs>>>(p); });
+        else if (hist)
+            launch(GP_K_BWD_AGG, bytes, 2.0 * e * d.din, e * d.sin * 4.0,
+                   [&]() { k_bwd<PREV_AGG_HIST, OUT_DHIN><<<grid, kBlock, 0, cs>>>(p); });
+        else
+            launch(GP_K_BWD_AGG, bytes, 2.0 * e * d.din, e * d.sin * 4.0,
+                   [&]() { k_bwd<PREV_AGG, OUT_DHIN><<<grid, kBlock, 0, cs>>>(p); });
+    }
+
+    XentParams xent_params(uint32_t r0, uint32_t r1) {
+        auto& d = L[len - 1];
+        XentParams p{};
+        p.r0 = r0;
+        p.r1 = r1;
+        p.classes = d.dout;
+        p.logits = d.h;
+        p.lstride = d.sout;
+        p.labels = labels;
+        p.split = split;
+        p.inv_count = inv_train;
+        p.grad = dtop;
+        p.gstride = d.sout;
+        p.part_loss = part_loss;
+        p.part_correct = part_correct;
+        return p;
+    }
+
+    void param_step() {
+        ++step;  // Optimizer::step (nn.hpp:456-467): one update per epoch per stage
+        const double c1d = 1.0 - std::pow(cfg.beta1, double(step));
+        const double c2d = 1.0 - std::pow(cfg.beta2, double(step));
+        for (uint32_t i = 0; i < len; ++i) {
+            auto& d = L[i];
+            const uint32_t ti = (d.din + 63) / 64, tj = (d.dout + 63) / 64;
+            const uint32_t rps = (n + splits - 1) / splits;
+            PgradParams pp{n, rps, d.pre, d.sin, d.dz, d.sout, d.din, d.dout, ws, d.gb ? wsb : nullptr};
+            dim3 grid(splits, ti, tj);
+            launch(GP_K_PGRAD, double(n) * (d.din * tj + d.dout * ti) * 4.0 + double(splits) * d.din * d.dout * 4.0,
+                   2.0 * double(n) * d.din * d.dout, 0,
+                   [&]() { k_pgrad_partial<<<grid, 256, 0, cs>>>(pp); });
+            const uint32_t tot = d.din * d.dout + d.dout;
+            const bool gcn2 = d.spec.kind == GP_GCN2CONV;
+            launch(GP_K_PGRAD, double(splits) * tot * 4.0 + tot * 4.0, 0, 0, [&]() {
+                k_pgrad_fold<<<(tot + 255) / 256, 256, 0, cs>>>(ws, d.gb ? wsb : nullptr, splits, d.din, d.dout,
+                                                                float(d.spec.beta), gcn2, d.gW, d.gb);
+            });
+            AdamParams a{};
+            a.sgd = cfg.optimizer == 1;
+            a.lr = float(cfg.lr);
+            a.b1 = float(cfg.beta1);
+            a.b2 = float(cfg.beta2);
+            a.omb1 = 1.f - a.b1;
+            a.omb2 = 1.f - a.b2;
+            a.eps = float(cfg.eps);
+            a.c1 = float(c1d);
+            a.c2 = float(c2d);
+            a.p = d.W;
+            a.g = d.gW;
+            a.m = d.mW;
+            a.v = d.vW;
+            a.n = d.din * d.dout;
+            launch(GP_K_OPTIM, a.n * 20.0, 0, 0, [&]() { k_adam<<<(a.n + 255) / 256, 256, 0, cs>>>(a); });
+            if (d.b) {
+                a.p = d.b;
+                a.g = d.gb;
+                a.m = d.mb;
+                a.v = d.vb;
+                a.n = d.dout;
+                launch(GP_K_OPTIM, a.n * 20.0, 0, 0, [&]() { k_adam<<<1, 256, 0, cs>>>(a); });
+            }
+        }
+    }
+
+    // ---- transport ------------------------------------------------------------
+    uint64_t bytes_sent[6] = {0, 0, 0, 0, 0, 0};
+    uint64_t msgs_sent[6] = {0, 0, 0, 0, 0, 0};
+
+    std::vector<Piece> fwd_pieces(uint32_t k, bool as_sender) {
+        const uint32_t r0 = cstart[k], rows = cstart[k + 1] - cstart[k];
+        std::vector<Piece> v;
+        if (as_sender) {
+            auto& d = L[len - 1];
+            v.push_back({d.h + size_t(r0) * d.sout, size_t(rows) * d.sout});
+            if (needs_h0) v.push_back({(first ? L[0].h : h0) + size_t(r0) * pad8(H), size_t(rows) * pad8(H)});
+        } else {
+            v.push_back({in_cur + size_t(r0) * sin0, size_t(rows) * sin0});
+            if (needs_h0) v.push_back({h0 + size_t(r0) * pad8(H), size_t(rows) * pad8(H)});
+        }
+        return v;
+    }
+    std::vector<Piece> bwd_pieces(uint32_t k, bool as_sender) {
+        const uint32_t r0 = cstart[k], rows = cstart[k + 1] - cstart[k];
+        std::vector<Piece> v;
+        if (as_sender) {
+            v.push_back({dh_in + size_t(r0) * sin0, size_t(rows) * sin0});
+        } else {
+            auto& d = L[len - 1];
+            v.push_back({dtop + size_t(r0) * d.sout, size_t(rows) * d.sout});
+        }
+        if (needs_h0) v.push_back({dh0 + size_t(r0) * pad8(H), size_t(rows) * pad8(H)});
+        return v;
+    }
+
+    cudaEvent_t pool_event() {
+        auto& tr_ = tr;
+        if (tr_.ev_next == tr_.ev_pool.size()) {
+            cudaEvent_t e;
+            GP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            tr_.ev_pool.push_back(e);
+        }
+        return tr_.ev_pool[tr_.ev_next++];
+    }
+
+    void account(int tag, uint32_t k, uint32_t width) {
+        const uint64_t rows = cstart[k + 1] - cstart[k];
+        bytes_sent[tag] += rows * (uint64_t(width) + (needs_h0 ? H : 0)) * 4;  // 4 B/value (fabric.hpp:59)
+        ++msgs_sent[tag];
+    }
+
+    void wait_local(LocalQueue& q, uint32_t k, LocalQueue::Msg& out) {
+        std::unique_lock<std::mutex> lk(q.mu);
+        const auto deadline = std::chrono::steady_clock::now() + std::chrono::seconds(600);
+        while (q.q.empty()) {
+            if (q.aborted || aborted) throw Error(GP_EFABRIC, "transport aborted");
+            if (q.cv.wait_until(lk, deadline) == std::cv_status::timeout && q.q.empty())
+                throw Error(GP_EFABRIC, "watchdog: stage " + std::to_string(s) + " blocked on recv of chunk " +
+                                            std::to_string(k));
+        }
+        out = std::move(q.q.front());
+        q.q.pop_front();
+        if (out.chunk != k)
+            throw Error(GP_EFABRIC, "transport: expected chunk " + std::to_string(k) + ", got " +
+                                        std::to_string(out.chunk));
+    }
+
+    void post_local(LocalQueue& q, uint32_t k, std::vector<Piece> src) {
+        cudaEvent_t ev = pool_event();
+        GP_CUDA(cudaEventRecord(ev, cs));
+        std::lock_guard<std::mutex> lk(q.mu);
+        if (q.aborted) throw Error(GP_EFABRIC, "transport aborted");
+        q.q.push_back({k, ev, std::move(src), device});
+        q.cv.notify_all();
+    }
+
+    void copy_in(const LocalQueue::Msg& m, const std::vector<Piece>& dst) {
+        GP_CUDA(cudaStreamWaitEvent(cs, m.ready, 0));
+        for (size_t i = 0; i < dst.size(); ++i) {
+            if (m.device == device)
+                GP_CUDA(cudaMemcpyAsync(dst[i].ptr, m.src[i].ptr, dst[i].floats * 4, cudaMemcpyDeviceToDevice, cs));
+            else
+                GP_CUDA(cudaMemcpyPeerAsync(dst[i].ptr, device, m.src[i].ptr, m.device, dst[i].floats * 4, cs));
+        }
+    }
+
+    void nccl_xfer(void* comm, cudaStream_t st, int peer, const std::vector<Piece>& pcs, bool send) {
+        cudaEvent_t ev = pool_event();
+        GP_CUDA(cudaEventRecord(ev, cs));
+        GP_CUDA(cudaStreamWaitEvent(st, ev, 0));
+        nccl_check(g_nccl.group_start(), "ncclGroupStart");
+        for (const auto& p : pcs) {
+            if (send)
+                nccl_check(g_nccl.send(p.ptr, p.floats, kNcclFloat, peer, comm, st), "ncclSend");
+            else
+                nccl_check(((NcclRecvFn)g_nccl.recv)(p.ptr, p.floats, kNcclFloat, peer, comm, st), "ncclRecv");
+        }
+        nccl_check(g_nccl.group_end(), "ncclGroupEnd");
+        cudaEvent_t done = pool_event();
+        GP_CUDA(cudaEventRecord(done, st));
+        GP_CUDA(cudaStreamWaitEvent(cs, done, 0));
+    }
+
+    void send_fwd(uint32_t k) {
+        account(0, k, L[len - 1].dout);
+        if (tr.down_local) post_local(tr.down_local->fwd, k, fwd_pieces(k, true));
+        else if (tr.down_comm) nccl_xfer(tr.down_comm, tr.down_stream, 1, fwd_pieces(k, true), true);
+        else throw Error(GP_EFABRIC, "no downstream link");
+    }
+    void recv_fwd(uint32_t k) {
+        if (tr.up_local) {
+            LocalQueue::Msg m;
+            wait_local(tr.up_local->fwd, k, m);
+            copy_in(m, fwd_pieces(k, false));
+        } else if (tr.up_comm) {
+            nccl_xfer(tr.up_comm, tr.up_stream, 0, fwd_pieces(k, false), false);
+        } else {
+            throw Error(GP_EFABRIC, "no upstream link");
+        }
+    }
+    void send_bwd(uint32_t k) {
+        account(1, k, in0);
+        if (tr.up_local) post_local(tr.up_local->bwd, k, bwd_pieces(k, true));
+        else if (tr.up_comm) nccl_xfer(tr.up_comm, tr.up_stream, 0, bwd_pieces(k, true), true);
+        else throw Error(GP_EFABRIC, "no upstream link");
+    }
+    void recv_bwd(uint32_t k) {
+        if (tr.down_local) {
+            LocalQueue::Msg m;
+            wait_local(tr.down_local->bwd, k, m);
+            copy_in(m, bwd_pieces(k, false));
+        } else if (tr.down_comm) {
+            nccl_xfer(tr.down_comm, tr.down_stream, 1, bwd_pieces(k, false), false);
+        } else {
+            throw Error(GP_EFABRIC, "no downstream link");
+        }
+    }
+
+    // ---- one epoch ---------------------------------------------------------------
+    void run_epoch(uint32_t t, const uint32_t* order, gp_epoch_stats* out) {
+        GP_CUDA(cudaSetDevice(device));
+        if (!graph_ready) throw Error(GP_EINVAL, "graph not uploaded");
+        if (first && !x_ready) throw Error(GP_EINVAL, "features not uploaded");
+        if (last && !labels_ready) throw Error(GP_EINVAL, "labels not uploaded");
+        if (t == 0) throw Error(GP_EINVAL, "epochs are 1-based");
+        std::vector<uint32_t> ord(order, order + K);
+        {
+            std::vector<uint8_t> seen(K, 0);
+            for (uint32_t k : ord) {
+                if (k >= K || seen[k]) throw Error(GP_EINVAL, "order is not a permutation of 0..K-1");
+                seen[k] = 1;
+            }
+        }
+        std::fill(bytes_sent, bytes_sent + 6, 0);
+        std::fill(msgs_sent, msgs_sent + 6, 0);
+        launches = 0;
+        tr.ev_next = 0;
+        GP_CUDA(cudaEventRecord(ev_start, cs));
+
+        // Snapshot (engines_impl.hpp:671-679): snap := cur. Every cur row is
+        // rewritten before it is read again, so a pointer swap is exact.
+        const uint32_t fix_alpha = std::max<uint32_t>(1, cfg.fix_alpha);
+        if (!sync && (t - 1) % fix_alpha == 0) {
+            if (in_snap) std::swap(in_snap, in_cur);
+            for (auto& d : L) {
+                if (d.hs) std::swap(d.hs, d.h);
+                if (d.bgs) std::swap(d.bgs, d.bg);
+            }
+        }
+        // Masked gather sources start from the snapshot rows (stale reads).
+        for (uint32_t i = 0; i < len; ++i) {
+            if (!L[i].agg) continue;
+            if (i == 0 && first) {
+                remask(0, x0, 0, n, drop_key(t, L[0].l, L[0].din));  // cur == snap == x0
+            } else if (!sync) {
+                remask(i, snap_src(i), 0, n, drop_key(t, L[i].l, L[i].din));
+            }
+        }
+
+        // ---- forward -----------------------------------------------------------
+        if (!sync) {
+            for (uint32_t kk = 0; kk < K; ++kk) {
+                const uint32_t k = ord[kk];
+                const uint32_t r0 = cstart[k], r1 = cstart[k + 1];
+                if (!first) {
+                    recv_fwd(k);
+                    if (L[0].agg) remask(0, in_cur, r0, r1, drop_key(t, L[0].l, L[0].din));
+                }
+                for (uint32_t i = 0; i < len; ++i) forward_layer(i, r0, r1, t);
+                if (!last) send_fwd(k);
+            }
+        } else {
+            if (!first) {
+                for (uint32_t kk = 0; kk < K; ++kk) recv_fwd(ord[kk]);
+                if (L[0].agg) remask(0, in_cur, 0, n, drop_key(t, L[0].l, L[0].din));
+            }
+            for (uint32_t i = 0; i < len; ++i) forward_layer(i, 0, n, t);
+            if (!last)
+                for (uint32_t kk = 0; kk < K; ++kk) send_fwd(ord[kk]);
+        }
+
+        // ---- metrics (last stage) ---------------------------------------------------
+        if (last) {
+            XentParams p = xent_params(0, n);
+            launch(GP_K_XENT, double(n) * L[len - 1].dout * 4.0, 0, 0,
+                   [&]() { k_xent_stats<<<xent_blocks, kBlock, 0, cs>>>(p); });
+            launch(GP_K_XENT, 0, 0, 0, [&]() {
+                k_xent_fold<<<1, 32, 0, cs>>>(part_loss, part_correct, xent_blocks, red_loss, red_correct);
+            });
+            if (needs_h0) GP_CUDA(cudaMemsetAsync(dh0, 0, size_t(n) * pad8(H) * 4, cs));
+        }
+
+        // ---- backward ---------------------------------------------------------------
+        if (!sync) {
+            uint64_t done = 0;
+            for (uint32_t kk = K; kk-- > 0;) {
+                const uint32_t k = ord[kk];
+                const uint32_t r0 = cstart[k], r1 = cstart[k + 1];
+                done |= 1ull << k;
+                if (last) {
+                    XentParams p = xent_params(r0, r1);
+                    launch(GP_K_XENT, double(r1 - r0) * L[len - 1].dout * 8.0, 0, 0,
+                           [&]() { k_xent_grad<<<row_grid(r1 - r0, occ_row), kBlock, 0, cs>>>(p); });
+                } else {
+                    recv_bwd(k);
+                }
+                for (uint32_t i = len; i-- > 0;) backward_layer(i, r0, r1, t, done);
+                if (!first) {
+                    backward_dhin(r0, r1, t, done);
+                    send_bwd(k);
+                }
+            }
+        } else {
+            const uint64_t done = K == 64 ? ~0ull : ((1ull << K) - 1);
+            if (last) {
+                XentParams p = xent_params(0, n);
+                launch(GP_K_XENT, double(n) * L[len - 1].dout * 8.0, 0, 0,
+                       [&]() { k_xent_grad<<<row_grid(n, occ_row), kBlock, 0, cs>>>(p); });
+            } else {
+                for (uint32_t kk = K; kk-- > 0;) recv_bwd(ord[kk]);
+            }
+            for (uint32_t i = len; i-- > 0;) backward_layer(i, 0, n, t, done);
+            if (!first) {
+                backward_dhin(0, n, t, done);
+                for (uint32_t kk = K; kk-- > 0;) send_bwd(ord[kk]);
+            }
+        }
+
+        param_step();
+        GP_CUDA(cudaEventRecord(ev_end, cs));
+        GP_CUDA(cudaStreamSynchronize(cs));
+        if (tr.up_stream) GP_CUDA(cudaStreamSynchronize(tr.up_stream));
+        if (tr.down_stream) GP_CUDA(cudaStreamSynchronize(tr.down_stream));
+        last_epoch = t;
+
+        gp_epoch_stats st{};
+        st.epoch = t;
+        if (last) {
+            st.has_quality = 1;
+            GP_CUDA(cudaMemcpy(&st.loss_sum, red_loss, 8, cudaMemcpyDeviceToHost));
+            unsigned long long c[3];
+            GP_CUDA(cudaMemcpy(c, red_correct, 24, cudaMemcpyDeviceToHost));
+            for (int i = 0; i < 3; ++i) st.correct[i] = c[i];
+        }
+        for (int i = 0; i < 6; ++i) {
+            st.bytes_sent[i] = bytes_sent[i];
+            st.msgs_sent[i] = msgs_sent[i];
+        }
+        GP_CUDA(cudaEventElapsedTime(&st.epoch_ms, ev_start, ev_end));
+        st.kernel_launches = launches;
+        float busy = 0.f;
+        for (auto& tm : timed) {
+            float ms = 0.f;
+            GP_CUDA(cudaEventElapsedTime(&ms, tm.a, tm.b));
+            busy += ms;
+            prof.ms[tm.cls] += ms;
+            prof.launches[tm.cls] += 1;
+            prof.alg_bytes[tm.cls] += tm.bytes;
+            prof.flops[tm.cls] += tm.flops;
+            prof.gather_bytes[tm.cls] += tm.gather;
+            ev_free.push_back(tm.a);
+            ev_free.push_back(tm.b);
+        }
+        timed.clear();
+        st.busy_ms = busy;
+        if (out) *out = st;
+    }
+
+    void download(uint32_t which, uint32_t i, float* out, uint64_t count) {
+        GP_CUDA(cudaSetDevice(device));
+        GP_CUDA(cudaStreamSynchronize(cs));
+        if (!graph_ready) throw Error(GP_EINVAL, "graph not uploaded");
+        const float* src = nullptr;
+        uint32_t width = 0, stride = 0;
+        auto need_layer = [&]() -> LayerDev& {
+            if (i >= len) throw Error(GP_EINVAL, "local layer out of range");
+            return L[i];
+        };
+        switch (which) {
+            case GP_BUF_H: { auto& d = need_layer(); src = d.h; width = d.dout; stride = d.sout; break; }
+            case GP_BUF_PRE: { auto& d = need_layer(); src = d.pre; width = d.din; stride = d.sin; break; }
+            case GP_BUF_DZ: { auto& d = need_layer(); src = d.dz; width = d.dout; stride = d.sout; break; }
+            case GP_BUF_DAGG: { auto& d = need_layer(); src = d.bg; width = d.din; stride = d.sin; break; }
+            case GP_BUF_HSNAP: { auto& d = need_layer(); src = d.hs; width = d.dout; stride = d.sout; break; }
+            case GP_BUF_GATHER: { auto& d = need_layer(); src = d.G; width = d.din; stride = d.sin; break; }
+            case GP_BUF_DH0: src = dh0; width = H; stride = pad8(H); break;
+            case GP_BUF_IN: src = in_cur; width = in0; stride = sin0; break;
+            case GP_BUF_DH_IN: src = dh_in; width = in0; stride = sin0; break;
+            default: throw Error(GP_EINVAL, "unknown buffer");
+        }
+        if (!src) throw Error(GP_EINVAL, "buffer not allocated on this stage");
+        if (count != uint64_t(n) * width) throw Error(GP_EINVAL, "count != N * width");
+        std::vector<float> tmp(size_t(n) * stride);
+        GP_CUDA(cudaMemcpy(tmp.data(), src, tmp.size() * 4, cudaMemcpyDeviceToHost));
+        for (uint32_t r = 0; r < n; ++r)
+            std::memcpy(out + size_t(inv[r]) * width, &tmp[size_t(r) * stride], size_t(width) * 4);
+    }
+};
+
+gp_status fail(Stage* st, const std::exception& e) {
+    gp_status code = GP_ERUNTIME;
+    if (auto* ge = dynamic_cast<const Error*>(&e)) code = ge->code;
+    else if (dynamic_cast<const std::invalid_argument*>(&e)) code = GP_EINVAL;
+    if (st) st->err = e.what();
+    g_tls_error = e.what();
+    return code;
+}
+
+template <typename F>
+gp_status guard(Stage* st, F&& f) {
+    try {
+        f();
+        return GP_OK;
+    } catch (const std::exception& e) {
+        return fail(st, e);
+    }
+}
+
+}  // namespace
+}  // namespace gp
+
+struct gp_ctx {
+    gp::Stage st;
+};
+
+extern "C" {
+
+uint32_t gp_abi_version(void) { return GP_ABI_VERSION; }
+
+gp_status gp_device_count(int* out) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) n = 0;
+    if (out) *out = n;
+    return GP_OK;
+}
+
+gp_status gp_create(const gp_stage_config* cfg, gp_ctx** out) {
+    if (!cfg || !out) {
+        gp::g_tls_error = "gp_create: null argument";
+        return GP_EINVAL;
+    }
+    *out = nullptr;
+    gp_ctx* c = new gp_ctx();
+    const gp_status s = gp::guard(&c->st, [&]() { c->st.init(*cfg); });
+    if (s != GP_OK) {
+        gp::g_tls_error = c->st.err;
+        delete c;
+        return s;
+    }
+    *out = c;
+    return GP_OK;
+}
+
+void gp_destroy(gp_ctx* ctx) { delete ctx; }
+
+const char* gp_last_error(const gp_ctx* ctx) {
+    if (ctx && !ctx->st.err.empty()) return ctx->st.err.c_str();
+    return gp::g_tls_error.c_str();
+}
+
+gp_status gp_upload_graph(gp_ctx* ctx, const uint64_t* offsets, const uint32_t* cols, const float* vals,
+                          uint64_t nnz, const uint32_t* chunk_of) {
+    return gp::guard(&ctx->st, [&]() { ctx->st.upload_graph(offsets, cols, vals, nnz, chunk_of); });
+}
+
+gp_status gp_share_graph(gp_ctx* ctx, const gp_ctx* owner) {
+    return gp::guard(&ctx->st, [&]() { ctx->st.share_graph(owner->st); });
+}
+
+gp_status gp_upload_features(gp_ctx* ctx, const float* x, uint32_t F) {
+    return gp::guard(&ctx->st, [&]() { ctx->st.upload_features(x, F); });
+}
+
+gp_status gp_upload_labels(gp_ctx* ctx, const uint32_t* labels, const uint8_t* split) {
+    return gp::guard(&ctx->st, [&]() { ctx->st.upload_labels(labels, split); });
+}
+
+gp_status gp_set_layer_params(gp_ctx* ctx, uint32_t layer, const float* W, const float* b) {
+    return gp::guard(&ctx->st, [&]() { ctx->st.set_params(layer, W, b); });
+}
+
+gp_status gp_get_layer_params(gp_ctx* ctx, uint32_t layer, float* W, float* b) {
+    return gp::guard(&ctx->st, [&]() { ctx->st.get_params(layer, W, b); });
+}
+
+gp_status gp_link_local(gp_ctx* up, gp_ctx* down) {
+    return gp::guard(&down->st, [&]() {
+        if (up->st.s + 1 != down->st.s) throw gp::Error(GP_EINVAL, "gp_link_local: stages not adjacent");
+        if (up->st.n != down->st.n || up->st.K != down->st.K)
+            throw gp::Error(GP_EINVAL, "gp_link_local: N/K mismatch");
+        auto link = std::make_shared<gp::LocalLink>();
+        up->st.tr.down_local = link;
+        down->st.tr.up_local = link;
+        if (up->st.device != down->st.device) {
+            int can = 0;
+            cudaDeviceCanAccessPeer(&can, down->st.device, up->st.device);
+            if (can) {
+                cudaSetDevice(down->st.device);
+                cudaDeviceEnablePeerAccess(up->st.device, 0);
+                cudaGetLastError();
+                cudaSetDevice(up->st.device);
+                cudaDeviceEnablePeerAccess(down->st.device, 0);
+                cudaGetLastError();
+            }
+        }
+    });
+}
+
+gp_status gp_nccl_unique_id(uint8_t out[128]) {
+    if (!gp::g_nccl.load()) {
+        gp::g_tls_error = "libnccl.so.2 not loadable";
+        return GP_ECUDA;
+    }
+    const int r = gp::g_nccl.get_unique_id(out);
+    if (r != 0) {
+        gp::g_tls_error = "ncclGetUniqueId failed";
+        return GP_ECUDA;
+    }
+    return GP_OK;
+}
+
+gp_status gp_link_nccl(gp_ctx* ctx, const uint8_t* up_id, const uint8_t* down_id) {
+    return gp::guard(&ctx->st, [&]() {
+        auto& st = ctx->st;
+        if (!gp::g_nccl.load()) throw gp::Error(GP_ECUDA, "libnccl.so.2 not loadable");
+        GP_CUDA(cudaSetDevice(st.device));
+        auto init = (gp::NcclInitFn)gp::g_nccl.comm_init_rank;
+        if (up_id && !st.first) {
+            gp::NcclId id;
+            std::memcpy(id.b, up_id, 128);
+            gp::nccl_check(init(&st.tr.up_comm, 2, id, 1), "ncclCommInitRank(up)");
+            GP_CUDA(cudaStreamCreateWithFlags(&st.tr.up_stream, cudaStreamNonBlocking));
+        }
+        if (down_id && !st.last) {
+            gp::NcclId id;
+            std::memcpy(id.b, down_id, 128);
+            gp::nccl_check(init(&st.tr.down_comm, 2, id, 0), "ncclCommInitRank(down)");
+            GP_CUDA(cudaStreamCreateWithFlags(&st.tr.down_stream, cudaStreamNonBlocking));
+        }
+    });
+}
+
+void gp_abort(gp_ctx* ctx) {
+    if (!ctx) return;
+    auto& st = ctx->st;
+    st.aborted = true;
+    for (auto* l : {st.tr.up_local.get(), st.tr.down_local.get()}) {
+        if (!l) continue;
+        for (auto* q : {&l->fwd, &l->bwd}) {
+            std::lock_guard<std::mutex> lk(q->mu);
+            q->aborted = true;
+            q->cv.notify_all();
+        }
+    }
+}
+
+gp_status gp_run_epoch(gp_ctx* ctx, uint32_t t, const uint32_t* order, gp_epoch_stats* out) {
+    return gp::guard(&ctx->st, [&]() { ctx->st.run_epoch(t, order, out); });
+}
+
+gp_status gp_download(gp_ctx* ctx, uint32_t which, uint32_t local_layer, float* out, uint64_t count) {
+    return gp::guard(&ctx->st, [&]() { ctx->st.download(which, local_layer, out, count); });
+}
+
+gp_status gp_set_profiling(gp_ctx* ctx, int enable) {
+    ctx->st.profiling = enable != 0;
+    return GP_OK;
+}
+
+gp_status gp_get_profile(gp_ctx* ctx, gp_profile* out) {
+    if (out) *out = ctx->st.prof;
+    return GP_OK;
+}
+
+gp_status gp_reset_profile(gp_ctx* ctx) {
+    ctx->st.prof = gp_profile{};
+    return GP_OK;
+}
+
+gp_status gp_device_bytes(gp_ctx* ctx, uint64_t* out) {
+    if (out) *out = ctx->st.dev_bytes;
+    return GP_OK;
+}
+
+}  // extern "C"

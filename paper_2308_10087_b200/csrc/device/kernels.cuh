@@ -1,0 +1,756 @@
+// sm_100a kernels of the stage engine. Every kernel is a restatement of a
+// reference per-row routine; arithmetic that the reference performs in a fixed
+// scalar order (ascending neighbour, ascending inner index, mul then add) is
+// performed in the same order with explicitly rounded IEEE operations, so the
+// forward pass is bit-identical to the CPU reference for the same parameters.
+//
+// Layout: vertices are renumbered chunk-contiguously; every
+// N x d activation is row-major with a row stride padded to a multiple of 8
+// floats (32-byte sectors); the normalised adjacency is CSR with one packed
+// 8-byte entry per non-zero: {col | chunk << 26, float weight}. One warp owns
+// one row; lane l owns columns 4l..4l+3 (d <= 128), so every neighbour gather is
+// one 16-byte load per lane and one contiguous sector run per warp.
+#pragma once
+
+#include "common.cuh"
+
+namespace gp {
+
+constexpr int kWarpsPerBlock = 8;
+constexpr int kBlock = kWarpsPerBlock * 32;
+constexpr unsigned kFull = 0xffffffffu;
+
+enum FwdKind { FWD_DENSE = 0, FWD_GCN = 1, FWD_GCN2 = 2 };
+enum PrevKind { PREV_TOP = 0, PREV_AGG = 1, PREV_AGG_HIST = 2, PREV_OWN = 3 };
+enum OutKind { OUT_LAYER = 0, OUT_DHIN = 1 };
+
+__device__ __forceinline__ float4 ld4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+__device__ __forceinline__ float4 ld4_rw(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+
+// ---------------------------------------------------------------------------
+// CSR row gather: acc[c] = sum over the row's entries in ascending column order
+// of w * src[col][c]  (kernel::spmv_row, nn.hpp:143-154, one mul and one add per
+// term). FILTER skips entries whose chunk is not in `done` (backward_prev_row's
+// nullptr getter, nn.hpp:249-250, engines_impl.hpp:771-778); HIST reads those
+// from `src_snap` instead (historical-gradient ablation, :773-776).
+// The 32 entries of a batch are loaded once, coalesced, and broadcast by
+// shuffle; 8 gathers are kept in flight per lane.
+// ---------------------------------------------------------------------------
+template <bool FILTER, bool HIST>
+__device__ __forceinline__ float4 gather_row(const uint64_t* __restrict__ rowptr,
+                                             const uint2* __restrict__ edges, uint32_t v,
+                                             const float* __restrict__ src,
+                                             const float* __restrict__ src_snap, uint32_t stride,
+                                             uint64_t done, int lane, bool active) {
+    float4 acc = f4_zero();
+    const uint64_t e0 = rowptr[v], e1 = rowptr[v + 1];
+    for (uint64_t base = e0; base < e1; base += 32) {
+        const int cnt = int(e1 - base < 32 ? e1 - base : 32);
+        const uint2 my = lane < cnt ? __ldg(edges + base + lane) : make_uint2(0u, 0u);
+        for (int t = 0; t < cnt; t += 8) {
+            float4 x[8];
+            float w[8];
+            bool ok[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int tt = t + i;
+                const uint32_t packed = __shfl_sync(kFull, my.x, tt & 31);
+                w[i] = __uint_as_float(__shfl_sync(kFull, my.y, tt & 31));
+                bool valid = tt < cnt;
+                const float* s = src;
+                if (FILTER) {
+                    const bool dn = (done >> (packed >> kColBits)) & 1ull;
+                    if (HIST) {
+                        if (!dn) s = src_snap;
+                    } else {
+                        valid = valid && dn;
+                    }
+                }
+                ok[i] = valid;
+                x[i] = (valid && active) ? ld4(s + size_t(packed & kColMask) * stride + 4 * lane)
+                                         : f4_zero();
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                if (ok[i]) {
+                    acc.x = mul_add(acc.x, w[i], x[i].x);
+                    acc.y = mul_add(acc.y, w[i], x[i].y);
+                    acc.z = mul_add(acc.z, w[i], x[i].z);
+                    acc.w = mul_add(acc.w, w[i], x[i].w);
+                }
+            }
+        }
+    }
+    return acc;
+}
+
+__device__ __forceinline__ float4 drop4(const DropKey& m, uint32_t vo, uint32_t c0, uint32_t width,
+                                        float4 x) {
+    float4 r;
+    r.x = c0 + 0 < width ? drop_apply(m, vo, c0 + 0, x.x) : 0.f;
+    r.y = c0 + 1 < width ? drop_apply(m, vo, c0 + 1, x.y) : 0.f;
+    r.z = c0 + 2 < width ? drop_apply(m, vo, c0 + 2, x.z) : 0.f;
+    r.w = c0 + 3 < width ? drop_apply(m, vo, c0 + 3, x.w) : 0.f;
+    return r;
+}
+
+// ---------------------------------------------------------------------------
+// Masked gather source: dst[v] = DropMask::apply(src[v]) for rows [r0, r1)
+// (the dropout the reference applies on every read of a layer input,
+// nn.hpp:152, :167). Used once per epoch per layer over the snapshot rows and
+// once per chunk over freshly received stage-input rows.
+// ---------------------------------------------------------------------------
+struct RemaskParams {
+    uint32_t r0, r1, width;
+    const float* src;
+    uint32_t sstride;
+    float* dst;
+    uint32_t dstride;
+    const uint32_t* orig;
+    DropKey mask;
+};
+
+__global__ void __launch_bounds__(kBlock) k_remask(RemaskParams p) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t nw = gridDim.x * kWarpsPerBlock;
+    for (uint32_t v = p.r0 + blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5); v < p.r1; v += nw) {
+        const uint32_t vo = p.orig[v];
+        for (uint32_t c0 = 4 * lane; c0 < p.width; c0 += 128) {
+            const float4 x = ld4_rw(p.src + size_t(v) * p.sstride + c0);
+            st4(p.dst + size_t(v) * p.dstride + c0, drop4(p.mask, vo, c0, p.width, x));
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Fused forward of one layer over the rows of one chunk (kernel::forward_row,
+// nn.hpp:159-197), d_in, d_out <= 128:
+//   Dense   : pre = drop(x_v)
+//   GcnConv : pre = sum_u w_vu * G[u]          (G = dropped layer input)
+//   Gcn2Conv: pre = (1-a) * sum_u w_vu G[u] + a * h0[v]
+//   out = b + pre . W   (ascending inner index, exact-zero skip, matrix.hpp:63-74)
+//   Gcn2Conv: out = (1-beta) pre + beta out;  ReLU
+// and, in the epilogue, the next layer's gather source gnext[v] = drop'(out).
+// W is staged in shared memory (<= 64 KB).
+// ---------------------------------------------------------------------------
+struct FwdParams {
+    uint32_t r0, r1;
+    const uint64_t* rowptr;
+    const uint2* edges;
+    const float* gsrc;
+    uint32_t gstride;
+    const float* xsrc;
+    uint32_t xstride;
+    DropKey in_mask;
+    const uint32_t* orig;
+    const float* h0;
+    uint32_t h0stride;
+    float alpha, oma, beta, omb;
+    const float* W;
+    const float* bias;
+    uint32_t din, dout;
+    uint32_t relu;
+    float* pre;
+    uint32_t prestride;
+    float* out;
+    uint32_t outstride;
+    float* gnext;
+    uint32_t gnstride;
+    DropKey next_mask;
+};
+
+template <int KIND>
+__global__ void __launch_bounds__(kBlock) k_fwd_fused(FwdParams p) {
+    extern __shared__ float4 smem4[];
+    const uint32_t dout4 = (p.dout + 3) / 4;
+    float* Ws = reinterpret_cast<float*>(smem4);
+    float* bs = Ws + size_t(p.din) * dout4 * 4;
+    for (uint32_t idx = threadIdx.x; idx < p.din * dout4 * 4; idx += blockDim.x) {
+        const uint32_t i = idx / (dout4 * 4), c = idx % (dout4 * 4);
+        Ws[idx] = c < p.dout ? p.W[size_t(i) * p.dout + c] : 0.f;
+    }
+    for (uint32_t c = threadIdx.x; c < dout4 * 4; c += blockDim.x)
+        bs[c] = (p.bias && c < p.dout) ? p.bias[c] : 0.f;
+    __syncthreads();
+    const float4* Ws4 = reinterpret_cast<const float4*>(Ws);
+
+    const int lane = threadIdx.x & 31;
+    const bool in_act = uint32_t(4 * lane) < p.din;
+    const bool out_act = uint32_t(4 * lane) < p.dout;
+    const uint32_t din4 = (p.din + 3) / 4;
+    const uint32_t nw = gridDim.x * kWarpsPerBlock;
+    for (uint32_t v = p.r0 + blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5); v < p.r1; v += nw) {
+        float4 pre;
+        if (KIND == FWD_DENSE) {
+            const float4 x = in_act ? ld4_rw(p.xsrc + size_t(v) * p.xstride + 4 * lane) : f4_zero();
+            pre = drop4(p.in_mask, p.orig[v], 4 * lane, p.din, x);
+        } else {
+            const float4 z = gather_row<false, false>(p.rowptr, p.edges, v, p.gsrc, nullptr, p.gstride,
+                                                      0ull, lane, in_act);
+            if (KIND == FWD_GCN2) {
+                const float4 h = in_act ? ld4_rw(p.h0 + size_t(v) * p.h0stride + 4 * lane) : f4_zero();
+                pre.x = __fadd_rn(__fmul_rn(p.oma, z.x), __fmul_rn(p.alpha, h.x));
+                pre.y = __fadd_rn(__fmul_rn(p.oma, z.y), __fmul_rn(p.alpha, h.y));
+                pre.z = __fadd_rn(__fmul_rn(p.oma, z.z), __fmul_rn(p.alpha, h.z));
+                pre.w = __fadd_rn(__fmul_rn(p.oma, z.w), __fmul_rn(p.alpha, h.w));
+            } else {
+                pre = z;
+            }
+        }
+        if (in_act) st4(p.pre + size_t(v) * p.prestride + 4 * lane, pre);
+
+        float4 o = out_act ? reinterpret_cast<const float4*>(bs)[lane] : f4_zero();
+        for (uint32_t ib = 0; ib < din4; ++ib) {
+            const float4 pb = shfl4(pre, int(ib));
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint32_t i = 4 * ib + q;
+                const float xi = f4_get(pb, q);
+                if (i < p.din && xi != 0.f && out_act) {
+                    const float4 wr = Ws4[size_t(i) * dout4 + lane];
+                    o.x = mul_add(o.x, xi, wr.x);
+                    o.y = mul_add(o.y, xi, wr.y);
+                    o.z = mul_add(o.z, xi, wr.z);
+                    o.w = mul_add(o.w, xi, wr.w);
+                }
+            }
+        }
+        if (KIND == FWD_GCN2) {
+            o.x = __fadd_rn(__fmul_rn(p.omb, pre.x), __fmul_rn(p.beta, o.x));
+            o.y = __fadd_rn(__fmul_rn(p.omb, pre.y), __fmul_rn(p.beta, o.y));
+            o.z = __fadd_rn(__fmul_rn(p.omb, pre.z), __fmul_rn(p.beta, o.z));
+            o.w = __fadd_rn(__fmul_rn(p.omb, pre.w), __fmul_rn(p.beta, o.w));
+        }
+        if (p.relu) {
+            if (o.x < 0.f) o.x = 0.f;
+            if (o.y < 0.f) o.y = 0.f;
+            if (o.z < 0.f) o.z = 0.f;
+            if (o.w < 0.f) o.w = 0.f;
+        }
+        if (out_act) {
+            st4(p.out + size_t(v) * p.outstride + 4 * lane, o);
+            if (p.gnext)
+                st4(p.gnext + size_t(v) * p.gnstride + 4 * lane,
+                    drop4(p.next_mask, p.orig[v], 4 * lane, p.dout, o));
+        }
+    }
+}
+
+// GcnConv aggregation for d_in > 128 (column blocks of 128): pre = A_hat . G.
+struct SpmmParams {
+    uint32_t r0, r1, width;
+    const uint64_t* rowptr;
+    const uint2* edges;
+    const float* gsrc;
+    uint32_t gstride;
+    float* pre;
+    uint32_t prestride;
+};
+
+__global__ void __launch_bounds__(kBlock) k_spmm_pre(SpmmParams p) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t nw = gridDim.x * kWarpsPerBlock;
+    for (uint32_t v = p.r0 + blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5); v < p.r1; v += nw)
+        for (uint32_t c0 = 0; c0 < p.width; c0 += 128) {
+            const bool act = c0 + 4 * lane < p.width;
+            const float4 z = gather_row<false, false>(p.rowptr, p.edges, v, p.gsrc + c0, nullptr,
+                                                      p.gstride, 0ull, lane, act);
+            if (act) st4(p.pre + size_t(v) * p.prestride + c0 + 4 * lane, z);
+        }
+}
+
+// ---------------------------------------------------------------------------
+// Dense transform for d_in > 128 (GCNII's Dense F->H input layer): out = b + pre.W
+// with the same ascending-k, mul-then-add, zero-skip order as dense_rows
+// (matrix.hpp:63-74), followed by the bias/ReLU/next-mask epilogue.
+// CTA tile: 64 rows x 128 output columns; thread: 8 rows x 4 columns.
+// ---------------------------------------------------------------------------
+struct GemmParams {
+    uint32_t r0, r1;
+    const float* A;
+    uint32_t astride;
+    const float* W;
+    const float* bias;
+    uint32_t din, dout;
+    uint32_t relu;
+    float* out;
+    uint32_t outstride;
+    float* gnext;
+    uint32_t gnstride;
+    DropKey next_mask;
+    const uint32_t* orig;
+};
+
+__global__ void __launch_bounds__(kBlock) k_dense_gemm(GemmParams p) {
+    __shared__ float As[64][33];
+    __shared__ float4 Bs[32][32];
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const uint32_t row0 = p.r0 + blockIdx.x * 64;
+    const bool col_act = uint32_t(4 * tx) < p.dout;
+    float4 acc[8];
+    const float4 b0 = make_float4(
+        (p.bias && 4 * tx + 0 < p.dout) ? p.bias[4 * tx + 0] : 0.f,
+        (p.bias && 4 * tx + 1 < p.dout) ? p.bias[4 * tx + 1] : 0.f,
+        (p.bias && 4 * tx + 2 < p.dout) ? p.bias[4 * tx + 2] : 0.f,
+        (p.bias && 4 * tx + 3 < p.dout) ? p.bias[4 * tx + 3] : 0.f);
+#pragma unroll
+    for (int r = 0; r < 8; ++r) acc[r] = b0;
+    for (uint32_t k0 = 0; k0 < p.din; k0 += 32) {
+        for (int idx = threadIdx.x; idx < 64 * 32; idx += kBlock) {
+            const int r = idx / 32, kk = idx % 32;
+            const uint32_t row = row0 + r, k = k0 + kk;
+            As[r][kk] = (row < p.r1 && k < p.din) ? p.A[size_t(row) * p.astride + k] : 0.f;
+        }
+        for (int idx = threadIdx.x; idx < 32 * 32; idx += kBlock) {
+            const int kk = idx / 32, c4 = idx % 32;
+            const uint32_t k = k0 + kk;
+            float4 w = f4_zero();
+            if (k < p.din) {
+                const float* wr = p.W + size_t(k) * p.dout;
+                const uint32_t c = 4 * c4;
+                w.x = c + 0 < p.dout ? wr[c + 0] : 0.f;
+                w.y = c + 1 < p.dout ? wr[c + 1] : 0.f;
+                w.z = c + 2 < p.dout ? wr[c + 2] : 0.f;
+                w.w = c + 3 < p.dout ? wr[c + 3] : 0.f;
+            }
+            Bs[kk][c4] = w;
+        }
+        __syncthreads();
+        const uint32_t kmax = p.din - k0 < 32 ? p.din - k0 : 32;
+        for (uint32_t kk = 0; kk < kmax; ++kk) {
+            const float4 b = Bs[kk][tx];
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                const float a = As[ty * 8 + r][kk];
+                if (a != 0.f) {
+                    acc[r].x = mul_add(acc[r].x, a, b.x);
+                    acc[r].y = mul_add(acc[r].y, a, b.y);
+                    acc[r].z = mul_add(acc[r].z, a, b.z);
+                    acc[r].w = mul_add(acc[r].w, a, b.w);
+                }
+            }
+        }
+        __syncthreads();
+    }
+    if (!col_act) return;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+        const uint32_t row = row0 + ty * 8 + r;
+        if (row >= p.r1) continue;
+        float4 o = acc[r];
+        if (p.relu) {
+            if (o.x < 0.f) o.x = 0.f;
+            if (o.y < 0.f) o.y = 0.f;
+            if (o.z < 0.f) o.z = 0.f;
+            if (o.w < 0.f) o.w = 0.f;
+        }
+        if (4 * tx + 3 >= p.dout) {  // keep padding columns zero
+            if (4 * tx + 0 >= p.dout) o.x = 0.f;
+            if (4 * tx + 1 >= p.dout) o.y = 0.f;
+            if (4 * tx + 2 >= p.dout) o.z = 0.f;
+            if (4 * tx + 3 >= p.dout) o.w = 0.f;
+        }
+        st4(p.out + size_t(row) * p.outstride + 4 * tx, o);
+        if (p.gnext)
+            st4(p.gnext + size_t(row) * p.gnstride + 4 * tx,
+                drop4(p.next_mask, p.orig[row], 4 * tx, p.dout, o));
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Fused backward step for the rows of one chunk:
+//   (1) incoming gradient dh of layer i =
+//         PREV_TOP : dtop[u]  (received from the next stage, or logits grad)
+//         PREV_AGG : drop_{i+1}( sum_v w_uv * bg_{i+1}[v] over done chunks )
+//                    (backward_prev_row of layer i+1, nn.hpp:222-257; bg holds
+//                     (1-a)*dagg for Gcn2Conv and dagg for GcnConv)
+//         PREV_OWN : drop_{i+1}( bg_{i+1}[u] )     (Dense layer i+1)
+//       (+ dh0_run[u] when layer i is global layer 0 of a GCNII, :753-758)
+//   (2) OUT_LAYER: backward_out_row of layer i (nn.hpp:202-218):
+//         dz = relu ? (h>0 ? dh : 0) : dh ; dagg = dz . W^T (ascending j)
+//         Gcn2Conv: dagg = (1-beta) dz + beta dagg ; dh0 += a dagg
+//       and stores dz and bg_i (the gather source of layer i's backward_prev);
+//       OUT_DHIN : stores dh into dh_in (gradient sent to the previous stage).
+// ---------------------------------------------------------------------------
+struct BwdParams {
+    uint32_t r0, r1;
+    const uint64_t* rowptr;
+    const uint2* edges;
+    const float* bgn;
+    const float* bgn_snap;
+    uint32_t bgnstride;
+    uint64_t done;
+    DropKey prev_mask;
+    const float* dtop;
+    uint32_t dtopstride;
+    const uint32_t* orig;
+    uint32_t dh_width;
+    const float* dh0_add;
+    uint32_t dh0stride;
+    const float* h;
+    uint32_t hstride;
+    uint32_t relu;
+    float* dz;
+    uint32_t dzstride;
+    const float* W;
+    uint32_t din, dout;
+    uint32_t need_dagg;
+    uint32_t gcn2;
+    float alpha, oma, beta, omb;
+    float* dh0;
+    float* bg;
+    uint32_t bgstride;
+    float* dh_in;
+    uint32_t dhinstride;
+};
+
+template <int PREV, int OUT>
+__global__ void __launch_bounds__(kBlock) k_bwd(BwdParams p) {
+    extern __shared__ float4 smem4[];
+    float* Wt = reinterpret_cast<float*>(smem4);
+    const uint32_t din4 = (p.din + 3) / 4;
+    if (OUT == OUT_LAYER && p.need_dagg) {
+        // Wt[j][c] = W[c][j]  (dout rows x din4*4 cols)
+        for (uint32_t idx = threadIdx.x; idx < p.dout * din4 * 4; idx += blockDim.x) {
+            const uint32_t j = idx / (din4 * 4), c = idx % (din4 * 4);
+            Wt[idx] = c < p.din ? p.W[size_t(c) * p.dout + j] : 0.f;
+        }
+        __syncthreads();
+    }
+    const float4* Wt4 = reinterpret_cast<const float4*>(Wt);
+    const int lane = threadIdx.x & 31;
+    const bool dh_act = uint32_t(4 * lane) < p.dh_width;
+    const uint32_t nw = gridDim.x * kWarpsPerBlock;
+    const uint32_t dout4 = (p.dout + 3) / 4;
+    for (uint32_t u = p.r0 + blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5); u < p.r1; u += nw) {
+        float4 dh;
+        if (PREV == PREV_TOP) {
+            dh = dh_act ? ld4_rw(p.dtop + size_t(u) * p.dtopstride + 4 * lane) : f4_zero();
+        } else {
+            float4 s;
+            if (PREV == PREV_OWN)
+                s = dh_act ? ld4_rw(p.bgn + size_t(u) * p.bgnstride + 4 * lane) : f4_zero();
+            else
+                s = gather_row<true, PREV == PREV_AGG_HIST>(p.rowptr, p.edges, u, p.bgn, p.bgn_snap,
+                                                            p.bgnstride, p.done, lane, dh_act);
+            dh = drop4(p.prev_mask, p.orig[u], 4 * lane, p.dh_width, s);
+        }
+        if (OUT == OUT_DHIN) {
+            if (dh_act) st4(p.dh_in + size_t(u) * p.dhinstride + 4 * lane, dh);
+            continue;
+        }
+        if (p.dh0_add && dh_act) {
+            const float4 a = ld4_rw(p.dh0_add + size_t(u) * p.dh0stride + 4 * lane);
+            dh.x = __fadd_rn(dh.x, a.x);
+            dh.y = __fadd_rn(dh.y, a.y);
+            dh.z = __fadd_rn(dh.z, a.z);
+            dh.w = __fadd_rn(dh.w, a.w);
+        }
+        float4 dz = dh;
+        if (p.relu) {
+            const float4 h = dh_act ? ld4_rw(p.h + size_t(u) * p.hstride + 4 * lane) : f4_zero();
+            dz.x = h.x > 0.f ? dh.x : 0.f;
+            dz.y = h.y > 0.f ? dh.y : 0.f;
+            dz.z = h.z > 0.f ? dh.z : 0.f;
+            dz.w = h.w > 0.f ? dh.w : 0.f;
+        }
+        if (dh_act) st4(p.dz + size_t(u) * p.dzstride + 4 * lane, dz);
+        if (!p.need_dagg) continue;
+        const bool in_act = uint32_t(4 * lane) < p.din;
+        float4 g = f4_zero();
+        for (uint32_t jb = 0; jb < dout4; ++jb) {
+            const float4 db = shfl4(dz, int(jb));
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint32_t j = 4 * jb + q;
+                if (j < p.dout && in_act) {
+                    const float dj = f4_get(db, q);
+                    const float4 w = Wt4[size_t(j) * din4 + lane];
+                    g.x = mul_add(g.x, dj, w.x);
+                    g.y = mul_add(g.y, dj, w.y);
+                    g.z = mul_add(g.z, dj, w.z);
+                    g.w = mul_add(g.w, dj, w.w);
+                }
+            }
+        }
+        if (!in_act) continue;
+        if (p.gcn2) {
+            g.x = __fadd_rn(__fmul_rn(p.omb, dz.x), __fmul_rn(p.beta, g.x));
+            g.y = __fadd_rn(__fmul_rn(p.omb, dz.y), __fmul_rn(p.beta, g.y));
+            g.z = __fadd_rn(__fmul_rn(p.omb, dz.z), __fmul_rn(p.beta, g.z));
+            g.w = __fadd_rn(__fmul_rn(p.omb, dz.w), __fmul_rn(p.beta, g.w));
+            float* d0 = p.dh0 + size_t(u) * p.dh0stride + 4 * lane;
+            float4 a = ld4_rw(d0);
+            a.x = __fadd_rn(a.x, __fmul_rn(p.alpha, g.x));
+            a.y = __fadd_rn(a.y, __fmul_rn(p.alpha, g.y));
+            a.z = __fadd_rn(a.z, __fmul_rn(p.alpha, g.z));
+            a.w = __fadd_rn(a.w, __fmul_rn(p.alpha, g.w));
+            st4(d0, a);
+            g.x = __fmul_rn(p.oma, g.x);
+            g.y = __fmul_rn(p.oma, g.y);
+            g.z = __fmul_rn(p.oma, g.z);
+            g.w = __fmul_rn(p.oma, g.w);
+        }
+        st4(p.bg + size_t(u) * p.bgstride + 4 * lane, g);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Softmax cross-entropy head (nn.hpp:373-403, engines_impl.hpp:39-51, :725-734).
+// Warp per row, C <= 128. Loss is summed in double; per-block partials are
+// folded in a fixed order so a run is reproducible.
+// ---------------------------------------------------------------------------
+struct XentParams {
+    uint32_t r0, r1, classes;
+    const float* logits;
+    uint32_t lstride;
+    const uint32_t* labels;
+    const uint8_t* split;
+    float inv_count;
+    float* grad;
+    uint32_t gstride;
+    double* part_loss;
+    unsigned long long* part_correct;  // 3 per block
+};
+
+struct RowSoftmax {
+    float mx, sum;
+    uint32_t argmax;
+};
+
+__device__ __forceinline__ RowSoftmax row_softmax(const float4 l, uint32_t classes, int lane) {
+    const uint32_t c0 = 4 * lane;
+    float best = -INFINITY;
+    uint32_t bi = 0xffffffffu;
+    const float vals[4] = {l.x, l.y, l.z, l.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+        if (c0 + q < classes && (bi == 0xffffffffu || vals[q] > best)) {
+            best = vals[q];
+            bi = c0 + q;
+        }
+    for (int off = 16; off > 0; off >>= 1) {
+        const float ob = __shfl_xor_sync(kFull, best, off);
+        const uint32_t oi = __shfl_xor_sync(kFull, bi, off);
+        if (oi != 0xffffffffu && (bi == 0xffffffffu || ob > best || (ob == best && oi < bi))) {
+            best = ob;
+            bi = oi;
+        }
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+        if (c0 + q < classes) s += expf(vals[q] - best);
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(kFull, s, off);
+    return {best, s, bi};
+}
+
+__global__ void __launch_bounds__(kBlock) k_xent_stats(XentParams p) {
+    __shared__ double sl[kWarpsPerBlock];
+    __shared__ unsigned long long sc[kWarpsPerBlock][3];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double loss = 0.0;
+    unsigned long long corr[3] = {0, 0, 0};
+    const uint32_t nw = gridDim.x * kWarpsPerBlock;
+    for (uint32_t v = p.r0 + blockIdx.x * kWarpsPerBlock + warp; v < p.r1; v += nw) {
+        const uint8_t s = p.split[v];
+        if (s == 0 || s > 3) continue;
+        const float4 l = uint32_t(4 * lane) < p.classes
+                             ? ld4_rw(p.logits + size_t(v) * p.lstride + 4 * lane)
+                             : f4_zero();
+        const RowSoftmax r = row_softmax(l, p.classes, lane);
+        const uint32_t label = p.labels[v];
+        if (lane == 0) {
+            corr[s - 1] += r.argmax == label;
+            if (s == 1) {
+                const float ll = p.logits[size_t(v) * p.lstride + label];
+                loss += double(logf(r.sum)) - double(ll - r.mx);
+            }
+        }
+    }
+    if (lane == 0) {
+        sl[warp] = loss;
+        sc[warp][0] = corr[0];
+        sc[warp][1] = corr[1];
+        sc[warp][2] = corr[2];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0;
+        unsigned long long c[3] = {0, 0, 0};
+        for (int w = 0; w < kWarpsPerBlock; ++w) {
+            t += sl[w];
+            for (int k = 0; k < 3; ++k) c[k] += sc[w][k];
+        }
+        p.part_loss[blockIdx.x] = t;
+        for (int k = 0; k < 3; ++k) p.part_correct[3 * blockIdx.x + k] = c[k];
+    }
+}
+
+__global__ void k_xent_fold(const double* part_loss, const unsigned long long* part_correct, uint32_t parts,
+                            double* out_loss, unsigned long long* out_correct) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double t = 0;
+    unsigned long long c[3] = {0, 0, 0};
+    for (uint32_t b = 0; b < parts; ++b) {
+        t += part_loss[b];
+        for (int k = 0; k < 3; ++k) c[k] += part_correct[3 * b + k];
+    }
+    *out_loss = t;
+    for (int k = 0; k < 3; ++k) out_correct[k] = c[k];
+}
+
+// grad = (softmax - onehot) / n_train on train rows, 0 elsewhere (xent_row_grad).
+__global__ void __launch_bounds__(kBlock) k_xent_grad(XentParams p) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t nw = gridDim.x * kWarpsPerBlock;
+    const bool act = uint32_t(4 * lane) < p.classes;
+    for (uint32_t v = p.r0 + blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5); v < p.r1; v += nw) {
+        float4 g = f4_zero();
+        if (p.split[v] == 1) {
+            const float4 l = act ? ld4_rw(p.logits + size_t(v) * p.lstride + 4 * lane) : f4_zero();
+            const RowSoftmax r = row_softmax(l, p.classes, lane);
+            const uint32_t label = p.labels[v];
+            const float vals[4] = {l.x, l.y, l.z, l.w};
+            float outv[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint32_t j = 4 * lane + q;
+                float e = j < p.classes ? __fmul_rn(__fdiv_rn(expf(vals[q] - r.mx), r.sum), p.inv_count) : 0.f;
+                if (j == label) e = __fsub_rn(e, p.inv_count);
+                outv[q] = e;
+            }
+            g = make_float4(outv[0], outv[1], outv[2], outv[3]);
+        }
+        if (act) st4(p.grad + size_t(v) * p.gstride + 4 * lane, g);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Parameter gradients (param_grads_for_rows, nn.hpp:269-293): dW = pre^T dz
+// (x beta for Gcn2Conv), db = sum dz, over ALL rows, once per epoch
+// (engines_impl.hpp:873-876). Split-K over row ranges into a workspace, then a
+// fixed-order fold: deterministic run to run (not bitwise equal to the
+// reference's single ascending sum; tolerance-level, SURVEY §8a' item 7).
+// CTA tile: 64 (k_in) x 64 (out); thread: 4 x 4; rows staged 32 at a time.
+// ---------------------------------------------------------------------------
+struct PgradParams {
+    uint32_t n, rows_per_split;
+    const float* pre;
+    uint32_t prestride;
+    const float* dz;
+    uint32_t dzstride;
+    uint32_t din, dout;
+    float* ws;   // splits x din x dout
+    float* wsb;  // splits x dout
+};
+
+__global__ void __launch_bounds__(256) k_pgrad_partial(PgradParams p) {
+    __shared__ float Ps[32][64];
+    __shared__ float Ds[32][64];
+    const uint32_t split = blockIdx.x;
+    const uint32_t i0 = blockIdx.y * 64, j0 = blockIdx.z * 64;
+    const uint32_t rbeg = split * p.rows_per_split;
+    const uint32_t rend = min(p.n, rbeg + p.rows_per_split);
+    const int ti = threadIdx.x / 16, tj = threadIdx.x % 16;
+    float acc[4][4];
+    float bacc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = 0.f;
+    for (uint32_t r0 = rbeg; r0 < rend; r0 += 32) {
+        for (int idx = threadIdx.x; idx < 32 * 64; idx += 256) {
+            const int r = idx / 64, c = idx % 64;
+            const uint32_t row = r0 + r;
+            Ps[r][c] = (row < rend && i0 + c < p.din) ? p.pre[size_t(row) * p.prestride + i0 + c] : 0.f;
+            Ds[r][c] = (row < rend && j0 + c < p.dout) ? p.dz[size_t(row) * p.dzstride + j0 + c] : 0.f;
+        }
+        __syncthreads();
+#pragma unroll 4
+        for (int r = 0; r < 32; ++r) {
+            float pa[4], db[4];
+#pragma unroll
+            for (int a = 0; a < 4; ++a) pa[a] = Ps[r][ti * 4 + a];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) db[b] = Ds[r][tj * 4 + b];
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) acc[a][b] = fmaf(pa[a], db[b], acc[a][b]);
+            if (ti == 0)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) bacc[b] += db[b];
+        }
+        __syncthreads();
+    }
+    float* w = p.ws + size_t(split) * p.din * p.dout;
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        const uint32_t i = i0 + ti * 4 + a;
+        if (i >= p.din) continue;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const uint32_t j = j0 + tj * 4 + b;
+            if (j < p.dout) w[size_t(i) * p.dout + j] = acc[a][b];
+        }
+    }
+    if (blockIdx.y == 0 && ti == 0 && p.wsb)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const uint32_t j = j0 + tj * 4 + b;
+            if (j < p.dout) p.wsb[size_t(split) * p.dout + j] = bacc[b];
+        }
+}
+
+__global__ void k_pgrad_fold(const float* ws, const float* wsb, uint32_t splits, uint32_t din,
+                             uint32_t dout, float scale, uint32_t apply_scale, float* gW, float* gb) {
+    const uint32_t total = din * dout;
+    for (uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total + dout;
+         idx += gridDim.x * blockDim.x) {
+        if (idx < total) {
+            float s = 0.f;
+            for (uint32_t k = 0; k < splits; ++k) s += ws[size_t(k) * total + idx];
+            gW[idx] = apply_scale ? __fmul_rn(s, scale) : s;
+        } else if (wsb && gb) {
+            const uint32_t j = idx - total;
+            float s = 0.f;
+            for (uint32_t k = 0; k < splits; ++k) s += wsb[size_t(k) * dout + j];
+            gb[j] = s;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Adam / SGD (Optimizer::update, nn.hpp:474-490) with the reference's float
+// operation order; c1/c2 are computed on the host in double and rounded.
+// ---------------------------------------------------------------------------
+struct AdamParams {
+    float* p;
+    const float* g;
+    float* m;
+    float* v;
+    uint32_t n;
+    uint32_t sgd;
+    float lr, b1, b2, omb1, omb2, eps, c1, c2;
+};
+
+__global__ void k_adam(AdamParams a) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += gridDim.x * blockDim.x) {
+        const float g = a.g[i];
+        if (a.sgd) {
+            a.p[i] = __fsub_rn(a.p[i], __fmul_rn(a.lr, g));
+            continue;
+        }
+        const float m = __fadd_rn(__fmul_rn(a.b1, a.m[i]), __fmul_rn(a.omb1, g));
+        const float v = __fadd_rn(__fmul_rn(a.b2, a.v[i]), __fmul_rn(__fmul_rn(a.omb2, g), g));
+        a.m[i] = m;
+        a.v[i] = v;
+        const float mhat = __fdiv_rn(m, a.c1);
+        const float vhat = __fdiv_rn(v, a.c2);
+        a.p[i] = __fsub_rn(a.p[i], __fdiv_rn(__fmul_rn(a.lr, mhat), __fadd_rn(__fsqrt_rn(vhat), a.eps)));
+    }
+}
+
+}  // namespace gp

@@ -1,0 +1,302 @@
+// gs_* — flat C wrappers over the C++ API (include/gnnpipe.h, host section).
+// Exceptions map to the gp_status codes of the reference's error classes.
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "gnnsim_b200.hpp"
+
+using namespace gnnsim;
+
+struct gs_dataset {
+    Dataset d;
+};
+struct gs_result {
+    TrainResult<float> r;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        f();
+        g_err.clear();
+        return GP_OK;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return GP_EINVAL;
+    } catch (const NumericError& e) {
+        g_err = e.what();
+        return GP_ENUMERIC;
+    } catch (const FabricError& e) {
+        g_err = e.what();
+        return GP_EFABRIC;
+    } catch (const GpError& e) {
+        g_err = e.what();
+        return e.code;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return GP_ERUNTIME;
+    }
+}
+
+ModelConfig model_of(const gs_model_config* m) {
+    if (!m) throw std::invalid_argument("null model config");
+    ModelConfig c;
+    switch (m->kind) {
+        case 0: c.kind = ModelKind::GCN; break;
+        case 1: c.kind = ModelKind::Sage; break;
+        case 2: c.kind = ModelKind::GCNII; break;
+        default: throw std::invalid_argument("unknown model kind");
+    }
+    c.layers = m->layers;
+    c.hidden = m->hidden;
+    c.dropout = m->dropout;
+    c.gcnii_alpha = m->gcnii_alpha;
+    c.gcnii_lambda = m->gcnii_lambda;
+    c.self_loops = m->self_loops != 0;
+    return c;
+}
+
+TrainOptions<float> options_of(const gs_train_options* o) {
+    if (!o) throw std::invalid_argument("null train options");
+    TrainOptions<float> t;
+    t.model = model_of(&o->model);
+    t.optimizer.kind = o->optimizer == 1 ? OptimizerKind::Sgd : OptimizerKind::Adam;
+    t.optimizer.lr = o->lr;
+    t.optimizer.beta1 = o->beta1;
+    t.optimizer.beta2 = o->beta2;
+    t.optimizer.eps = o->eps;
+    t.epochs = o->epochs;
+    t.seed = o->seed;
+    t.staleness.shuffle_chunks = o->shuffle_chunks != 0;
+    t.staleness.fix_alpha = o->fix_alpha;
+    t.staleness.historical_gradients = o->historical_gradients != 0;
+    t.staleness.synchronous_mode = o->synchronous_mode != 0;
+    t.device = o->device;
+    t.profile = o->profile != 0;
+    return t;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* gs_last_error(void) { return g_err.c_str(); }
+
+int gs_dataset_from_edges(uint32_t n, const uint32_t* uv, uint64_t m, const float* x, uint32_t F,
+                          const uint32_t* labels, uint32_t C, const uint8_t* split, gs_dataset** out) {
+    return guarded([&]() {
+        auto* h = new gs_dataset();
+        std::unique_ptr<gs_dataset> own(h);
+        std::vector<std::pair<VertexId, VertexId>> e(m);
+        for (uint64_t i = 0; i < m; ++i) e[i] = {uv[2 * i], uv[2 * i + 1]};
+        h->d.graph = build_graph(n, std::move(e));
+        h->d.features = MatF(n, F);
+        if (x && F) std::memcpy(h->d.features.data(), x, size_t(n) * F * 4);
+        h->d.num_classes = C;
+        h->d.labels.assign(labels, labels + n);
+        h->d.split.assign(split, split + n);
+        h->d.validate();
+        *out = own.release();
+    });
+}
+
+int gs_dataset_synthetic_er(uint32_t n, double p, uint64_t gseed, uint32_t F, uint32_t C, uint64_t fseed,
+                            gs_dataset** out) {
+    return guarded([&]() {
+        auto own = std::make_unique<gs_dataset>();
+        own->d = synthetic_er_dataset(n, p, gseed, F, C, fseed);
+        *out = own.release();
+    });
+}
+
+int gs_dataset_load(const char* dir, gs_dataset** out) {
+    return guarded([&]() {
+        auto own = std::make_unique<gs_dataset>();
+        own->d = load_dataset(dir);
+        *out = own.release();
+    });
+}
+
+int gs_dataset_save(const gs_dataset* d, const char* dir) {
+    return guarded([&]() { save_dataset(d->d, dir); });
+}
+
+void gs_dataset_free(gs_dataset* d) { delete d; }
+
+int gs_dataset_shape(const gs_dataset* d, uint32_t* n, uint64_t* m, uint32_t* F, uint32_t* C) {
+    return guarded([&]() {
+        if (n) *n = d->d.graph.num_vertices;
+        if (m) *m = d->d.graph.num_edges;
+        if (F) *F = d->d.num_features();
+        if (C) *C = d->d.num_classes;
+    });
+}
+
+int gs_dataset_graph(const gs_dataset* d, uint64_t* offsets, uint32_t* neighbors, uint32_t* degrees) {
+    return guarded([&]() {
+        const Graph& g = d->d.graph;
+        if (offsets) std::memcpy(offsets, g.csr_offsets.data(), g.csr_offsets.size() * 8);
+        if (neighbors) std::memcpy(neighbors, g.csr_neighbors.data(), g.csr_neighbors.size() * 4);
+        if (degrees) std::memcpy(degrees, g.degrees.data(), g.degrees.size() * 4);
+    });
+}
+
+int gs_dataset_arrays(const gs_dataset* d, float* x, uint32_t* labels, uint8_t* split) {
+    return guarded([&]() {
+        if (x) std::memcpy(x, d->d.features.data(), d->d.features.size() * 4);
+        if (labels) std::memcpy(labels, d->d.labels.data(), d->d.labels.size() * 4);
+        if (split) std::memcpy(split, d->d.split.data(), d->d.split.size());
+    });
+}
+
+int gs_normalize_adjacency(const gs_dataset* d, int self_loops, uint64_t* offsets, uint32_t* cols, float* vals) {
+    return guarded([&]() {
+        auto m = normalize_adjacency<float>(d->d.graph, self_loops != 0);
+        if (offsets) std::memcpy(offsets, m.offsets.data(), m.offsets.size() * 8);
+        if (cols) std::memcpy(cols, m.cols.data(), m.cols.size() * 4);
+        if (vals) std::memcpy(vals, m.vals.data(), m.vals.size() * 4);
+    });
+}
+
+int gs_make_chunks(const gs_dataset* d, uint32_t K, uint64_t seed, uint32_t* chunk_of) {
+    return guarded([&]() {
+        auto plan = make_chunks(d->d.graph, K, seed);
+        std::memcpy(chunk_of, plan.chunk_of.data(), plan.chunk_of.size() * 4);
+    });
+}
+
+int gs_partition_vertices(const gs_dataset* d, uint32_t parts, uint64_t seed, uint32_t* assignment,
+                          uint64_t* edge_cut, uint64_t* boundary_total) {
+    return guarded([&]() {
+        auto p = partition_vertices(d->d.graph, parts, seed);
+        if (assignment) std::memcpy(assignment, p.assignment.data(), p.assignment.size() * 4);
+        if (edge_cut) *edge_cut = p.edge_cut(d->d.graph);
+        if (boundary_total) *boundary_total = p.boundary_total();
+    });
+}
+
+int gs_shuffle_chunk_order(uint32_t K, uint64_t epoch, uint64_t seed, uint32_t* order) {
+    return guarded([&]() {
+        ChunkPlan plan;
+        plan.num_chunks = K;
+        auto o = shuffle_chunk_order(plan, epoch, seed);
+        std::memcpy(order, o.data(), o.size() * 4);
+    });
+}
+
+int gs_make_stage_assignment(uint32_t layers, uint32_t stages, uint32_t* ranges) {
+    return guarded([&]() {
+        auto sa = make_stage_assignment(layers, stages);
+        for (uint32_t s = 0; s < stages; ++s) {
+            ranges[2 * s] = sa.begin(s);
+            ranges[2 * s + 1] = sa.end(s);
+        }
+    });
+}
+
+int gs_num_layers(const gs_model_config* m, uint32_t* L) {
+    return guarded([&]() { *L = uint32_t(build_layer_specs(model_of(m), 1, 1).size()); });
+}
+
+int gs_build_layer_specs(const gs_model_config* m, uint32_t F, uint32_t C, gp_layer_spec* out) {
+    return guarded([&]() {
+        auto specs = build_layer_specs(model_of(m), F, C);
+        for (size_t l = 0; l < specs.size(); ++l) {
+            out[l].kind = uint32_t(specs[l].kind);
+            out[l].in_dim = specs[l].in_dim;
+            out[l].out_dim = specs[l].out_dim;
+            out[l].relu = specs[l].relu;
+            out[l].alpha = specs[l].alpha;
+            out[l].beta = specs[l].beta;
+        }
+    });
+}
+
+int gs_init_params(const gs_model_config* m, uint32_t F, uint32_t C, uint64_t seed, float* flat) {
+    return guarded([&]() {
+        auto specs = build_layer_specs(model_of(m), F, C);
+        auto ps = init_params<float>(specs, seed);
+        size_t at = 0;
+        for (const auto& p : ps) {
+            std::memcpy(flat + at, p.weight.data(), p.weight.size() * 4);
+            at += p.weight.size();
+            std::memcpy(flat + at, p.bias.data(), p.bias.size() * 4);
+            at += p.bias.size();
+        }
+    });
+}
+
+int gs_train_pipeline(const gs_dataset* d, const uint32_t* chunk_of, uint32_t K, uint32_t S,
+                      const gs_train_options* o, gs_result** out) {
+    return guarded([&]() {
+        TrainOptions<float> opt = options_of(o);
+        const uint32_t L = uint32_t(build_layer_specs(opt.model, d->d.num_features(), d->d.num_classes).size());
+        ChunkPlan plan = chunk_plan_from_assignment(d->d.num_vertices(),
+                                                    std::vector<uint32_t>(chunk_of, chunk_of + d->d.num_vertices()));
+        if (plan.num_chunks != K) throw std::invalid_argument("chunk_of does not use exactly K chunks");
+        auto own = std::make_unique<gs_result>();
+        own->r = train_pipeline<float>(d->d, plan, make_stage_assignment(L, S), opt);
+        *out = own.release();
+    });
+}
+
+int gs_train_sequential(const gs_dataset* d, const gs_train_options* o, gs_result** out) {
+    return guarded([&]() {
+        auto own = std::make_unique<gs_result>();
+        own->r = train_sequential<float>(d->d, options_of(o));
+        *out = own.release();
+    });
+}
+
+int gs_result_metrics(const gs_result* r, uint32_t* epochs, double* metrics, uint64_t* comm) {
+    return guarded([&]() {
+        if (epochs) *epochs = uint32_t(r->r.metrics.size());
+        for (size_t t = 0; t < r->r.metrics.size(); ++t) {
+            const auto& m = r->r.metrics[t];
+            if (metrics) {
+                double* row = metrics + 7 * t;
+                row[0] = m.epoch;
+                row[1] = m.train_loss;
+                row[2] = m.train_acc;
+                row[3] = m.val_acc;
+                row[4] = m.test_acc;
+                row[5] = m.wall_time_s;
+                row[6] = m.bubble_fraction;
+            }
+            if (comm) {
+                comm[3 * t] = m.comm_bytes_graph;
+                comm[3 * t + 1] = m.comm_bytes_pipeline;
+                comm[3 * t + 2] = m.comm_bytes_weightsync;
+            }
+        }
+    });
+}
+
+int gs_result_params(const gs_result* r, float* flat) {
+    return guarded([&]() {
+        size_t at = 0;
+        for (const auto& p : r->r.params) {
+            std::memcpy(flat + at, p.weight.data(), p.weight.size() * 4);
+            at += p.weight.size();
+            std::memcpy(flat + at, p.bias.data(), p.bias.size() * 4);
+            at += p.bias.size();
+        }
+    });
+}
+
+int gs_result_profile(const gs_result* r, gp_profile* out) {
+    return guarded([&]() { *out = r->r.profile; });
+}
+
+int gs_result_peak_bytes(const gs_result* r, uint64_t* out) {
+    return guarded([&]() { *out = r->r.peak_buffer_bytes; });
+}
+
+void gs_result_free(gs_result* r) { delete r; }
+
+}  // extern "C"

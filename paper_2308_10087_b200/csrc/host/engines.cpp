@@ -1,0 +1,319 @@
+// Trainers of the C++ API (engines.hpp:79-99) on the GPU engine.
+//
+// train_pipeline<float> keeps the reference's contract (engines_impl.hpp:515-537
+// validation, :901-907 result assembly) and runs one gp_ctx per stage, one host
+// thread per stage (the reference's Fabric::Mode::Concurrent shape,
+// fabric.cpp:401-422). The chunk schedule (shuffle_chunk_order) is computed on
+// the host and handed to every stage, so schedule order is bit-exact. Stage
+// boundaries use gp_link_local (device-to-device copies ordered by CUDA events);
+// the one-process-per-GPU NCCL path is driven directly through the C-ABI
+// (bench.py).
+#include <chrono>
+#include <condition_variable>
+#include <cstring>
+#include <exception>
+#include <mutex>
+#include <thread>
+#include <type_traits>
+
+#include "gnnsim_b200.hpp"
+
+namespace gnnsim {
+
+namespace {
+
+void check(gp_status s, gp_ctx* ctx, const char* what) {
+    if (s == GP_OK) return;
+    const std::string msg = std::string(what) + ": " + gp_last_error(ctx);
+    switch (s) {
+        case GP_EINVAL: throw std::invalid_argument(msg);
+        case GP_ENUMERIC: throw NumericError(msg);
+        case GP_EFABRIC: throw FabricError(msg);
+        default: throw GpError(s, msg);
+    }
+}
+
+// Epoch barrier that can be aborted when a stage thread fails.
+class StageBarrier {
+  public:
+    explicit StageBarrier(uint32_t n) : n_(n) {}
+    bool arrive_and_wait() {
+        std::unique_lock<std::mutex> lk(mu_);
+        if (aborted_) return false;
+        const uint64_t gen = gen_;
+        if (++waiting_ == n_) {
+            waiting_ = 0;
+            ++gen_;
+            cv_.notify_all();
+            return true;
+        }
+        cv_.wait(lk, [&] { return gen_ != gen || aborted_; });
+        return !aborted_;
+    }
+    void abort() {
+        std::lock_guard<std::mutex> lk(mu_);
+        aborted_ = true;
+        cv_.notify_all();
+    }
+
+  private:
+    std::mutex mu_;
+    std::condition_variable cv_;
+    uint32_t n_, waiting_ = 0;
+    uint64_t gen_ = 0;
+    bool aborted_ = false;
+};
+
+gp_layer_spec to_gp(const LayerSpec& s) {
+    gp_layer_spec g{};
+    g.kind = uint32_t(s.kind);
+    g.in_dim = s.in_dim;
+    g.out_dim = s.out_dim;
+    g.relu = s.relu ? 1u : 0u;
+    g.alpha = s.alpha;
+    g.beta = s.beta;
+    return g;
+}
+
+struct Ctxs {
+    std::vector<gp_ctx*> v;
+    ~Ctxs() {
+        for (auto* c : v) gp_destroy(c);
+    }
+};
+
+void validate_run(const Dataset& ds, const ChunkPlan& plan, const StageAssignment& sa, uint32_t L) {
+    const uint32_t S = sa.num_stages;
+    if (plan.chunk_of.size() != ds.num_vertices())
+        throw std::invalid_argument("train_hybrid: plan/partition do not cover the graph");
+    if (plan.num_chunks == 0) throw std::invalid_argument("train_pipeline: empty chunk plan");
+    if (sa.ranges.size() != S || S == 0 || sa.begin(0) != 0 || sa.end(S - 1) != L)
+        throw std::invalid_argument("train_hybrid: stage ranges must cover all layers");
+    for (uint32_t s = 0; s + 1 < S; ++s)
+        if (sa.end(s) != sa.begin(s + 1) || sa.end(s) <= sa.begin(s))
+            throw std::invalid_argument("train_hybrid: stage ranges must be consecutive");
+    if (sa.end(S - 1) <= sa.begin(S - 1)) throw std::invalid_argument("train_hybrid: empty stage");
+}
+
+}  // namespace
+
+namespace {
+
+TrainResult<float> run_pipeline_f32(const Dataset& ds, const ChunkPlan& plan, const StageAssignment& sa,
+                                    const TrainOptions<float>& opt) {
+    ds.validate();
+    const auto specs = build_layer_specs(opt.model, ds.num_features(), ds.num_classes);
+    const uint32_t L = uint32_t(specs.size());
+    validate_run(ds, plan, sa, L);
+    const uint32_t S = sa.num_stages, K = plan.num_chunks;
+    const VertexId n = ds.num_vertices();
+    uint64_t split_count[3] = {0, 0, 0};
+    for (uint8_t s : ds.split)
+        if (s >= 1 && s <= 3) ++split_count[s - 1];
+    if (split_count[0] == 0) throw std::invalid_argument("train_hybrid: empty train mask");
+    for (const auto& s : specs)
+        if (s.kind == LayerKind::SageConv)
+            throw std::invalid_argument("SageConv is outside the GPU engine's scope (GCN/GCNII only)");
+
+    std::vector<gp_layer_spec> gspecs;
+    for (const auto& s : specs) gspecs.push_back(to_gp(s));
+    const auto adj = normalize_adjacency<float>(ds.graph, opt.model.self_loops);
+    auto params = init_params<float>(specs, opt.seed);
+
+    int ndev = 0;
+    gp_device_count(&ndev);
+    if (ndev == 0) throw GpError(GP_ECUDA, "train_pipeline: no CUDA device (the GPU engine has no CPU fallback)");
+
+    Ctxs ctx;
+    for (uint32_t s = 0; s < S; ++s) {
+        gp_stage_config c{};
+        c.device = opt.device >= 0 ? opt.device : int(s % uint32_t(ndev));
+        c.num_vertices = n;
+        c.num_chunks = K;
+        c.num_stages = S;
+        c.stage = s;
+        c.layer_begin = sa.begin(s);
+        c.layer_end = sa.end(s);
+        c.num_layers = L;
+        c.specs = gspecs.data();
+        c.hidden = opt.model.hidden;
+        c.num_classes = ds.num_classes;
+        c.dropout = opt.model.dropout;
+        c.seed = opt.seed;
+        c.optimizer = opt.optimizer.kind == OptimizerKind::Sgd ? 1u : 0u;
+        c.lr = opt.optimizer.lr;
+        c.beta1 = opt.optimizer.beta1;
+        c.beta2 = opt.optimizer.beta2;
+        c.eps = opt.optimizer.eps;
+        c.fix_alpha = opt.staleness.fix_alpha;
+        c.historical_gradients = opt.staleness.historical_gradients ? 1u : 0u;
+        c.synchronous_mode = opt.staleness.synchronous_mode ? 1u : 0u;
+        gp_ctx* g = nullptr;
+        check(gp_create(&c, &g), nullptr, "gp_create");
+        ctx.v.push_back(g);
+        if (s == 0 || c.device != (opt.device >= 0 ? opt.device : 0)) {
+            check(gp_upload_graph(g, adj.offsets.data(), adj.cols.data(), adj.vals.data(), adj.cols.size(),
+                                  plan.chunk_of.data()),
+                  g, "gp_upload_graph");
+        } else {
+            check(gp_share_graph(g, ctx.v[0]), g, "gp_share_graph");
+        }
+        if (s == 0) check(gp_upload_features(g, ds.features.data(), ds.num_features()), g, "gp_upload_features");
+        if (s + 1 == S) check(gp_upload_labels(g, ds.labels.data(), ds.split.data()), g, "gp_upload_labels");
+        for (uint32_t l = sa.begin(s); l < sa.end(s); ++l)
+            check(gp_set_layer_params(g, l, params[l].weight.data(), params[l].bias.empty() ? nullptr : params[l].bias.data()),
+                  g, "gp_set_layer_params");
+        if (opt.profile) gp_set_profiling(g, 1);
+        if (s > 0) check(gp_link_local(ctx.v[s - 1], g), g, "gp_link_local");
+    }
+
+    const uint32_t T = opt.epochs;
+    std::vector<std::vector<gp_epoch_stats>> stats(S, std::vector<gp_epoch_stats>(T));
+    std::vector<std::exception_ptr> errs(S);
+    StageBarrier barrier(S);
+    auto body = [&](uint32_t s) {
+        try {
+            for (uint32_t t = 1; t <= T; ++t) {
+                if (!barrier.arrive_and_wait()) return;  // epoch entry sync (engines_impl.hpp:668)
+                std::vector<uint32_t> order(K);
+                for (uint32_t k = 0; k < K; ++k) order[k] = k;
+                if (opt.staleness.shuffle_chunks) order = shuffle_chunk_order(plan, t, opt.seed);
+                check(gp_run_epoch(ctx.v[s], t, order.data(), &stats[s][t - 1]), ctx.v[s], "gp_run_epoch");
+                if (s + 1 == S) {
+                    const double loss = stats[s][t - 1].loss_sum / double(split_count[0]);
+                    if (!std::isfinite(loss))
+                        throw NumericError("non-finite training loss at epoch " + std::to_string(t));
+                }
+            }
+        } catch (...) {
+            errs[s] = std::current_exception();
+            barrier.abort();
+            for (auto* c : ctx.v) gp_abort(c);
+        }
+    };
+    if (S == 1) {
+        body(0);
+    } else {
+        std::vector<std::thread> pool;
+        for (uint32_t s = 0; s < S; ++s) pool.emplace_back(body, s);
+        for (auto& th : pool) th.join();
+    }
+    // Prefer the root cause over "transport aborted" follow-on errors.
+    for (uint32_t pass = 0; pass < 2; ++pass)
+        for (uint32_t s = 0; s < S; ++s) {
+            if (!errs[s]) continue;
+            if (pass == 0) {
+                try {
+                    std::rethrow_exception(errs[s]);
+                } catch (const FabricError& e) {
+                    if (std::string(e.what()).find("aborted") != std::string::npos) continue;
+                    throw;
+                }
+            }
+            std::rethrow_exception(errs[s]);
+        }
+
+    TrainResult<float> res;
+    std::vector<uint32_t> node_of = opt.fabric.node_of;
+    if (node_of.empty())
+        for (uint32_t w = 0; w < S; ++w) node_of.push_back(w / 4);  // assign_groups(S, 4, S, 1)
+    res.metrics.resize(T);
+    res.comm.resize(T);
+    for (uint32_t t = 0; t < T; ++t) {
+        EpochMetrics& m = res.metrics[t];
+        const gp_epoch_stats& q = stats[S - 1][t];
+        m.epoch = t + 1;
+        m.train_loss = split_count[0] ? q.loss_sum / double(split_count[0]) : 0.0;  // :164-171
+        m.train_acc = split_count[0] ? double(q.correct[0]) / double(split_count[0]) : 0.0;
+        m.val_acc = split_count[1] ? double(q.correct[1]) / double(split_count[1]) : 0.0;
+        m.test_acc = split_count[2] ? double(q.correct[2]) / double(split_count[2]) : 0.0;
+        EpochComm& e = res.comm[t];
+        double span = 0, busy = 0;
+        for (uint32_t s = 0; s < S; ++s) {
+            const auto& st = stats[s][t];
+            span = std::max(span, double(st.epoch_ms));
+            busy += st.busy_ms;
+            // forward goes s -> s+1, backward s -> s-1
+            if (s + 1 < S) e.by_tag_link[0][node_of[s] == node_of[s + 1] ? 0 : 1] += st.bytes_sent[0];
+            if (s > 0) e.by_tag_link[1][node_of[s] == node_of[s - 1] ? 0 : 1] += st.bytes_sent[1];
+        }
+        m.comm_bytes_graph = e.graph_bytes();
+        m.comm_bytes_pipeline = e.pipeline_bytes();
+        m.comm_bytes_weightsync = e.weight_sync_bytes();
+        m.wall_time_s = span / 1000.0;
+        m.bubble_fraction = (opt.profile && span > 0) ? std::max(0.0, 1.0 - busy / (span * S)) : 0.0;
+    }
+    for (uint32_t s = 0; s < S; ++s) {
+        WorkerParams<float> wp;
+        wp.layer_begin = sa.begin(s);
+        wp.layer_end = sa.end(s);
+        for (uint32_t l = sa.begin(s); l < sa.end(s); ++l) {
+            LayerParams<float> p;
+            p.weight = MatF(specs[l].k_in(), specs[l].out_dim);
+            if (specs[l].has_bias()) p.bias.assign(specs[l].out_dim, 0.f);
+            check(gp_get_layer_params(ctx.v[s], l, p.weight.data(), p.bias.empty() ? nullptr : p.bias.data()),
+                  ctx.v[s], "gp_get_layer_params");
+            res.params.push_back(p);
+            wp.params.push_back(std::move(p));
+        }
+        res.worker_params.push_back(std::move(wp));
+        uint64_t bytes = 0;
+        gp_device_bytes(ctx.v[s], &bytes);
+        res.peak_buffer_bytes = std::max(res.peak_buffer_bytes, bytes);
+        gp_profile pr{};
+        gp_get_profile(ctx.v[s], &pr);
+        for (int k = 0; k < GP_K_NUM; ++k) {
+            res.profile.ms[k] += pr.ms[k];
+            res.profile.launches[k] += pr.launches[k];
+            res.profile.alg_bytes[k] += pr.alg_bytes[k];
+            res.profile.flops[k] += pr.flops[k];
+            res.profile.gather_bytes[k] += pr.gather_bytes[k];
+        }
+    }
+    return res;
+}
+
+}  // namespace
+
+template <typename T>
+TrainResult<T> train_pipeline(const Dataset& ds, const ChunkPlan& plan, const StageAssignment& sa,
+                              const TrainOptions<T>& opt) {
+    static_assert(std::is_same_v<T, float>, "the GPU engine computes in fp32");
+    return run_pipeline_f32(ds, plan, sa, opt);
+}
+
+template <typename T>
+TrainResult<T> train_sequential(const Dataset& ds, const TrainOptions<T>& opt) {
+    // The S=1, K=1 pipeline reproduces train_sequential bitwise in the
+    // reference (test_engines.cpp:103-113); it is the GPU engine's full-graph mode.
+    ds.validate();
+    const uint32_t L = uint32_t(build_layer_specs(opt.model, ds.num_features(), ds.num_classes).size());
+    ChunkPlan whole = chunk_plan_from_assignment(ds.num_vertices(), std::vector<uint32_t>(ds.num_vertices(), 0));
+    return train_pipeline<T>(ds, whole, make_stage_assignment(L, 1), opt);
+}
+
+template <typename T>
+TrainResult<T> train_hybrid(const Dataset& ds, const Partition& part, const ChunkPlan& plan,
+                            const StageAssignment& sa, const GroupMap& gmap, const TrainOptions<T>& opt) {
+    ds.validate();
+    const uint32_t S = sa.num_stages, G = gmap.group_size;
+    if (gmap.num_workers != S * G || gmap.num_groups() != S)
+        throw std::invalid_argument("train_hybrid: worker count != stages * group_size");
+    if (part.num_parts != G) throw std::invalid_argument("train_hybrid: partition parts != group size");
+    if (plan.chunk_of.size() != ds.num_vertices() || part.assignment.size() != ds.num_vertices())
+        throw std::invalid_argument("train_hybrid: plan/partition do not cover the graph");
+    if (G != 1)
+        throw std::invalid_argument(
+            "train_hybrid: graph-parallel groups (G > 1) are not implemented by the GPU engine yet");
+    TrainOptions<T> o = opt;
+    if (o.fabric.node_of.empty()) o.fabric.node_of = gmap.node_of;
+    return train_pipeline<T>(ds, plan, sa, o);
+}
+
+template TrainResult<float> train_sequential<float>(const Dataset&, const TrainOptions<float>&);
+template TrainResult<float> train_pipeline<float>(const Dataset&, const ChunkPlan&, const StageAssignment&,
+                                                  const TrainOptions<float>&);
+template TrainResult<float> train_hybrid<float>(const Dataset&, const Partition&, const ChunkPlan&,
+                                                const StageAssignment&, const GroupMap&, const TrainOptions<float>&);
+
+}  // namespace gnnsim

@@ -1,0 +1,56 @@
+"""Generate the golden fixtures in tests/golden/ from the reference itself.
+
+Runs oracle/_ref/ref_driver (the unmodified gnnsim sources compiled by oracle/Makefile) and
+stores its outputs as small .npz files. Re-run after changing a scenario:
+
+    make -C oracle && python tests/golden/make_golden.py
+"""
+import os
+import sys
+import tempfile
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+from oracle.blob import run_ref  # noqa: E402
+
+# Dataset spec strings are passed verbatim to both the reference and the product.
+ER500 = "er:500:0.02:3:16:5:9"
+ER300W = "er:300:0.03:11:40:7:2"  # F=40 > nothing special; used for GCN first layer width != H
+
+SCENARIOS = {
+    # name: (cmd, kwargs)
+    "graph_er500": ("graph", dict(spec=ER500)),
+    "graph_g8": ("graph", dict(spec="g8:2:2")),
+    "chunks_er500_k1": ("chunks", dict(spec=ER500, K=1, seed=5)),
+    "chunks_er500_k4": ("chunks", dict(spec=ER500, K=4, seed=5)),
+    "chunks_er500_k7": ("chunks", dict(spec=ER500, K=7, seed=5)),
+    "graph_sbm4x100": ("graph", dict(spec="sbm:4:100:0.2:0.002:31")),
+    "chunks_sbm4x100_k4": ("chunks", dict(spec="sbm:4:100:0.2:0.002:31", K=4, seed=31)),
+    "shuffle_k8": ("shuffle", dict(K=8, seed=3, epochs=20)),
+    "forward_gcn": ("forward", dict(spec=ER500, model="gcn", layers=3, hidden=16, seed=7, epoch=1)),
+    "forward_gcnii": ("forward", dict(spec=ER500, model="gcnii", layers=5, hidden=16, seed=7, epoch=1)),
+    "train_gcn_s1k1": ("train", dict(spec=ER500, model="gcn", layers=4, hidden=16, S=1, K=1, epochs=10, seed=42)),
+    "train_gcn_s2k4": ("train", dict(spec=ER500, model="gcn", layers=4, hidden=16, S=2, K=4, chunk_seed=3,
+                                     epochs=10, seed=42, fix_alpha=3)),
+    "train_gcnii_s2k4": ("train", dict(spec=ER500, model="gcnii", layers=6, hidden=16, S=2, K=4, chunk_seed=3,
+                                       epochs=10, seed=43, fix_alpha=3)),
+    "train_gcnii_s1k4_sync": ("train", dict(spec=ER500, model="gcnii", layers=6, hidden=16, S=1, K=4,
+                                            chunk_seed=3, epochs=10, seed=44, sync=1)),
+    "train_gcn_s3k6_w40": ("train", dict(spec=ER300W, model="gcn", layers=6, hidden=24, S=3, K=6, chunk_seed=1,
+                                         epochs=8, seed=45, fix_alpha=2)),
+}
+
+
+def main():
+    with tempfile.TemporaryDirectory() as td:
+        for name, (cmd, kw) in SCENARIOS.items():
+            d = run_ref(cmd, os.path.join(td, name + ".blob"), **kw)
+            meta = {"cmd": cmd, **{k: str(v) for k, v in kw.items()}}
+            np.savez_compressed(os.path.join(HERE, name + ".npz"), __meta__=np.array(repr(meta)), **d)
+            print(name, sorted(d)[:6], "...")
+
+
+if __name__ == "__main__":
+    main()
