@@ -716,10 +716,8 @@ struct Stage {
                 prev = PREV_OWN;
             }
         }
-        if (d.l == 0 && needs_h0) {
-            p.dh0_add = dh0;
-            p.dh0stride = pad8(H);
-        }
+        p.dh0stride = pad8(H);
+        if (d.l == 0 && needs_h0) p.dh0_add = dh0;
         p.h = d.h;
         p.hstride = d.sout;
         p.relu = d.spec.relu;
