@@ -173,6 +173,11 @@ gp_status gp_set_profiling(gp_ctx* ctx, int enable);
 gp_status gp_get_profile(gp_ctx* ctx, gp_profile* out);
 gp_status gp_reset_profile(gp_ctx* ctx);
 gp_status gp_device_bytes(gp_ctx* ctx, uint64_t* out); /* stash footprint */
+/* Device timestamps on the stage's compute stream (bench timing): record event
+ * `slot` (0..15); gp_elapsed synchronises and returns ms between two slots. */
+gp_status gp_mark(gp_ctx* ctx, uint32_t slot);
+gp_status gp_elapsed(gp_ctx* ctx, uint32_t slot_a, uint32_t slot_b, float* ms);
+gp_status gp_synchronize(gp_ctx* ctx);
 
 /* ====================== host API (libgnnsim_b200.so) ===================== */
 

@@ -369,73 +369,80 @@ void cmd_save(const Args& a) {
 }
 
 // CPU baseline sample (bench.py --impl reference / cpu_baseline). Times the
-// reference's own per-row kernels (nn.hpp:159-257, param_grads nn.hpp:269-293)
-// for one Gcn2Conv/GcnConv layer over a bounded row sample, split across T
-// threads (rows are independent: nn.hpp kernels are pure per row), and
-// extrapolates to a full epoch: per-row cost x N x aggregating layers plus the
-// measured dense layers. Reports seconds per epoch.
+// reference's own per-row kernels — kernel::forward_row, backward_out_row,
+// backward_prev_row (nn.hpp:159-257) and param_grads_for_rows (nn.hpp:269-293) —
+// plus DropMask::make (nn.hpp:112-127) for every distinct layer shape of the
+// model, over a bounded, evenly strided row sample, with `threads` workers over
+// disjoint rows (the kernels are pure per row). Output: per-layer seconds for
+// one epoch of that layer over all N rows (per-row cost x N + mask cost), from
+// which bench.py assembles the epoch time of any stage split.
 void cmd_bench(const Args& a) {
     Dataset d = make_dataset(arg(a, "spec"));
     ModelConfig mc = model_from(a);
     const uint32_t threads = uint32_t(argu(a, "threads", "1"));
-    const uint32_t sample = uint32_t(argu(a, "rows", "2000"));
+    const uint32_t sample = uint32_t(argu(a, "rows", "1000"));
     const uint32_t steps = uint32_t(argu(a, "steps", "1"));
     auto specs = build_layer_specs(mc, d.num_features(), d.num_classes);
     auto params = init_params<float>(specs, 1);
     auto adj = build_adj_bundle<float>(d.graph, mc.self_loops);
     const VertexId n = d.num_vertices();
     const uint32_t L = uint32_t(specs.size());
-    // pick the representative aggregating layer (index 1 for GCNII, 1 for GCN)
-    const uint32_t li = L > 1 ? 1 : 0;
-    const auto& sp = specs[li];
-    MatF h_prev(n, sp.in_dim), h0(n, mc.hidden), pre(n, sp.k_in()), out(n, sp.out_dim);
-    for (size_t i = 0; i < h_prev.size(); ++i) h_prev.data()[i] = float(hash_unit(mix64(3, i)) - 0.5);
-    for (size_t i = 0; i < h0.size(); ++i) h0.data()[i] = float(hash_unit(mix64(4, i)) - 0.5);
-    MatF dz(n, sp.out_dim), dagg(n, sp.k_in()), dprev(n, sp.in_dim), dh0(n, mc.hidden), dout(n, sp.out_dim);
-    for (size_t i = 0; i < dout.size(); ++i) dout.data()[i] = float(hash_unit(mix64(5, i)) - 0.5);
-    auto mask = DropMask<float>::make(mc.dropout, 1, 1, li, n, sp.in_dim);
-    // dense layers: first and last, timed the same way
-    std::vector<double> per_step;
-    const uint32_t stride = std::max<uint32_t>(1, n / sample);
+    const bool needs_h0 = model_needs_h0(specs);
+    const uint32_t stride = std::max<uint32_t>(1, n / std::max<uint32_t>(1, sample));
     std::vector<VertexId> rows;
     for (VertexId v = 0; v < n && rows.size() < sample; v += stride) rows.push_back(v);
+    // representative layers: first, one middle (aggregating) layer, last
+    std::vector<uint32_t> reps = {0};
+    if (L > 2) reps.push_back(1);
+    if (L > 1) reps.push_back(L - 1);
+    std::vector<double> per_layer_epoch(size_t(steps) * L, 0.0);
+    std::vector<double> mask_secs(L, 0.0);
     for (uint32_t s = 0; s < steps; ++s) {
-        const auto t0 = std::chrono::steady_clock::now();
-        std::vector<std::thread> pool;
-        for (uint32_t t = 0; t < threads; ++t)
-            pool.emplace_back([&, t]() {
-                for (size_t r = t; r < rows.size(); r += threads) {
-                    const VertexId v = rows[r];
-                    kernel::forward_row(sp, params[li], adj, v,
-                                        [&](VertexId u) { return h_prev.row(u); }, mask,
-                                        h0.row(v), pre.row(v), out.row(v));
-                    kernel::backward_out_row(sp, params[li], dout.row(v), out.row(v), dz.row(v),
-                                             dagg.row(v), sp.kind == LayerKind::Gcn2Conv ? dh0.row(v) : nullptr);
-                    kernel::backward_prev_row(sp, adj, v, [&](VertexId u) { return dagg.row(u); },
-                                              dagg.row(v), mask, dprev.row(v));
-                }
-            });
-        for (auto& th : pool) th.join();
-        // param grads over the sampled rows (the reference sums over all N at epoch end)
-        auto g = param_grads_for_rows(sp, rows, pre, dz);
-        (void)g;
-        const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-        const double per_row = secs / double(rows.size());
-        uint32_t agg_layers = 0;
-        for (const auto& s2 : specs) agg_layers += s2.aggregates();
-        // dense layers cost (GCNII first/last) approximated by GEMV cost ratio
-        double dense_rel = 0;
-        for (const auto& s2 : specs)
-            if (!s2.aggregates())
-                dense_rel += double(s2.in_dim) * s2.out_dim * 3.0 /
-                             (double(sp.in_dim) * sp.out_dim * 3.0 + 2.0 * double(adj.norm.cols.size()) / n * sp.in_dim);
-        per_step.push_back(per_row * double(n) * (double(agg_layers) + dense_rel));
+        std::vector<double> rep_cost(L, 0.0);
+        for (uint32_t li : reps) {
+            const auto& sp = specs[li];
+            MatF h_prev(n, sp.in_dim), h0(needs_h0 ? n : 0, mc.hidden), pre(n, sp.k_in()), out(n, sp.out_dim);
+            for (size_t i = 0; i < h_prev.size(); ++i) h_prev.data()[i] = float(hash_unit(mix64(3, i)) - 0.5);
+            for (size_t i = 0; i < h0.size(); ++i) h0.data()[i] = float(hash_unit(mix64(4, i)) - 0.5);
+            MatF dz(n, sp.out_dim), dagg(n, sp.k_in()), dprev(n, sp.in_dim), dh0(needs_h0 ? n : 0, mc.hidden),
+                dout(n, sp.out_dim);
+            for (size_t i = 0; i < dout.size(); ++i) dout.data()[i] = float(hash_unit(mix64(5, i)) - 0.5);
+            const auto tm0 = std::chrono::steady_clock::now();
+            auto mask = DropMask<float>::make(mc.dropout, 1, 1, li, n, sp.in_dim);
+            mask_secs[li] = std::chrono::duration<double>(std::chrono::steady_clock::now() - tm0).count();
+            const auto t0 = std::chrono::steady_clock::now();
+            std::vector<std::thread> pool;
+            for (uint32_t t = 0; t < threads; ++t)
+                pool.emplace_back([&, t]() {
+                    for (size_t r = t; r < rows.size(); r += threads) {
+                        const VertexId v = rows[r];
+                        kernel::forward_row(sp, params[li], adj, v, [&](VertexId u) { return h_prev.row(u); },
+                                            mask, needs_h0 && li > 0 ? h0.row(v) : nullptr, pre.row(v), out.row(v));
+                        kernel::backward_out_row(sp, params[li], dout.row(v), out.row(v), dz.row(v), dagg.row(v),
+                                                 sp.kind == LayerKind::Gcn2Conv ? dh0.row(v) : nullptr);
+                        if (li > 0)
+                            kernel::backward_prev_row(sp, adj, v, [&](VertexId u) { return dagg.row(u); },
+                                                      dagg.row(v), mask, dprev.row(v));
+                    }
+                });
+            for (auto& th : pool) th.join();
+            auto g = param_grads_for_rows(sp, rows, pre, dz);
+            (void)g;
+            const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            // wall time of `threads` workers over the sample -> per-row wall cost
+            rep_cost[li] = secs / double(rows.size()) * double(n) + mask_secs[li];
+        }
+        for (uint32_t l = 0; l < L; ++l) {
+            const uint32_t src = l == 0 ? 0 : (l + 1 == L ? L - 1 : (L > 2 ? 1 : 0));
+            per_layer_epoch[size_t(s) * L + l] = rep_cost[src];
+        }
     }
     Blob b(arg(a, "out"));
-    b.f64("epoch_seconds", per_step);
+    b.f64("layer_epoch_seconds", per_layer_epoch);  // steps x L
     b.u64("rows_sampled", {rows.size()});
     b.u64("threads", {threads});
     b.u64("nnz", {adj.norm.cols.size()});
+    b.u64("num_layers", {L});
 }
 
 }  // namespace

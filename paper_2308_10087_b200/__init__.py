@@ -172,6 +172,9 @@ def _L():
         "gp_get_profile": (C.c_int, [vp, P(gp_profile)]),
         "gp_reset_profile": (C.c_int, [vp]),
         "gp_device_bytes": (C.c_int, [vp, u64p]),
+        "gp_mark": (C.c_int, [vp, C.c_uint32]),
+        "gp_elapsed": (C.c_int, [vp, C.c_uint32, C.c_uint32, P(C.c_float)]),
+        "gp_synchronize": (C.c_int, [vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -586,6 +589,17 @@ class StageEngine:
         return {name: {"ms": pr.ms[i], "launches": pr.launches[i], "alg_bytes": pr.alg_bytes[i],
                        "flops": pr.flops[i], "gather_bytes": pr.gather_bytes[i]}
                 for i, name in enumerate(PROFILE_CLASSES)}
+
+    def mark(self, slot: int):
+        _gp(_L().gp_mark(self._h, slot), self._h)
+
+    def elapsed_ms(self, a: int, b: int) -> float:
+        v = C.c_float()
+        _gp(_L().gp_elapsed(self._h, a, b, C.byref(v)), self._h)
+        return v.value
+
+    def synchronize(self):
+        _gp(_L().gp_synchronize(self._h), self._h)
 
     def device_bytes(self) -> int:
         v = C.c_uint64()

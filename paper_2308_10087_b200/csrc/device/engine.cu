@@ -209,6 +209,7 @@ struct Stage {
     std::vector<cudaEvent_t> ev_free;
     uint64_t launches = 0;
     cudaEvent_t ev_start = nullptr, ev_end = nullptr;
+    cudaEvent_t marks[16] = {};
     int num_sms = 148;
     int occ_fwd = 4, occ_bwd = 4, occ_row = 8;
     std::atomic<bool> aborted{false};
@@ -235,6 +236,8 @@ struct Stage {
         }
         for (auto e : ev_free) cudaEventDestroy(e);
         for (auto e : tr.ev_pool) cudaEventDestroy(e);
+        for (auto e : marks)
+            if (e) cudaEventDestroy(e);
         if (ev_start) cudaEventDestroy(ev_start);
         if (ev_end) cudaEventDestroy(ev_end);
         if (tr.up_comm) g_nccl.comm_destroy(tr.up_comm);
@@ -1348,6 +1351,33 @@ gp_status gp_get_profile(gp_ctx* ctx, gp_profile* out) {
 gp_status gp_reset_profile(gp_ctx* ctx) {
     ctx->st.prof = gp_profile{};
     return GP_OK;
+}
+
+gp_status gp_mark(gp_ctx* ctx, uint32_t slot) {
+    return gp::guard(&ctx->st, [&]() {
+        auto& st = ctx->st;
+        if (slot >= 16) throw gp::Error(GP_EINVAL, "mark slot must be < 16");
+        GP_CUDA(cudaSetDevice(st.device));
+        if (!st.marks[slot]) GP_CUDA(cudaEventCreate(&st.marks[slot]));
+        GP_CUDA(cudaEventRecord(st.marks[slot], st.cs));
+    });
+}
+
+gp_status gp_elapsed(gp_ctx* ctx, uint32_t a, uint32_t b, float* ms) {
+    return gp::guard(&ctx->st, [&]() {
+        auto& st = ctx->st;
+        if (a >= 16 || b >= 16 || !st.marks[a] || !st.marks[b]) throw gp::Error(GP_EINVAL, "unrecorded mark");
+        GP_CUDA(cudaSetDevice(st.device));
+        GP_CUDA(cudaEventSynchronize(st.marks[b]));
+        GP_CUDA(cudaEventElapsedTime(ms, st.marks[a], st.marks[b]));
+    });
+}
+
+gp_status gp_synchronize(gp_ctx* ctx) {
+    return gp::guard(&ctx->st, [&]() {
+        GP_CUDA(cudaSetDevice(ctx->st.device));
+        GP_CUDA(cudaStreamSynchronize(ctx->st.cs));
+    });
 }
 
 gp_status gp_device_bytes(gp_ctx* ctx, uint64_t* out) {
