@@ -20,6 +20,7 @@
 #include <condition_variable>
 #include <cstring>
 #include <deque>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <stdexcept>
@@ -211,7 +212,7 @@ struct Stage {
     cudaEvent_t ev_start = nullptr, ev_end = nullptr;
     cudaEvent_t marks[16] = {};
     int num_sms = 148;
-    int occ_fwd = 4, occ_bwd = 4, occ_row = 8;
+    std::map<std::pair<const void*, size_t>, int> occ_cache;
     std::atomic<bool> aborted{false};
 
     // ---- memory -----------------------------------------------------------
@@ -333,12 +334,13 @@ struct Stage {
             d.h = dalloc<float>(size_t(n) * d.sout);
             d.pre = dalloc<float>(size_t(n) * d.sin);
             d.dz = dalloc<float>(size_t(n) * d.sout);
-            if (d.agg) d.G = dalloc<float>(size_t(n) * d.sin);
+            // gather tables carry one extra all-zero row (row n, see gather_row)
+            if (d.agg) d.G = dalloc<float>(size_t(n + 1) * d.sin);
             if (!sync && i + 1 < len && specs[lb + i + 1].kind != GP_DENSE)
                 d.hs = dalloc<float>(size_t(n) * d.sout);
             if (d.l > 0) {
-                d.bg = dalloc<float>(size_t(n) * d.sin);
-                if (hist && d.agg) d.bgs = dalloc<float>(size_t(n) * d.sin);
+                d.bg = dalloc<float>(size_t(n + 1) * d.sin);
+                if (hist && d.agg) d.bgs = dalloc<float>(size_t(n + 1) * d.sin);
             }
         }
         if (!first) {
@@ -350,10 +352,7 @@ struct Stage {
         if (needs_h0) dh0 = dalloc<float>(size_t(n) * pad8(H));
         dtop = dalloc<float>(size_t(n) * L[len - 1].sout);
         // pgrad workspace: ~2 waves of CTAs
-        uint32_t max_tiles = 1;
-        for (auto& d : L) max_tiles = std::max(max_tiles, ((d.din + 63) / 64) * ((d.dout + 63) / 64));
-        splits = std::max<uint32_t>(1, std::min<uint32_t>((2 * num_sms + max_tiles - 1) / max_tiles,
-                                                          (n + 255) / 256));
+        splits = std::max<uint32_t>(1, std::min<uint32_t>(2 * num_sms, (n + 63) / 64));
         size_t wmax = 1;
         for (auto& d : L) wmax = std::max(wmax, size_t(d.din) * d.dout);
         ws = dalloc<float>(size_t(splits) * wmax, false);
@@ -377,6 +376,15 @@ struct Stage {
         SETB(PREV_OWN, OUT_LAYER) SETB(PREV_AGG, OUT_DHIN) SETB(PREV_AGG_HIST, OUT_DHIN)
         SETB(PREV_OWN, OUT_DHIN)
 #undef SETB
+        // Gathers bypass L1 (no_allocate): give the SM's unified L1/shared to shared
+        // memory so 4 CTAs with a staged weight matrix fit per SM.
+        const void* big[] = {(const void*)k_fwd_fused<FWD_DENSE>, (const void*)k_fwd_fused<FWD_GCN>,
+                             (const void*)k_fwd_fused<FWD_GCN2>,  (const void*)k_bwd<PREV_TOP, OUT_LAYER>,
+                             (const void*)k_bwd<PREV_AGG, OUT_LAYER>, (const void*)k_bwd<PREV_AGG_HIST, OUT_LAYER>,
+                             (const void*)k_bwd<PREV_OWN, OUT_LAYER>};
+        for (const void* f : big)
+            GP_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                         int(cudaSharedmemCarveoutMaxShared)));
     }
 
     // ---- graph --------------------------------------------------------------
@@ -542,9 +550,20 @@ struct Stage {
         timed.push_back(t);
     }
 
-    uint32_t row_grid(uint32_t rows, int occ) const {
+    // Persistent grid: exactly the resident capacity (occupancy x SMs), capped by
+    // the number of 8-row blocks, so there is no partial second wave.
+    uint32_t row_grid(uint32_t rows, const void* fn, size_t smem) {
+        auto key = std::make_pair(fn, smem);
+        auto it = occ_cache.find(key);
+        int occ = 0;
+        if (it == occ_cache.end()) {
+            GP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kBlock, smem));
+            occ_cache[key] = occ = std::max(occ, 1);
+        } else {
+            occ = it->second;
+        }
         const uint64_t want = (uint64_t(rows) + kWarpsPerBlock - 1) / kWarpsPerBlock;
-        const uint64_t cap = uint64_t(num_sms) * std::max(occ, 1);
+        const uint64_t cap = uint64_t(num_sms) * occ;
         return uint32_t(std::max<uint64_t>(1, std::min(want, cap)));
     }
 
@@ -576,7 +595,7 @@ struct Stage {
         RemaskParams p{r0, r1, d.din, src, src_stride(i), d.G, d.sin, orig, key};
         const uint32_t rows = r1 - r0;
         launch(GP_K_REMASK, double(rows) * d.din * 8.0, 0, 0,
-               [&]() { k_remask<<<row_grid(rows, occ_row), kBlock, 0, cs>>>(p); });
+               [&]() { k_remask<<<row_grid(rows, (const void*)k_remask, 0), kBlock, 0, cs>>>(p); });
     }
 
     void forward_layer(uint32_t i, uint32_t r0, uint32_t r1, uint32_t t) {
@@ -602,6 +621,7 @@ struct Stage {
             p.edges = edges;
             p.gsrc = d.G;
             p.gstride = d.sin;
+            p.zrow = n;
             p.xsrc = cur_src(i);
             p.xstride = src_stride(i);
             p.in_mask = drop_key(t, d.l, d.din);
@@ -625,7 +645,6 @@ struct Stage {
             p.gnstride = gnstride;
             p.next_mask = nk;
             const size_t smem = (size_t(d.din) + 1) * ((d.dout + 3) / 4) * 16;
-            const uint32_t grid = row_grid(rows, occ_fwd);
             const double e = d.agg ? double(rowptr_nnz(r0, r1)) : 0.0;
             const double bytes = (d.agg ? e * 8.0 + double(rows + 1) * 8.0 + double(n) * d.din * 4.0
                                         : double(rows) * d.din * 4.0) +
@@ -636,26 +655,26 @@ struct Stage {
             const double gather = e * double(d.sin) * 4.0;
             const int cls = d.agg ? GP_K_FWD_AGG : GP_K_FWD_DENSE;
             if (d.spec.kind == GP_DENSE)
-                launch(cls, bytes, flops, 0, [&]() { k_fwd_fused<FWD_DENSE><<<grid, kBlock, smem, cs>>>(p); });
+                launch(cls, bytes, flops, 0, [&]() { k_fwd_fused<FWD_DENSE><<<row_grid(rows, (const void*)k_fwd_fused<FWD_DENSE>, smem), kBlock, smem, cs>>>(p); });
             else if (d.spec.kind == GP_GCNCONV)
-                launch(cls, bytes, flops, gather, [&]() { k_fwd_fused<FWD_GCN><<<grid, kBlock, smem, cs>>>(p); });
+                launch(cls, bytes, flops, gather, [&]() { k_fwd_fused<FWD_GCN><<<row_grid(rows, (const void*)k_fwd_fused<FWD_GCN>, smem), kBlock, smem, cs>>>(p); });
             else
-                launch(cls, bytes, flops, gather, [&]() { k_fwd_fused<FWD_GCN2><<<grid, kBlock, smem, cs>>>(p); });
+                launch(cls, bytes, flops, gather, [&]() { k_fwd_fused<FWD_GCN2><<<row_grid(rows, (const void*)k_fwd_fused<FWD_GCN2>, smem), kBlock, smem, cs>>>(p); });
             return;
         }
         // wide input (layer 0 with F > 128): pre first, then the tiled transform
         if (d.spec.kind == GP_GCN2CONV) throw Error(GP_EINVAL, "Gcn2Conv wider than 128");
         if (d.agg) {
-            SpmmParams sp{r0, r1, d.din, rowptr, edges, d.G, d.sin, d.pre, d.sin};
+            SpmmParams sp{r0, r1, d.din, n, rowptr, edges, d.G, d.sin, d.pre, d.sin};
             const double e = double(rowptr_nnz(r0, r1));
             launch(GP_K_FWD_AGG, e * 8.0 + double(n) * d.din * 4.0 + double(rows) * d.din * 4.0,
                    2.0 * e * d.din, e * d.sin * 4.0,
-                   [&]() { k_spmm_pre<<<row_grid(rows, occ_row), kBlock, 0, cs>>>(sp); });
+                   [&]() { k_spmm_pre<<<row_grid(rows, (const void*)k_spmm_pre, 0), kBlock, 0, cs>>>(sp); });
         } else {
             RemaskParams rp{r0, r1, d.din, cur_src(i), src_stride(i), d.pre, d.sin, orig,
                             drop_key(t, d.l, d.din)};
             launch(GP_K_FWD_DENSE, double(rows) * d.din * 8.0, 0, 0,
-                   [&]() { k_remask<<<row_grid(rows, occ_row), kBlock, 0, cs>>>(rp); });
+                   [&]() { k_remask<<<row_grid(rows, (const void*)k_remask, 0), kBlock, 0, cs>>>(rp); });
         }
         GemmParams g{};
         g.r0 = r0;
@@ -711,6 +730,7 @@ struct Stage {
             p.bgn = nx.bg;
             p.bgn_snap = nx.bgs;
             p.bgnstride = nx.sin;
+            p.zrow = n;
             p.prev_mask = drop_key(t, nx.l, nx.din);
             if (nx.agg) {
                 prev = hist ? PREV_AGG_HIST : PREV_AGG;
@@ -740,7 +760,6 @@ struct Stage {
         p.bg = d.bg;
         p.bgstride = d.sin;
         const size_t smem = p.need_dagg ? size_t(d.dout) * ((d.din + 3) / 4) * 16 : 0;
-        const uint32_t grid = row_grid(rows, occ_bwd);
         const double bytes = e * 8.0 + (e > 0 ? double(n) * d.dout * 4.0 : double(rows) * d.dout * 4.0) +
                              double(rows) * d.dout * 8.0 + (p.need_dagg ? double(rows) * d.din * 4.0 : 0.0) +
                              (p.gcn2 ? double(rows) * d.din * 8.0 : 0.0);
@@ -749,17 +768,17 @@ struct Stage {
         const int cls = prev == PREV_AGG || prev == PREV_AGG_HIST ? GP_K_BWD_AGG : GP_K_BWD_DENSE;
         switch (prev) {
             case PREV_TOP:
-                launch(cls, bytes, flops, 0, [&]() { k_bwd<PREV_TOP, OUT_LAYER><<<grid, kBlock, smem, cs>>>(p); });
+                launch(cls, bytes, flops, 0, [&]() { k_bwd<PREV_TOP, OUT_LAYER><<<row_grid(rows, (const void*)k_bwd<PREV_TOP, OUT_LAYER>, smem), kBlock, smem, cs>>>(p); });
                 break;
             case PREV_AGG:
-                launch(cls, bytes, flops, gather, [&]() { k_bwd<PREV_AGG, OUT_LAYER><<<grid, kBlock, smem, cs>>>(p); });
+                launch(cls, bytes, flops, gather, [&]() { k_bwd<PREV_AGG, OUT_LAYER><<<row_grid(rows, (const void*)k_bwd<PREV_AGG, OUT_LAYER>, smem), kBlock, smem, cs>>>(p); });
                 break;
             case PREV_AGG_HIST:
                 launch(cls, bytes, flops, gather,
-                       [&]() { k_bwd<PREV_AGG_HIST, OUT_LAYER><<<grid, kBlock, smem, cs>>>(p); });
+                       [&]() { k_bwd<PREV_AGG_HIST, OUT_LAYER><<<row_grid(rows, (const void*)k_bwd<PREV_AGG_HIST, OUT_LAYER>, smem), kBlock, smem, cs>>>(p); });
                 break;
             default:
-                launch(cls, bytes, flops, 0, [&]() { k_bwd<PREV_OWN, OUT_LAYER><<<grid, kBlock, smem, cs>>>(p); });
+                launch(cls, bytes, flops, 0, [&]() { k_bwd<PREV_OWN, OUT_LAYER><<<row_grid(rows, (const void*)k_bwd<PREV_OWN, OUT_LAYER>, smem), kBlock, smem, cs>>>(p); });
         }
     }
 
@@ -779,20 +798,20 @@ struct Stage {
         p.bgn = d.bg;
         p.bgn_snap = d.bgs;
         p.bgnstride = d.sin;
+        p.zrow = n;
         p.prev_mask = drop_key(t, d.l, d.din);
         p.dh_in = dh_in;
         p.dhinstride = sin0;
-        const uint32_t grid = row_grid(rows, occ_bwd);
         const double e = d.agg ? double(rowptr_nnz(r0, r1)) : 0.0;
         const double bytes = e * 8.0 + (d.agg ? double(n) : double(rows)) * d.din * 4.0 + double(rows) * d.din * 4.0;
         if (!d.agg)
-            launch(GP_K_BWD_DENSE, bytes, 0, 0, [&]() { k_bwd<PREV_OWN, OUT_DHIN><<<grid, kBlock, 0, cs>>>(p); });
+            launch(GP_K_BWD_DENSE, bytes, 0, 0, [&]() { k_bwd<PREV_OWN, OUT_DHIN><<<row_grid(rows, (const void*)k_bwd<PREV_OWN, OUT_DHIN>, 0), kBlock, 0, cs>>>(p); });
         else if (hist)
             launch(GP_K_BWD_AGG, bytes, 2.0 * e * d.din, e * d.sin * 4.0,
-                   [&]() { k_bwd<PREV_AGG_HIST, OUT_DHIN><<<grid, kBlock, 0, cs>>>(p); });
+                   [&]() { k_bwd<PREV_AGG_HIST, OUT_DHIN><<<row_grid(rows, (const void*)k_bwd<PREV_AGG_HIST, OUT_DHIN>, 0), kBlock, 0, cs>>>(p); });
         else
             launch(GP_K_BWD_AGG, bytes, 2.0 * e * d.din, e * d.sin * 4.0,
-                   [&]() { k_bwd<PREV_AGG, OUT_DHIN><<<grid, kBlock, 0, cs>>>(p); });
+                   [&]() { k_bwd<PREV_AGG, OUT_DHIN><<<row_grid(rows, (const void*)k_bwd<PREV_AGG, OUT_DHIN>, 0), kBlock, 0, cs>>>(p); });
     }
 
     XentParams xent_params(uint32_t r0, uint32_t r1) {
@@ -819,10 +838,10 @@ struct Stage {
         const double c2d = 1.0 - std::pow(cfg.beta2, double(step));
         for (uint32_t i = 0; i < len; ++i) {
             auto& d = L[i];
-            const uint32_t ti = (d.din + 63) / 64, tj = (d.dout + 63) / 64;
+            const uint32_t ti = (d.din + 127) / 128, tj = 1;
             const uint32_t rps = (n + splits - 1) / splits;
             PgradParams pp{n, rps, d.pre, d.sin, d.dz, d.sout, d.din, d.dout, ws, d.gb ? wsb : nullptr};
-            dim3 grid(splits, ti, tj);
+            dim3 grid(splits, ti, 1);
             launch(GP_K_PGRAD, double(n) * (d.din * tj + d.dout * ti) * 4.0 + double(splits) * d.din * d.dout * 4.0,
                    2.0 * double(n) * d.din * d.dout, 0,
                    [&]() { k_pgrad_partial<<<grid, 256, 0, cs>>>(pp); });
@@ -1076,7 +1095,7 @@ struct Stage {
                 if (last) {
                     XentParams p = xent_params(r0, r1);
                     launch(GP_K_XENT, double(r1 - r0) * L[len - 1].dout * 8.0, 0, 0,
-                           [&]() { k_xent_grad<<<row_grid(r1 - r0, occ_row), kBlock, 0, cs>>>(p); });
+                           [&]() { k_xent_grad<<<row_grid(r1 - r0, (const void*)k_xent_grad, 0), kBlock, 0, cs>>>(p); });
                 } else {
                     recv_bwd(k);
                 }
@@ -1091,7 +1110,7 @@ struct Stage {
             if (last) {
                 XentParams p = xent_params(0, n);
                 launch(GP_K_XENT, double(n) * L[len - 1].dout * 8.0, 0, 0,
-                       [&]() { k_xent_grad<<<row_grid(n, occ_row), kBlock, 0, cs>>>(p); });
+                       [&]() { k_xent_grad<<<row_grid(n, (const void*)k_xent_grad, 0), kBlock, 0, cs>>>(p); });
             } else {
                 for (uint32_t kk = K; kk-- > 0;) recv_bwd(ord[kk]);
             }

@@ -37,6 +37,85 @@ __device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<floa
 // The 32 entries of a batch are loaded once, coalesced, and broadcast by
 // shuffle; 8 gathers are kept in flight per lane.
 // ---------------------------------------------------------------------------
+// Streaming (evict-first) load of the CSR entries so they do not displace the
+// gather table from L2; gathers use the read-only path with default policy.
+__device__ __forceinline__ uint64_t evict_first_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ uint2 ld_edge(const uint2* p) {
+    uint2 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0, %1}, [%2], %3;"
+                 : "=r"(r.x), "=r"(r.y)
+                 : "l"(p), "l"(evict_first_policy()));
+    return r;
+}
+__device__ __forceinline__ uint64_t evict_last_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+// Gather-table reads: kept in L2 (evict_last) — the table (N x d, ~97 MB at
+// Reddit shape) is re-read ~deg times per row and must survive the streams.
+__device__ __forceinline__ float4 ld_gather(const float* p, uint64_t pol) {
+    float4 r;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+        : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+        : "l"(p), "l"(pol));
+    return r;
+}
+// Row-local streams (pre, h, dz, h0, ...): evict_first so they never displace
+// the gather table.
+__device__ __forceinline__ float4 ld_stream(const float* p) {
+    float4 r;
+    asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+                 : "l"(p), "l"(evict_first_policy()));
+    return r;
+}
+__device__ __forceinline__ void st_stream(float* p, float4 v) {
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p),
+                 "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "l"(evict_first_policy())
+                 : "memory");
+}
+
+// Gathers of one batch are issued back to back, without branches or selects
+// on the loaded values (a select after a load forces a scoreboard wait):
+//  * padding entries past the end of a batch re-read the batch's first row with
+//    weight 0; acc starts at +0 and a sum of products never becomes -0, so
+//    acc + 0*x == acc bit-for-bit — padding is indistinguishable from skipping;
+//  * lanes beyond the row width alias lane 0's address (no extra sectors); their
+//    values are never stored.
+template <int NB, bool HIST>
+__device__ __forceinline__ void gather_batch(float4& acc, uint2 my, int t, int cnt, uint64_t pol, const float* lsrc,
+                                             const float* lsnap, uint32_t stride, uint64_t done) {
+    const uint32_t first = __shfl_sync(kFull, my.x, 0) & kColMask;
+    float4 x[NB];
+    float w[NB];
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+        const int tt = (t + i) & 31;
+        const uint32_t packed = __shfl_sync(kFull, my.x, tt);
+        const float wv = __uint_as_float(__shfl_sync(kFull, my.y, tt));
+        const bool valid = t + i < cnt;
+        const float* s = lsrc;
+        if (HIST && valid && !((done >> (packed >> kColBits)) & 1ull)) s = lsnap;
+        w[i] = valid ? wv : 0.f;
+        x[i] = ld_gather(s + size_t(valid ? (packed & kColMask) : first) * stride, pol);
+    }
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+        acc.x = mul_add(acc.x, w[i], x[i].x);
+        acc.y = mul_add(acc.y, w[i], x[i].y);
+        acc.z = mul_add(acc.z, w[i], x[i].z);
+        acc.w = mul_add(acc.w, w[i], x[i].w);
+    }
+}
+
+// FILTER (backward, zeroed historical gradients): entries whose chunk is not in
+// `done` are dropped from each 32-entry batch by a warp ballot and a stable
+// compaction (ascending order kept), so they cost neither loads nor FMAs.
 template <bool FILTER, bool HIST>
 __device__ __forceinline__ float4 gather_row(const uint64_t* __restrict__ rowptr,
                                              const uint2* __restrict__ edges, uint32_t v,
@@ -45,42 +124,28 @@ __device__ __forceinline__ float4 gather_row(const uint64_t* __restrict__ rowptr
                                              uint64_t done, int lane, bool active) {
     float4 acc = f4_zero();
     const uint64_t e0 = rowptr[v], e1 = rowptr[v + 1];
+    const uint32_t loff = active ? 4u * lane : 0u;
+    const float* lsrc = src + loff;
+    const float* lsnap = HIST ? src_snap + loff : nullptr;
+    const uint64_t pol = evict_last_policy();
     for (uint64_t base = e0; base < e1; base += 32) {
-        const int cnt = int(e1 - base < 32 ? e1 - base : 32);
-        const uint2 my = lane < cnt ? __ldg(edges + base + lane) : make_uint2(0u, 0u);
-        for (int t = 0; t < cnt; t += 8) {
-            float4 x[8];
-            float w[8];
-            bool ok[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const int tt = t + i;
-                const uint32_t packed = __shfl_sync(kFull, my.x, tt & 31);
-                w[i] = __uint_as_float(__shfl_sync(kFull, my.y, tt & 31));
-                bool valid = tt < cnt;
-                const float* s = src;
-                if (FILTER) {
-                    const bool dn = (done >> (packed >> kColBits)) & 1ull;
-                    if (HIST) {
-                        if (!dn) s = src_snap;
-                    } else {
-                        valid = valid && dn;
-                    }
-                }
-                ok[i] = valid;
-                x[i] = (valid && active) ? ld4(s + size_t(packed & kColMask) * stride + 4 * lane)
-                                         : f4_zero();
-            }
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                if (ok[i]) {
-                    acc.x = mul_add(acc.x, w[i], x[i].x);
-                    acc.y = mul_add(acc.y, w[i], x[i].y);
-                    acc.z = mul_add(acc.z, w[i], x[i].z);
-                    acc.w = mul_add(acc.w, w[i], x[i].w);
-                }
-            }
+        int cnt = int(e1 - base < 32 ? e1 - base : 32);
+        uint2 my = lane < cnt ? ld_edge(edges + base + lane) : make_uint2(0u, 0u);
+        if (FILTER && !HIST) {
+            const bool ok = lane < cnt && ((done >> (my.x >> kColBits)) & 1ull);
+            const unsigned m = __ballot_sync(kFull, ok);
+            cnt = __popc(m);
+            if (cnt == 0) continue;
+            const int from = lane < cnt ? int(__fns(m, 0, lane + 1)) : 0;
+            my.x = __shfl_sync(kFull, my.x, from);
+            my.y = __shfl_sync(kFull, my.y, from);
         }
+        int t = 0;
+        for (; t + 8 <= cnt; t += 8) gather_batch<8, HIST>(acc, my, t, cnt, pol, lsrc, lsnap, stride, done);
+        if (cnt - t > 4)
+            gather_batch<8, HIST>(acc, my, t, cnt, pol, lsrc, lsnap, stride, done);
+        else if (cnt > t)
+            gather_batch<4, HIST>(acc, my, t, cnt, pol, lsrc, lsnap, stride, done);
     }
     return acc;
 }
@@ -140,6 +205,7 @@ struct FwdParams {
     const uint2* edges;
     const float* gsrc;
     uint32_t gstride;
+    uint32_t zrow;
     const float* xsrc;
     uint32_t xstride;
     DropKey in_mask;
@@ -161,7 +227,7 @@ struct FwdParams {
 };
 
 template <int KIND>
-__global__ void __launch_bounds__(kBlock) k_fwd_fused(FwdParams p) {
+__global__ void __launch_bounds__(kBlock, 4) k_fwd_fused(FwdParams p) {
     extern __shared__ float4 smem4[];
     const uint32_t dout4 = (p.dout + 3) / 4;
     float* Ws = reinterpret_cast<float*>(smem4);
@@ -183,13 +249,13 @@ __global__ void __launch_bounds__(kBlock) k_fwd_fused(FwdParams p) {
     for (uint32_t v = p.r0 + blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5); v < p.r1; v += nw) {
         float4 pre;
         if (KIND == FWD_DENSE) {
-            const float4 x = in_act ? ld4_rw(p.xsrc + size_t(v) * p.xstride + 4 * lane) : f4_zero();
+            const float4 x = in_act ? ld_stream(p.xsrc + size_t(v) * p.xstride + 4 * lane) : f4_zero();
             pre = drop4(p.in_mask, p.orig[v], 4 * lane, p.din, x);
         } else {
             const float4 z = gather_row<false, false>(p.rowptr, p.edges, v, p.gsrc, nullptr, p.gstride,
                                                       0ull, lane, in_act);
             if (KIND == FWD_GCN2) {
-                const float4 h = in_act ? ld4_rw(p.h0 + size_t(v) * p.h0stride + 4 * lane) : f4_zero();
+                const float4 h = in_act ? ld_stream(p.h0 + size_t(v) * p.h0stride + 4 * lane) : f4_zero();
                 pre.x = __fadd_rn(__fmul_rn(p.oma, z.x), __fmul_rn(p.alpha, h.x));
                 pre.y = __fadd_rn(__fmul_rn(p.oma, z.y), __fmul_rn(p.alpha, h.y));
                 pre.z = __fadd_rn(__fmul_rn(p.oma, z.z), __fmul_rn(p.alpha, h.z));
@@ -198,7 +264,7 @@ __global__ void __launch_bounds__(kBlock) k_fwd_fused(FwdParams p) {
                 pre = z;
             }
         }
-        if (in_act) st4(p.pre + size_t(v) * p.prestride + 4 * lane, pre);
+        if (in_act) st_stream(p.pre + size_t(v) * p.prestride + 4 * lane, pre);
 
         float4 o = out_act ? reinterpret_cast<const float4*>(bs)[lane] : f4_zero();
         for (uint32_t ib = 0; ib < din4; ++ib) {
@@ -229,9 +295,9 @@ __global__ void __launch_bounds__(kBlock) k_fwd_fused(FwdParams p) {
             if (o.w < 0.f) o.w = 0.f;
         }
         if (out_act) {
-            st4(p.out + size_t(v) * p.outstride + 4 * lane, o);
+            st_stream(p.out + size_t(v) * p.outstride + 4 * lane, o);
             if (p.gnext)
-                st4(p.gnext + size_t(v) * p.gnstride + 4 * lane,
+                st_stream(p.gnext + size_t(v) * p.gnstride + 4 * lane,
                     drop4(p.next_mask, p.orig[v], 4 * lane, p.dout, o));
         }
     }
@@ -239,7 +305,7 @@ __global__ void __launch_bounds__(kBlock) k_fwd_fused(FwdParams p) {
 
 // GcnConv aggregation for d_in > 128 (column blocks of 128): pre = A_hat . G.
 struct SpmmParams {
-    uint32_t r0, r1, width;
+    uint32_t r0, r1, width, zrow;
     const uint64_t* rowptr;
     const uint2* edges;
     const float* gsrc;
@@ -380,6 +446,7 @@ struct BwdParams {
     const float* bgn;
     const float* bgn_snap;
     uint32_t bgnstride;
+    uint32_t zrow;
     uint64_t done;
     DropKey prev_mask;
     const float* dtop;
@@ -406,7 +473,7 @@ struct BwdParams {
 };
 
 template <int PREV, int OUT>
-__global__ void __launch_bounds__(kBlock) k_bwd(BwdParams p) {
+__global__ void __launch_bounds__(kBlock, 4) k_bwd(BwdParams p) {
     extern __shared__ float4 smem4[];
     float* Wt = reinterpret_cast<float*>(smem4);
     const uint32_t din4 = (p.din + 3) / 4;
@@ -426,22 +493,22 @@ __global__ void __launch_bounds__(kBlock) k_bwd(BwdParams p) {
     for (uint32_t u = p.r0 + blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5); u < p.r1; u += nw) {
         float4 dh;
         if (PREV == PREV_TOP) {
-            dh = dh_act ? ld4_rw(p.dtop + size_t(u) * p.dtopstride + 4 * lane) : f4_zero();
+            dh = dh_act ? ld_stream(p.dtop + size_t(u) * p.dtopstride + 4 * lane) : f4_zero();
         } else {
             float4 s;
             if (PREV == PREV_OWN)
-                s = dh_act ? ld4_rw(p.bgn + size_t(u) * p.bgnstride + 4 * lane) : f4_zero();
+                s = dh_act ? ld_stream(p.bgn + size_t(u) * p.bgnstride + 4 * lane) : f4_zero();
             else
                 s = gather_row<true, PREV == PREV_AGG_HIST>(p.rowptr, p.edges, u, p.bgn, p.bgn_snap,
                                                             p.bgnstride, p.done, lane, dh_act);
             dh = drop4(p.prev_mask, p.orig[u], 4 * lane, p.dh_width, s);
         }
         if (OUT == OUT_DHIN) {
-            if (dh_act) st4(p.dh_in + size_t(u) * p.dhinstride + 4 * lane, dh);
+            if (dh_act) st_stream(p.dh_in + size_t(u) * p.dhinstride + 4 * lane, dh);
             continue;
         }
         if (p.dh0_add && dh_act) {
-            const float4 a = ld4_rw(p.dh0_add + size_t(u) * p.dh0stride + 4 * lane);
+            const float4 a = ld_stream(p.dh0_add + size_t(u) * p.dh0stride + 4 * lane);
             dh.x = __fadd_rn(dh.x, a.x);
             dh.y = __fadd_rn(dh.y, a.y);
             dh.z = __fadd_rn(dh.z, a.z);
@@ -449,13 +516,13 @@ __global__ void __launch_bounds__(kBlock) k_bwd(BwdParams p) {
         }
         float4 dz = dh;
         if (p.relu) {
-            const float4 h = dh_act ? ld4_rw(p.h + size_t(u) * p.hstride + 4 * lane) : f4_zero();
+            const float4 h = dh_act ? ld_stream(p.h + size_t(u) * p.hstride + 4 * lane) : f4_zero();
             dz.x = h.x > 0.f ? dh.x : 0.f;
             dz.y = h.y > 0.f ? dh.y : 0.f;
             dz.z = h.z > 0.f ? dh.z : 0.f;
             dz.w = h.w > 0.f ? dh.w : 0.f;
         }
-        if (dh_act) st4(p.dz + size_t(u) * p.dzstride + 4 * lane, dz);
+        if (dh_act) st_stream(p.dz + size_t(u) * p.dzstride + 4 * lane, dz);
         if (!p.need_dagg) continue;
         const bool in_act = uint32_t(4 * lane) < p.din;
         float4 g = f4_zero();
@@ -481,18 +548,18 @@ __global__ void __launch_bounds__(kBlock) k_bwd(BwdParams p) {
             g.z = __fadd_rn(__fmul_rn(p.omb, dz.z), __fmul_rn(p.beta, g.z));
             g.w = __fadd_rn(__fmul_rn(p.omb, dz.w), __fmul_rn(p.beta, g.w));
             float* d0 = p.dh0 + size_t(u) * p.dh0stride + 4 * lane;
-            float4 a = ld4_rw(d0);
+            float4 a = ld_stream(d0);
             a.x = __fadd_rn(a.x, __fmul_rn(p.alpha, g.x));
             a.y = __fadd_rn(a.y, __fmul_rn(p.alpha, g.y));
             a.z = __fadd_rn(a.z, __fmul_rn(p.alpha, g.z));
             a.w = __fadd_rn(a.w, __fmul_rn(p.alpha, g.w));
-            st4(d0, a);
+            st_stream(d0, a);
             g.x = __fmul_rn(p.oma, g.x);
             g.y = __fmul_rn(p.oma, g.y);
             g.z = __fmul_rn(p.oma, g.z);
             g.w = __fmul_rn(p.oma, g.w);
         }
-        st4(p.bg + size_t(u) * p.bgstride + 4 * lane, g);
+        st_stream(p.bg + size_t(u) * p.bgstride + 4 * lane, g);
     }
 }
 
@@ -646,60 +713,92 @@ struct PgradParams {
     float* wsb;  // splits x dout
 };
 
-__global__ void __launch_bounds__(256) k_pgrad_partial(PgradParams p) {
-    __shared__ float Ps[32][64];
-    __shared__ float Ds[32][64];
+// CTA tile 128 (k_in) x 128 (out): each row of pre/dz is read once per CTA.
+// Thread (ti, tj) owns i in {4ti..4ti+3, 64+4ti..+3} and j likewise, so the
+// shared-memory float4 reads of a warp are contiguous (conflict-free).
+// Rows are staged 16 at a time, double-buffered through registers.
+constexpr int kPgRows = 16;
+__global__ void __launch_bounds__(256, 2) k_pgrad_partial(PgradParams p) {
+    __shared__ __align__(16) float Ps[2][kPgRows][128];
+    __shared__ __align__(16) float Ds[2][kPgRows][128];
     const uint32_t split = blockIdx.x;
-    const uint32_t i0 = blockIdx.y * 64, j0 = blockIdx.z * 64;
+    const uint32_t i0 = blockIdx.y * 128;
     const uint32_t rbeg = split * p.rows_per_split;
     const uint32_t rend = min(p.n, rbeg + p.rows_per_split);
-    const int ti = threadIdx.x / 16, tj = threadIdx.x % 16;
-    float acc[4][4];
-    float bacc[4] = {0.f, 0.f, 0.f, 0.f};
+    const int tid = threadIdx.x;
+    const int ti = tid / 16, tj = tid % 16;
+    float acc[8][8];
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+    for (int a = 0; a < 8; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] = 0.f;
-    for (uint32_t r0 = rbeg; r0 < rend; r0 += 32) {
-        for (int idx = threadIdx.x; idx < 32 * 64; idx += 256) {
-            const int r = idx / 64, c = idx % 64;
-            const uint32_t row = r0 + r;
-            Ps[r][c] = (row < rend && i0 + c < p.din) ? p.pre[size_t(row) * p.prestride + i0 + c] : 0.f;
-            Ds[r][c] = (row < rend && j0 + c < p.dout) ? p.dz[size_t(row) * p.dzstride + j0 + c] : 0.f;
+        for (int b = 0; b < 8; ++b) acc[a][b] = 0.f;
+    float bacc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    // staging: 16 rows x 128 cols x 2 arrays = 4096 floats = 1024 float4; 4 per thread
+    const int lr = tid / 16, lc = (tid % 16) * 8;  // thread loads row lr, cols lc..lc+7 of both arrays
+    float4 rp[2], rd[2];
+    auto fetch = [&](uint32_t r0) {
+        const uint32_t row = r0 + lr;
+        const bool ok = row < rend;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const uint32_t ci = i0 + lc + 4 * h, cj = lc + 4 * h;
+            rp[h] = (ok && ci < p.din) ? *reinterpret_cast<const float4*>(p.pre + size_t(row) * p.prestride + ci)
+                                       : f4_zero();
+            rd[h] = (ok && cj < p.dout) ? *reinterpret_cast<const float4*>(p.dz + size_t(row) * p.dzstride + cj)
+                                        : f4_zero();
         }
-        __syncthreads();
+    };
+    auto stash = [&](int buf) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            *reinterpret_cast<float4*>(&Ps[buf][lr][lc + 4 * h]) = rp[h];
+            *reinterpret_cast<float4*>(&Ds[buf][lr][lc + 4 * h]) = rd[h];
+        }
+    };
+    int buf = 0;
+    if (rbeg < rend) {
+        fetch(rbeg);
+        stash(0);
+    }
+    __syncthreads();
+    for (uint32_t r0 = rbeg; r0 < rend; r0 += kPgRows) {
+        const bool more = r0 + kPgRows < rend;
+        if (more) fetch(r0 + kPgRows);
 #pragma unroll 4
-        for (int r = 0; r < 32; ++r) {
-            float pa[4], db[4];
+        for (int r = 0; r < kPgRows; ++r) {
+            const float4 a0 = *reinterpret_cast<const float4*>(&Ps[buf][r][4 * ti]);
+            const float4 a1 = *reinterpret_cast<const float4*>(&Ps[buf][r][64 + 4 * ti]);
+            const float4 b0 = *reinterpret_cast<const float4*>(&Ds[buf][r][4 * tj]);
+            const float4 b1 = *reinterpret_cast<const float4*>(&Ds[buf][r][64 + 4 * tj]);
+            const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+            const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
 #pragma unroll
-            for (int a = 0; a < 4; ++a) pa[a] = Ps[r][ti * 4 + a];
+            for (int a = 0; a < 8; ++a)
 #pragma unroll
-            for (int b = 0; b < 4; ++b) db[b] = Ds[r][tj * 4 + b];
-#pragma unroll
-            for (int a = 0; a < 4; ++a)
-#pragma unroll
-                for (int b = 0; b < 4; ++b) acc[a][b] = fmaf(pa[a], db[b], acc[a][b]);
+                for (int b = 0; b < 8; ++b) acc[a][b] = fmaf(av[a], bv[b], acc[a][b]);
             if (ti == 0)
 #pragma unroll
-                for (int b = 0; b < 4; ++b) bacc[b] += db[b];
+                for (int b = 0; b < 8; ++b) bacc[b] += bv[b];
         }
+        if (more) stash(buf ^ 1);
         __syncthreads();
+        buf ^= 1;
     }
     float* w = p.ws + size_t(split) * p.din * p.dout;
 #pragma unroll
-    for (int a = 0; a < 4; ++a) {
-        const uint32_t i = i0 + ti * 4 + a;
+    for (int a = 0; a < 8; ++a) {
+        const uint32_t i = i0 + (a < 4 ? 4 * ti + a : 64 + 4 * ti + a - 4);
         if (i >= p.din) continue;
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
-            const uint32_t j = j0 + tj * 4 + b;
+        for (int b = 0; b < 8; ++b) {
+            const uint32_t j = b < 4 ? 4 * tj + b : 64 + 4 * tj + b - 4;
             if (j < p.dout) w[size_t(i) * p.dout + j] = acc[a][b];
         }
     }
     if (blockIdx.y == 0 && ti == 0 && p.wsb)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
-            const uint32_t j = j0 + tj * 4 + b;
+        for (int b = 0; b < 8; ++b) {
+            const uint32_t j = b < 4 ? 4 * tj + b : 64 + 4 * tj + b - 4;
             if (j < p.dout) p.wsb[size_t(split) * p.dout + j] = bacc[b];
         }
 }
