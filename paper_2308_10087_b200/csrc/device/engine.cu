@@ -29,7 +29,7 @@
 #include <vector>
 
 #include "../../../include/gnnpipe.h"
-#include "kernels.cuh"
+#include "rows8.cuh"
 
 namespace gp {
 namespace {
@@ -367,21 +367,21 @@ struct Stage {
 
     void setup_kernels() {
         const int smem_max = 64 * 1024 + 1024;
-        GP_CUDA(cudaFuncSetAttribute(k_fwd_fused<FWD_DENSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
-        GP_CUDA(cudaFuncSetAttribute(k_fwd_fused<FWD_GCN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
-        GP_CUDA(cudaFuncSetAttribute(k_fwd_fused<FWD_GCN2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
+        GP_CUDA(cudaFuncSetAttribute(k_fwd8<FWD_DENSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
+        GP_CUDA(cudaFuncSetAttribute(k_fwd8<FWD_GCN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
+        GP_CUDA(cudaFuncSetAttribute(k_fwd8<FWD_GCN2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
 #define SETB(P, O) \
-    GP_CUDA(cudaFuncSetAttribute(k_bwd<P, O>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
+    GP_CUDA(cudaFuncSetAttribute(k_bwd8<P, O>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
         SETB(PREV_TOP, OUT_LAYER) SETB(PREV_AGG, OUT_LAYER) SETB(PREV_AGG_HIST, OUT_LAYER)
         SETB(PREV_OWN, OUT_LAYER) SETB(PREV_AGG, OUT_DHIN) SETB(PREV_AGG_HIST, OUT_DHIN)
         SETB(PREV_OWN, OUT_DHIN)
 #undef SETB
         // Gathers bypass L1 (no_allocate): give the SM's unified L1/shared to shared
         // memory so 4 CTAs with a staged weight matrix fit per SM.
-        const void* big[] = {(const void*)k_fwd_fused<FWD_DENSE>, (const void*)k_fwd_fused<FWD_GCN>,
-                             (const void*)k_fwd_fused<FWD_GCN2>,  (const void*)k_bwd<PREV_TOP, OUT_LAYER>,
-                             (const void*)k_bwd<PREV_AGG, OUT_LAYER>, (const void*)k_bwd<PREV_AGG_HIST, OUT_LAYER>,
-                             (const void*)k_bwd<PREV_OWN, OUT_LAYER>};
+        const void* big[] = {(const void*)k_fwd8<FWD_DENSE>, (const void*)k_fwd8<FWD_GCN>,
+                             (const void*)k_fwd8<FWD_GCN2>,  (const void*)k_bwd8<PREV_TOP, OUT_LAYER>,
+                             (const void*)k_bwd8<PREV_AGG, OUT_LAYER>, (const void*)k_bwd8<PREV_AGG_HIST, OUT_LAYER>,
+                             (const void*)k_bwd8<PREV_OWN, OUT_LAYER>};
         for (const void* f : big)
             GP_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
                                          int(cudaSharedmemCarveoutMaxShared)));
@@ -644,7 +644,7 @@ struct Stage {
             p.gnext = gnext;
             p.gnstride = gnstride;
             p.next_mask = nk;
-            const size_t smem = (size_t(d.din) + 1) * ((d.dout + 3) / 4) * 16;
+            const size_t smem = (size_t(d.din) + 1) * ((d.dout + 7) / 8) * 32;
             const double e = d.agg ? double(rowptr_nnz(r0, r1)) : 0.0;
             const double bytes = (d.agg ? e * 8.0 + double(rows + 1) * 8.0 + double(n) * d.din * 4.0
                                         : double(rows) * d.din * 4.0) +
@@ -655,11 +655,11 @@ struct Stage {
             const double gather = e * double(d.sin) * 4.0;
             const int cls = d.agg ? GP_K_FWD_AGG : GP_K_FWD_DENSE;
             if (d.spec.kind == GP_DENSE)
-                launch(cls, bytes, flops, 0, [&]() { k_fwd_fused<FWD_DENSE><<<row_grid(rows, (const void*)k_fwd_fused<FWD_DENSE>, smem), kBlock, smem, cs>>>(p); });
+                launch(cls, bytes, flops, 0, [&]() { k_fwd8<FWD_DENSE><<<row_grid(rows, (const void*)k_fwd8<FWD_DENSE>, smem), kBlock, smem, cs>>>(p); });
             else if (d.spec.kind == GP_GCNCONV)
-                launch(cls, bytes, flops, gather, [&]() { k_fwd_fused<FWD_GCN><<<row_grid(rows, (const void*)k_fwd_fused<FWD_GCN>, smem), kBlock, smem, cs>>>(p); });
+                launch(cls, bytes, flops, gather, [&]() { k_fwd8<FWD_GCN><<<row_grid(rows, (const void*)k_fwd8<FWD_GCN>, smem), kBlock, smem, cs>>>(p); });
             else
-                launch(cls, bytes, flops, gather, [&]() { k_fwd_fused<FWD_GCN2><<<row_grid(rows, (const void*)k_fwd_fused<FWD_GCN2>, smem), kBlock, smem, cs>>>(p); });
+                launch(cls, bytes, flops, gather, [&]() { k_fwd8<FWD_GCN2><<<row_grid(rows, (const void*)k_fwd8<FWD_GCN2>, smem), kBlock, smem, cs>>>(p); });
             return;
         }
         // wide input (layer 0 with F > 128): pre first, then the tiled transform
@@ -759,7 +759,7 @@ struct Stage {
         p.dh0 = dh0;
         p.bg = d.bg;
         p.bgstride = d.sin;
-        const size_t smem = p.need_dagg ? size_t(d.dout) * ((d.din + 3) / 4) * 16 : 0;
+        const size_t smem = p.need_dagg ? size_t(d.dout) * ((d.din + 7) / 8) * 32 : 0;
         const double bytes = e * 8.0 + (e > 0 ? double(n) * d.dout * 4.0 : double(rows) * d.dout * 4.0) +
                              double(rows) * d.dout * 8.0 + (p.need_dagg ? double(rows) * d.din * 4.0 : 0.0) +
                              (p.gcn2 ? double(rows) * d.din * 8.0 : 0.0);
@@ -768,17 +768,17 @@ struct Stage {
         const int cls = prev == PREV_AGG || prev == PREV_AGG_HIST ? GP_K_BWD_AGG : GP_K_BWD_DENSE;
         switch (prev) {
             case PREV_TOP:
-                launch(cls, bytes, flops, 0, [&]() { k_bwd<PREV_TOP, OUT_LAYER><<<row_grid(rows, (const void*)k_bwd<PREV_TOP, OUT_LAYER>, smem), kBlock, smem, cs>>>(p); });
+                launch(cls, bytes, flops, 0, [&]() { k_bwd8<PREV_TOP, OUT_LAYER><<<row_grid(rows, (const void*)k_bwd8<PREV_TOP, OUT_LAYER>, smem), kBlock, smem, cs>>>(p); });
                 break;
             case PREV_AGG:
-                launch(cls, bytes, flops, gather, [&]() { k_bwd<PREV_AGG, OUT_LAYER><<<row_grid(rows, (const void*)k_bwd<PREV_AGG, OUT_LAYER>, smem), kBlock, smem, cs>>>(p); });
+                launch(cls, bytes, flops, gather, [&]() { k_bwd8<PREV_AGG, OUT_LAYER><<<row_grid(rows, (const void*)k_bwd8<PREV_AGG, OUT_LAYER>, smem), kBlock, smem, cs>>>(p); });
                 break;
             case PREV_AGG_HIST:
                 launch(cls, bytes, flops, gather,
-                       [&]() { k_bwd<PREV_AGG_HIST, OUT_LAYER><<<row_grid(rows, (const void*)k_bwd<PREV_AGG_HIST, OUT_LAYER>, smem), kBlock, smem, cs>>>(p); });
+                       [&]() { k_bwd8<PREV_AGG_HIST, OUT_LAYER><<<row_grid(rows, (const void*)k_bwd8<PREV_AGG_HIST, OUT_LAYER>, smem), kBlock, smem, cs>>>(p); });
                 break;
             default:
-                launch(cls, bytes, flops, 0, [&]() { k_bwd<PREV_OWN, OUT_LAYER><<<row_grid(rows, (const void*)k_bwd<PREV_OWN, OUT_LAYER>, smem), kBlock, smem, cs>>>(p); });
+                launch(cls, bytes, flops, 0, [&]() { k_bwd8<PREV_OWN, OUT_LAYER><<<row_grid(rows, (const void*)k_bwd8<PREV_OWN, OUT_LAYER>, smem), kBlock, smem, cs>>>(p); });
         }
     }
 
@@ -805,13 +805,13 @@ struct Stage {
         const double e = d.agg ? double(rowptr_nnz(r0, r1)) : 0.0;
         const double bytes = e * 8.0 + (d.agg ? double(n) : double(rows)) * d.din * 4.0 + double(rows) * d.din * 4.0;
         if (!d.agg)
-            launch(GP_K_BWD_DENSE, bytes, 0, 0, [&]() { k_bwd<PREV_OWN, OUT_DHIN><<<row_grid(rows, (const void*)k_bwd<PREV_OWN, OUT_DHIN>, 0), kBlock, 0, cs>>>(p); });
+            launch(GP_K_BWD_DENSE, bytes, 0, 0, [&]() { k_bwd8<PREV_OWN, OUT_DHIN><<<row_grid(rows, (const void*)k_bwd8<PREV_OWN, OUT_DHIN>, 0), kBlock, 0, cs>>>(p); });
         else if (hist)
             launch(GP_K_BWD_AGG, bytes, 2.0 * e * d.din, e * d.sin * 4.0,
-                   [&]() { k_bwd<PREV_AGG_HIST, OUT_DHIN><<<row_grid(rows, (const void*)k_bwd<PREV_AGG_HIST, OUT_DHIN>, 0), kBlock, 0, cs>>>(p); });
+                   [&]() { k_bwd8<PREV_AGG_HIST, OUT_DHIN><<<row_grid(rows, (const void*)k_bwd8<PREV_AGG_HIST, OUT_DHIN>, 0), kBlock, 0, cs>>>(p); });
         else
             launch(GP_K_BWD_AGG, bytes, 2.0 * e * d.din, e * d.sin * 4.0,
-                   [&]() { k_bwd<PREV_AGG, OUT_DHIN><<<row_grid(rows, (const void*)k_bwd<PREV_AGG, OUT_DHIN>, 0), kBlock, 0, cs>>>(p); });
+                   [&]() { k_bwd8<PREV_AGG, OUT_DHIN><<<row_grid(rows, (const void*)k_bwd8<PREV_AGG, OUT_DHIN>, 0), kBlock, 0, cs>>>(p); });
     }
 
     XentParams xent_params(uint32_t r0, uint32_t r1) {

@@ -226,83 +226,6 @@ struct FwdParams {
     DropKey next_mask;
 };
 
-template <int KIND>
-__global__ void __launch_bounds__(kBlock, 4) k_fwd_fused(FwdParams p) {
-    extern __shared__ float4 smem4[];
-    const uint32_t dout4 = (p.dout + 3) / 4;
-    float* Ws = reinterpret_cast<float*>(smem4);
-    float* bs = Ws + size_t(p.din) * dout4 * 4;
-    for (uint32_t idx = threadIdx.x; idx < p.din * dout4 * 4; idx += blockDim.x) {
-        const uint32_t i = idx / (dout4 * 4), c = idx % (dout4 * 4);
-        Ws[idx] = c < p.dout ? p.W[size_t(i) * p.dout + c] : 0.f;
-    }
-    for (uint32_t c = threadIdx.x; c < dout4 * 4; c += blockDim.x)
-        bs[c] = (p.bias && c < p.dout) ? p.bias[c] : 0.f;
-    __syncthreads();
-    const float4* Ws4 = reinterpret_cast<const float4*>(Ws);
-
-    const int lane = threadIdx.x & 31;
-    const bool in_act = uint32_t(4 * lane) < p.din;
-    const bool out_act = uint32_t(4 * lane) < p.dout;
-    const uint32_t din4 = (p.din + 3) / 4;
-    const uint32_t nw = gridDim.x * kWarpsPerBlock;
-    for (uint32_t v = p.r0 + blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5); v < p.r1; v += nw) {
-        float4 pre;
-        if (KIND == FWD_DENSE) {
-            const float4 x = in_act ? ld_stream(p.xsrc + size_t(v) * p.xstride + 4 * lane) : f4_zero();
-            pre = drop4(p.in_mask, p.orig[v], 4 * lane, p.din, x);
-        } else {
-            const float4 z = gather_row<false, false>(p.rowptr, p.edges, v, p.gsrc, nullptr, p.gstride,
-                                                      0ull, lane, in_act);
-            if (KIND == FWD_GCN2) {
-                const float4 h = in_act ? ld_stream(p.h0 + size_t(v) * p.h0stride + 4 * lane) : f4_zero();
-                pre.x = __fadd_rn(__fmul_rn(p.oma, z.x), __fmul_rn(p.alpha, h.x));
-                pre.y = __fadd_rn(__fmul_rn(p.oma, z.y), __fmul_rn(p.alpha, h.y));
-                pre.z = __fadd_rn(__fmul_rn(p.oma, z.z), __fmul_rn(p.alpha, h.z));
-                pre.w = __fadd_rn(__fmul_rn(p.oma, z.w), __fmul_rn(p.alpha, h.w));
-            } else {
-                pre = z;
-            }
-        }
-        if (in_act) st_stream(p.pre + size_t(v) * p.prestride + 4 * lane, pre);
-
-        float4 o = out_act ? reinterpret_cast<const float4*>(bs)[lane] : f4_zero();
-        for (uint32_t ib = 0; ib < din4; ++ib) {
-            const float4 pb = shfl4(pre, int(ib));
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const uint32_t i = 4 * ib + q;
-                const float xi = f4_get(pb, q);
-                if (i < p.din && xi != 0.f && out_act) {
-                    const float4 wr = Ws4[size_t(i) * dout4 + lane];
-                    o.x = mul_add(o.x, xi, wr.x);
-                    o.y = mul_add(o.y, xi, wr.y);
-                    o.z = mul_add(o.z, xi, wr.z);
-                    o.w = mul_add(o.w, xi, wr.w);
-                }
-            }
-        }
-        if (KIND == FWD_GCN2) {
-            o.x = __fadd_rn(__fmul_rn(p.omb, pre.x), __fmul_rn(p.beta, o.x));
-            o.y = __fadd_rn(__fmul_rn(p.omb, pre.y), __fmul_rn(p.beta, o.y));
-            o.z = __fadd_rn(__fmul_rn(p.omb, pre.z), __fmul_rn(p.beta, o.z));
-            o.w = __fadd_rn(__fmul_rn(p.omb, pre.w), __fmul_rn(p.beta, o.w));
-        }
-        if (p.relu) {
-            if (o.x < 0.f) o.x = 0.f;
-            if (o.y < 0.f) o.y = 0.f;
-            if (o.z < 0.f) o.z = 0.f;
-            if (o.w < 0.f) o.w = 0.f;
-        }
-        if (out_act) {
-            st_stream(p.out + size_t(v) * p.outstride + 4 * lane, o);
-            if (p.gnext)
-                st_stream(p.gnext + size_t(v) * p.gnstride + 4 * lane,
-                    drop4(p.next_mask, p.orig[v], 4 * lane, p.dout, o));
-        }
-    }
-}
-
 // GcnConv aggregation for d_in > 128 (column blocks of 128): pre = A_hat . G.
 struct SpmmParams {
     uint32_t r0, r1, width, zrow;
@@ -471,97 +394,6 @@ struct BwdParams {
     float* dh_in;
     uint32_t dhinstride;
 };
-
-template <int PREV, int OUT>
-__global__ void __launch_bounds__(kBlock, 4) k_bwd(BwdParams p) {
-    extern __shared__ float4 smem4[];
-    float* Wt = reinterpret_cast<float*>(smem4);
-    const uint32_t din4 = (p.din + 3) / 4;
-    if (OUT == OUT_LAYER && p.need_dagg) {
-        // Wt[j][c] = W[c][j]  (dout rows x din4*4 cols)
-        for (uint32_t idx = threadIdx.x; idx < p.dout * din4 * 4; idx += blockDim.x) {
-            const uint32_t j = idx / (din4 * 4), c = idx % (din4 * 4);
-            Wt[idx] = c < p.din ? p.W[size_t(c) * p.dout + j] : 0.f;
-        }
-        __syncthreads();
-    }
-    const float4* Wt4 = reinterpret_cast<const float4*>(Wt);
-    const int lane = threadIdx.x & 31;
-    const bool dh_act = uint32_t(4 * lane) < p.dh_width;
-    const uint32_t nw = gridDim.x * kWarpsPerBlock;
-    const uint32_t dout4 = (p.dout + 3) / 4;
-    for (uint32_t u = p.r0 + blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5); u < p.r1; u += nw) {
-        float4 dh;
-        if (PREV == PREV_TOP) {
-            dh = dh_act ? ld_stream(p.dtop + size_t(u) * p.dtopstride + 4 * lane) : f4_zero();
-        } else {
-            float4 s;
-            if (PREV == PREV_OWN)
-                s = dh_act ? ld_stream(p.bgn + size_t(u) * p.bgnstride + 4 * lane) : f4_zero();
-            else
-                s = gather_row<true, PREV == PREV_AGG_HIST>(p.rowptr, p.edges, u, p.bgn, p.bgn_snap,
-                                                            p.bgnstride, p.done, lane, dh_act);
-            dh = drop4(p.prev_mask, p.orig[u], 4 * lane, p.dh_width, s);
-        }
-        if (OUT == OUT_DHIN) {
-            if (dh_act) st_stream(p.dh_in + size_t(u) * p.dhinstride + 4 * lane, dh);
-            continue;
-        }
-        if (p.dh0_add && dh_act) {
-            const float4 a = ld_stream(p.dh0_add + size_t(u) * p.dh0stride + 4 * lane);
-            dh.x = __fadd_rn(dh.x, a.x);
-            dh.y = __fadd_rn(dh.y, a.y);
-            dh.z = __fadd_rn(dh.z, a.z);
-            dh.w = __fadd_rn(dh.w, a.w);
-        }
-        float4 dz = dh;
-        if (p.relu) {
-            const float4 h = dh_act ? ld_stream(p.h + size_t(u) * p.hstride + 4 * lane) : f4_zero();
-            dz.x = h.x > 0.f ? dh.x : 0.f;
-            dz.y = h.y > 0.f ? dh.y : 0.f;
-            dz.z = h.z > 0.f ? dh.z : 0.f;
-            dz.w = h.w > 0.f ? dh.w : 0.f;
-        }
-        if (dh_act) st_stream(p.dz + size_t(u) * p.dzstride + 4 * lane, dz);
-        if (!p.need_dagg) continue;
-        const bool in_act = uint32_t(4 * lane) < p.din;
-        float4 g = f4_zero();
-        for (uint32_t jb = 0; jb < dout4; ++jb) {
-            const float4 db = shfl4(dz, int(jb));
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const uint32_t j = 4 * jb + q;
-                if (j < p.dout && in_act) {
-                    const float dj = f4_get(db, q);
-                    const float4 w = Wt4[size_t(j) * din4 + lane];
-                    g.x = mul_add(g.x, dj, w.x);
-                    g.y = mul_add(g.y, dj, w.y);
-                    g.z = mul_add(g.z, dj, w.z);
-                    g.w = mul_add(g.w, dj, w.w);
-                }
-            }
-        }
-        if (!in_act) continue;
-        if (p.gcn2) {
-            g.x = __fadd_rn(__fmul_rn(p.omb, dz.x), __fmul_rn(p.beta, g.x));
-            g.y = __fadd_rn(__fmul_rn(p.omb, dz.y), __fmul_rn(p.beta, g.y));
-            g.z = __fadd_rn(__fmul_rn(p.omb, dz.z), __fmul_rn(p.beta, g.z));
-            g.w = __fadd_rn(__fmul_rn(p.omb, dz.w), __fmul_rn(p.beta, g.w));
-            float* d0 = p.dh0 + size_t(u) * p.dh0stride + 4 * lane;
-            float4 a = ld_stream(d0);
-            a.x = __fadd_rn(a.x, __fmul_rn(p.alpha, g.x));
-            a.y = __fadd_rn(a.y, __fmul_rn(p.alpha, g.y));
-            a.z = __fadd_rn(a.z, __fmul_rn(p.alpha, g.z));
-            a.w = __fadd_rn(a.w, __fmul_rn(p.alpha, g.w));
-            st_stream(d0, a);
-            g.x = __fmul_rn(p.oma, g.x);
-            g.y = __fmul_rn(p.oma, g.y);
-            g.z = __fmul_rn(p.oma, g.z);
-            g.w = __fmul_rn(p.oma, g.w);
-        }
-        st_stream(p.bg + size_t(u) * p.bgstride + 4 * lane, g);
-    }
-}
 
 // ---------------------------------------------------------------------------
 // Softmax cross-entropy head (nn.hpp:373-403, engines_impl.hpp:39-51, :725-734).
