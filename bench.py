@@ -191,13 +191,10 @@ def main():
         if dist:
             dist.barrier()
 
+    from paper_2308_10087_b200 import distributed as D
+
     def max_over_ranks(x):
-        if not dist:
-            return x
-        import torch
-        t = torch.tensor([x], dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return D.max_over_ranks(dist, x)
 
     S = world
     K = args.chunks or 4 * S
@@ -234,9 +231,8 @@ def main():
     def link(eng):
         if S == 1:
             return
-        ids = [gp.nccl_unique_id() for _ in range(S - 1)] if rank == 0 else [None] * (S - 1)
-        dist.broadcast_object_list(ids, src=0)
-        eng.link_nccl(ids[rank - 1] if rank > 0 else None, ids[rank] if rank < S - 1 else None)
+        ids = D.exchange_unique_ids(dist, rank, S, gp.nccl_unique_id)
+        eng.link_nccl(*D.boundary_ids(ids, rank, S))
 
     def order(t):
         return gp.shuffle_chunk_order(K, t, 1)
