@@ -322,7 +322,11 @@ def main():
     tp = os.path.join(ROOT, "profiles", "roofline_traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get(args.workload)
+            t = json.load(open(tp)).get(args.workload)
+            if t and L == WORKLOADS[args.workload][6]:
+                # ncu DRAM bytes per row x the average rows of one launch (one chunk)
+                traffic = {"value": t["dram_bytes_per_row"] * N / K / 1e9, "unit": "GB/launch",
+                           "source": t["source"]}
         except Exception:
             traffic = None
     agg_layers = sum(1 for s in specs if s.aggregates)
@@ -339,7 +343,7 @@ def main():
         "e2e": e2e,
         "gpu_launches": int(launches),
         "edges_per_s": edges_per_s,
-        "roofline": {"kernel": "k_fwd_fused<FWD_GCN2> (CSR SpMM + GCNII mix + W + ReLU + next-layer dropout)",
+        "roofline": {"kernel": "k_fwd8<FWD_GCN2> (CSR SpMM + GCNII mix + W + ReLU + next-layer dropout)",
                      "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": (achieved / hbm) if achieved else None, "peak_source": src, "traffic": traffic,
                      "l2_gather_gbs": gather_rate,
