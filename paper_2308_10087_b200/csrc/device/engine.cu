@@ -18,6 +18,7 @@
 #include <chrono>
 #include <cmath>
 #include <condition_variable>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <map>
@@ -365,26 +366,67 @@ struct Stage {
         GP_CUDA(cudaDeviceSynchronize());
     }
 
-    void setup_kernels() {
-        const int smem_max = 64 * 1024 + 1024;
-        GP_CUDA(cudaFuncSetAttribute(k_fwd8<FWD_DENSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
-        GP_CUDA(cudaFuncSetAttribute(k_fwd8<FWD_GCN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
-        GP_CUDA(cudaFuncSetAttribute(k_fwd8<FWD_GCN2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
-#define SETB(P, O) \
-    GP_CUDA(cudaFuncSetAttribute(k_bwd8<P, O>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
-        SETB(PREV_TOP, OUT_LAYER) SETB(PREV_AGG, OUT_LAYER) SETB(PREV_AGG_HIST, OUT_LAYER)
-        SETB(PREV_OWN, OUT_LAYER) SETB(PREV_AGG, OUT_DHIN) SETB(PREV_AGG_HIST, OUT_DHIN)
-        SETB(PREV_OWN, OUT_DHIN)
-#undef SETB
-        // Gathers bypass L1 (no_allocate): give the SM's unified L1/shared to shared
-        // memory so 4 CTAs with a staged weight matrix fit per SM.
-        const void* big[] = {(const void*)k_fwd8<FWD_DENSE>, (const void*)k_fwd8<FWD_GCN>,
-                             (const void*)k_fwd8<FWD_GCN2>,  (const void*)k_bwd8<PREV_TOP, OUT_LAYER>,
-                             (const void*)k_bwd8<PREV_AGG, OUT_LAYER>, (const void*)k_bwd8<PREV_AGG_HIST, OUT_LAYER>,
-                             (const void*)k_bwd8<PREV_OWN, OUT_LAYER>};
-        for (const void* f : big)
+    // Gathers in flight per lane (template NB of the row kernels); GP_NB overrides.
+    int nb = 4;
+
+    // Row kernels stage a weight matrix (<= 66 KB) in shared memory; gathers bypass
+    // L1 (no_allocate), so the unified L1/shared carveout goes to shared memory.
+    template <int NB>
+    void setup_nb() {
+        const int smem_max = 66 * 1024;
+        const void* fns[] = {(const void*)k_fwd8<FWD_DENSE, NB>,
+                             (const void*)k_fwd8<FWD_GCN, NB>,
+                             (const void*)k_fwd8<FWD_GCN2, NB>,
+                             (const void*)k_bwd8<PREV_TOP, OUT_LAYER, NB>,
+                             (const void*)k_bwd8<PREV_AGG, OUT_LAYER, NB>,
+                             (const void*)k_bwd8<PREV_AGG_HIST, OUT_LAYER, NB>,
+                             (const void*)k_bwd8<PREV_OWN, OUT_LAYER, NB>,
+                             (const void*)k_bwd8<PREV_AGG, OUT_DHIN, NB>,
+                             (const void*)k_bwd8<PREV_AGG_HIST, OUT_DHIN, NB>,
+                             (const void*)k_bwd8<PREV_OWN, OUT_DHIN, NB>};
+        for (const void* f : fns) {
+            GP_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
             GP_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
                                          int(cudaSharedmemCarveoutMaxShared)));
+        }
+    }
+
+    void setup_kernels() {
+        if (const char* e = std::getenv("GP_NB")) {
+            const int v = std::atoi(e);
+            if (v == 2 || v == 4 || v == 6 || v == 8) nb = v;
+        }
+        setup_nb<2>();
+        setup_nb<4>();
+        setup_nb<6>();
+        setup_nb<8>();
+    }
+
+    template <int KIND, int NB>
+    void fwd_go(uint32_t rows, size_t smem, const FwdParams& p) {
+        k_fwd8<KIND, NB><<<row_grid(rows, (const void*)k_fwd8<KIND, NB>, smem, 16), kBlock, smem, cs>>>(p);
+    }
+    template <int KIND>
+    void fwd_nb(uint32_t rows, size_t smem, const FwdParams& p) {
+        switch (nb) {
+            case 2: fwd_go<KIND, 2>(rows, smem, p); break;
+            case 6: fwd_go<KIND, 6>(rows, smem, p); break;
+            case 8: fwd_go<KIND, 8>(rows, smem, p); break;
+            default: fwd_go<KIND, 4>(rows, smem, p);
+        }
+    }
+    template <int PREV, int OUT, int NB>
+    void bwd_go(uint32_t rows, size_t smem, const BwdParams& p) {
+        k_bwd8<PREV, OUT, NB><<<row_grid(rows, (const void*)k_bwd8<PREV, OUT, NB>, smem, 16), kBlock, smem, cs>>>(p);
+    }
+    template <int PREV, int OUT>
+    void bwd_nb(uint32_t rows, size_t smem, const BwdParams& p) {
+        switch (nb) {
+            case 2: bwd_go<PREV, OUT, 2>(rows, smem, p); break;
+            case 6: bwd_go<PREV, OUT, 6>(rows, smem, p); break;
+            case 8: bwd_go<PREV, OUT, 8>(rows, smem, p); break;
+            default: bwd_go<PREV, OUT, 4>(rows, smem, p);
+        }
     }
 
     // ---- graph --------------------------------------------------------------
@@ -552,7 +594,7 @@ struct Stage {
 
     // Persistent grid: exactly the resident capacity (occupancy x SMs), capped by
     // the number of 8-row blocks, so there is no partial second wave.
-    uint32_t row_grid(uint32_t rows, const void* fn, size_t smem) {
+    uint32_t row_grid(uint32_t rows, const void* fn, size_t smem, uint32_t rows_per_block = kWarpsPerBlock) {
         auto key = std::make_pair(fn, smem);
         auto it = occ_cache.find(key);
         int occ = 0;
@@ -562,7 +604,7 @@ struct Stage {
         } else {
             occ = it->second;
         }
-        const uint64_t want = (uint64_t(rows) + kWarpsPerBlock - 1) / kWarpsPerBlock;
+        const uint64_t want = (uint64_t(rows) + rows_per_block - 1) / rows_per_block;
         const uint64_t cap = uint64_t(num_sms) * occ;
         return uint32_t(std::max<uint64_t>(1, std::min(want, cap)));
     }
@@ -655,11 +697,11 @@ struct Stage {
             const double gather = e * double(d.sin) * 4.0;
             const int cls = d.agg ? GP_K_FWD_AGG : GP_K_FWD_DENSE;
             if (d.spec.kind == GP_DENSE)
-                launch(cls, bytes, flops, 0, [&]() { k_fwd8<FWD_DENSE><<<row_grid(rows, (const void*)k_fwd8<FWD_DENSE>, smem), kBlock, smem, cs>>>(p); });
+                launch(cls, bytes, flops, 0, [&]() { fwd_nb<FWD_DENSE>(rows, smem, p); });
             else if (d.spec.kind == GP_GCNCONV)
-                launch(cls, bytes, flops, gather, [&]() { k_fwd8<FWD_GCN><<<row_grid(rows, (const void*)k_fwd8<FWD_GCN>, smem), kBlock, smem, cs>>>(p); });
+                launch(cls, bytes, flops, gather, [&]() { fwd_nb<FWD_GCN>(rows, smem, p); });
             else
-                launch(cls, bytes, flops, gather, [&]() { k_fwd8<FWD_GCN2><<<row_grid(rows, (const void*)k_fwd8<FWD_GCN2>, smem), kBlock, smem, cs>>>(p); });
+                launch(cls, bytes, flops, gather, [&]() { fwd_nb<FWD_GCN2>(rows, smem, p); });
             return;
         }
         // wide input (layer 0 with F > 128): pre first, then the tiled transform
@@ -768,17 +810,17 @@ struct Stage {
         const int cls = prev == PREV_AGG || prev == PREV_AGG_HIST ? GP_K_BWD_AGG : GP_K_BWD_DENSE;
         switch (prev) {
             case PREV_TOP:
-                launch(cls, bytes, flops, 0, [&]() { k_bwd8<PREV_TOP, OUT_LAYER><<<row_grid(rows, (const void*)k_bwd8<PREV_TOP, OUT_LAYER>, smem), kBlock, smem, cs>>>(p); });
+                launch(cls, bytes, flops, 0, [&]() { bwd_nb<PREV_TOP, OUT_LAYER>(rows, smem, p); });
                 break;
             case PREV_AGG:
-                launch(cls, bytes, flops, gather, [&]() { k_bwd8<PREV_AGG, OUT_LAYER><<<row_grid(rows, (const void*)k_bwd8<PREV_AGG, OUT_LAYER>, smem), kBlock, smem, cs>>>(p); });
+                launch(cls, bytes, flops, gather, [&]() { bwd_nb<PREV_AGG, OUT_LAYER>(rows, smem, p); });
                 break;
             case PREV_AGG_HIST:
                 launch(cls, bytes, flops, gather,
-                       [&]() { k_bwd8<PREV_AGG_HIST, OUT_LAYER><<<row_grid(rows, (const void*)k_bwd8<PREV_AGG_HIST, OUT_LAYER>, smem), kBlock, smem, cs>>>(p); });
+                       [&]() { bwd_nb<PREV_AGG_HIST, OUT_LAYER>(rows, smem, p); });
                 break;
             default:
-                launch(cls, bytes, flops, 0, [&]() { k_bwd8<PREV_OWN, OUT_LAYER><<<row_grid(rows, (const void*)k_bwd8<PREV_OWN, OUT_LAYER>, smem), kBlock, smem, cs>>>(p); });
+                launch(cls, bytes, flops, 0, [&]() { bwd_nb<PREV_OWN, OUT_LAYER>(rows, smem, p); });
         }
     }
 
@@ -805,13 +847,13 @@ struct Stage {
         const double e = d.agg ? double(rowptr_nnz(r0, r1)) : 0.0;
         const double bytes = e * 8.0 + (d.agg ? double(n) : double(rows)) * d.din * 4.0 + double(rows) * d.din * 4.0;
         if (!d.agg)
-            launch(GP_K_BWD_DENSE, bytes, 0, 0, [&]() { k_bwd8<PREV_OWN, OUT_DHIN><<<row_grid(rows, (const void*)k_bwd8<PREV_OWN, OUT_DHIN>, 0), kBlock, 0, cs>>>(p); });
+            launch(GP_K_BWD_DENSE, bytes, 0, 0, [&]() { bwd_nb<PREV_OWN, OUT_DHIN>(rows, 0, p); });
         else if (hist)
             launch(GP_K_BWD_AGG, bytes, 2.0 * e * d.din, e * d.sin * 4.0,
-                   [&]() { k_bwd8<PREV_AGG_HIST, OUT_DHIN><<<row_grid(rows, (const void*)k_bwd8<PREV_AGG_HIST, OUT_DHIN>, 0), kBlock, 0, cs>>>(p); });
+                   [&]() { bwd_nb<PREV_AGG_HIST, OUT_DHIN>(rows, 0, p); });
         else
             launch(GP_K_BWD_AGG, bytes, 2.0 * e * d.din, e * d.sin * 4.0,
-                   [&]() { k_bwd8<PREV_AGG, OUT_DHIN><<<row_grid(rows, (const void*)k_bwd8<PREV_AGG, OUT_DHIN>, 0), kBlock, 0, cs>>>(p); });
+                   [&]() { bwd_nb<PREV_AGG, OUT_DHIN>(rows, 0, p); });
     }
 
     XentParams xent_params(uint32_t r0, uint32_t r1) {

@@ -68,13 +68,13 @@ __device__ __forceinline__ F8 shfl8(const F8& x, int src) {
     return r;
 }
 
-constexpr int kNB = 4;  // gathers in flight per lane (x 2 rows per warp)
+// NB = gathers in flight per lane (x 2 rows per warp), a template parameter.
 
 // Sum over the CSR row of w * src[col] (8 columns per lane). FILTER drops
 // entries of not-yet-done chunks (stable ballot compaction per 16-entry batch);
 // HIST reads those from `snap` instead. Padding slots use weight 0 and keep the
 // previous registers: acc starts at +0 and never becomes -0, so acc + 0*x == acc.
-template <bool FILTER, bool HIST>
+template <bool FILTER, bool HIST, int NB>
 __device__ __forceinline__ F8 gather_row8(const uint64_t* __restrict__ rowptr, const uint2* __restrict__ edges,
                                           uint32_t v, bool has_row, const float* __restrict__ src,
                                           const float* __restrict__ snap, uint32_t stride, uint64_t done,
@@ -106,11 +106,11 @@ __device__ __forceinline__ F8 gather_row8(const uint64_t* __restrict__ rowptr, c
             my.y = __shfl_sync(kFull, my.y, hb + from);
         }
         const int cmax = max(cnt, __shfl_xor_sync(kFull, cnt, 16));
-        for (int t = 0; t < cmax; t += kNB) {
-            float w[kNB];
-            F8 x[kNB];
+        for (int t = 0; t < cmax; t += NB) {
+            float w[NB];
+            F8 x[NB];
 #pragma unroll
-            for (int i = 0; i < kNB; ++i) {
+            for (int i = 0; i < NB; ++i) {
                 const int tt = t + i;
                 const int sl = hb + (tt & 15);
                 const uint32_t packed = __shfl_sync(kFull, my.x, sl);
@@ -122,7 +122,7 @@ __device__ __forceinline__ F8 gather_row8(const uint64_t* __restrict__ rowptr, c
                 x[i] = ld8_gather(valid ? s + size_t(packed & kColMask) * stride : lpad);
             }
 #pragma unroll
-            for (int i = 0; i < kNB; ++i)
+            for (int i = 0; i < NB; ++i)
 #pragma unroll
                 for (int c = 0; c < 8; ++c) acc.v[c] = mul_add(acc.v[c], w[i], x[i].v[c]);
         }
@@ -184,8 +184,8 @@ __device__ __forceinline__ void gemv8(F8& o, const F8& x, const float4* Ws4, uin
 // -0 and x*W = +-0 leaves a non -0 accumulator unchanged) -> identity mix ->
 // ReLU -> h, and the next layer's dropped gather source.
 // ---------------------------------------------------------------------------
-template <int KIND>
-__global__ void __launch_bounds__(kBlock, 3) k_fwd8(FwdParams p) {
+template <int KIND, int NB>
+__global__ void __launch_bounds__(kBlock, NB <= 4 ? 3 : 2) k_fwd8(FwdParams p) {
     extern __shared__ float4 smem4[];
     const uint32_t c8 = (p.dout + 7) / 8;
     float* Ws = reinterpret_cast<float*>(smem4);
@@ -212,7 +212,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_fwd8(FwdParams p) {
             const F8 x = (has && in_act) ? ld8_stream(p.xsrc + size_t(v) * p.xstride + 8 * hl) : f8_zero();
             pre = drop8(p.in_mask, has ? p.orig[v] : 0u, 8 * hl, p.din, x);
         } else {
-            const F8 z = gather_row8<false, false>(p.rowptr, p.edges, v, has, p.gsrc, nullptr, p.gstride, 0ull, lane,
+            const F8 z = gather_row8<false, false, NB>(p.rowptr, p.edges, v, has, p.gsrc, nullptr, p.gstride, 0ull, lane,
                                                    in_act);
             if (KIND == FWD_GCN2) {
                 const F8 h = (has && in_act) ? ld8_stream(p.h0 + size_t(v) * p.h0stride + 8 * hl) : f8_zero();
@@ -255,8 +255,8 @@ __global__ void __launch_bounds__(kBlock, 3) k_fwd8(FwdParams p) {
 // layer i (nn.hpp:202-218): dz, dagg = dz.W^T, GCNII mixes, dh0 += a*dagg, and
 // bg_i = (1-a)*dagg (Gcn2Conv) or dagg.
 // ---------------------------------------------------------------------------
-template <int PREV, int OUT>
-__global__ void __launch_bounds__(kBlock, 3) k_bwd8(BwdParams p) {
+template <int PREV, int OUT, int NB>
+__global__ void __launch_bounds__(kBlock, NB <= 4 ? 3 : 2) k_bwd8(BwdParams p) {
     extern __shared__ float4 smem4[];
     float* Wt = reinterpret_cast<float*>(smem4);
     const uint32_t c8 = (p.din + 7) / 8;
@@ -281,7 +281,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_bwd8(BwdParams p) {
             if (PREV == PREV_OWN)
                 s = (has && dh_act) ? ld8_stream(p.bgn + size_t(u) * p.bgnstride + 8 * hl) : f8_zero();
             else
-                s = gather_row8<true, PREV == PREV_AGG_HIST>(p.rowptr, p.edges, u, has, p.bgn, p.bgn_snap, p.bgnstride,
+                s = gather_row8<true, PREV == PREV_AGG_HIST, NB>(p.rowptr, p.edges, u, has, p.bgn, p.bgn_snap, p.bgnstride,
                                                              p.done, lane, dh_act);
             dh = drop8(p.prev_mask, has ? p.orig[u] : 0u, 8 * hl, p.dh_width, s);
         }
