@@ -147,6 +147,8 @@ gp_status gp_upload_labels(gp_ctx* ctx, const uint32_t* labels, const uint8_t* s
 /* LayerParams (nn.hpp:54-58): W k_in x out row-major, b out (NULL if none). */
 gp_status gp_set_layer_params(gp_ctx* ctx, uint32_t layer, const float* W, const float* b);
 gp_status gp_get_layer_params(gp_ctx* ctx, uint32_t layer, float* W, float* b);
+/* ParamGrads of the last epoch (nn.hpp:264-293, Gcn2Conv already scaled by beta). */
+gp_status gp_get_layer_grads(gp_ctx* ctx, uint32_t layer, float* W, float* b);
 
 /* ---- transport (stage boundaries, engines_impl.hpp:690-724) -------------- */
 /* Same process: upstream stage s and downstream stage s+1 exchange chunk rows

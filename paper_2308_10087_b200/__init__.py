@@ -162,6 +162,7 @@ def _L():
         "gp_upload_labels": (C.c_int, [vp, u32p, u8p]),
         "gp_set_layer_params": (C.c_int, [vp, C.c_uint32, f32p, f32p]),
         "gp_get_layer_params": (C.c_int, [vp, C.c_uint32, f32p, f32p]),
+        "gp_get_layer_grads": (C.c_int, [vp, C.c_uint32, f32p, f32p]),
         "gp_link_local": (C.c_int, [vp, vp]),
         "gp_nccl_unique_id": (C.c_int, [P(C.c_uint8)]),
         "gp_link_nccl": (C.c_int, [vp, P(C.c_uint8), P(C.c_uint8)]),
@@ -543,6 +544,14 @@ class StageEngine:
         W = np.zeros((s.in_dim, s.out_dim), np.float32)
         b = np.zeros(s.out_dim if s.has_bias else 0, np.float32)
         _gp(_L().gp_get_layer_params(self._h, layer, _ptr(W, C.c_float), _ptr(b, C.c_float) if b.size else None),
+            self._h)
+        return W, b
+
+    def get_grads(self, layer: int):
+        s = self.specs[layer]
+        W = np.zeros((s.in_dim, s.out_dim), np.float32)
+        b = np.zeros(s.out_dim if s.has_bias else 0, np.float32)
+        _gp(_L().gp_get_layer_grads(self._h, layer, _ptr(W, C.c_float), _ptr(b, C.c_float) if b.size else None),
             self._h)
         return W, b
 

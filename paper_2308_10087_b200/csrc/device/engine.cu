@@ -31,6 +31,7 @@
 
 #include "../../../include/gnnpipe.h"
 #include "rows8.cuh"
+#include "tc_pgrad.cuh"
 
 namespace gp {
 namespace {
@@ -391,7 +392,12 @@ struct Stage {
         }
     }
 
+    // Parameter gradients on tcgen05 (default) or CUDA cores (GP_PGRAD=simt).
+    bool use_tc_pgrad = true;
+
     void setup_kernels() {
+        if (const char* e = std::getenv("GP_PGRAD")) use_tc_pgrad = std::string(e) != "simt";
+        GP_CUDA(cudaFuncSetAttribute(k_pgrad_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         if (const char* e = std::getenv("GP_NB")) {
             const int v = std::atoi(e);
             if (v == 2 || v == 4 || v == 6 || v == 8) nb = v;
@@ -554,6 +560,14 @@ struct Stage {
             if (!b) throw Error(GP_EINVAL, "layer has a bias");
             GP_CUDA(cudaMemcpy(d.b, b, size_t(d.dout) * 4, cudaMemcpyHostToDevice));
         }
+    }
+
+    void get_grads(uint32_t l, float* W, float* b) {
+        GP_CUDA(cudaSetDevice(device));
+        GP_CUDA(cudaStreamSynchronize(cs));
+        auto& d = layer(l);
+        if (W) GP_CUDA(cudaMemcpy(W, d.gW, size_t(d.din) * d.dout * 4, cudaMemcpyDeviceToHost));
+        if (d.gb && b) GP_CUDA(cudaMemcpy(b, d.gb, size_t(d.dout) * 4, cudaMemcpyDeviceToHost));
     }
 
     void get_params(uint32_t l, float* W, float* b) {
@@ -881,16 +895,27 @@ struct Stage {
         for (uint32_t i = 0; i < len; ++i) {
             auto& d = L[i];
             const uint32_t ti = (d.din + 127) / 128, tj = 1;
-            const uint32_t rps = (n + splits - 1) / splits;
-            PgradParams pp{n, rps, d.pre, d.sin, d.dz, d.sout, d.din, d.dout, ws, d.gb ? wsb : nullptr};
-            dim3 grid(splits, ti, 1);
-            launch(GP_K_PGRAD, double(n) * (d.din * tj + d.dout * ti) * 4.0 + double(splits) * d.din * d.dout * 4.0,
-                   2.0 * double(n) * d.din * d.dout, 0,
-                   [&]() { k_pgrad_partial<<<grid, 256, 0, cs>>>(pp); });
+            const double pg_bytes = double(n) * (d.din * tj + d.dout * ti) * 4.0 + double(splits) * d.din * d.dout * 4.0;
+            const double pg_flops = 2.0 * double(n) * d.din * d.dout;
+            uint32_t used_splits = splits;
+            if (use_tc_pgrad) {
+                // tcgen05 (3xTF32) split-K GEMM, one CTA per SM (TMEM accumulator, ~120 KB smem)
+                used_splits = std::min<uint32_t>(splits, uint32_t(num_sms));
+                TcPgradParams tp{n, (n + used_splits - 1) / used_splits, d.pre, d.sin, d.dz, d.sout, d.din, d.dout,
+                                 (d.dout + 15) / 16 * 16, ws, d.gb ? wsb : nullptr};
+                const size_t smem = 2 * (2 * size_t(kTcM) * kTcKt * 4 + 2 * size_t(tp.npad) * kTcKt * 4);
+                dim3 grid(used_splits, ti, 1);
+                launch(GP_K_PGRAD, pg_bytes, pg_flops, 0, [&]() { k_pgrad_tc<<<grid, kTcThreads, smem, cs>>>(tp); });
+            } else {
+                const uint32_t rps = (n + splits - 1) / splits;
+                PgradParams pp{n, rps, d.pre, d.sin, d.dz, d.sout, d.din, d.dout, ws, d.gb ? wsb : nullptr};
+                dim3 grid(splits, ti, 1);
+                launch(GP_K_PGRAD, pg_bytes, pg_flops, 0, [&]() { k_pgrad_partial<<<grid, 256, 0, cs>>>(pp); });
+            }
             const uint32_t tot = d.din * d.dout + d.dout;
             const bool gcn2 = d.spec.kind == GP_GCN2CONV;
             launch(GP_K_PGRAD, double(splits) * tot * 4.0 + tot * 4.0, 0, 0, [&]() {
-                k_pgrad_fold<<<(tot + 255) / 256, 256, 0, cs>>>(ws, d.gb ? wsb : nullptr, splits, d.din, d.dout,
+                k_pgrad_fold<<<(tot + 255) / 256, 256, 0, cs>>>(ws, d.gb ? wsb : nullptr, used_splits, d.din, d.dout,
                                                                 float(d.spec.beta), gcn2, d.gW, d.gb);
             });
             AdamParams a{};
@@ -1318,6 +1343,10 @@ gp_status gp_set_layer_params(gp_ctx* ctx, uint32_t layer, const float* W, const
 
 gp_status gp_get_layer_params(gp_ctx* ctx, uint32_t layer, float* W, float* b) {
     return gp::guard(&ctx->st, [&]() { ctx->st.get_params(layer, W, b); });
+}
+
+gp_status gp_get_layer_grads(gp_ctx* ctx, uint32_t layer, float* W, float* b) {
+    return gp::guard(&ctx->st, [&]() { ctx->st.get_grads(layer, W, b); });
 }
 
 gp_status gp_link_local(gp_ctx* up, gp_ctx* down) {

@@ -185,7 +185,7 @@ __device__ __forceinline__ void gemv8(F8& o, const F8& x, const float4* Ws4, uin
 // ReLU -> h, and the next layer's dropped gather source.
 // ---------------------------------------------------------------------------
 template <int KIND, int NB>
-__global__ void __launch_bounds__(kBlock, NB <= 4 ? 3 : 2) k_fwd8(FwdParams p) {
+__global__ void __launch_bounds__(kBlock, NB == 2 ? 4 : (NB == 4 ? 3 : 2)) k_fwd8(FwdParams p) {
     extern __shared__ float4 smem4[];
     const uint32_t c8 = (p.dout + 7) / 8;
     float* Ws = reinterpret_cast<float*>(smem4);
@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(kBlock, NB <= 4 ? 3 : 2) k_fwd8(FwdParams p) {
 // bg_i = (1-a)*dagg (Gcn2Conv) or dagg.
 // ---------------------------------------------------------------------------
 template <int PREV, int OUT, int NB>
-__global__ void __launch_bounds__(kBlock, NB <= 4 ? 3 : 2) k_bwd8(BwdParams p) {
+__global__ void __launch_bounds__(kBlock, NB == 2 ? 4 : (NB == 4 ? 3 : 2)) k_bwd8(BwdParams p) {
     extern __shared__ float4 smem4[];
     float* Wt = reinterpret_cast<float*>(smem4);
     const uint32_t c8 = (p.din + 7) / 8;

@@ -91,6 +91,37 @@ def test_epoch1_forward_bitexact_and_backward_close(gp, name, kind, layers):
         assert rel(eng.download("dh0"), ref["dh0"]) < 1e-4
 
 
+@pytest.mark.parametrize("mode", ["tc", "simt"])
+@pytest.mark.parametrize("name,kind,layers", [("forward_gcn", 0, 3), ("forward_gcnii", 2, 5)])
+def test_param_grads_match_reference(gp, name, kind, layers, mode, monkeypatch):
+    """param_grads_for_rows (nn.hpp:269-293): tcgen05 3xTF32 (default) and CUDA-core paths."""
+    monkeypatch.setenv("GP_PGRAD", mode)
+    ref = golden(name)
+    ds = er500(gp)
+    model = gp.ModelConfig(kind=kind, layers=layers, hidden=16)
+    eng, specs = single_stage(gp, ds, model, seed=7)
+    eng.run_epoch(1, [0])
+    for l in range(layers):
+        gW, gb = eng.get_grads(l)
+        assert rel(gW, ref[f"gW{l}"]) < 1e-4, (mode, l, rel(gW, ref[f"gW{l}"]))
+        if gb.size:
+            assert rel(gb, ref[f"gb{l}"]) < 1e-4, (mode, l)
+
+
+def test_param_grads_wide_layer_tc(gp, monkeypatch):
+    """tcgen05 path with k_in = 300 (three M tiles, last partial) and N = 40 (padded to 48)."""
+    monkeypatch.setenv("GP_PGRAD", "tc")
+    ds = gp.Dataset.synthetic_er(2000, 0.004, 4, 300, 40, 6)
+    model = gp.ModelConfig(kind=2, layers=3, hidden=40)
+    eng, specs = single_stage(gp, ds, model, seed=3)
+    eng.run_epoch(1, [0])
+    pre = eng.download("pre", 0).astype(np.float64)
+    dz = eng.download("dz", 0).astype(np.float64)
+    gW, gb = eng.get_grads(0)
+    assert rel(gW, pre.T @ dz) < 1e-5
+    assert rel(gb, dz.sum(0)) < 1e-5
+
+
 def test_params_after_one_adam_step(gp):
     ref = golden("forward_gcnii")
     ds = er500(gp)
