@@ -24,7 +24,7 @@
 
 namespace gp {
 
-constexpr int kTcThreads = 128;  // 4 warps: all load, warp 0 lane 0 issues MMAs
+constexpr int kTcThreads = 256;  // 8 warps stage operands; warps 0-3 read TMEM; one thread issues MMAs
 constexpr int kTcKt = 32;        // rows (K) per pipeline stage
 constexpr int kTcM = 128;        // M tile (rows of dW)
 
@@ -108,11 +108,56 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// Staging work item: (4 consecutive M/N indices q, one k-core c = 4 rows). The
+// thread loads 4 x float4 (rows r0+4c..+3, columns 4q..4q+3; coalesced across
+// threads), transposes in registers, splits hi/lo and writes 4 x 16 B core-matrix
+// rows (K-major). Loads for stage it+1 are issued before stage it's MMAs wait.
+struct TcItem {
+    float4 v[4];
+};
+
+__device__ __forceinline__ void tc_load(TcItem& it, const float* src, uint32_t stride, uint32_t col0,
+                                        uint32_t cols_valid, uint32_t row0, uint32_t rend) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const uint32_t row = row0 + e;
+        if (row < rend && col0 < cols_valid)
+            it.v[e] = *reinterpret_cast<const float4*>(src + size_t(row) * stride + col0);
+        else
+            it.v[e] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+}
+
+// Write the 4 (index) x 4 (k) block at core (c, q) of a K-major stage buffer.
+__device__ __forceinline__ void tc_store(const TcItem& it, uint8_t* hi, uint8_t* lo, uint32_t lbo, uint32_t c,
+                                         uint32_t q, uint32_t cols_valid, uint32_t col0, float* colsum) {
+    const float t[4][4] = {{it.v[0].x, it.v[0].y, it.v[0].z, it.v[0].w},
+                           {it.v[1].x, it.v[1].y, it.v[1].z, it.v[1].w},
+                           {it.v[2].x, it.v[2].y, it.v[2].z, it.v[2].w},
+                           {it.v[3].x, it.v[3].y, it.v[3].z, it.v[3].w}};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {  // index 4q+j; its 4 k values are t[0..3][j]
+        const uint32_t m = 4 * q + j;
+        float h[4], l[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const float x = (col0 + j < cols_valid) ? t[e][j] : 0.f;
+            if (colsum) colsum[j] += x;
+            h[e] = to_tf32(x);
+            l[e] = to_tf32(x - h[e]);
+        }
+        const uint32_t off = c * lbo + (m >> 3) * 128 + (m & 7) * 16;
+        *reinterpret_cast<float4*>(hi + off) = make_float4(h[0], h[1], h[2], h[3]);
+        *reinterpret_cast<float4*>(lo + off) = make_float4(l[0], l[1], l[2], l[3]);
+    }
+}
+
 // Dynamic shared memory: 2 stages x {A_hi, A_lo (128 x 32), B_hi, B_lo (npad x 32)} tf32.
 __global__ void __launch_bounds__(kTcThreads, 1) k_pgrad_tc(TcPgradParams p) {
     extern __shared__ __align__(1024) uint8_t tsm[];
     __shared__ __align__(8) uint64_t bars[3];
     __shared__ uint32_t tmem_base_sh;
+    __shared__ float bsum_sh[kTcThreads / 32][128];
     const int tid = threadIdx.x, warp = tid >> 5;
     const uint32_t split = blockIdx.x;
     const uint32_t i0 = blockIdx.y * kTcM;
@@ -123,6 +168,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_pgrad_tc(TcPgradParams p) {
     const uint32_t a_bytes = kTcM * kTcKt * 4, b_bytes = npad * kTcKt * 4;
     const uint32_t stage_bytes = 2 * a_bytes + 2 * b_bytes;
     const uint32_t a_lbo = (kTcM / 8) * 128, b_lbo = (npad / 8) * 128;
+    // work items: A has 32 q x 8 c = 256 (one per thread); B has npad/4 q x 8 c
+    const uint32_t a_q = tid & 31, a_c = tid >> 5;
+    const uint32_t b_items = (npad / 4) * (kTcKt / 4);
+    const bool has_b = uint32_t(tid) < b_items;
+    const uint32_t b_q = tid % (npad / 4), b_c = tid / (npad / 4);
+    const bool do_bias = p.wsb && blockIdx.y == 0;
 
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(&tmem_base_sh)));
@@ -140,56 +191,28 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_pgrad_tc(TcPgradParams p) {
     const uint32_t tmem = tmem_base_sh;
     const uint32_t idesc = umma_idesc_tf32(kTcM, npad);
 
-    float bsum = 0.f;
+    float bcol[4] = {0.f, 0.f, 0.f, 0.f};
     const uint32_t nst = (rend > rbeg) ? (rend - rbeg + kTcKt - 1) / kTcKt : 0;
+    TcItem ia, ib;
+    if (nst > 0) {
+        tc_load(ia, p.pre, p.prestride, i0 + 4 * a_q, p.din, rbeg + 4 * a_c, rend);
+        if (has_b) tc_load(ib, p.dz, p.dzstride, 4 * b_q, p.dout, rbeg + 4 * b_c, rend);
+    }
     uint32_t uses[2] = {0, 0};
     for (uint32_t it = 0; it < nst; ++it) {
         const uint32_t st = it & 1;
         if (uses[st] > 0) mbar_wait(&bars[st], (uses[st] - 1) & 1);  // MMAs that read this stage are done
         uint8_t* base = tsm + st * stage_bytes;
-        float* a_hi = reinterpret_cast<float*>(base);
-        float* a_lo = reinterpret_cast<float*>(base + a_bytes);
-        float* b_hi = reinterpret_cast<float*>(base + 2 * a_bytes);
-        float* b_lo = reinterpret_cast<float*>(base + 2 * a_bytes + b_bytes);
-        const uint32_t r0 = rbeg + it * kTcKt;
-        // A: thread m owns dW row i0+m; k-core c covers rows r0+4c..r0+4c+3
-        {
-            const uint32_t m = tid;
-            const bool mok = m < mvalid;
-#pragma unroll 2
-            for (uint32_t c = 0; c < kTcKt / 4; ++c) {
-                float hv[4], lv[4];
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const uint32_t row = r0 + 4 * c + e;
-                    const float x = (mok && row < rend) ? p.pre[size_t(row) * p.prestride + i0 + m] : 0.f;
-                    hv[e] = to_tf32(x);
-                    lv[e] = to_tf32(x - hv[e]);
-                }
-                const uint32_t off = c * a_lbo + (m >> 3) * 128 + (m & 7) * 16;
-                *reinterpret_cast<float4*>(reinterpret_cast<uint8_t*>(a_hi) + off) = make_float4(hv[0], hv[1], hv[2], hv[3]);
-                *reinterpret_cast<float4*>(reinterpret_cast<uint8_t*>(a_lo) + off) = make_float4(lv[0], lv[1], lv[2], lv[3]);
-            }
-        }
-        // B: thread n owns dW column n
-        if (uint32_t(tid) < npad) {
-            const uint32_t nn = tid;
-            const bool nok = nn < p.dout;
-#pragma unroll 2
-            for (uint32_t c = 0; c < kTcKt / 4; ++c) {
-                float hv[4], lv[4];
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const uint32_t row = r0 + 4 * c + e;
-                    const float x = (nok && row < rend) ? p.dz[size_t(row) * p.dzstride + nn] : 0.f;
-                    if (blockIdx.y == 0) bsum += x;
-                    hv[e] = to_tf32(x);
-                    lv[e] = to_tf32(x - hv[e]);
-                }
-                const uint32_t off = c * b_lbo + (nn >> 3) * 128 + (nn & 7) * 16;
-                *reinterpret_cast<float4*>(reinterpret_cast<uint8_t*>(b_hi) + off) = make_float4(hv[0], hv[1], hv[2], hv[3]);
-                *reinterpret_cast<float4*>(reinterpret_cast<uint8_t*>(b_lo) + off) = make_float4(lv[0], lv[1], lv[2], lv[3]);
-            }
+        uint8_t* a_hi = base;
+        uint8_t* a_lo = base + a_bytes;
+        uint8_t* b_hi = base + 2 * a_bytes;
+        uint8_t* b_lo = base + 2 * a_bytes + b_bytes;
+        tc_store(ia, a_hi, a_lo, a_lbo, a_c, a_q, i0 + mvalid, i0 + 4 * a_q, nullptr);
+        if (has_b) tc_store(ib, b_hi, b_lo, b_lbo, b_c, b_q, p.dout, 4 * b_q, do_bias ? bcol : nullptr);
+        if (it + 1 < nst) {  // prefetch the next stage while this one is multiplied
+            const uint32_t r1 = rbeg + (it + 1) * kTcKt;
+            tc_load(ia, p.pre, p.prestride, i0 + 4 * a_q, p.din, r1 + 4 * a_c, rend);
+            if (has_b) tc_load(ib, p.dz, p.dzstride, 4 * b_q, p.dout, r1 + 4 * b_c, rend);
         }
         // generic-proxy smem writes -> visible to the tensor-core (async) proxy
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -212,24 +235,39 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_pgrad_tc(TcPgradParams p) {
         }
         ++uses[st];
     }
-    // all MMAs done -> read the accumulator
+    // bias partials: thread (b_q, b_c) summed columns 4b_q..+3 over its rows; fold the 8 k-cores
+    if (do_bias) {
+        for (int i = tid; i < (kTcThreads / 32) * 128; i += kTcThreads) (&bsum_sh[0][0])[i] = 0.f;
+        __syncthreads();
+        if (has_b)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) atomicAdd(&bsum_sh[b_c][4 * b_q + j], bcol[j]);
+        __syncthreads();
+        if (uint32_t(tid) < p.dout) {
+            float sacc = 0.f;
+            for (int c = 0; c < kTcKt / 4; ++c) sacc += bsum_sh[c][tid];
+            p.wsb[size_t(split) * p.dout + tid] = sacc;
+        }
+    }
+    // all MMAs done -> read the accumulator (warps 0-3 own TMEM lanes 0-127)
     if (tid == 0) umma_commit(&bars[2]);
     if (nst > 0) mbar_wait(&bars[2], 0);
     asm volatile("tcgen05.fence::after_thread_sync;");
-    float* w = p.ws + size_t(split) * p.din * p.dout;
-    const uint32_t m = 32 * warp + (tid & 31);
-    for (uint32_t c0 = 0; c0 < npad; c0 += 16) {
-        float v[16];
-        tmem_ld16<16>(tmem + ((32u * warp) << 16) + c0, v);
-        if (m < mvalid) {
+    if (warp < 4) {
+        float* w = p.ws + size_t(split) * p.din * p.dout;
+        const uint32_t m = 32 * warp + (tid & 31);
+        for (uint32_t c0 = 0; c0 < npad; c0 += 16) {
+            float v[16];
+            tmem_ld16<16>(tmem + ((32u * warp) << 16) + c0, v);
+            if (m < mvalid) {
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                const uint32_t n = c0 + j;
-                if (n < p.dout) w[size_t(i0 + m) * p.dout + n] = nst > 0 ? v[j] : 0.f;
+                for (int j = 0; j < 16; ++j) {
+                    const uint32_t nn = c0 + j;
+                    if (nn < p.dout) w[size_t(i0 + m) * p.dout + nn] = nst > 0 ? v[j] : 0.f;
+                }
             }
         }
     }
-    if (p.wsb && blockIdx.y == 0 && uint32_t(tid) < p.dout) p.wsb[size_t(split) * p.dout + tid] = bsum;
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
