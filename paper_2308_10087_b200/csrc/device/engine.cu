@@ -368,7 +368,7 @@ struct Stage {
     }
 
     // Gathers in flight per lane (template NB of the row kernels); GP_NB overrides.
-    int nb = 4;
+    int nb = 2;
 
     // Row kernels stage a weight matrix (<= 66 KB) in shared memory; gathers bypass
     // L1 (no_allocate), so the unified L1/shared carveout goes to shared memory.
