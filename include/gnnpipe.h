@@ -79,6 +79,8 @@ typedef struct {
     uint32_t fix_alpha;          /* StalenessConfig (engines.hpp:28-33)         */
     uint32_t historical_gradients;
     uint32_t synchronous_mode;
+    uint32_t group_size;         /* G graph partitions per stage (0/1 = pure pipeline) */
+    uint32_t group_rank;         /* r: this worker owns Partition::inner_sets[r]      */
 } gp_stage_config;
 
 typedef struct gp_ctx gp_ctx;
@@ -138,6 +140,9 @@ gp_status gp_device_count(int* out);
  * device; neighbour order inside each row is preserved. */
 gp_status gp_upload_graph(gp_ctx* ctx, const uint64_t* offsets, const uint32_t* cols,
                           const float* vals, uint64_t nnz, const uint32_t* chunk_of);
+/* Hybrid (train_hybrid, engines_impl.hpp:515-909, G > 1): the vertex partition
+ * (Partition::assignment, partition.hpp:13-21). Call before gp_upload_graph. */
+gp_status gp_upload_partition(gp_ctx* ctx, const uint32_t* part_of);
 /* Reuse another stage's device graph (same device) instead of a second copy. */
 gp_status gp_share_graph(gp_ctx* ctx, const gp_ctx* owner);
 /* Dataset::features (dataset.hpp:17) N x F row-major; stage 0 only. */
@@ -159,6 +164,11 @@ gp_status gp_link_local(gp_ctx* upstream, gp_ctx* downstream);
  * 2-rank communicator (rank 0 = upstream stage). Pass NULL for a missing side. */
 gp_status gp_nccl_unique_id(uint8_t out[128]);
 gp_status gp_link_nccl(gp_ctx* ctx, const uint8_t* up_id, const uint8_t* down_id);
+/* Hybrid: join the G workers of one stage group (same process). Halo rows of each
+ * aggregating layer (exchange_rows, engines_impl.hpp:626-643) are pulled by the
+ * receiver from its peers' buffers after an event handshake; weight gradients
+ * are folded in rank order at rank 0 and broadcast (group_weight_sync :102-128). */
+gp_status gp_link_group(gp_ctx** members, uint32_t group_size);
 /* Abort a blocked local transport (error propagation across stage threads). */
 void gp_abort(gp_ctx* ctx);
 
@@ -242,6 +252,10 @@ int gs_init_params(const gs_model_config* m, uint32_t F, uint32_t C, uint64_t se
 int gs_train_pipeline(const gs_dataset* d, const uint32_t* chunk_of, uint32_t K, uint32_t S,
                       const gs_train_options* opt, gs_result** out);
 int gs_train_sequential(const gs_dataset* d, const gs_train_options* opt, gs_result** out);
+/* train_hybrid (engines.hpp:96-99): S stages x G graph partitions; part_of is
+ * Partition::assignment (G = max + 1), groups as assign_groups(S*G, 4, S, G). */
+int gs_train_hybrid(const gs_dataset* d, const uint32_t* part_of, const uint32_t* chunk_of, uint32_t K,
+                    uint32_t S, const gs_train_options* opt, gs_result** out);
 /* T x {epoch, train_loss, train_acc, val_acc, test_acc, wall_time_s, bubble_fraction} */
 int gs_result_metrics(const gs_result* r, uint32_t* epochs, double* metrics,
                       uint64_t* comm /* T x {graph, pipeline, weightsync} */);

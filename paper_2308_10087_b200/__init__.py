@@ -24,7 +24,7 @@ __all__ = [
     "GnnsimError", "InvalidArgument", "NumericError", "FabricError", "GpuEngineError",
     "LayerKind", "ModelKind", "ModelConfig", "TrainOptions", "TrainResult", "LayerSpec",
     "Dataset", "make_chunks", "partition_vertices", "shuffle_chunk_order", "make_stage_assignment",
-    "build_layer_specs", "init_params", "train_pipeline", "train_sequential", "StageEngine",
+    "build_layer_specs", "init_params", "train_pipeline", "train_sequential", "train_hybrid", "StageEngine",
     "nccl_unique_id", "device_count", "lib_paths", "PROFILE_CLASSES",
 ]
 
@@ -80,7 +80,8 @@ class gp_stage_config(C.Structure):
                 ("hidden", C.c_uint32), ("num_classes", C.c_uint32), ("dropout", C.c_double),
                 ("seed", C.c_uint64), ("optimizer", C.c_uint32), ("lr", C.c_double), ("beta1", C.c_double),
                 ("beta2", C.c_double), ("eps", C.c_double), ("fix_alpha", C.c_uint32),
-                ("historical_gradients", C.c_uint32), ("synchronous_mode", C.c_uint32)]
+                ("historical_gradients", C.c_uint32), ("synchronous_mode", C.c_uint32),
+                ("group_size", C.c_uint32), ("group_rank", C.c_uint32)]
 
 
 class gp_epoch_stats(C.Structure):
@@ -146,6 +147,9 @@ def _L():
         "gs_init_params": (C.c_int, [P(gs_model_config), C.c_uint32, C.c_uint32, C.c_uint64, f32p]),
         "gs_train_pipeline": (C.c_int, [vp, u32p, C.c_uint32, C.c_uint32, P(gs_train_options), P(vp)]),
         "gs_train_sequential": (C.c_int, [vp, P(gs_train_options), P(vp)]),
+        "gs_train_hybrid": (C.c_int, [vp, u32p, u32p, C.c_uint32, C.c_uint32, P(gs_train_options), P(vp)]),
+        "gp_upload_partition": (C.c_int, [vp, u32p]),
+        "gp_link_group": (C.c_int, [P(vp), C.c_uint32]),
         "gs_result_metrics": (C.c_int, [vp, u32p, f64p, u64p]),
         "gs_result_params": (C.c_int, [vp, f32p]),
         "gs_result_profile": (C.c_int, [vp, P(gp_profile)]),
@@ -445,6 +449,18 @@ def train_pipeline(ds: Dataset, chunk_of: np.ndarray, num_stages: int, opt: Trai
     K = int(co.max()) + 1 if co.size else 0
     h = C.c_void_p()
     _gs(_L().gs_train_pipeline(ds._h, _ptr(co, C.c_uint32), K, num_stages, C.byref(opt.c()), C.byref(h)))
+    return _result(h, build_layer_specs(opt.model, ds.num_features, ds.num_classes))
+
+
+def train_hybrid(ds: Dataset, part_of: np.ndarray, chunk_of: np.ndarray, num_stages: int,
+                 opt: TrainOptions) -> TrainResult:
+    """train_hybrid<float> (engines.hpp:96-99): S pipeline stages x G graph partitions."""
+    po = np.ascontiguousarray(part_of, np.uint32)
+    co = np.ascontiguousarray(chunk_of, np.uint32)
+    K = int(co.max()) + 1 if co.size else 0
+    h = C.c_void_p()
+    _gs(_L().gs_train_hybrid(ds._h, _ptr(po, C.c_uint32), _ptr(co, C.c_uint32), K, num_stages, C.byref(opt.c()),
+                             C.byref(h)))
     return _result(h, build_layer_specs(opt.model, ds.num_features, ds.num_classes))
 
 

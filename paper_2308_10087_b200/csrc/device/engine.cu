@@ -127,9 +127,30 @@ struct LocalLink {
     LocalQueue fwd, bwd;
 };
 
+// Hybrid group (G workers of one stage): one FIFO per (src, dst, kind).
+// kind 0 = forward halo, 1 = backward halo, 2 = weight-gradient sync.
+struct GroupLink {
+    uint32_t G = 1;
+    std::vector<Stage*> members;
+    std::vector<LocalQueue> q;  // (src * G + dst) * 3 + kind
+    explicit GroupLink(uint32_t g) : G(g), q(size_t(g) * g * 3) {}
+    LocalQueue& at(uint32_t src, uint32_t dst, uint32_t kind) { return q[(size_t(src) * G + dst) * 3 + kind]; }
+};
+
+// Host copy of the renumbered graph, shared by the contexts that share the
+// device graph (needed to derive each rank's halo lists).
+struct HostGraph {
+    std::vector<uint64_t> rp;       // renumbered row pointers
+    std::vector<uint32_t> col;      // renumbered columns
+    std::vector<uint32_t> part;     // new id -> partition
+    std::vector<uint32_t> chunk;    // new id -> chunk
+    std::vector<uint32_t> bstart;   // (G x (K+1)) block starts: rows of (rank r, chunk k)
+};
+
 struct Transport {
     // Forward: upstream stage sends chunk rows of its last layer (+h0).
     std::shared_ptr<LocalLink> up_local, down_local;  // links to s-1 and s+1
+    std::shared_ptr<GroupLink> group;                 // hybrid peers (same stage)
     void* up_comm = nullptr;                          // NCCL 2-rank comms
     void* down_comm = nullptr;
     cudaStream_t up_stream = nullptr, down_stream = nullptr;
@@ -169,9 +190,20 @@ struct Stage {
     uint32_t* orig = nullptr;          // new -> original id (device)
     std::vector<uint32_t> perm;        // original -> new (host)
     std::vector<uint32_t> inv;         // new -> original (host)
-    std::vector<uint32_t> cstart;      // chunk row ranges (host), K+1
     uint64_t nnz = 0;
     bool graph_ready = false;
+    // hybrid: vertices renumbered by (partition, chunk, id); block (r, k) contiguous
+    uint32_t G = 1, grank = 0;
+    std::vector<uint32_t> part_host;             // original id -> partition (before upload)
+    std::shared_ptr<HostGraph> hg;
+    std::vector<uint32_t> bstart;                // (G x (K+1))
+    uint32_t* pull_idx = nullptr;                // halo rows to pull, grouped by (peer, chunk)
+    std::vector<uint32_t> pull_off;              // (G x (K+1)) offsets into pull_idx
+    std::vector<uint64_t> push_cnt;              // (K x G) rows this rank pushes to each peer
+    uint32_t row_begin(uint32_t k) const { return bstart[size_t(grank) * (K + 1) + k]; }
+    uint32_t row_end(uint32_t k) const { return bstart[size_t(grank) * (K + 1) + k + 1]; }
+    uint32_t own_begin() const { return row_begin(0); }
+    uint32_t own_end() const { return row_begin(K); }
 
     // stage-level buffers
     float* x0 = nullptr;               // features (stage 0)
@@ -275,6 +307,9 @@ struct Stage {
         last = s + 1 == S;
         sync = c.synchronous_mode != 0;
         hist = c.historical_gradients != 0 && !sync;
+        G = c.group_size ? c.group_size : 1;
+        grank = c.group_rank;
+        if (G > 8 || grank >= G) throw Error(GP_EINVAL, "group_size must be in [1, 8] and group_rank < group_size");
         needs_h0 = false;
         for (const auto& sp : specs) {
             if (sp.kind == GP_SAGECONV)
@@ -436,33 +471,61 @@ struct Stage {
     }
 
     // ---- graph --------------------------------------------------------------
+    void upload_partition(const uint32_t* part_of) {
+        if (!part_of) throw Error(GP_EINVAL, "null partition");
+        if (graph_ready) throw Error(GP_EINVAL, "upload the partition before the graph");
+        part_host.assign(part_of, part_of + n);
+        for (uint32_t p : part_host)
+            if (p >= G) throw Error(GP_EINVAL, "partition id >= group_size");
+    }
+
+    // Vertex renumbering: (partition, chunk, original id) order, so that the rows
+    // of (rank r, chunk k) form the contiguous block [bstart(r,k), bstart(r,k+1)):
+    // stage messages (engines_impl.hpp:690-724) are slices, and a rank's own rows
+    // (Partition::inner_sets[r]) are one range. Row content keeps the original
+    // ascending neighbour order, so every reduction stays bit-exact.
     void upload_graph(const uint64_t* off, const uint32_t* cols, const float* vals, uint64_t nz,
                       const uint32_t* chunk_of) {
         GP_CUDA(cudaSetDevice(device));
         if (!off || !cols || !vals || !chunk_of) throw Error(GP_EINVAL, "null graph array");
         if (off[0] != 0 || off[n] != nz) throw Error(GP_EINVAL, "CSR offsets inconsistent with nnz");
-        // chunk-contiguous renumbering: chunk-major, ascending original id inside
-        std::vector<uint32_t> count(K + 1, 0);
+        if (G > 1 && part_host.size() != n) throw Error(GP_EINVAL, "hybrid: upload the partition first");
+        auto partof = [&](uint32_t v) -> uint32_t { return G > 1 ? part_host[v] : 0u; };
+        auto h = std::make_shared<HostGraph>();
+        const uint32_t KB = K + 1;
+        std::vector<uint32_t> count(size_t(G) * KB, 0);
         for (uint32_t v = 0; v < n; ++v) {
             if (chunk_of[v] >= K) throw Error(GP_EINVAL, "chunk id out of range");
-            ++count[chunk_of[v] + 1];
+            ++count[size_t(partof(v)) * KB + chunk_of[v]];
         }
-        cstart.assign(K + 1, 0);
-        for (uint32_t k = 0; k < K; ++k) cstart[k + 1] = cstart[k] + count[k + 1];
+        h->bstart.assign(size_t(G) * KB, 0);
+        uint32_t at = 0;
+        for (uint32_t r = 0; r < G; ++r)
+            for (uint32_t k = 0; k <= K; ++k) {
+                h->bstart[size_t(r) * KB + k] = at;
+                if (k < K) at += count[size_t(r) * KB + k];
+            }
         perm.assign(n, 0);
         inv.assign(n, 0);
-        std::vector<uint32_t> cur(cstart.begin(), cstart.end() - 1);
+        std::vector<uint32_t> cur(size_t(G) * KB);
+        for (uint32_t r = 0; r < G; ++r)
+            for (uint32_t k = 0; k < K; ++k) cur[size_t(r) * KB + k] = h->bstart[size_t(r) * KB + k];
         for (uint32_t v = 0; v < n; ++v) {
-            const uint32_t r = cur[chunk_of[v]]++;
+            const uint32_t r = cur[size_t(partof(v)) * KB + chunk_of[v]]++;
             perm[v] = r;
             inv[r] = v;
         }
-        std::vector<uint64_t> rp(size_t(n) + 1, 0);
+        h->rp.assign(size_t(n) + 1, 0);
+        h->part.assign(n, 0);
+        h->chunk.assign(n, 0);
         for (uint32_t r = 0; r < n; ++r) {
             const uint32_t v = inv[r];
             if (off[v + 1] < off[v]) throw Error(GP_EINVAL, "CSR offsets not monotone");
-            rp[r + 1] = rp[r] + (off[v + 1] - off[v]);
+            h->rp[r + 1] = h->rp[r] + (off[v + 1] - off[v]);
+            h->part[r] = partof(v);
+            h->chunk[r] = chunk_of[v];
         }
+        h->col.resize(nz);
         std::vector<uint2> e(nz);
         const unsigned nth = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
         std::vector<std::thread> pool;
@@ -471,7 +534,7 @@ struct Stage {
             pool.emplace_back([&, t]() {
                 for (uint32_t r = t; r < n; r += nth) {
                     const uint32_t v = inv[r];
-                    uint64_t w = rp[r];
+                    uint64_t w = h->rp[r];
                     for (uint64_t i = off[v]; i < off[v + 1]; ++i, ++w) {
                         const uint32_t u = cols[i];
                         if (u >= n) {
@@ -481,6 +544,7 @@ struct Stage {
                         uint32_t bits;
                         std::memcpy(&bits, &vals[i], 4);
                         e[w] = make_uint2(perm[u] | (chunk_of[u] << kColBits), bits);
+                        h->col[w] = perm[u];
                     }
                 }
             });
@@ -490,23 +554,61 @@ struct Stage {
         rowptr = dalloc<uint64_t>(size_t(n) + 1, false);
         edges = dalloc<uint2>(std::max<uint64_t>(nz, 1), false);
         orig = dalloc<uint32_t>(n, false);
-        GP_CUDA(cudaMemcpy(rowptr, rp.data(), rp.size() * 8, cudaMemcpyHostToDevice));
+        GP_CUDA(cudaMemcpy(rowptr, h->rp.data(), h->rp.size() * 8, cudaMemcpyHostToDevice));
         if (nz) GP_CUDA(cudaMemcpy(edges, e.data(), nz * 8, cudaMemcpyHostToDevice));
         GP_CUDA(cudaMemcpy(orig, inv.data(), size_t(n) * 4, cudaMemcpyHostToDevice));
+        hg = h;
+        if (G == 1) hg->col.clear();  // only hybrid needs the host columns
+        bstart = hg->bstart;
+        build_halo();
         graph_ready = true;
+    }
+
+    // Halo lists (chunk_push_sets, engines_impl.hpp:488-499): peer r2 pushes, in
+    // chunk k, its rows v (part r2, chunk k) that have a neighbour in my partition;
+    // I push mine likewise. Derived from the (symmetric) normalised adjacency.
+    void build_halo() {
+        pull_off.assign(size_t(G) * (K + 1), 0);
+        push_cnt.assign(size_t(K) * G, 0);
+        if (G == 1) return;
+        const HostGraph& h = *hg;
+        std::vector<std::vector<uint32_t>> lists(size_t(G) * K);
+        std::vector<uint32_t> seen(G, 0xffffffffu);
+        for (uint32_t v = 0; v < n; ++v) {
+            const uint32_t pv = h.part[v], kv = h.chunk[v];
+            for (uint64_t i = h.rp[v]; i < h.rp[v + 1]; ++i) {
+                const uint32_t pu = h.part[h.col[i]];
+                if (pu == pv || seen[pu] == v) continue;
+                seen[pu] = v;  // v is in B_pu (boundary of pu)
+                if (pu == grank) lists[size_t(pv) * K + kv].push_back(v);
+                if (pv == grank) ++push_cnt[size_t(kv) * G + pu];
+            }
+        }
+        std::vector<uint32_t> flat;
+        for (uint32_t r2 = 0; r2 < G; ++r2)
+            for (uint32_t k = 0; k < K; ++k) {
+                pull_off[size_t(r2) * (K + 1) + k] = uint32_t(flat.size());
+                auto& l = lists[size_t(r2) * K + k];
+                flat.insert(flat.end(), l.begin(), l.end());
+                pull_off[size_t(r2) * (K + 1) + k + 1] = uint32_t(flat.size());
+            }
+        pull_idx = dalloc<uint32_t>(std::max<size_t>(flat.size(), 1), false);
+        if (!flat.empty()) GP_CUDA(cudaMemcpy(pull_idx, flat.data(), flat.size() * 4, cudaMemcpyHostToDevice));
     }
 
     void share_graph(const Stage& o) {
         if (!o.graph_ready) throw Error(GP_EINVAL, "owner stage has no graph");
-        if (o.n != n || o.K != K || o.device != device)
-            throw Error(GP_EINVAL, "graph sharing needs the same N, K and device");
+        if (o.n != n || o.K != K || o.device != device || o.G != G)
+            throw Error(GP_EINVAL, "graph sharing needs the same N, K, G and device");
         rowptr = o.rowptr;
         edges = o.edges;
         orig = o.orig;
         perm = o.perm;
         inv = o.inv;
-        cstart = o.cstart;
+        hg = o.hg;
+        bstart = o.bstart;
         nnz = o.nnz;
+        build_halo();
         graph_ready = true;
     }
 
@@ -888,27 +990,30 @@ struct Stage {
         return p;
     }
 
+    // Parameter gradients over this rank's own rows (param_grads_for_rows over
+    // inner_sets[r], engines_impl.hpp:873-876), group sync (:877), optimizer (:878).
     void param_step() {
         ++step;  // Optimizer::step (nn.hpp:456-467): one update per epoch per stage
         const double c1d = 1.0 - std::pow(cfg.beta1, double(step));
         const double c2d = 1.0 - std::pow(cfg.beta2, double(step));
+        const uint32_t rb = own_begin(), re = own_end(), nown = re - rb;
         for (uint32_t i = 0; i < len; ++i) {
             auto& d = L[i];
             const uint32_t ti = (d.din + 127) / 128, tj = 1;
-            const double pg_bytes = double(n) * (d.din * tj + d.dout * ti) * 4.0 + double(splits) * d.din * d.dout * 4.0;
-            const double pg_flops = 2.0 * double(n) * d.din * d.dout;
+            const double pg_bytes = double(nown) * (d.din * tj + d.dout * ti) * 4.0 + double(splits) * d.din * d.dout * 4.0;
+            const double pg_flops = 2.0 * double(nown) * d.din * d.dout;
             uint32_t used_splits = splits;
             if (use_tc_pgrad) {
                 // tcgen05 (3xTF32) split-K GEMM, one CTA per SM (TMEM accumulator, ~120 KB smem)
                 used_splits = std::min<uint32_t>(splits, uint32_t(num_sms));
-                TcPgradParams tp{n, (n + used_splits - 1) / used_splits, d.pre, d.sin, d.dz, d.sout, d.din, d.dout,
-                                 (d.dout + 15) / 16 * 16, ws, d.gb ? wsb : nullptr};
+                TcPgradParams tp{re, (nown + used_splits - 1) / used_splits, rb, d.pre, d.sin, d.dz, d.sout, d.din,
+                                 d.dout, (d.dout + 15) / 16 * 16, ws, d.gb ? wsb : nullptr};
                 const size_t smem = 2 * (2 * size_t(kTcM) * kTcKt * 4 + 2 * size_t(tp.npad) * kTcKt * 4);
                 dim3 grid(used_splits, ti, 1);
                 launch(GP_K_PGRAD, pg_bytes, pg_flops, 0, [&]() { k_pgrad_tc<<<grid, kTcThreads, smem, cs>>>(tp); });
             } else {
-                const uint32_t rps = (n + splits - 1) / splits;
-                PgradParams pp{n, rps, d.pre, d.sin, d.dz, d.sout, d.din, d.dout, ws, d.gb ? wsb : nullptr};
+                const uint32_t rps = (nown + splits - 1) / splits;
+                PgradParams pp{re, rps, rb, d.pre, d.sin, d.dz, d.sout, d.din, d.dout, ws, d.gb ? wsb : nullptr};
                 dim3 grid(splits, ti, 1);
                 launch(GP_K_PGRAD, pg_bytes, pg_flops, 0, [&]() { k_pgrad_partial<<<grid, 256, 0, cs>>>(pp); });
             }
@@ -918,6 +1023,10 @@ struct Stage {
                 k_pgrad_fold<<<(tot + 255) / 256, 256, 0, cs>>>(ws, d.gb ? wsb : nullptr, used_splits, d.din, d.dout,
                                                                 float(d.spec.beta), gcn2, d.gW, d.gb);
             });
+        }
+        if (G > 1) group_sync_grads();
+        for (uint32_t i = 0; i < len; ++i) {
+            auto& d = L[i];
             AdamParams a{};
             a.sgd = cfg.optimizer == 1;
             a.lr = float(cfg.lr);
@@ -950,7 +1059,7 @@ struct Stage {
     uint64_t msgs_sent[6] = {0, 0, 0, 0, 0, 0};
 
     std::vector<Piece> fwd_pieces(uint32_t k, bool as_sender) {
-        const uint32_t r0 = cstart[k], rows = cstart[k + 1] - cstart[k];
+        const uint32_t r0 = row_begin(k), rows = row_end(k) - row_begin(k);
         std::vector<Piece> v;
         if (as_sender) {
             auto& d = L[len - 1];
@@ -963,7 +1072,7 @@ struct Stage {
         return v;
     }
     std::vector<Piece> bwd_pieces(uint32_t k, bool as_sender) {
-        const uint32_t r0 = cstart[k], rows = cstart[k + 1] - cstart[k];
+        const uint32_t r0 = row_begin(k), rows = row_end(k) - row_begin(k);
         std::vector<Piece> v;
         if (as_sender) {
             v.push_back({dh_in + size_t(r0) * sin0, size_t(rows) * sin0});
@@ -986,7 +1095,7 @@ struct Stage {
     }
 
     void account(int tag, uint32_t k, uint32_t width) {
-        const uint64_t rows = cstart[k + 1] - cstart[k];
+        const uint64_t rows = row_end(k) - row_begin(k);
         bytes_sent[tag] += rows * (uint64_t(width) + (needs_h0 ? H : 0)) * 4;  // 4 B/value (fabric.hpp:59)
         ++msgs_sent[tag];
     }
@@ -1078,6 +1187,127 @@ struct Stage {
         }
     }
 
+    // ---- hybrid group operations (G > 1) ----------------------------------------
+    // FIFO tags: (kind-specific id) so every pull checks it got the expected message.
+    static uint32_t halo_tag(uint32_t layer, uint32_t k) { return (layer << 8) | (k & 0xff); }
+
+    void group_post(uint32_t kind, uint32_t tag, std::vector<Piece> src) {
+        auto& gl = *tr.group;
+        cudaEvent_t ev = pool_event();
+        GP_CUDA(cudaEventRecord(ev, cs));
+        for (uint32_t r2 = 0; r2 < G; ++r2) {
+            if (r2 == grank) continue;
+            auto& q = gl.at(grank, r2, kind);
+            std::lock_guard<std::mutex> lk(q.mu);
+            if (q.aborted) throw Error(GP_EFABRIC, "transport aborted");
+            q.q.push_back({tag, ev, src, device});
+            q.cv.notify_all();
+        }
+    }
+
+    // Pull the halo rows of chunks [k_lo, k_hi) from every peer's buffer.
+    void halo_pull(uint32_t kind, uint32_t tag, uint32_t k_lo, uint32_t k_hi, float* dst, uint32_t stride,
+                   float* dstG, uint32_t gstride, uint32_t width, const DropKey& key) {
+        auto& gl = *tr.group;
+        for (uint32_t r2 = 0; r2 < G; ++r2) {
+            if (r2 == grank) continue;
+            LocalQueue::Msg m;
+            wait_local(gl.at(r2, grank, kind), tag, m);
+            GP_CUDA(cudaStreamWaitEvent(cs, m.ready, 0));
+            const uint32_t a = pull_off[size_t(r2) * (K + 1) + k_lo], b = pull_off[size_t(r2) * (K + 1) + k_hi];
+            if (b == a) continue;
+            PullParams p{pull_idx + a, b - a, m.src[0].ptr, dst, stride, dstG, gstride, width, orig, key};
+            launch(GP_K_XFER, double(b - a) * width * (dstG ? 12.0 : 8.0), 0, 0,
+                   [&]() { k_pull_rows<<<row_grid(b - a, (const void*)k_pull_rows, 0), kBlock, 0, cs>>>(p); });
+        }
+    }
+
+    // Ledger of one halo exchange (sender side, 4 B/value): rows this rank pushes.
+    void count_halo(int tag, uint32_t k_lo, uint32_t k_hi, uint32_t width) {
+        for (uint32_t r2 = 0; r2 < G; ++r2) {
+            if (r2 == grank) continue;
+            uint64_t rows = 0;
+            for (uint32_t k = k_lo; k < k_hi; ++k) rows += push_cnt[size_t(k) * G + r2];
+            bytes_sent[tag] += rows * width * 4;
+            if (rows) ++msgs_sent[tag];
+        }
+    }
+
+    // Forward halo of local layer i for chunks [k_lo, k_hi): before layer i reads
+    // neighbours, pull peers' current input rows (and their dropped copies).
+    void halo_fwd(uint32_t i, uint32_t k_lo, uint32_t k_hi, uint32_t t) {
+        auto& d = L[i];
+        count_halo(2, k_lo, k_hi, d.din);
+        if (i == 0 && first) return;  // stage-0 features are replicated: identical rows
+        float* cur = const_cast<float*>(cur_src(i));
+        const uint32_t tag = halo_tag(d.l, k_hi - k_lo == K ? 0xff : k_lo);
+        group_post(0, tag, {Piece{cur, 0}});
+        halo_pull(0, tag, k_lo, k_hi, cur, src_stride(i), d.G, d.sin, d.din, drop_key(t, d.l, d.din));
+    }
+
+    // Backward halo of local layer i: after backward_out_row wrote this layer's
+    // dagg rows, pull the peers' boundary rows before backward_prev_row reads them.
+    void halo_bwd(uint32_t i, uint32_t k_lo, uint32_t k_hi) {
+        auto& d = L[i];
+        count_halo(3, k_lo, k_hi, d.din);
+        if (d.l == 0) return;  // global layer 0 never propagates further (no dagg kept)
+        const uint32_t tag = halo_tag(d.l, k_hi - k_lo == K ? 0xff : k_lo);
+        group_post(1, tag, {Piece{d.bg, 0}});
+        halo_pull(1, tag, k_lo, k_hi, d.bg, d.sin, nullptr, 0, d.din, DropKey{});
+    }
+
+    // group_weight_sync: rank 0 folds in rank order and everyone takes its result.
+    void group_sync_grads() {
+        auto& gl = *tr.group;
+        std::vector<Piece> mine;
+        uint64_t values = 0;
+        for (auto& d : L) {
+            mine.push_back({d.gW, size_t(d.din) * d.dout});
+            values += uint64_t(d.din) * d.dout;
+            if (d.gb) {
+                mine.push_back({d.gb, d.dout});
+                values += d.dout;
+            }
+        }
+        if (grank != 0) {
+            cudaEvent_t ev = pool_event();
+            GP_CUDA(cudaEventRecord(ev, cs));
+            {
+                auto& q = gl.at(grank, 0, 2);
+                std::lock_guard<std::mutex> lk(q.mu);
+                if (q.aborted) throw Error(GP_EFABRIC, "transport aborted");
+                q.q.push_back({0u, ev, mine, device});
+                q.cv.notify_all();
+            }
+            bytes_sent[4] += values * 4;
+            ++msgs_sent[4];
+            LocalQueue::Msg m;
+            wait_local(gl.at(0, grank, 2), 1u, m);
+            GP_CUDA(cudaStreamWaitEvent(cs, m.ready, 0));
+            for (size_t j = 0; j < mine.size(); ++j)
+                GP_CUDA(cudaMemcpyAsync(mine[j].ptr, m.src[j].ptr, mine[j].floats * 4, cudaMemcpyDeviceToDevice, cs));
+            return;
+        }
+        std::vector<LocalQueue::Msg> peers(G);
+        for (uint32_t r2 = 1; r2 < G; ++r2) {
+            wait_local(gl.at(r2, 0, 2), 0u, peers[r2]);
+            GP_CUDA(cudaStreamWaitEvent(cs, peers[r2].ready, 0));
+        }
+        for (size_t j = 0; j < mine.size(); ++j) {
+            FoldParams f{};
+            f.src[0] = mine[j].ptr;
+            for (uint32_t r2 = 1; r2 < G; ++r2) f.src[r2] = peers[r2].src[j].ptr;
+            f.dst = mine[j].ptr;
+            f.G = G;
+            f.n = uint32_t(mine[j].floats);
+            launch(GP_K_XFER, double(f.n) * 4.0 * (G + 1), 0, 0,
+                   [&]() { k_group_fold<<<(f.n + 255) / 256, 256, 0, cs>>>(f); });
+        }
+        group_post(2, 1u, mine);
+        bytes_sent[4] += uint64_t(G - 1) * values * 4;
+        msgs_sent[4] += G - 1;
+    }
+
     // ---- one epoch ---------------------------------------------------------------
     void run_epoch(uint32_t t, const uint32_t* order, gp_epoch_stats* out) {
         GP_CUDA(cudaSetDevice(device));
@@ -1123,28 +1353,34 @@ struct Stage {
         if (!sync) {
             for (uint32_t kk = 0; kk < K; ++kk) {
                 const uint32_t k = ord[kk];
-                const uint32_t r0 = cstart[k], r1 = cstart[k + 1];
+                const uint32_t r0 = row_begin(k), r1 = row_end(k);
                 if (!first) {
                     recv_fwd(k);
                     if (L[0].agg) remask(0, in_cur, r0, r1, drop_key(t, L[0].l, L[0].din));
                 }
-                for (uint32_t i = 0; i < len; ++i) forward_layer(i, r0, r1, t);
+                for (uint32_t i = 0; i < len; ++i) {
+                    if (G > 1 && L[i].agg) halo_fwd(i, k, k + 1, t);  // exchange_rows (:792-794)
+                    forward_layer(i, r0, r1, t);
+                }
                 if (!last) send_fwd(k);
             }
         } else {
             if (!first) {
                 for (uint32_t kk = 0; kk < K; ++kk) recv_fwd(ord[kk]);
-                if (L[0].agg) remask(0, in_cur, 0, n, drop_key(t, L[0].l, L[0].din));
+                if (L[0].agg) remask(0, in_cur, own_begin(), own_end(), drop_key(t, L[0].l, L[0].din));
             }
-            for (uint32_t i = 0; i < len; ++i) forward_layer(i, 0, n, t);
+            for (uint32_t i = 0; i < len; ++i) {
+                if (G > 1 && L[i].agg) halo_fwd(i, 0, K, t);  // exchange_rows_full (:806-808)
+                forward_layer(i, own_begin(), own_end(), t);
+            }
             if (!last)
                 for (uint32_t kk = 0; kk < K; ++kk) send_fwd(ord[kk]);
         }
 
         // ---- metrics (last stage) ---------------------------------------------------
         if (last) {
-            XentParams p = xent_params(0, n);
-            launch(GP_K_XENT, double(n) * L[len - 1].dout * 4.0, 0, 0,
+            XentParams p = xent_params(own_begin(), own_end());
+            launch(GP_K_XENT, double(own_end() - own_begin()) * L[len - 1].dout * 4.0, 0, 0,
                    [&]() { k_xent_stats<<<xent_blocks, kBlock, 0, cs>>>(p); });
             launch(GP_K_XENT, 0, 0, 0, [&]() {
                 k_xent_fold<<<1, 32, 0, cs>>>(part_loss, part_correct, xent_blocks, red_loss, red_correct);
@@ -1157,7 +1393,7 @@ struct Stage {
             uint64_t done = 0;
             for (uint32_t kk = K; kk-- > 0;) {
                 const uint32_t k = ord[kk];
-                const uint32_t r0 = cstart[k], r1 = cstart[k + 1];
+                const uint32_t r0 = row_begin(k), r1 = row_end(k);
                 done |= 1ull << k;
                 if (last) {
                     XentParams p = xent_params(r0, r1);
@@ -1166,7 +1402,11 @@ struct Stage {
                 } else {
                     recv_bwd(k);
                 }
-                for (uint32_t i = len; i-- > 0;) backward_layer(i, r0, r1, t, done);
+                for (uint32_t i = len; i-- > 0;) {
+                    if (G > 1 && i + 1 < len && L[i + 1].agg) halo_bwd(i + 1, k, k + 1);  // (:838-844)
+                    backward_layer(i, r0, r1, t, done);
+                }
+                if (G > 1 && L[0].agg) halo_bwd(0, k, k + 1);
                 if (!first) {
                     backward_dhin(r0, r1, t, done);
                     send_bwd(k);
@@ -1174,16 +1414,21 @@ struct Stage {
             }
         } else {
             const uint64_t done = K == 64 ? ~0ull : ((1ull << K) - 1);
+            const uint32_t ob = own_begin(), oe = own_end();
             if (last) {
-                XentParams p = xent_params(0, n);
-                launch(GP_K_XENT, double(n) * L[len - 1].dout * 8.0, 0, 0,
-                       [&]() { k_xent_grad<<<row_grid(n, (const void*)k_xent_grad, 0), kBlock, 0, cs>>>(p); });
+                XentParams p = xent_params(ob, oe);
+                launch(GP_K_XENT, double(oe - ob) * L[len - 1].dout * 8.0, 0, 0,
+                       [&]() { k_xent_grad<<<row_grid(oe - ob, (const void*)k_xent_grad, 0), kBlock, 0, cs>>>(p); });
             } else {
                 for (uint32_t kk = K; kk-- > 0;) recv_bwd(ord[kk]);
             }
-            for (uint32_t i = len; i-- > 0;) backward_layer(i, 0, n, t, done);
+            for (uint32_t i = len; i-- > 0;) {
+                if (G > 1 && i + 1 < len && L[i + 1].agg) halo_bwd(i + 1, 0, K);
+                backward_layer(i, ob, oe, t, done);
+            }
+            if (G > 1 && L[0].agg) halo_bwd(0, 0, K);
             if (!first) {
-                backward_dhin(0, n, t, done);
+                backward_dhin(ob, oe, t, done);
                 for (uint32_t kk = K; kk-- > 0;) send_bwd(ord[kk]);
             }
         }
@@ -1325,6 +1570,27 @@ gp_status gp_upload_graph(gp_ctx* ctx, const uint64_t* offsets, const uint32_t* 
     return gp::guard(&ctx->st, [&]() { ctx->st.upload_graph(offsets, cols, vals, nnz, chunk_of); });
 }
 
+gp_status gp_upload_partition(gp_ctx* ctx, const uint32_t* part_of) {
+    return gp::guard(&ctx->st, [&]() { ctx->st.upload_partition(part_of); });
+}
+
+gp_status gp_link_group(gp_ctx** members, uint32_t G) {
+    if (!members || G == 0) {
+        gp::g_tls_error = "gp_link_group: no members";
+        return GP_EINVAL;
+    }
+    return gp::guard(&members[0]->st, [&]() {
+        auto link = std::make_shared<gp::GroupLink>(G);
+        for (uint32_t r = 0; r < G; ++r) {
+            auto& st = members[r]->st;
+            if (st.G != G || st.grank != r) throw gp::Error(GP_EINVAL, "gp_link_group: member order must be rank order");
+            if (st.s != members[0]->st.s) throw gp::Error(GP_EINVAL, "gp_link_group: members must share a stage");
+            link->members.push_back(&st);
+        }
+        for (uint32_t r = 0; r < G; ++r) members[r]->st.tr.group = link;
+    });
+}
+
 gp_status gp_share_graph(gp_ctx* ctx, const gp_ctx* owner) {
     return gp::guard(&ctx->st, [&]() { ctx->st.share_graph(owner->st); });
 }
@@ -1410,6 +1676,12 @@ void gp_abort(gp_ctx* ctx) {
     if (!ctx) return;
     auto& st = ctx->st;
     st.aborted = true;
+    if (st.tr.group)
+        for (auto& q : st.tr.group->q) {
+            std::lock_guard<std::mutex> lk(q.mu);
+            q.aborted = true;
+            q.cv.notify_all();
+        }
     for (auto* l : {st.tr.up_local.get(), st.tr.down_local.get()}) {
         if (!l) continue;
         for (auto* q : {&l->fwd, &l->bwd}) {

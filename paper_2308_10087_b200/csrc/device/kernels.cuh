@@ -535,7 +535,8 @@ __global__ void __launch_bounds__(kBlock) k_xent_grad(XentParams p) {
 // CTA tile: 64 (k_in) x 64 (out); thread: 4 x 4; rows staged 32 at a time.
 // ---------------------------------------------------------------------------
 struct PgradParams {
-    uint32_t n, rows_per_split;
+    uint32_t n, rows_per_split;  // n = end row (exclusive); rows start at row0
+    uint32_t row0;
     const float* pre;
     uint32_t prestride;
     const float* dz;
@@ -555,7 +556,7 @@ __global__ void __launch_bounds__(256, 2) k_pgrad_partial(PgradParams p) {
     __shared__ __align__(16) float Ds[2][kPgRows][128];
     const uint32_t split = blockIdx.x;
     const uint32_t i0 = blockIdx.y * 128;
-    const uint32_t rbeg = split * p.rows_per_split;
+    const uint32_t rbeg = p.row0 + split * p.rows_per_split;
     const uint32_t rend = min(p.n, rbeg + p.rows_per_split);
     const int tid = threadIdx.x;
     const int ti = tid / 16, tj = tid % 16;
@@ -681,6 +682,58 @@ __global__ void k_adam(AdamParams a) {
         const float mhat = __fdiv_rn(m, a.c1);
         const float vhat = __fdiv_rn(v, a.c2);
         a.p[i] = __fsub_rn(a.p[i], __fdiv_rn(__fmul_rn(a.lr, mhat), __fadd_rn(__fsqrt_rn(vhat), a.eps)));
+    }
+}
+
+}  // namespace gp
+
+namespace gp {
+
+// ---------------------------------------------------------------------------
+// Hybrid halo pull (exchange_rows / unpack_rows, engines_impl.hpp:626-643,
+// :62-70): copy the listed rows of a peer's buffer into ours; for the forward
+// also write the dropped copy into this layer's gather table.
+// ---------------------------------------------------------------------------
+struct PullParams {
+    const uint32_t* rows;
+    uint32_t count;
+    const float* src;
+    float* dst;
+    uint32_t stride;
+    float* dstG;
+    uint32_t gstride;
+    uint32_t width;
+    const uint32_t* orig;
+    DropKey mask;
+};
+
+__global__ void __launch_bounds__(kBlock) k_pull_rows(PullParams p) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t nw = gridDim.x * kWarpsPerBlock;
+    for (uint32_t i = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5); i < p.count; i += nw) {
+        const uint32_t v = p.rows[i];
+        for (uint32_t c0 = 4 * lane; c0 < p.width; c0 += 128) {
+            const float4 x = ld4_rw(p.src + size_t(v) * p.stride + c0);
+            st4(p.dst + size_t(v) * p.stride + c0, x);
+            if (p.dstG) st4(p.dstG + size_t(v) * p.gstride + c0, drop4(p.mask, p.orig[v], c0, p.width, x));
+        }
+    }
+}
+
+// group_weight_sync (engines_impl.hpp:102-128): rank 0 folds the group's
+// gradients in rank order, g = ((g0 + g1) + g2) + ..., one rounding per add.
+struct FoldParams {
+    const float* src[8];
+    float* dst;
+    uint32_t G;
+    uint32_t n;
+};
+
+__global__ void k_group_fold(FoldParams p) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < p.n; i += gridDim.x * blockDim.x) {
+        float s = p.src[0][i];
+        for (uint32_t r = 1; r < p.G; ++r) s = __fadd_rn(s, p.src[r][i]);
+        p.dst[i] = s;
     }
 }
 

@@ -29,7 +29,8 @@ constexpr int kTcKt = 32;        // rows (K) per pipeline stage
 constexpr int kTcM = 128;        // M tile (rows of dW)
 
 struct TcPgradParams {
-    uint32_t n, rows_per_split;
+    uint32_t n, rows_per_split;  // n = end row (exclusive); rows start at row0
+    uint32_t row0;
     const float* pre;
     uint32_t prestride;
     const float* dz;
@@ -162,7 +163,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_pgrad_tc(TcPgradParams p) {
     const uint32_t split = blockIdx.x;
     const uint32_t i0 = blockIdx.y * kTcM;
     const uint32_t mvalid = min(uint32_t(kTcM), p.din - i0);
-    const uint32_t rbeg = split * p.rows_per_split;
+    const uint32_t rbeg = p.row0 + split * p.rows_per_split;
     const uint32_t rend = min(p.n, rbeg + p.rows_per_split);
     const uint32_t npad = p.npad;
     const uint32_t a_bytes = kTcM * kTcKt * 4, b_bytes = npad * kTcKt * 4;

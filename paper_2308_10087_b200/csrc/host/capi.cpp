@@ -245,6 +245,23 @@ int gs_train_pipeline(const gs_dataset* d, const uint32_t* chunk_of, uint32_t K,
     });
 }
 
+int gs_train_hybrid(const gs_dataset* d, const uint32_t* part_of, const uint32_t* chunk_of, uint32_t K, uint32_t S,
+                    const gs_train_options* o, gs_result** out) {
+    return guarded([&]() {
+        TrainOptions<float> opt = options_of(o);
+        const VertexId n = d->d.num_vertices();
+        const uint32_t L = uint32_t(build_layer_specs(opt.model, d->d.num_features(), d->d.num_classes).size());
+        Partition part = partition_from_assignment(d->d.graph, std::vector<uint32_t>(part_of, part_of + n));
+        ChunkPlan plan = chunk_plan_from_assignment(n, std::vector<uint32_t>(chunk_of, chunk_of + n));
+        if (plan.num_chunks != K) throw std::invalid_argument("chunk_of does not use exactly K chunks");
+        const uint32_t G = part.num_parts;
+        GroupMap gmap = assign_groups(S * G, 4, S, G);
+        auto own = std::make_unique<gs_result>();
+        own->r = train_hybrid<float>(d->d, part, plan, make_stage_assignment(L, S), gmap, opt);
+        *out = own.release();
+    });
+}
+
 int gs_train_sequential(const gs_dataset* d, const gs_train_options* o, gs_result** out) {
     return guarded([&]() {
         auto own = std::make_unique<gs_result>();

@@ -99,13 +99,18 @@ void validate_run(const Dataset& ds, const ChunkPlan& plan, const StageAssignmen
 
 namespace {
 
-TrainResult<float> run_pipeline_f32(const Dataset& ds, const ChunkPlan& plan, const StageAssignment& sa,
-                                    const TrainOptions<float>& opt) {
+// The worker body of train_hybrid (engines_impl.hpp:515-909) for S stages x G
+// graph partitions: worker (s, r) is one gp_ctx; `part` is null for G = 1.
+// `worker_id[s*G + r]` is the fabric worker id (GroupMap::groups[s][r]) and
+// node_of is indexed by it (link classes of the ledger).
+TrainResult<float> run_hybrid_f32(const Dataset& ds, const Partition* part, const ChunkPlan& plan,
+                                  const StageAssignment& sa, uint32_t G, const std::vector<uint32_t>& worker_id,
+                                  std::vector<uint32_t> node_of, const TrainOptions<float>& opt) {
     ds.validate();
     const auto specs = build_layer_specs(opt.model, ds.num_features(), ds.num_classes);
     const uint32_t L = uint32_t(specs.size());
     validate_run(ds, plan, sa, L);
-    const uint32_t S = sa.num_stages, K = plan.num_chunks;
+    const uint32_t S = sa.num_stages, K = plan.num_chunks, W = S * G;
     const VertexId n = ds.num_vertices();
     uint64_t split_count[3] = {0, 0, 0};
     for (uint8_t s : ds.split)
@@ -125,9 +130,10 @@ TrainResult<float> run_pipeline_f32(const Dataset& ds, const ChunkPlan& plan, co
     if (ndev == 0) throw GpError(GP_ECUDA, "train_pipeline: no CUDA device (the GPU engine has no CPU fallback)");
 
     Ctxs ctx;
-    for (uint32_t s = 0; s < S; ++s) {
+    for (uint32_t w = 0; w < W; ++w) {
+        const uint32_t s = w / G, r = w % G;
         gp_stage_config c{};
-        c.device = opt.device >= 0 ? opt.device : int(s % uint32_t(ndev));
+        c.device = opt.device >= 0 ? opt.device : int(w % uint32_t(ndev));
         c.num_vertices = n;
         c.num_chunks = K;
         c.num_stages = S;
@@ -148,10 +154,14 @@ TrainResult<float> run_pipeline_f32(const Dataset& ds, const ChunkPlan& plan, co
         c.fix_alpha = opt.staleness.fix_alpha;
         c.historical_gradients = opt.staleness.historical_gradients ? 1u : 0u;
         c.synchronous_mode = opt.staleness.synchronous_mode ? 1u : 0u;
+        c.group_size = G;
+        c.group_rank = r;
         gp_ctx* g = nullptr;
         check(gp_create(&c, &g), nullptr, "gp_create");
         ctx.v.push_back(g);
-        if (s == 0 || c.device != (opt.device >= 0 ? opt.device : 0)) {
+        if (G > 1) check(gp_upload_partition(g, part->assignment.data()), g, "gp_upload_partition");
+        const int dev0 = opt.device >= 0 ? opt.device : 0;
+        if (w == 0 || c.device != dev0) {
             check(gp_upload_graph(g, adj.offsets.data(), adj.cols.data(), adj.vals.data(), adj.cols.size(),
                                   plan.chunk_of.data()),
                   g, "gp_upload_graph");
@@ -164,104 +174,114 @@ TrainResult<float> run_pipeline_f32(const Dataset& ds, const ChunkPlan& plan, co
             check(gp_set_layer_params(g, l, params[l].weight.data(), params[l].bias.empty() ? nullptr : params[l].bias.data()),
                   g, "gp_set_layer_params");
         if (opt.profile) gp_set_profiling(g, 1);
-        if (s > 0) check(gp_link_local(ctx.v[s - 1], g), g, "gp_link_local");
+        if (s > 0) check(gp_link_local(ctx.v[w - G], g), g, "gp_link_local");  // same rank, previous stage
     }
+    if (G > 1)
+        for (uint32_t s = 0; s < S; ++s)
+            check(gp_link_group(&ctx.v[size_t(s) * G], G), ctx.v[size_t(s) * G], "gp_link_group");
 
     const uint32_t T = opt.epochs;
-    std::vector<std::vector<gp_epoch_stats>> stats(S, std::vector<gp_epoch_stats>(T));
-    std::vector<std::exception_ptr> errs(S);
-    StageBarrier barrier(S);
-    auto body = [&](uint32_t s) {
+    std::vector<std::vector<gp_epoch_stats>> stats(W, std::vector<gp_epoch_stats>(T));
+    std::vector<std::exception_ptr> errs(W);
+    StageBarrier barrier(W);
+    auto body = [&](uint32_t w) {
         try {
             for (uint32_t t = 1; t <= T; ++t) {
                 if (!barrier.arrive_and_wait()) return;  // epoch entry sync (engines_impl.hpp:668)
                 std::vector<uint32_t> order(K);
                 for (uint32_t k = 0; k < K; ++k) order[k] = k;
                 if (opt.staleness.shuffle_chunks) order = shuffle_chunk_order(plan, t, opt.seed);
-                check(gp_run_epoch(ctx.v[s], t, order.data(), &stats[s][t - 1]), ctx.v[s], "gp_run_epoch");
-                if (s + 1 == S) {
-                    const double loss = stats[s][t - 1].loss_sum / double(split_count[0]);
-                    if (!std::isfinite(loss))
-                        throw NumericError("non-finite training loss at epoch " + std::to_string(t));
-                }
+                check(gp_run_epoch(ctx.v[w], t, order.data(), &stats[w][t - 1]), ctx.v[w], "gp_run_epoch");
             }
         } catch (...) {
-            errs[s] = std::current_exception();
+            errs[w] = std::current_exception();
             barrier.abort();
             for (auto* c : ctx.v) gp_abort(c);
         }
     };
-    if (S == 1) {
+    if (W == 1) {
         body(0);
     } else {
         std::vector<std::thread> pool;
-        for (uint32_t s = 0; s < S; ++s) pool.emplace_back(body, s);
+        for (uint32_t w = 0; w < W; ++w) pool.emplace_back(body, w);
         for (auto& th : pool) th.join();
     }
     // Prefer the root cause over "transport aborted" follow-on errors.
     for (uint32_t pass = 0; pass < 2; ++pass)
-        for (uint32_t s = 0; s < S; ++s) {
-            if (!errs[s]) continue;
+        for (uint32_t w = 0; w < W; ++w) {
+            if (!errs[w]) continue;
             if (pass == 0) {
                 try {
-                    std::rethrow_exception(errs[s]);
+                    std::rethrow_exception(errs[w]);
                 } catch (const FabricError& e) {
                     if (std::string(e.what()).find("aborted") != std::string::npos) continue;
                     throw;
                 }
             }
-            std::rethrow_exception(errs[s]);
+            std::rethrow_exception(errs[w]);
         }
 
     TrainResult<float> res;
-    std::vector<uint32_t> node_of = opt.fabric.node_of;
     if (node_of.empty())
-        for (uint32_t w = 0; w < S; ++w) node_of.push_back(w / 4);  // assign_groups(S, 4, S, 1)
+        for (uint32_t w = 0; w < W; ++w) node_of.push_back(w / 4);
+    auto node = [&](uint32_t s, uint32_t r) { return node_of[worker_id[size_t(s) * G + r]]; };
     res.metrics.resize(T);
     res.comm.resize(T);
     for (uint32_t t = 0; t < T; ++t) {
         EpochMetrics& m = res.metrics[t];
-        const gp_epoch_stats& q = stats[S - 1][t];
         m.epoch = t + 1;
-        m.train_loss = split_count[0] ? q.loss_sum / double(split_count[0]) : 0.0;  // :164-171
-        m.train_acc = split_count[0] ? double(q.correct[0]) / double(split_count[0]) : 0.0;
-        m.val_acc = split_count[1] ? double(q.correct[1]) / double(split_count[1]) : 0.0;
-        m.test_acc = split_count[2] ? double(q.correct[2]) / double(split_count[2]) : 0.0;
+        // reduce_metrics (engines_impl.hpp:131-151): group rank 0 adds ranks in order
+        double loss = 0;
+        uint64_t cor[3] = {0, 0, 0};
+        for (uint32_t r = 0; r < G; ++r) {
+            const gp_epoch_stats& q = stats[size_t(S - 1) * G + r][t];
+            loss += q.loss_sum;
+            for (int i = 0; i < 3; ++i) cor[i] += q.correct[i];
+        }
+        m.train_loss = split_count[0] ? loss / double(split_count[0]) : 0.0;  // :164-171
+        if (!std::isfinite(m.train_loss)) throw NumericError("non-finite training loss at epoch " + std::to_string(t + 1));
+        m.train_acc = split_count[0] ? double(cor[0]) / double(split_count[0]) : 0.0;
+        m.val_acc = split_count[1] ? double(cor[1]) / double(split_count[1]) : 0.0;
+        m.test_acc = split_count[2] ? double(cor[2]) / double(split_count[2]) : 0.0;
         EpochComm& e = res.comm[t];
         double span = 0, busy = 0;
-        for (uint32_t s = 0; s < S; ++s) {
-            const auto& st = stats[s][t];
+        for (uint32_t w = 0; w < W; ++w) {
+            const uint32_t s = w / G, r = w % G;
+            const auto& st = stats[w][t];
             span = std::max(span, double(st.epoch_ms));
             busy += st.busy_ms;
-            // forward goes s -> s+1, backward s -> s-1
-            if (s + 1 < S) e.by_tag_link[0][node_of[s] == node_of[s + 1] ? 0 : 1] += st.bytes_sent[0];
-            if (s > 0) e.by_tag_link[1][node_of[s] == node_of[s - 1] ? 0 : 1] += st.bytes_sent[1];
+            // forward goes (s,r) -> (s+1,r), backward (s,r) -> (s-1,r)
+            if (s + 1 < S) e.by_tag_link[0][node(s, r) == node(s + 1, r) ? 0 : 1] += st.bytes_sent[0];
+            if (s > 0) e.by_tag_link[1][node(s, r) == node(s - 1, r) ? 0 : 1] += st.bytes_sent[1];
+            // halo and weight sync stay inside the stage group; one NVSwitch node here
+            for (int tag = 2; tag <= 4; ++tag) e.by_tag_link[tag][node(s, r) == node(s, 0) ? 0 : 1] += st.bytes_sent[tag];
         }
         m.comm_bytes_graph = e.graph_bytes();
         m.comm_bytes_pipeline = e.pipeline_bytes();
         m.comm_bytes_weightsync = e.weight_sync_bytes();
         m.wall_time_s = span / 1000.0;
-        m.bubble_fraction = (opt.profile && span > 0) ? std::max(0.0, 1.0 - busy / (span * S)) : 0.0;
+        m.bubble_fraction = (opt.profile && span > 0) ? std::max(0.0, 1.0 - busy / (span * W)) : 0.0;
     }
-    for (uint32_t s = 0; s < S; ++s) {
-        WorkerParams<float> wp;
+    res.worker_params.resize(W);
+    for (uint32_t w = 0; w < W; ++w) {
+        const uint32_t s = w / G;
+        WorkerParams<float>& wp = res.worker_params[worker_id[w]];
         wp.layer_begin = sa.begin(s);
         wp.layer_end = sa.end(s);
         for (uint32_t l = sa.begin(s); l < sa.end(s); ++l) {
             LayerParams<float> p;
             p.weight = MatF(specs[l].k_in(), specs[l].out_dim);
             if (specs[l].has_bias()) p.bias.assign(specs[l].out_dim, 0.f);
-            check(gp_get_layer_params(ctx.v[s], l, p.weight.data(), p.bias.empty() ? nullptr : p.bias.data()),
-                  ctx.v[s], "gp_get_layer_params");
-            res.params.push_back(p);
+            check(gp_get_layer_params(ctx.v[w], l, p.weight.data(), p.bias.empty() ? nullptr : p.bias.data()),
+                  ctx.v[w], "gp_get_layer_params");
+            if (w % G == 0) res.params.push_back(p);  // each group's rank 0 (:901-905)
             wp.params.push_back(std::move(p));
         }
-        res.worker_params.push_back(std::move(wp));
         uint64_t bytes = 0;
-        gp_device_bytes(ctx.v[s], &bytes);
+        gp_device_bytes(ctx.v[w], &bytes);
         res.peak_buffer_bytes = std::max(res.peak_buffer_bytes, bytes);
         gp_profile pr{};
-        gp_get_profile(ctx.v[s], &pr);
+        gp_get_profile(ctx.v[w], &pr);
         for (int k = 0; k < GP_K_NUM; ++k) {
             res.profile.ms[k] += pr.ms[k];
             res.profile.launches[k] += pr.launches[k];
@@ -271,6 +291,13 @@ TrainResult<float> run_pipeline_f32(const Dataset& ds, const ChunkPlan& plan, co
         }
     }
     return res;
+}
+
+TrainResult<float> run_pipeline_f32(const Dataset& ds, const ChunkPlan& plan, const StageAssignment& sa,
+                                    const TrainOptions<float>& opt) {
+    std::vector<uint32_t> ids(sa.num_stages);
+    for (uint32_t s = 0; s < sa.num_stages; ++s) ids[s] = s;  // assign_groups(S, 4, S, 1)
+    return run_hybrid_f32(ds, nullptr, plan, sa, 1, ids, opt.fabric.node_of, opt);
 }
 
 }  // namespace
@@ -302,12 +329,13 @@ TrainResult<T> train_hybrid(const Dataset& ds, const Partition& part, const Chun
     if (part.num_parts != G) throw std::invalid_argument("train_hybrid: partition parts != group size");
     if (plan.chunk_of.size() != ds.num_vertices() || part.assignment.size() != ds.num_vertices())
         throw std::invalid_argument("train_hybrid: plan/partition do not cover the graph");
-    if (G != 1)
-        throw std::invalid_argument(
-            "train_hybrid: graph-parallel groups (G > 1) are not implemented by the GPU engine yet");
-    TrainOptions<T> o = opt;
-    if (o.fabric.node_of.empty()) o.fabric.node_of = gmap.node_of;
-    return train_pipeline<T>(ds, plan, sa, o);
+    if (G > 8) throw std::invalid_argument("train_hybrid: group size must be <= 8");
+    static_assert(std::is_same_v<T, float>, "the GPU engine computes in fp32");
+    std::vector<uint32_t> ids(size_t(S) * G);
+    for (uint32_t s = 0; s < S; ++s)
+        for (uint32_t r = 0; r < G; ++r) ids[size_t(s) * G + r] = gmap.groups[s][r];
+    return run_hybrid_f32(ds, G > 1 ? &part : nullptr, plan, sa, G, ids,
+                          opt.fabric.node_of.empty() ? gmap.node_of : opt.fabric.node_of, opt);
 }
 
 template TrainResult<float> train_sequential<float>(const Dataset&, const TrainOptions<float>&);

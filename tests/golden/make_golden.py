@@ -38,6 +38,14 @@ SCENARIOS = {
                                        epochs=10, seed=43, fix_alpha=3)),
     "train_gcnii_s1k4_sync": ("train", dict(spec=ER500, model="gcnii", layers=6, hidden=16, S=1, K=4,
                                             chunk_seed=3, epochs=10, seed=44, sync=1)),
+    "train_gcn_hyb_s2g2": ("train", dict(spec=ER500, model="gcn", layers=4, hidden=16, S=2, G=2, K=4, chunk_seed=3,
+                                         part_seed=1, epochs=8, seed=42, fix_alpha=3)),
+    "train_gcnii_hyb_s2g2": ("train", dict(spec=ER500, model="gcnii", layers=6, hidden=16, S=2, G=2, K=4,
+                                           chunk_seed=3, part_seed=2, epochs=8, seed=43, fix_alpha=3)),
+    "train_gcnii_hyb_s1g3_sync": ("train", dict(spec=ER500, model="gcnii", layers=5, hidden=16, S=1, G=3, K=3,
+                                                chunk_seed=5, part_seed=3, epochs=6, seed=44, sync=1)),
+    "train_gcn_hyb_s3g2_hist": ("train", dict(spec=ER500, model="gcn", layers=6, hidden=12, S=3, G=2, K=6,
+                                              chunk_seed=7, part_seed=4, epochs=6, seed=45, fix_alpha=2, hist=1)),
     "train_gcn_s3k6_w40": ("train", dict(spec=ER300W, model="gcn", layers=6, hidden=24, S=3, K=6, chunk_seed=1,
                                          epochs=8, seed=45, fix_alpha=2)),
 }

@@ -254,3 +254,37 @@ def test_invalid_arguments_raise(gp):
     with pytest.raises(gp.InvalidArgument):
         gp.train_pipeline(ds, np.zeros(ds.num_vertices, np.uint32), 1,
                           gp.TrainOptions(model=gp.ModelConfig(kind=1, layers=2, hidden=8)))
+
+
+HYB = [
+    # golden, model kind, L, H, S, G, K, chunk seed, part seed, epochs, seed, staleness kwargs
+    ("train_gcn_hyb_s2g2", 0, 4, 16, 2, 2, 4, 3, 1, 8, 42, dict(fix_alpha=3)),
+    ("train_gcnii_hyb_s2g2", 2, 6, 16, 2, 2, 4, 3, 2, 8, 43, dict(fix_alpha=3)),
+    ("train_gcnii_hyb_s1g3_sync", 2, 5, 16, 1, 3, 3, 5, 3, 6, 44, dict(synchronous_mode=True)),
+    ("train_gcn_hyb_s3g2_hist", 0, 6, 12, 3, 2, 6, 7, 4, 6, 45, dict(fix_alpha=2, historical_gradients=True)),
+]
+
+
+@pytest.mark.parametrize("case", HYB, ids=[c[0] for c in HYB])
+def test_train_hybrid_matches_reference(gp, case):
+    """train_hybrid (engines_impl.hpp:515-909) with G graph partitions per stage: halo
+    exchange, rank-ordered weight-gradient fold; ledger exact for all three classes."""
+    name, kind, L, H, S, G, K, cs, ps, ep, seed, kw = case
+    ref = golden(name)
+    ds = er500(gp)
+    part, _, _ = gp.partition_vertices(ds, G, ps)
+    co = gp.make_chunks(ds, K, cs)
+    assert np.array_equal(co, ref["chunk_of"])
+    opt = gp.TrainOptions(model=gp.ModelConfig(kind=kind, layers=L, hidden=H), epochs=ep, seed=seed, **kw)
+    res = gp.train_hybrid(ds, part, co, S, opt)
+    met = ref["metrics"].reshape(ep, 5)
+    assert np.max(np.abs(res.train_loss - met[:, 1]) / np.abs(met[:, 1])) < 1e-4, (res.train_loss, met[:, 1])
+    assert np.max(np.abs(res.metrics[:, 2:5] - met[:, 2:5])) <= 3.0 / (0.2 * ds.num_vertices)
+    assert np.array_equal(res.comm.astype(np.uint64), ref["comm"].reshape(ep, 3)), (res.comm, ref["comm"])
+    worst, med = 0.0, []
+    for l, (W, b) in enumerate(res.params):
+        rW = ref[f"W{l}"]
+        d = np.abs(W.astype(np.float64) - rW) / np.maximum(np.abs(rW), 1e-3)
+        worst = max(worst, float(d.max()))
+        med.append(float(np.median(d)))
+    assert worst < 2e-3 and max(med) < 1e-4, (worst, med)
