@@ -256,6 +256,9 @@ int gs_train_sequential(const gs_dataset* d, const gs_train_options* opt, gs_res
  * Partition::assignment (G = max + 1), groups as assign_groups(S*G, 4, S, G). */
 int gs_train_hybrid(const gs_dataset* d, const uint32_t* part_of, const uint32_t* chunk_of, uint32_t K,
                     uint32_t S, const gs_train_options* opt, gs_result** out);
+/* train_graph_parallel (engines.hpp:83-87) = hybrid at S = 1, K = 1. */
+int gs_train_graph_parallel(const gs_dataset* d, const uint32_t* part_of, const gs_train_options* opt,
+                            gs_result** out);
 /* T x {epoch, train_loss, train_acc, val_acc, test_acc, wall_time_s, bubble_fraction} */
 int gs_result_metrics(const gs_result* r, uint32_t* epochs, double* metrics,
                       uint64_t* comm /* T x {graph, pipeline, weightsync} */);

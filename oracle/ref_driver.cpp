@@ -328,6 +328,9 @@ void cmd_train(const Args& a) {
     const auto t0 = std::chrono::steady_clock::now();
     if (mode == "seq") {
         res = train_sequential(d, opt);
+    } else if (mode == "graph") {
+        Partition part = partition_vertices(d.graph, uint32_t(argu(a, "G", "2")), argu(a, "part_seed", "1"));
+        res = train_graph_parallel(d, part, opt);
     } else {
         const uint32_t S = uint32_t(argu(a, "S", "1"));
         const uint32_t K = uint32_t(argu(a, "K", "1"));

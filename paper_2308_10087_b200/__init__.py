@@ -148,6 +148,7 @@ def _L():
         "gs_train_pipeline": (C.c_int, [vp, u32p, C.c_uint32, C.c_uint32, P(gs_train_options), P(vp)]),
         "gs_train_sequential": (C.c_int, [vp, P(gs_train_options), P(vp)]),
         "gs_train_hybrid": (C.c_int, [vp, u32p, u32p, C.c_uint32, C.c_uint32, P(gs_train_options), P(vp)]),
+        "gs_train_graph_parallel": (C.c_int, [vp, u32p, P(gs_train_options), P(vp)]),
         "gp_upload_partition": (C.c_int, [vp, u32p]),
         "gp_link_group": (C.c_int, [P(vp), C.c_uint32]),
         "gs_result_metrics": (C.c_int, [vp, u32p, f64p, u64p]),
@@ -461,6 +462,14 @@ def train_hybrid(ds: Dataset, part_of: np.ndarray, chunk_of: np.ndarray, num_sta
     h = C.c_void_p()
     _gs(_L().gs_train_hybrid(ds._h, _ptr(po, C.c_uint32), _ptr(co, C.c_uint32), K, num_stages, C.byref(opt.c()),
                              C.byref(h)))
+    return _result(h, build_layer_specs(opt.model, ds.num_features, ds.num_classes))
+
+
+def train_graph_parallel(ds: Dataset, part_of: np.ndarray, opt: TrainOptions) -> TrainResult:
+    """train_graph_parallel<float> (engines.hpp:83-87): hybrid at S = 1, K = 1."""
+    po = np.ascontiguousarray(part_of, np.uint32)
+    h = C.c_void_p()
+    _gs(_L().gs_train_graph_parallel(ds._h, _ptr(po, C.c_uint32), C.byref(opt.c()), C.byref(h)))
     return _result(h, build_layer_specs(opt.model, ds.num_features, ds.num_classes))
 
 

@@ -262,6 +262,17 @@ int gs_train_hybrid(const gs_dataset* d, const uint32_t* part_of, const uint32_t
     });
 }
 
+int gs_train_graph_parallel(const gs_dataset* d, const uint32_t* part_of, const gs_train_options* o,
+                            gs_result** out) {
+    return guarded([&]() {
+        const VertexId n = d->d.num_vertices();
+        Partition part = partition_from_assignment(d->d.graph, std::vector<uint32_t>(part_of, part_of + n));
+        auto own = std::make_unique<gs_result>();
+        own->r = train_graph_parallel<float>(d->d, part, options_of(o));
+        *out = own.release();
+    });
+}
+
 int gs_train_sequential(const gs_dataset* d, const gs_train_options* o, gs_result** out) {
     return guarded([&]() {
         auto own = std::make_unique<gs_result>();

@@ -338,7 +338,19 @@ TrainResult<T> train_hybrid(const Dataset& ds, const Partition& part, const Chun
                           opt.fabric.node_of.empty() ? gmap.node_of : opt.fabric.node_of, opt);
 }
 
+template <typename T>
+TrainResult<T> train_graph_parallel(const Dataset& ds, const Partition& part, const TrainOptions<T>& opt) {
+    ds.validate();
+    if (part.assignment.size() != ds.num_vertices())
+        throw std::invalid_argument("train_graph_parallel: partition does not cover the graph");
+    const uint32_t P = part.num_parts, L = uint32_t(build_layer_specs(opt.model, ds.num_features(), ds.num_classes).size());
+    ChunkPlan whole = chunk_plan_from_assignment(ds.num_vertices(), std::vector<uint32_t>(ds.num_vertices(), 0));
+    GroupMap gmap = assign_groups(P, 4, 1, P);
+    return train_hybrid<T>(ds, part, whole, make_stage_assignment(L, 1), gmap, opt);
+}
+
 template TrainResult<float> train_sequential<float>(const Dataset&, const TrainOptions<float>&);
+template TrainResult<float> train_graph_parallel<float>(const Dataset&, const Partition&, const TrainOptions<float>&);
 template TrainResult<float> train_pipeline<float>(const Dataset&, const ChunkPlan&, const StageAssignment&,
                                                   const TrainOptions<float>&);
 template TrainResult<float> train_hybrid<float>(const Dataset&, const Partition&, const ChunkPlan&,

@@ -322,10 +322,16 @@ template <typename T>
 TrainResult<T> train_hybrid(const Dataset& ds, const Partition& part, const ChunkPlan& plan,
                             const StageAssignment& stages, const GroupMap& gmap,
                             const TrainOptions<T>& opt);
+// Graph parallelism (engines.hpp:83-87): the reference's hybrid engine at S = 1,
+// K = 1 reproduces it bitwise (test_engines.cpp:238-251), and so does this one.
+template <typename T>
+TrainResult<T> train_graph_parallel(const Dataset& ds, const Partition& part, const TrainOptions<T>& opt);
 
 extern template TrainResult<float> train_sequential<float>(const Dataset&, const TrainOptions<float>&);
 extern template TrainResult<float> train_pipeline<float>(const Dataset&, const ChunkPlan&,
                                                          const StageAssignment&, const TrainOptions<float>&);
+extern template TrainResult<float> train_graph_parallel<float>(const Dataset&, const Partition&,
+                                                               const TrainOptions<float>&);
 extern template TrainResult<float> train_hybrid<float>(const Dataset&, const Partition&, const ChunkPlan&,
                                                        const StageAssignment&, const GroupMap&,
                                                        const TrainOptions<float>&);

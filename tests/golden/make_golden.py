@@ -46,6 +46,10 @@ SCENARIOS = {
                                                 chunk_seed=5, part_seed=3, epochs=6, seed=44, sync=1)),
     "train_gcn_hyb_s3g2_hist": ("train", dict(spec=ER500, model="gcn", layers=6, hidden=12, S=3, G=2, K=6,
                                               chunk_seed=7, part_seed=4, epochs=6, seed=45, fix_alpha=2, hist=1)),
+    "train_gcn_graph_p3": ("train", dict(spec=ER500, model="gcn", layers=3, hidden=16, mode="graph", G=3,
+                                         part_seed=5, epochs=6, seed=53)),
+    "train_gcnii_graph_p2": ("train", dict(spec=ER500, model="gcnii", layers=5, hidden=16, mode="graph", G=2,
+                                           part_seed=6, epochs=6, seed=54)),
     "train_gcn_s3k6_w40": ("train", dict(spec=ER300W, model="gcn", layers=6, hidden=24, S=3, K=6, chunk_seed=1,
                                          epochs=8, seed=45, fix_alpha=2)),
 }
