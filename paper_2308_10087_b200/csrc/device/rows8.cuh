@@ -152,35 +152,27 @@ __device__ __forceinline__ void w8_row(const float4* Ws4, uint32_t r, uint32_t c
 
 // Row-local GEMV: o[c] += sum_i x_i * M[i][c] over i ascending (x held 8 per
 // lane across the half-warp), one rounded mul and add per term.
-__device__ __forceinline__ void gemv8_step(F8& o, float xi, const float4* Ws4, uint32_t i, uint32_t c8, int hl) {
-    float4 a, b;
-    w8_row(Ws4, i, c8, hl, a, b);
-    o.v[0] = mul_add(o.v[0], xi, a.x);
-    o.v[1] = mul_add(o.v[1], xi, a.y);
-    o.v[2] = mul_add(o.v[2], xi, a.z);
-    o.v[3] = mul_add(o.v[3], xi, a.w);
-    o.v[4] = mul_add(o.v[4], xi, b.x);
-    o.v[5] = mul_add(o.v[5], xi, b.y);
-    o.v[6] = mul_add(o.v[6], xi, b.z);
-    o.v[7] = mul_add(o.v[7], xi, b.w);
-}
-
-// The two half-warps run skewed by one step (half 1 at i-1 while half 0 is at
-// i): each still accumulates in ascending i, but a quarter-warp never fetches
-// the W row the other half is fetching, halving shared-memory wavefronts.
 __device__ __forceinline__ void gemv8(F8& o, const F8& x, const float4* Ws4, uint32_t rows, uint32_t c8, int hl,
                                       int hb) {
     const uint32_t r8 = (rows + 7) / 8;
-    const bool h1 = hb != 0;
-    for (uint32_t jb = 0; jb <= r8; ++jb) {
+    for (uint32_t ib = 0; ib < r8; ++ib) {
+        const F8 xb = shfl8(x, hb + int(ib));
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-            // half 0: i = 8jb + q ; half 1: i = 8jb + q - 1
-            const int i = int(8 * jb) + q - (h1 ? 1 : 0);
-            const float sendv = h1 ? x.v[(q + 7) & 7] : x.v[q];
-            const int src_blk = h1 ? (q >= 1 ? int(jb) : int(jb) - 1) : int(jb);
-            const float xi = __shfl_sync(kFull, sendv, hb + (src_blk < 0 ? 0 : (src_blk > 15 ? 15 : src_blk)));
-            if (i >= 0 && uint32_t(i) < rows) gemv8_step(o, xi, Ws4, uint32_t(i), c8, hl);
+            const uint32_t i = 8 * ib + q;
+            if (i < rows) {
+                float4 a, b;
+                w8_row(Ws4, i, c8, hl, a, b);
+                const float xi = xb.v[q];
+                o.v[0] = mul_add(o.v[0], xi, a.x);
+                o.v[1] = mul_add(o.v[1], xi, a.y);
+                o.v[2] = mul_add(o.v[2], xi, a.z);
+                o.v[3] = mul_add(o.v[3], xi, a.w);
+                o.v[4] = mul_add(o.v[4], xi, b.x);
+                o.v[5] = mul_add(o.v[5], xi, b.y);
+                o.v[6] = mul_add(o.v[6], xi, b.z);
+                o.v[7] = mul_add(o.v[7], xi, b.w);
+            }
         }
     }
 }
