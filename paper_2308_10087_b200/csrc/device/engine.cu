@@ -399,7 +399,20 @@ struct Stage {
         part_correct = dalloc<unsigned long long>(3ull * xent_blocks);
         red_loss = dalloc<double>(1);
         red_correct = dalloc<unsigned long long>(3);
+        tickets = dalloc<uint32_t>(kTickets);
         GP_CUDA(cudaDeviceSynchronize());
+    }
+
+    // Work counters of the dynamically scheduled row kernels (one per launch).
+    uint32_t* tickets = nullptr;
+    uint32_t ticket_next = 0;
+    static constexpr uint32_t kTickets = 16384;
+    uint32_t* take_ticket() {
+        if (ticket_next == kTickets) {
+            GP_CUDA(cudaMemsetAsync(tickets, 0, kTickets * 4, cs));
+            ticket_next = 0;
+        }
+        return tickets + ticket_next++;
     }
 
     // Gathers in flight per lane (template NB of the row kernels); GP_NB overrides.
@@ -775,6 +788,7 @@ struct Stage {
             FwdParams p{};
             p.r0 = r0;
             p.r1 = r1;
+            p.ticket = take_ticket();
             p.rowptr = rowptr;
             p.edges = edges;
             p.gsrc = d.G;
@@ -873,6 +887,7 @@ struct Stage {
         BwdParams p{};
         p.r0 = r0;
         p.r1 = r1;
+        p.ticket = take_ticket();
         p.rowptr = rowptr;
         p.edges = edges;
         p.done = done;
@@ -948,6 +963,7 @@ struct Stage {
         BwdParams p{};
         p.r0 = r0;
         p.r1 = r1;
+        p.ticket = take_ticket();
         p.rowptr = rowptr;
         p.edges = edges;
         p.done = done;
@@ -1327,6 +1343,8 @@ struct Stage {
         std::fill(msgs_sent, msgs_sent + 6, 0);
         launches = 0;
         tr.ev_next = 0;
+        GP_CUDA(cudaMemsetAsync(tickets, 0, kTickets * 4, cs));
+        ticket_next = 0;
         GP_CUDA(cudaEventRecord(ev_start, cs));
 
         // Snapshot (engines_impl.hpp:671-679): snap := cur. Every cur row is

@@ -201,6 +201,7 @@ __global__ void __launch_bounds__(kBlock) k_remask(RemaskParams p) {
 // ---------------------------------------------------------------------------
 struct FwdParams {
     uint32_t r0, r1;
+    uint32_t* ticket;  // zeroed work counter (row pairs handed out)
     const uint64_t* rowptr;
     const uint2* edges;
     const float* gsrc;
@@ -364,6 +365,7 @@ __global__ void __launch_bounds__(kBlock) k_dense_gemm(GemmParams p) {
 // ---------------------------------------------------------------------------
 struct BwdParams {
     uint32_t r0, r1;
+    uint32_t* ticket;
     const uint64_t* rowptr;
     const uint2* edges;
     const float* bgn;

@@ -94,9 +94,16 @@ __device__ __forceinline__ F8 gather_row8(const uint64_t* __restrict__ rowptr, c
     // half-warp, so padding never concentrates on one L2 line)
     const float* lpad = ls + size_t(has_row ? v : 0u) * stride;
     F8 acc = f8_zero();
+    // CSR batch of the next iteration is loaded one batch ahead
+    uint2 nxt = hl < int(min(16u, n_my)) ? ld_edge(edges + e0 + hl) : make_uint2(0u, 0u);
     for (uint32_t off = 0; off < n_max; off += 16) {
         int cnt = n_my > off ? int(min(16u, n_my - off)) : 0;
-        uint2 my = hl < cnt ? ld_edge(edges + e0 + off + hl) : make_uint2(0u, 0u);
+        uint2 my = nxt;
+        {
+            const uint32_t noff = off + 16;
+            const int ncnt = n_my > noff ? int(min(16u, n_my - noff)) : 0;
+            nxt = hl < ncnt ? ld_edge(edges + e0 + noff + hl) : make_uint2(0u, 0u);
+        }
         if (FILTER && !HIST) {
             const bool ok = hl < cnt && ((done >> (my.x >> kColBits)) & 1ull);
             const unsigned m = (__ballot_sync(kFull, ok) >> hb) & 0xffffu;
@@ -202,9 +209,13 @@ __global__ void __launch_bounds__(kBlock, NB == 2 ? 4 : (NB == 4 ? 3 : 2)) k_fwd
     const int lane = threadIdx.x & 31, hl = lane & 15, hb = lane & 16;
     const bool in_act = uint32_t(8 * hl) < p.din;
     const bool out_act = uint32_t(8 * hl) < p.dout;
-    const uint32_t gw = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
-    const uint32_t nw = gridDim.x * kWarpsPerBlock;
-    for (uint32_t base = p.r0 + 2 * gw; base < p.r1; base += 2 * nw) {
+    for (;;) {
+        // dynamic row-pair scheduling: no static tail across a ~6-pair-per-warp launch
+        uint32_t pair = 0;
+        if (lane == 0) pair = atomicAdd(p.ticket, 1u);
+        pair = __shfl_sync(kFull, pair, 0);
+        const uint32_t base = p.r0 + 2 * pair;
+        if (base >= p.r1) break;
         const uint32_t v = base + (hb ? 1u : 0u);
         const bool has = v < p.r1;
         F8 pre;
@@ -268,9 +279,13 @@ __global__ void __launch_bounds__(kBlock, NB == 2 ? 4 : (NB == 4 ? 3 : 2)) k_bwd
     const int lane = threadIdx.x & 31, hl = lane & 15, hb = lane & 16;
     const bool dh_act = uint32_t(8 * hl) < p.dh_width;
     const bool in_act = uint32_t(8 * hl) < p.din;
-    const uint32_t gw = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
-    const uint32_t nw = gridDim.x * kWarpsPerBlock;
-    for (uint32_t base = p.r0 + 2 * gw; base < p.r1; base += 2 * nw) {
+    for (;;) {
+        // dynamic row-pair scheduling: no static tail across a ~6-pair-per-warp launch
+        uint32_t pair = 0;
+        if (lane == 0) pair = atomicAdd(p.ticket, 1u);
+        pair = __shfl_sync(kFull, pair, 0);
+        const uint32_t base = p.r0 + 2 * pair;
+        if (base >= p.r1) break;
         const uint32_t u = base + (hb ? 1u : 0u);
         const bool has = u < p.r1;
         F8 dh;
