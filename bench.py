@@ -171,6 +171,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-rows", type=int, default=600)
+    ap.add_argument("--transport", default="ipc", choices=["ipc", "nccl"],
+                    help="stage boundary transport for N>1: CUDA-IPC copy-engine rings (default) or NCCL send/recv")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -182,10 +184,14 @@ def main():
 
     import paper_2308_10087_b200 as gp
 
+    # one rank per GPU; more ranks than GPUs share devices round-robin (a
+    # functional check of the multi-process path on a 1-GPU box, not a timing)
+    ndev = gp.device_count()
+    dev = local % ndev if ndev else local
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("gloo")  # control plane only; stage data moves over NCCL (gp_link_nccl)
+        dist.init_process_group("gloo")  # control plane only; stage data moves over gp_link_ipc / gp_link_nccl
 
     def barrier():
         if dist:
@@ -216,7 +222,7 @@ def main():
 
     def make_engine():
         eng = gp.StageEngine(num_vertices=N, num_chunks=K, specs=specs, stage=rank, num_stages=S,
-                             layer_range=(lo, hi), hidden=H, num_classes=Cc, dropout=0.5, seed=1, device=local)
+                             layer_range=(lo, hi), hidden=H, num_classes=Cc, dropout=0.5, seed=1, device=dev)
         return eng
 
     def upload(eng):
@@ -231,8 +237,11 @@ def main():
     def link(eng):
         if S == 1:
             return
-        ids = D.exchange_unique_ids(dist, rank, S, gp.nccl_unique_id)
-        eng.link_nccl(*D.boundary_ids(ids, rank, S))
+        if args.transport == "ipc":
+            eng.link_ipc(*D.exchange_ipc_blobs(dist, rank, S, eng.ipc_export()))
+        else:
+            ids = D.exchange_unique_ids(dist, rank, S, gp.nccl_unique_id)
+            eng.link_nccl(*D.boundary_ids(ids, rank, S))
 
     def order(t):
         return gp.shuffle_chunk_order(K, t, 1)
@@ -247,7 +256,7 @@ def main():
     eng.synchronize()
     barrier()
     launches = 0
-    with ClockSampler(local) as clk:
+    with ClockSampler(dev) as clk:
         eng.mark(0)
         losses = []
         for _ in range(args.steps):
@@ -260,6 +269,10 @@ def main():
         ms = eng.elapsed_ms(0, 1)
     barrier()
     ms = max_over_ranks(ms)
+    if dist:  # the loss lives on the last stage
+        box = [losses]
+        dist.broadcast_object_list(box, src=S - 1)
+        losses = box[0]
     ms_step = ms / args.steps
 
     # per-kernel device times from one extra, untimed profiling epoch
@@ -278,7 +291,7 @@ def main():
     if not args.no_e2e:
         if S == 1:
             barrier()
-            opt = gp.TrainOptions(model=model, epochs=args.steps, seed=1, device=local)
+            opt = gp.TrainOptions(model=model, epochs=args.steps, seed=1, device=dev)
             t0 = time.perf_counter()
             res = gp.train_pipeline(ds, chunk_of, 1, opt)
             e2e_s = time.perf_counter() - t0
@@ -338,7 +351,8 @@ def main():
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (generate_er graph + hashed features, seed 1)",
         "config": {"workload": desc, "num_vertices": N, "nnz_norm_adj": int(cols.size), "features": F,
                    "classes": Cc, "hidden": H, "layers": L, "model": mk, "stages": S, "chunks": K,
-                   "parallelism": f"pp{S}", "l2_policy": f"inputs larger than L2 (stage stash {dev_bytes/2**30:.1f} GiB)"},
+                   "parallelism": f"pp{S}", "transport": args.transport if S > 1 else None,
+                   "ranks_per_gpu": -(-world // max(1, ndev)), "l2_policy": f"inputs larger than L2 (stage stash {dev_bytes/2**30:.1f} GiB)"},
         "clocks": clk.summary(),
         "e2e": e2e,
         "gpu_launches": int(launches),

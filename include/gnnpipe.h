@@ -164,6 +164,20 @@ gp_status gp_link_local(gp_ctx* upstream, gp_ctx* downstream);
  * 2-rank communicator (rank 0 = upstream stage). Pass NULL for a missing side. */
 gp_status gp_nccl_unique_id(uint8_t out[128]);
 gp_status gp_link_nccl(gp_ctx* ctx, const uint8_t* up_id, const uint8_t* down_id);
+/* One process per GPU: CUDA-IPC peer-memory rings (replaces the reference's
+ * in-process fabric channels, WorkerCtx::send/recv fabric.cpp:288-359, for stages in different
+ * processes of one node). The receiving side of each direction owns a ring of
+ * message slots; the sender pushes chunk rows into the peer's slot with the copy
+ * engine over NVLink and signals with in-stream memory ops, so the transfer
+ * overlaps the next chunk's kernels without taking SMs. Protocol:
+ *   1. gp_ipc_export after gp_upload_graph: fills an opaque blob per boundary
+ *      (up: shared with stage s-1, down: with stage s+1; NULL for a missing side);
+ *   2. exchange blobs out of band (any control plane);
+ *   3. gp_link_ipc(ctx, blob exported as `down` by stage s-1, blob exported as
+ *      `up` by stage s+1). Both processes may use the same device. */
+#define GP_IPC_BLOB_BYTES 256
+gp_status gp_ipc_export(gp_ctx* ctx, uint8_t* up_blob, uint8_t* down_blob);
+gp_status gp_link_ipc(gp_ctx* ctx, const uint8_t* up_peer_blob, const uint8_t* down_peer_blob);
 /* Hybrid: join the G workers of one stage group (same process). Halo rows of each
  * aggregating layer (exchange_rows, engines_impl.hpp:626-643) are pulled by the
  * receiver from its peers' buffers after an event handshake; weight gradients

@@ -33,6 +33,7 @@ _LIBDIR = os.path.join(_HERE, "lib")
 
 GP_OK, GP_EINVAL, GP_ENUMERIC, GP_EFABRIC, GP_ECUDA, GP_ERUNTIME = 0, 1, 2, 3, 4, 5
 PROFILE_CLASSES = ["remask", "fwd_agg", "fwd_dense", "bwd_agg", "bwd_dense", "xent", "pgrad", "optim", "xfer"]
+IPC_BLOB_BYTES = 256  # GP_IPC_BLOB_BYTES
 GP_BUF = {"h": 0, "pre": 1, "dz": 2, "dagg": 3, "dh0": 4, "hsnap": 5, "in": 6, "dh_in": 7, "gather": 8}
 
 
@@ -123,7 +124,7 @@ def _L():
     path = lib_paths()[0]
     if not os.path.exists(path):
         raise GpuEngineError(f"{path} is missing: run __graft_entry__.build() (make -C paper_2308_10087_b200/csrc)")
-    lib = C.CDLL(path, mode=C.RTLD_GLOBAL)
+    lib = C.CDLL(path, mode=C.RTLD_LOCAL)  # never interpose symbols of torch / other libraries
     P = C.POINTER
     u32p, u64p, f32p, u8p, f64p = P(C.c_uint32), P(C.c_uint64), P(C.c_float), P(C.c_uint8), P(C.c_double)
     vp = C.c_void_p
@@ -171,6 +172,8 @@ def _L():
         "gp_link_local": (C.c_int, [vp, vp]),
         "gp_nccl_unique_id": (C.c_int, [P(C.c_uint8)]),
         "gp_link_nccl": (C.c_int, [vp, P(C.c_uint8), P(C.c_uint8)]),
+        "gp_ipc_export": (C.c_int, [vp, P(C.c_uint8), P(C.c_uint8)]),
+        "gp_link_ipc": (C.c_int, [vp, P(C.c_uint8), P(C.c_uint8)]),
         "gp_abort": (None, [vp]),
         "gp_run_epoch": (C.c_int, [vp, C.c_uint32, u32p, P(gp_epoch_stats)]),
         "gp_download": (C.c_int, [vp, C.c_uint32, C.c_uint32, f32p, C.c_uint64]),
@@ -587,6 +590,22 @@ class StageEngine:
         up = (C.c_uint8 * 128).from_buffer_copy(up_id) if up_id else None
         down = (C.c_uint8 * 128).from_buffer_copy(down_id) if down_id else None
         _gp(_L().gp_link_nccl(self._h, up, down), self._h)
+
+    def ipc_export(self):
+        """Ring regions for the CUDA-IPC transport: (up_blob, down_blob), None for a
+        missing side. Call after upload_graph; exchange the blobs out of band."""
+        first, last = self.stage == 0, self.stage == self.S - 1
+        up = (C.c_uint8 * IPC_BLOB_BYTES)() if not first else None
+        down = (C.c_uint8 * IPC_BLOB_BYTES)() if not last else None
+        _gp(_L().gp_ipc_export(self._h, up, down), self._h)
+        return (bytes(up) if up is not None else None, bytes(down) if down is not None else None)
+
+    def link_ipc(self, up_peer: Optional[bytes], down_peer: Optional[bytes]):
+        """Link to the neighbour stages' exported blobs: `up_peer` is the `down` blob
+        of stage s-1, `down_peer` the `up` blob of stage s+1."""
+        up = (C.c_uint8 * IPC_BLOB_BYTES).from_buffer_copy(up_peer) if up_peer else None
+        down = (C.c_uint8 * IPC_BLOB_BYTES).from_buffer_copy(down_peer) if down_peer else None
+        _gp(_L().gp_link_ipc(self._h, up, down), self._h)
 
     def abort(self):
         _L().gp_abort(self._h)

@@ -9,9 +9,11 @@
 //   metrics           :816-825  -> k_xent_stats / k_xent_fold
 //   backward loop     :827-870  -> run_epoch() backward section
 //   param grads + step:872-878  -> k_pgrad_* + k_adam
-//   stage messages    :690-724  -> Transport (local D2D or NCCL)
+//   stage messages    :690-724  -> Transport (local D2D, CUDA-IPC peer rings, or NCCL)
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <atomic>
@@ -72,7 +74,7 @@ struct NcclApi {
     ErrStr err = nullptr;
     bool load() {
         if (h) return true;
-        h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
         if (!h) return false;
         get_unique_id = (GetUniqueId)dlsym(h, "ncclGetUniqueId");
         comm_init_rank = dlsym(h, "ncclCommInitRank");
@@ -98,6 +100,34 @@ constexpr int kNcclFloat = 7;  // ncclFloat32
 void nccl_check(int r, const char* what) {
     if (r != 0)
         throw Error(GP_ECUDA, std::string(what) + ": " + (g_nccl.err ? g_nccl.err(r) : "nccl error"));
+}
+
+// ------------------------------------------------------------------ stream memory ops
+// cuStreamWaitValue32 / cuStreamWriteValue32 (driver API, resolved through the
+// runtime so nothing links libcuda directly): the IPC transport's flags are
+// waited on and bumped in-stream, so no host thread sits in the data path.
+struct MemOps {
+    typedef CUresult (*Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+    Fn wait = nullptr, write = nullptr;
+    std::mutex mu;
+    void load() {
+        std::lock_guard<std::mutex> lk(mu);
+        if (wait && write) return;
+        for (int i = 0; i < 2; ++i) {
+            void* f = nullptr;
+            cudaDriverEntryPointQueryResult q = cudaDriverEntryPointSymbolNotFound;
+            const char* sym = i == 0 ? "cuStreamWaitValue32" : "cuStreamWriteValue32";
+            if (cudaGetDriverEntryPointByVersion(sym, &f, 12000, cudaEnableDefault, &q) != cudaSuccess ||
+                q != cudaDriverEntryPointSuccess || !f)
+                throw Error(GP_ECUDA, std::string(sym) + " unavailable");
+            (i == 0 ? wait : write) = (Fn)f;
+        }
+    }
+};
+MemOps g_memops;
+
+void cu_check(CUresult r, const char* what) {
+    if (r != CUDA_SUCCESS) throw Error(GP_ECUDA, std::string(what) + " failed (CUresult " + std::to_string(int(r)) + ")");
 }
 
 // ------------------------------------------------------------------ transport
@@ -147,6 +177,41 @@ struct HostGraph {
     std::vector<uint32_t> bstart;   // (G x (K+1)) block starts: rows of (rank r, chunk k)
 };
 
+// One stage boundary between processes over CUDA IPC (one process per GPU on a
+// node; NVLink P2P between GPUs, plain device memory when both share one).
+// Each side owns a region {ready @0, ack @128, ring of R message slots @4096}:
+// the sender pushes a message into the receiver's ring with the copy engine
+// (no SMs taken from the stage's kernels) and bumps the receiver's `ready`
+// counter with an in-stream write; the receiver waits on `ready` in its compute
+// stream, unpacks the slot and bumps the sender's `ack`, which the sender waits
+// on before reusing a slot. Counters are message sequence numbers (1-based,
+// monotone over the run), so each direction stays a FIFO like the reference
+// channel (fabric.cpp:190).
+constexpr size_t kIpcReady = 0, kIpcAck = 128, kIpcRing = 4096;
+constexpr uint32_t kIpcMagic = 0x50495047u;  // "GPIP"
+
+struct IpcBlob {
+    uint32_t magic, version, stage, role;  // role 0: up boundary (receives fwd), 1: down (receives bwd)
+    uint32_t n, K, R, pad0;
+    uint64_t slot_floats, bytes, ptr;
+    int32_t pid, device;
+    cudaIpcMemHandle_t handle;
+};
+static_assert(sizeof(IpcBlob) <= GP_IPC_BLOB_BYTES, "IPC blob too large");
+
+struct IpcSide {
+    char* own = nullptr;  // own region (allocated by export)
+    uint64_t own_slot = 0, own_bytes = 0;
+    uint32_t own_R = 0;
+    char* peer = nullptr;  // peer region (opened from the peer's blob)
+    bool peer_opened = false;  // true: cudaIpcOpenMemHandle (close on destroy)
+    uint64_t peer_slot = 0;
+    uint32_t peer_R = 0;
+    uint32_t send_seq = 0, recv_seq = 0;
+    cudaStream_t stream = nullptr;  // send stream (copy engine work overlaps the next chunk)
+    bool linked() const { return peer != nullptr; }
+};
+
 struct Transport {
     // Forward: upstream stage sends chunk rows of its last layer (+h0).
     std::shared_ptr<LocalLink> up_local, down_local;  // links to s-1 and s+1
@@ -156,6 +221,7 @@ struct Transport {
     cudaStream_t up_stream = nullptr, down_stream = nullptr;
     std::vector<cudaEvent_t> ev_pool;
     size_t ev_next = 0;
+    IpcSide ipc_up, ipc_down;  // cross-process boundaries (gp_link_ipc)
 };
 
 // ------------------------------------------------------------------ stage
@@ -263,6 +329,19 @@ struct Stage {
 
     ~Stage() {
         if (device >= 0) cudaSetDevice(device);
+        if (tr.ipc_up.linked() || tr.ipc_down.linked()) {
+            // a dead peer leaves in-stream waits pending: bounded wait, then leak
+            try {
+                for (cudaStream_t st : {cs, tr.ipc_up.stream, tr.ipc_down.stream})
+                    if (st) sync_watchdog(st, 30.0);
+            } catch (...) {
+                return;
+            }
+            for (IpcSide* x : {&tr.ipc_up, &tr.ipc_down}) {
+                if (x->peer_opened) cudaIpcCloseMemHandle(x->peer);
+                if (x->stream) cudaStreamDestroy(x->stream);
+            }
+        }
         if (cs) cudaStreamSynchronize(cs);
         for (void* p : allocs) cudaFree(p);
         for (auto& t : timed) {
@@ -1168,14 +1247,159 @@ struct Stage {
         GP_CUDA(cudaStreamWaitEvent(cs, done, 0));
     }
 
+    // ---- CUDA-IPC rings (gp_link_ipc) --------------------------------------------
+    // Host-side wait with a watchdog: an in-stream wait on a dead peer never
+    // completes, so the epoch fails with GP_EFABRIC instead of hanging.
+    void sync_watchdog(cudaStream_t st, double seconds) {
+        cudaEvent_t e;
+        GP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        GP_CUDA(cudaEventRecord(e, st));
+        const auto deadline = std::chrono::steady_clock::now() + std::chrono::duration<double>(seconds);
+        for (;;) {
+            const cudaError_t q = cudaEventQuery(e);
+            if (q == cudaSuccess) break;
+            if (q != cudaErrorNotReady) {
+                cudaEventDestroy(e);
+                GP_CUDA(q);
+            }
+            if (aborted || std::chrono::steady_clock::now() > deadline) {
+                // the event stays recorded on a stuck stream: leak it
+                throw Error(GP_EFABRIC, "watchdog: stage " + std::to_string(s) +
+                                            (aborted ? " aborted" : " blocked on a peer stage (IPC transport)"));
+            }
+            std::this_thread::sleep_for(std::chrono::microseconds(50));
+        }
+        cudaEventDestroy(e);
+    }
+
+    // Receive-ring slot sizes: the largest message of any chunk in that direction.
+    uint64_t ipc_slot_floats(bool up_side) {
+        uint64_t m = 0;
+        for (uint32_t k = 0; k < K; ++k) {
+            uint64_t t = 0;
+            for (const auto& p : up_side ? fwd_pieces(k, false) : bwd_pieces(k, false)) t += p.floats;
+            m = std::max(m, t);
+        }
+        return m;
+    }
+
+    void ipc_export(uint8_t* up_blob, uint8_t* down_blob) {
+        GP_CUDA(cudaSetDevice(device));
+        if (!graph_ready) throw Error(GP_EINVAL, "gp_ipc_export: upload the graph first");
+        if (G > 1) throw Error(GP_EINVAL, "gp_ipc_export: hybrid groups link in-process (gp_link_group)");
+        g_memops.load();
+        for (int side = 0; side < 2; ++side) {
+            uint8_t* out = side == 0 ? up_blob : down_blob;
+            if (!out) continue;
+            const bool present = side == 0 ? !first : !last;
+            if (!present) throw Error(GP_EINVAL, side == 0 ? "gp_ipc_export: stage 0 has no upstream boundary"
+                                                           : "gp_ipc_export: last stage has no downstream boundary");
+            IpcSide& x = side == 0 ? tr.ipc_up : tr.ipc_down;
+            if (!x.own) {
+                x.own_R = std::min<uint32_t>(K, 3);
+                x.own_slot = (ipc_slot_floats(side == 0) + 63) & ~uint64_t(63);
+                x.own_bytes = kIpcRing + x.own_slot * 4 * x.own_R;
+                x.own = dalloc<char>(x.own_bytes);  // zeroed: counters start at 0
+                GP_CUDA(cudaStreamCreateWithFlags(&x.stream, cudaStreamNonBlocking));
+            }
+            IpcBlob b{};
+            b.magic = kIpcMagic;
+            b.version = GP_ABI_VERSION;
+            b.stage = s;
+            b.role = uint32_t(side);
+            b.n = n;
+            b.K = K;
+            b.R = x.own_R;
+            b.slot_floats = x.own_slot;
+            b.bytes = x.own_bytes;
+            b.ptr = uint64_t(reinterpret_cast<uintptr_t>(x.own));
+            b.pid = int32_t(getpid());
+            b.device = device;
+            GP_CUDA(cudaIpcGetMemHandle(&b.handle, x.own));
+            std::memset(out, 0, GP_IPC_BLOB_BYTES);
+            std::memcpy(out, &b, sizeof(b));
+        }
+    }
+
+    void ipc_link(const uint8_t* up_peer, const uint8_t* down_peer) {
+        GP_CUDA(cudaSetDevice(device));
+        for (int side = 0; side < 2; ++side) {
+            const uint8_t* in = side == 0 ? up_peer : down_peer;
+            if (!in) continue;
+            IpcSide& x = side == 0 ? tr.ipc_up : tr.ipc_down;
+            if (!x.own) throw Error(GP_EINVAL, "gp_link_ipc: call gp_ipc_export for this side first");
+            if (x.peer) throw Error(GP_EINVAL, "gp_link_ipc: side already linked");
+            IpcBlob b;
+            std::memcpy(&b, in, sizeof(b));
+            // up side pairs with the upstream stage's down region and vice versa
+            const uint32_t want_stage = side == 0 ? s - 1 : s + 1, want_role = side == 0 ? 1u : 0u;
+            if (b.magic != kIpcMagic || b.version != GP_ABI_VERSION) throw Error(GP_EINVAL, "gp_link_ipc: not an IPC blob");
+            if (b.stage != want_stage || b.role != want_role)
+                throw Error(GP_EINVAL, "gp_link_ipc: blob of stage " + std::to_string(b.stage) + " role " +
+                                           std::to_string(b.role) + " does not face this boundary");
+            if (b.n != n || b.K != K) throw Error(GP_EINVAL, "gp_link_ipc: N/K mismatch");
+            if (b.pid == int32_t(getpid())) {
+                x.peer = reinterpret_cast<char*>(uintptr_t(b.ptr));  // same process: plain UVA pointer
+                if (b.device != device) {
+                    cudaDeviceEnablePeerAccess(b.device, 0);
+                    cudaGetLastError();
+                }
+            } else {
+                void* p = nullptr;
+                GP_CUDA(cudaIpcOpenMemHandle(&p, b.handle, cudaIpcMemLazyEnablePeerAccess));
+                x.peer = static_cast<char*>(p);
+                x.peer_opened = true;
+            }
+            x.peer_slot = b.slot_floats;
+            x.peer_R = b.R;
+        }
+    }
+
+    CUdeviceptr dptr(char* base, size_t off) { return CUdeviceptr(reinterpret_cast<uintptr_t>(base + off)); }
+
+    void ipc_send(IpcSide& x, uint32_t k, const std::vector<Piece>& pcs) {
+        uint64_t tot = 0;
+        for (const auto& p : pcs) tot += p.floats;
+        if (tot > x.peer_slot)
+            throw Error(GP_EFABRIC, "IPC send of chunk " + std::to_string(k) + " exceeds the peer's slot");
+        const uint32_t seq = ++x.send_seq, slot = (seq - 1) % x.peer_R;
+        cudaEvent_t ev = pool_event();
+        GP_CUDA(cudaEventRecord(ev, cs));
+        GP_CUDA(cudaStreamWaitEvent(x.stream, ev, 0));
+        if (seq > x.peer_R)  // slot reuse: the receiver has unpacked message seq - R
+            cu_check(g_memops.wait(x.stream, dptr(x.own, kIpcAck), seq - x.peer_R, CU_STREAM_WAIT_VALUE_GEQ),
+                     "cuStreamWaitValue32(ack)");
+        float* dst = reinterpret_cast<float*>(x.peer + kIpcRing) + size_t(slot) * x.peer_slot;
+        for (const auto& p : pcs) {
+            GP_CUDA(cudaMemcpyAsync(dst, p.ptr, p.floats * 4, cudaMemcpyDefault, x.stream));
+            dst += p.floats;
+        }
+        cu_check(g_memops.write(x.stream, dptr(x.peer, kIpcReady), seq, CU_STREAM_WRITE_VALUE_DEFAULT),
+                 "cuStreamWriteValue32(ready)");
+    }
+
+    void ipc_recv(IpcSide& x, const std::vector<Piece>& pcs) {
+        const uint32_t seq = ++x.recv_seq, slot = (seq - 1) % x.own_R;
+        cu_check(g_memops.wait(cs, dptr(x.own, kIpcReady), seq, CU_STREAM_WAIT_VALUE_GEQ), "cuStreamWaitValue32(ready)");
+        const float* src = reinterpret_cast<const float*>(x.own + kIpcRing) + size_t(slot) * x.own_slot;
+        for (const auto& p : pcs) {
+            GP_CUDA(cudaMemcpyAsync(p.ptr, src, p.floats * 4, cudaMemcpyDeviceToDevice, cs));
+            src += p.floats;
+        }
+        cu_check(g_memops.write(cs, dptr(x.peer, kIpcAck), seq, CU_STREAM_WRITE_VALUE_DEFAULT), "cuStreamWriteValue32(ack)");
+    }
+
     void send_fwd(uint32_t k) {
         account(0, k, L[len - 1].dout);
-        if (tr.down_local) post_local(tr.down_local->fwd, k, fwd_pieces(k, true));
+        if (tr.ipc_down.linked()) ipc_send(tr.ipc_down, k, fwd_pieces(k, true));
+        else if (tr.down_local) post_local(tr.down_local->fwd, k, fwd_pieces(k, true));
         else if (tr.down_comm) nccl_xfer(tr.down_comm, tr.down_stream, 1, fwd_pieces(k, true), true);
         else throw Error(GP_EFABRIC, "no downstream link");
     }
     void recv_fwd(uint32_t k) {
-        if (tr.up_local) {
+        if (tr.ipc_up.linked()) {
+            ipc_recv(tr.ipc_up, fwd_pieces(k, false));
+        } else if (tr.up_local) {
             LocalQueue::Msg m;
             wait_local(tr.up_local->fwd, k, m);
             copy_in(m, fwd_pieces(k, false));
@@ -1187,12 +1411,15 @@ struct Stage {
     }
     void send_bwd(uint32_t k) {
         account(1, k, in0);
-        if (tr.up_local) post_local(tr.up_local->bwd, k, bwd_pieces(k, true));
+        if (tr.ipc_up.linked()) ipc_send(tr.ipc_up, k, bwd_pieces(k, true));
+        else if (tr.up_local) post_local(tr.up_local->bwd, k, bwd_pieces(k, true));
         else if (tr.up_comm) nccl_xfer(tr.up_comm, tr.up_stream, 0, bwd_pieces(k, true), true);
         else throw Error(GP_EFABRIC, "no upstream link");
     }
     void recv_bwd(uint32_t k) {
-        if (tr.down_local) {
+        if (tr.ipc_down.linked()) {
+            ipc_recv(tr.ipc_down, bwd_pieces(k, false));
+        } else if (tr.down_local) {
             LocalQueue::Msg m;
             wait_local(tr.down_local->bwd, k, m);
             copy_in(m, bwd_pieces(k, false));
@@ -1453,6 +1680,11 @@ struct Stage {
 
         param_step();
         GP_CUDA(cudaEventRecord(ev_end, cs));
+        if (tr.ipc_up.linked() || tr.ipc_down.linked()) {
+            sync_watchdog(cs, 600.0);
+            for (cudaStream_t st : {tr.ipc_up.stream, tr.ipc_down.stream})
+                if (st) sync_watchdog(st, 600.0);
+        }
         GP_CUDA(cudaStreamSynchronize(cs));
         if (tr.up_stream) GP_CUDA(cudaStreamSynchronize(tr.up_stream));
         if (tr.down_stream) GP_CUDA(cudaStreamSynchronize(tr.down_stream));
@@ -1688,6 +1920,14 @@ gp_status gp_link_nccl(gp_ctx* ctx, const uint8_t* up_id, const uint8_t* down_id
             GP_CUDA(cudaStreamCreateWithFlags(&st.tr.down_stream, cudaStreamNonBlocking));
         }
     });
+}
+
+gp_status gp_ipc_export(gp_ctx* ctx, uint8_t* up_blob, uint8_t* down_blob) {
+    return gp::guard(&ctx->st, [&]() { ctx->st.ipc_export(up_blob, down_blob); });
+}
+
+gp_status gp_link_ipc(gp_ctx* ctx, const uint8_t* up_peer_blob, const uint8_t* down_peer_blob) {
+    return gp::guard(&ctx->st, [&]() { ctx->st.ipc_link(up_peer_blob, down_peer_blob); });
 }
 
 void gp_abort(gp_ctx* ctx) {

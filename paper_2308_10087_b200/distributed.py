@@ -1,8 +1,9 @@
 """One-process-per-GPU plumbing for the pipeline (launched by torchrun, one rank = one stage).
 
-The data path is the engine's own NCCL send/recv over NVLink (gp_link_nccl: one 2-rank
+The data path is the engine's own transport: CUDA-IPC peer-memory rings pushed by the copy
+engine over NVLink (gp_link_ipc, the default) or NCCL send/recv (gp_link_nccl: one 2-rank
 communicator per stage boundary). torch.distributed (gloo) is only the control plane:
-unique-id exchange, the epoch barrier and max-over-ranks timing.
+blob / unique-id exchange, the epoch barrier and max-over-ranks timing.
 
 `message_schedule` is the host-side statement of the transport order the engine follows in
 gp_run_epoch (engines_impl.hpp:784-870): it is what guarantees that every ncclSend of
@@ -11,7 +12,7 @@ yields the per-stage ledger (4 bytes per value, fabric.hpp:59).
 """
 from __future__ import annotations
 
-from typing import Callable, List, Sequence, Tuple
+from typing import Callable, List, Optional, Sequence, Tuple
 
 
 def stage_ranges(num_layers: int, num_stages: int) -> List[Tuple[int, int]]:
@@ -83,6 +84,20 @@ def boundary_ids(ids: Sequence[bytes], rank: int, world: int):
     """(up_id, down_id) of this stage: boundary b joins stage b (rank 0 of the comm) and b+1."""
     up = ids[rank - 1] if rank > 0 else None
     down = ids[rank] if rank < world - 1 else None
+    return up, down
+
+
+def exchange_ipc_blobs(dist, rank: int, world: int, mine) -> Tuple[Optional[bytes], Optional[bytes]]:
+    """All-gather every stage's (up, down) IPC blobs (StageEngine.ipc_export) and
+    return this stage's (up_peer, down_peer) for StageEngine.link_ipc: the `down`
+    blob of stage s-1 and the `up` blob of stage s+1."""
+    allb = [None] * world
+    if world > 1:
+        dist.all_gather_object(allb, tuple(mine))
+    else:
+        allb[0] = tuple(mine)
+    up = allb[rank - 1][1] if rank > 0 else None
+    down = allb[rank + 1][0] if rank < world - 1 else None
     return up, down
 
 

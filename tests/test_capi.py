@@ -65,3 +65,14 @@ def test_sass_contains_256bit_gathers():
     dev = os.path.join(ROOT, "paper_2308_10087_b200", "lib", "libgpcuda.so")
     sass = subprocess.run(["cuobjdump", "-sass", dev], capture_output=True, text=True).stdout
     assert "LDG.E.NA.ELL2.256" in sass
+
+
+def test_libraries_do_not_interpose_torch():
+    """Loading the engine before torch must not break torch (RTLD_LOCAL load)."""
+    import subprocess
+    import sys
+    code = ("import paper_2308_10087_b200 as gp; gp.device_count(); import torch.distributed as d; "
+            "import torch.fx; print('ok')")
+    r = subprocess.run([sys.executable, "-c", code], cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]

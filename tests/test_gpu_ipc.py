@@ -1,0 +1,124 @@
+"""One process per stage over the CUDA-IPC transport (gp_ipc_export / gp_link_ipc).
+
+The in-process pipeline (train_pipeline: stage threads, local D2D links) is the
+ground truth here — it is itself pinned to the reference by test_gpu_parity.py —
+and the cross-process run must reproduce it BIT-EXACTLY: the transport only moves
+rows, it never changes an operation. The box has one GPU, so all stage processes
+share device 0 (cudaIpcOpenMemHandle works between processes on one device); on an
+8-GPU node the same code pushes over NVLink.
+"""
+import os
+import socket
+import subprocess
+import sys
+import threading
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+import ipc_stage_worker as W  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def need_gpu(gp):
+    if gp.device_count() == 0:
+        pytest.fail("no CUDA device visible: GPU tests must run on the B200 box")
+
+
+def free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def in_process(gp, S, epochs):
+    ds, model, chunk_of = W.problem()
+    res = gp.train_pipeline(ds, chunk_of, S, gp.TrainOptions(model=model, epochs=epochs, seed=1))
+    x, lab, sp = ds.arrays()
+    return res, float((sp == 1).sum())
+
+
+def check_same(res, n_train, losses, params):
+    assert len(losses) == len(res.train_loss)
+    np.testing.assert_allclose(np.asarray(losses) / n_train, res.train_loss, rtol=1e-12, atol=0)
+    for l, (Wr, br) in enumerate(res.params):
+        assert np.array_equal(params[l][0].view(np.uint32), Wr.view(np.uint32)), f"W{l} differs"
+        if br.size:
+            assert np.array_equal(params[l][1].view(np.uint32), br.view(np.uint32)), f"b{l} differs"
+
+
+@pytest.mark.parametrize("S", [2, 3])
+def test_ipc_stage_processes_match_in_process_pipeline(gp, tmp_path, S):
+    epochs = 12  # crosses the fix_alpha=10 snapshot at t=11
+    out = str(tmp_path / "ipc.npz")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={S}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.join(HERE, "ipc_stage_worker.py"),
+           out, str(epochs)]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    z = np.load(out)
+    res, n_train = in_process(gp, S, epochs)
+    L = len(res.params)
+    check_same(res, n_train, z["losses"], [(z[f"W{l}"], z[f"b{l}"]) for l in range(L)])
+
+
+def test_ipc_stage_threads_same_process(gp):
+    """Same-process peers take the UVA-pointer path of gp_link_ipc (no IPC handle)."""
+    S, epochs = 2, 5
+    ds, model, chunk_of = W.problem()
+    engs = [W.stage_engine(ds, model, chunk_of, r, S, 0) for r in range(S)]
+    blobs = [e.ipc_export() for e, _ in engs]
+    engs[0][0].link_ipc(None, blobs[1][0])
+    engs[1][0].link_ipc(blobs[0][1], None)
+    losses, errs = [], []
+
+    def run(r):
+        try:
+            for t in range(1, epochs + 1):
+                st = engs[r][0].run_epoch(t, gp.shuffle_chunk_order(W.K, t, 1))
+                if st.has_quality:
+                    losses.append(st.loss_sum)
+        except Exception as e:  # surfaced below
+            errs.append(e)
+            for e2, _ in engs:
+                e2.abort()
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(S)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    assert not errs, errs
+    params = {}
+    for e, (lo, hi) in engs:
+        for l in range(lo, hi):
+            params[l] = e.get_params(l)
+    res, n_train = in_process(gp, S, epochs)
+    check_same(res, n_train, losses, params)
+    # ledger: the IPC transport accounts the same bytes as the reference fabric (4 B/value)
+    for e, _ in engs:
+        e.close()
+
+
+def test_ipc_link_errors(gp):
+    ds, model, chunk_of = W.problem()
+    specs = gp.build_layer_specs(model, W.F, W.CLASSES)
+    e0 = gp.StageEngine(num_vertices=W.N, num_chunks=W.K, specs=specs, stage=0, num_stages=2, layer_range=(0, 4),
+                        hidden=W.H, num_classes=W.CLASSES, dropout=0.5, seed=1)
+    with pytest.raises(gp.InvalidArgument, match="upload the graph"):
+        e0.ipc_export()
+    e0.close()
+    a, _ = W.stage_engine(ds, model, chunk_of, 0, 3, 0)
+    b, _ = W.stage_engine(ds, model, chunk_of, 1, 3, 0)
+    c, _ = W.stage_engine(ds, model, chunk_of, 2, 3, 0)
+    ba, bb, bc = a.ipc_export(), b.ipc_export(), c.ipc_export()
+    assert ba[0] is None and bc[1] is None and len(bb[0]) == gp.IPC_BLOB_BYTES
+    with pytest.raises(gp.InvalidArgument, match="does not face"):
+        c.link_ipc(ba[1], None)  # stage 0's blob offered to stage 2
+    with pytest.raises(gp.InvalidArgument, match="not an IPC blob"):
+        b.link_ipc(bytes(gp.IPC_BLOB_BYTES), None)
+    for e in (a, b, c):
+        e.close()
