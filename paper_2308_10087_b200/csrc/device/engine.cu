@@ -496,22 +496,33 @@ struct Stage {
 
     // Gathers in flight per lane (template NB of the row kernels); GP_NB overrides.
     int nb = 2;
+    // GP_SPLIT=1: aggregating layers run as two kernels, the latency-bound gather
+    // (-> pre / dz) and the row transform (GEMV + epilogue). Default: fused (one
+    // kernel; measured faster at Reddit shape for K = 4..32 chunks).
+    bool split_rows = false;
 
-    // Row kernels stage a weight matrix (<= 66 KB) in shared memory; gathers bypass
-    // L1 (no_allocate), so the unified L1/shared carveout goes to shared memory.
+    // Row kernels stage a weight matrix (+ x rows; <= 100 KB) in shared memory;
+    // gathers bypass L1 (no_allocate), so the unified carveout goes to shared memory.
     template <int NB>
     void setup_nb() {
-        const int smem_max = 66 * 1024;
+        const int smem_max = int(row_smem_bytes(kMaxWidth, kMaxWidth, kDenseRows));
         const void* fns[] = {(const void*)k_fwd8<FWD_DENSE, NB>,
                              (const void*)k_fwd8<FWD_GCN, NB>,
                              (const void*)k_fwd8<FWD_GCN2, NB>,
+                             (const void*)k_fwd8<FWD_GCN, NB, true>,
+                             (const void*)k_fwd8<FWD_GCN2, NB, true>,
                              (const void*)k_bwd8<PREV_TOP, OUT_LAYER, NB>,
                              (const void*)k_bwd8<PREV_AGG, OUT_LAYER, NB>,
                              (const void*)k_bwd8<PREV_AGG_HIST, OUT_LAYER, NB>,
                              (const void*)k_bwd8<PREV_OWN, OUT_LAYER, NB>,
+                             (const void*)k_bwd8<PREV_AGG, OUT_LAYER, NB, true>,
+                             (const void*)k_bwd8<PREV_AGG_HIST, OUT_LAYER, NB, true>,
                              (const void*)k_bwd8<PREV_AGG, OUT_DHIN, NB>,
                              (const void*)k_bwd8<PREV_AGG_HIST, OUT_DHIN, NB>,
-                             (const void*)k_bwd8<PREV_OWN, OUT_DHIN, NB>};
+                             (const void*)k_bwd8<PREV_OWN, OUT_DHIN, NB>,
+                             (const void*)k_fwd_dense8<false>,
+                             (const void*)k_fwd_dense8<true>,
+                             (const void*)k_bwd_dense8};
         for (const void* f : fns) {
             GP_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
             GP_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
@@ -527,39 +538,35 @@ struct Stage {
         GP_CUDA(cudaFuncSetAttribute(k_pgrad_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         if (const char* e = std::getenv("GP_NB")) {
             const int v = std::atoi(e);
-            if (v == 2 || v == 4 || v == 6 || v == 8) nb = v;
+            if (v == 2 || v == 4) nb = v;
         }
+        if (const char* e = std::getenv("GP_SPLIT")) split_rows = std::string(e) == "1";
         setup_nb<2>();
         setup_nb<4>();
-        setup_nb<6>();
-        setup_nb<8>();
     }
 
-    template <int KIND, int NB>
+    template <int KIND, int NB, bool SPLIT = false>
     void fwd_go(uint32_t rows, size_t smem, const FwdParams& p) {
-        k_fwd8<KIND, NB><<<row_grid(rows, (const void*)k_fwd8<KIND, NB>, smem, 16), kBlock, smem, cs>>>(p);
+        k_fwd8<KIND, NB, SPLIT><<<row_grid(rows, (const void*)k_fwd8<KIND, NB, SPLIT>, smem, 16), kBlock, smem, cs>>>(p);
     }
-    template <int KIND>
+    template <int KIND, bool SPLIT = false>
     void fwd_nb(uint32_t rows, size_t smem, const FwdParams& p) {
-        switch (nb) {
-            case 2: fwd_go<KIND, 2>(rows, smem, p); break;
-            case 6: fwd_go<KIND, 6>(rows, smem, p); break;
-            case 8: fwd_go<KIND, 8>(rows, smem, p); break;
-            default: fwd_go<KIND, 4>(rows, smem, p);
-        }
+        if (nb == 2) fwd_go<KIND, 2, SPLIT>(rows, smem, p);
+        else fwd_go<KIND, 4, SPLIT>(rows, smem, p);
     }
-    template <int PREV, int OUT, int NB>
+    template <bool GCN2>
+    void fwd_dense_go(uint32_t rows, size_t smem, const FwdParams& p) {
+        k_fwd_dense8<GCN2><<<row_grid(rows, (const void*)k_fwd_dense8<GCN2>, smem, 64), kBlock, smem, cs>>>(p);
+    }
+    template <int PREV, int OUT, int NB, bool SPLIT = false>
     void bwd_go(uint32_t rows, size_t smem, const BwdParams& p) {
-        k_bwd8<PREV, OUT, NB><<<row_grid(rows, (const void*)k_bwd8<PREV, OUT, NB>, smem, 16), kBlock, smem, cs>>>(p);
+        k_bwd8<PREV, OUT, NB, SPLIT>
+            <<<row_grid(rows, (const void*)k_bwd8<PREV, OUT, NB, SPLIT>, smem, 16), kBlock, smem, cs>>>(p);
     }
-    template <int PREV, int OUT>
+    template <int PREV, int OUT, bool SPLIT = false>
     void bwd_nb(uint32_t rows, size_t smem, const BwdParams& p) {
-        switch (nb) {
-            case 2: bwd_go<PREV, OUT, 2>(rows, smem, p); break;
-            case 6: bwd_go<PREV, OUT, 6>(rows, smem, p); break;
-            case 8: bwd_go<PREV, OUT, 8>(rows, smem, p); break;
-            default: bwd_go<PREV, OUT, 4>(rows, smem, p);
-        }
+        if (nb == 2) bwd_go<PREV, OUT, 2, SPLIT>(rows, smem, p);
+        else bwd_go<PREV, OUT, 4, SPLIT>(rows, smem, p);
     }
 
     // ---- graph --------------------------------------------------------------
@@ -895,7 +902,7 @@ struct Stage {
             p.gnext = gnext;
             p.gnstride = gnstride;
             p.next_mask = nk;
-            const size_t smem = (size_t(d.din) + 1) * ((d.dout + 7) / 8) * 32;
+            const size_t smem = row_smem_bytes(d.din, d.dout, 2);
             const double e = d.agg ? double(rowptr_nnz(r0, r1)) : 0.0;
             const double bytes = (d.agg ? e * 8.0 + double(rows + 1) * 8.0 + double(n) * d.din * 4.0
                                         : double(rows) * d.din * 4.0) +
@@ -905,6 +912,24 @@ struct Stage {
             const double flops = 2.0 * e * d.din + 2.0 * double(rows) * d.din * d.dout;
             const double gather = e * double(d.sin) * 4.0;
             const int cls = d.agg ? GP_K_FWD_AGG : GP_K_FWD_DENSE;
+            if (d.agg && split_rows) {
+                // gather + initial-residual mix -> pre, then b + pre.W + epilogue
+                const bool g2 = d.spec.kind == GP_GCN2CONV;
+                const double eb = e * 8.0 + double(rows + 1) * 8.0 + double(n) * d.din * 4.0 +
+                                  double(rows) * d.din * 4.0 * (g2 ? 2.0 : 1.0);
+                const double db = double(rows) * (d.din + d.dout + (gnext ? d.dout : 0)) * 4.0 +
+                                  double(d.din) * d.dout * 4.0;
+                launch(GP_K_FWD_AGG, eb, 2.0 * e * d.din, gather, [&]() {
+                    if (g2) fwd_nb<FWD_GCN2, true>(rows, 0, p);
+                    else fwd_nb<FWD_GCN, true>(rows, 0, p);
+                });
+                const size_t dsm = row_smem_bytes(d.din, d.dout, kDenseRows);
+                launch(GP_K_FWD_DENSE, db, 2.0 * double(rows) * d.din * d.dout, 0, [&]() {
+                    if (g2) fwd_dense_go<true>(rows, dsm, p);
+                    else fwd_dense_go<false>(rows, dsm, p);
+                });
+                return;
+            }
             if (d.spec.kind == GP_DENSE)
                 launch(cls, bytes, flops, 0, [&]() { fwd_nb<FWD_DENSE>(rows, smem, p); });
             else if (d.spec.kind == GP_GCNCONV)
@@ -1011,13 +1036,30 @@ struct Stage {
         p.dh0 = dh0;
         p.bg = d.bg;
         p.bgstride = d.sin;
-        const size_t smem = p.need_dagg ? size_t(d.dout) * ((d.din + 7) / 8) * 32 : 0;
+        const size_t smem = p.need_dagg ? row_smem_bytes(d.dout, d.din, 2) : 0;
         const double bytes = e * 8.0 + (e > 0 ? double(n) * d.dout * 4.0 : double(rows) * d.dout * 4.0) +
                              double(rows) * d.dout * 8.0 + (p.need_dagg ? double(rows) * d.din * 4.0 : 0.0) +
                              (p.gcn2 ? double(rows) * d.din * 8.0 : 0.0);
         const double flops = 2.0 * e * d.dout + (p.need_dagg ? 2.0 * double(rows) * d.din * d.dout : 0.0);
         const double gather = e * double(pad8(d.dout)) * 4.0;
         const int cls = prev == PREV_AGG || prev == PREV_AGG_HIST ? GP_K_BWD_AGG : GP_K_BWD_DENSE;
+        if (split_rows && cls == GP_K_BWD_AGG) {
+            // gather (+ mask, dh0 term, ReLU) -> dz, then dz.W^T + mixes -> bg, dh0
+            const double ab = e * 8.0 + double(n) * d.dout * 4.0 + double(rows) * d.dout * 8.0;
+            launch(GP_K_BWD_AGG, ab, 2.0 * e * d.dout, gather, [&]() {
+                if (prev == PREV_AGG) bwd_nb<PREV_AGG, OUT_LAYER, true>(rows, 0, p);
+                else bwd_nb<PREV_AGG_HIST, OUT_LAYER, true>(rows, 0, p);
+            });
+            if (p.need_dagg) {
+                const double db = double(rows) * (d.dout + d.din) * 4.0 + (p.gcn2 ? double(rows) * d.din * 8.0 : 0.0) +
+                                  double(d.din) * d.dout * 4.0;
+                const size_t dsm = row_smem_bytes(d.dout, d.din, kDenseRows);
+                launch(GP_K_BWD_DENSE, db, 2.0 * double(rows) * d.din * d.dout, 0, [&]() {
+                    k_bwd_dense8<<<row_grid(rows, (const void*)k_bwd_dense8, dsm, 64), kBlock, dsm, cs>>>(p);
+                });
+            }
+            return;
+        }
         switch (prev) {
             case PREV_TOP:
                 launch(cls, bytes, flops, 0, [&]() { bwd_nb<PREV_TOP, OUT_LAYER>(rows, smem, p); });

@@ -68,12 +68,21 @@ __device__ __forceinline__ F8 shfl8(const F8& x, int src) {
     return r;
 }
 
-// NB = gathers in flight per lane (x 2 rows per warp), a template parameter.
-
-// Sum over the CSR row of w * src[col] (8 columns per lane). FILTER drops
-// entries of not-yet-done chunks (stable ballot compaction per 16-entry batch);
-// HIST reads those from `snap` instead. Padding slots use weight 0 and keep the
-// previous registers: acc starts at +0 and never becomes -0, so acc + 0*x == acc.
+// Sum over the CSR row of w * src[col] (8 columns per lane), in ascending entry
+// order with one rounded multiply and add per term.
+//
+// Entries are consumed in full batches of 16 per half-warp whose 16 gathers are
+// fully unrolled (NB issued per group), so the compiler can keep loads of later
+// groups in flight under the arithmetic of earlier ones; the CSR batch after the
+// current one is prefetched. Unused slots are padding: the half's own row with
+// weight 0 (acc starts at +0 and never becomes -0, so acc + 0*x == acc, and the
+// address is always valid, so there is no predication on the loads).
+//
+// FILTER keeps only entries of done chunks: each CSR batch is compacted (ballot +
+// __fns, order-preserving) and appended to a per-half queue of up to 15 carried
+// entries; a batch of 16 is gathered as soon as either half's queue is full, so
+// sparse done-sets do not pay for padded slots. HIST (historical-gradient
+// ablation) keeps every entry and reads not-done chunks from `snap`.
 template <bool FILTER, bool HIST, int NB>
 __device__ __forceinline__ F8 gather_row8(const uint64_t* __restrict__ rowptr, const uint2* __restrict__ edges,
                                           uint32_t v, bool has_row, const float* __restrict__ src,
@@ -90,96 +99,195 @@ __device__ __forceinline__ F8 gather_row8(const uint64_t* __restrict__ rowptr, c
     const uint32_t loff = active ? 8u * hl : 0u;
     const float* ls = src + loff;
     const float* lsn = HIST ? snap + loff : nullptr;
-    // padding slots re-read this half's own row (the self-loop row: distinct per
-    // half-warp, so padding never concentrates on one L2 line)
-    const float* lpad = ls + size_t(has_row ? v : 0u) * stride;
+    // padding entry: this half's own row (distinct per half-warp, so padding never
+    // concentrates on one L2 line), weight 0, chunk bits 0
+    const uint2 pad = make_uint2(has_row ? v : 0u, 0u);
     F8 acc = f8_zero();
-    // CSR batch of the next iteration is loaded one batch ahead
-    uint2 nxt = hl < int(min(16u, n_my)) ? ld_edge(edges + e0 + hl) : make_uint2(0u, 0u);
-    for (uint32_t off = 0; off < n_max; off += 16) {
-        int cnt = n_my > off ? int(min(16u, n_my - off)) : 0;
-        uint2 my = nxt;
-        {
-            const uint32_t noff = off + 16;
-            const int ncnt = n_my > noff ? int(min(16u, n_my - noff)) : 0;
-            nxt = hl < ncnt ? ld_edge(edges + e0 + noff + hl) : make_uint2(0u, 0u);
-        }
-        if (FILTER && !HIST) {
-            const bool ok = hl < cnt && ((done >> (my.x >> kColBits)) & 1ull);
-            const unsigned m = (__ballot_sync(kFull, ok) >> hb) & 0xffffu;
-            cnt = __popc(m);
-            const int from = hl < cnt ? int(__fns(m, 0, hl + 1)) : 0;
-            my.x = __shfl_sync(kFull, my.x, hb + from);
-            my.y = __shfl_sync(kFull, my.y, hb + from);
-        }
-        const int cmax = max(cnt, __shfl_xor_sync(kFull, cnt, 16));
-        for (int t = 0; t < cmax; t += NB) {
+    auto batch16 = [&](const uint2 my) {
+#pragma unroll
+        for (int t = 0; t < 16; t += NB) {
             float w[NB];
             F8 x[NB];
 #pragma unroll
             for (int i = 0; i < NB; ++i) {
-                const int tt = t + i;
-                const int sl = hb + (tt & 15);
-                const uint32_t packed = __shfl_sync(kFull, my.x, sl);
-                const float wv = __uint_as_float(__shfl_sync(kFull, my.y, sl));
-                const bool valid = tt < cnt;
+                const uint32_t packed = __shfl_sync(kFull, my.x, hb + t + i);
+                w[i] = __uint_as_float(__shfl_sync(kFull, my.y, hb + t + i));
                 const float* s = ls;
                 if (HIST && !((done >> (packed >> kColBits)) & 1ull)) s = lsn;
-                w[i] = valid ? wv : 0.f;
-                x[i] = ld8_gather(valid ? s + size_t(packed & kColMask) * stride : lpad);
+                x[i] = ld8_gather(s + size_t(packed & kColMask) * stride);
             }
 #pragma unroll
             for (int i = 0; i < NB; ++i)
 #pragma unroll
                 for (int c = 0; c < 8; ++c) acc.v[c] = mul_add(acc.v[c], w[i], x[i].v[c]);
         }
+    };
+    uint2 nxt = hl < int(n_my) ? ld_edge(edges + e0 + hl) : pad;
+    if (!FILTER || HIST) {
+        for (uint32_t off = 0; off < n_max; off += 16) {
+            const uint2 my = nxt;
+            nxt = off + 16 + hl < n_my ? ld_edge(edges + e0 + off + 16 + hl) : pad;
+            batch16(my);
+        }
+        return acc;
     }
+    uint2 carry = pad;  // queued (compacted) entries in lanes [0, nq)
+    int nq = 0;
+    for (uint32_t off = 0; off < n_max; off += 16) {
+        uint2 e = nxt;
+        const bool ok = off + hl < n_my && ((done >> (e.x >> kColBits)) & 1ull);
+        nxt = off + 16 + hl < n_my ? ld_edge(edges + e0 + off + 16 + hl) : pad;
+        const unsigned m = (__ballot_sync(kFull, ok) >> hb) & 0xffffu;
+        const int cnt = __popc(m);
+        // compact the batch, then append it behind the queue: lane hl takes
+        // queue[hl] if hl < nq, else new[hl - nq]
+        const int from = hl < cnt ? int(__fns(m, 0, hl + 1)) : hl;
+        e.x = __shfl_sync(kFull, e.x, hb + from);
+        e.y = __shfl_sync(kFull, e.y, hb + from);
+        const int j = hl - nq;
+        const uint32_t ax = __shfl_sync(kFull, e.x, hb + (j < 0 ? 0 : j));
+        const uint32_t ay = __shfl_sync(kFull, e.y, hb + (j < 0 ? 0 : j));
+        const int tot = nq + cnt;
+        const uint2 cur = j < 0 ? carry : (j < cnt ? make_uint2(ax, ay) : pad);
+        const int tmax = max(tot, __shfl_xor_sync(kFull, tot, 16));
+        if (tmax >= 16) {
+            batch16(cur);
+            // entries of the new batch beyond this 16-slot batch stay queued
+            const int k = 16 - nq + hl;
+            const uint32_t rx = __shfl_sync(kFull, e.x, hb + (k < 16 ? k : 15));
+            const uint32_t ry = __shfl_sync(kFull, e.y, hb + (k < 16 ? k : 15));
+            nq = tot > 16 ? tot - 16 : 0;
+            carry = hl < nq ? make_uint2(rx, ry) : pad;
+        } else {
+            carry = cur;
+            nq = tot;
+        }
+    }
+    if (__shfl_xor_sync(kFull, nq, 16) + nq > 0) batch16(carry);
     return acc;
 }
 
-// Weight staging: row i of an (rows x cols) matrix is stored as 2*cols8 float4
-// slots, slot (part, h) = part * cols8 + h holding columns 8h+4part..8h+4part+3,
-// so the two LDS.128 of a half-warp are each 256 contiguous bytes.
-__device__ __forceinline__ void stage_w8(float* Ws, const float* W, uint32_t rows, uint32_t cols, bool transpose,
-                                         uint32_t ld) {
-    const uint32_t c8 = (cols + 7) / 8;
-    for (uint32_t idx = threadIdx.x; idx < rows * c8 * 8; idx += blockDim.x) {
-        const uint32_t r = idx / (c8 * 8), c = idx % (c8 * 8);
-        const uint32_t h = c / 8, part = (c % 8) / 4, q = c % 4;
+// ---------------------------------------------------------------------------
+// Row transforms (dense_rows matrix.hpp:63-74, dense_rows_wt :77-86) as warp
+// GEMVs over R rows at once: lane L owns output columns L, L+32, L+64, L+96 of
+// all R rows. Per input index i the warp reads the staged matrix row i once
+// (consecutive lanes, consecutive words: conflict-free, ~4 wavefronts per row
+// instead of the 13-15 of a half-warp-per-row layout) and x[.][i] of the R rows by
+// broadcast from a [i][R] staging area. Each output still accumulates one rounded
+// product per i in ascending i, so results are bit-identical to the reference.
+// ---------------------------------------------------------------------------
+// Matrix staging: rows x cols, row stride ms = pad8(cols) words, + 32 words of
+// tail padding (lanes whose 4th column is past `cols` read padding or the next row
+// and discard it). transpose: Ms[r][c] = W[c][r] (W has leading dimension ld).
+__host__ __device__ constexpr uint32_t mat_stride(uint32_t cols) { return (cols + 7u) & ~7u; }
+__host__ __device__ constexpr size_t row_smem_bytes(uint32_t mrows, uint32_t mcols, uint32_t R) {
+    // matrix + tail pad + bias (128) + x staging (8 warps x 128 x R)
+    return (size_t(mrows) * mat_stride(mcols) + 32 + 128 + size_t(kWarpsPerBlock) * 128 * R) * 4;
+}
+
+__device__ __forceinline__ void stage_mat(float* Ms, const float* W, uint32_t rows, uint32_t cols, bool transpose,
+                                          uint32_t ld) {
+    const uint32_t ms = mat_stride(cols);
+    for (uint32_t idx = threadIdx.x; idx < rows * ms + 32; idx += blockDim.x) {
+        const uint32_t r = idx / ms, c = idx % ms;
         float val = 0.f;
-        if (c < cols) val = transpose ? W[size_t(c) * ld + r] : W[size_t(r) * ld + c];
-        Ws[(size_t(r) * 2 * c8 + part * c8 + h) * 4 + q] = val;
+        if (r < rows && c < cols) val = transpose ? W[size_t(c) * ld + r] : W[size_t(r) * ld + c];
+        Ms[idx] = val;
     }
 }
 
-__device__ __forceinline__ void w8_row(const float4* Ws4, uint32_t r, uint32_t c8, int hl, float4& a, float4& b) {
-    a = Ws4[size_t(r) * 2 * c8 + hl];
-    b = Ws4[size_t(r) * 2 * c8 + c8 + hl];
+template <int R>
+__device__ __forceinline__ void gemv_w(float (&o)[R][4], const float* __restrict__ xs, const float* __restrict__ Ms,
+                                       uint32_t rows, uint32_t ms, int lane) {
+    const float* mcol = Ms + lane;
+#pragma unroll 2
+    for (uint32_t i = 0; i < rows; ++i) {
+        float x[R];
+        if (R == 2) {
+            const float2 t = *reinterpret_cast<const float2*>(xs + 2 * i);
+            x[0] = t.x;
+            x[1] = t.y;
+        } else {
+#pragma unroll
+            for (int q = 0; q < R / 4; ++q) {
+                const float4 t = *reinterpret_cast<const float4*>(xs + R * i + 4 * q);
+                x[4 * q] = t.x, x[4 * q + 1] = t.y, x[4 * q + 2] = t.z, x[4 * q + 3] = t.w;
+            }
+        }
+        const float* mrow = mcol + size_t(i) * ms;
+        const float w0 = mrow[0], w1 = mrow[32], w2 = mrow[64], w3 = mrow[96];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            o[r][0] = mul_add(o[r][0], x[r], w0);
+            o[r][1] = mul_add(o[r][1], x[r], w1);
+            o[r][2] = mul_add(o[r][2], x[r], w2);
+            o[r][3] = mul_add(o[r][3], x[r], w3);
+        }
+    }
 }
 
-// Row-local GEMV: o[c] += sum_i x_i * M[i][c] over i ascending (x held 8 per
-// lane across the half-warp), one rounded mul and add per term.
-__device__ __forceinline__ void gemv8(F8& o, const F8& x, const float4* Ws4, uint32_t rows, uint32_t c8, int hl,
-                                      int hb) {
-    const uint32_t r8 = (rows + 7) / 8;
-    for (uint32_t ib = 0; ib < r8; ++ib) {
-        const F8 xb = shfl8(x, hb + int(ib));
+// Stage the warp's two half-warp rows (8 values per lane) as xs[i][2].
+__device__ __forceinline__ void stage_x2(float* xs, const F8& x, int hl, int hb, bool active) {
+    if (active) {
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            const uint32_t i = 8 * ib + q;
-            if (i < rows) {
-                float4 a, b;
-                w8_row(Ws4, i, c8, hl, a, b);
-                const float xi = xb.v[q];
-                o.v[0] = mul_add(o.v[0], xi, a.x);
-                o.v[1] = mul_add(o.v[1], xi, a.y);
-                o.v[2] = mul_add(o.v[2], xi, a.z);
-                o.v[3] = mul_add(o.v[3], xi, a.w);
-                o.v[4] = mul_add(o.v[4], xi, b.x);
-                o.v[5] = mul_add(o.v[5], xi, b.y);
-                o.v[6] = mul_add(o.v[6], xi, b.z);
-                o.v[7] = mul_add(o.v[7], xi, b.w);
+        for (int c = 0; c < 8; ++c) xs[(8 * hl + c) * 2 + (hb ? 1 : 0)] = x.v[c];
+    }
+    __syncwarp();
+}
+
+__device__ __forceinline__ void st1_stream(float* p, float v, uint64_t pol) {
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(p), "f"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ float ld1_stream(const float* p, uint64_t pol) {
+    float v;
+    asm volatile("ld.global.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+    return v;
+}
+
+// Forward epilogue of row v for the lane's columns: (Gcn2Conv) identity mix with
+// pre, ReLU, h, and the next layer's dropped gather source (nn.hpp:188-196).
+template <int R, bool GCN2>
+__device__ __forceinline__ void fwd_epilogue(const FwdParams& p, float (&o)[R][4], const float* xs, uint32_t v0,
+                                             int lane, uint64_t pol) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const uint32_t v = v0 + r;
+        if (v >= p.r1) break;
+        const uint32_t vo = p.gnext ? p.orig[v] : 0u;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t c = lane + 32 * k;
+            if (c >= p.dout) break;
+            float val = o[r][k];
+            if (GCN2) val = __fadd_rn(__fmul_rn(p.omb, xs[c * R + r]), __fmul_rn(p.beta, val));
+            if (p.relu && val < 0.f) val = 0.f;
+            st1_stream(p.out + size_t(v) * p.outstride + c, val, pol);
+            if (p.gnext) st1_stream(p.gnext + size_t(v) * p.gnstride + c, drop_apply(p.next_mask, vo, c, val), pol);
+        }
+    }
+}
+
+// Backward transform of row u: dagg = dz.W^T (R rows in o), Gcn2Conv mixes,
+// dh0 += a*dagg, bg = (1-a)*dagg or dagg (nn.hpp:202-218).
+template <int R>
+__device__ __forceinline__ void bwd_epilogue(const BwdParams& p, float (&g)[R][4], const float* xs, uint32_t u0,
+                                             int lane, uint64_t pol) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const uint32_t u = u0 + r;
+        if (u >= p.r1) break;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t c = lane + 32 * k;
+            if (c >= p.din) break;
+            float val = g[r][k];
+            if (p.gcn2) {
+                float* d0 = p.dh0 + size_t(u) * p.dh0stride + c;
+                val = __fadd_rn(__fmul_rn(p.omb, xs[c * R + r]), __fmul_rn(p.beta, val));
+                st1_stream(d0, __fadd_rn(ld1_stream(d0, pol), __fmul_rn(p.alpha, val)), pol);
+                val = __fmul_rn(p.oma, val);
             }
+            st1_stream(p.bg + size_t(u) * p.bgstride + c, val, pol);
         }
     }
 }
@@ -189,26 +297,24 @@ __device__ __forceinline__ void gemv8(F8& o, const F8& x, const float4* Ws4, uin
 // gather (or dropped own row for Dense) -> GCNII initial-residual mix -> pre ->
 // b + pre.W (the reference's exact-zero skip is an identity here: pre is never
 // -0 and x*W = +-0 leaves a non -0 accumulator unchanged) -> identity mix ->
-// ReLU -> h, and the next layer's dropped gather source.
+// ReLU -> h, and the next layer's dropped gather source. SPLIT: stop at pre
+// (k_fwd_dense8 does the transform).
 // ---------------------------------------------------------------------------
-template <int KIND, int NB>
+template <int KIND, int NB, bool SPLIT = false>
 __global__ void __launch_bounds__(kBlock, NB == 2 ? 4 : (NB == 4 ? 3 : 2)) k_fwd8(FwdParams p) {
     extern __shared__ float4 smem4[];
-    const uint32_t c8 = (p.dout + 7) / 8;
-    float* Ws = reinterpret_cast<float*>(smem4);
-    stage_w8(Ws, p.W, p.din, p.dout, false, p.dout);
-    float* bs = Ws + size_t(p.din) * c8 * 8;
-    for (uint32_t c = threadIdx.x; c < c8 * 8; c += blockDim.x) {
-        const uint32_t h = c / 8, part = (c % 8) / 4, q = c % 4;
-        bs[(part * c8 + h) * 4 + q] = (p.bias && c < p.dout) ? p.bias[c] : 0.f;
+    const uint32_t ms = mat_stride(p.dout);
+    float* Ms = reinterpret_cast<float*>(smem4);
+    float* bs = Ms + size_t(p.din) * ms + 32;
+    float* xs = bs + 128 + (threadIdx.x / 32) * 256;
+    if (!SPLIT) {
+        stage_mat(Ms, p.W, p.din, p.dout, false, p.dout);
+        for (uint32_t c = threadIdx.x; c < 128; c += blockDim.x) bs[c] = (p.bias && c < p.dout) ? p.bias[c] : 0.f;
+        __syncthreads();
     }
-    __syncthreads();
-    const float4* Ws4 = reinterpret_cast<const float4*>(Ws);
-    const float4* bs4 = reinterpret_cast<const float4*>(bs);
-
+    const uint64_t pol = evict_first_policy();
     const int lane = threadIdx.x & 31, hl = lane & 15, hb = lane & 16;
     const bool in_act = uint32_t(8 * hl) < p.din;
-    const bool out_act = uint32_t(8 * hl) < p.dout;
     for (;;) {
         // dynamic row-pair scheduling: no static tail across a ~6-pair-per-warp launch
         uint32_t pair = 0;
@@ -234,28 +340,54 @@ __global__ void __launch_bounds__(kBlock, NB == 2 ? 4 : (NB == 4 ? 3 : 2)) k_fwd
             }
         }
         if (has && in_act) st8_stream(p.pre + size_t(v) * p.prestride + 8 * hl, pre);
+        if (SPLIT) continue;  // transform + epilogue in k_fwd_dense8
 
-        F8 o;
-        {
-            const float4 a = bs4[hl < int(c8) ? hl : 0], b = bs4[c8 + (hl < int(c8) ? hl : 0)];
-            o.v[0] = a.x, o.v[1] = a.y, o.v[2] = a.z, o.v[3] = a.w;
-            o.v[4] = b.x, o.v[5] = b.y, o.v[6] = b.z, o.v[7] = b.w;
-        }
-        gemv8(o, pre, Ws4, p.din, c8, hl < int(c8) ? hl : 0, hb);
-        if (KIND == FWD_GCN2) {
+        stage_x2(xs, pre, hl, hb, in_act);
+        float o[2][4];
 #pragma unroll
-            for (int c = 0; c < 8; ++c) o.v[c] = __fadd_rn(__fmul_rn(p.omb, pre.v[c]), __fmul_rn(p.beta, o.v[c]));
+        for (int k = 0; k < 4; ++k) o[0][k] = o[1][k] = bs[(lane + 32 * k) & 127];
+        gemv_w<2>(o, xs, Ms, p.din, ms, lane);
+        fwd_epilogue<2, KIND == FWD_GCN2>(p, o, xs, base, lane, pol);
+        __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Row transform + epilogue of a split forward (k_fwd8<KIND, NB, true> wrote pre),
+// 8 rows per warp: the gather kernel stays a pure latency-bound stream and this
+// one is a short FMA-issue-bound pass (pre is read back from L2).
+// ---------------------------------------------------------------------------
+constexpr int kDenseRows = 8;
+
+template <bool GCN2>
+__global__ void __launch_bounds__(kBlock, 3) k_fwd_dense8(FwdParams p) {
+    extern __shared__ float4 smem4[];
+    const uint32_t ms = mat_stride(p.dout);
+    float* Ms = reinterpret_cast<float*>(smem4);
+    float* bs = Ms + size_t(p.din) * ms + 32;
+    float* xs = bs + 128 + (threadIdx.x / 32) * 128 * kDenseRows;
+    stage_mat(Ms, p.W, p.din, p.dout, false, p.dout);
+    for (uint32_t c = threadIdx.x; c < 128; c += blockDim.x) bs[c] = (p.bias && c < p.dout) ? p.bias[c] : 0.f;
+    __syncthreads();
+    const uint64_t pol = evict_first_policy();
+    const int lane = threadIdx.x & 31;
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t v0 = p.r0 + kDenseRows * ((blockIdx.x * blockDim.x + threadIdx.x) >> 5); v0 < p.r1;
+         v0 += kDenseRows * nw) {
+        // stage 8 pre rows as xs[i][8]
+        for (uint32_t idx = lane; idx < kDenseRows * p.din; idx += 32) {
+            const uint32_t r = idx / p.din, i = idx % p.din;
+            xs[i * kDenseRows + r] = v0 + r < p.r1 ? ld1_stream(p.pre + size_t(v0 + r) * p.prestride + i, pol) : 0.f;
         }
-        if (p.relu) {
+        __syncwarp();
+        float o[kDenseRows][4];
 #pragma unroll
-            for (int c = 0; c < 8; ++c)
-                if (o.v[c] < 0.f) o.v[c] = 0.f;
-        }
-        if (has && out_act) {
-            st8_stream(p.out + size_t(v) * p.outstride + 8 * hl, o);
-            if (p.gnext)
-                st8_stream(p.gnext + size_t(v) * p.gnstride + 8 * hl, drop8(p.next_mask, p.orig[v], 8 * hl, p.dout, o));
-        }
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int r = 0; r < kDenseRows; ++r) o[r][k] = bs[(lane + 32 * k) & 127];
+        gemv_w<kDenseRows>(o, xs, Ms, p.din, ms, lane);
+        fwd_epilogue<kDenseRows, GCN2>(p, o, xs, v0, lane, pol);
+        __syncwarp();
     }
 }
 
@@ -264,21 +396,21 @@ __global__ void __launch_bounds__(kBlock, NB == 2 ? 4 : (NB == 4 ? 3 : 2)) k_fwd
 // gradient of layer i (dtop | drop_{i+1}(A_hat . bg_{i+1}) over done chunks |
 // drop_{i+1}(bg_{i+1}[u])) (+ dh0 at global layer 0), then backward_out_row of
 // layer i (nn.hpp:202-218): dz, dagg = dz.W^T, GCNII mixes, dh0 += a*dagg, and
-// bg_i = (1-a)*dagg (Gcn2Conv) or dagg.
+// bg_i = (1-a)*dagg (Gcn2Conv) or dagg. SPLIT: stop at dz (k_bwd_dense8).
 // ---------------------------------------------------------------------------
-template <int PREV, int OUT, int NB>
+template <int PREV, int OUT, int NB, bool SPLIT = false>
 __global__ void __launch_bounds__(kBlock, NB == 2 ? 4 : (NB == 4 ? 3 : 2)) k_bwd8(BwdParams p) {
     extern __shared__ float4 smem4[];
-    float* Wt = reinterpret_cast<float*>(smem4);
-    const uint32_t c8 = (p.din + 7) / 8;
-    if (OUT == OUT_LAYER && p.need_dagg) {
-        stage_w8(Wt, p.W, p.dout, p.din, true, p.dout);  // Wt[j][c] = W[c][j]
+    const uint32_t ms = mat_stride(p.din);
+    float* Ms = reinterpret_cast<float*>(smem4);
+    float* xs = Ms + size_t(p.dout) * ms + 32 + 128 + (threadIdx.x / 32) * 256;
+    if (!SPLIT && OUT == OUT_LAYER && p.need_dagg) {
+        stage_mat(Ms, p.W, p.dout, p.din, true, p.dout);  // Ms[j][c] = W[c][j]
         __syncthreads();
     }
-    const float4* Wt4 = reinterpret_cast<const float4*>(Wt);
+    const uint64_t pol = evict_first_policy();
     const int lane = threadIdx.x & 31, hl = lane & 15, hb = lane & 16;
     const bool dh_act = uint32_t(8 * hl) < p.dh_width;
-    const bool in_act = uint32_t(8 * hl) < p.din;
     for (;;) {
         // dynamic row-pair scheduling: no static tail across a ~6-pair-per-warp launch
         uint32_t pair = 0;
@@ -316,22 +448,44 @@ __global__ void __launch_bounds__(kBlock, NB == 2 ? 4 : (NB == 4 ? 3 : 2)) k_bwd
             for (int c = 0; c < 8; ++c) dz.v[c] = h.v[c] > 0.f ? dh.v[c] : 0.f;
         }
         if (has && dh_act) st8_stream(p.dz + size_t(u) * p.dzstride + 8 * hl, dz);
-        if (!p.need_dagg) continue;
-        F8 g = f8_zero();
-        gemv8(g, dz, Wt4, p.dout, c8, hl < int(c8) ? hl : 0, hb);
-        if (!(has && in_act)) continue;
-        if (p.gcn2) {
-            float* d0 = p.dh0 + size_t(u) * p.dh0stride + 8 * hl;
-            F8 a = ld8_stream(d0);
+        if (SPLIT || !p.need_dagg) continue;  // dz.W^T in k_bwd_dense8
+        stage_x2(xs, dz, hl, hb, dh_act);
+        float g[2][4];
 #pragma unroll
-            for (int c = 0; c < 8; ++c) {
-                g.v[c] = __fadd_rn(__fmul_rn(p.omb, dz.v[c]), __fmul_rn(p.beta, g.v[c]));
-                a.v[c] = __fadd_rn(a.v[c], __fmul_rn(p.alpha, g.v[c]));
-                g.v[c] = __fmul_rn(p.oma, g.v[c]);
-            }
-            st8_stream(d0, a);
+        for (int k = 0; k < 4; ++k) g[0][k] = g[1][k] = 0.f;
+        gemv_w<2>(g, xs, Ms, p.dout, ms, lane);
+        bwd_epilogue<2>(p, g, xs, base, lane, pol);
+        __syncwarp();
+    }
+}
+
+// Transform half of a split backward step (k_bwd8<PREV, OUT_LAYER, NB, true>
+// wrote dz), 8 rows per warp.
+__global__ void __launch_bounds__(kBlock, 3) k_bwd_dense8(BwdParams p) {
+    extern __shared__ float4 smem4[];
+    const uint32_t ms = mat_stride(p.din);
+    float* Ms = reinterpret_cast<float*>(smem4);
+    float* xs = Ms + size_t(p.dout) * ms + 32 + 128 + (threadIdx.x / 32) * 128 * kDenseRows;
+    stage_mat(Ms, p.W, p.dout, p.din, true, p.dout);  // Ms[j][c] = W[c][j]
+    __syncthreads();
+    const uint64_t pol = evict_first_policy();
+    const int lane = threadIdx.x & 31;
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t u0 = p.r0 + kDenseRows * ((blockIdx.x * blockDim.x + threadIdx.x) >> 5); u0 < p.r1;
+         u0 += kDenseRows * nw) {
+        for (uint32_t idx = lane; idx < kDenseRows * p.dout; idx += 32) {
+            const uint32_t r = idx / p.dout, j = idx % p.dout;
+            xs[j * kDenseRows + r] = u0 + r < p.r1 ? ld1_stream(p.dz + size_t(u0 + r) * p.dzstride + j, pol) : 0.f;
         }
-        st8_stream(p.bg + size_t(u) * p.bgstride + 8 * hl, g);
+        __syncwarp();
+        float g[kDenseRows][4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int r = 0; r < kDenseRows; ++r) g[r][k] = 0.f;
+        gemv_w<kDenseRows>(g, xs, Ms, p.dout, ms, lane);
+        bwd_epilogue<kDenseRows>(p, g, xs, u0, lane, pol);
+        __syncwarp();
     }
 }
 

@@ -34,7 +34,15 @@ __global__ void gather8(const float* __restrict__ tab, const unsigned* __restric
     if (acc == 1234.5f) out[0] = acc;
 }
 
-int main() {
+__global__ void fill_rand(float* p, size_t n) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        unsigned long long z = i * 0x9E3779B97F4A7C15ull;
+        z = (z ^ (z >> 31)) * 0xBF58476D1CE4E5B9ull;
+        p[i] = (float)(z >> 40) * (1.0f / 16777216.0f) - 0.5f;
+    }
+}
+
+int main(int argc, char** argv) {
     int nsm; cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
     const long nidx = 114818775;
     float* out; cudaMalloc(&out, 4);
@@ -46,6 +54,7 @@ int main() {
     for (long i = 0; i < nidx; ++i) { s ^= s << 13; s ^= s >> 7; s ^= s << 17; h[i] = s % N; }
     cudaMemcpy(idx, h.data(), nidx * 4, cudaMemcpyHostToDevice);
     float* tab; cudaMalloc(&tab, (size_t)(N + 1) * stride * 4); cudaMemset(tab, 0, (size_t)(N + 1) * stride * 4);
+    if (argc > 1) { fill_rand<<<1184, 256>>>(tab, (size_t)(N + 1) * stride); cudaDeviceSynchronize(); printf("random table\n"); }
     const double gb = (double)nidx * stride * 4 / 1e9;
     auto run = [&](auto kern, const char* name, int occ) {
         float ms = 0;
@@ -55,7 +64,7 @@ int main() {
         }
         printf("v8 %s occ=%d : %.3f ms  %.0f GB/s\n", name, occ, ms, gb / ms * 1e3);
     };
-    for (int occ : {2, 3, 4, 6, 8}) {
+    for (int occ : {4}) {
         run(gather8<2>, "NB2", occ);
         run(gather8<4>, "NB4", occ);
         run(gather8<8>, "NB8", occ);
