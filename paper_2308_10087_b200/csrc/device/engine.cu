@@ -609,11 +609,22 @@ struct Stage {
         std::vector<uint32_t> cur(size_t(G) * KB);
         for (uint32_t r = 0; r < G; ++r)
             for (uint32_t k = 0; k < K; ++k) cur[size_t(r) * KB + k] = h->bstart[size_t(r) * KB + k];
-        for (uint32_t v = 0; v < n; ++v) {
-            const uint32_t r = cur[size_t(partof(v)) * KB + chunk_of[v]]++;
-            perm[v] = r;
-            inv[r] = v;
+        for (uint32_t v = 0; v < n; ++v) inv[cur[size_t(partof(v)) * KB + chunk_of[v]]++] = v;
+        // Inside each (rank, chunk) block rows go by descending degree (ties by id):
+        // the two rows of a warp then have near-equal lengths (no padded slots on
+        // the lighter half) and the dynamic row scheduler hands out the longest
+        // rows first. Row contents are untouched, so results stay bit-exact;
+        // GP_ROW_ORDER=id keeps plain id order.
+        const char* ro = std::getenv("GP_ROW_ORDER");
+        if (!(ro && std::string(ro) == "id")) {
+            for (size_t b = 0; b + 1 < h->bstart.size(); ++b) {
+                if ((b + 1) % KB == 0) continue;  // last entry of a rank's row of starts
+                const uint32_t b0 = h->bstart[b], b1 = h->bstart[b + 1];
+                std::stable_sort(inv.begin() + b0, inv.begin() + b1,
+                                 [&](uint32_t a, uint32_t c) { return off[a + 1] - off[a] > off[c + 1] - off[c]; });
+            }
         }
+        for (uint32_t r = 0; r < n; ++r) perm[inv[r]] = r;
         h->rp.assign(size_t(n) + 1, 0);
         h->part.assign(n, 0);
         h->chunk.assign(n, 0);

@@ -200,8 +200,15 @@ def test_pipeline_ledger_closed_form(gp):
             assert all(int(c[0]) == 0 and int(c[2]) == 0 for c in res.comm)
 
 
-def test_stale_equals_exact_on_chunk_disconnected_graph(gp):
-    """test_engines.cpp:138-155: no cross-chunk edge -> stale pipeline == full-graph run."""
+@pytest.mark.parametrize("row_order", ["id", "degree"])
+def test_stale_equals_exact_on_chunk_disconnected_graph(gp, row_order, monkeypatch):
+    """test_engines.cpp:138-155: no cross-chunk edge -> stale pipeline == full-graph run.
+
+    With GP_ROW_ORDER=id both runs reduce parameter gradients over rows in the same
+    (id) order and must agree bit for bit, as in the reference. The default
+    (chunk, degree) row order changes that reduction order between K=1 and K=2, so
+    the runs then agree to rounding only."""
+    monkeypatch.setenv("GP_ROW_ORDER", row_order)
     n = 80
     rng = np.random.default_rng(9)
     edges = [(u, v) for u in range(n) for v in range(u + 1, n) if u // 40 == v // 40 and rng.random() < 0.3]
@@ -214,8 +221,14 @@ def test_stale_equals_exact_on_chunk_disconnected_graph(gp):
     seq = gp.train_sequential(ds, opt)
     pipe = gp.train_pipeline(ds, (np.arange(n) // 40).astype(np.uint32), 2, opt)
     for (a, _), (b, _) in zip(seq.params, pipe.params):
-        assert bits_equal(a, b)
-    assert np.array_equal(seq.train_loss, pipe.train_loss)
+        if row_order == "id":
+            assert bits_equal(a, b)
+        else:
+            assert rel(a, b) < 1e-5
+    if row_order == "id":
+        assert np.array_equal(seq.train_loss, pipe.train_loss)
+    else:
+        np.testing.assert_allclose(seq.train_loss, pipe.train_loss, rtol=1e-6)
 
 
 def test_deterministic_reruns(gp):
