@@ -208,7 +208,8 @@ struct IpcSide {
     uint64_t peer_slot = 0;
     uint32_t peer_R = 0;
     uint32_t send_seq = 0, recv_seq = 0;
-    cudaStream_t stream = nullptr;  // send stream (copy engine work overlaps the next chunk)
+    cudaStream_t stream = nullptr;   // send stream (copy engine work overlaps the next chunk)
+    cudaStream_t rstream = nullptr;  // receive stream: waits/unpacks/acks in message order
     bool linked() const { return peer != nullptr; }
 };
 
@@ -235,7 +236,8 @@ struct LayerDev {
     float *mW = nullptr, *vW = nullptr, *mb = nullptr, *vb = nullptr;
     float *h = nullptr, *hs = nullptr;   // h_cur / h_snap
     float *pre = nullptr, *dz = nullptr;
-    float *G = nullptr;                  // masked gather source (input of this layer)
+    float *G = nullptr;                  // masked gather source (input of this layer): rows of done chunks
+    float *Gs = nullptr;                 // masked snapshot rows (rows of not-done chunks); == G if cur == snap
     float *bg = nullptr, *bgs = nullptr; // backward gather source (+ snapshot, hist mode)
 };
 
@@ -246,7 +248,10 @@ struct Stage {
     bool first = true, last = true, needs_h0 = false, sync = false, hist = false;
     int device = 0;
     std::string err;
-    cudaStream_t cs = nullptr;
+    cudaStream_t cs = nullptr;       // compute stream (the current one: see the backward wavefront)
+    static constexpr int kMaxWave = 4;
+    cudaStream_t cs_side[kMaxWave] = {};  // extra compute streams of the chunk wavefront
+    int wave_w = 2;                        // streams in the wavefront (GP_WAVE=1: one stream)
     std::vector<LayerDev> L;
 
     // graph (renumbered chunk-contiguous)
@@ -332,7 +337,7 @@ struct Stage {
         if (tr.ipc_up.linked() || tr.ipc_down.linked()) {
             // a dead peer leaves in-stream waits pending: bounded wait, then leak
             try {
-                for (cudaStream_t st : {cs, tr.ipc_up.stream, tr.ipc_down.stream})
+                for (cudaStream_t st : {cs, tr.ipc_up.stream, tr.ipc_down.stream, tr.ipc_up.rstream, tr.ipc_down.rstream})
                     if (st) sync_watchdog(st, 30.0);
             } catch (...) {
                 return;
@@ -340,9 +345,12 @@ struct Stage {
             for (IpcSide* x : {&tr.ipc_up, &tr.ipc_down}) {
                 if (x->peer_opened) cudaIpcCloseMemHandle(x->peer);
                 if (x->stream) cudaStreamDestroy(x->stream);
+                if (x->rstream) cudaStreamDestroy(x->rstream);
             }
         }
         if (cs) cudaStreamSynchronize(cs);
+        for (auto st : cs_side)
+            if (st) cudaStreamSynchronize(st);
         for (void* p : allocs) cudaFree(p);
         for (auto& t : timed) {
             cudaEventDestroy(t.a);
@@ -359,6 +367,8 @@ struct Stage {
         if (tr.up_stream) cudaStreamDestroy(tr.up_stream);
         if (tr.down_stream) cudaStreamDestroy(tr.down_stream);
         if (cs) cudaStreamDestroy(cs);
+        for (auto st : cs_side)
+            if (st) cudaStreamDestroy(st);
     }
 
     // ---- configuration ------------------------------------------------------
@@ -416,6 +426,8 @@ struct Stage {
         GP_CUDA(cudaSetDevice(device));
         GP_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, device));
         GP_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        if (const char* e = std::getenv("GP_WAVE")) wave_w = std::max(1, std::min(kMaxWave, std::atoi(e)));
+        for (int w = 1; w < wave_w; ++w) GP_CUDA(cudaStreamCreateWithFlags(&cs_side[w], cudaStreamNonBlocking));
         GP_CUDA(cudaEventCreate(&ev_start));
         GP_CUDA(cudaEventCreate(&ev_end));
         alloc();
@@ -451,7 +463,11 @@ struct Stage {
             d.pre = dalloc<float>(size_t(n) * d.sin);
             d.dz = dalloc<float>(size_t(n) * d.sout);
             // gather tables carry one extra all-zero row (row n, see gather_row)
-            if (d.agg) d.G = dalloc<float>(size_t(n + 1) * d.sin);
+            if (d.agg) {
+                d.G = dalloc<float>(size_t(n + 1) * d.sin);
+                // stage 0's layer-0 input is x0 (cur == snap); sync mode never reads snapshots
+                d.Gs = (first && i == 0) || sync ? d.G : dalloc<float>(size_t(n + 1) * d.sin);
+            }
             if (!sync && i + 1 < len && specs[lb + i + 1].kind != GP_DENSE)
                 d.hs = dalloc<float>(size_t(n) * d.sout);
             if (d.l > 0) {
@@ -858,15 +874,16 @@ struct Stage {
         return L[i - 1].h;
     }
 
-    void remask(uint32_t i, const float* src, uint32_t r0, uint32_t r1, const DropKey& key) {
+    // G (rows of done chunks) or Gs (snapshot rows, rebuilt once per epoch)
+    void remask(uint32_t i, const float* src, uint32_t r0, uint32_t r1, const DropKey& key, bool snapshot = false) {
         auto& d = L[i];
-        RemaskParams p{r0, r1, d.din, src, src_stride(i), d.G, d.sin, orig, key};
+        RemaskParams p{r0, r1, d.din, src, src_stride(i), snapshot ? d.Gs : d.G, d.sin, orig, key};
         const uint32_t rows = r1 - r0;
         launch(GP_K_REMASK, double(rows) * d.din * 8.0, 0, 0,
                [&]() { k_remask<<<row_grid(rows, (const void*)k_remask, 0), kBlock, 0, cs>>>(p); });
     }
 
-    void forward_layer(uint32_t i, uint32_t r0, uint32_t r1, uint32_t t) {
+    void forward_layer(uint32_t i, uint32_t r0, uint32_t r1, uint32_t t, uint64_t done) {
         auto& d = L[i];
         const uint32_t rows = r1 - r0;
         if (rows == 0) return;
@@ -889,6 +906,8 @@ struct Stage {
             p.rowptr = rowptr;
             p.edges = edges;
             p.gsrc = d.G;
+            p.gsnap = d.agg ? d.Gs : nullptr;
+            p.done = done;
             p.gstride = d.sin;
             p.zrow = n;
             p.xsrc = cur_src(i);
@@ -1354,6 +1373,7 @@ struct Stage {
                 x.own_bytes = kIpcRing + x.own_slot * 4 * x.own_R;
                 x.own = dalloc<char>(x.own_bytes);  // zeroed: counters start at 0
                 GP_CUDA(cudaStreamCreateWithFlags(&x.stream, cudaStreamNonBlocking));
+                GP_CUDA(cudaStreamCreateWithFlags(&x.rstream, cudaStreamNonBlocking));
             }
             IpcBlob b{};
             b.magic = kIpcMagic;
@@ -1431,15 +1451,24 @@ struct Stage {
                  "cuStreamWriteValue32(ready)");
     }
 
+    // Receive on the side's own stream, in message order (the ack counter stays
+    // monotone whichever compute stream consumes the chunk); compute waits on it.
     void ipc_recv(IpcSide& x, const std::vector<Piece>& pcs) {
         const uint32_t seq = ++x.recv_seq, slot = (seq - 1) % x.own_R;
-        cu_check(g_memops.wait(cs, dptr(x.own, kIpcReady), seq, CU_STREAM_WAIT_VALUE_GEQ), "cuStreamWaitValue32(ready)");
+        cudaStream_t rs = x.rstream;
+        cudaEvent_t go = pool_event();
+        GP_CUDA(cudaEventRecord(go, cs));  // destination rows are free once cs got here
+        GP_CUDA(cudaStreamWaitEvent(rs, go, 0));
+        cu_check(g_memops.wait(rs, dptr(x.own, kIpcReady), seq, CU_STREAM_WAIT_VALUE_GEQ), "cuStreamWaitValue32(ready)");
         const float* src = reinterpret_cast<const float*>(x.own + kIpcRing) + size_t(slot) * x.own_slot;
         for (const auto& p : pcs) {
-            GP_CUDA(cudaMemcpyAsync(p.ptr, src, p.floats * 4, cudaMemcpyDeviceToDevice, cs));
+            GP_CUDA(cudaMemcpyAsync(p.ptr, src, p.floats * 4, cudaMemcpyDeviceToDevice, rs));
             src += p.floats;
         }
-        cu_check(g_memops.write(cs, dptr(x.peer, kIpcAck), seq, CU_STREAM_WRITE_VALUE_DEFAULT), "cuStreamWriteValue32(ack)");
+        cu_check(g_memops.write(rs, dptr(x.peer, kIpcAck), seq, CU_STREAM_WRITE_VALUE_DEFAULT), "cuStreamWriteValue32(ack)");
+        cudaEvent_t done = pool_event();
+        GP_CUDA(cudaEventRecord(done, rs));
+        GP_CUDA(cudaStreamWaitEvent(cs, done, 0));
     }
 
     void send_fwd(uint32_t k) {
@@ -1605,6 +1634,30 @@ struct Stage {
     }
 
     // ---- one epoch ---------------------------------------------------------------
+    // ---- chunk wavefront helpers ------------------------------------------------
+    // W compute streams; chunk j runs on stream j % W. Off for hybrid groups (halo
+    // exchange is ordered on one stream), K = 1, and in profiling mode (clean
+    // per-kernel times).
+    int wave_width() const { return G == 1 && K > 1 && !profiling ? wave_w : 1; }
+    cudaStream_t wave_stream(uint32_t j, int W, cudaStream_t main) const { return j % W ? cs_side[j % W] : main; }
+    cudaEvent_t record_event() {
+        cudaEvent_t e = pool_event();
+        GP_CUDA(cudaEventRecord(e, cs));
+        return e;
+    }
+    void wave_fork(int W) {
+        if (W < 2) return;
+        cudaEvent_t e = record_event();
+        for (int w = 1; w < W; ++w) GP_CUDA(cudaStreamWaitEvent(cs_side[w], e, 0));
+    }
+    void wave_join(int W, cudaStream_t main) {
+        for (int w = 1; w < W; ++w) {
+            cudaEvent_t e = pool_event();
+            GP_CUDA(cudaEventRecord(e, cs_side[w]));
+            GP_CUDA(cudaStreamWaitEvent(main, e, 0));
+        }
+    }
+
     void run_epoch(uint32_t t, const uint32_t* order, gp_epoch_stats* out) {
         GP_CUDA(cudaSetDevice(device));
         if (!graph_ready) throw Error(GP_EINVAL, "graph not uploaded");
@@ -1643,25 +1696,52 @@ struct Stage {
             if (i == 0 && first) {
                 remask(0, x0, 0, n, drop_key(t, L[0].l, L[0].din));  // cur == snap == x0
             } else if (!sync) {
-                remask(i, snap_src(i), 0, n, drop_key(t, L[i].l, L[i].din));
+                remask(i, snap_src(i), 0, n, drop_key(t, L[i].l, L[i].din), true);
             }
         }
 
         // ---- forward -----------------------------------------------------------
+        const uint64_t all_done = K == 64 ? ~0ull : ((1ull << K) - 1);
         if (!sync) {
+            // Two-stream wavefront (SURVEY §8(a')9): chunk j+1 runs layer i while chunk
+            // j runs layer i+1. Legal because gathers read done chunks from G (rows
+            // written this epoch) and not-done chunks from the separate snapshot table
+            // Gs, so a chunk never reads rows the concurrent chunk is writing; the one
+            // cross-chunk dependency ("layer i of chunk j+1 reads G_i rows of chunk j,
+            // written by chunk j's layer i-1 / input remask") is one event.
+            const int W = wave_width();
+            cudaStream_t main = cs;
+            struct Restore {
+                cudaStream_t& ref;
+                cudaStream_t v;
+                ~Restore() { ref = v; }
+            } restore{cs, main};
+            // ev[j % W][i]: chunk j's input (i = 0) / layer i-1 output (i >= 1) is written
+            std::vector<std::vector<cudaEvent_t>> ev(W, std::vector<cudaEvent_t>(len + 1, nullptr));
+            wave_fork(W);
+            uint64_t done = 0;
             for (uint32_t kk = 0; kk < K; ++kk) {
                 const uint32_t k = ord[kk];
                 const uint32_t r0 = row_begin(k), r1 = row_end(k);
+                done |= 1ull << k;  // "processed" includes the current chunk (:789)
+                cs = wave_stream(kk, W, main);
+                auto& mine = ev[kk % W];
                 if (!first) {
                     recv_fwd(k);
                     if (L[0].agg) remask(0, in_cur, r0, r1, drop_key(t, L[0].l, L[0].din));
                 }
+                if (W > 1) mine[0] = record_event();
                 for (uint32_t i = 0; i < len; ++i) {
                     if (G > 1 && L[i].agg) halo_fwd(i, k, k + 1, t);  // exchange_rows (:792-794)
-                    forward_layer(i, r0, r1, t);
+                    if (L[i].agg)  // G_i rows of the W-1 previous chunks (other streams)
+                        for (uint32_t w = 1; w < uint32_t(W) && w <= kk; ++w)
+                            GP_CUDA(cudaStreamWaitEvent(cs, ev[(kk - w) % W][i], 0));
+                    forward_layer(i, r0, r1, t, done);
+                    if (W > 1) mine[i + 1] = record_event();
                 }
                 if (!last) send_fwd(k);
             }
+            wave_join(W, main);
         } else {
             if (!first) {
                 for (uint32_t kk = 0; kk < K; ++kk) recv_fwd(ord[kk]);
@@ -1669,7 +1749,7 @@ struct Stage {
             }
             for (uint32_t i = 0; i < len; ++i) {
                 if (G > 1 && L[i].agg) halo_fwd(i, 0, K, t);  // exchange_rows_full (:806-808)
-                forward_layer(i, own_begin(), own_end(), t);
+                forward_layer(i, own_begin(), own_end(), t, all_done);
             }
             if (!last)
                 for (uint32_t kk = 0; kk < K; ++kk) send_fwd(ord[kk]);
@@ -1688,11 +1768,33 @@ struct Stage {
 
         // ---- backward ---------------------------------------------------------------
         if (!sync) {
+            // Wavefront over W streams (SURVEY §8(a')9): chunk j+1 of the backward order
+            // runs layer i+1 while chunk j runs layer i. Legal because a chunk only
+            // gathers from chunks already done (the others are filtered out), so the only
+            // cross-chunk dependency is "layer i of chunk j+1 reads bg_{i+1} of chunk j",
+            // one event per (chunk, layer).
+            const int W = wave_width();
+            cudaStream_t main = cs;
+            struct Restore {
+                cudaStream_t& ref;
+                cudaStream_t v;
+                ~Restore() { ref = v; }
+            } restore{cs, main};
+            // ev[j % W][i]: bg_i rows of the j-th chunk (backward order) are written
+            std::vector<std::vector<cudaEvent_t>> ev(W, std::vector<cudaEvent_t>(len + 1, nullptr));
+            wave_fork(W);
             uint64_t done = 0;
-            for (uint32_t kk = K; kk-- > 0;) {
+            uint32_t j = 0;
+            for (uint32_t kk = K; kk-- > 0; ++j) {
                 const uint32_t k = ord[kk];
                 const uint32_t r0 = row_begin(k), r1 = row_end(k);
                 done |= 1ull << k;
+                cs = wave_stream(j, W, main);
+                auto& mine = ev[j % W];
+                auto wait_prev = [&](uint32_t i) {
+                    for (uint32_t w = 1; w < uint32_t(W) && w <= j; ++w)
+                        GP_CUDA(cudaStreamWaitEvent(cs, ev[(j - w) % W][i], 0));
+                };
                 if (last) {
                     XentParams p = xent_params(r0, r1);
                     launch(GP_K_XENT, double(r1 - r0) * L[len - 1].dout * 8.0, 0, 0,
@@ -1702,14 +1804,18 @@ struct Stage {
                 }
                 for (uint32_t i = len; i-- > 0;) {
                     if (G > 1 && i + 1 < len && L[i + 1].agg) halo_bwd(i + 1, k, k + 1);  // (:838-844)
+                    if (i + 1 < len && L[i + 1].agg) wait_prev(i + 1);
                     backward_layer(i, r0, r1, t, done);
+                    if (W > 1) mine[i] = record_event();
                 }
                 if (G > 1 && L[0].agg) halo_bwd(0, k, k + 1);
                 if (!first) {
+                    if (L[0].agg) wait_prev(0);
                     backward_dhin(r0, r1, t, done);
                     send_bwd(k);
                 }
             }
+            wave_join(W, main);
         } else {
             const uint64_t done = K == 64 ? ~0ull : ((1ull << K) - 1);
             const uint32_t ob = own_begin(), oe = own_end();
@@ -1735,7 +1841,7 @@ struct Stage {
         GP_CUDA(cudaEventRecord(ev_end, cs));
         if (tr.ipc_up.linked() || tr.ipc_down.linked()) {
             sync_watchdog(cs, 600.0);
-            for (cudaStream_t st : {tr.ipc_up.stream, tr.ipc_down.stream})
+            for (cudaStream_t st : {tr.ipc_up.stream, tr.ipc_down.stream, tr.ipc_up.rstream, tr.ipc_down.rstream})
                 if (st) sync_watchdog(st, 600.0);
         }
         GP_CUDA(cudaStreamSynchronize(cs));

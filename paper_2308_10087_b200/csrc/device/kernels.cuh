@@ -204,7 +204,9 @@ struct FwdParams {
     uint32_t* ticket;  // zeroed work counter (row pairs handed out)
     const uint64_t* rowptr;
     const uint2* edges;
-    const float* gsrc;
+    const float* gsrc;   // gather table rows of done chunks (cur)
+    const float* gsnap;  // gather table rows of not-done chunks (snapshot); may equal gsrc
+    uint64_t done;       // chunks processed so far this epoch, including the current one
     uint32_t gstride;
     uint32_t zrow;
     const float* xsrc;

@@ -329,8 +329,9 @@ __global__ void __launch_bounds__(kBlock, NB == 2 ? 4 : (NB == 4 ? 3 : 2)) k_fwd
             const F8 x = (has && in_act) ? ld8_stream(p.xsrc + size_t(v) * p.xstride + 8 * hl) : f8_zero();
             pre = drop8(p.in_mask, has ? p.orig[v] : 0u, 8 * hl, p.din, x);
         } else {
-            const F8 z = gather_row8<false, false, NB>(p.rowptr, p.edges, v, has, p.gsrc, nullptr, p.gstride, 0ull, lane,
-                                                   in_act);
+            // "cur if the neighbour's chunk is done, else snapshot" (engines_impl.hpp:740-744)
+            const F8 z = gather_row8<false, true, NB>(p.rowptr, p.edges, v, has, p.gsrc, p.gsnap, p.gstride, p.done, lane,
+                                                  in_act);
             if (KIND == FWD_GCN2) {
                 const F8 h = (has && in_act) ? ld8_stream(p.h0 + size_t(v) * p.h0stride + 8 * hl) : f8_zero();
 #pragma unroll

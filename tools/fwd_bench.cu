@@ -157,6 +157,8 @@ int main(int argc, char** argv) {
     p.rowptr = d_rp;
     p.edges = d_e;
     p.gsrc = G;
+    p.gsnap = G;
+    p.done = ~0ull;
     p.gstride = S8;
     p.orig = orig;
     p.h0 = h0;
