@@ -950,8 +950,8 @@ struct Stage {
                 const double db = double(rows) * (d.din + d.dout + (gnext ? d.dout : 0)) * 4.0 +
                                   double(d.din) * d.dout * 4.0;
                 launch(GP_K_FWD_AGG, eb, 2.0 * e * d.din, gather, [&]() {
-                    if (g2) fwd_nb<FWD_GCN2, true>(rows, 0, p);
-                    else fwd_nb<FWD_GCN, true>(rows, 0, p);
+                    if (g2) fwd_nb<FWD_GCN2, true>(rows, kEdgeSlotBytes, p);
+                    else fwd_nb<FWD_GCN, true>(rows, kEdgeSlotBytes, p);
                 });
                 const size_t dsm = row_smem_bytes(d.din, d.dout, kDenseRows);
                 launch(GP_K_FWD_DENSE, db, 2.0 * double(rows) * d.din * d.dout, 0, [&]() {
@@ -1066,7 +1066,7 @@ struct Stage {
         p.dh0 = dh0;
         p.bg = d.bg;
         p.bgstride = d.sin;
-        const size_t smem = p.need_dagg ? row_smem_bytes(d.dout, d.din, 2) : 0;
+        const size_t smem = p.need_dagg ? row_smem_bytes(d.dout, d.din, 2) : kEdgeSlotBytes;
         const double bytes = e * 8.0 + (e > 0 ? double(n) * d.dout * 4.0 : double(rows) * d.dout * 4.0) +
                              double(rows) * d.dout * 8.0 + (p.need_dagg ? double(rows) * d.din * 4.0 : 0.0) +
                              (p.gcn2 ? double(rows) * d.din * 8.0 : 0.0);
@@ -1077,8 +1077,8 @@ struct Stage {
             // gather (+ mask, dh0 term, ReLU) -> dz, then dz.W^T + mixes -> bg, dh0
             const double ab = e * 8.0 + double(n) * d.dout * 4.0 + double(rows) * d.dout * 8.0;
             launch(GP_K_BWD_AGG, ab, 2.0 * e * d.dout, gather, [&]() {
-                if (prev == PREV_AGG) bwd_nb<PREV_AGG, OUT_LAYER, true>(rows, 0, p);
-                else bwd_nb<PREV_AGG_HIST, OUT_LAYER, true>(rows, 0, p);
+                if (prev == PREV_AGG) bwd_nb<PREV_AGG, OUT_LAYER, true>(rows, kEdgeSlotBytes, p);
+                else bwd_nb<PREV_AGG_HIST, OUT_LAYER, true>(rows, kEdgeSlotBytes, p);
             });
             if (p.need_dagg) {
                 const double db = double(rows) * (d.dout + d.din) * 4.0 + (p.gcn2 ? double(rows) * d.din * 8.0 : 0.0) +
@@ -1130,13 +1130,13 @@ struct Stage {
         const double e = d.agg ? double(rowptr_nnz(r0, r1)) : 0.0;
         const double bytes = e * 8.0 + (d.agg ? double(n) : double(rows)) * d.din * 4.0 + double(rows) * d.din * 4.0;
         if (!d.agg)
-            launch(GP_K_BWD_DENSE, bytes, 0, 0, [&]() { bwd_nb<PREV_OWN, OUT_DHIN>(rows, 0, p); });
+            launch(GP_K_BWD_DENSE, bytes, 0, 0, [&]() { bwd_nb<PREV_OWN, OUT_DHIN>(rows, kEdgeSlotBytes, p); });
         else if (hist)
             launch(GP_K_BWD_AGG, bytes, 2.0 * e * d.din, e * d.sin * 4.0,
-                   [&]() { bwd_nb<PREV_AGG_HIST, OUT_DHIN>(rows, 0, p); });
+                   [&]() { bwd_nb<PREV_AGG_HIST, OUT_DHIN>(rows, kEdgeSlotBytes, p); });
         else
             launch(GP_K_BWD_AGG, bytes, 2.0 * e * d.din, e * d.sin * 4.0,
-                   [&]() { bwd_nb<PREV_AGG, OUT_DHIN>(rows, 0, p); });
+                   [&]() { bwd_nb<PREV_AGG, OUT_DHIN>(rows, kEdgeSlotBytes, p); });
     }
 
     XentParams xent_params(uint32_t r0, uint32_t r1) {

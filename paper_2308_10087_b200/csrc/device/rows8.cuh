@@ -83,11 +83,21 @@ __device__ __forceinline__ F8 shfl8(const F8& x, int src) {
 // entries; a batch of 16 is gathered as soon as either half's queue is full, so
 // sparse done-sets do not pay for padded slots. HIST (historical-gradient
 // ablation) keeps every entry and reads not-done chunks from `snap`.
+#ifndef GP_SMEM_EDGES
+#define GP_SMEM_EDGES 1
+#endif
+// CSR entries of the current batch are broadcast to the half-warp through a
+// 16-entry shared-memory slot (one LDS.64 per entry for both halves) instead of
+// two shuffles per entry: fewer L1TEX data-pipe wavefronts, which the gather
+// saturates first.
+constexpr bool kSmemEdges = GP_SMEM_EDGES != 0;
+constexpr uint32_t kEdgeSlotBytes = kWarpsPerBlock * 32 * 8;  // per CTA: 16 entries x 2 halves x 8 warps
+
 template <bool FILTER, bool HIST, int NB>
 __device__ __forceinline__ F8 gather_row8(const uint64_t* __restrict__ rowptr, const uint2* __restrict__ edges,
                                           uint32_t v, bool has_row, const float* __restrict__ src,
                                           const float* __restrict__ snap, uint32_t stride, uint64_t done,
-                                          int lane, bool active) {
+                                          int lane, bool active, uint2* eslot) {
     const int hl = lane & 15, hb = lane & 16;
     uint64_t e0 = 0, e1 = 0;
     if (has_row) {
@@ -103,15 +113,28 @@ __device__ __forceinline__ F8 gather_row8(const uint64_t* __restrict__ rowptr, c
     // concentrates on one L2 line), weight 0, chunk bits 0
     const uint2 pad = make_uint2(has_row ? v : 0u, 0u);
     F8 acc = f8_zero();
+    uint2* es = eslot + (hb ? 16 : 0);
     auto batch16 = [&](const uint2 my) {
+        if (kSmemEdges) {
+            __syncwarp();
+            es[hl] = my;
+            __syncwarp();
+        }
 #pragma unroll
         for (int t = 0; t < 16; t += NB) {
             float w[NB];
             F8 x[NB];
 #pragma unroll
             for (int i = 0; i < NB; ++i) {
-                const uint32_t packed = __shfl_sync(kFull, my.x, hb + t + i);
-                w[i] = __uint_as_float(__shfl_sync(kFull, my.y, hb + t + i));
+                uint32_t packed;
+                if (kSmemEdges) {
+                    const uint2 e = es[t + i];
+                    packed = e.x;
+                    w[i] = __uint_as_float(e.y);
+                } else {
+                    packed = __shfl_sync(kFull, my.x, hb + t + i);
+                    w[i] = __uint_as_float(__shfl_sync(kFull, my.y, hb + t + i));
+                }
                 const float* s = ls;
                 if (HIST && !((done >> (packed >> kColBits)) & 1ull)) s = lsn;
                 x[i] = ld8_gather(s + size_t(packed & kColMask) * stride);
@@ -182,7 +205,7 @@ __device__ __forceinline__ F8 gather_row8(const uint64_t* __restrict__ rowptr, c
 __host__ __device__ constexpr uint32_t mat_stride(uint32_t cols) { return (cols + 7u) & ~7u; }
 __host__ __device__ constexpr size_t row_smem_bytes(uint32_t mrows, uint32_t mcols, uint32_t R) {
     // matrix + tail pad + bias (128) + x staging (8 warps x 128 x R)
-    return (size_t(mrows) * mat_stride(mcols) + 32 + 128 + size_t(kWarpsPerBlock) * 128 * R) * 4;
+    return (size_t(mrows) * mat_stride(mcols) + 32 + 128 + size_t(kWarpsPerBlock) * 128 * R) * 4 + kEdgeSlotBytes;
 }
 
 __device__ __forceinline__ void stage_mat(float* Ms, const float* W, uint32_t rows, uint32_t cols, bool transpose,
@@ -304,7 +327,7 @@ template <int KIND, int NB, bool SPLIT = false>
 __global__ void __launch_bounds__(kBlock, NB == 2 ? 4 : (NB == 4 ? 3 : 2)) k_fwd8(FwdParams p) {
     extern __shared__ float4 smem4[];
     const uint32_t ms = mat_stride(p.dout);
-    float* Ms = reinterpret_cast<float*>(smem4);
+    float* Ms = reinterpret_cast<float*>(reinterpret_cast<char*>(smem4) + kEdgeSlotBytes);
     float* bs = Ms + size_t(p.din) * ms + 32;
     float* xs = bs + 128 + (threadIdx.x / 32) * 256;
     if (!SPLIT) {
@@ -331,7 +354,7 @@ __global__ void __launch_bounds__(kBlock, NB == 2 ? 4 : (NB == 4 ? 3 : 2)) k_fwd
         } else {
             // "cur if the neighbour's chunk is done, else snapshot" (engines_impl.hpp:740-744)
             const F8 z = gather_row8<false, true, NB>(p.rowptr, p.edges, v, has, p.gsrc, p.gsnap, p.gstride, p.done, lane,
-                                                  in_act);
+                                                  in_act, reinterpret_cast<uint2*>(smem4) + (threadIdx.x / 32) * 32);
             if (KIND == FWD_GCN2) {
                 const F8 h = (has && in_act) ? ld8_stream(p.h0 + size_t(v) * p.h0stride + 8 * hl) : f8_zero();
 #pragma unroll
@@ -364,7 +387,7 @@ template <bool GCN2>
 __global__ void __launch_bounds__(kBlock, 3) k_fwd_dense8(FwdParams p) {
     extern __shared__ float4 smem4[];
     const uint32_t ms = mat_stride(p.dout);
-    float* Ms = reinterpret_cast<float*>(smem4);
+    float* Ms = reinterpret_cast<float*>(reinterpret_cast<char*>(smem4) + kEdgeSlotBytes);
     float* bs = Ms + size_t(p.din) * ms + 32;
     float* xs = bs + 128 + (threadIdx.x / 32) * 128 * kDenseRows;
     stage_mat(Ms, p.W, p.din, p.dout, false, p.dout);
@@ -403,7 +426,7 @@ template <int PREV, int OUT, int NB, bool SPLIT = false>
 __global__ void __launch_bounds__(kBlock, NB == 2 ? 4 : (NB == 4 ? 3 : 2)) k_bwd8(BwdParams p) {
     extern __shared__ float4 smem4[];
     const uint32_t ms = mat_stride(p.din);
-    float* Ms = reinterpret_cast<float*>(smem4);
+    float* Ms = reinterpret_cast<float*>(reinterpret_cast<char*>(smem4) + kEdgeSlotBytes);
     float* xs = Ms + size_t(p.dout) * ms + 32 + 128 + (threadIdx.x / 32) * 256;
     if (!SPLIT && OUT == OUT_LAYER && p.need_dagg) {
         stage_mat(Ms, p.W, p.dout, p.din, true, p.dout);  // Ms[j][c] = W[c][j]
@@ -430,7 +453,8 @@ __global__ void __launch_bounds__(kBlock, NB == 2 ? 4 : (NB == 4 ? 3 : 2)) k_bwd
                 s = (has && dh_act) ? ld8_stream(p.bgn + size_t(u) * p.bgnstride + 8 * hl) : f8_zero();
             else
                 s = gather_row8<true, PREV == PREV_AGG_HIST, NB>(p.rowptr, p.edges, u, has, p.bgn, p.bgn_snap, p.bgnstride,
-                                                             p.done, lane, dh_act);
+                                                             p.done, lane, dh_act,
+                                                             reinterpret_cast<uint2*>(smem4) + (threadIdx.x / 32) * 32);
             dh = drop8(p.prev_mask, has ? p.orig[u] : 0u, 8 * hl, p.dh_width, s);
         }
         if (OUT == OUT_DHIN) {
@@ -465,7 +489,7 @@ __global__ void __launch_bounds__(kBlock, NB == 2 ? 4 : (NB == 4 ? 3 : 2)) k_bwd
 __global__ void __launch_bounds__(kBlock, 3) k_bwd_dense8(BwdParams p) {
     extern __shared__ float4 smem4[];
     const uint32_t ms = mat_stride(p.din);
-    float* Ms = reinterpret_cast<float*>(smem4);
+    float* Ms = reinterpret_cast<float*>(reinterpret_cast<char*>(smem4) + kEdgeSlotBytes);
     float* xs = Ms + size_t(p.dout) * ms + 32 + 128 + (threadIdx.x / 32) * 128 * kDenseRows;
     stage_mat(Ms, p.W, p.dout, p.din, true, p.dout);  // Ms[j][c] = W[c][j]
     __syncthreads();

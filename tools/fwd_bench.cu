@@ -330,8 +330,8 @@ int main(int argc, char** argv) {
     for (int K : {4, 32}) {
         run("k_fwd8<GCN2,2> (engine)", (const void*)k_fwd8<FWD_GCN2, 2>, wsm, K);
         run("k_fwd8<GCN2,4> (engine)", (const void*)k_fwd8<FWD_GCN2, 4>, wsm, K);
-        run("split gather k_fwd8<GCN2,2,1>", (const void*)k_fwd8<FWD_GCN2, 2, true>, 0, K);
-        run("split gather k_fwd8<GCN2,4,1>", (const void*)k_fwd8<FWD_GCN2, 4, true>, 0, K);
+        run("split gather k_fwd8<GCN2,2,1>", (const void*)k_fwd8<FWD_GCN2, 2, true>, kEdgeSlotBytes, K);
+        run("split gather k_fwd8<GCN2,4,1>", (const void*)k_fwd8<FWD_GCN2, 4, true>, kEdgeSlotBytes, K);
         run("split dense k_fwd_dense8<1>", (const void*)k_fwd_dense8<true>, dsm, K);
         run("k_fwd8 again", (const void*)k_fwd8<FWD_GCN2, 2>, wsm, K);
     }
@@ -357,7 +357,7 @@ int main(int argc, char** argv) {
         printf("fwd out checksum (all rows): %016llx\n", (unsigned long long)hsh);
     }
     {
-        full((const void*)k_fwd8<FWD_GCN2, 2, true>, 0);
+        full((const void*)k_fwd8<FWD_GCN2, 2, true>, kEdgeSlotBytes);
         full((const void*)k_fwd_dense8<true>, dsm);
         snap(got);
         size_t bad = 0;
