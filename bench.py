@@ -269,6 +269,11 @@ def main():
         ms = eng.elapsed_ms(0, 1)
     barrier()
     ms = max_over_ranks(ms)
+    if dist:  # whole-job kernel count
+        import torch
+        lt = torch.tensor([float(launches)], dtype=torch.float64)
+        dist.all_reduce(lt)
+        launches = int(lt.item())
     if dist:  # the loss lives on the last stage
         box = [losses]
         dist.broadcast_object_list(box, src=S - 1)

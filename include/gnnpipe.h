@@ -183,6 +183,18 @@ gp_status gp_link_ipc(gp_ctx* ctx, const uint8_t* up_peer_blob, const uint8_t* d
  * receiver from its peers' buffers after an event handshake; weight gradients
  * are folded in rank order at rank 0 and broadcast (group_weight_sync :102-128). */
 gp_status gp_link_group(gp_ctx** members, uint32_t group_size);
+/* Hybrid group across processes (one process per GPU; replaces the in-process
+ * group channels of exchange_rows engines_impl.hpp:626-643 and group_weight_sync
+ * :102-128). Each member maps its peers' activation / gradient-table / weight-
+ * gradient buffers over CUDA IPC and pulls halo rows straight from them after an
+ * in-stream counter handshake; rank 0 folds weight gradients in rank order.
+ *   1. after gp_upload_graph (and before the first epoch): gp_group_export fills
+ *      this member's blob (call with blob = NULL to get the length);
+ *   2. exchange blobs out of band within the stage group;
+ *   3. gp_link_group_ipc(ctx, blobs, lengths): blobs[r] = member r's blob (own entry
+ *      ignored). Stage links between groups use gp_ipc_export / gp_link_ipc. */
+gp_status gp_group_export(gp_ctx* ctx, uint8_t* blob, uint64_t capacity, uint64_t* length);
+gp_status gp_link_group_ipc(gp_ctx* ctx, const uint8_t* const* blobs, const uint64_t* lengths);
 /* Abort a blocked local transport (error propagation across stage threads). */
 void gp_abort(gp_ctx* ctx);
 

@@ -173,6 +173,8 @@ def _L():
         "gp_nccl_unique_id": (C.c_int, [P(C.c_uint8)]),
         "gp_link_nccl": (C.c_int, [vp, P(C.c_uint8), P(C.c_uint8)]),
         "gp_ipc_export": (C.c_int, [vp, P(C.c_uint8), P(C.c_uint8)]),
+        "gp_group_export": (C.c_int, [vp, P(C.c_uint8), C.c_uint64, P(C.c_uint64)]),
+        "gp_link_group_ipc": (C.c_int, [vp, P(P(C.c_uint8)), P(C.c_uint64)]),
         "gp_link_ipc": (C.c_int, [vp, P(C.c_uint8), P(C.c_uint8)]),
         "gp_abort": (None, [vp]),
         "gp_run_epoch": (C.c_int, [vp, C.c_uint32, u32p, P(gp_epoch_stats)]),
@@ -497,7 +499,8 @@ class StageEngine:
                  num_stages: int, layer_range, hidden: int, num_classes: int, dropout: float, seed: int,
                  lr: float = 1e-3, optimizer: str = "adam", fix_alpha: int = 10,
                  historical_gradients: bool = False, synchronous_mode: bool = False, device: int = 0,
-                 beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8):
+                 beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8, group_size: int = 1,
+                 group_rank: int = 0):
         self.specs = list(specs)
         self._specs_c = (gp_layer_spec * len(specs))(*[
             gp_layer_spec(s.kind, s.in_dim, s.out_dim, int(s.relu), s.alpha, s.beta) for s in specs])
@@ -519,7 +522,10 @@ class StageEngine:
         cfg.fix_alpha = fix_alpha
         cfg.historical_gradients = int(historical_gradients)
         cfg.synchronous_mode = int(synchronous_mode)
+        cfg.group_size = group_size
+        cfg.group_rank = group_rank
         self.n, self.K, self.stage, self.S = num_vertices, num_chunks, stage, num_stages
+        self.G, self.grank = group_size, group_rank
         self.layer_range = tuple(layer_range)
         self.hidden = hidden
         h = C.c_void_p()
@@ -538,6 +544,29 @@ class StageEngine:
             self.close()
         except Exception:
             pass
+
+    def upload_partition(self, part_of):
+        """Partition::assignment (hybrid, group_size > 1); call before upload_graph."""
+        p = np.ascontiguousarray(part_of, np.uint32)
+        _gp(_L().gp_upload_partition(self._h, _ptr(p, C.c_uint32)), self._h)
+
+    def group_export(self) -> bytes:
+        """This hybrid member's group blob (gp_group_export): share it with the other
+        members of the stage group, then call link_group_ipc."""
+        n = C.c_uint64()
+        _gp(_L().gp_group_export(self._h, None, 0, C.byref(n)), self._h)
+        buf = (C.c_uint8 * n.value)()
+        _gp(_L().gp_group_export(self._h, buf, n.value, C.byref(n)), self._h)
+        return bytes(buf)
+
+    def link_group_ipc(self, blobs):
+        """blobs[r] = group member r's blob (own entry ignored; may be None)."""
+        G = len(blobs)
+        arrs = [(C.c_uint8 * len(b)).from_buffer_copy(b) if b else None for b in blobs]
+        ptrs = (C.POINTER(C.c_uint8) * G)(*[C.cast(a, C.POINTER(C.c_uint8)) if a is not None else None
+                                          for a in arrs])
+        lens = (C.c_uint64 * G)(*[len(b) if b else 0 for b in blobs])
+        _gp(_L().gp_link_group_ipc(self._h, ptrs, lens), self._h)
 
     def upload_graph(self, offsets, cols, vals, chunk_of):
         off = np.ascontiguousarray(offsets, np.uint64)

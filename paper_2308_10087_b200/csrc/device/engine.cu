@@ -213,6 +213,31 @@ struct IpcSide {
     bool linked() const { return peer != nullptr; }
 };
 
+// Hybrid group across processes (gp_group_export / gp_link_group_ipc): every
+// member maps its peers' activation, gradient-table and weight-gradient buffers
+// (CUDA IPC; NVLink P2P between GPUs) and a small counter region. A halo message
+// is "rows of chunk k of buffer X are final": the sender bumps a counter in each
+// peer's region with an in-stream write, the receiver waits on it in-stream and
+// pulls the halo rows straight from the peer's buffer (k_pull_rows). Buffers are
+// matched by export index; all members swap cur/snapshot buffers at the same
+// epochs, so "my current buffer j" is "peer's current buffer j".
+constexpr uint32_t kGroupMagic = 0x52475047u;  // "GPGR"
+constexpr uint32_t kGroupKinds = 5;            // 0 fwd halo, 1 bwd halo, 2 grads ready, 3 fold done, 4 copied
+constexpr uint32_t kGroupMaxRanks = 8;
+
+struct IpcGroup {
+    bool linked = false;
+    char* own_flags = nullptr;                  // kGroupKinds x kGroupMaxRanks u32 counters
+    std::vector<char*> own_bufs;                // export order
+    std::vector<std::vector<char*>> peer_bufs;  // [rank][export index]
+    std::vector<char*> peer_flags;              // [rank]
+    std::vector<char*> opened;                  // IPC mappings to close
+    uint32_t post_seq[kGroupKinds] = {};
+    uint32_t recv_seq[kGroupKinds][kGroupMaxRanks] = {};
+    uint32_t sync_seq = 0;
+    static size_t off(uint32_t kind, uint32_t src) { return (size_t(kind) * kGroupMaxRanks + src) * 4; }
+};
+
 struct Transport {
     // Forward: upstream stage sends chunk rows of its last layer (+h0).
     std::shared_ptr<LocalLink> up_local, down_local;  // links to s-1 and s+1
@@ -223,6 +248,7 @@ struct Transport {
     std::vector<cudaEvent_t> ev_pool;
     size_t ev_next = 0;
     IpcSide ipc_up, ipc_down;  // cross-process boundaries (gp_link_ipc)
+    IpcGroup ipcg;             // cross-process hybrid group (gp_link_group_ipc)
 };
 
 // ------------------------------------------------------------------ stage
@@ -334,7 +360,7 @@ struct Stage {
 
     ~Stage() {
         if (device >= 0) cudaSetDevice(device);
-        if (tr.ipc_up.linked() || tr.ipc_down.linked()) {
+        if (tr.ipc_up.linked() || tr.ipc_down.linked() || tr.ipcg.linked) {
             // a dead peer leaves in-stream waits pending: bounded wait, then leak
             try {
                 for (cudaStream_t st : {cs, tr.ipc_up.stream, tr.ipc_down.stream, tr.ipc_up.rstream, tr.ipc_down.rstream})
@@ -342,6 +368,7 @@ struct Stage {
             } catch (...) {
                 return;
             }
+            for (char* p : tr.ipcg.opened) cudaIpcCloseMemHandle(p);
             for (IpcSide* x : {&tr.ipc_up, &tr.ipc_down}) {
                 if (x->peer_opened) cudaIpcCloseMemHandle(x->peer);
                 if (x->stream) cudaStreamDestroy(x->stream);
@@ -1358,7 +1385,6 @@ struct Stage {
     void ipc_export(uint8_t* up_blob, uint8_t* down_blob) {
         GP_CUDA(cudaSetDevice(device));
         if (!graph_ready) throw Error(GP_EINVAL, "gp_ipc_export: upload the graph first");
-        if (G > 1) throw Error(GP_EINVAL, "gp_ipc_export: hybrid groups link in-process (gp_link_group)");
         g_memops.load();
         for (int side = 0; side < 2; ++side) {
             uint8_t* out = side == 0 ? up_blob : down_blob;
@@ -1383,6 +1409,7 @@ struct Stage {
             b.n = n;
             b.K = K;
             b.R = x.own_R;
+            b.pad0 = grank;  // a stage link joins the same partition rank of adjacent stages
             b.slot_floats = x.own_slot;
             b.bytes = x.own_bytes;
             b.ptr = uint64_t(reinterpret_cast<uintptr_t>(x.own));
@@ -1411,6 +1438,7 @@ struct Stage {
                 throw Error(GP_EINVAL, "gp_link_ipc: blob of stage " + std::to_string(b.stage) + " role " +
                                            std::to_string(b.role) + " does not face this boundary");
             if (b.n != n || b.K != K) throw Error(GP_EINVAL, "gp_link_ipc: N/K mismatch");
+            if (b.pad0 != grank) throw Error(GP_EINVAL, "gp_link_ipc: peer is another partition rank");
             if (b.pid == int32_t(getpid())) {
                 x.peer = reinterpret_cast<char*>(uintptr_t(b.ptr));  // same process: plain UVA pointer
                 if (b.device != device) {
@@ -1512,11 +1540,141 @@ struct Stage {
         }
     }
 
+    // ---- hybrid group across processes ------------------------------------------
+    std::vector<char*> group_buffers() const {
+        std::vector<char*> v;
+        auto add = [&](const void* p) {
+            if (p) v.push_back(static_cast<char*>(const_cast<void*>(p)));
+        };
+        for (const auto& d : L) {
+            add(d.h);
+            add(d.hs);
+            add(d.bg);
+            add(d.bgs);
+            add(d.gW);
+            add(d.gb);
+        }
+        add(in_cur);
+        add(in_snap);
+        return v;
+    }
+
+    struct GroupBlobHead {
+        uint32_t magic, version, stage, G, grank, nbufs, n, K;
+        int32_t pid, device;
+        uint64_t flags_ptr;
+        cudaIpcMemHandle_t flags;
+    };
+    struct GroupBlobBuf {
+        uint64_t ptr;
+        cudaIpcMemHandle_t h;
+    };
+
+    size_t group_export(uint8_t* out, size_t cap) {
+        GP_CUDA(cudaSetDevice(device));
+        if (G < 2) throw Error(GP_EINVAL, "gp_group_export: not a hybrid worker (group_size < 2)");
+        if (G > kGroupMaxRanks) throw Error(GP_EINVAL, "gp_group_export: group_size > 8");
+        if (!graph_ready) throw Error(GP_EINVAL, "gp_group_export: upload the graph first");
+        if (last_epoch != 0) throw Error(GP_EINVAL, "gp_group_export: link before the first epoch");
+        g_memops.load();
+        auto& ig = tr.ipcg;
+        if (!ig.own_flags) {
+            ig.own_flags = dalloc<char>(size_t(kGroupKinds) * kGroupMaxRanks * 4);
+            ig.own_bufs = group_buffers();
+        }
+        const size_t need = sizeof(GroupBlobHead) + ig.own_bufs.size() * sizeof(GroupBlobBuf);
+        if (!out) return need;
+        if (cap < need) throw Error(GP_EINVAL, "gp_group_export: blob buffer too small");
+        GroupBlobHead h{};
+        h.magic = kGroupMagic;
+        h.version = GP_ABI_VERSION;
+        h.stage = s;
+        h.G = G;
+        h.grank = grank;
+        h.nbufs = uint32_t(ig.own_bufs.size());
+        h.n = n;
+        h.K = K;
+        h.pid = int32_t(getpid());
+        h.device = device;
+        h.flags_ptr = uint64_t(reinterpret_cast<uintptr_t>(ig.own_flags));
+        GP_CUDA(cudaIpcGetMemHandle(&h.flags, ig.own_flags));
+        std::memcpy(out, &h, sizeof(h));
+        for (size_t j = 0; j < ig.own_bufs.size(); ++j) {
+            GroupBlobBuf b{};
+            b.ptr = uint64_t(reinterpret_cast<uintptr_t>(ig.own_bufs[j]));
+            GP_CUDA(cudaIpcGetMemHandle(&b.h, ig.own_bufs[j]));
+            std::memcpy(out + sizeof(h) + j * sizeof(b), &b, sizeof(b));
+        }
+        return need;
+    }
+
+    void group_link_ipc(const uint8_t* const* blobs, const uint64_t* lens) {
+        GP_CUDA(cudaSetDevice(device));
+        auto& ig = tr.ipcg;
+        if (!ig.own_flags) throw Error(GP_EINVAL, "gp_link_group_ipc: call gp_group_export first");
+        if (ig.linked || tr.group) throw Error(GP_EINVAL, "gp_link_group_ipc: group already linked");
+        ig.peer_bufs.assign(G, {});
+        ig.peer_flags.assign(G, nullptr);
+        const int32_t me = int32_t(getpid());
+        auto open = [&](const cudaIpcMemHandle_t& h, uint64_t ptr, int32_t pid) -> char* {
+            if (pid == me) return reinterpret_cast<char*>(uintptr_t(ptr));
+            void* p = nullptr;
+            GP_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+            ig.opened.push_back(static_cast<char*>(p));
+            return static_cast<char*>(p);
+        };
+        for (uint32_t r = 0; r < G; ++r) {
+            if (r == grank) continue;
+            if (!blobs || !blobs[r] || lens[r] < sizeof(GroupBlobHead))
+                throw Error(GP_EINVAL, "gp_link_group_ipc: missing blob of rank " + std::to_string(r));
+            GroupBlobHead h;
+            std::memcpy(&h, blobs[r], sizeof(h));
+            if (h.magic != kGroupMagic || h.version != GP_ABI_VERSION)
+                throw Error(GP_EINVAL, "gp_link_group_ipc: not a group blob");
+            if (h.stage != s || h.G != G || h.grank != r || h.n != n || h.K != K ||
+                h.nbufs != ig.own_bufs.size() || lens[r] < sizeof(h) + size_t(h.nbufs) * sizeof(GroupBlobBuf))
+                throw Error(GP_EINVAL, "gp_link_group_ipc: blob of rank " + std::to_string(r) +
+                                           " does not match this group member");
+            ig.peer_flags[r] = open(h.flags, h.flags_ptr, h.pid);
+            for (uint32_t j = 0; j < h.nbufs; ++j) {
+                GroupBlobBuf b;
+                std::memcpy(&b, blobs[r] + sizeof(h) + size_t(j) * sizeof(b), sizeof(b));
+                ig.peer_bufs[r].push_back(open(b.h, b.ptr, h.pid));
+            }
+        }
+        ig.linked = true;
+    }
+
+    // Peer r's buffer that plays the role of my buffer `mine` (same export index).
+    const float* peer_of(uint32_t r, const void* mine) const {
+        const auto& ig = tr.ipcg;
+        for (size_t j = 0; j < ig.own_bufs.size(); ++j)
+            if (ig.own_bufs[j] == mine) return reinterpret_cast<const float*>(ig.peer_bufs[r][j]);
+        throw Error(GP_ERUNTIME, "group transport: buffer not exported");
+    }
+
+    void ipcg_signal(uint32_t dst, uint32_t kind, uint32_t value) {
+        cu_check(g_memops.write(cs, dptr(tr.ipcg.peer_flags[dst], IpcGroup::off(kind, grank)), value,
+                                CU_STREAM_WRITE_VALUE_DEFAULT),
+                 "cuStreamWriteValue32(group)");
+    }
+    void ipcg_wait(uint32_t src, uint32_t kind, uint32_t value) {
+        cu_check(g_memops.wait(cs, dptr(tr.ipcg.own_flags, IpcGroup::off(kind, src)), value, CU_STREAM_WAIT_VALUE_GEQ),
+                 "cuStreamWaitValue32(group)");
+    }
+
     // ---- hybrid group operations (G > 1) ----------------------------------------
     // FIFO tags: (kind-specific id) so every pull checks it got the expected message.
     static uint32_t halo_tag(uint32_t layer, uint32_t k) { return (layer << 8) | (k & 0xff); }
 
     void group_post(uint32_t kind, uint32_t tag, std::vector<Piece> src) {
+        if (tr.ipcg.linked) {  // rows are final once cs gets here: bump every peer's counter
+            const uint32_t seq = ++tr.ipcg.post_seq[kind];
+            for (uint32_t r2 = 0; r2 < G; ++r2)
+                if (r2 != grank) ipcg_signal(r2, kind, seq);
+            return;
+        }
+        if (!tr.group) throw Error(GP_EFABRIC, "hybrid worker without a group link");
         auto& gl = *tr.group;
         cudaEvent_t ev = pool_event();
         GP_CUDA(cudaEventRecord(ev, cs));
@@ -1533,15 +1691,22 @@ struct Stage {
     // Pull the halo rows of chunks [k_lo, k_hi) from every peer's buffer.
     void halo_pull(uint32_t kind, uint32_t tag, uint32_t k_lo, uint32_t k_hi, float* dst, uint32_t stride,
                    float* dstG, uint32_t gstride, uint32_t width, const DropKey& key) {
-        auto& gl = *tr.group;
         for (uint32_t r2 = 0; r2 < G; ++r2) {
             if (r2 == grank) continue;
-            LocalQueue::Msg m;
-            wait_local(gl.at(r2, grank, kind), tag, m);
-            GP_CUDA(cudaStreamWaitEvent(cs, m.ready, 0));
+            const float* src = nullptr;
+            if (tr.ipcg.linked) {
+                ipcg_wait(r2, kind, ++tr.ipcg.recv_seq[kind][r2]);
+                src = peer_of(r2, dst);
+            } else {
+                if (!tr.group) throw Error(GP_EFABRIC, "hybrid worker without a group link");
+                LocalQueue::Msg m;
+                wait_local(tr.group->at(r2, grank, kind), tag, m);
+                GP_CUDA(cudaStreamWaitEvent(cs, m.ready, 0));
+                src = m.src[0].ptr;
+            }
             const uint32_t a = pull_off[size_t(r2) * (K + 1) + k_lo], b = pull_off[size_t(r2) * (K + 1) + k_hi];
             if (b == a) continue;
-            PullParams p{pull_idx + a, b - a, m.src[0].ptr, dst, stride, dstG, gstride, width, orig, key};
+            PullParams p{pull_idx + a, b - a, src, dst, stride, dstG, gstride, width, orig, key};
             launch(GP_K_XFER, double(b - a) * width * (dstG ? 12.0 : 8.0), 0, 0,
                    [&]() { k_pull_rows<<<row_grid(b - a, (const void*)k_pull_rows, 0), kBlock, 0, cs>>>(p); });
         }
@@ -1583,7 +1748,6 @@ struct Stage {
 
     // group_weight_sync: rank 0 folds in rank order and everyone takes its result.
     void group_sync_grads() {
-        auto& gl = *tr.group;
         std::vector<Piece> mine;
         uint64_t values = 0;
         for (auto& d : L) {
@@ -1594,6 +1758,40 @@ struct Stage {
                 values += d.dout;
             }
         }
+        if (tr.ipcg.linked) {
+            // counters: 2 grads ready (-> rank 0), 3 fold done (-> rank r), 4 copied (-> rank 0)
+            const uint32_t seq = ++tr.ipcg.sync_seq;
+            if (grank != 0) {
+                ipcg_signal(0, 2, seq);
+                ipcg_wait(0, 3, seq);
+                for (auto& m : mine)
+                    GP_CUDA(cudaMemcpyAsync(m.ptr, peer_of(0, m.ptr), m.floats * 4, cudaMemcpyDefault, cs));
+                ipcg_signal(0, 4, seq);
+                bytes_sent[4] += values * 4;
+                ++msgs_sent[4];
+                return;
+            }
+            for (uint32_t r2 = 1; r2 < G; ++r2) ipcg_wait(r2, 2, seq);
+            for (auto& m : mine) {
+                FoldParams f{};
+                f.src[0] = m.ptr;
+                for (uint32_t r2 = 1; r2 < G; ++r2) f.src[r2] = peer_of(r2, m.ptr);
+                f.dst = m.ptr;
+                f.G = G;
+                f.n = uint32_t(m.floats);
+                launch(GP_K_XFER, double(f.n) * 4.0 * (G + 1), 0, 0,
+                       [&]() { k_group_fold<<<(f.n + 255) / 256, 256, 0, cs>>>(f); });
+            }
+            for (uint32_t r2 = 1; r2 < G; ++r2) ipcg_signal(r2, 3, seq);
+            // the folded result lives in this rank's gradient buffers, which the next
+            // epoch overwrites: wait until every peer has copied it
+            for (uint32_t r2 = 1; r2 < G; ++r2) ipcg_wait(r2, 4, seq);
+            bytes_sent[4] += uint64_t(G - 1) * values * 4;
+            msgs_sent[4] += G - 1;
+            return;
+        }
+        if (!tr.group) throw Error(GP_EFABRIC, "hybrid worker without a group link");
+        auto& gl = *tr.group;
         if (grank != 0) {
             cudaEvent_t ev = pool_event();
             GP_CUDA(cudaEventRecord(ev, cs));
@@ -1839,7 +2037,7 @@ struct Stage {
 
         param_step();
         GP_CUDA(cudaEventRecord(ev_end, cs));
-        if (tr.ipc_up.linked() || tr.ipc_down.linked()) {
+        if (tr.ipc_up.linked() || tr.ipc_down.linked() || tr.ipcg.linked) {
             sync_watchdog(cs, 600.0);
             for (cudaStream_t st : {tr.ipc_up.stream, tr.ipc_down.stream, tr.ipc_up.rstream, tr.ipc_down.rstream})
                 if (st) sync_watchdog(st, 600.0);
@@ -2087,6 +2285,17 @@ gp_status gp_ipc_export(gp_ctx* ctx, uint8_t* up_blob, uint8_t* down_blob) {
 
 gp_status gp_link_ipc(gp_ctx* ctx, const uint8_t* up_peer_blob, const uint8_t* down_peer_blob) {
     return gp::guard(&ctx->st, [&]() { ctx->st.ipc_link(up_peer_blob, down_peer_blob); });
+}
+
+gp_status gp_group_export(gp_ctx* ctx, uint8_t* blob, uint64_t capacity, uint64_t* length) {
+    return gp::guard(&ctx->st, [&]() {
+        const size_t need = ctx->st.group_export(blob, capacity);
+        if (length) *length = need;
+    });
+}
+
+gp_status gp_link_group_ipc(gp_ctx* ctx, const uint8_t* const* blobs, const uint64_t* lengths) {
+    return gp::guard(&ctx->st, [&]() { ctx->st.group_link_ipc(blobs, lengths); });
 }
 
 void gp_abort(gp_ctx* ctx) {

@@ -101,6 +101,22 @@ def exchange_ipc_blobs(dist, rank: int, world: int, mine) -> Tuple[Optional[byte
     return up, down
 
 
+def exchange_group_blobs(dist, stage: int, grank: int, group_size: int, blob: bytes) -> List[Optional[bytes]]:
+    """All-gather (stage, group rank, blob) and return the blobs of this stage's group
+    in group-rank order (for StageEngine.link_group_ipc)."""
+    world = dist.get_world_size() if dist is not None and dist.is_initialized() else 1
+    allb = [None] * world
+    if world > 1:
+        dist.all_gather_object(allb, (stage, grank, blob))
+    else:
+        allb[0] = (stage, grank, blob)
+    out: List[Optional[bytes]] = [None] * group_size
+    for st, r, b in allb:
+        if st == stage:
+            out[r] = b
+    return out
+
+
 def max_over_ranks(dist, x: float) -> float:
     if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
         return x

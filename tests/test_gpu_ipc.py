@@ -122,3 +122,76 @@ def test_ipc_link_errors(gp):
         b.link_ipc(bytes(gp.IPC_BLOB_BYTES), None)
     for e in (a, b, c):
         e.close()
+
+
+HYB_IPC = [
+    # kind, L, H, S, G, K, chunk seed, part seed, epochs, seed, staleness
+    dict(kind=2, L=5, H=16, S=1, G=2, K=4, cs=3, ps=2, epochs=6, seed=43, fix_alpha=3),
+    dict(kind=0, L=4, H=16, S=2, G=2, K=4, cs=3, ps=1, epochs=5, seed=42, fix_alpha=3),
+    dict(kind=2, L=5, H=16, S=1, G=3, K=3, cs=5, ps=3, epochs=4, seed=44, sync=True),
+    dict(kind=0, L=6, H=12, S=2, G=2, K=6, cs=7, ps=4, epochs=4, seed=45, fix_alpha=2, hist=True),
+]
+
+
+@pytest.mark.parametrize("case", HYB_IPC, ids=[f"k{c['kind']}_s{c['S']}g{c['G']}" for c in HYB_IPC])
+def test_ipc_hybrid_processes_match_in_process_hybrid(gp, tmp_path, case):
+    """S x G worker processes (gp_link_group_ipc + gp_link_ipc) == train_hybrid in one
+    process (gp_link_group + gp_link_local), bit for bit."""
+    import json
+    out = str(tmp_path / "hyb.npz")
+    W = case["S"] * case["G"]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={W}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.join(HERE, "ipc_hybrid_worker.py"),
+           out, json.dumps(case)]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    z = np.load(out)
+    ds = gp.Dataset.synthetic_er(500, 0.02, 3, 16, 5, 9)
+    part, _, _ = gp.partition_vertices(ds, case["G"], case["ps"])
+    co = gp.make_chunks(ds, case["K"], case["cs"])
+    kw = {}
+    if "fix_alpha" in case:
+        kw["fix_alpha"] = case["fix_alpha"]
+    if case.get("hist"):
+        kw["historical_gradients"] = True
+    if case.get("sync"):
+        kw["synchronous_mode"] = True
+    opt = gp.TrainOptions(model=gp.ModelConfig(kind=case["kind"], layers=case["L"], hidden=case["H"]),
+                          epochs=case["epochs"], seed=case["seed"], **kw)
+    res = gp.train_hybrid(ds, part, co, case["S"], opt)
+    x, lab, sp = ds.arrays()
+    np.testing.assert_allclose(z["loss_sum"] / float((sp == 1).sum()), res.train_loss, rtol=1e-12, atol=0)
+    for l, (Wr, br) in enumerate(res.params):
+        assert np.array_equal(z[f"W{l}"].view(np.uint32), Wr.view(np.uint32)), f"W{l} differs"
+        if br.size:
+            assert np.array_equal(z[f"b{l}"].view(np.uint32), br.view(np.uint32)), f"b{l} differs"
+
+
+def test_group_link_errors(gp):
+    ds = gp.Dataset.synthetic_er(500, 0.02, 3, 16, 5, 9)
+    model = gp.ModelConfig(kind=0, layers=3, hidden=8)
+    specs = gp.build_layer_specs(model, ds.num_features, ds.num_classes)
+    part, _, _ = gp.partition_vertices(ds, 2, 1)
+    co = gp.make_chunks(ds, 2, 1)
+    off, cols, vals = ds.normalize_adjacency(True)
+
+    def member(r, G=2):
+        e = gp.StageEngine(num_vertices=ds.num_vertices, num_chunks=2, specs=specs, stage=0, num_stages=1,
+                           layer_range=(0, 3), hidden=8, num_classes=ds.num_classes, dropout=0.5, seed=1,
+                           group_size=G, group_rank=r)
+        if G > 1:
+            e.upload_partition(part)
+        e.upload_graph(off, cols, vals, co)
+        return e
+
+    solo = member(0, G=1)
+    with pytest.raises(gp.InvalidArgument, match="not a hybrid worker"):
+        solo.group_export()
+    a, b = member(0), member(1)
+    ba, bb = a.group_export(), b.group_export()
+    with pytest.raises(gp.InvalidArgument, match="does not match"):
+        a.link_group_ipc([None, ba])  # rank 0's own blob offered as rank 1
+    with pytest.raises(gp.InvalidArgument, match="not a group blob"):
+        a.link_group_ipc([None, bytes(len(bb))])
+    for e in (solo, a, b):
+        e.close()
