@@ -32,6 +32,7 @@
 #include <vector>
 
 #include "../../../include/gnnpipe.h"
+#include "dense_tile.cuh"
 #include "rows8.cuh"
 #include "tc_pgrad.cuh"
 
@@ -259,6 +260,7 @@ struct LayerDev {
     uint32_t sin, sout;  // padded strides
     bool agg;
     float *W = nullptr, *b = nullptr, *gW = nullptr, *gb = nullptr;
+    float* WT = nullptr;  // W^T, refreshed whenever W changes (set_params, optimizer step)
     float *mW = nullptr, *vW = nullptr, *mb = nullptr, *vb = nullptr;
     float *h = nullptr, *hs = nullptr;   // h_cur / h_snap
     float *pre = nullptr, *dz = nullptr;
@@ -477,6 +479,7 @@ struct Stage {
             const bool bias = d.spec.kind != GP_GCN2CONV;
             const size_t wn = size_t(d.din) * d.dout;
             d.W = dalloc<float>(wn);
+            d.WT = dalloc<float>(wn);
             d.gW = dalloc<float>(wn);
             d.mW = dalloc<float>(wn);
             d.vW = dalloc<float>(wn);
@@ -539,10 +542,12 @@ struct Stage {
 
     // Gathers in flight per lane (template NB of the row kernels); GP_NB overrides.
     int nb = 2;
-    // GP_SPLIT=1: aggregating layers run as two kernels, the latency-bound gather
-    // (-> pre / dz) and the row transform (GEMV + epilogue). Default: fused (one
-    // kernel; measured faster at Reddit shape for K = 4..32 chunks).
-    bool split_rows = false;
+    // Aggregating layers run as two kernels (default): the gather (-> pre / dz)
+    // and the register-tiled row transform + epilogue (k_fwd_tile / k_bwd_tile,
+    // dense_tile.cuh). GP_SPLIT=0: one fused kernel with a 2-rows-per-warp GEMV
+    // (its shared-memory wavefronts compete with the gather). Reddit shape, one
+    // B200: split 0.439 vs fused 0.450 s/epoch at K = 4, 0.465 vs 0.519 at K = 32.
+    bool split_rows = true;
 
     // Row kernels stage a weight matrix (+ x rows; <= 100 KB) in shared memory;
     // gathers bypass L1 (no_allocate), so the unified carveout goes to shared memory.
@@ -571,6 +576,17 @@ struct Stage {
             GP_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
                                          int(cudaSharedmemCarveoutMaxShared)));
         }
+        const void* tiles[] = {(const void*)k_fwd_tile<false, 1>, (const void*)k_fwd_tile<true, 1>,
+                               (const void*)k_fwd_tile<false, 2>, (const void*)k_fwd_tile<true, 2>,
+                               (const void*)k_fwd_tile<false, 4>, (const void*)k_fwd_tile<true, 4>,
+                               (const void*)k_bwd_tile<1>,        (const void*)k_bwd_tile<2>,
+                               (const void*)k_bwd_tile<4>};
+        for (const void* f : tiles) {
+            GP_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(tile_smem_bytes(kMaxWidth, kMaxWidth, 4))));
+            GP_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                         int(cudaSharedmemCarveoutMaxShared)));
+        }
     }
 
     // Parameter gradients on tcgen05 (default) or CUDA cores (GP_PGRAD=simt).
@@ -583,7 +599,7 @@ struct Stage {
             const int v = std::atoi(e);
             if (v == 2 || v == 4) nb = v;
         }
-        if (const char* e = std::getenv("GP_SPLIT")) split_rows = std::string(e) == "1";
+        if (const char* e = std::getenv("GP_SPLIT")) split_rows = std::string(e) != "0";
         setup_nb<2>();
         setup_nb<4>();
     }
@@ -597,9 +613,47 @@ struct Stage {
         if (nb == 2) fwd_go<KIND, 2, SPLIT>(rows, smem, p);
         else fwd_go<KIND, 4, SPLIT>(rows, smem, p);
     }
+    // Split-path transforms: register-tiled (dense_tile.cuh), one tile of
+    // tile_geom(width).tm rows per CTA iteration.
+    uint32_t tile_grid(uint32_t rows, const void* fn, size_t smem, uint32_t tm) {
+        auto key = std::make_pair(fn, smem);
+        auto it = occ_cache.find(key);
+        int occ = 0;
+        if (it == occ_cache.end()) {
+            GP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kTileThreads, smem));
+            occ_cache[key] = occ = std::max(occ, 1);
+        } else {
+            occ = it->second;
+        }
+        const uint64_t want = (uint64_t(rows) + tm - 1) / tm;
+        return uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(want, uint64_t(num_sms) * occ)));
+    }
+    template <bool GCN2, int TR>
+    void fwd_tile_go(uint32_t rows, const FwdParams& p) {
+        const size_t smem = tile_smem_bytes(p.din, p.dout, TR);
+        const void* fn = (const void*)k_fwd_tile<GCN2, TR>;
+        k_fwd_tile<GCN2, TR><<<tile_grid(rows, fn, smem, tile_geom(p.din, p.dout, TR).tm), kTileThreads, smem, cs>>>(p);
+    }
     template <bool GCN2>
-    void fwd_dense_go(uint32_t rows, size_t smem, const FwdParams& p) {
-        k_fwd_dense8<GCN2><<<row_grid(rows, (const void*)k_fwd_dense8<GCN2>, smem, 64), kBlock, smem, cs>>>(p);
+    void fwd_dense_go(uint32_t rows, const FwdParams& p) {
+        switch (tile_rows_per_thread(rows, p.dout, num_sms)) {
+            case 4: fwd_tile_go<GCN2, 4>(rows, p); break;
+            case 2: fwd_tile_go<GCN2, 2>(rows, p); break;
+            default: fwd_tile_go<GCN2, 1>(rows, p); break;
+        }
+    }
+    template <int TR>
+    void bwd_tile_go(uint32_t rows, const BwdParams& p) {
+        const size_t smem = tile_smem_bytes(p.dout, p.din, TR);
+        const void* fn = (const void*)k_bwd_tile<TR>;
+        k_bwd_tile<TR><<<tile_grid(rows, fn, smem, tile_geom(p.dout, p.din, TR).tm), kTileThreads, smem, cs>>>(p);
+    }
+    void bwd_dense_go(uint32_t rows, const BwdParams& p) {
+        switch (tile_rows_per_thread(rows, p.din, num_sms)) {
+            case 4: bwd_tile_go<4>(rows, p); break;
+            case 2: bwd_tile_go<2>(rows, p); break;
+            default: bwd_tile_go<1>(rows, p); break;
+        }
     }
     template <int PREV, int OUT, int NB, bool SPLIT = false>
     void bwd_go(uint32_t rows, size_t smem, const BwdParams& p) {
@@ -807,10 +861,18 @@ struct Stage {
         return L[l - lb];
     }
 
+    void transpose_w(const LayerDev& d) {
+        const uint32_t nw = d.din * d.dout;
+        launch(GP_K_OPTIM, nw * 8.0, 0, 0,
+               [&]() { k_transpose<<<(nw + 255) / 256, 256, 0, cs>>>(d.W, d.WT, d.din, d.dout); });
+    }
+
     void set_params(uint32_t l, const float* W, const float* b) {
         GP_CUDA(cudaSetDevice(device));
         auto& d = layer(l);
         GP_CUDA(cudaMemcpy(d.W, W, size_t(d.din) * d.dout * 4, cudaMemcpyHostToDevice));
+        transpose_w(d);
+        GP_CUDA(cudaStreamSynchronize(cs));
         if (d.b) {
             if (!b) throw Error(GP_EINVAL, "layer has a bias");
             GP_CUDA(cudaMemcpy(d.b, b, size_t(d.dout) * 4, cudaMemcpyHostToDevice));
@@ -980,10 +1042,9 @@ struct Stage {
                     if (g2) fwd_nb<FWD_GCN2, true>(rows, kEdgeSlotBytes, p);
                     else fwd_nb<FWD_GCN, true>(rows, kEdgeSlotBytes, p);
                 });
-                const size_t dsm = row_smem_bytes(d.din, d.dout, kDenseRows);
                 launch(GP_K_FWD_DENSE, db, 2.0 * double(rows) * d.din * d.dout, 0, [&]() {
-                    if (g2) fwd_dense_go<true>(rows, dsm, p);
-                    else fwd_dense_go<false>(rows, dsm, p);
+                    if (g2) fwd_dense_go<true>(rows, p);
+                    else fwd_dense_go<false>(rows, p);
                 });
                 return;
             }
@@ -1081,6 +1142,7 @@ struct Stage {
         p.dz = d.dz;
         p.dzstride = d.sout;
         p.W = d.W;
+        p.WT = d.WT;
         p.din = d.din;
         p.dout = d.dout;
         p.need_dagg = d.l > 0;
@@ -1110,10 +1172,7 @@ struct Stage {
             if (p.need_dagg) {
                 const double db = double(rows) * (d.dout + d.din) * 4.0 + (p.gcn2 ? double(rows) * d.din * 8.0 : 0.0) +
                                   double(d.din) * d.dout * 4.0;
-                const size_t dsm = row_smem_bytes(d.dout, d.din, kDenseRows);
-                launch(GP_K_BWD_DENSE, db, 2.0 * double(rows) * d.din * d.dout, 0, [&]() {
-                    k_bwd_dense8<<<row_grid(rows, (const void*)k_bwd_dense8, dsm, 64), kBlock, dsm, cs>>>(p);
-                });
+                launch(GP_K_BWD_DENSE, db, 2.0 * double(rows) * d.din * d.dout, 0, [&]() { bwd_dense_go(rows, p); });
             }
             return;
         }
@@ -1237,6 +1296,7 @@ struct Stage {
             a.v = d.vW;
             a.n = d.din * d.dout;
             launch(GP_K_OPTIM, a.n * 20.0, 0, 0, [&]() { k_adam<<<(a.n + 255) / 256, 256, 0, cs>>>(a); });
+            transpose_w(d);
             if (d.b) {
                 a.p = d.b;
                 a.g = d.gb;

@@ -388,6 +388,7 @@ struct BwdParams {
     float* dz;
     uint32_t dzstride;
     const float* W;
+    const float* WT;  // W^T (dout x din), staged by the split path's k_bwd_tile
     uint32_t din, dout;
     uint32_t need_dagg;
     uint32_t gcn2;

@@ -11,6 +11,7 @@
 #include <string>
 #include <vector>
 
+#include "dense_tile.cuh"
 #include "rows8.cuh"  // -I paper_2308_10087_b200/csrc/device (or an older copy, to compare)
 
 using namespace gp;
@@ -264,6 +265,12 @@ int main(int argc, char** argv) {
         q.dz = dz;
         q.dzstride = S8;
         q.W = W;
+        {
+            float* WT;
+            CK(cudaMalloc(&WT, H * H * 4));
+            k_transpose<<<40, 256>>>(W, WT, H, H);
+            q.WT = WT;
+        }
         q.din = H, q.dout = H;
         q.need_dagg = 1;
         q.gcn2 = 1;
@@ -303,6 +310,7 @@ int main(int argc, char** argv) {
             runb("split k_bwd8<AGG,LAYER,2,1>", (const void*)k_bwd8<PREV_AGG, OUT_LAYER, 2, true>, done);
             runb("split k_bwd8<AGG,LAYER,4,1>", (const void*)k_bwd8<PREV_AGG, OUT_LAYER, 4, true>, done);
             runb("split k_bwd_dense8", (const void*)k_bwd_dense8, done, dsm);
+            runb("split k_bwd_tile<4>", (const void*)k_bwd_tile<4>, done, tile_smem_bytes(H, H, 4));
         }
         runb("k_bwd8<AGG_HIST,LAYER,2>", (const void*)k_bwd8<PREV_AGG_HIST, OUT_LAYER, 2>, 0x3ull);
         std::vector<float> hb(tab);
@@ -323,6 +331,28 @@ int main(int argc, char** argv) {
             uint64_t hsh = 1469598103934665603ull;
             for (size_t i = 0; i < tab; ++i) hsh = (hsh ^ reinterpret_cast<uint32_t&>(hb[i])) * 1099511628211ull;
             printf("bwd bg checksum (done=0x3, all rows): %016llx\n", (unsigned long long)hsh);
+            // split gather + tiled transform must reproduce bg and dh0 bit for bit
+            std::vector<float> hd0(tab), gb(tab), gd0(tab);
+            CK(cudaMemcpy(hd0.data(), dh0, tab * 4, cudaMemcpyDeviceToHost));
+            const void* fns[2] = {(const void*)k_bwd8<PREV_AGG, OUT_LAYER, 2, true>, (const void*)k_bwd_tile<4>};
+            const size_t sms[2] = {kEdgeSlotBytes, tile_smem_bytes(H, H, 4)};
+            CK(cudaMemset(dh0, 0, tab * 4));
+            CK(cudaMemset(bg, 0, tab * 4));
+            for (int f = 0; f < 2; ++f) {
+                x.ticket = tickets + 301 + f;
+                CK(cudaMemset(x.ticket, 0, 4));
+                CK(cudaFuncSetAttribute(fns[f], cudaFuncAttributeMaxDynamicSharedMemorySize, int(sms[f])));
+                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fns[f], kBlock, sms[f]));
+                CK(cudaLaunchKernel(fns[f], dim3(nsm * occ), dim3(kBlock), args, sms[f], 0));
+            }
+            CK(cudaDeviceSynchronize());
+            CK(cudaMemcpy(gb.data(), bg, tab * 4, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(gd0.data(), dh0, tab * 4, cudaMemcpyDeviceToHost));
+            size_t bad = 0;
+            for (size_t i = 0; i < tab; ++i)
+                bad += (reinterpret_cast<uint32_t&>(hb[i]) != reinterpret_cast<uint32_t&>(gb[i])) +
+                       (reinterpret_cast<uint32_t&>(hd0[i]) != reinterpret_cast<uint32_t&>(gd0[i]));
+            printf("bwd split (gather + tile) vs fused: %zu differing floats\n", bad);
         }
     }
     std::vector<float> ref(tab), got(tab);
@@ -333,6 +363,9 @@ int main(int argc, char** argv) {
         run("split gather k_fwd8<GCN2,2,1>", (const void*)k_fwd8<FWD_GCN2, 2, true>, kEdgeSlotBytes, K);
         run("split gather k_fwd8<GCN2,4,1>", (const void*)k_fwd8<FWD_GCN2, 4, true>, kEdgeSlotBytes, K);
         run("split dense k_fwd_dense8<1>", (const void*)k_fwd_dense8<true>, dsm, K);
+        run("split dense k_fwd_tile<1,4>", (const void*)k_fwd_tile<true, 4>, tile_smem_bytes(H, H, 4), K);
+        run("split dense k_fwd_tile<1,2>", (const void*)k_fwd_tile<true, 2>, tile_smem_bytes(H, H, 2), K);
+        run("split dense k_fwd_tile<1,1>", (const void*)k_fwd_tile<true, 1>, tile_smem_bytes(H, H, 1), K);
         run("k_fwd8 again", (const void*)k_fwd8<FWD_GCN2, 2>, wsm, K);
     }
     // bit-equality of the variants over all rows (K=1 launch)
@@ -363,6 +396,12 @@ int main(int argc, char** argv) {
         size_t bad = 0;
         for (size_t i = 0; i < tab; ++i) bad += (reinterpret_cast<uint32_t&>(ref[i]) != reinterpret_cast<uint32_t&>(got[i]));
         printf("split (gather + dense) vs fused: %zu differing floats\n", bad);
+        full((const void*)k_fwd8<FWD_GCN2, 2, true>, kEdgeSlotBytes);
+        full((const void*)k_fwd_tile<true, 2>, tile_smem_bytes(H, H, 2));
+        snap(got);
+        bad = 0;
+        for (size_t i = 0; i < tab; ++i) bad += (reinterpret_cast<uint32_t&>(ref[i]) != reinterpret_cast<uint32_t&>(got[i]));
+        printf("split (gather + tile) vs fused: %zu differing floats\n", bad);
     }
     return 0;
 }

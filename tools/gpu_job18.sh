@@ -1,0 +1,6 @@
+#!/bin/bash
+mkdir -p gpurun_out
+for K in 4 32; do for s in 0 1; do
+GP_SPLIT=$s timeout 300 python bench.py --steps 5 --warmup 3 --chunks $K --no-e2e --no-cpu-baseline > gpurun_out/j18_K${K}_s$s.json 2>/dev/null
+python -c "import json;d=json.load(open('gpurun_out/j18_K${K}_s$s.json'));print('K=$K split=$s', round(d['value'],4), d['kernel_ms_per_epoch'], d['loss_last'])"
+done; done
