@@ -9,6 +9,8 @@
 // the one-process-per-GPU NCCL path is driven directly through the C-ABI
 // (bench.py).
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <condition_variable>
 #include <cstring>
 #include <exception>
@@ -64,6 +66,22 @@ class StageBarrier {
     bool aborted_ = false;
 };
 
+// GP_HOST_TIMING=1: wall time of each phase of a trainer call on stderr (e2e diagnosis).
+struct PhaseTimer {
+    bool on = false;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    PhaseTimer() {
+        const char* e = std::getenv("GP_HOST_TIMING");
+        on = e && std::string(e) == "1";
+    }
+    void mark(const char* what) {
+        if (!on) return;
+        const auto t1 = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[gp host] %-20s %8.3f s\n", what, std::chrono::duration<double>(t1 - t0).count());
+        t0 = t1;
+    }
+};
+
 gp_layer_spec to_gp(const LayerSpec& s) {
     gp_layer_spec g{};
     g.kind = uint32_t(s.kind);
@@ -106,10 +124,12 @@ namespace {
 TrainResult<float> run_hybrid_f32(const Dataset& ds, const Partition* part, const ChunkPlan& plan,
                                   const StageAssignment& sa, uint32_t G, const std::vector<uint32_t>& worker_id,
                                   std::vector<uint32_t> node_of, const TrainOptions<float>& opt) {
+    PhaseTimer timer;
     ds.validate();
     const auto specs = build_layer_specs(opt.model, ds.num_features(), ds.num_classes);
     const uint32_t L = uint32_t(specs.size());
     validate_run(ds, plan, sa, L);
+    timer.mark("validate");
     const uint32_t S = sa.num_stages, K = plan.num_chunks, W = S * G;
     const VertexId n = ds.num_vertices();
     uint64_t split_count[3] = {0, 0, 0};
@@ -123,7 +143,9 @@ TrainResult<float> run_hybrid_f32(const Dataset& ds, const Partition* part, cons
     std::vector<gp_layer_spec> gspecs;
     for (const auto& s : specs) gspecs.push_back(to_gp(s));
     const auto adj = normalize_adjacency<float>(ds.graph, opt.model.self_loops);
+    timer.mark("normalize_adjacency");
     auto params = init_params<float>(specs, opt.seed);
+    timer.mark("init_params");
 
     int ndev = 0;
     gp_device_count(&ndev);
@@ -180,6 +202,7 @@ TrainResult<float> run_hybrid_f32(const Dataset& ds, const Partition* part, cons
         for (uint32_t s = 0; s < S; ++s)
             check(gp_link_group(&ctx.v[size_t(s) * G], G), ctx.v[size_t(s) * G], "gp_link_group");
 
+    timer.mark("create+upload");
     const uint32_t T = opt.epochs;
     std::vector<std::vector<gp_epoch_stats>> stats(W, std::vector<gp_epoch_stats>(T));
     std::vector<std::exception_ptr> errs(W);
@@ -206,6 +229,7 @@ TrainResult<float> run_hybrid_f32(const Dataset& ds, const Partition* part, cons
         for (uint32_t w = 0; w < W; ++w) pool.emplace_back(body, w);
         for (auto& th : pool) th.join();
     }
+    timer.mark("epochs");
     // Prefer the root cause over "transport aborted" follow-on errors.
     for (uint32_t pass = 0; pass < 2; ++pass)
         for (uint32_t w = 0; w < W; ++w) {
@@ -290,6 +314,7 @@ TrainResult<float> run_hybrid_f32(const Dataset& ds, const Partition* part, cons
             res.profile.gather_bytes[k] += pr.gather_bytes[k];
         }
     }
+    timer.mark("results");
     return res;
 }
 
