@@ -362,7 +362,7 @@ def main():
         "e2e": e2e,
         "gpu_launches": int(launches),
         "edges_per_s": edges_per_s,
-        "roofline": {"kernel": "k_fwd8<FWD_GCN2> (CSR SpMM + GCNII mix + W + ReLU + next-layer dropout)",
+        "roofline": {"kernel": "k_fwd8<FWD_GCN2, split> (CSR SpMM gather + GCNII initial-residual mix -> pre; the transform runs in k_fwd_tile)",
                      "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": (achieved / hbm) if achieved else None, "peak_source": src, "traffic": traffic,
                      "l2_gather_gbs": gather_rate,

@@ -208,6 +208,30 @@ gp_status gp_run_epoch(gp_ctx* ctx, uint32_t t, const uint32_t* order, gp_epoch_
 gp_status gp_download(gp_ctx* ctx, uint32_t which, uint32_t local_layer, float* out,
                       uint64_t count);
 gp_status gp_set_profiling(gp_ctx* ctx, int enable);
+
+/* Trace of a stage's epochs (replaces the simulated-clock trace of the fabric,
+ * TraceEvent fabric.hpp, Fabric::trace fabric.cpp:256-264; collect_trace
+ * fabric.cpp:222-227). Kinds follow TraceEvent::Kind. Times are the device's
+ * %globaltimer in nanoseconds (one timebase for all stages of a node); a
+ * compute span covers one chunk's layers [layer_lo, layer_hi] of the stage
+ * (chunk -1: the whole partition in synchronous mode, or the epoch-close
+ * parameter step). Tracing runs chunks serially (no wavefront). */
+enum { GP_TRACE_COMPUTE = 0, GP_TRACE_SEND = 1, GP_TRACE_RECV = 2, GP_TRACE_IDLE = 3 };
+typedef struct {
+    uint32_t epoch;
+    uint32_t kind;
+    int32_t chunk;
+    int32_t layer_lo;
+    int32_t layer_hi;
+    uint32_t reserved;
+    double t_start_ns;
+    double t_end_ns;
+} gp_trace_event;
+gp_status gp_set_trace(gp_ctx* ctx, int enable);
+/* Copies up to `cap` resolved events (all epochs since the last clear) into
+ * `out` (may be NULL) and stores the total in *count. */
+gp_status gp_get_trace(gp_ctx* ctx, gp_trace_event* out, uint64_t cap, uint64_t* count);
+gp_status gp_clear_trace(gp_ctx* ctx);
 gp_status gp_get_profile(gp_ctx* ctx, gp_profile* out);
 gp_status gp_reset_profile(gp_ctx* ctx);
 gp_status gp_device_bytes(gp_ctx* ctx, uint64_t* out); /* stash footprint */
@@ -241,7 +265,27 @@ typedef struct {
     uint32_t shuffle_chunks, fix_alpha, historical_gradients, synchronous_mode;
     int32_t device;       /* first CUDA device; stages are placed round-robin */
     uint32_t profile;     /* collect per-kernel device times                  */
+    uint32_t collect_trace; /* FabricOptions::collect_trace (fabric.hpp): measured trace */
 } gs_train_options;       /* TrainOptions engines.hpp:69-77 */
+
+/* TraceEvent (fabric.hpp): seconds from the first event of the run. */
+typedef struct {
+    uint32_t worker;
+    uint32_t kind;        /* GP_TRACE_* (TraceEvent::Kind order) */
+    int32_t chunk, layer_lo, layer_hi;
+    uint32_t reserved;
+    double t_start, t_end;
+} gs_trace_event;
+
+typedef struct {
+    double measured_bubble, ideal_bubble;
+    uint32_t stages, chunks;
+    double span;
+} gs_bubble_report;       /* BubbleReport analytics.hpp:47-54 */
+
+typedef struct {
+    double n, layers, hidden, stages, ways, alpha, vecs, bytes_per_value;
+} gs_comm_model_input;    /* CommModelInput analytics.hpp:14-24 */
 
 const char* gs_last_error(void);
 
@@ -290,6 +334,27 @@ int gs_result_metrics(const gs_result* r, uint32_t* epochs, double* metrics,
                       uint64_t* comm /* T x {graph, pipeline, weightsync} */);
 int gs_result_params(const gs_result* r, float* flat);
 int gs_result_profile(const gs_result* r, gp_profile* out);
+/* Measured trace (collect_trace runs): copies up to cap events, *count = total. */
+int gs_result_trace(const gs_result* r, gs_trace_event* out, uint64_t cap, uint64_t* count);
+/* Communication ledger: T x 6 tags x 2 link classes (EpochComm::by_tag_link). */
+int gs_result_ledger(const gs_result* r, uint64_t* out);
+
+/* Run outputs and analytics (engines.cpp:23-38, fabric.cpp:136-182,
+ * analytics.cpp:12-103). */
+int gs_write_metrics_csv(const char* path, const double* metrics /* T x 7 as gs_result_metrics */,
+                         const uint64_t* comm /* T x 3 */, uint32_t epochs);
+int gs_write_trace_jsonl(const char* path, const gs_trace_event* events, uint64_t n);
+int gs_write_comm_report_csv(const char* path, const uint64_t* ledger /* T x 6 x 2 */, uint32_t epochs);
+int gs_bubble_analysis(const gs_trace_event* events, uint64_t n, gs_bubble_report* out);
+int gs_comm_volumes(const gs_comm_model_input* in, double* graph, double* pipeline, double* hybrid);
+/* crossover_report (analytics.cpp:26-56): bytes[3] = graph, pipeline, hybrid;
+ * text = "winner\nordering (comma-separated)\ntie 0|1\ninequality lines...". */
+int gs_crossover_report(const gs_comm_model_input* graph_in, const gs_comm_model_input* pipe_in,
+                        const gs_comm_model_input* hybrid_in, double* bytes, char* text, uint64_t cap);
+/* write_compare_csv (analytics.cpp:88-103): modes = n newline-separated names;
+ * vals = n x 9 (N, L, H, S, W, alpha, vecs, predicted_bytes, rel_error). */
+int gs_write_compare_csv(const char* path, const char* modes, const double* vals, const uint64_t* measured,
+                         uint64_t n);
 int gs_result_peak_bytes(const gs_result* r, uint64_t* out);
 void gs_result_free(gs_result* r);
 

@@ -16,6 +16,10 @@
 //           out=...                           metrics + final params
 //   save    spec=... dir=...                 save_dataset (reference writer)
 //   bench   spec=... ...                     CPU baseline sample (see run_bench)
+//   analytics in=EVENTS dir=DIR out=...      bubble_analysis of the trace in EVENTS (one
+//                                            "worker kind chunk lo hi t0 t1" per line),
+//                                            volume_* / crossover_report of fixed inputs,
+//                                            and the reference writers' files in DIR
 //
 // Dataset spec strings:
 //   er:N:P:GSEED:F:C:FSEED   generate_er (graph.cpp:119-156) + hashed features
@@ -35,6 +39,7 @@
 #include <thread>
 #include <vector>
 
+#include "gnnsim/analytics.hpp"
 #include "gnnsim/engines.hpp"
 #include "gnnsim/partition.hpp"
 
@@ -448,6 +453,74 @@ void cmd_bench(const Args& a) {
     b.u64("num_layers", {L});
 }
 
+void cmd_analytics(const Args& a) {
+    std::ifstream in(arg(a, "in"));
+    if (!in) throw std::runtime_error("cannot read events");
+    std::vector<TraceEvent> tr;
+    uint32_t w, k;
+    int32_t c, lo, hi;
+    double t0, t1;
+    while (in >> w >> k >> c >> lo >> hi >> t0 >> t1) tr.push_back({w, t0, t1, TraceEvent::Kind(k), c, lo, hi});
+    const std::string dir = arg(a, "dir");
+    Blob b(arg(a, "out"));
+    const BubbleReport br = bubble_analysis(tr);
+    b.f64("bubble", {br.measured_bubble, br.ideal_bubble, double(br.stages), double(br.chunks), br.span});
+    write_trace_jsonl(dir + "/trace.jsonl", tr);
+    // volumes / crossover on the paper-shaped inputs (Reddit: N, L, H; alpha values)
+    std::vector<double> vols;
+    std::string cross;
+    for (double alpha : {0.0, 0.35, 2.5}) {
+        CommModelInput g, p, h;
+        g.n = p.n = h.n = 232965;
+        g.layers = p.layers = h.layers = 64;
+        g.hidden = p.hidden = h.hidden = 100;
+        g.ways = 8;
+        g.alpha = alpha;
+        p.stages = 8;
+        p.vecs = 2;
+        h.stages = 4;
+        h.ways = 2;
+        h.alpha = alpha / 3;
+        h.vecs = 2;
+        const CrossoverReport r = crossover_report(g, p, h);
+        vols.insert(vols.end(), {r.bytes_graph, r.bytes_pipeline, r.bytes_hybrid});
+        cross += r.winner + "|" + (r.tie ? "tie" : "-") + "|";
+        for (const auto& o : r.ordering) cross += o + ",";
+        for (const auto& q : r.inequalities) cross += "|" + q;
+        cross += "\n";
+    }
+    b.f64("volumes", vols);
+    b.u8("crossover", std::vector<uint8_t>(cross.begin(), cross.end()));
+    // writers: a fixed ledger / metrics / compare set
+    std::vector<CommReportRow> rows;
+    for (uint32_t e = 0; e < 3; ++e)
+        for (uint32_t t = 0; t < kNumTags; ++t)
+            for (uint32_t l = 0; l < 2; ++l) {
+                const uint64_t bytes = ((e + 1) * 1000003ull * (t + 1) + l * 77) % 5 == 0 ? 0 : (e + 1) * 123456789ull * (t + 1) + l;
+                if (bytes) rows.push_back({e, MsgTag(t), LinkClass(l), bytes, double(bytes) / double(1ull << 30)});
+            }
+    write_comm_report_csv(dir + "/comm_report.csv", rows);
+    std::vector<EpochMetrics> ms;
+    for (uint32_t e = 1; e <= 3; ++e) {
+        EpochMetrics m;
+        m.epoch = e;
+        m.train_loss = 3.7 / e;
+        m.train_acc = 0.1 * e;
+        m.val_acc = 0.09 * e;
+        m.test_acc = 0.08 * e;
+        m.comm_bytes_graph = 11 * e;
+        m.comm_bytes_pipeline = 373000000ull * e;
+        m.comm_bytes_weightsync = 7 * e;
+        m.wall_time_s = 0.4 + e * 1e-3;
+        m.bubble_fraction = 0.18 / e;
+        ms.push_back(m);
+    }
+    write_metrics_csv(dir + "/metrics.csv", ms);
+    std::vector<CompareRow> cr = {{"pipeline", 232965, 64, 100, 8, 1, 0, 2, 2.6e9, 2600000123ull, 4.7e-8},
+                                  {"graph", 1000, 4, 16, 1, 3, 0.25, 1, 128000, 127990, 7.8125e-5}};
+    write_compare_csv(dir + "/compare.csv", cr);
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -474,6 +547,7 @@ int main(int argc, char** argv) {
         else if (cmd == "train") cmd_train(a);
         else if (cmd == "save") cmd_save(a);
         else if (cmd == "bench") cmd_bench(a);
+        else if (cmd == "analytics") cmd_analytics(a);
         else {
             std::fprintf(stderr, "unknown command %s\n", cmd.c_str());
             return 2;

@@ -29,7 +29,13 @@ __all__ = [
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIBDIR = os.path.join(_HERE, "lib")
+_LIBDIR = os.environ.get("GP_LIBDIR") or os.path.join(_HERE, "lib")
+
+# Eager CUDA module loading (read by the driver at initialisation, so set before the
+# engine library makes its first CUDA call). With lazy loading, the first launch of a
+# kernel synchronises the context; two stages of one process linked by in-stream
+# waits (gp_link_ipc between threads) then deadlock on a first launch.
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
 
 GP_OK, GP_EINVAL, GP_ENUMERIC, GP_EFABRIC, GP_ECUDA, GP_ERUNTIME = 0, 1, 2, 3, 4, 5
 PROFILE_CLASSES = ["remask", "fwd_agg", "fwd_dense", "bwd_agg", "bwd_dense", "xent", "pgrad", "optim", "xfer"]
@@ -106,7 +112,29 @@ class gs_train_options(C.Structure):
                 ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double), ("epochs", C.c_uint32),
                 ("seed", C.c_uint64), ("shuffle_chunks", C.c_uint32), ("fix_alpha", C.c_uint32),
                 ("historical_gradients", C.c_uint32), ("synchronous_mode", C.c_uint32), ("device", C.c_int32),
-                ("profile", C.c_uint32)]
+                ("profile", C.c_uint32), ("collect_trace", C.c_uint32)]
+
+
+class gs_trace_event(C.Structure):
+    _fields_ = [("worker", C.c_uint32), ("kind", C.c_uint32), ("chunk", C.c_int32), ("layer_lo", C.c_int32),
+                ("layer_hi", C.c_int32), ("reserved", C.c_uint32), ("t_start", C.c_double), ("t_end", C.c_double)]
+
+
+class gs_bubble_report(C.Structure):
+    _fields_ = [("measured_bubble", C.c_double), ("ideal_bubble", C.c_double), ("stages", C.c_uint32),
+                ("chunks", C.c_uint32), ("span", C.c_double)]
+
+
+class gs_comm_model_input(C.Structure):
+    _fields_ = [(k, C.c_double) for k in ("n", "layers", "hidden", "stages", "ways", "alpha", "vecs",
+                                          "bytes_per_value")]
+
+
+# TraceEvent (fabric.hpp) as a numpy record; kind: 0 compute, 1 send, 2 recv, 3 idle
+TRACE_DTYPE = np.dtype([("worker", np.uint32), ("kind", np.uint32), ("chunk", np.int32), ("layer_lo", np.int32),
+                        ("layer_hi", np.int32), ("reserved", np.uint32), ("t_start", np.float64),
+                        ("t_end", np.float64)])
+TRACE_KINDS = ("compute", "send", "recv", "idle")
 
 
 _lib = None
@@ -156,6 +184,19 @@ def _L():
         "gs_result_params": (C.c_int, [vp, f32p]),
         "gs_result_profile": (C.c_int, [vp, P(gp_profile)]),
         "gs_result_peak_bytes": (C.c_int, [vp, u64p]),
+        "gs_result_trace": (C.c_int, [vp, vp, C.c_uint64, u64p]),
+        "gs_result_ledger": (C.c_int, [vp, u64p]),
+        "gs_write_metrics_csv": (C.c_int, [C.c_char_p, f64p, u64p, C.c_uint32]),
+        "gs_write_trace_jsonl": (C.c_int, [C.c_char_p, vp, C.c_uint64]),
+        "gs_write_comm_report_csv": (C.c_int, [C.c_char_p, u64p, C.c_uint32]),
+        "gs_bubble_analysis": (C.c_int, [vp, C.c_uint64, P(gs_bubble_report)]),
+        "gs_comm_volumes": (C.c_int, [P(gs_comm_model_input), f64p, f64p, f64p]),
+        "gs_crossover_report": (C.c_int, [P(gs_comm_model_input), P(gs_comm_model_input), P(gs_comm_model_input),
+                                          f64p, P(C.c_char), C.c_uint64]),
+        "gs_write_compare_csv": (C.c_int, [C.c_char_p, C.c_char_p, f64p, u64p, C.c_uint64]),
+        "gp_set_trace": (C.c_int, [vp, C.c_int]),
+        "gp_get_trace": (C.c_int, [vp, vp, C.c_uint64, u64p]),
+        "gp_clear_trace": (C.c_int, [vp]),
         "gs_result_free": (None, [vp]),
         "gp_abi_version": (C.c_uint32, []),
         "gp_device_count": (C.c_int, [P(C.c_int)]),
@@ -251,12 +292,13 @@ class TrainOptions:
     synchronous_mode: bool = False
     device: int = 0
     profile: bool = False
+    collect_trace: bool = False  # FabricOptions::collect_trace: measured per-chunk trace (chunks run serially)
 
     def c(self) -> gs_train_options:
         return gs_train_options(self.model.c(), 1 if self.optimizer == "sgd" else 0, self.lr, self.beta1,
                                 self.beta2, self.eps, self.epochs, self.seed, int(self.shuffle_chunks),
                                 self.fix_alpha, int(self.historical_gradients), int(self.synchronous_mode),
-                                self.device, int(self.profile))
+                                self.device, int(self.profile), int(self.collect_trace))
 
 
 @dataclass
@@ -421,10 +463,83 @@ class TrainResult:
     params: list                 # [(W, b)]
     profile: dict
     peak_buffer_bytes: int
+    trace: np.ndarray = field(default_factory=lambda: np.zeros(0, TRACE_DTYPE))  # TRACE_DTYPE records
+    ledger: np.ndarray = field(default_factory=lambda: np.zeros((0, 6, 2), np.uint64))  # T x tag x link bytes
 
     @property
     def train_loss(self) -> np.ndarray:
         return self.metrics[:, 1]
+
+
+def bubble_analysis(trace: np.ndarray) -> dict:
+    """bubble_analysis (analytics.cpp:59-86) over a measured trace."""
+    tr = np.ascontiguousarray(trace, TRACE_DTYPE)
+    out = gs_bubble_report()
+    _gs(_L().gs_bubble_analysis(tr.ctypes.data_as(C.c_void_p), tr.size, C.byref(out)))
+    return {"measured_bubble": out.measured_bubble, "ideal_bubble": out.ideal_bubble, "stages": out.stages,
+            "chunks": out.chunks, "span": out.span}
+
+
+def comm_volumes(n, layers, hidden, stages=1, ways=1, alpha=0.0, vecs=1, bytes_per_value=4) -> dict:
+    """volume_graph / volume_pipeline / volume_hybrid (analytics.cpp:12-24), bytes per epoch."""
+    c = gs_comm_model_input(n, layers, hidden, stages, ways, alpha, vecs, bytes_per_value)
+    g, p, h = C.c_double(), C.c_double(), C.c_double()
+    _gs(_L().gs_comm_volumes(C.byref(c), C.byref(g), C.byref(p), C.byref(h)))
+    return {"graph": g.value, "pipeline": p.value, "hybrid": h.value}
+
+
+@dataclass
+class CommModelInput:
+    """CommModelInput (analytics.hpp:14-24)."""
+    n: float = 0
+    layers: float = 0
+    hidden: float = 0
+    stages: float = 1
+    ways: float = 1
+    alpha: float = 0
+    vecs: float = 1
+    bytes_per_value: float = 4
+
+    def c(self) -> gs_comm_model_input:
+        return gs_comm_model_input(self.n, self.layers, self.hidden, self.stages, self.ways, self.alpha, self.vecs,
+                                   self.bytes_per_value)
+
+
+def crossover_report(graph_in: CommModelInput, pipe_in: CommModelInput, hybrid_in: CommModelInput) -> dict:
+    """crossover_report (analytics.cpp:26-56): predicted bytes, ordering, winner, inequalities."""
+    b = np.zeros(3, np.float64)
+    buf = C.create_string_buffer(4096)
+    _gs(_L().gs_crossover_report(C.byref(graph_in.c()), C.byref(pipe_in.c()), C.byref(hybrid_in.c()),
+                                 _ptr(b, C.c_double), buf, len(buf)))
+    lines = buf.value.decode().split("\n")
+    return {"bytes_graph": b[0], "bytes_pipeline": b[1], "bytes_hybrid": b[2], "winner": lines[0],
+            "ordering": lines[1].split(","), "tie": lines[2] == "1", "inequalities": lines[3:]}
+
+
+def write_compare_csv(path: str, rows) -> None:
+    """write_compare_csv (analytics.cpp:88-103); rows: dicts with mode, n, layers, hidden, stages, ways,
+    alpha, vecs, predicted_bytes, measured_bytes, rel_error."""
+    keys = ("n", "layers", "hidden", "stages", "ways", "alpha", "vecs", "predicted_bytes", "rel_error")
+    vals = np.array([[float(r[k]) for k in keys] for r in rows], np.float64).reshape(-1, 9)
+    meas = np.array([int(r["measured_bytes"]) for r in rows], np.uint64)
+    modes = "\n".join(r["mode"] for r in rows).encode()
+    _gs(_L().gs_write_compare_csv(path.encode(), modes, _ptr(vals, C.c_double), _ptr(meas, C.c_uint64), len(rows)))
+
+
+def write_run_outputs(res: "TrainResult", out_dir: str) -> None:
+    """metrics.csv, trace.jsonl and comm_report.csv of a run (gnnsim.cpp:242-258 formats)."""
+    os.makedirs(out_dir, exist_ok=True)
+    lib = _L()
+    met = np.ascontiguousarray(res.metrics, np.float64)
+    comm = np.ascontiguousarray(res.comm, np.uint64)
+    _gs(lib.gs_write_metrics_csv(os.path.join(out_dir, "metrics.csv").encode(), _ptr(met, C.c_double),
+                                 _ptr(comm, C.c_uint64), met.shape[0]))
+    tr = np.ascontiguousarray(res.trace, TRACE_DTYPE)
+    _gs(lib.gs_write_trace_jsonl(os.path.join(out_dir, "trace.jsonl").encode(), tr.ctypes.data_as(C.c_void_p),
+                                 tr.size))
+    led = np.ascontiguousarray(res.ledger, np.uint64)
+    _gs(lib.gs_write_comm_report_csv(os.path.join(out_dir, "comm_report.csv").encode(), _ptr(led, C.c_uint64),
+                                     led.shape[0]))
 
 
 def _result(h, specs) -> TrainResult:
@@ -444,7 +559,14 @@ def _result(h, specs) -> TrainResult:
         prof = {name: {"ms": pr.ms[i], "launches": pr.launches[i], "alg_bytes": pr.alg_bytes[i],
                        "flops": pr.flops[i], "gather_bytes": pr.gather_bytes[i]}
                 for i, name in enumerate(PROFILE_CLASSES)}
-        return TrainResult(met, comm, _split_params(specs, flat), prof, peak.value)
+        n = C.c_uint64()
+        _gs(lib.gs_result_trace(h, None, 0, C.byref(n)))
+        trace = np.zeros(n.value, TRACE_DTYPE)
+        if n.value:
+            _gs(lib.gs_result_trace(h, trace.ctypes.data_as(C.c_void_p), n.value, C.byref(n)))
+        ledger = np.zeros((T.value, 6, 2), np.uint64)
+        _gs(lib.gs_result_ledger(h, _ptr(ledger, C.c_uint64)))
+        return TrainResult(met, comm, _split_params(specs, flat), prof, peak.value, trace, ledger)
     finally:
         lib.gs_result_free(h)
 

@@ -127,6 +127,7 @@ struct MemOps {
 };
 MemOps g_memops;
 
+
 void cu_check(CUresult r, const char* what) {
     if (r != CUDA_SUCCESS) throw Error(GP_ECUDA, std::string(what) + " failed (CUresult " + std::to_string(int(r)) + ")");
 }
@@ -335,6 +336,23 @@ struct Stage {
     Transport tr;
     // profiling
     bool profiling = false;
+
+    // ---- trace (FabricOptions::collect_trace, fabric.cpp:222-227, :256-264) ----
+    // Per epoch: one anchor (event + %globaltimer stamp) and a pair of timing
+    // events per trace record; resolved to globaltimer nanoseconds after the
+    // epoch's synchronize. Tracing runs the chunks serially (no wavefront), so a
+    // stage's compute spans never overlap, as in the reference's worker clock.
+    bool tracing = false;
+    struct TraceRec {
+        uint32_t epoch, kind;
+        int32_t chunk, llo, lhi;
+        cudaEvent_t a, b;
+    };
+    std::vector<TraceRec> trace_pending;
+    std::vector<gp_trace_event> trace_done;
+    cudaEvent_t trace_origin = nullptr;
+    unsigned long long* trace_stamp = nullptr;  // mapped pinned host slot
+    uint32_t trace_epoch = 0;
     gp_profile prof{};
     struct Timed {
         int cls;
@@ -392,6 +410,15 @@ struct Stage {
         for (auto e : marks)
             if (e) cudaEventDestroy(e);
         if (ev_start) cudaEventDestroy(ev_start);
+        if (trace_origin) cudaEventDestroy(trace_origin);
+        if (trace_stamp) cudaFreeHost(trace_stamp);
+        {
+            std::vector<cudaEvent_t> used;
+            for (const auto& r : trace_pending) used.insert(used.end(), {r.a, r.b});
+            std::sort(used.begin(), used.end());
+            used.erase(std::unique(used.begin(), used.end()), used.end());
+            for (auto e : used) cudaEventDestroy(e);
+        }
         if (ev_end) cudaEventDestroy(ev_end);
         if (tr.up_comm) g_nccl.comm_destroy(tr.up_comm);
         if (tr.down_comm) g_nccl.comm_destroy(tr.down_comm);
@@ -536,7 +563,7 @@ struct Stage {
     static constexpr uint32_t kTickets = 16384;
     uint32_t* take_ticket() {
         if (ticket_next == kTickets) {
-            GP_CUDA(cudaMemsetAsync(tickets, 0, kTickets * 4, cs));
+            zero_words(tickets, kTickets);
             ticket_next = 0;
         }
         return tickets + ticket_next++;
@@ -594,7 +621,31 @@ struct Stage {
     // Parameter gradients on tcgen05 (default) or CUDA cores (GP_PGRAD=simt).
     bool use_tc_pgrad = true;
 
+    // Load every kernel now. With CUDA's lazy module loading the first launch of a
+    // kernel loads it, and loading synchronises the context: if another stage of
+    // this process has an in-stream wait pending on a value this stage has yet to
+    // write (gp_link_ipc peers in one process), that first launch never returns.
+    void preload_kernels() {
+        const void* fns[] = {(const void*)k_adam,        (const void*)k_copy,          (const void*)k_dense_gemm,
+                             (const void*)k_group_fold,  (const void*)k_pgrad_fold,    (const void*)k_pgrad_partial,
+                             (const void*)k_pgrad_tc,    (const void*)k_pull_rows,     (const void*)k_remask,
+                             (const void*)k_spmm_pre,    (const void*)k_stamp,         (const void*)k_transpose,
+                             (const void*)k_xent_fold,   (const void*)k_xent_grad,     (const void*)k_xent_stats,
+                             (const void*)k_zero};
+        for (const void* f : fns) {
+            cudaFuncAttributes a;
+            GP_CUDA(cudaFuncGetAttributes(&a, f));
+        }
+    }
+
+    void zero_words(uint32_t* p, size_t words) {
+        const uint32_t blocks = uint32_t(std::min<size_t>(size_t(num_sms) * 4, (words + 255) / 256));
+        k_zero<<<std::max<uint32_t>(blocks, 1), 256, 0, cs>>>(p, words);
+        GP_CUDA(cudaGetLastError());
+    }
+
     void setup_kernels() {
+        preload_kernels();
         if (const char* e = std::getenv("GP_PGRAD")) use_tc_pgrad = std::string(e) != "simt";
         GP_CUDA(cudaFuncSetAttribute(k_pgrad_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         if (const char* e = std::getenv("GP_NB")) {
@@ -602,6 +653,7 @@ struct Stage {
             if (v == 2 || v == 4) nb = v;
         }
         if (const char* e = std::getenv("GP_SPLIT")) split_rows = std::string(e) != "0";
+        if (const char* e = std::getenv("GP_IPC_SMCOPY")) ipc_smcopy = std::string(e) == "1";
         setup_nb<2>();
         setup_nb<4>();
     }
@@ -1520,6 +1572,18 @@ struct Stage {
 
     CUdeviceptr dptr(char* base, size_t off) { return CUdeviceptr(reinterpret_cast<uintptr_t>(base + off)); }
 
+    bool ipc_smcopy = false;  // GP_IPC_SMCOPY=1: message copies as kernels instead of copy-engine memcpy
+    void ipc_copy(float* dst, const float* src, size_t floats, cudaStream_t st) {
+        if (!floats) return;
+        if (ipc_smcopy) {
+            const uint32_t blocks = uint32_t(std::min<size_t>(size_t(num_sms) * 2, (floats / 4 + 255) / 256 + 1));
+            k_copy<<<blocks, 256, 0, st>>>(dst, src, floats);
+            GP_CUDA(cudaGetLastError());
+        } else {
+            GP_CUDA(cudaMemcpyAsync(dst, src, floats * 4, cudaMemcpyDefault, st));
+        }
+    }
+
     void ipc_send(IpcSide& x, uint32_t k, const std::vector<Piece>& pcs) {
         uint64_t tot = 0;
         for (const auto& p : pcs) tot += p.floats;
@@ -1534,7 +1598,7 @@ struct Stage {
                      "cuStreamWaitValue32(ack)");
         float* dst = reinterpret_cast<float*>(x.peer + kIpcRing) + size_t(slot) * x.peer_slot;
         for (const auto& p : pcs) {
-            GP_CUDA(cudaMemcpyAsync(dst, p.ptr, p.floats * 4, cudaMemcpyDefault, x.stream));
+            ipc_copy(dst, p.ptr, p.floats, x.stream);
             dst += p.floats;
         }
         cu_check(g_memops.write(x.stream, dptr(x.peer, kIpcReady), seq, CU_STREAM_WRITE_VALUE_DEFAULT),
@@ -1552,7 +1616,7 @@ struct Stage {
         cu_check(g_memops.wait(rs, dptr(x.own, kIpcReady), seq, CU_STREAM_WAIT_VALUE_GEQ), "cuStreamWaitValue32(ready)");
         const float* src = reinterpret_cast<const float*>(x.own + kIpcRing) + size_t(slot) * x.own_slot;
         for (const auto& p : pcs) {
-            GP_CUDA(cudaMemcpyAsync(p.ptr, src, p.floats * 4, cudaMemcpyDeviceToDevice, rs));
+            ipc_copy(p.ptr, src, p.floats, rs);
             src += p.floats;
         }
         cu_check(g_memops.write(rs, dptr(x.peer, kIpcAck), seq, CU_STREAM_WRITE_VALUE_DEFAULT), "cuStreamWriteValue32(ack)");
@@ -1893,12 +1957,79 @@ struct Stage {
         msgs_sent[4] += G - 1;
     }
 
+    // ---- trace helpers ----------------------------------------------------------
+    cudaEvent_t trace_mark() {
+        if (!tracing) return nullptr;
+        cudaEvent_t e = take_event();
+        GP_CUDA(cudaEventRecord(e, cs));
+        return e;
+    }
+    void trace_add(uint32_t kind, int32_t chunk, cudaEvent_t a, cudaEvent_t b) {
+        if (!tracing) return;
+        trace_pending.push_back({trace_epoch, kind, chunk, int32_t(lb), int32_t(le) - 1, a, b});
+    }
+    // Idle span while blocked on the message of chunk k, then the Recv instant
+    // (fabric.cpp:350-357).
+    template <class F>
+    void traced_recv(uint32_t k, F&& recv) {
+        cudaEvent_t a = trace_mark();
+        recv();
+        cudaEvent_t b = trace_mark();
+        trace_add(GP_TRACE_IDLE, int32_t(k), a, b);
+        trace_add(GP_TRACE_RECV, int32_t(k), b, b);
+    }
+    template <class F>
+    void traced_send(uint32_t k, F&& send) {
+        cudaEvent_t a = trace_mark();
+        trace_add(GP_TRACE_SEND, int32_t(k), a, a);  // instant at send time (fabric.cpp:293-295)
+        send();
+    }
+    void trace_begin_epoch(uint32_t t) {
+        if (!tracing) return;
+        if (!trace_origin) GP_CUDA(cudaEventCreate(&trace_origin));
+        if (!trace_stamp) GP_CUDA(cudaHostAlloc(&trace_stamp, 8, cudaHostAllocMapped));
+        trace_epoch = t;
+        GP_CUDA(cudaEventRecord(trace_origin, cs));
+        unsigned long long* dptr = nullptr;
+        GP_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dptr), trace_stamp, 0));
+        k_stamp<<<1, 1, 0, cs>>>(dptr);
+        GP_CUDA(cudaGetLastError());
+    }
+    // after the epoch's stream synchronize
+    void trace_resolve() {
+        if (trace_pending.empty()) return;
+        const double base = double(*trace_stamp);
+        auto at = [&](cudaEvent_t e) {
+            float ms = 0.f;
+            GP_CUDA(cudaEventElapsedTime(&ms, trace_origin, e));
+            return base + double(ms) * 1e6;
+        };
+        for (const auto& r : trace_pending) {
+            gp_trace_event e{};
+            e.epoch = r.epoch;
+            e.kind = r.kind;
+            e.chunk = r.chunk;
+            e.layer_lo = r.llo;
+            e.layer_hi = r.lhi;
+            e.t_start_ns = at(r.a);
+            e.t_end_ns = r.b == r.a ? e.t_start_ns : at(r.b);
+            trace_done.push_back(e);
+        }
+        // an event can close one record and open the next (idle -> recv): recycle once
+        std::vector<cudaEvent_t> used;
+        for (const auto& r : trace_pending) used.insert(used.end(), {r.a, r.b});
+        std::sort(used.begin(), used.end());
+        used.erase(std::unique(used.begin(), used.end()), used.end());
+        ev_free.insert(ev_free.end(), used.begin(), used.end());
+        trace_pending.clear();
+    }
+
     // ---- one epoch ---------------------------------------------------------------
     // ---- chunk wavefront helpers ------------------------------------------------
     // W compute streams; chunk j runs on stream j % W. Off for hybrid groups (halo
     // exchange is ordered on one stream), K = 1, and in profiling mode (clean
     // per-kernel times).
-    int wave_width() const { return G == 1 && K > 1 && !profiling ? wave_w : 1; }
+    int wave_width() const { return G == 1 && K > 1 && !profiling && !tracing ? wave_w : 1; }
     cudaStream_t wave_stream(uint32_t j, int W, cudaStream_t main) const { return j % W ? cs_side[j % W] : main; }
     cudaEvent_t record_event() {
         cudaEvent_t e = pool_event();
@@ -1936,9 +2067,10 @@ struct Stage {
         std::fill(msgs_sent, msgs_sent + 6, 0);
         launches = 0;
         tr.ev_next = 0;
-        GP_CUDA(cudaMemsetAsync(tickets, 0, kTickets * 4, cs));
+        zero_words(tickets, kTickets);
         ticket_next = 0;
         GP_CUDA(cudaEventRecord(ev_start, cs));
+        trace_begin_epoch(t);
 
         // Snapshot (engines_impl.hpp:671-679): snap := cur. Every cur row is
         // rewritten before it is read again, so a pointer swap is exact.
@@ -1986,10 +2118,9 @@ struct Stage {
                 done |= 1ull << k;  // "processed" includes the current chunk (:789)
                 cs = wave_stream(kk, W, main);
                 auto& mine = ev[kk % W];
-                if (!first) {
-                    recv_fwd(k);
-                    if (L[0].agg) remask(0, in_cur, r0, r1, drop_key(t, L[0].l, L[0].din));
-                }
+                if (!first) traced_recv(k, [&]() { recv_fwd(k); });
+                cudaEvent_t c0 = trace_mark();
+                if (!first && L[0].agg) remask(0, in_cur, r0, r1, drop_key(t, L[0].l, L[0].din));
                 if (W > 1) mine[0] = record_event();
                 for (uint32_t i = 0; i < len; ++i) {
                     if (G > 1 && L[i].agg) halo_fwd(i, k, k + 1, t);  // exchange_rows (:792-794)
@@ -1999,20 +2130,22 @@ struct Stage {
                     forward_layer(i, r0, r1, t, done);
                     if (W > 1) mine[i + 1] = record_event();
                 }
-                if (!last) send_fwd(k);
+                trace_add(GP_TRACE_COMPUTE, int32_t(k), c0, trace_mark());
+                if (!last) traced_send(k, [&]() { send_fwd(k); });
             }
             wave_join(W, main);
         } else {
-            if (!first) {
-                for (uint32_t kk = 0; kk < K; ++kk) recv_fwd(ord[kk]);
-                if (L[0].agg) remask(0, in_cur, own_begin(), own_end(), drop_key(t, L[0].l, L[0].din));
-            }
+            if (!first)
+                for (uint32_t kk = 0; kk < K; ++kk) traced_recv(ord[kk], [&]() { recv_fwd(ord[kk]); });
+            cudaEvent_t c0 = trace_mark();
+            if (!first && L[0].agg) remask(0, in_cur, own_begin(), own_end(), drop_key(t, L[0].l, L[0].din));
             for (uint32_t i = 0; i < len; ++i) {
                 if (G > 1 && L[i].agg) halo_fwd(i, 0, K, t);  // exchange_rows_full (:806-808)
                 forward_layer(i, own_begin(), own_end(), t, all_done);
             }
+            trace_add(GP_TRACE_COMPUTE, -1, c0, trace_mark());  // whole partition (:811)
             if (!last)
-                for (uint32_t kk = 0; kk < K; ++kk) send_fwd(ord[kk]);
+                for (uint32_t kk = 0; kk < K; ++kk) traced_send(ord[kk], [&]() { send_fwd(ord[kk]); });
         }
 
         // ---- metrics (last stage) ---------------------------------------------------
@@ -2023,7 +2156,7 @@ struct Stage {
             launch(GP_K_XENT, 0, 0, 0, [&]() {
                 k_xent_fold<<<1, 32, 0, cs>>>(part_loss, part_correct, xent_blocks, red_loss, red_correct);
             });
-            if (needs_h0) GP_CUDA(cudaMemsetAsync(dh0, 0, size_t(n) * pad8(H) * 4, cs));
+            if (needs_h0) zero_words(reinterpret_cast<uint32_t*>(dh0), size_t(n) * pad8(H));
         }
 
         // ---- backward ---------------------------------------------------------------
@@ -2055,12 +2188,12 @@ struct Stage {
                     for (uint32_t w = 1; w < uint32_t(W) && w <= j; ++w)
                         GP_CUDA(cudaStreamWaitEvent(cs, ev[(j - w) % W][i], 0));
                 };
+                if (!last) traced_recv(k, [&]() { recv_bwd(k); });
+                cudaEvent_t c0 = trace_mark();
                 if (last) {
                     XentParams p = xent_params(r0, r1);
                     launch(GP_K_XENT, double(r1 - r0) * L[len - 1].dout * 8.0, 0, 0,
                            [&]() { k_xent_grad<<<row_grid(r1 - r0, (const void*)k_xent_grad, 0), kBlock, 0, cs>>>(p); });
-                } else {
-                    recv_bwd(k);
                 }
                 for (uint32_t i = len; i-- > 0;) {
                     if (G > 1 && i + 1 < len && L[i + 1].agg) halo_bwd(i + 1, k, k + 1);  // (:838-844)
@@ -2072,32 +2205,38 @@ struct Stage {
                 if (!first) {
                     if (L[0].agg) wait_prev(0);
                     backward_dhin(r0, r1, t, done);
-                    send_bwd(k);
                 }
+                trace_add(GP_TRACE_COMPUTE, int32_t(k), c0, trace_mark());
+                if (!first) traced_send(k, [&]() { send_bwd(k); });
             }
             wave_join(W, main);
         } else {
             const uint64_t done = K == 64 ? ~0ull : ((1ull << K) - 1);
             const uint32_t ob = own_begin(), oe = own_end();
+            if (!last)
+                for (uint32_t kk = K; kk-- > 0;) traced_recv(ord[kk], [&]() { recv_bwd(ord[kk]); });
+            cudaEvent_t c0 = trace_mark();
             if (last) {
                 XentParams p = xent_params(ob, oe);
                 launch(GP_K_XENT, double(oe - ob) * L[len - 1].dout * 8.0, 0, 0,
                        [&]() { k_xent_grad<<<row_grid(oe - ob, (const void*)k_xent_grad, 0), kBlock, 0, cs>>>(p); });
-            } else {
-                for (uint32_t kk = K; kk-- > 0;) recv_bwd(ord[kk]);
             }
             for (uint32_t i = len; i-- > 0;) {
                 if (G > 1 && i + 1 < len && L[i + 1].agg) halo_bwd(i + 1, 0, K);
                 backward_layer(i, ob, oe, t, done);
             }
             if (G > 1 && L[0].agg) halo_bwd(0, 0, K);
-            if (!first) {
-                backward_dhin(ob, oe, t, done);
-                for (uint32_t kk = K; kk-- > 0;) send_bwd(ord[kk]);
-            }
+            if (!first) backward_dhin(ob, oe, t, done);
+            trace_add(GP_TRACE_COMPUTE, -1, c0, trace_mark());  // whole partition (:867)
+            if (!first)
+                for (uint32_t kk = K; kk-- > 0;) traced_send(ord[kk], [&]() { send_bwd(ord[kk]); });
         }
 
-        param_step();
+        {
+            cudaEvent_t c0 = trace_mark();
+            param_step();
+            trace_add(GP_TRACE_COMPUTE, -1, c0, trace_mark());  // epoch-close parameter step
+        }
         GP_CUDA(cudaEventRecord(ev_end, cs));
         if (tr.ipc_up.linked() || tr.ipc_down.linked() || tr.ipcg.linked) {
             sync_watchdog(cs, 600.0);
@@ -2139,6 +2278,7 @@ struct Stage {
         }
         timed.clear();
         st.busy_ms = busy;
+        trace_resolve();
         if (out) *out = st;
     }
 
@@ -2390,6 +2530,23 @@ gp_status gp_download(gp_ctx* ctx, uint32_t which, uint32_t local_layer, float* 
 
 gp_status gp_set_profiling(gp_ctx* ctx, int enable) {
     ctx->st.profiling = enable != 0;
+    return GP_OK;
+}
+
+gp_status gp_set_trace(gp_ctx* ctx, int enable) {
+    ctx->st.tracing = enable != 0;
+    return GP_OK;
+}
+
+gp_status gp_get_trace(gp_ctx* ctx, gp_trace_event* out, uint64_t cap, uint64_t* count) {
+    const auto& v = ctx->st.trace_done;
+    if (count) *count = v.size();
+    if (out) std::copy_n(v.begin(), std::min<uint64_t>(cap, v.size()), out);
+    return GP_OK;
+}
+
+gp_status gp_clear_trace(gp_ctx* ctx) {
+    ctx->st.trace_done.clear();
     return GP_OK;
 }
 

@@ -673,6 +673,34 @@ struct AdamParams {
     float lr, b1, b2, omb1, omb2, eps, c1, c2;
 };
 
+// Stage-message copy on the SMs (16-byte vectors when aligned): used by the IPC
+// transport instead of copy-engine memcpy when GP_IPC_SMCOPY=1.
+__global__ void k_copy(float* __restrict__ dst, const float* __restrict__ src, size_t n) {
+    const size_t tid = blockIdx.x * size_t(blockDim.x) + threadIdx.x, step = size_t(gridDim.x) * blockDim.x;
+    if (((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) == 0) {
+        const size_t n4 = n / 4;
+        for (size_t i = tid; i < n4; i += step)
+            reinterpret_cast<float4*>(dst)[i] = reinterpret_cast<const float4*>(src)[i];
+        for (size_t i = n4 * 4 + tid; i < n; i += step) dst[i] = src[i];
+    } else {
+        for (size_t i = tid; i < n; i += step) dst[i] = src[i];
+    }
+}
+
+// Zero n 32-bit words (in-epoch resets; a kernel of this module instead of the
+// runtime's memset, so nothing is loaded lazily while peers wait in-stream).
+__global__ void k_zero(uint32_t* __restrict__ p, size_t n) {
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) p[i] = 0u;
+}
+
+// Trace anchor: the device's global timer (ns) at this point of the stream, so
+// CUDA-event times of different stages (devices, processes) share one timebase.
+__global__ void k_stamp(unsigned long long* out) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    *out = t;
+}
+
 __global__ void k_adam(AdamParams a) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += gridDim.x * blockDim.x) {
         const float g = a.g[i];

@@ -1,5 +1,6 @@
 // gs_* — flat C wrappers over the C++ API (include/gnnpipe.h, host section).
 // Exceptions map to the gp_status codes of the reference's error classes.
+#include <algorithm>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -78,9 +79,23 @@ TrainOptions<float> options_of(const gs_train_options* o) {
     t.staleness.synchronous_mode = o->synchronous_mode != 0;
     t.device = o->device;
     t.profile = o->profile != 0;
+    t.fabric.collect_trace = o->collect_trace != 0;
     return t;
 }
 
+CommModelInput cmi(const gs_comm_model_input* in) {
+    if (!in) throw std::invalid_argument("null input");
+    CommModelInput c;
+    c.n = in->n;
+    c.layers = in->layers;
+    c.hidden = in->hidden;
+    c.stages = in->stages;
+    c.ways = in->ways;
+    c.alpha = in->alpha;
+    c.vecs = in->vecs;
+    c.bytes_per_value = in->bytes_per_value;
+    return c;
+}
 }  // namespace
 
 extern "C" {
@@ -319,6 +334,139 @@ int gs_result_params(const gs_result* r, float* flat) {
 
 int gs_result_profile(const gs_result* r, gp_profile* out) {
     return guarded([&]() { *out = r->r.profile; });
+}
+
+int gs_result_trace(const gs_result* r, gs_trace_event* out, uint64_t cap, uint64_t* count) {
+    return guarded([&]() {
+        const auto& tr = r->r.trace;
+        if (count) *count = tr.size();
+        for (uint64_t i = 0; out && i < std::min<uint64_t>(cap, tr.size()); ++i) {
+            const auto& e = tr[i];
+            out[i] = gs_trace_event{e.worker, uint32_t(e.kind), e.chunk, e.layer_lo, e.layer_hi, 0u, e.t_start, e.t_end};
+        }
+    });
+}
+
+int gs_result_ledger(const gs_result* r, uint64_t* out) {
+    return guarded([&]() {
+        for (size_t t = 0; t < r->r.comm.size(); ++t)
+            for (uint32_t tag = 0; tag < kNumTags; ++tag)
+                for (uint32_t l = 0; l < 2; ++l) out[(t * kNumTags + tag) * 2 + l] = r->r.comm[t].by_tag_link[tag][l];
+    });
+}
+
+namespace {
+std::vector<TraceEvent> trace_of(const gs_trace_event* ev, uint64_t n) {
+    if (n && !ev) throw std::invalid_argument("null trace");
+    std::vector<TraceEvent> v(n);
+    for (uint64_t i = 0; i < n; ++i) {
+        if (ev[i].kind > 3) throw std::invalid_argument("unknown trace event kind");
+        v[i] = TraceEvent{ev[i].worker, ev[i].t_start, ev[i].t_end, TraceEvent::Kind(ev[i].kind), ev[i].chunk,
+                          ev[i].layer_lo, ev[i].layer_hi};
+    }
+    return v;
+}
+}  // namespace
+
+int gs_write_metrics_csv(const char* path, const double* metrics, const uint64_t* comm, uint32_t epochs) {
+    return guarded([&]() {
+        if (!path || (epochs && (!metrics || !comm))) throw std::invalid_argument("null argument");
+        std::vector<EpochMetrics> m(epochs);
+        for (uint32_t t = 0; t < epochs; ++t) {
+            const double* row = metrics + 7 * size_t(t);
+            m[t].epoch = uint32_t(row[0]);
+            m[t].train_loss = row[1];
+            m[t].train_acc = row[2];
+            m[t].val_acc = row[3];
+            m[t].test_acc = row[4];
+            m[t].wall_time_s = row[5];
+            m[t].bubble_fraction = row[6];
+            m[t].comm_bytes_graph = comm[3 * size_t(t)];
+            m[t].comm_bytes_pipeline = comm[3 * size_t(t) + 1];
+            m[t].comm_bytes_weightsync = comm[3 * size_t(t) + 2];
+        }
+        write_metrics_csv(path, m);
+    });
+}
+
+int gs_write_trace_jsonl(const char* path, const gs_trace_event* events, uint64_t n) {
+    return guarded([&]() {
+        if (!path) throw std::invalid_argument("null path");
+        write_trace_jsonl(path, trace_of(events, n));
+    });
+}
+
+int gs_write_comm_report_csv(const char* path, const uint64_t* ledger, uint32_t epochs) {
+    return guarded([&]() {
+        if (!path || (epochs && !ledger)) throw std::invalid_argument("null argument");
+        std::vector<CommReportRow> rows;
+        for (uint32_t t = 0; t < epochs; ++t) {
+            EpochComm e;
+            for (uint32_t tag = 0; tag < kNumTags; ++tag)
+                for (uint32_t l = 0; l < 2; ++l) e.by_tag_link[tag][l] = ledger[(size_t(t) * kNumTags + tag) * 2 + l];
+            for (const auto& r : ledger_report(e, t)) rows.push_back(r);
+        }
+        write_comm_report_csv(path, rows);
+    });
+}
+
+int gs_bubble_analysis(const gs_trace_event* events, uint64_t n, gs_bubble_report* out) {
+    return guarded([&]() {
+        if (!out) throw std::invalid_argument("null output");
+        const BubbleReport b = bubble_analysis(trace_of(events, n));
+        *out = gs_bubble_report{b.measured_bubble, b.ideal_bubble, b.stages, b.chunks, b.span};
+    });
+}
+
+int gs_comm_volumes(const gs_comm_model_input* in, double* graph, double* pipeline, double* hybrid) {
+    return guarded([&]() {
+        const CommModelInput c = cmi(in);
+        if (graph) *graph = volume_graph(c);
+        if (pipeline) *pipeline = volume_pipeline(c);
+        if (hybrid) *hybrid = volume_hybrid(c);
+    });
+}
+
+int gs_crossover_report(const gs_comm_model_input* g, const gs_comm_model_input* p, const gs_comm_model_input* h,
+                        double* bytes, char* text, uint64_t cap) {
+    return guarded([&]() {
+        const CrossoverReport r = crossover_report(cmi(g), cmi(p), cmi(h));
+        if (bytes) {
+            bytes[0] = r.bytes_graph;
+            bytes[1] = r.bytes_pipeline;
+            bytes[2] = r.bytes_hybrid;
+        }
+        std::string t = r.winner + "\n";
+        for (size_t i = 0; i < r.ordering.size(); ++i) t += (i ? "," : "") + r.ordering[i];
+        t += std::string("\n") + (r.tie ? "1" : "0");
+        for (const auto& q : r.inequalities) t += "\n" + q;
+        if (text && cap) {
+            const size_t m = std::min<size_t>(cap - 1, t.size());
+            std::memcpy(text, t.data(), m);
+            text[m] = 0;
+        }
+    });
+}
+
+int gs_write_compare_csv(const char* path, const char* modes, const double* vals, const uint64_t* measured,
+                         uint64_t n) {
+    return guarded([&]() {
+        if (!path || (n && (!modes || !vals || !measured))) throw std::invalid_argument("null argument");
+        std::vector<CompareRow> rows;
+        std::string all(modes ? modes : ""), cur;
+        std::vector<std::string> names;
+        for (char ch : all) {
+            if (ch == '\n') names.push_back(cur), cur.clear();
+            else cur += ch;
+        }
+        names.push_back(cur);
+        if (names.size() < n) throw std::invalid_argument("fewer mode names than rows");
+        for (uint64_t i = 0; i < n; ++i) {
+            const double* v = vals + 9 * i;
+            rows.push_back({names[i], v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7], measured[i], v[8]});
+        }
+        write_compare_csv(path, rows);
+    });
 }
 
 int gs_result_peak_bytes(const gs_result* r, uint64_t* out) {

@@ -8,6 +8,7 @@
 // boundaries use gp_link_local (device-to-device copies ordered by CUDA events);
 // the one-process-per-GPU NCCL path is driven directly through the C-ABI
 // (bench.py).
+#include <algorithm>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -196,6 +197,7 @@ TrainResult<float> run_hybrid_f32(const Dataset& ds, const Partition* part, cons
             check(gp_set_layer_params(g, l, params[l].weight.data(), params[l].bias.empty() ? nullptr : params[l].bias.data()),
                   g, "gp_set_layer_params");
         if (opt.profile) gp_set_profiling(g, 1);
+        if (opt.fabric.collect_trace) gp_set_trace(g, 1);
         if (s > 0) check(gp_link_local(ctx.v[w - G], g), g, "gp_link_local");  // same rank, previous stage
     }
     if (G > 1)
@@ -246,6 +248,50 @@ TrainResult<float> run_hybrid_f32(const Dataset& ds, const Partition* part, cons
         }
 
     TrainResult<float> res;
+    // measured trace (Fabric::trace fabric.cpp:256-264): all workers on one
+    // timebase, seconds from the first event, stable-sorted by (start, worker)
+    std::vector<double> trace_bubble(T, -1.0);
+    if (opt.fabric.collect_trace) {
+        std::vector<std::vector<gp_trace_event>> ev(W);
+        double t0 = 0;
+        bool any = false;
+        for (uint32_t w = 0; w < W; ++w) {
+            uint64_t cnt = 0;
+            gp_get_trace(ctx.v[w], nullptr, 0, &cnt);
+            ev[w].resize(cnt);
+            gp_get_trace(ctx.v[w], ev[w].data(), cnt, &cnt);
+            for (const auto& e : ev[w]) {
+                t0 = any ? std::min(t0, e.t_start_ns) : e.t_start_ns;
+                any = true;
+            }
+        }
+        std::vector<double> lo(T, 0), hi(T, 0), busy(T, 0);
+        std::vector<uint8_t> seen(T, 0);
+        for (uint32_t w = 0; w < W; ++w)
+            for (const auto& e : ev[w]) {
+                TraceEvent te{};
+                te.worker = worker_id[w];
+                te.t_start = (e.t_start_ns - t0) * 1e-9;
+                te.t_end = (e.t_end_ns - t0) * 1e-9;
+                te.kind = TraceEvent::Kind(e.kind);
+                te.chunk = e.chunk;
+                te.layer_lo = e.layer_lo;
+                te.layer_hi = e.layer_hi;
+                res.trace.push_back(te);
+                if (e.epoch >= 1 && e.epoch <= T) {
+                    const uint32_t i = e.epoch - 1;
+                    lo[i] = seen[i] ? std::min(lo[i], te.t_start) : te.t_start;
+                    hi[i] = seen[i] ? std::max(hi[i], te.t_end) : te.t_end;
+                    seen[i] = 1;
+                    if (te.kind == TraceEvent::Kind::Compute) busy[i] += te.t_end - te.t_start;
+                }
+            }
+        std::stable_sort(res.trace.begin(), res.trace.end(), [](const TraceEvent& a, const TraceEvent& b) {
+            return a.t_start != b.t_start ? a.t_start < b.t_start : a.worker < b.worker;
+        });
+        for (uint32_t i = 0; i < T; ++i)
+            if (seen[i] && hi[i] > lo[i]) trace_bubble[i] = std::max(0.0, 1.0 - busy[i] / (double(W) * (hi[i] - lo[i])));
+    }
     if (node_of.empty())
         for (uint32_t w = 0; w < W; ++w) node_of.push_back(w / 4);
     auto node = [&](uint32_t s, uint32_t r) { return node_of[worker_id[size_t(s) * G + r]]; };
@@ -285,6 +331,7 @@ TrainResult<float> run_hybrid_f32(const Dataset& ds, const Partition* part, cons
         m.comm_bytes_weightsync = e.weight_sync_bytes();
         m.wall_time_s = span / 1000.0;
         m.bubble_fraction = (opt.profile && span > 0) ? std::max(0.0, 1.0 - busy / (span * W)) : 0.0;
+        if (trace_bubble[t] >= 0) m.bubble_fraction = trace_bubble[t];  // measured compute spans
     }
     res.worker_params.resize(W);
     for (uint32_t w = 0; w < W; ++w) {

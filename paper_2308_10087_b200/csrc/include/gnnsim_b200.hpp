@@ -327,6 +327,63 @@ TrainResult<T> train_hybrid(const Dataset& ds, const Partition& part, const Chun
 template <typename T>
 TrainResult<T> train_graph_parallel(const Dataset& ds, const Partition& part, const TrainOptions<T>& opt);
 
+// ---------------------------------------------------------------- run outputs and analytics
+// (fabric.hpp/fabric.cpp:20-35, :136-182; analytics.hpp/analytics.cpp; engines.cpp:23-38)
+const char* tag_name(MsgTag t);
+enum class LinkClass : uint32_t { IntraNode = 0, InterNode = 1 };
+const char* link_class_name(LinkClass c);
+const char* trace_kind_name(TraceEvent::Kind k);
+
+struct CommReportRow {
+    uint32_t epoch;
+    MsgTag tag;
+    LinkClass link;
+    uint64_t bytes;
+    double gib;  // bytes / 2^30
+};
+// Non-zero (tag, link) cells of one closed epoch (ledger_report fabric.cpp:136-146).
+std::vector<CommReportRow> ledger_report(const EpochComm& e, uint32_t epoch);
+void write_comm_report_csv(const std::string& path, const std::vector<CommReportRow>& rows);
+void write_trace_jsonl(const std::string& path, const std::vector<TraceEvent>& events);
+void write_metrics_csv(const std::string& path, const std::vector<EpochMetrics>& metrics);
+
+struct CommModelInput {
+    double n = 0, layers = 0, hidden = 0, stages = 1, ways = 1, alpha = 0, vecs = 1;
+    double bytes_per_value = 4;
+};
+constexpr double kGiB = 1024.0 * 1024.0 * 1024.0;
+double volume_pipeline(const CommModelInput& in);  // 2 (S-1) N H vecs * bytes
+double volume_graph(const CommModelInput& in);     // 2 alpha L N H * bytes
+double volume_hybrid(const CommModelInput& in);    // graph + pipeline
+
+struct CrossoverReport {
+    double bytes_graph = 0, bytes_pipeline = 0, bytes_hybrid = 0;
+    std::vector<std::string> ordering;
+    bool tie = false;
+    std::vector<std::string> inequalities;
+    std::string winner;
+};
+CrossoverReport crossover_report(const CommModelInput& graph_in, const CommModelInput& pipe_in,
+                                 const CommModelInput& hybrid_in);
+
+struct BubbleReport {
+    double measured_bubble = 0;  // idle fraction of workers x span
+    double ideal_bubble = 0;     // (S-1) / (K+S-1)
+    uint32_t stages = 0;
+    uint32_t chunks = 0;
+    double span = 0;
+};
+BubbleReport bubble_analysis(const std::vector<TraceEvent>& trace);
+
+struct CompareRow {
+    std::string mode;
+    double n, layers, hidden, stages, ways, alpha, vecs;
+    double predicted_bytes;
+    uint64_t measured_bytes;
+    double rel_error;
+};
+void write_compare_csv(const std::string& path, const std::vector<CompareRow>& rows);
+
 extern template TrainResult<float> train_sequential<float>(const Dataset&, const TrainOptions<float>&);
 extern template TrainResult<float> train_pipeline<float>(const Dataset&, const ChunkPlan&,
                                                          const StageAssignment&, const TrainOptions<float>&);

@@ -55,8 +55,49 @@ SCENARIOS = {
 }
 
 
+def analytics_events():
+    """A deterministic 3-worker, 5-chunk trace with every event kind (input of the analytics golden)."""
+    rng = np.random.default_rng(2308)
+    rows = []
+    for w in range(3):
+        t = 0.01 * w
+        for k in range(5):
+            if w:
+                idle = float(rng.uniform(0, 0.004))
+                rows.append((w, 3, k, 2 * w, 2 * w + 1, t, t + idle))
+                t += idle
+                rows.append((w, 2, k, 2 * w, 2 * w + 1, t, t))
+            dt = float(rng.uniform(0.005, 0.02))
+            rows.append((w, 0, k, 2 * w, 2 * w + 1, t, t + dt))
+            t += dt
+            if w < 2:
+                rows.append((w, 1, k, 2 * w, 2 * w + 1, t, t))
+        rows.append((w, 0, -1, 2 * w, 2 * w + 1, t, t + 0.002))
+    return rows
+
+
+def golden_analytics(td):
+    ev = analytics_events()
+    path = os.path.join(td, "events.txt")
+    with open(path, "w") as f:
+        for r in ev:
+            f.write(" ".join(repr(x) for x in r) + "\n")
+    d = run_ref("analytics", os.path.join(td, "analytics.blob"), **{"in": path, "dir": td})
+    files = {}
+    for name in ("trace.jsonl", "comm_report.csv", "metrics.csv", "compare.csv"):
+        with open(os.path.join(td, name)) as f:
+            files["file_" + name.replace(".", "_")] = np.array(f.read())
+    arr = np.array([(w, k, c, lo, hi, 0, t0, t1) for (w, k, c, lo, hi, t0, t1) in ev],
+                   dtype=[("worker", np.uint32), ("kind", np.uint32), ("chunk", np.int32), ("layer_lo", np.int32),
+                          ("layer_hi", np.int32), ("reserved", np.uint32), ("t_start", np.float64),
+                          ("t_end", np.float64)])
+    np.savez_compressed(os.path.join(HERE, "analytics.npz"), events=arr, **d, **files)
+    print("analytics", sorted(d))
+
+
 def main():
     with tempfile.TemporaryDirectory() as td:
+        golden_analytics(td)
         for name, (cmd, kw) in SCENARIOS.items():
             d = run_ref(cmd, os.path.join(td, name + ".blob"), **kw)
             meta = {"cmd": cmd, **{k: str(v) for k, v in kw.items()}}

@@ -1,0 +1,65 @@
+"""Measured trace (FabricOptions::collect_trace, fabric.cpp:222-264) and the run outputs built on it:
+per-chunk compute spans from CUDA events on one %globaltimer timebase, the reference's event
+kinds and order, bubble_analysis (analytics.cpp:59-86) over real device time."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ER500 = (500, 0.02, 3, 16, 5, 9)
+
+
+@pytest.fixture(scope="module", autouse=True)
+def need_gpu(gp):
+    if gp.device_count() == 0:
+        pytest.fail("no CUDA device visible: GPU tests must run on the B200 box")
+
+
+@pytest.mark.parametrize("model_kind,S,K", [("gcn", 2, 4), ("gcnii", 3, 6)])
+def test_trace_structure_and_bubble(gp, tmp_path, model_kind, S, K):
+    ds = gp.Dataset.synthetic_er(*ER500)
+    kind = gp.ModelKind.GCN if model_kind == "gcn" else gp.ModelKind.GCNII
+    model = gp.ModelConfig(kind=kind, layers=6, hidden=16)
+    co = gp.make_chunks(ds, K, 3)
+    T = 3
+    base = gp.train_pipeline(ds, co, S, gp.TrainOptions(model=model, epochs=T, seed=5, fix_alpha=2))
+    res = gp.train_pipeline(ds, co, S, gp.TrainOptions(model=model, epochs=T, seed=5, fix_alpha=2,
+                                                       collect_trace=True))
+    # tracing runs chunks serially: same arithmetic, same results
+    np.testing.assert_array_equal(res.train_loss, base.train_loss)
+    assert len(base.trace) == 0
+    tr = res.trace
+    assert len(tr) > 0
+    assert np.all(tr["t_end"] >= tr["t_start"]) and tr["t_start"].min() == 0.0
+    assert np.all(np.diff(tr["t_start"]) >= 0)  # sorted by start (then worker)
+    ranges = gp.make_stage_assignment(6, S)
+    for w in range(S):
+        ev = tr[tr["worker"] == w]
+        comp = ev[ev["kind"] == 0]
+        # per epoch: K forward + K backward chunk spans + the parameter step
+        assert len(comp) == T * (2 * K + 1)
+        assert np.all(comp["layer_lo"] == ranges[w][0]) and np.all(comp["layer_hi"] == ranges[w][1] - 1)
+        # a stage's compute spans never overlap
+        c = np.sort(comp, order="t_start")
+        assert np.all(c["t_start"][1:] >= c["t_end"][:-1] - 1e-9)
+        nsend = (ev["kind"] == 1).sum()
+        nrecv = (ev["kind"] == 2).sum()
+        assert nsend == T * K * ((w < S - 1) + (w > 0))
+        assert nrecv == nsend and (ev["kind"] == 3).sum() == nrecv
+        assert sorted(set(comp["chunk"].tolist())) == [-1] + list(range(K))
+    # every forward message is received no earlier than it was sent
+    for w in range(1, S):
+        sends = tr[(tr["worker"] == w - 1) & (tr["kind"] == 1)]
+        recvs = tr[(tr["worker"] == w) & (tr["kind"] == 2)]
+        for k in range(K):
+            assert recvs[recvs["chunk"] == k]["t_start"].min() >= sends[sends["chunk"] == k]["t_start"].min() - 1e-6
+    b = gp.bubble_analysis(tr)
+    assert b["stages"] == S and b["chunks"] == K
+    assert b["ideal_bubble"] == pytest.approx((S - 1) / (K + S - 1))
+    assert 0.0 <= b["measured_bubble"] < 1.0
+    assert np.all((res.metrics[:, 6] >= 0) & (res.metrics[:, 6] < 1))
+    gp.write_run_outputs(res, str(tmp_path))
+    assert sum(1 for _ in open(tmp_path / "trace.jsonl")) == len(tr)
+    assert open(tmp_path / "metrics.csv").read().count("\n") == T + 1
+    pipe = res.ledger[:, 0:2, :].sum()
+    assert pipe == res.comm[:, 1].sum()
