@@ -154,6 +154,14 @@ gp_status gp_set_layer_params(gp_ctx* ctx, uint32_t layer, const float* W, const
 gp_status gp_get_layer_params(gp_ctx* ctx, uint32_t layer, float* W, float* b);
 /* ParamGrads of the last epoch (nn.hpp:264-293, Gcn2Conv already scaled by beta). */
 gp_status gp_get_layer_grads(gp_ctx* ctx, uint32_t layer, float* W, float* b);
+/* Optimizer state of a layer (Optimizer m_/v_ and step count t_, nn.hpp:431-495),
+ * for checkpoint/resume (the reference's checkpoints hold parameters only,
+ * nn.hpp:497-531). mb/vb are ignored for layers without a bias; step is the
+ * stage's optimizer step count (one per epoch). */
+gp_status gp_get_optimizer_state(gp_ctx* ctx, uint32_t layer, float* mW, float* vW, float* mb, float* vb,
+                                 uint64_t* step);
+gp_status gp_set_optimizer_state(gp_ctx* ctx, uint32_t layer, const float* mW, const float* vW,
+                                 const float* mb, const float* vb, uint64_t step);
 
 /* ---- transport (stage boundaries, engines_impl.hpp:690-724) -------------- */
 /* Same process: upstream stage s and downstream stage s+1 exchange chunk rows
@@ -266,7 +274,9 @@ typedef struct {
     int32_t device;       /* first CUDA device; stages are placed round-robin */
     uint32_t profile;     /* collect per-kernel device times                  */
     uint32_t collect_trace; /* FabricOptions::collect_trace (fabric.hpp): measured trace */
-} gs_train_options;       /* TrainOptions engines.hpp:69-77 */
+    const char* resume_path;     /* NULL/"" or a save_state_path file: continue from it   */
+    const char* save_state_path; /* NULL/"" or where to write the final TrainState       */
+} gs_train_options;       /* TrainOptions engines.hpp:69-77 (+ resume, an extension) */
 
 /* TraceEvent (fabric.hpp): seconds from the first event of the run. */
 typedef struct {
@@ -334,6 +344,14 @@ int gs_result_metrics(const gs_result* r, uint32_t* epochs, double* metrics,
                       uint64_t* comm /* T x {graph, pipeline, weightsync} */);
 int gs_result_params(const gs_result* r, float* flat);
 int gs_result_profile(const gs_result* r, gp_profile* out);
+/* Checkpoints (nn.hpp:497-531, nn.cpp:82-124): save_stage_checkpoint of layers
+ * [lo, hi) from flat parameters (gs_init_params layout); load_checkpoint returns
+ * newline-separated names, (rows, cols) pairs and the concatenated data (call
+ * with NULL buffers first to get n_tensors / n_floats). */
+int gs_save_stage_checkpoint(const char* path, const gs_model_config* m, uint32_t F, uint32_t C,
+                             const float* flat, uint32_t lo, uint32_t hi);
+int gs_load_checkpoint(const char* path, char* names, uint64_t names_cap, uint64_t* shapes, float* data,
+                       uint64_t* n_tensors, uint64_t* n_floats);
 /* Measured trace (collect_trace runs): copies up to cap events, *count = total. */
 int gs_result_trace(const gs_result* r, gs_trace_event* out, uint64_t cap, uint64_t* count);
 /* Communication ledger: T x 6 tags x 2 link classes (EpochComm::by_tag_link). */

@@ -16,6 +16,8 @@
 //           out=...                           metrics + final params
 //   save    spec=... dir=...                 save_dataset (reference writer)
 //   bench   spec=... ...                     CPU baseline sample (see run_bench)
+//   ckpt    model=.. layers=.. hidden=.. F=.. C=.. seed=.. lo=.. hi=.. path=.. out=...
+//                                            save_stage_checkpoint of init_params(seed)
 //   analytics in=EVENTS dir=DIR out=...      bubble_analysis of the trace in EVENTS (one
 //                                            "worker kind chunk lo hi t0 t1" per line),
 //                                            volume_* / crossover_report of fixed inputs,
@@ -371,6 +373,17 @@ void cmd_train(const Args& a) {
     dump_params(b, "", res.params);
 }
 
+// save_stage_checkpoint of init_params(seed) for layers [lo, hi) (nn.hpp:511-531).
+void cmd_ckpt(const Args& a) {
+    const ModelConfig m = model_from(a);
+    const auto specs = build_layer_specs(m, uint32_t(std::stoul(arg(a, "F"))), uint32_t(std::stoul(arg(a, "C"))));
+    const auto params = init_params<float>(specs, std::stoull(arg(a, "seed", "1")));
+    save_stage_checkpoint(arg(a, "path"), specs, params, std::stoul(arg(a, "lo", "0")),
+                          std::stoul(arg(a, "hi", std::to_string(specs.size()))));
+    Blob b(arg(a, "out"));
+    b.u64("num_layers", {specs.size()});
+}
+
 void cmd_save(const Args& a) {
     Dataset d = make_dataset(arg(a, "spec"));
     save_dataset(d, arg(a, "dir"));
@@ -548,6 +561,7 @@ int main(int argc, char** argv) {
         else if (cmd == "save") cmd_save(a);
         else if (cmd == "bench") cmd_bench(a);
         else if (cmd == "analytics") cmd_analytics(a);
+        else if (cmd == "ckpt") cmd_ckpt(a);
         else {
             std::fprintf(stderr, "unknown command %s\n", cmd.c_str());
             return 2;

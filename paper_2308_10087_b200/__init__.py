@@ -112,7 +112,8 @@ class gs_train_options(C.Structure):
                 ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double), ("epochs", C.c_uint32),
                 ("seed", C.c_uint64), ("shuffle_chunks", C.c_uint32), ("fix_alpha", C.c_uint32),
                 ("historical_gradients", C.c_uint32), ("synchronous_mode", C.c_uint32), ("device", C.c_int32),
-                ("profile", C.c_uint32), ("collect_trace", C.c_uint32)]
+                ("profile", C.c_uint32), ("collect_trace", C.c_uint32), ("resume_path", C.c_char_p),
+                ("save_state_path", C.c_char_p)]
 
 
 class gs_trace_event(C.Structure):
@@ -191,6 +192,11 @@ def _L():
         "gs_write_comm_report_csv": (C.c_int, [C.c_char_p, u64p, C.c_uint32]),
         "gs_bubble_analysis": (C.c_int, [vp, C.c_uint64, P(gs_bubble_report)]),
         "gs_comm_volumes": (C.c_int, [P(gs_comm_model_input), f64p, f64p, f64p]),
+        "gs_save_stage_checkpoint": (C.c_int, [C.c_char_p, P(gs_model_config), C.c_uint32, C.c_uint32, f32p,
+                                               C.c_uint32, C.c_uint32]),
+        "gs_load_checkpoint": (C.c_int, [C.c_char_p, P(C.c_char), C.c_uint64, u64p, f32p, u64p, u64p]),
+        "gp_get_optimizer_state": (C.c_int, [vp, C.c_uint32, f32p, f32p, f32p, f32p, u64p]),
+        "gp_set_optimizer_state": (C.c_int, [vp, C.c_uint32, f32p, f32p, f32p, f32p, C.c_uint64]),
         "gs_crossover_report": (C.c_int, [P(gs_comm_model_input), P(gs_comm_model_input), P(gs_comm_model_input),
                                           f64p, P(C.c_char), C.c_uint64]),
         "gs_write_compare_csv": (C.c_int, [C.c_char_p, C.c_char_p, f64p, u64p, C.c_uint64]),
@@ -293,12 +299,15 @@ class TrainOptions:
     device: int = 0
     profile: bool = False
     collect_trace: bool = False  # FabricOptions::collect_trace: measured per-chunk trace (chunks run serially)
+    resume_path: str = ""        # continue from a state written by save_state_path (epochs continue)
+    save_state_path: str = ""    # write parameters + optimizer state after the last epoch
 
     def c(self) -> gs_train_options:
         return gs_train_options(self.model.c(), 1 if self.optimizer == "sgd" else 0, self.lr, self.beta1,
                                 self.beta2, self.eps, self.epochs, self.seed, int(self.shuffle_chunks),
                                 self.fix_alpha, int(self.historical_gradients), int(self.synchronous_mode),
-                                self.device, int(self.profile), int(self.collect_trace))
+                                self.device, int(self.profile), int(self.collect_trace),
+                                self.resume_path.encode() or None, self.save_state_path.encode() or None)
 
 
 @dataclass
@@ -486,6 +495,34 @@ def comm_volumes(n, layers, hidden, stages=1, ways=1, alpha=0.0, vecs=1, bytes_p
     g, p, h = C.c_double(), C.c_double(), C.c_double()
     _gs(_L().gs_comm_volumes(C.byref(c), C.byref(g), C.byref(p), C.byref(h)))
     return {"graph": g.value, "pipeline": p.value, "hybrid": h.value}
+
+
+def save_stage_checkpoint(path: str, model: "ModelConfig", in_features: int, num_classes: int, params,
+                          lo: int, hi: int) -> None:
+    """save_stage_checkpoint (nn.hpp:511-531): layers [lo, hi) in the reference's checkpoint format."""
+    flat = np.concatenate([np.concatenate([np.ascontiguousarray(W, np.float32).ravel(),
+                                           np.ascontiguousarray(b if b is not None else [], np.float32).ravel()])
+                           for W, b in params]).astype(np.float32)
+    _gs(_L().gs_save_stage_checkpoint(path.encode(), C.byref(model.c()), in_features, num_classes,
+                                      _ptr(flat, C.c_float), lo, hi))
+
+
+def load_checkpoint(path: str):
+    """load_checkpoint (nn.cpp:104-124): [(name, float32 array of shape (rows, cols))]."""
+    lib = _L()
+    nt, nf = C.c_uint64(), C.c_uint64()
+    _gs(lib.gs_load_checkpoint(path.encode(), None, 0, None, None, C.byref(nt), C.byref(nf)))
+    shapes = np.zeros(2 * nt.value, np.uint64)
+    data = np.zeros(nf.value, np.float32)
+    names = C.create_string_buffer(64 * nt.value + 64)
+    _gs(lib.gs_load_checkpoint(path.encode(), names, len(names), _ptr(shapes, C.c_uint64), _ptr(data, C.c_float),
+                               C.byref(nt), C.byref(nf)))
+    out, at = [], 0
+    for i, name in enumerate(names.value.decode().split("\n") if nt.value else []):
+        r, c = int(shapes[2 * i]), int(shapes[2 * i + 1])
+        out.append((name, data[at:at + r * c].reshape(r, c).copy()))
+        at += r * c
+    return out
 
 
 @dataclass

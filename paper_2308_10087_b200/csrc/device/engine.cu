@@ -941,6 +941,34 @@ struct Stage {
         if (d.gb && b) GP_CUDA(cudaMemcpy(b, d.gb, size_t(d.dout) * 4, cudaMemcpyDeviceToHost));
     }
 
+    // Optimizer state (Optimizer::m_/v_/t_, nn.hpp:431-495) for checkpoint/resume.
+    void get_opt_state(uint32_t l, float* mW, float* vW, float* mb, float* vb, uint64_t* t) {
+        GP_CUDA(cudaSetDevice(device));
+        GP_CUDA(cudaStreamSynchronize(cs));
+        auto& d = layer(l);
+        const size_t wn = size_t(d.din) * d.dout * 4;
+        if (mW) GP_CUDA(cudaMemcpy(mW, d.mW, wn, cudaMemcpyDeviceToHost));
+        if (vW) GP_CUDA(cudaMemcpy(vW, d.vW, wn, cudaMemcpyDeviceToHost));
+        if (d.mb && mb) GP_CUDA(cudaMemcpy(mb, d.mb, size_t(d.dout) * 4, cudaMemcpyDeviceToHost));
+        if (d.vb && vb) GP_CUDA(cudaMemcpy(vb, d.vb, size_t(d.dout) * 4, cudaMemcpyDeviceToHost));
+        if (t) *t = step;
+    }
+    void set_opt_state(uint32_t l, const float* mW, const float* vW, const float* mb, const float* vb, uint64_t t) {
+        GP_CUDA(cudaSetDevice(device));
+        GP_CUDA(cudaStreamSynchronize(cs));
+        auto& d = layer(l);
+        const size_t wn = size_t(d.din) * d.dout * 4;
+        if (!mW || !vW) throw Error(GP_EINVAL, "optimizer state: null weight moments");
+        GP_CUDA(cudaMemcpy(d.mW, mW, wn, cudaMemcpyHostToDevice));
+        GP_CUDA(cudaMemcpy(d.vW, vW, wn, cudaMemcpyHostToDevice));
+        if (d.mb) {
+            if (!mb || !vb) throw Error(GP_EINVAL, "optimizer state: layer has a bias");
+            GP_CUDA(cudaMemcpy(d.mb, mb, size_t(d.dout) * 4, cudaMemcpyHostToDevice));
+            GP_CUDA(cudaMemcpy(d.vb, vb, size_t(d.dout) * 4, cudaMemcpyHostToDevice));
+        }
+        step = t;
+    }
+
     void get_params(uint32_t l, float* W, float* b) {
         GP_CUDA(cudaSetDevice(device));
         GP_CUDA(cudaStreamSynchronize(cs));
@@ -2422,6 +2450,16 @@ gp_status gp_get_layer_params(gp_ctx* ctx, uint32_t layer, float* W, float* b) {
 
 gp_status gp_get_layer_grads(gp_ctx* ctx, uint32_t layer, float* W, float* b) {
     return gp::guard(&ctx->st, [&]() { ctx->st.get_grads(layer, W, b); });
+}
+
+gp_status gp_get_optimizer_state(gp_ctx* ctx, uint32_t layer, float* mW, float* vW, float* mb, float* vb,
+                                 uint64_t* step) {
+    return gp::guard(&ctx->st, [&]() { ctx->st.get_opt_state(layer, mW, vW, mb, vb, step); });
+}
+
+gp_status gp_set_optimizer_state(gp_ctx* ctx, uint32_t layer, const float* mW, const float* vW, const float* mb,
+                                 const float* vb, uint64_t step) {
+    return gp::guard(&ctx->st, [&]() { ctx->st.set_opt_state(layer, mW, vW, mb, vb, step); });
 }
 
 gp_status gp_link_local(gp_ctx* up, gp_ctx* down) {

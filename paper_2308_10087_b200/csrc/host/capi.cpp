@@ -83,6 +83,20 @@ TrainOptions<float> options_of(const gs_train_options* o) {
     return t;
 }
 
+// options + the resume state named by o->resume_path (shapes from the dataset)
+TrainOptions<float> options_for(const gs_train_options* o, const Dataset& d) {
+    TrainOptions<float> t = options_of(o);
+    if (o->resume_path && *o->resume_path)
+        t.resume = std::make_shared<TrainState>(
+            load_train_state(o->resume_path, build_layer_specs(t.model, d.num_features(), d.num_classes)));
+    return t;
+}
+
+gs_result* finish(std::unique_ptr<gs_result> own, const gs_train_options* o) {
+    if (o->save_state_path && *o->save_state_path) save_train_state(o->save_state_path, own->r.final_state);
+    return own.release();
+}
+
 CommModelInput cmi(const gs_comm_model_input* in) {
     if (!in) throw std::invalid_argument("null input");
     CommModelInput c;
@@ -249,21 +263,21 @@ int gs_init_params(const gs_model_config* m, uint32_t F, uint32_t C, uint64_t se
 int gs_train_pipeline(const gs_dataset* d, const uint32_t* chunk_of, uint32_t K, uint32_t S,
                       const gs_train_options* o, gs_result** out) {
     return guarded([&]() {
-        TrainOptions<float> opt = options_of(o);
+        TrainOptions<float> opt = options_for(o, d->d);
         const uint32_t L = uint32_t(build_layer_specs(opt.model, d->d.num_features(), d->d.num_classes).size());
         ChunkPlan plan = chunk_plan_from_assignment(d->d.num_vertices(),
                                                     std::vector<uint32_t>(chunk_of, chunk_of + d->d.num_vertices()));
         if (plan.num_chunks != K) throw std::invalid_argument("chunk_of does not use exactly K chunks");
         auto own = std::make_unique<gs_result>();
         own->r = train_pipeline<float>(d->d, plan, make_stage_assignment(L, S), opt);
-        *out = own.release();
+        *out = finish(std::move(own), o);
     });
 }
 
 int gs_train_hybrid(const gs_dataset* d, const uint32_t* part_of, const uint32_t* chunk_of, uint32_t K, uint32_t S,
                     const gs_train_options* o, gs_result** out) {
     return guarded([&]() {
-        TrainOptions<float> opt = options_of(o);
+        TrainOptions<float> opt = options_for(o, d->d);
         const VertexId n = d->d.num_vertices();
         const uint32_t L = uint32_t(build_layer_specs(opt.model, d->d.num_features(), d->d.num_classes).size());
         Partition part = partition_from_assignment(d->d.graph, std::vector<uint32_t>(part_of, part_of + n));
@@ -273,7 +287,7 @@ int gs_train_hybrid(const gs_dataset* d, const uint32_t* part_of, const uint32_t
         GroupMap gmap = assign_groups(S * G, 4, S, G);
         auto own = std::make_unique<gs_result>();
         own->r = train_hybrid<float>(d->d, part, plan, make_stage_assignment(L, S), gmap, opt);
-        *out = own.release();
+        *out = finish(std::move(own), o);
     });
 }
 
@@ -283,16 +297,16 @@ int gs_train_graph_parallel(const gs_dataset* d, const uint32_t* part_of, const 
         const VertexId n = d->d.num_vertices();
         Partition part = partition_from_assignment(d->d.graph, std::vector<uint32_t>(part_of, part_of + n));
         auto own = std::make_unique<gs_result>();
-        own->r = train_graph_parallel<float>(d->d, part, options_of(o));
-        *out = own.release();
+        own->r = train_graph_parallel<float>(d->d, part, options_for(o, d->d));
+        *out = finish(std::move(own), o);
     });
 }
 
 int gs_train_sequential(const gs_dataset* d, const gs_train_options* o, gs_result** out) {
     return guarded([&]() {
         auto own = std::make_unique<gs_result>();
-        own->r = train_sequential<float>(d->d, options_of(o));
-        *out = own.release();
+        own->r = train_sequential<float>(d->d, options_for(o, d->d));
+        *out = finish(std::move(own), o);
     });
 }
 
@@ -466,6 +480,53 @@ int gs_write_compare_csv(const char* path, const char* modes, const double* vals
             rows.push_back({names[i], v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7], measured[i], v[8]});
         }
         write_compare_csv(path, rows);
+    });
+}
+
+int gs_save_stage_checkpoint(const char* path, const gs_model_config* m, uint32_t F, uint32_t C, const float* flat,
+                             uint32_t lo, uint32_t hi) {
+    return guarded([&]() {
+        if (!path || !flat) throw std::invalid_argument("null argument");
+        const auto specs = build_layer_specs(model_of(m), F, C);
+        if (lo >= hi || hi > specs.size()) throw std::invalid_argument("bad layer range");
+        std::vector<LayerParams<float>> params(specs.size());
+        size_t at = 0;
+        for (size_t l = 0; l < specs.size(); ++l) {
+            params[l].weight = MatF(specs[l].k_in(), specs[l].out_dim);
+            std::memcpy(params[l].weight.data(), flat + at, params[l].weight.size() * 4);
+            at += params[l].weight.size();
+            if (specs[l].has_bias()) {
+                params[l].bias.assign(flat + at, flat + at + specs[l].out_dim);
+                at += specs[l].out_dim;
+            }
+        }
+        save_stage_checkpoint(path, specs, params, lo, hi);
+    });
+}
+
+int gs_load_checkpoint(const char* path, char* names, uint64_t names_cap, uint64_t* shapes, float* data,
+                       uint64_t* n_tensors, uint64_t* n_floats) {
+    return guarded([&]() {
+        if (!path) throw std::invalid_argument("null path");
+        const auto ts = load_checkpoint(path);
+        std::string all;
+        uint64_t floats = 0;
+        for (size_t i = 0; i < ts.size(); ++i) {
+            all += (i ? "\n" : "") + ts[i].name;
+            if (shapes) {
+                shapes[2 * i] = ts[i].rows;
+                shapes[2 * i + 1] = ts[i].cols;
+            }
+            if (data) std::memcpy(data + floats, ts[i].data.data(), ts[i].data.size() * 4);
+            floats += ts[i].data.size();
+        }
+        if (n_tensors) *n_tensors = ts.size();
+        if (n_floats) *n_floats = floats;
+        if (names && names_cap) {
+            const size_t k = std::min<size_t>(names_cap - 1, all.size());
+            std::memcpy(names, all.data(), k);
+            names[k] = 0;
+        }
     });
 }
 

@@ -146,6 +146,18 @@ TrainResult<float> run_hybrid_f32(const Dataset& ds, const Partition* part, cons
     const auto adj = normalize_adjacency<float>(ds.graph, opt.model.self_loops);
     timer.mark("normalize_adjacency");
     auto params = init_params<float>(specs, opt.seed);
+    const uint32_t t0 = opt.resume ? opt.resume->epoch : 0;  // epochs already trained
+    if (opt.resume) {
+        const auto& rs = *opt.resume;
+        if (rs.params.size() != L || rs.adam_m.size() != L || rs.adam_v.size() != L)
+            throw std::invalid_argument("resume: state does not match the model's layers");
+        for (uint32_t l = 0; l < L; ++l)
+            for (const auto* p : {&rs.params[l], &rs.adam_m[l], &rs.adam_v[l]})
+                if (p->weight.rows() != specs[l].k_in() || p->weight.cols() != specs[l].out_dim ||
+                    p->bias.size() != (specs[l].has_bias() ? specs[l].out_dim : 0u))
+                    throw std::invalid_argument("resume: layer " + std::to_string(l) + " has the wrong shape");
+        params = rs.params;
+    }
     timer.mark("init_params");
 
     int ndev = 0;
@@ -196,6 +208,14 @@ TrainResult<float> run_hybrid_f32(const Dataset& ds, const Partition* part, cons
         for (uint32_t l = sa.begin(s); l < sa.end(s); ++l)
             check(gp_set_layer_params(g, l, params[l].weight.data(), params[l].bias.empty() ? nullptr : params[l].bias.data()),
                   g, "gp_set_layer_params");
+        if (opt.resume)
+            for (uint32_t l = sa.begin(s); l < sa.end(s); ++l) {
+                const auto& m = opt.resume->adam_m[l];
+                const auto& v = opt.resume->adam_v[l];
+                check(gp_set_optimizer_state(g, l, m.weight.data(), v.weight.data(), m.bias.empty() ? nullptr : m.bias.data(),
+                                             v.bias.empty() ? nullptr : v.bias.data(), opt.resume->optimizer_step),
+                      g, "gp_set_optimizer_state");
+            }
         if (opt.profile) gp_set_profiling(g, 1);
         if (opt.fabric.collect_trace) gp_set_trace(g, 1);
         if (s > 0) check(gp_link_local(ctx.v[w - G], g), g, "gp_link_local");  // same rank, previous stage
@@ -211,12 +231,12 @@ TrainResult<float> run_hybrid_f32(const Dataset& ds, const Partition* part, cons
     StageBarrier barrier(W);
     auto body = [&](uint32_t w) {
         try {
-            for (uint32_t t = 1; t <= T; ++t) {
+            for (uint32_t t = t0 + 1; t <= t0 + T; ++t) {
                 if (!barrier.arrive_and_wait()) return;  // epoch entry sync (engines_impl.hpp:668)
                 std::vector<uint32_t> order(K);
                 for (uint32_t k = 0; k < K; ++k) order[k] = k;
                 if (opt.staleness.shuffle_chunks) order = shuffle_chunk_order(plan, t, opt.seed);
-                check(gp_run_epoch(ctx.v[w], t, order.data(), &stats[w][t - 1]), ctx.v[w], "gp_run_epoch");
+                check(gp_run_epoch(ctx.v[w], t, order.data(), &stats[w][t - t0 - 1]), ctx.v[w], "gp_run_epoch");
             }
         } catch (...) {
             errs[w] = std::current_exception();
@@ -278,8 +298,8 @@ TrainResult<float> run_hybrid_f32(const Dataset& ds, const Partition* part, cons
                 te.layer_lo = e.layer_lo;
                 te.layer_hi = e.layer_hi;
                 res.trace.push_back(te);
-                if (e.epoch >= 1 && e.epoch <= T) {
-                    const uint32_t i = e.epoch - 1;
+                if (e.epoch > t0 && e.epoch <= t0 + T) {
+                    const uint32_t i = e.epoch - t0 - 1;
                     lo[i] = seen[i] ? std::min(lo[i], te.t_start) : te.t_start;
                     hi[i] = seen[i] ? std::max(hi[i], te.t_end) : te.t_end;
                     seen[i] = 1;
@@ -299,7 +319,7 @@ TrainResult<float> run_hybrid_f32(const Dataset& ds, const Partition* part, cons
     res.comm.resize(T);
     for (uint32_t t = 0; t < T; ++t) {
         EpochMetrics& m = res.metrics[t];
-        m.epoch = t + 1;
+        m.epoch = t0 + t + 1;
         // reduce_metrics (engines_impl.hpp:131-151): group rank 0 adds ranks in order
         double loss = 0;
         uint64_t cor[3] = {0, 0, 0};
@@ -332,6 +352,30 @@ TrainResult<float> run_hybrid_f32(const Dataset& ds, const Partition* part, cons
         m.wall_time_s = span / 1000.0;
         m.bubble_fraction = (opt.profile && span > 0) ? std::max(0.0, 1.0 - busy / (span * W)) : 0.0;
         if (trace_bubble[t] >= 0) m.bubble_fraction = trace_bubble[t];  // measured compute spans
+    }
+    // resumable state: every stage's group rank 0 holds its layers' parameters + moments
+    res.final_state.epoch = t0 + T;
+    res.final_state.params.resize(L);
+    res.final_state.adam_m.resize(L);
+    res.final_state.adam_v.resize(L);
+    for (uint32_t s = 0; s < S; ++s) {
+        gp_ctx* g = ctx.v[size_t(s) * G];
+        for (uint32_t l = sa.begin(s); l < sa.end(s); ++l) {
+            for (auto* p : {&res.final_state.params[l], &res.final_state.adam_m[l], &res.final_state.adam_v[l]}) {
+                p->weight = MatF(specs[l].k_in(), specs[l].out_dim);
+                if (specs[l].has_bias()) p->bias.assign(specs[l].out_dim, 0.f);
+            }
+            auto& P = res.final_state.params[l];
+            auto& M = res.final_state.adam_m[l];
+            auto& V = res.final_state.adam_v[l];
+            check(gp_get_layer_params(g, l, P.weight.data(), P.bias.empty() ? nullptr : P.bias.data()), g,
+                  "gp_get_layer_params");
+            uint64_t step = 0;
+            check(gp_get_optimizer_state(g, l, M.weight.data(), V.weight.data(), M.bias.empty() ? nullptr : M.bias.data(),
+                                         V.bias.empty() ? nullptr : V.bias.data(), &step),
+                  g, "gp_get_optimizer_state");
+            res.final_state.optimizer_step = step;
+        }
     }
     res.worker_params.resize(W);
     for (uint32_t w = 0; w < W; ++w) {

@@ -15,6 +15,7 @@
 #include <random>
 #include <span>
 #include <stdexcept>
+#include <memory>
 #include <string>
 #include <utility>
 #include <vector>
@@ -197,6 +198,42 @@ std::vector<LayerParams<T>> init_params(const std::vector<LayerSpec>& specs, uin
     return out;
 }
 
+// ---------------------------------------------------------------- checkpoints (nn.hpp:497-531)
+// One file per stage: u64 header length, JSON header {"tensors":[{"cols","name","rows"}...]},
+// then the tensors as little-endian f32 (byte-compatible with the reference's files).
+void save_checkpoint(const std::string& path, const std::vector<std::string>& names,
+                     const std::vector<const float*>& data,
+                     const std::vector<std::pair<uint64_t, uint64_t>>& shapes);
+struct CheckpointTensor {
+    std::string name;
+    uint64_t rows = 0, cols = 0;
+    std::vector<float> data;
+};
+std::vector<CheckpointTensor> load_checkpoint(const std::string& path);
+
+template <typename T>
+void save_stage_checkpoint(const std::string& path, const std::vector<LayerSpec>& specs,
+                           const std::vector<LayerParams<T>>& params, size_t lo, size_t hi) {
+    (void)specs;
+    std::vector<std::string> names;
+    std::vector<std::vector<float>> store;
+    std::vector<std::pair<uint64_t, uint64_t>> shapes;
+    for (size_t l = lo; l < hi; ++l) {
+        const auto& w = params[l].weight;
+        store.emplace_back(w.data(), w.data() + w.size());
+        names.push_back("layer" + std::to_string(l) + ".weight");
+        shapes.push_back({w.rows(), w.cols()});
+        if (!params[l].bias.empty()) {
+            store.emplace_back(params[l].bias.begin(), params[l].bias.end());
+            names.push_back("layer" + std::to_string(l) + ".bias");
+            shapes.push_back({1, params[l].bias.size()});
+        }
+    }
+    std::vector<const float*> ptrs;
+    for (const auto& v : store) ptrs.push_back(v.data());
+    save_checkpoint(path, names, ptrs, shapes);
+}
+
 template <typename T>
 struct OptimizerConfig {
     OptimizerKind kind = OptimizerKind::Adam;
@@ -290,6 +327,19 @@ struct WorkerParams {
     std::vector<LayerParams<T>> params;
 };
 
+// Resumable training state (extension: the reference's checkpoints are
+// parameters only and there is no resume path). epoch = last completed epoch;
+// adam_m / adam_v mirror params (Optimizer m_/v_, nn.hpp:431-495).
+struct TrainState {
+    uint32_t epoch = 0;
+    uint64_t optimizer_step = 0;
+    std::vector<LayerParams<float>> params, adam_m, adam_v;
+};
+// Stored in the checkpoint format: layerL.weight/.bias (as save_stage_checkpoint),
+// layerL.{weight,bias}.adam_{m,v}, and train.state = [epoch, optimizer_step].
+void save_train_state(const std::string& path, const TrainState& st);
+TrainState load_train_state(const std::string& path, const std::vector<LayerSpec>& specs);
+
 template <typename T>
 struct TrainResult {
     std::vector<EpochMetrics> metrics;
@@ -299,6 +349,7 @@ struct TrainResult {
     std::vector<EpochComm> comm;
     uint64_t peak_buffer_bytes = 0;  // max per-stage device footprint
     gp_profile profile{};            // summed over stages (profiling runs)
+    TrainState final_state;          // parameters + optimizer state after the last epoch
 };
 
 template <typename T>
@@ -311,6 +362,11 @@ struct TrainOptions {
     FabricOptions fabric;
     int device = 0;        // first CUDA device (stages round-robin over visible GPUs)
     bool profile = false;  // per-kernel device timing
+    // Continue from a saved state: parameters and optimizer moments are restored
+    // and epochs run from resume->epoch + 1 (dropout keys, chunk order and the
+    // snapshot schedule continue). The historical-embedding stashes restart empty,
+    // so a resumed run equals an uninterrupted one exactly in synchronous mode.
+    std::shared_ptr<const TrainState> resume;
 };
 
 template <typename T>

@@ -95,9 +95,30 @@ def golden_analytics(td):
     print("analytics", sorted(d))
 
 
+CKPTS = {
+    # name: (model, layers, hidden, F, C, seed, lo, hi)
+    "ckpt_gcnii": ("gcnii", 5, 6, 7, 3, 12, 0, 5),
+    "ckpt_gcn_stage1": ("gcn", 4, 8, 10, 4, 3, 2, 4),
+}
+
+
+def golden_checkpoints(td):
+    out = {}
+    for name, (model, L, H, F, Cc, seed, lo, hi) in CKPTS.items():
+        path = os.path.join(td, name + ".ckpt")
+        run_ref("ckpt", os.path.join(td, name + ".blob"), model=model, layers=L, hidden=H, F=F, C=Cc, seed=seed,
+                lo=lo, hi=hi, path=path)
+        with open(path, "rb") as f:
+            out[name] = np.frombuffer(f.read(), np.uint8)
+        out[name + "_args"] = np.array([L, H, F, Cc, seed, lo, hi], np.int64)
+    np.savez_compressed(os.path.join(HERE, "checkpoints.npz"), **out)
+    print("checkpoints", sorted(out))
+
+
 def main():
     with tempfile.TemporaryDirectory() as td:
         golden_analytics(td)
+        golden_checkpoints(td)
         for name, (cmd, kw) in SCENARIOS.items():
             d = run_ref(cmd, os.path.join(td, name + ".blob"), **kw)
             meta = {"cmd": cmd, **{k: str(v) for k, v in kw.items()}}
