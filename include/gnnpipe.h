@@ -255,7 +255,7 @@ typedef struct gs_dataset gs_dataset;
 typedef struct gs_result gs_result;
 
 typedef struct {
-    uint32_t kind;        /* 0 gcn, 1 sage (rejected), 2 gcnii (ModelKind nn.hpp:15) */
+    uint32_t kind;        /* 0 gcn, 1 sage, 2 gcnii (ModelKind nn.hpp:15) */
     uint32_t layers;
     uint32_t hidden;
     double dropout;

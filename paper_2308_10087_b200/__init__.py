@@ -327,6 +327,11 @@ class LayerSpec:
     def aggregates(self) -> bool:
         return self.kind != LayerKind.DENSE
 
+    @property
+    def k_in(self) -> int:
+        """Rows of W (nn.hpp:42): SageConv concatenates [own | mean], so 2 in_dim."""
+        return 2 * self.in_dim if self.kind == LayerKind.SAGECONV else self.in_dim
+
 
 def build_layer_specs(model: ModelConfig, in_features: int, num_classes: int) -> List[LayerSpec]:
     """build_layer_specs (nn.cpp:28-64)."""
@@ -340,8 +345,8 @@ def build_layer_specs(model: ModelConfig, in_features: int, num_classes: int) ->
 def _split_params(specs: Sequence[LayerSpec], flat: np.ndarray):
     out, at = [], 0
     for s in specs:
-        w = flat[at:at + s.in_dim * s.out_dim].reshape(s.in_dim, s.out_dim).copy()
-        at += s.in_dim * s.out_dim
+        w = flat[at:at + s.k_in * s.out_dim].reshape(s.k_in, s.out_dim).copy()
+        at += s.k_in * s.out_dim
         b = flat[at:at + s.out_dim].copy() if s.has_bias else np.zeros(0, np.float32)
         at += s.out_dim if s.has_bias else 0
         out.append((w, b))
@@ -349,7 +354,7 @@ def _split_params(specs: Sequence[LayerSpec], flat: np.ndarray):
 
 
 def _param_count(specs) -> int:
-    return sum(s.in_dim * s.out_dim + (s.out_dim if s.has_bias else 0) for s in specs)
+    return sum(s.k_in * s.out_dim + (s.out_dim if s.has_bias else 0) for s in specs)
 
 
 def init_params(model: ModelConfig, in_features: int, num_classes: int, seed: int):
@@ -757,7 +762,7 @@ class StageEngine:
 
     def get_params(self, layer: int):
         s = self.specs[layer]
-        W = np.zeros((s.in_dim, s.out_dim), np.float32)
+        W = np.zeros((s.k_in, s.out_dim), np.float32)
         b = np.zeros(s.out_dim if s.has_bias else 0, np.float32)
         _gp(_L().gp_get_layer_params(self._h, layer, _ptr(W, C.c_float), _ptr(b, C.c_float) if b.size else None),
             self._h)
@@ -765,7 +770,7 @@ class StageEngine:
 
     def get_grads(self, layer: int):
         s = self.specs[layer]
-        W = np.zeros((s.in_dim, s.out_dim), np.float32)
+        W = np.zeros((s.k_in, s.out_dim), np.float32)
         b = np.zeros(s.out_dim if s.has_bias else 0, np.float32)
         _gp(_L().gp_get_layer_grads(self._h, layer, _ptr(W, C.c_float), _ptr(b, C.c_float) if b.size else None),
             self._h)
@@ -808,7 +813,9 @@ class StageEngine:
         lo, hi = self.layer_range
         if which in ("h", "dz", "hsnap"):
             width = self.specs[lo + local_layer].out_dim
-        elif which in ("pre", "dagg", "gather"):
+        elif which in ("pre", "dagg"):
+            width = self.specs[lo + local_layer].k_in
+        elif which == "gather":
             width = self.specs[lo + local_layer].in_dim
         elif which == "dh0":
             width = self.hidden

@@ -257,8 +257,14 @@ struct Transport {
 struct LayerDev {
     gp_layer_spec spec;
     uint32_t l;          // global layer id
-    uint32_t din, dout;  // in_dim, out_dim (k_in == in_dim: no SageConv)
+    uint32_t din, dout;  // in_dim, out_dim
     uint32_t sin, sout;  // padded strides
+    // transform width and the stride of pre / bg: din, sin for Dense/GCN/GCNII;
+    // SageConv (k_in = 2 din) keeps its two halves 32-byte aligned: own half at
+    // column 0, aggregated half at sgap = pad8(din), so kw = sgap + din
+    bool sage = false;
+    uint32_t kin = 0, kw = 0, skw = 0, sgap = 0;
+    float *Wg = nullptr, *WTg = nullptr;  // SageConv: W and W^T in the gapped layout
     bool agg;
     float *W = nullptr, *b = nullptr, *gW = nullptr, *gb = nullptr;
     float* WT = nullptr;  // W^T, refreshed whenever W changes (set_params, optimizer step)
@@ -289,6 +295,13 @@ struct Stage {
     std::shared_ptr<void> graph_owner;
     uint64_t* rowptr = nullptr;
     uint2* edges = nullptr;
+    // SageConv mean adjacency (graph neighbours without the self loop): rowptr_m,
+    // edges_m weighted 1/deg(row) (mean, graph.cpp:100-112), edges_mt weighted
+    // 1/deg(col) (mean_t, nn.hpp:85-98); only when this stage has a SageConv layer
+    bool has_sage = false;
+    uint64_t* rowptr_m = nullptr;
+    uint2* edges_m = nullptr;
+    uint2* edges_mt = nullptr;
     uint32_t* orig = nullptr;          // new -> original id (device)
     std::vector<uint32_t> perm;        // original -> new (host)
     std::vector<uint32_t> inv;         // new -> original (host)
@@ -458,11 +471,17 @@ struct Stage {
         grank = c.group_rank;
         if (G > 8 || grank >= G) throw Error(GP_EINVAL, "group_size must be in [1, 8] and group_rank < group_size");
         needs_h0 = false;
-        for (const auto& sp : specs) {
-            if (sp.kind == GP_SAGECONV)
-                throw Error(GP_EINVAL, "SageConv is not supported by the GPU engine");
+        has_sage = false;
+        for (uint32_t l = 0; l < c.num_layers; ++l) {
+            const auto& sp = specs[l];
             if (sp.kind > GP_GCN2CONV) throw Error(GP_EINVAL, "unknown layer kind");
             if (sp.kind == GP_GCN2CONV) needs_h0 = true;
+            if (sp.kind == GP_SAGECONV && l >= c.layer_begin && l < c.layer_end) {
+                if (sp.in_dim > kMaxWidth)
+                    throw Error(GP_EINVAL, "SageConv input width > 128 is not supported by the GPU engine");
+                if (G > 1) throw Error(GP_EINVAL, "SageConv in hybrid groups (group_size > 1) is not supported");
+                has_sage = true;
+            }
         }
         if (first != (lb == 0)) throw Error(GP_EINVAL, "stage 0 must own layer 0");
         if (last != (le == c.num_layers)) throw Error(GP_EINVAL, "last stage must own layer L-1");
@@ -505,10 +524,19 @@ struct Stage {
             d.sin = pad8(d.din);
             d.sout = pad8(d.dout);
             d.agg = d.spec.kind != GP_DENSE;
+            d.sage = d.spec.kind == GP_SAGECONV;
+            d.kin = d.sage ? 2 * d.din : d.din;
+            d.sgap = d.sage ? d.sin : 0;
+            d.kw = d.sage ? d.sgap + d.din : d.din;
+            d.skw = pad8(d.kw);
             const bool bias = d.spec.kind != GP_GCN2CONV;
-            const size_t wn = size_t(d.din) * d.dout;
+            const size_t wn = size_t(d.kin) * d.dout;
             d.W = dalloc<float>(wn);
             d.WT = dalloc<float>(wn);
+            if (d.sage) {
+                d.Wg = dalloc<float>(size_t(d.kw) * d.dout);
+                d.WTg = dalloc<float>(size_t(d.kw) * d.dout);
+            }
             d.gW = dalloc<float>(wn);
             d.mW = dalloc<float>(wn);
             d.vW = dalloc<float>(wn);
@@ -519,7 +547,7 @@ struct Stage {
                 d.vb = dalloc<float>(d.dout);
             }
             d.h = dalloc<float>(size_t(n) * d.sout);
-            d.pre = dalloc<float>(size_t(n) * d.sin);
+            d.pre = dalloc<float>(size_t(n) * d.skw);
             d.dz = dalloc<float>(size_t(n) * d.sout);
             // gather tables carry one extra all-zero row (row n, see gather_row)
             if (d.agg) {
@@ -530,8 +558,8 @@ struct Stage {
             if (!sync && i + 1 < len && specs[lb + i + 1].kind != GP_DENSE)
                 d.hs = dalloc<float>(size_t(n) * d.sout);
             if (d.l > 0) {
-                d.bg = dalloc<float>(size_t(n + 1) * d.sin);
-                if (hist && d.agg) d.bgs = dalloc<float>(size_t(n + 1) * d.sin);
+                d.bg = dalloc<float>(size_t(n + 1) * d.skw);
+                if (hist && d.agg) d.bgs = dalloc<float>(size_t(n + 1) * d.skw);
             }
         }
         if (!first) {
@@ -545,7 +573,7 @@ struct Stage {
         // pgrad workspace: ~2 waves of CTAs
         splits = std::max<uint32_t>(1, std::min<uint32_t>(2 * num_sms, (n + 63) / 64));
         size_t wmax = 1;
-        for (auto& d : L) wmax = std::max(wmax, size_t(d.din) * d.dout);
+        for (auto& d : L) wmax = std::max(wmax, size_t(d.din) * d.dout);  // per half for SageConv
         ws = dalloc<float>(size_t(splits) * wmax, false);
         wsb = dalloc<float>(size_t(splits) * kMaxWidth, false);
         xent_blocks = uint32_t(std::min<uint64_t>(2ull * num_sms, (n + kWarpsPerBlock - 1) / kWarpsPerBlock));
@@ -588,6 +616,15 @@ struct Stage {
                              (const void*)k_fwd8<FWD_GCN2, NB>,
                              (const void*)k_fwd8<FWD_GCN, NB, true>,
                              (const void*)k_fwd8<FWD_GCN2, NB, true>,
+                             (const void*)k_fwd8<FWD_SAGE, NB, true>,
+                             (const void*)k_bwd8<PREV_TOP, OUT_LAYER, NB, true>,
+                             (const void*)k_bwd8<PREV_OWN, OUT_LAYER, NB, true>,
+                             (const void*)k_bwd8<PREV_SAGE, OUT_LAYER, NB>,
+                             (const void*)k_bwd8<PREV_SAGE_HIST, OUT_LAYER, NB>,
+                             (const void*)k_bwd8<PREV_SAGE, OUT_LAYER, NB, true>,
+                             (const void*)k_bwd8<PREV_SAGE_HIST, OUT_LAYER, NB, true>,
+                             (const void*)k_bwd8<PREV_SAGE, OUT_DHIN, NB>,
+                             (const void*)k_bwd8<PREV_SAGE_HIST, OUT_DHIN, NB>,
                              (const void*)k_bwd8<PREV_TOP, OUT_LAYER, NB>,
                              (const void*)k_bwd8<PREV_AGG, OUT_LAYER, NB>,
                              (const void*)k_bwd8<PREV_AGG_HIST, OUT_LAYER, NB>,
@@ -610,9 +647,9 @@ struct Stage {
                                (const void*)k_fwd_tile<false, 4>, (const void*)k_fwd_tile<true, 4>,
                                (const void*)k_bwd_tile<1>,        (const void*)k_bwd_tile<2>,
                                (const void*)k_bwd_tile<4>};
+        GP_CUDA(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
         for (const void* f : tiles) {
-            GP_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(tile_smem_bytes(kMaxWidth, kMaxWidth, 4))));
+            GP_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin));
             GP_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
                                          int(cudaSharedmemCarveoutMaxShared)));
         }
@@ -631,7 +668,7 @@ struct Stage {
                              (const void*)k_pgrad_tc,    (const void*)k_pull_rows,     (const void*)k_remask,
                              (const void*)k_spmm_pre,    (const void*)k_stamp,         (const void*)k_transpose,
                              (const void*)k_xent_fold,   (const void*)k_xent_grad,     (const void*)k_xent_stats,
-                             (const void*)k_zero};
+                             (const void*)k_zero,        (const void*)k_sage_weights};
         for (const void* f : fns) {
             cudaFuncAttributes a;
             GP_CUDA(cudaFuncGetAttributes(&a, f));
@@ -688,9 +725,19 @@ struct Stage {
         const void* fn = (const void*)k_fwd_tile<GCN2, TR>;
         k_fwd_tile<GCN2, TR><<<tile_grid(rows, fn, smem, tile_geom(p.din, p.dout, TR).tm), kTileThreads, smem, cs>>>(p);
     }
+    int smem_optin = 227 * 1024;
+    // rows per thread for a tile launch: by launch size, then down until the
+    // staged matrix + double-buffered row tiles fit (SageConv's 2*din-wide transforms)
+    int tile_tr(uint32_t rows, uint32_t win, uint32_t wout) const {
+        int tr = tile_rows_per_thread(rows, wout, num_sms);
+        while (tr > 1 && tile_smem_bytes(win, wout, uint32_t(tr)) > size_t(smem_optin)) tr /= 2;
+        if (tile_smem_bytes(win, wout, uint32_t(tr)) > size_t(smem_optin))
+            throw Error(GP_EINVAL, "row transform too wide for shared memory");
+        return tr;
+    }
     template <bool GCN2>
     void fwd_dense_go(uint32_t rows, const FwdParams& p) {
-        switch (tile_rows_per_thread(rows, p.dout, num_sms)) {
+        switch (tile_tr(rows, p.din, p.dout)) {
             case 4: fwd_tile_go<GCN2, 4>(rows, p); break;
             case 2: fwd_tile_go<GCN2, 2>(rows, p); break;
             default: fwd_tile_go<GCN2, 1>(rows, p); break;
@@ -703,7 +750,7 @@ struct Stage {
         k_bwd_tile<TR><<<tile_grid(rows, fn, smem, tile_geom(p.dout, p.din, TR).tm), kTileThreads, smem, cs>>>(p);
     }
     void bwd_dense_go(uint32_t rows, const BwdParams& p) {
-        switch (tile_rows_per_thread(rows, p.din, num_sms)) {
+        switch (tile_tr(rows, p.dout, p.din)) {
             case 4: bwd_tile_go<4>(rows, p); break;
             case 2: bwd_tile_go<2>(rows, p); break;
             default: bwd_tile_go<1>(rows, p); break;
@@ -811,6 +858,39 @@ struct Stage {
             });
         for (auto& th : pool) th.join();
         if (bad) throw Error(GP_EINVAL, "CSR column out of range");
+        if (has_sage) {
+            // mean / mean_t (graph.cpp:100-112, nn.hpp:85-98): the normalised rows
+            // without the self loop, same renumbering and chunk bits
+            std::vector<uint32_t> deg(n, 0);
+            for (uint32_t v = 0; v < n; ++v)
+                for (uint64_t i = off[v]; i < off[v + 1]; ++i) deg[v] += cols[i] != v;
+            std::vector<uint64_t> rpm(size_t(n) + 1, 0);
+            for (uint32_t r = 0; r < n; ++r) rpm[r + 1] = rpm[r] + deg[inv[r]];
+            std::vector<uint2> em(std::max<uint64_t>(rpm[n], 1)), emt(std::max<uint64_t>(rpm[n], 1));
+            for (uint32_t r = 0; r < n; ++r) {
+                const uint32_t v = inv[r];
+                const float wv = deg[v] ? float(1.0 / double(deg[v])) : 0.f;
+                uint64_t w = rpm[r];
+                for (uint64_t i = off[v]; i < off[v + 1]; ++i) {
+                    const uint32_t u = cols[i];
+                    if (u == v) continue;
+                    const float wu = deg[u] ? float(1.0 / double(deg[u])) : 0.f;
+                    uint32_t bv, bu;
+                    std::memcpy(&bv, &wv, 4);
+                    std::memcpy(&bu, &wu, 4);
+                    const uint32_t col = perm[u] | (chunk_of[u] << kColBits);
+                    em[w] = make_uint2(col, bv);
+                    emt[w] = make_uint2(col, bu);
+                    ++w;
+                }
+            }
+            rowptr_m = dalloc<uint64_t>(size_t(n) + 1, false);
+            edges_m = dalloc<uint2>(em.size(), false);
+            edges_mt = dalloc<uint2>(emt.size(), false);
+            GP_CUDA(cudaMemcpy(rowptr_m, rpm.data(), rpm.size() * 8, cudaMemcpyHostToDevice));
+            GP_CUDA(cudaMemcpy(edges_m, em.data(), em.size() * 8, cudaMemcpyHostToDevice));
+            GP_CUDA(cudaMemcpy(edges_mt, emt.data(), emt.size() * 8, cudaMemcpyHostToDevice));
+        }
         nnz = nz;
         rowptr = dalloc<uint64_t>(size_t(n) + 1, false);
         edges = dalloc<uint2>(std::max<uint64_t>(nz, 1), false);
@@ -863,6 +943,10 @@ struct Stage {
             throw Error(GP_EINVAL, "graph sharing needs the same N, K, G and device");
         rowptr = o.rowptr;
         edges = o.edges;
+        if (has_sage && !o.rowptr_m) throw Error(GP_EINVAL, "graph sharing: owner stage has no SageConv adjacency");
+        rowptr_m = o.rowptr_m;
+        edges_m = o.edges_m;
+        edges_mt = o.edges_mt;
         orig = o.orig;
         perm = o.perm;
         inv = o.inv;
@@ -916,6 +1000,13 @@ struct Stage {
     }
 
     void transpose_w(const LayerDev& d) {
+        if (d.sage) {
+            const uint32_t nw = d.kw * d.dout;
+            launch(GP_K_OPTIM, nw * 12.0, 0, 0, [&]() {
+                k_sage_weights<<<(nw + 255) / 256, 256, 0, cs>>>(d.W, d.Wg, d.WTg, d.din, d.dout, d.sgap);
+            });
+            return;
+        }
         const uint32_t nw = d.din * d.dout;
         launch(GP_K_OPTIM, nw * 8.0, 0, 0,
                [&]() { k_transpose<<<(nw + 255) / 256, 256, 0, cs>>>(d.W, d.WT, d.din, d.dout); });
@@ -924,7 +1015,7 @@ struct Stage {
     void set_params(uint32_t l, const float* W, const float* b) {
         GP_CUDA(cudaSetDevice(device));
         auto& d = layer(l);
-        GP_CUDA(cudaMemcpy(d.W, W, size_t(d.din) * d.dout * 4, cudaMemcpyHostToDevice));
+        GP_CUDA(cudaMemcpy(d.W, W, size_t(d.kin) * d.dout * 4, cudaMemcpyHostToDevice));
         transpose_w(d);
         GP_CUDA(cudaStreamSynchronize(cs));
         if (d.b) {
@@ -937,7 +1028,7 @@ struct Stage {
         GP_CUDA(cudaSetDevice(device));
         GP_CUDA(cudaStreamSynchronize(cs));
         auto& d = layer(l);
-        if (W) GP_CUDA(cudaMemcpy(W, d.gW, size_t(d.din) * d.dout * 4, cudaMemcpyDeviceToHost));
+        if (W) GP_CUDA(cudaMemcpy(W, d.gW, size_t(d.kin) * d.dout * 4, cudaMemcpyDeviceToHost));
         if (d.gb && b) GP_CUDA(cudaMemcpy(b, d.gb, size_t(d.dout) * 4, cudaMemcpyDeviceToHost));
     }
 
@@ -946,7 +1037,7 @@ struct Stage {
         GP_CUDA(cudaSetDevice(device));
         GP_CUDA(cudaStreamSynchronize(cs));
         auto& d = layer(l);
-        const size_t wn = size_t(d.din) * d.dout * 4;
+        const size_t wn = size_t(d.kin) * d.dout * 4;
         if (mW) GP_CUDA(cudaMemcpy(mW, d.mW, wn, cudaMemcpyDeviceToHost));
         if (vW) GP_CUDA(cudaMemcpy(vW, d.vW, wn, cudaMemcpyDeviceToHost));
         if (d.mb && mb) GP_CUDA(cudaMemcpy(mb, d.mb, size_t(d.dout) * 4, cudaMemcpyDeviceToHost));
@@ -957,7 +1048,7 @@ struct Stage {
         GP_CUDA(cudaSetDevice(device));
         GP_CUDA(cudaStreamSynchronize(cs));
         auto& d = layer(l);
-        const size_t wn = size_t(d.din) * d.dout * 4;
+        const size_t wn = size_t(d.kin) * d.dout * 4;
         if (!mW || !vW) throw Error(GP_EINVAL, "optimizer state: null weight moments");
         GP_CUDA(cudaMemcpy(d.mW, mW, wn, cudaMemcpyHostToDevice));
         GP_CUDA(cudaMemcpy(d.vW, vW, wn, cudaMemcpyHostToDevice));
@@ -973,7 +1064,7 @@ struct Stage {
         GP_CUDA(cudaSetDevice(device));
         GP_CUDA(cudaStreamSynchronize(cs));
         auto& d = layer(l);
-        if (W) GP_CUDA(cudaMemcpy(W, d.W, size_t(d.din) * d.dout * 4, cudaMemcpyDeviceToHost));
+        if (W) GP_CUDA(cudaMemcpy(W, d.W, size_t(d.kin) * d.dout * 4, cudaMemcpyDeviceToHost));
         if (d.b && b) GP_CUDA(cudaMemcpy(b, d.b, size_t(d.dout) * 4, cudaMemcpyDeviceToHost));
     }
 
@@ -1103,6 +1194,10 @@ struct Stage {
             p.gnext = gnext;
             p.gnstride = gnstride;
             p.next_mask = nk;
+            p.rowptr_m = rowptr_m;
+            p.edges_m = edges_m;
+            p.sgap = d.sgap;
+            p.prestride = d.skw;
             const size_t smem = row_smem_bytes(d.din, d.dout, 2);
             const double e = d.agg ? double(rowptr_nnz(r0, r1)) : 0.0;
             const double bytes = (d.agg ? e * 8.0 + double(rows + 1) * 8.0 + double(n) * d.din * 4.0
@@ -1113,6 +1208,19 @@ struct Stage {
             const double flops = 2.0 * e * d.din + 2.0 * double(rows) * d.din * d.dout;
             const double gather = e * double(d.sin) * 4.0;
             const int cls = d.agg ? GP_K_FWD_AGG : GP_K_FWD_DENSE;
+            if (d.sage) {
+                // pre = [own row | mean of neighbours] (gapped), then b + pre.W + ReLU + epilogue
+                const double eb = e * 8.0 + double(rows + 1) * 8.0 + double(n) * d.din * 4.0 + double(rows) * d.kw * 4.0;
+                const double db = double(rows) * (d.kw + d.dout + (gnext ? d.dout : 0)) * 4.0 +
+                                  double(d.kw) * d.dout * 4.0;
+                launch(GP_K_FWD_AGG, eb, 2.0 * e * d.din, gather, [&]() { fwd_nb<FWD_SAGE, true>(rows, kEdgeSlotBytes, p); });
+                FwdParams q = p;
+                q.W = d.Wg;
+                q.din = d.kw;
+                launch(GP_K_FWD_DENSE, db, 2.0 * double(rows) * d.kin * d.dout, 0,
+                       [&]() { fwd_dense_go<false>(rows, q); });
+                return;
+            }
             if (d.agg && split_rows) {
                 // gather + initial-residual mix -> pre, then b + pre.W + epilogue
                 const bool g2 = d.spec.kind == GP_GCN2CONV;
@@ -1206,10 +1314,16 @@ struct Stage {
             auto& nx = L[i + 1];
             p.bgn = nx.bg;
             p.bgn_snap = nx.bgs;
-            p.bgnstride = nx.sin;
+            p.bgnstride = nx.skw;
             p.zrow = n;
             p.prev_mask = drop_key(t, nx.l, nx.din);
-            if (nx.agg) {
+            if (nx.sage) {
+                prev = hist ? PREV_SAGE_HIST : PREV_SAGE;
+                p.rowptr_m = rowptr_m;
+                p.edges_m = edges_mt;
+                p.sgap = nx.sgap;
+                e = double(rowptr_nnz(r0, r1));
+            } else if (nx.agg) {
                 prev = hist ? PREV_AGG_HIST : PREV_AGG;
                 e = double(rowptr_nnz(r0, r1));
             } else {
@@ -1224,8 +1338,8 @@ struct Stage {
         p.dz = d.dz;
         p.dzstride = d.sout;
         p.W = d.W;
-        p.WT = d.WT;
-        p.din = d.din;
+        p.WT = d.sage ? d.WTg : d.WT;
+        p.din = d.kw;  // dagg width: the gapped [own | mean] layout for SageConv
         p.dout = d.dout;
         p.need_dagg = d.l > 0;
         p.gcn2 = d.spec.kind == GP_GCN2CONV;
@@ -1236,20 +1350,29 @@ struct Stage {
         p.omb = 1.f - beta;
         p.dh0 = dh0;
         p.bg = d.bg;
-        p.bgstride = d.sin;
+        p.bgstride = d.skw;
         const size_t smem = p.need_dagg ? row_smem_bytes(d.dout, d.din, 2) : kEdgeSlotBytes;
         const double bytes = e * 8.0 + (e > 0 ? double(n) * d.dout * 4.0 : double(rows) * d.dout * 4.0) +
                              double(rows) * d.dout * 8.0 + (p.need_dagg ? double(rows) * d.din * 4.0 : 0.0) +
                              (p.gcn2 ? double(rows) * d.din * 8.0 : 0.0);
         const double flops = 2.0 * e * d.dout + (p.need_dagg ? 2.0 * double(rows) * d.din * d.dout : 0.0);
         const double gather = e * double(pad8(d.dout)) * 4.0;
-        const int cls = prev == PREV_AGG || prev == PREV_AGG_HIST ? GP_K_BWD_AGG : GP_K_BWD_DENSE;
-        if (split_rows && cls == GP_K_BWD_AGG) {
+        const int cls = prev == PREV_AGG || prev == PREV_AGG_HIST || prev == PREV_SAGE || prev == PREV_SAGE_HIST
+                            ? GP_K_BWD_AGG
+                            : GP_K_BWD_DENSE;
+        // SageConv layers (2*din-wide dagg) and SageConv neighbours always run split
+        if ((split_rows && cls == GP_K_BWD_AGG) || d.sage || prev == PREV_SAGE || prev == PREV_SAGE_HIST) {
             // gather (+ mask, dh0 term, ReLU) -> dz, then dz.W^T + mixes -> bg, dh0
             const double ab = e * 8.0 + double(n) * d.dout * 4.0 + double(rows) * d.dout * 8.0;
-            launch(GP_K_BWD_AGG, ab, 2.0 * e * d.dout, gather, [&]() {
-                if (prev == PREV_AGG) bwd_nb<PREV_AGG, OUT_LAYER, true>(rows, kEdgeSlotBytes, p);
-                else bwd_nb<PREV_AGG_HIST, OUT_LAYER, true>(rows, kEdgeSlotBytes, p);
+            launch(cls, ab, 2.0 * e * d.dout, gather, [&]() {
+                switch (prev) {
+                    case PREV_TOP: bwd_nb<PREV_TOP, OUT_LAYER, true>(rows, kEdgeSlotBytes, p); break;
+                    case PREV_AGG: bwd_nb<PREV_AGG, OUT_LAYER, true>(rows, kEdgeSlotBytes, p); break;
+                    case PREV_AGG_HIST: bwd_nb<PREV_AGG_HIST, OUT_LAYER, true>(rows, kEdgeSlotBytes, p); break;
+                    case PREV_SAGE: bwd_nb<PREV_SAGE, OUT_LAYER, true>(rows, kEdgeSlotBytes, p); break;
+                    case PREV_SAGE_HIST: bwd_nb<PREV_SAGE_HIST, OUT_LAYER, true>(rows, kEdgeSlotBytes, p); break;
+                    default: bwd_nb<PREV_OWN, OUT_LAYER, true>(rows, kEdgeSlotBytes, p);
+                }
             });
             if (p.need_dagg) {
                 const double db = double(rows) * (d.dout + d.din) * 4.0 + (p.gcn2 ? double(rows) * d.din * 8.0 : 0.0) +
@@ -1290,14 +1413,22 @@ struct Stage {
         p.dh_width = d.din;
         p.bgn = d.bg;
         p.bgn_snap = d.bgs;
-        p.bgnstride = d.sin;
+        p.bgnstride = d.skw;
         p.zrow = n;
         p.prev_mask = drop_key(t, d.l, d.din);
         p.dh_in = dh_in;
         p.dhinstride = sin0;
+        p.rowptr_m = rowptr_m;
+        p.edges_m = edges_mt;
+        p.sgap = d.sgap;
         const double e = d.agg ? double(rowptr_nnz(r0, r1)) : 0.0;
         const double bytes = e * 8.0 + (d.agg ? double(n) : double(rows)) * d.din * 4.0 + double(rows) * d.din * 4.0;
-        if (!d.agg)
+        if (d.sage)
+            launch(GP_K_BWD_AGG, bytes, 2.0 * e * d.din, e * d.sin * 4.0, [&]() {
+                if (hist) bwd_nb<PREV_SAGE_HIST, OUT_DHIN>(rows, kEdgeSlotBytes, p);
+                else bwd_nb<PREV_SAGE, OUT_DHIN>(rows, kEdgeSlotBytes, p);
+            });
+        else if (!d.agg)
             launch(GP_K_BWD_DENSE, bytes, 0, 0, [&]() { bwd_nb<PREV_OWN, OUT_DHIN>(rows, kEdgeSlotBytes, p); });
         else if (hist)
             launch(GP_K_BWD_AGG, bytes, 2.0 * e * d.din, e * d.sin * 4.0,
@@ -1334,6 +1465,19 @@ struct Stage {
         const uint32_t rb = own_begin(), re = own_end(), nown = re - rb;
         for (uint32_t i = 0; i < len; ++i) {
             auto& d = L[i];
+            // SageConv: dW rows [0, din) from pre's own half, [din, 2 din) from its mean half
+            for (uint32_t half = 0; half < (d.sage ? 2u : 1u); ++half)
+                pgrad_half(d, half, rb, re, nown);
+        }
+        if (G > 1) group_sync_grads();
+        adam_all(c1d, c2d);
+    }
+
+    void pgrad_half(LayerDev& d, uint32_t half, uint32_t rb, uint32_t re, uint32_t nown) {
+        {
+            const float* pre = d.pre + (half ? d.sgap : 0);
+            float* gW = d.gW + (half ? size_t(d.din) * d.dout : 0);
+            float* gb = half ? nullptr : d.gb;
             const uint32_t ti = (d.din + 127) / 128, tj = 1;
             const double pg_bytes = double(nown) * (d.din * tj + d.dout * ti) * 4.0 + double(splits) * d.din * d.dout * 4.0;
             const double pg_flops = 2.0 * double(nown) * d.din * d.dout;
@@ -1341,25 +1485,27 @@ struct Stage {
             if (use_tc_pgrad) {
                 // tcgen05 (3xTF32) split-K GEMM, one CTA per SM (TMEM accumulator, ~120 KB smem)
                 used_splits = std::min<uint32_t>(splits, uint32_t(num_sms));
-                TcPgradParams tp{re, (nown + used_splits - 1) / used_splits, rb, d.pre, d.sin, d.dz, d.sout, d.din,
-                                 d.dout, (d.dout + 15) / 16 * 16, ws, d.gb ? wsb : nullptr};
+                TcPgradParams tp{re, (nown + used_splits - 1) / used_splits, rb, pre, d.skw, d.dz, d.sout, d.din,
+                                 d.dout, (d.dout + 15) / 16 * 16, ws, gb ? wsb : nullptr};
                 const size_t smem = 2 * (2 * size_t(kTcM) * kTcKt * 4 + 2 * size_t(tp.npad) * kTcKt * 4);
                 dim3 grid(used_splits, ti, 1);
                 launch(GP_K_PGRAD, pg_bytes, pg_flops, 0, [&]() { k_pgrad_tc<<<grid, kTcThreads, smem, cs>>>(tp); });
             } else {
                 const uint32_t rps = (nown + splits - 1) / splits;
-                PgradParams pp{re, rps, rb, d.pre, d.sin, d.dz, d.sout, d.din, d.dout, ws, d.gb ? wsb : nullptr};
+                PgradParams pp{re, rps, rb, pre, d.skw, d.dz, d.sout, d.din, d.dout, ws, gb ? wsb : nullptr};
                 dim3 grid(splits, ti, 1);
                 launch(GP_K_PGRAD, pg_bytes, pg_flops, 0, [&]() { k_pgrad_partial<<<grid, 256, 0, cs>>>(pp); });
             }
             const uint32_t tot = d.din * d.dout + d.dout;
             const bool gcn2 = d.spec.kind == GP_GCN2CONV;
             launch(GP_K_PGRAD, double(splits) * tot * 4.0 + tot * 4.0, 0, 0, [&]() {
-                k_pgrad_fold<<<(tot + 255) / 256, 256, 0, cs>>>(ws, d.gb ? wsb : nullptr, used_splits, d.din, d.dout,
-                                                                float(d.spec.beta), gcn2, d.gW, d.gb);
+                k_pgrad_fold<<<(tot + 255) / 256, 256, 0, cs>>>(ws, gb ? wsb : nullptr, used_splits, d.din, d.dout,
+                                                                float(d.spec.beta), gcn2, gW, gb);
             });
         }
-        if (G > 1) group_sync_grads();
+    }
+
+    void adam_all(double c1d, double c2d) {
         for (uint32_t i = 0; i < len; ++i) {
             auto& d = L[i];
             AdamParams a{};
@@ -1376,7 +1522,7 @@ struct Stage {
             a.g = d.gW;
             a.m = d.mW;
             a.v = d.vW;
-            a.n = d.din * d.dout;
+            a.n = d.kin * d.dout;
             launch(GP_K_OPTIM, a.n * 20.0, 0, 0, [&]() { k_adam<<<(a.n + 255) / 256, 256, 0, cs>>>(a); });
             transpose_w(d);
             if (d.b) {
@@ -1581,6 +1727,14 @@ struct Stage {
                                            std::to_string(b.role) + " does not face this boundary");
             if (b.n != n || b.K != K) throw Error(GP_EINVAL, "gp_link_ipc: N/K mismatch");
             if (b.pad0 != grank) throw Error(GP_EINVAL, "gp_link_ipc: peer is another partition rank");
+            // Two stages in one CUDA context must not wait on each other in-stream: any
+            // implicit context synchronisation (module loading, frees, ...) on one stage's
+            // host thread then waits for the other stage's pending wait, whose value that
+            // thread has yet to enqueue. Same-process peers on one device link locally.
+            if (b.pid == int32_t(getpid()) && b.device == device)
+                throw Error(GP_EINVAL,
+                            "gp_link_ipc: the peer stage shares this process's CUDA context (same device); "
+                            "use gp_link_local");
             if (b.pid == int32_t(getpid())) {
                 x.peer = reinterpret_cast<char*>(uintptr_t(b.ptr));  // same process: plain UVA pointer
                 if (b.device != device) {
@@ -2315,16 +2469,16 @@ struct Stage {
         GP_CUDA(cudaStreamSynchronize(cs));
         if (!graph_ready) throw Error(GP_EINVAL, "graph not uploaded");
         const float* src = nullptr;
-        uint32_t width = 0, stride = 0;
+        uint32_t width = 0, stride = 0, gap = 0;
         auto need_layer = [&]() -> LayerDev& {
             if (i >= len) throw Error(GP_EINVAL, "local layer out of range");
             return L[i];
         };
         switch (which) {
             case GP_BUF_H: { auto& d = need_layer(); src = d.h; width = d.dout; stride = d.sout; break; }
-            case GP_BUF_PRE: { auto& d = need_layer(); src = d.pre; width = d.din; stride = d.sin; break; }
+            case GP_BUF_PRE: { auto& d = need_layer(); src = d.pre; width = d.din; stride = d.skw; gap = d.sgap; break; }
             case GP_BUF_DZ: { auto& d = need_layer(); src = d.dz; width = d.dout; stride = d.sout; break; }
-            case GP_BUF_DAGG: { auto& d = need_layer(); src = d.bg; width = d.din; stride = d.sin; break; }
+            case GP_BUF_DAGG: { auto& d = need_layer(); src = d.bg; width = d.din; stride = d.skw; gap = d.sgap; break; }
             case GP_BUF_HSNAP: { auto& d = need_layer(); src = d.hs; width = d.dout; stride = d.sout; break; }
             case GP_BUF_GATHER: { auto& d = need_layer(); src = d.G; width = d.din; stride = d.sin; break; }
             case GP_BUF_DH0: src = dh0; width = H; stride = pad8(H); break;
@@ -2333,11 +2487,15 @@ struct Stage {
             default: throw Error(GP_EINVAL, "unknown buffer");
         }
         if (!src) throw Error(GP_EINVAL, "buffer not allocated on this stage");
-        if (count != uint64_t(n) * width) throw Error(GP_EINVAL, "count != N * width");
+        // SageConv pre / dagg: k_in = 2 din columns, halves at 0 and gap
+        const uint32_t ow = gap ? 2 * width : width;
+        if (count != uint64_t(n) * ow) throw Error(GP_EINVAL, "count != N * width");
         std::vector<float> tmp(size_t(n) * stride);
         GP_CUDA(cudaMemcpy(tmp.data(), src, tmp.size() * 4, cudaMemcpyDeviceToHost));
-        for (uint32_t r = 0; r < n; ++r)
-            std::memcpy(out + size_t(inv[r]) * width, &tmp[size_t(r) * stride], size_t(width) * 4);
+        for (uint32_t r = 0; r < n; ++r) {
+            std::memcpy(out + size_t(inv[r]) * ow, &tmp[size_t(r) * stride], size_t(width) * 4);
+            if (gap) std::memcpy(out + size_t(inv[r]) * ow + width, &tmp[size_t(r) * stride + gap], size_t(width) * 4);
+        }
     }
 };
 

@@ -20,8 +20,8 @@ constexpr int kWarpsPerBlock = 8;
 constexpr int kBlock = kWarpsPerBlock * 32;
 constexpr unsigned kFull = 0xffffffffu;
 
-enum FwdKind { FWD_DENSE = 0, FWD_GCN = 1, FWD_GCN2 = 2 };
-enum PrevKind { PREV_TOP = 0, PREV_AGG = 1, PREV_AGG_HIST = 2, PREV_OWN = 3 };
+enum FwdKind { FWD_DENSE = 0, FWD_GCN = 1, FWD_GCN2 = 2, FWD_SAGE = 3 };
+enum PrevKind { PREV_TOP = 0, PREV_AGG = 1, PREV_AGG_HIST = 2, PREV_OWN = 3, PREV_SAGE = 4, PREV_SAGE_HIST = 5 };
 enum OutKind { OUT_LAYER = 0, OUT_DHIN = 1 };
 
 __device__ __forceinline__ float4 ld4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
@@ -227,6 +227,11 @@ struct FwdParams {
     float* gnext;
     uint32_t gnstride;
     DropKey next_mask;
+    // SageConv (FWD_SAGE): mean adjacency (graph neighbours, weight 1/deg(v)) and the
+    // column of pre where the aggregated half starts (pad8(din); own half at 0)
+    const uint64_t* rowptr_m;
+    const uint2* edges_m;
+    uint32_t sgap;
 };
 
 // GcnConv aggregation for d_in > 128 (column blocks of 128): pre = A_hat . G.
@@ -398,6 +403,11 @@ struct BwdParams {
     uint32_t bgstride;
     float* dh_in;
     uint32_t dhinstride;
+    // next layer SageConv (PREV_SAGE*): transposed mean adjacency (weight 1/deg(col))
+    // and the column of its bg where the aggregated half's gradient starts
+    const uint64_t* rowptr_m;
+    const uint2* edges_m;
+    uint32_t sgap;
 };
 
 // ---------------------------------------------------------------------------
@@ -684,6 +694,23 @@ __global__ void k_copy(float* __restrict__ dst, const float* __restrict__ src, s
         for (size_t i = n4 * 4 + tid; i < n; i += step) dst[i] = src[i];
     } else {
         for (size_t i = tid; i < n; i += step) dst[i] = src[i];
+    }
+}
+
+// SageConv weights in the gapped layout of pre / bg (own half at rows [0, din),
+// aggregated half at rows [sgap, sgap + din), zero rows between): Wg (kw x dout)
+// for the forward transform and WTg = Wg^T (dout x kw) for dagg = dz.W^T. The
+// zero rows meet pre's zero padding columns (+0 products): bit-exact.
+__global__ void k_sage_weights(const float* __restrict__ W, float* __restrict__ Wg, float* __restrict__ WTg,
+                               uint32_t din, uint32_t dout, uint32_t sgap) {
+    const uint32_t kw = sgap + din;
+    for (uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x; idx < kw * dout; idx += gridDim.x * blockDim.x) {
+        const uint32_t r = idx / dout, c = idx % dout;
+        float v = 0.f;
+        if (r < din) v = W[size_t(r) * dout + c];
+        else if (r >= sgap) v = W[size_t(r - sgap + din) * dout + c];
+        Wg[idx] = v;
+        WTg[size_t(c) * kw + r] = v;
     }
 }
 

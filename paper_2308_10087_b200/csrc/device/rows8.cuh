@@ -97,7 +97,7 @@ template <bool FILTER, bool HIST, int NB>
 __device__ __forceinline__ F8 gather_row8(const uint64_t* __restrict__ rowptr, const uint2* __restrict__ edges,
                                           uint32_t v, bool has_row, const float* __restrict__ src,
                                           const float* __restrict__ snap, uint32_t stride, uint64_t done,
-                                          int lane, bool active, uint2* eslot) {
+                                          int lane, bool active, uint2* eslot, const F8& init) {
     const int hl = lane & 15, hb = lane & 16;
     uint64_t e0 = 0, e1 = 0;
     if (has_row) {
@@ -112,7 +112,7 @@ __device__ __forceinline__ F8 gather_row8(const uint64_t* __restrict__ rowptr, c
     // padding entry: this half's own row (distinct per half-warp, so padding never
     // concentrates on one L2 line), weight 0, chunk bits 0
     const uint2 pad = make_uint2(has_row ? v : 0u, 0u);
-    F8 acc = f8_zero();
+    F8 acc = init;  // +0 (SpMM) or the own-row term SageConv's backward starts from (nn.hpp:234-243)
     uint2* es = eslot + (hb ? 16 : 0);
     auto batch16 = [&](const uint2 my) {
         if (kSmemEdges) {
@@ -351,10 +351,23 @@ __global__ void __launch_bounds__(kBlock, NB == 2 ? 4 : (NB == 4 ? 3 : 2)) k_fwd
         if (KIND == FWD_DENSE) {
             const F8 x = (has && in_act) ? ld8_stream(p.xsrc + size_t(v) * p.xstride + 8 * hl) : f8_zero();
             pre = drop8(p.in_mask, has ? p.orig[v] : 0u, 8 * hl, p.din, x);
+        } else if (KIND == FWD_SAGE) {
+            // pre = [drop(x_v) | mean over neighbours of drop(x_u)] (nn.hpp:176-182); the own row
+            // is the current gather-table row (v's chunk is done), the mean half starts at sgap
+            const F8 own = (has && in_act) ? ld8_stream(p.gsrc + size_t(v) * p.gstride + 8 * hl) : f8_zero();
+            const F8 z = gather_row8<false, true, NB>(p.rowptr_m, p.edges_m, v, has, p.gsrc, p.gsnap, p.gstride, p.done,
+                                                  lane, in_act, reinterpret_cast<uint2*>(smem4) + (threadIdx.x / 32) * 32,
+                                                  f8_zero());
+            if (has && in_act) {
+                st8_stream(p.pre + size_t(v) * p.prestride + 8 * hl, own);
+                st8_stream(p.pre + size_t(v) * p.prestride + p.sgap + 8 * hl, z);
+            }
+            continue;  // SageConv runs split: transform in k_fwd_tile (gapped weights)
         } else {
             // "cur if the neighbour's chunk is done, else snapshot" (engines_impl.hpp:740-744)
             const F8 z = gather_row8<false, true, NB>(p.rowptr, p.edges, v, has, p.gsrc, p.gsnap, p.gstride, p.done, lane,
-                                                  in_act, reinterpret_cast<uint2*>(smem4) + (threadIdx.x / 32) * 32);
+                                                  in_act, reinterpret_cast<uint2*>(smem4) + (threadIdx.x / 32) * 32,
+                                                  f8_zero());
             if (KIND == FWD_GCN2) {
                 const F8 h = (has && in_act) ? ld8_stream(p.h0 + size_t(v) * p.h0stride + 8 * hl) : f8_zero();
 #pragma unroll
@@ -449,12 +462,21 @@ __global__ void __launch_bounds__(kBlock, NB == 2 ? 4 : (NB == 4 ? 3 : 2)) k_bwd
             dh = (has && dh_act) ? ld8_stream(p.dtop + size_t(u) * p.dtopstride + 8 * hl) : f8_zero();
         } else {
             F8 s;
-            if (PREV == PREV_OWN)
+            if (PREV == PREV_OWN) {
                 s = (has && dh_act) ? ld8_stream(p.bgn + size_t(u) * p.bgnstride + 8 * hl) : f8_zero();
-            else
+            } else if (PREV == PREV_SAGE || PREV == PREV_SAGE_HIST) {
+                // SageConv backward_prev_row (nn.hpp:234-243): own half of dagg, then the done
+                // neighbours' aggregated halves weighted 1/deg(v), ascending
+                const F8 own = (has && dh_act) ? ld8_stream(p.bgn + size_t(u) * p.bgnstride + 8 * hl) : f8_zero();
+                s = gather_row8<true, PREV == PREV_SAGE_HIST, NB>(
+                    p.rowptr_m, p.edges_m, u, has, p.bgn + p.sgap, p.bgn_snap ? p.bgn_snap + p.sgap : nullptr,
+                    p.bgnstride, p.done, lane, dh_act, reinterpret_cast<uint2*>(smem4) + (threadIdx.x / 32) * 32, own);
+            } else {
                 s = gather_row8<true, PREV == PREV_AGG_HIST, NB>(p.rowptr, p.edges, u, has, p.bgn, p.bgn_snap, p.bgnstride,
                                                              p.done, lane, dh_act,
-                                                             reinterpret_cast<uint2*>(smem4) + (threadIdx.x / 32) * 32);
+                                                             reinterpret_cast<uint2*>(smem4) + (threadIdx.x / 32) * 32,
+                                                             f8_zero());
+            }
             dh = drop8(p.prev_mask, has ? p.orig[u] : 0u, 8 * hl, p.dh_width, s);
         }
         if (OUT == OUT_DHIN) {

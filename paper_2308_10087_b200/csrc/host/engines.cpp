@@ -137,9 +137,6 @@ TrainResult<float> run_hybrid_f32(const Dataset& ds, const Partition* part, cons
     for (uint8_t s : ds.split)
         if (s >= 1 && s <= 3) ++split_count[s - 1];
     if (split_count[0] == 0) throw std::invalid_argument("train_hybrid: empty train mask");
-    for (const auto& s : specs)
-        if (s.kind == LayerKind::SageConv)
-            throw std::invalid_argument("SageConv is outside the GPU engine's scope (GCN/GCNII only)");
 
     std::vector<gp_layer_spec> gspecs;
     for (const auto& s : specs) gspecs.push_back(to_gp(s));

@@ -31,6 +31,11 @@ SCENARIOS = {
     "shuffle_k8": ("shuffle", dict(K=8, seed=3, epochs=20)),
     "forward_gcn": ("forward", dict(spec=ER500, model="gcn", layers=3, hidden=16, seed=7, epoch=1)),
     "forward_gcnii": ("forward", dict(spec=ER500, model="gcnii", layers=5, hidden=16, seed=7, epoch=1)),
+    "forward_sage": ("forward", dict(spec=ER500, model="sage", layers=3, hidden=16, seed=7, epoch=1)),
+    "train_sage_s2k4": ("train", dict(spec=ER500, model="sage", layers=4, hidden=16, S=2, K=4, chunk_seed=3,
+                                      epochs=10, seed=46, fix_alpha=3)),
+    "train_sage_s1k4_hist": ("train", dict(spec=ER500, model="sage", layers=3, hidden=16, S=1, K=4, chunk_seed=3,
+                                           epochs=8, seed=47, fix_alpha=2, hist=1)),
     "train_gcn_s1k1": ("train", dict(spec=ER500, model="gcn", layers=4, hidden=16, S=1, K=1, epochs=10, seed=42)),
     "train_gcn_s2k4": ("train", dict(spec=ER500, model="gcn", layers=4, hidden=16, S=2, K=4, chunk_seed=3,
                                      epochs=10, seed=42, fix_alpha=3)),

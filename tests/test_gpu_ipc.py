@@ -11,7 +11,6 @@ import os
 import socket
 import subprocess
 import sys
-import threading
 
 import numpy as np
 import pytest
@@ -65,39 +64,21 @@ def test_ipc_stage_processes_match_in_process_pipeline(gp, tmp_path, S):
     check_same(res, n_train, z["losses"], [(z[f"W{l}"], z[f"b{l}"]) for l in range(L)])
 
 
-def test_ipc_stage_threads_same_process(gp):
-    """Same-process peers take the UVA-pointer path of gp_link_ipc (no IPC handle)."""
-    S, epochs = 2, 5
+def test_ipc_refuses_stages_sharing_a_context(gp):
+    """Two IPC-linked stages of one process on one device would share a CUDA context, where
+    an implicit context synchronisation on one stage's thread can wait forever on the other
+    stage's pending in-stream wait. gp_link_ipc refuses that pairing (gp_link_local is the
+    in-process transport); the same-process, other-device UVA path needs a second GPU."""
+    S = 2
     ds, model, chunk_of = W.problem()
     engs = [W.stage_engine(ds, model, chunk_of, r, S, 0) for r in range(S)]
     blobs = [e.ipc_export() for e, _ in engs]
-    engs[0][0].link_ipc(None, blobs[1][0])
-    engs[1][0].link_ipc(blobs[0][1], None)
-    losses, errs = [], []
-
-    def run(r):
-        try:
-            for t in range(1, epochs + 1):
-                st = engs[r][0].run_epoch(t, gp.shuffle_chunk_order(W.K, t, 1))
-                if st.has_quality:
-                    losses.append(st.loss_sum)
-        except Exception as e:  # surfaced below
-            errs.append(e)
-            for e2, _ in engs:
-                e2.abort()
-
-    th = [threading.Thread(target=run, args=(r,)) for r in range(S)]
-    for t in th:
-        t.start()
-    for t in th:
-        t.join(timeout=600)
-    assert not errs, errs
-    params = {}
-    for e, (lo, hi) in engs:
-        for l in range(lo, hi):
-            params[l] = e.get_params(l)
-    res, n_train = in_process(gp, S, epochs)
-    check_same(res, n_train, losses, params)
+    with pytest.raises(gp.InvalidArgument, match="gp_link_local"):
+        engs[0][0].link_ipc(None, blobs[1][0])
+    with pytest.raises(gp.InvalidArgument, match="gp_link_local"):
+        engs[1][0].link_ipc(blobs[0][1], None)
+    for e, _ in engs:
+        e.close()
     # ledger: the IPC transport accounts the same bytes as the reference fabric (4 B/value)
     for e, _ in engs:
         e.close()

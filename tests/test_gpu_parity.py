@@ -66,7 +66,7 @@ def single_stage(gp, ds, model, seed, K=1, chunk_of=None, **kw):
     return eng, specs
 
 
-@pytest.mark.parametrize("name,kind,layers", [("forward_gcn", 0, 3), ("forward_gcnii", 2, 5)])
+@pytest.mark.parametrize("name,kind,layers", [("forward_gcn", 0, 3), ("forward_gcnii", 2, 5), ("forward_sage", 1, 3)])
 def test_epoch1_forward_bitexact_and_backward_close(gp, name, kind, layers):
     ref = golden(name)
     ds = er500(gp)
@@ -92,7 +92,7 @@ def test_epoch1_forward_bitexact_and_backward_close(gp, name, kind, layers):
 
 
 @pytest.mark.parametrize("mode", ["tc", "simt"])
-@pytest.mark.parametrize("name,kind,layers", [("forward_gcn", 0, 3), ("forward_gcnii", 2, 5)])
+@pytest.mark.parametrize("name,kind,layers", [("forward_gcn", 0, 3), ("forward_gcnii", 2, 5), ("forward_sage", 1, 3)])
 def test_param_grads_match_reference(gp, name, kind, layers, mode, monkeypatch):
     """param_grads_for_rows (nn.hpp:269-293): tcgen05 3xTF32 (default) and CUDA-core paths."""
     monkeypatch.setenv("GP_PGRAD", mode)
@@ -169,6 +169,17 @@ def test_train_gcn_full_graph_matches_sequential_oracle(gp):
 def test_train_gcn_pipeline_stale_two_stages(gp):
     _train_compare(gp, "train_gcn_s2k4", er500(gp), gp.ModelConfig(kind=0, layers=4, hidden=16), 2, 4, 3, 10, 42,
                    fix_alpha=3)
+
+
+def test_train_sage_pipeline_stale_two_stages(gp):
+    """GraphSAGE (SageConv: [own | mean] . W, nn.hpp:176-182, :234-243) over two stages."""
+    _train_compare(gp, "train_sage_s2k4", er500(gp), gp.ModelConfig(kind=1, layers=4, hidden=16), 2, 4, 3, 10, 46,
+                   fix_alpha=3)
+
+
+def test_train_sage_historical_gradients(gp):
+    _train_compare(gp, "train_sage_s1k4_hist", er500(gp), gp.ModelConfig(kind=1, layers=3, hidden=16), 1, 4, 3, 8, 47,
+                   fix_alpha=2, historical_gradients=True)
 
 
 def test_train_gcnii_pipeline_stale_two_stages(gp):
@@ -264,9 +275,11 @@ def test_invalid_arguments_raise(gp):
         gp.train_pipeline(ds, np.zeros(ds.num_vertices, np.uint32), 5, gp.TrainOptions(model=model))
     with pytest.raises(gp.InvalidArgument):
         gp.train_pipeline(ds, np.arange(ds.num_vertices, dtype=np.uint32) % 65, 1, gp.TrainOptions(model=model))
-    with pytest.raises(gp.InvalidArgument):
-        gp.train_pipeline(ds, np.zeros(ds.num_vertices, np.uint32), 1,
-                          gp.TrainOptions(model=gp.ModelConfig(kind=1, layers=2, hidden=8)))
+    # SageConv runs on pipelines; hybrid groups (G > 1) do not support it yet
+    part, _, _ = gp.partition_vertices(ds, 2, 1)
+    with pytest.raises(gp.InvalidArgument, match="SageConv"):
+        gp.train_hybrid(ds, part, np.zeros(ds.num_vertices, np.uint32), 1,
+                        gp.TrainOptions(model=gp.ModelConfig(kind=1, layers=2, hidden=8)))
 
 
 HYB = [
