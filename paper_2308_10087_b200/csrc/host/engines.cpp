@@ -96,9 +96,11 @@ gp_layer_spec to_gp(const LayerSpec& s) {
 
 struct Ctxs {
     std::vector<gp_ctx*> v;
-    ~Ctxs() {
+    void destroy() {
         for (auto* c : v) gp_destroy(c);
+        v.clear();
     }
+    ~Ctxs() { destroy(); }
 };
 
 void validate_run(const Dataset& ds, const ChunkPlan& plan, const StageAssignment& sa, uint32_t L) {
@@ -191,6 +193,7 @@ TrainResult<float> run_hybrid_f32(const Dataset& ds, const Partition* part, cons
         gp_ctx* g = nullptr;
         check(gp_create(&c, &g), nullptr, "gp_create");
         ctx.v.push_back(g);
+        timer.mark("gp_create");
         if (G > 1) check(gp_upload_partition(g, part->assignment.data()), g, "gp_upload_partition");
         const int dev0 = opt.device >= 0 ? opt.device : 0;
         if (w == 0 || c.device != dev0) {
@@ -200,6 +203,7 @@ TrainResult<float> run_hybrid_f32(const Dataset& ds, const Partition* part, cons
         } else {
             check(gp_share_graph(g, ctx.v[0]), g, "gp_share_graph");
         }
+        timer.mark("graph");
         if (s == 0) check(gp_upload_features(g, ds.features.data(), ds.num_features()), g, "gp_upload_features");
         if (s + 1 == S) check(gp_upload_labels(g, ds.labels.data(), ds.split.data()), g, "gp_upload_labels");
         for (uint32_t l = sa.begin(s); l < sa.end(s); ++l)
@@ -403,6 +407,8 @@ TrainResult<float> run_hybrid_f32(const Dataset& ds, const Partition* part, cons
         }
     }
     timer.mark("results");
+    ctx.destroy();
+    timer.mark("destroy");
     return res;
 }
 
