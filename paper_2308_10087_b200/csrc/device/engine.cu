@@ -621,6 +621,15 @@ struct Stage {
                              (const void*)k_fwd8<FWD_GCN, NB, true>,
                              (const void*)k_fwd8<FWD_GCN2, NB, true>,
                              (const void*)k_fwd8<FWD_SAGE, NB, true>,
+                             (const void*)k_fwd8<FWD_GCN, NB, true, 5>,
+                             (const void*)k_fwd8<FWD_GCN2, NB, true, 5>,
+                             (const void*)k_fwd8<FWD_SAGE, NB, true, 5>,
+                             (const void*)k_bwd8<PREV_TOP, OUT_LAYER, NB, true, 5>,
+                             (const void*)k_bwd8<PREV_AGG, OUT_LAYER, NB, true, 5>,
+                             (const void*)k_bwd8<PREV_AGG_HIST, OUT_LAYER, NB, true, 5>,
+                             (const void*)k_bwd8<PREV_OWN, OUT_LAYER, NB, true, 5>,
+                             (const void*)k_bwd8<PREV_SAGE, OUT_LAYER, NB, true, 5>,
+                             (const void*)k_bwd8<PREV_SAGE_HIST, OUT_LAYER, NB, true, 5>,
                              (const void*)k_bwd8<PREV_TOP, OUT_LAYER, NB, true>,
                              (const void*)k_bwd8<PREV_OWN, OUT_LAYER, NB, true>,
                              (const void*)k_bwd8<PREV_SAGE, OUT_LAYER, NB>,
@@ -695,12 +704,25 @@ struct Stage {
         }
         if (const char* e = std::getenv("GP_SPLIT")) split_rows = std::string(e) != "0";
         if (const char* e = std::getenv("GP_IPC_SMCOPY")) ipc_smcopy = std::string(e) == "1";
+        if (const char* e = std::getenv("GP_OCC5")) occ5_mode = std::atoi(e) ? 1 : 0;
         setup_nb<2>();
         setup_nb<4>();
     }
 
+    // Split gather kernels: 5 resident CTAs (48 registers) when the launch has
+    // enough row pairs to keep every warp busy for several pairs, else 4 (64
+    // registers: more gathers in flight per warp). GP_OCC5=0/1 forces one.
+    int occ5_mode = -1;
+    bool use_occ5(uint32_t rows) const {
+        if (occ5_mode >= 0) return occ5_mode == 1;
+        return uint64_t(rows) / 2 >= 2ull * uint64_t(num_sms) * 5 * kWarpsPerBlock;
+    }
     template <int KIND, int NB, bool SPLIT = false>
     void fwd_go(uint32_t rows, size_t smem, const FwdParams& p) {
+        if (SPLIT && NB == 2 && use_occ5(rows)) {
+            k_fwd8<KIND, NB, SPLIT, 5><<<row_grid(rows, (const void*)k_fwd8<KIND, NB, SPLIT, 5>, smem, 16), kBlock, smem, cs>>>(p);
+            return;
+        }
         k_fwd8<KIND, NB, SPLIT><<<row_grid(rows, (const void*)k_fwd8<KIND, NB, SPLIT>, smem, 16), kBlock, smem, cs>>>(p);
     }
     template <int KIND, bool SPLIT = false>
@@ -762,6 +784,11 @@ struct Stage {
     }
     template <int PREV, int OUT, int NB, bool SPLIT = false>
     void bwd_go(uint32_t rows, size_t smem, const BwdParams& p) {
+        if (SPLIT && NB == 2 && use_occ5(rows)) {
+            k_bwd8<PREV, OUT, NB, SPLIT, 5>
+                <<<row_grid(rows, (const void*)k_bwd8<PREV, OUT, NB, SPLIT, 5>, smem, 16), kBlock, smem, cs>>>(p);
+            return;
+        }
         k_bwd8<PREV, OUT, NB, SPLIT>
             <<<row_grid(rows, (const void*)k_bwd8<PREV, OUT, NB, SPLIT>, smem, 16), kBlock, smem, cs>>>(p);
     }

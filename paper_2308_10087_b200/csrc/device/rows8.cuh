@@ -323,8 +323,16 @@ __device__ __forceinline__ void bwd_epilogue(const BwdParams& p, float (&g)[R][4
 // ReLU -> h, and the next layer's dropped gather source. SPLIT: stop at pre
 // (k_fwd_dense8 does the transform).
 // ---------------------------------------------------------------------------
-template <int KIND, int NB, bool SPLIT = false>
-__global__ void __launch_bounds__(kBlock, NB == 2 ? 4 : (NB == 4 ? 3 : 2)) k_fwd8(FwdParams p) {
+// Resident CTAs per SM the split (gather-only) kernels are compiled for: no
+// staged matrix, so registers alone bound their occupancy.
+#ifndef GP_SPLIT_MINB
+#define GP_SPLIT_MINB 4
+#endif
+// MINB > 0 overrides the resident-CTA target of the launch bounds (the split
+// kernels are also built for 5 CTAs / 48 registers: better for large launches).
+template <int KIND, int NB, bool SPLIT = false, int MINB = 0>
+__global__ void __launch_bounds__(kBlock, MINB ? MINB : (SPLIT && NB == 2 ? GP_SPLIT_MINB : (NB == 2 ? 4 : (NB == 4 ? 3 : 2))))
+    k_fwd8(FwdParams p) {
     extern __shared__ float4 smem4[];
     const uint32_t ms = mat_stride(p.dout);
     float* Ms = reinterpret_cast<float*>(reinterpret_cast<char*>(smem4) + kEdgeSlotBytes);
@@ -435,8 +443,9 @@ __global__ void __launch_bounds__(kBlock, 3) k_fwd_dense8(FwdParams p) {
 // layer i (nn.hpp:202-218): dz, dagg = dz.W^T, GCNII mixes, dh0 += a*dagg, and
 // bg_i = (1-a)*dagg (Gcn2Conv) or dagg. SPLIT: stop at dz (k_bwd_dense8).
 // ---------------------------------------------------------------------------
-template <int PREV, int OUT, int NB, bool SPLIT = false>
-__global__ void __launch_bounds__(kBlock, NB == 2 ? 4 : (NB == 4 ? 3 : 2)) k_bwd8(BwdParams p) {
+template <int PREV, int OUT, int NB, bool SPLIT = false, int MINB = 0>
+__global__ void __launch_bounds__(kBlock, MINB ? MINB : (SPLIT && NB == 2 ? GP_SPLIT_MINB : (NB == 2 ? 4 : (NB == 4 ? 3 : 2))))
+    k_bwd8(BwdParams p) {
     extern __shared__ float4 smem4[];
     const uint32_t ms = mat_stride(p.din);
     float* Ms = reinterpret_cast<float*>(reinterpret_cast<char*>(smem4) + kEdgeSlotBytes);
