@@ -160,6 +160,45 @@ __device__ __forceinline__ void tile_mac(float (&acc)[TR][8], const float* __res
     }
 }
 
+// tile_mac with the geometry of a square WIDTH x WIDTH transform fixed at compile
+// time (the model widths the engine specialises for: H = 100, 128), so every
+// shared-memory offset inside a k-group is an immediate and no index arithmetic
+// is issued between the loads and the FP pipe. Same arithmetic order as tile_mac.
+template <int TR, int WIDTH>
+__device__ __forceinline__ void tile_mac_fixed(float (&acc)[TR][8], const float* __restrict__ As,
+                                               const float* __restrict__ Ws, uint32_t rg, uint32_t cg) {
+    constexpr uint32_t kNcg = (WIDTH + 7) / 8, kNrg = kTileThreads / kNcg, kKp = (WIDTH + 3) & ~3;
+    constexpr uint32_t kAms = kKp + 4, kMs = ws_col(kNcg - 1) + 8, kRa = kNrg * kAms;
+    const float* a = As + size_t(rg) * kAms;
+    const float* w = Ws + ws_col(cg);
+#pragma unroll 1
+    for (uint32_t i = 0; i < kKp; i += 4, a += 4, w += 4 * kMs) {
+        float4 x[TR];
+#pragma unroll
+        for (int r = 0; r < TR; ++r) x[r] = *reinterpret_cast<const float4*>(a + r * kRa);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+            const float4 w0 = *reinterpret_cast<const float4*>(w + kk * kMs);
+            const float4 w1 = *reinterpret_cast<const float4*>(w + kk * kMs + 4);
+            const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+            for (int r = 0; r < TR; ++r) {
+                const float xv = f4_get(x[r], kk);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[r][j] = mul_add(acc[r][j], xv, wv[j]);
+            }
+        }
+    }
+}
+
+template <int TR, int WIDTH>
+__device__ __forceinline__ void tile_mac_any(float (&acc)[TR][8], const float* __restrict__ As,
+                                             const float* __restrict__ Ws, const TileGeom& g, uint32_t rg,
+                                             uint32_t cg) {
+    if constexpr (WIDTH != 0) tile_mac_fixed<TR, WIDTH>(acc, As, Ws, rg, cg);
+    else tile_mac<TR>(acc, As, Ws, g, rg, cg);
+}
+
 __device__ __forceinline__ void st8_hint(float* p, const float (&x)[8], uint64_t pol) {
     asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "f"(x[0]),
                  "f"(x[1]), "f"(x[2]), "f"(x[3]), "l"(pol)
@@ -188,7 +227,8 @@ __host__ inline int tile_rows_per_thread(uint32_t rows, uint32_t width_out, int 
 // gather row. Padding columns (c >= dout, up to the 8-float row stride) are
 // written as the zeros they already hold.
 // ---------------------------------------------------------------------------
-template <bool GCN2, int TR>
+// WIDTH != 0: din == dout == WIDTH (host-checked), compile-time geometry.
+template <bool GCN2, int TR, int WIDTH = 0>
 __global__ void __launch_bounds__(kTileThreads, 2) k_fwd_tile(FwdParams p) {
     extern __shared__ float4 smem4[];
     const TileGeom g = tile_geom(p.din, p.dout, TR);
@@ -226,7 +266,7 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_fwd_tile(FwdParams p) {
             for (int r = 0; r < TR; ++r)
 #pragma unroll
                 for (int j = 0; j < 8; ++j) acc[r][j] = bs[8 * cg + j];
-            tile_mac<TR>(acc, As, Ws, g, rg, cg);
+            tile_mac_any<TR, WIDTH>(acc, As, Ws, g, rg, cg);
 #pragma unroll
             for (int r = 0; r < TR; ++r) {
                 const uint32_t lr = rg + r * g.nrg, v = v0 + lr;
@@ -258,7 +298,7 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_fwd_tile(FwdParams p) {
 // dagg = dz.W^T; Gcn2Conv: dagg = (1-beta) dz + beta dagg, dh0 += alpha dagg,
 // bg = (1-alpha) dagg; otherwise bg = dagg.
 // ---------------------------------------------------------------------------
-template <int TR>
+template <int TR, int WIDTH = 0>
 __global__ void __launch_bounds__(kTileThreads, 2) k_bwd_tile(BwdParams p) {
     extern __shared__ float4 smem4[];
     const TileGeom g = tile_geom(p.dout, p.din, TR);
@@ -287,7 +327,7 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_bwd_tile(BwdParams p) {
             for (int r = 0; r < TR; ++r)
 #pragma unroll
                 for (int j = 0; j < 8; ++j) acc[r][j] = 0.f;
-            tile_mac<TR>(acc, As, Ws, g, rg, cg);
+            tile_mac_any<TR, WIDTH>(acc, As, Ws, g, rg, cg);
             // dh0 rows of the tile, all in flight before the epilogue consumes them
             float4 d0v[TR][2];
             if (p.gcn2) {

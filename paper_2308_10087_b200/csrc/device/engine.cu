@@ -691,11 +691,14 @@ struct Stage {
             GP_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
                                          int(cudaSharedmemCarveoutMaxShared)));
         }
-        const void* tiles[] = {(const void*)k_fwd_tile<false, 1>, (const void*)k_fwd_tile<true, 1>,
-                               (const void*)k_fwd_tile<false, 2>, (const void*)k_fwd_tile<true, 2>,
-                               (const void*)k_fwd_tile<false, 4>, (const void*)k_fwd_tile<true, 4>,
-                               (const void*)k_bwd_tile<1>,        (const void*)k_bwd_tile<2>,
-                               (const void*)k_bwd_tile<4>};
+        const void* tiles[] = {(const void*)k_fwd_tile<false, 1>,      (const void*)k_fwd_tile<true, 1>,
+                               (const void*)k_fwd_tile<false, 2>,      (const void*)k_fwd_tile<true, 2>,
+                               (const void*)k_fwd_tile<false, 4>,      (const void*)k_fwd_tile<true, 4>,
+                               (const void*)k_bwd_tile<1>,             (const void*)k_bwd_tile<2>,
+                               (const void*)k_bwd_tile<4>,             (const void*)k_fwd_tile<false, 4, 100>,
+                               (const void*)k_fwd_tile<true, 4, 100>,  (const void*)k_fwd_tile<false, 4, 128>,
+                               (const void*)k_fwd_tile<true, 4, 128>,  (const void*)k_bwd_tile<4, 100>,
+                               (const void*)k_bwd_tile<4, 128>};
         GP_CUDA(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
         for (const void* f : tiles) {
             GP_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin));
@@ -781,12 +784,15 @@ struct Stage {
         const uint64_t want = (uint64_t(rows) + tm - 1) / tm;
         return uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(want, uint64_t(num_sms) * occ)));
     }
-    template <bool GCN2, int TR>
+    template <bool GCN2, int TR, int WIDTH = 0>
     void fwd_tile_go(uint32_t rows, const FwdParams& p) {
         const size_t smem = tile_smem_bytes(p.din, p.dout, TR);
-        const void* fn = (const void*)k_fwd_tile<GCN2, TR>;
-        k_fwd_tile<GCN2, TR><<<tile_grid(rows, fn, smem, tile_geom(p.din, p.dout, TR).tm), kTileThreads, smem, cs>>>(p);
+        const void* fn = (const void*)k_fwd_tile<GCN2, TR, WIDTH>;
+        k_fwd_tile<GCN2, TR, WIDTH>
+            <<<tile_grid(rows, fn, smem, tile_geom(p.din, p.dout, TR).tm), kTileThreads, smem, cs>>>(p);
     }
+    // compile-time geometry for the square H = 100 / 128 transforms (TR = 4)
+    static int square_width(uint32_t a, uint32_t b) { return a == b && (a == 100 || a == 128) ? int(a) : 0; }
     int smem_optin = 227 * 1024;
     // rows per thread for a tile launch: by launch size, then down until the
     // staged matrix + double-buffered row tiles fit (SageConv's 2*din-wide transforms)
@@ -800,20 +806,28 @@ struct Stage {
     template <bool GCN2>
     void fwd_dense_go(uint32_t rows, const FwdParams& p) {
         switch (tile_tr(rows, p.din, p.dout)) {
-            case 4: fwd_tile_go<GCN2, 4>(rows, p); break;
+            case 4:
+                if (square_width(p.din, p.dout) == 100) fwd_tile_go<GCN2, 4, 100>(rows, p);
+                else if (square_width(p.din, p.dout) == 128) fwd_tile_go<GCN2, 4, 128>(rows, p);
+                else fwd_tile_go<GCN2, 4>(rows, p);
+                break;
             case 2: fwd_tile_go<GCN2, 2>(rows, p); break;
             default: fwd_tile_go<GCN2, 1>(rows, p); break;
         }
     }
-    template <int TR>
+    template <int TR, int WIDTH = 0>
     void bwd_tile_go(uint32_t rows, const BwdParams& p) {
         const size_t smem = tile_smem_bytes(p.dout, p.din, TR);
-        const void* fn = (const void*)k_bwd_tile<TR>;
-        k_bwd_tile<TR><<<tile_grid(rows, fn, smem, tile_geom(p.dout, p.din, TR).tm), kTileThreads, smem, cs>>>(p);
+        const void* fn = (const void*)k_bwd_tile<TR, WIDTH>;
+        k_bwd_tile<TR, WIDTH><<<tile_grid(rows, fn, smem, tile_geom(p.dout, p.din, TR).tm), kTileThreads, smem, cs>>>(p);
     }
     void bwd_dense_go(uint32_t rows, const BwdParams& p) {
         switch (tile_tr(rows, p.dout, p.din)) {
-            case 4: bwd_tile_go<4>(rows, p); break;
+            case 4:
+                if (square_width(p.din, p.dout) == 100) bwd_tile_go<4, 100>(rows, p);
+                else if (square_width(p.din, p.dout) == 128) bwd_tile_go<4, 128>(rows, p);
+                else bwd_tile_go<4>(rows, p);
+                break;
             case 2: bwd_tile_go<2>(rows, p); break;
             default: bwd_tile_go<1>(rows, p); break;
         }
@@ -869,37 +883,37 @@ struct Stage {
     // most kStageChunk bytes, each chunk is filled in a pinned staging buffer by
     // `nth` threads (fill(r, out) writes row r's entries) and DMA'd while the next
     // chunk is filled.
-    template <class Fill>
-    void stage_rows_h2d(uint2* dst, const std::vector<uint64_t>& rp, unsigned nth, Fill&& fill) {
+    template <class T, class Fill>
+    void stage_rows_h2d(T* dst, const std::vector<uint64_t>& rp, unsigned nth, Fill&& fill) {
         const uint32_t rows = uint32_t(rp.size() - 1);
         if (rp[rows] == 0) return;
         for (int i = 0; i < 2; ++i) {
             if (!h2d_stage[i]) GP_CUDA(cudaMallocHost(&h2d_stage[i], kStageChunk));
             if (!h2d_done[i]) GP_CUDA(cudaEventCreateWithFlags(&h2d_done[i], cudaEventDisableTiming));
         }
-        const uint64_t cap = kStageChunk / sizeof(uint2);
+        const uint64_t cap = kStageChunk / sizeof(T);
         bool used[2] = {false, false};
         uint32_t r0 = 0;
         for (uint32_t j = 0; r0 < rows; ++j) {
             uint32_t r1 = r0;
             while (r1 < rows && rp[r1 + 1] - rp[r0] <= cap) ++r1;
             if (r1 == r0) {  // one row larger than a chunk: copy it on its own
-                std::vector<uint2> tmp(rp[r0 + 1] - rp[r0]);
+                std::vector<T> tmp(rp[r0 + 1] - rp[r0]);
                 fill(r0, tmp.data());
-                GP_CUDA(cudaMemcpy(dst + rp[r0], tmp.data(), tmp.size() * sizeof(uint2), cudaMemcpyHostToDevice));
+                GP_CUDA(cudaMemcpy(dst + rp[r0], tmp.data(), tmp.size() * sizeof(T), cudaMemcpyHostToDevice));
                 r0 = r0 + 1;
                 continue;
             }
             const int b = int(j & 1);
             if (used[b]) GP_CUDA(cudaEventSynchronize(h2d_done[b]));
-            uint2* buf = reinterpret_cast<uint2*>(h2d_stage[b]);
+            T* buf = reinterpret_cast<T*>(h2d_stage[b]);
             std::vector<std::thread> pool;
             for (unsigned t = 0; t < nth; ++t)
                 pool.emplace_back([&, t]() {
                     for (uint32_t r = r0 + t; r < r1; r += nth) fill(r, buf + (rp[r] - rp[r0]));
                 });
             for (auto& th : pool) th.join();
-            GP_CUDA(cudaMemcpyAsync(dst + rp[r0], buf, (rp[r1] - rp[r0]) * sizeof(uint2), cudaMemcpyHostToDevice, cs));
+            GP_CUDA(cudaMemcpyAsync(dst + rp[r0], buf, (rp[r1] - rp[r0]) * sizeof(T), cudaMemcpyHostToDevice, cs));
             GP_CUDA(cudaEventRecord(h2d_done[b], cs));
             used[b] = true;
             r0 = r1;
@@ -1098,11 +1112,15 @@ struct Stage {
         if (f != specs[0].in_dim) throw Error(GP_EINVAL, "feature width != layer 0 in_dim");
         F = f;
         sx = pad8(f);
-        std::vector<float> hx(size_t(n) * sx, 0.f);
-        for (uint32_t r = 0; r < n; ++r)
-            std::memcpy(&hx[size_t(r) * sx], x + size_t(inv[r]) * f, size_t(f) * 4);
-        if (!x0) x0 = dalloc<float>(hx.size(), false);
-        h2d(x0, hx.data(), hx.size() * 4);
+        if (!x0) x0 = dalloc<float>(size_t(n) * sx, false);
+        // rows renumbered and padded straight into the pinned staging chunks
+        std::vector<uint64_t> rp(size_t(n) + 1);
+        for (uint32_t r = 0; r <= n; ++r) rp[r] = uint64_t(r) * sx;
+        const unsigned nth = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+        stage_rows_h2d(x0, rp, nth, [&](uint32_t r, float* out) {
+            std::memcpy(out, x + size_t(inv[r]) * f, size_t(f) * 4);
+            std::memset(out + f, 0, size_t(sx - f) * 4);
+        });
         x_ready = true;
     }
 

@@ -311,6 +311,7 @@ int main(int argc, char** argv) {
             runb("split k_bwd8<AGG,LAYER,4,1>", (const void*)k_bwd8<PREV_AGG, OUT_LAYER, 4, true>, done);
             runb("split k_bwd_dense8", (const void*)k_bwd_dense8, done, dsm);
             runb("split k_bwd_tile<4>", (const void*)k_bwd_tile<4>, done, tile_smem_bytes(H, H, 4));
+            runb("split k_bwd_tile<4,100>", (const void*)k_bwd_tile<4, 100>, done, tile_smem_bytes(H, H, 4));
         }
         runb("k_bwd8<AGG_HIST,LAYER,2>", (const void*)k_bwd8<PREV_AGG_HIST, OUT_LAYER, 2>, 0x3ull);
         std::vector<float> hb(tab);
@@ -364,6 +365,7 @@ int main(int argc, char** argv) {
         run("split gather k_fwd8<GCN2,4,1>", (const void*)k_fwd8<FWD_GCN2, 4, true>, kEdgeSlotBytes, K);
         run("split dense k_fwd_dense8<1>", (const void*)k_fwd_dense8<true>, dsm, K);
         run("split dense k_fwd_tile<1,4>", (const void*)k_fwd_tile<true, 4>, tile_smem_bytes(H, H, 4), K);
+        run("split dense k_fwd_tile<1,4,100>", (const void*)k_fwd_tile<true, 4, 100>, tile_smem_bytes(H, H, 4), K);
         run("split dense k_fwd_tile<1,2>", (const void*)k_fwd_tile<true, 2>, tile_smem_bytes(H, H, 2), K);
         run("split dense k_fwd_tile<1,1>", (const void*)k_fwd_tile<true, 1>, tile_smem_bytes(H, H, 1), K);
         run("k_fwd8 again", (const void*)k_fwd8<FWD_GCN2, 2>, wsm, K);
@@ -397,7 +399,7 @@ int main(int argc, char** argv) {
         for (size_t i = 0; i < tab; ++i) bad += (reinterpret_cast<uint32_t&>(ref[i]) != reinterpret_cast<uint32_t&>(got[i]));
         printf("split (gather + dense) vs fused: %zu differing floats\n", bad);
         full((const void*)k_fwd8<FWD_GCN2, 2, true>, kEdgeSlotBytes);
-        full((const void*)k_fwd_tile<true, 2>, tile_smem_bytes(H, H, 2));
+        full((const void*)k_fwd_tile<true, 4, 100>, tile_smem_bytes(H, H, 4));
         snap(got);
         bad = 0;
         for (size_t i = 0; i < tab; ++i) bad += (reinterpret_cast<uint32_t&>(ref[i]) != reinterpret_cast<uint32_t&>(got[i]));
