@@ -34,6 +34,11 @@ WORKLOADS = {
               "ogbn-arxiv-shaped ER graph (169,343 vertices, 2.33M directed edges, 128 feat, 40 classes), 16-layer GCN"),
     "er4k": (4096, 65520, 128, 16, 128, "gcn", 8,
              "ER 4K vertices avg-deg 16, 128 feat, 16 classes, 8-layer GCN"),
+    # 64 layers need ~560 GB of stashes at S=1 (70 GB per stage at S=8); on one GPU use --layers 8,
+    # the work of one of the 8 stages
+    "products": (2449029, 123718280, 100, 47, 128, "gcnii", 64,
+                 "ogbn-products-shaped ER graph (2,449,029 vertices, 123.7M directed edges, 100 feat, 47 classes), "
+                 "GCNII H=128"),
 }
 METRIC = "epoch time, 64-layer GCNII full-graph, 1/2/4/8 B200; SpMM GB/s vs HBM peak"
 
