@@ -371,6 +371,10 @@ def main():
                      "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": (achieved / hbm) if achieved else None, "peak_source": src, "traffic": traffic,
                      "l2_gather_gbs": gather_rate,
+                     # the binding roof of the gather: random 416-byte rows from the
+                     # L2-resident table through LDG.256, measured by tools/tex_gather_bench.cu
+                     "gather_ceiling_gbs": 16374.0,
+                     "gather_frac": (gather_rate / 16374.0) if gather_rate else None,
                      "share_of_step": fa["ms"] / total_ms if total_ms else None},
         "cpu_baseline": cpu,
         "kernel_ms_per_epoch": {k: round(v["ms"], 3) for k, v in prof.items() if v["launches"]},
