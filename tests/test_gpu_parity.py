@@ -171,10 +171,35 @@ def test_train_gcn_pipeline_stale_two_stages(gp):
                    fix_alpha=3)
 
 
-def test_train_sage_pipeline_stale_two_stages(gp):
-    """GraphSAGE (SageConv: [own | mean] . W, nn.hpp:176-182, :234-243) over two stages."""
+@pytest.mark.parametrize("env", [{}, {"GP_SPLIT": "0"}, {"GP_WAVE": "1"}, {"GP_OCC5": "1"}],
+                         ids=["default", "fused", "one_stream", "occ5"])
+def test_train_sage_pipeline_stale_two_stages(gp, env, monkeypatch):
+    """GraphSAGE (SageConv: [own | mean] . W, nn.hpp:176-182, :234-243) over two stages, under every
+    engine variant switch (SageConv layers always run split; the others follow GP_SPLIT)."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
     _train_compare(gp, "train_sage_s2k4", er500(gp), gp.ModelConfig(kind=1, layers=4, hidden=16), 2, 4, 3, 10, 46,
                    fix_alpha=3)
+
+
+@pytest.mark.parametrize("env", [{"GP_SPLIT": "0"}, {"GP_WAVE": "1"}, {"GP_OCC5": "1"}, {"GP_PGRAD": "simt"}],
+                         ids=["fused", "one_stream", "occ5", "simt_pgrad"])
+def test_engine_variants_match_default_bitwise(gp, env, monkeypatch):
+    """The engine's switches change scheduling and kernel shapes, never arithmetic order (except the
+    pgrad reduction): losses and parameters equal the default run bit for bit."""
+    ds = er500(gp)
+    model = gp.ModelConfig(kind=2, layers=6, hidden=16)
+    co = gp.make_chunks(ds, 4, 3)
+    base = gp.train_pipeline(ds, co, 2, gp.TrainOptions(model=model, epochs=4, seed=9, fix_alpha=2))
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    res = gp.train_pipeline(ds, co, 2, gp.TrainOptions(model=model, epochs=4, seed=9, fix_alpha=2))
+    if "GP_PGRAD" in env:  # different parameter-gradient summation order: tolerance
+        np.testing.assert_allclose(res.train_loss, base.train_loss, rtol=1e-4)
+        return
+    np.testing.assert_array_equal(res.train_loss, base.train_loss)
+    for (Wa, _), (Wb, _) in zip(res.params, base.params):
+        assert np.array_equal(Wa.view(np.uint32), Wb.view(np.uint32))
 
 
 def test_train_sage_historical_gradients(gp):
