@@ -140,6 +140,13 @@ gp_status gp_device_count(int* out);
  * device; neighbour order inside each row is preserved. */
 gp_status gp_upload_graph(gp_ctx* ctx, const uint64_t* offsets, const uint32_t* cols,
                           const float* vals, uint64_t nnz, const uint32_t* chunk_of);
+/* Same, from the graph itself (Graph::csr_offsets / csr_neighbors, graph.hpp:15-34:
+ * strictly ascending neighbours, no self loops): normalize_adjacency<float>
+ * (graph.cpp:68-98) is applied row by row while the packed CSR is built, with the
+ * same double-precision expression, so the uploaded matrix is bit-identical and no
+ * N-sized host copy of it is made. num_neighbors = 2E. */
+gp_status gp_upload_graph_raw(gp_ctx* ctx, const uint64_t* offsets, const uint32_t* neighbors,
+                              uint64_t num_neighbors, int self_loops, const uint32_t* chunk_of);
 /* Hybrid (train_hybrid, engines_impl.hpp:515-909, G > 1): the vertex partition
  * (Partition::assignment, partition.hpp:13-21). Call before gp_upload_graph. */
 gp_status gp_upload_partition(gp_ctx* ctx, const uint32_t* part_of);

@@ -29,6 +29,7 @@
 #include <stdexcept>
 #include <string>
 #include <thread>
+#include <type_traits>
 #include <vector>
 
 #include "../../../include/gnnpipe.h"
@@ -934,11 +935,66 @@ struct Stage {
     // stage messages (engines_impl.hpp:690-724) are slices, and a rank's own rows
     // (Partition::inner_sets[r]) are one range. Row content keeps the original
     // ascending neighbour order, so every reduction stays bit-exact.
+    // Rows of the normalised adjacency, from an uploaded CSR (off, cols, vals) ...
+    struct NormCsr {
+        const uint64_t* off;
+        const uint32_t* cols;
+        const float* vals;
+        uint64_t len(uint32_t v) const { return off[v + 1] - off[v]; }
+        template <class F>
+        bool row(uint32_t v, uint32_t n, F&& f) const {
+            for (uint64_t i = off[v]; i < off[v + 1]; ++i) {
+                if (cols[i] >= n) return false;
+                f(cols[i], vals[i]);
+            }
+            return true;
+        }
+    };
+    // ... or normalised on the fly from the graph (normalize_adjacency<float>,
+    // graph.cpp:68-98: self loop at its sorted position, float(1/sqrt(dv*du)) with
+    // dv = deg + 1 in double), so no N-sized host copy of it exists.
+    struct RawGraph {
+        const uint64_t* off;
+        const uint32_t* nbr;
+        bool loops;
+        uint64_t len(uint32_t v) const { return off[v + 1] - off[v] + (loops ? 1 : 0); }
+        template <class F>
+        bool row(uint32_t v, uint32_t n, F&& f) const {
+            const double extra = loops ? 1.0 : 0.0;
+            const double dv = double(off[v + 1] - off[v]) + extra;
+            bool pending = loops;
+            for (uint64_t i = off[v]; i < off[v + 1]; ++i) {
+                const uint32_t u = nbr[i];
+                if (u >= n || u == v) return false;
+                if (pending && u > v) {
+                    f(v, float(1.0 / std::sqrt(dv * dv)));
+                    pending = false;
+                }
+                f(u, float(1.0 / std::sqrt(dv * (double(off[u + 1] - off[u]) + extra))));
+            }
+            if (pending) f(v, float(1.0 / std::sqrt(dv * dv)));
+            return true;
+        }
+    };
+
     void upload_graph(const uint64_t* off, const uint32_t* cols, const float* vals, uint64_t nz,
                       const uint32_t* chunk_of) {
         GP_CUDA(cudaSetDevice(device));
         if (!off || !cols || !vals || !chunk_of) throw Error(GP_EINVAL, "null graph array");
         if (off[0] != 0 || off[n] != nz) throw Error(GP_EINVAL, "CSR offsets inconsistent with nnz");
+        upload_graph_src(NormCsr{off, cols, vals}, nz, chunk_of);
+    }
+    void upload_graph_raw(const uint64_t* off, const uint32_t* nbr, uint64_t m2, bool loops, const uint32_t* chunk_of) {
+        GP_CUDA(cudaSetDevice(device));
+        if (!off || !nbr || !chunk_of) throw Error(GP_EINVAL, "null graph array");
+        if (off[0] != 0 || off[n] != m2) throw Error(GP_EINVAL, "graph offsets inconsistent with the neighbour count");
+        for (uint32_t v = 0; v < n; ++v)
+            if (off[v + 1] < off[v]) throw Error(GP_EINVAL, "graph offsets not monotone");
+        upload_graph_src(RawGraph{off, nbr, loops}, m2 + (loops ? n : 0), chunk_of);
+    }
+
+    template <class Src>
+    void upload_graph_src(const Src& src, uint64_t nz, const uint32_t* chunk_of) {
         if (G > 1 && part_host.size() != n) throw Error(GP_EINVAL, "hybrid: upload the partition first");
         auto partof = [&](uint32_t v) -> uint32_t { return G > 1 ? part_host[v] : 0u; };
         auto h = std::make_shared<HostGraph>();
@@ -972,7 +1028,7 @@ struct Stage {
                 if ((b + 1) % KB == 0) continue;  // last entry of a rank's row of starts
                 const uint32_t b0 = h->bstart[b], b1 = h->bstart[b + 1];
                 std::stable_sort(inv.begin() + b0, inv.begin() + b1,
-                                 [&](uint32_t a, uint32_t c) { return off[a + 1] - off[a] > off[c + 1] - off[c]; });
+                                 [&](uint32_t a, uint32_t c) { return src.len(a) > src.len(c); });
             }
         }
         for (uint32_t r = 0; r < n; ++r) perm[inv[r]] = r;
@@ -981,8 +1037,8 @@ struct Stage {
         h->chunk.assign(n, 0);
         for (uint32_t r = 0; r < n; ++r) {
             const uint32_t v = inv[r];
-            if (off[v + 1] < off[v]) throw Error(GP_EINVAL, "CSR offsets not monotone");
-            h->rp[r + 1] = h->rp[r] + (off[v + 1] - off[v]);
+            if (std::is_same<Src, NormCsr>::value && src.len(v) > nz) throw Error(GP_EINVAL, "CSR offsets not monotone");
+            h->rp[r + 1] = h->rp[r] + src.len(v);
             h->part[r] = partof(v);
             h->chunk[r] = chunk_of[v];
         }
@@ -995,25 +1051,21 @@ struct Stage {
         stage_rows_h2d(edges, h->rp, nth, [&](uint32_t r, uint2* out) {
             const uint32_t v = inv[r];
             uint64_t w = 0;
-            for (uint64_t i = off[v]; i < off[v + 1]; ++i, ++w) {
-                const uint32_t u = cols[i];
-                if (u >= n) {
-                    bad = true;
-                    return;
-                }
+            const bool ok = src.row(v, n, [&](uint32_t u, float val) {
                 uint32_t bits;
-                std::memcpy(&bits, &vals[i], 4);
+                std::memcpy(&bits, &val, 4);
                 out[w] = make_uint2(perm[u] | (chunk_of[u] << kColBits), bits);
                 if (G > 1) h->col[h->rp[r] + w] = perm[u];
-            }
+                ++w;
+            });
+            if (!ok) bad = true;
         });
-        if (bad) throw Error(GP_EINVAL, "CSR column out of range");
+        if (bad) throw Error(GP_EINVAL, "CSR column out of range (or a self loop in the graph)");
         if (has_sage) {
             // mean / mean_t (graph.cpp:100-112, nn.hpp:85-98): the normalised rows
             // without the self loop, same renumbering and chunk bits
             std::vector<uint32_t> deg(n, 0);
-            for (uint32_t v = 0; v < n; ++v)
-                for (uint64_t i = off[v]; i < off[v + 1]; ++i) deg[v] += cols[i] != v;
+            for (uint32_t v = 0; v < n; ++v) src.row(v, n, [&](uint32_t u, float) { deg[v] += u != v; });
             std::vector<uint64_t> rpm(size_t(n) + 1, 0);
             for (uint32_t r = 0; r < n; ++r) rpm[r + 1] = rpm[r] + deg[inv[r]];
             std::vector<uint2> em(std::max<uint64_t>(rpm[n], 1)), emt(std::max<uint64_t>(rpm[n], 1));
@@ -1021,9 +1073,8 @@ struct Stage {
                 const uint32_t v = inv[r];
                 const float wv = deg[v] ? float(1.0 / double(deg[v])) : 0.f;
                 uint64_t w = rpm[r];
-                for (uint64_t i = off[v]; i < off[v + 1]; ++i) {
-                    const uint32_t u = cols[i];
-                    if (u == v) continue;
+                src.row(v, n, [&](uint32_t u, float) {
+                    if (u == v) return;
                     const float wu = deg[u] ? float(1.0 / double(deg[u])) : 0.f;
                     uint32_t bv, bu;
                     std::memcpy(&bv, &wv, 4);
@@ -1032,7 +1083,7 @@ struct Stage {
                     em[w] = make_uint2(col, bv);
                     emt[w] = make_uint2(col, bu);
                     ++w;
-                }
+                });
             }
             rowptr_m = dalloc<uint64_t>(size_t(n) + 1, false);
             edges_m = dalloc<uint2>(em.size(), false);
@@ -2715,6 +2766,13 @@ const char* gp_last_error(const gp_ctx* ctx) {
 gp_status gp_upload_graph(gp_ctx* ctx, const uint64_t* offsets, const uint32_t* cols, const float* vals,
                           uint64_t nnz, const uint32_t* chunk_of) {
     return gp::guard(&ctx->st, [&]() { ctx->st.upload_graph(offsets, cols, vals, nnz, chunk_of); });
+}
+
+gp_status gp_upload_graph_raw(gp_ctx* ctx, const uint64_t* offsets, const uint32_t* neighbors,
+                              uint64_t num_neighbors, int self_loops, const uint32_t* chunk_of) {
+    return gp::guard(&ctx->st, [&]() {
+        ctx->st.upload_graph_raw(offsets, neighbors, num_neighbors, self_loops != 0, chunk_of);
+    });
 }
 
 gp_status gp_upload_partition(gp_ctx* ctx, const uint32_t* part_of) {

@@ -142,8 +142,7 @@ TrainResult<float> run_hybrid_f32(const Dataset& ds, const Partition* part, cons
 
     std::vector<gp_layer_spec> gspecs;
     for (const auto& s : specs) gspecs.push_back(to_gp(s));
-    const auto adj = normalize_adjacency<float>(ds.graph, opt.model.self_loops);
-    timer.mark("normalize_adjacency");
+    // normalize_adjacency<float> (graph.cpp:68-98) runs inside gp_upload_graph_raw
     auto params = init_params<float>(specs, opt.seed);
     const uint32_t t0 = opt.resume ? opt.resume->epoch : 0;  // epochs already trained
     if (opt.resume) {
@@ -197,9 +196,10 @@ TrainResult<float> run_hybrid_f32(const Dataset& ds, const Partition* part, cons
         if (G > 1) check(gp_upload_partition(g, part->assignment.data()), g, "gp_upload_partition");
         const int dev0 = opt.device >= 0 ? opt.device : 0;
         if (w == 0 || c.device != dev0) {
-            check(gp_upload_graph(g, adj.offsets.data(), adj.cols.data(), adj.vals.data(), adj.cols.size(),
-                                  plan.chunk_of.data()),
-                  g, "gp_upload_graph");
+            check(gp_upload_graph_raw(g, ds.graph.csr_offsets.data(), ds.graph.csr_neighbors.data(),
+                                      ds.graph.csr_neighbors.size(), opt.model.self_loops ? 1 : 0,
+                                      plan.chunk_of.data()),
+                  g, "gp_upload_graph_raw");
         } else {
             check(gp_share_graph(g, ctx.v[0]), g, "gp_share_graph");
         }
