@@ -799,7 +799,9 @@ struct Stage {
     // staged matrix + double-buffered row tiles fit (SageConv's 2*din-wide transforms)
     int tile_tr(uint32_t rows, uint32_t win, uint32_t wout) const {
         int tr = tile_rows_per_thread(rows, wout, num_sms);
-        while (tr > 1 && tile_smem_bytes(win, wout, uint32_t(tr)) > size_t(smem_optin)) tr /= 2;
+        // two resident CTAs (one stages rows while the other computes): H = 128 at 4 rows per
+        // thread needs 139 KB and would run one CTA per SM
+        while (tr > 1 && tile_smem_bytes(win, wout, uint32_t(tr)) > size_t(smem_optin) / 2) tr /= 2;
         if (tile_smem_bytes(win, wout, uint32_t(tr)) > size_t(smem_optin))
             throw Error(GP_EINVAL, "row transform too wide for shared memory");
         return tr;
