@@ -503,7 +503,6 @@ struct Stage {
             if (sp.kind == GP_SAGECONV && l >= c.layer_begin && l < c.layer_end) {
                 if (sp.in_dim > kMaxWidth)
                     throw Error(GP_EINVAL, "SageConv input width > 128 is not supported by the GPU engine");
-                if (G > 1) throw Error(GP_EINVAL, "SageConv in hybrid groups (group_size > 1) is not supported");
                 has_sage = true;
             }
         }
@@ -2202,20 +2201,22 @@ struct Stage {
     }
 
     // Pull the halo rows of chunks [k_lo, k_hi) from every peer's buffer.
+    // dst = base + col0 (col0: SageConv's aggregated half of bg); peers' rows are read
+    // from the matching column of their own buffer
     void halo_pull(uint32_t kind, uint32_t tag, uint32_t k_lo, uint32_t k_hi, float* dst, uint32_t stride,
-                   float* dstG, uint32_t gstride, uint32_t width, const DropKey& key) {
+                   float* dstG, uint32_t gstride, uint32_t width, const DropKey& key, uint32_t col0 = 0) {
         for (uint32_t r2 = 0; r2 < G; ++r2) {
             if (r2 == grank) continue;
             const float* src = nullptr;
             if (tr.ipcg.linked) {
                 ipcg_wait(r2, kind, ++tr.ipcg.recv_seq[kind][r2]);
-                src = peer_of(r2, dst);
+                src = peer_of(r2, dst - col0) + col0;
             } else {
                 if (!tr.group) throw Error(GP_EFABRIC, "hybrid worker without a group link");
                 LocalQueue::Msg m;
                 wait_local(tr.group->at(r2, grank, kind), tag, m);
                 GP_CUDA(cudaStreamWaitEvent(cs, m.ready, 0));
-                src = m.src[0].ptr;
+                src = m.src[0].ptr + col0;
             }
             const uint32_t a = pull_off[size_t(r2) * (K + 1) + k_lo], b = pull_off[size_t(r2) * (K + 1) + k_hi];
             if (b == a) continue;
@@ -2256,7 +2257,8 @@ struct Stage {
         if (d.l == 0) return;  // global layer 0 never propagates further (no dagg kept)
         const uint32_t tag = halo_tag(d.l, k_hi - k_lo == K ? 0xff : k_lo);
         group_post(1, tag, {Piece{d.bg, 0}});
-        halo_pull(1, tag, k_lo, k_hi, d.bg, d.sin, nullptr, 0, d.din, DropKey{});
+        // SageConv: neighbours read the aggregated half of dagg (exchange_rows offset in, :838-844)
+        halo_pull(1, tag, k_lo, k_hi, d.bg + d.sgap, d.skw, nullptr, 0, d.din, DropKey{}, d.sgap);
     }
 
     // group_weight_sync: rank 0 folds in rank order and everyone takes its result.
@@ -2264,8 +2266,8 @@ struct Stage {
         std::vector<Piece> mine;
         uint64_t values = 0;
         for (auto& d : L) {
-            mine.push_back({d.gW, size_t(d.din) * d.dout});
-            values += uint64_t(d.din) * d.dout;
+            mine.push_back({d.gW, size_t(d.kin) * d.dout});
+            values += uint64_t(d.kin) * d.dout;
             if (d.gb) {
                 mine.push_back({d.gb, d.dout});
                 values += d.dout;

@@ -111,10 +111,12 @@ HYB_IPC = [
     dict(kind=0, L=4, H=16, S=2, G=2, K=4, cs=3, ps=1, epochs=5, seed=42, fix_alpha=3),
     dict(kind=2, L=5, H=16, S=1, G=3, K=3, cs=5, ps=3, epochs=4, seed=44, sync=True),
     dict(kind=0, L=6, H=12, S=2, G=2, K=6, cs=7, ps=4, epochs=4, seed=45, fix_alpha=2, hist=True),
+    dict(kind=1, L=4, H=16, S=2, G=2, K=4, cs=3, ps=1, epochs=4, seed=48, fix_alpha=3),
 ]
 
 
-@pytest.mark.parametrize("case", HYB_IPC, ids=[f"k{c['kind']}_s{c['S']}g{c['G']}" for c in HYB_IPC])
+@pytest.mark.parametrize("case", HYB_IPC, ids=[f"k{c['kind']}_s{c['S']}g{c['G']}{'_hist' if c.get('hist') else ''}"
+                                               for c in HYB_IPC])
 def test_ipc_hybrid_processes_match_in_process_hybrid(gp, tmp_path, case):
     """S x G worker processes (gp_link_group_ipc + gp_link_ipc) == train_hybrid in one
     process (gp_link_group + gp_link_local), bit for bit."""

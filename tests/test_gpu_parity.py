@@ -300,11 +300,11 @@ def test_invalid_arguments_raise(gp):
         gp.train_pipeline(ds, np.zeros(ds.num_vertices, np.uint32), 5, gp.TrainOptions(model=model))
     with pytest.raises(gp.InvalidArgument):
         gp.train_pipeline(ds, np.arange(ds.num_vertices, dtype=np.uint32) % 65, 1, gp.TrainOptions(model=model))
-    # SageConv runs on pipelines; hybrid groups (G > 1) do not support it yet
-    part, _, _ = gp.partition_vertices(ds, 2, 1)
+    # SageConv input widths above 128 are not supported by the row kernels
+    wide = gp.Dataset.synthetic_er(300, 0.03, 11, 200, 7, 2)
     with pytest.raises(gp.InvalidArgument, match="SageConv"):
-        gp.train_hybrid(ds, part, np.zeros(ds.num_vertices, np.uint32), 1,
-                        gp.TrainOptions(model=gp.ModelConfig(kind=1, layers=2, hidden=8)))
+        gp.train_pipeline(wide, np.zeros(wide.num_vertices, np.uint32), 1,
+                          gp.TrainOptions(model=gp.ModelConfig(kind=1, layers=2, hidden=8)))
 
 
 HYB = [
@@ -313,6 +313,8 @@ HYB = [
     ("train_gcnii_hyb_s2g2", 2, 6, 16, 2, 2, 4, 3, 2, 8, 43, dict(fix_alpha=3)),
     ("train_gcnii_hyb_s1g3_sync", 2, 5, 16, 1, 3, 3, 5, 3, 6, 44, dict(synchronous_mode=True)),
     ("train_gcn_hyb_s3g2_hist", 0, 6, 12, 3, 2, 6, 7, 4, 6, 45, dict(fix_alpha=2, historical_gradients=True)),
+    ("train_sage_hyb_s2g2", 1, 4, 16, 2, 2, 4, 3, 1, 8, 48, dict(fix_alpha=3)),
+    ("train_sage_hyb_s1g2_hist", 1, 3, 12, 1, 2, 4, 5, 2, 6, 49, dict(fix_alpha=2, historical_gradients=True)),
 ]
 
 
