@@ -501,8 +501,8 @@ struct Stage {
             if (sp.kind > GP_GCN2CONV) throw Error(GP_EINVAL, "unknown layer kind");
             if (sp.kind == GP_GCN2CONV) needs_h0 = true;
             if (sp.kind == GP_SAGECONV && l >= c.layer_begin && l < c.layer_end) {
-                if (sp.in_dim > kMaxWidth)
-                    throw Error(GP_EINVAL, "SageConv input width > 128 is not supported by the GPU engine");
+                if (sp.in_dim > kMaxWidth && l > 0)  // layer 0 (features) takes the wide path
+                    throw Error(GP_EINVAL, "SageConv hidden width > 128 is not supported by the GPU engine");
                 has_sage = true;
             }
         }
@@ -1450,14 +1450,21 @@ struct Stage {
                 launch(cls, bytes, flops, gather, [&]() { fwd_nb<FWD_GCN2>(rows, smem, p); });
             return;
         }
-        // wide input (layer 0 with F > 128): pre first, then the tiled transform
+        // wide input (layer 0 with F > 128): pre first, then the tiled transform. SageConv:
+        // mean aggregate into the gapped second half, the dropped own row into the first
         if (d.spec.kind == GP_GCN2CONV) throw Error(GP_EINVAL, "Gcn2Conv wider than 128");
         if (d.agg) {
-            SpmmParams sp{r0, r1, d.din, n, rowptr, edges, d.G, d.sin, d.pre, d.sin};
+            SpmmParams sp{r0, r1, d.din, n, d.sage ? rowptr_m : rowptr, d.sage ? edges_m : edges, d.G, d.sin,
+                          d.pre + d.sgap, d.skw};
             const double e = double(rowptr_nnz(r0, r1));
             launch(GP_K_FWD_AGG, e * 8.0 + double(n) * d.din * 4.0 + double(rows) * d.din * 4.0,
                    2.0 * e * d.din, e * d.sin * 4.0,
                    [&]() { k_spmm_pre<<<row_grid(rows, (const void*)k_spmm_pre, 0), kBlock, 0, cs>>>(sp); });
+            if (d.sage) {
+                RemaskParams rp{r0, r1, d.din, cur_src(i), src_stride(i), d.pre, d.skw, orig, drop_key(t, d.l, d.din)};
+                launch(GP_K_FWD_DENSE, double(rows) * d.din * 8.0, 0, 0,
+                       [&]() { k_remask<<<row_grid(rows, (const void*)k_remask, 0), kBlock, 0, cs>>>(rp); });
+            }
         } else {
             RemaskParams rp{r0, r1, d.din, cur_src(i), src_stride(i), d.pre, d.sin, orig,
                             drop_key(t, d.l, d.din)};
@@ -1468,10 +1475,10 @@ struct Stage {
         g.r0 = r0;
         g.r1 = r1;
         g.A = d.pre;
-        g.astride = d.sin;
-        g.W = d.W;
+        g.astride = d.skw;
+        g.W = d.sage ? d.Wg : d.W;
         g.bias = d.b;
-        g.din = d.din;
+        g.din = d.kw;
         g.dout = d.dout;
         g.relu = d.spec.relu;
         g.out = d.h;

@@ -34,6 +34,10 @@ SCENARIOS = {
     "forward_sage": ("forward", dict(spec=ER500, model="sage", layers=3, hidden=16, seed=7, epoch=1)),
     "train_sage_s2k4": ("train", dict(spec=ER500, model="sage", layers=4, hidden=16, S=2, K=4, chunk_seed=3,
                                       epochs=10, seed=46, fix_alpha=3)),
+    "forward_sage_wide": ("forward", dict(spec="er:300:0.03:11:200:7:2", model="sage", layers=3, hidden=16, seed=7,
+                                          epoch=1)),
+    "train_sage_wide_s2k4": ("train", dict(spec="er:300:0.03:11:200:7:2", model="sage", layers=3, hidden=16, S=2, K=4,
+                                           chunk_seed=1, epochs=6, seed=50, fix_alpha=2)),
     "train_sage_hyb_s2g2": ("train", dict(spec=ER500, model="sage", layers=4, hidden=16, S=2, G=2, K=4, chunk_seed=3,
                                           part_seed=1, epochs=8, seed=48, fix_alpha=3)),
     "train_sage_hyb_s1g2_hist": ("train", dict(spec=ER500, model="sage", layers=3, hidden=12, S=1, G=2, K=4,

@@ -182,6 +182,29 @@ def test_train_sage_pipeline_stale_two_stages(gp, env, monkeypatch):
                    fix_alpha=3)
 
 
+def test_sage_wide_features_forward_bitexact(gp):
+    """SageConv layer 0 over F = 200 features (> 128): mean aggregate + own row through the wide
+    path (k_spmm_pre, k_remask, k_dense_gemm with the gapped weights), bit-exact."""
+    ref = golden("forward_sage_wide")
+    ds = gp.Dataset.synthetic_er(300, 0.03, 11, 200, 7, 2)
+    model = gp.ModelConfig(kind=1, layers=3, hidden=16)
+    eng, specs = single_stage(gp, ds, model, seed=7)
+    st = eng.run_epoch(1, [0])
+    for l in range(3):
+        assert bits_equal(eng.download("h", l), ref[f"h{l}"]), f"h{l} not bit-exact"
+        assert bits_equal(eng.download("pre", l), ref[f"pre{l}"]), f"pre{l} not bit-exact"
+    ntrain = int((ds.arrays()[2] == 1).sum())
+    assert abs(st.loss_sum / ntrain - float(ref["loss"][0])) <= 1e-6 * abs(float(ref["loss"][0]))
+    for l in range(3):
+        gW, gb = eng.get_grads(l)
+        assert rel(gW, ref[f"gW{l}"]) < 1e-4, l
+
+
+def test_train_sage_wide_features_two_stages(gp):
+    _train_compare(gp, "train_sage_wide_s2k4", gp.Dataset.synthetic_er(300, 0.03, 11, 200, 7, 2),
+                   gp.ModelConfig(kind=1, layers=3, hidden=16), 2, 4, 1, 6, 50, fix_alpha=2)
+
+
 @pytest.mark.parametrize("env", [{"GP_SPLIT": "0"}, {"GP_WAVE": "1"}, {"GP_OCC5": "1"}, {"GP_PGRAD": "simt"}],
                          ids=["fused", "one_stream", "occ5", "simt_pgrad"])
 def test_engine_variants_match_default_bitwise(gp, env, monkeypatch):
@@ -300,11 +323,10 @@ def test_invalid_arguments_raise(gp):
         gp.train_pipeline(ds, np.zeros(ds.num_vertices, np.uint32), 5, gp.TrainOptions(model=model))
     with pytest.raises(gp.InvalidArgument):
         gp.train_pipeline(ds, np.arange(ds.num_vertices, dtype=np.uint32) % 65, 1, gp.TrainOptions(model=model))
-    # SageConv input widths above 128 are not supported by the row kernels
-    wide = gp.Dataset.synthetic_er(300, 0.03, 11, 200, 7, 2)
+    # SageConv hidden widths above 128 are not supported by the row kernels
     with pytest.raises(gp.InvalidArgument, match="SageConv"):
-        gp.train_pipeline(wide, np.zeros(wide.num_vertices, np.uint32), 1,
-                          gp.TrainOptions(model=gp.ModelConfig(kind=1, layers=2, hidden=8)))
+        gp.train_pipeline(ds, np.zeros(ds.num_vertices, np.uint32), 1,
+                          gp.TrainOptions(model=gp.ModelConfig(kind=1, layers=3, hidden=136)))
 
 
 HYB = [
