@@ -38,6 +38,13 @@ SCENARIOS = {
                                           epoch=1)),
     "train_sage_wide_s2k4": ("train", dict(spec="er:300:0.03:11:200:7:2", model="sage", layers=3, hidden=16, S=2, K=4,
                                            chunk_seed=1, epochs=6, seed=50, fix_alpha=2)),
+    # BASELINE configs[4] in miniature: hybrid pipeline x graph parallel GCNII on a power-law graph
+    # (tests/golden/powerlaw_2k, make_powerlaw.py; hubs of degree 822 next to degree-1 leaves)
+    "train_gcnii_powerlaw_hyb_s2g2": ("train", dict(spec="dir:" + os.path.join(HERE, "powerlaw_2k"), model="gcnii",
+                                                    layers=8, hidden=16, S=2, G=2, K=4, chunk_seed=3, part_seed=1,
+                                                    epochs=8, seed=51, fix_alpha=3)),
+    "train_gcn_powerlaw_s2k8": ("train", dict(spec="dir:" + os.path.join(HERE, "powerlaw_2k"), model="gcn", layers=4,
+                                              hidden=16, S=2, K=8, chunk_seed=4, epochs=8, seed=52, fix_alpha=2)),
     "train_sage_hyb_s2g2": ("train", dict(spec=ER500, model="sage", layers=4, hidden=16, S=2, G=2, K=4, chunk_seed=3,
                                           part_seed=1, epochs=8, seed=48, fix_alpha=3)),
     "train_sage_hyb_s1g2_hist": ("train", dict(spec=ER500, model="sage", layers=3, hidden=12, S=1, G=2, K=4,

@@ -363,3 +363,31 @@ def test_train_hybrid_matches_reference(gp, case):
         worst = max(worst, float(d.max()))
         med.append(float(np.median(d)))
     assert worst < 2e-3 and max(med) < 1e-4, (worst, med)
+
+
+def _powerlaw(gp):
+    return gp.Dataset.load(os.path.join(GOLD, "powerlaw_2k"))
+
+
+def test_train_gcn_pipeline_powerlaw_graph(gp):
+    """Skewed degrees (Chung-Lu, max degree 822, median 5; tests/golden/make_powerlaw.py): long and
+    short rows in one chunk, the degree-ordered rows and dynamic row scheduling."""
+    _train_compare(gp, "train_gcn_powerlaw_s2k8", _powerlaw(gp), gp.ModelConfig(kind=0, layers=4, hidden=16), 2, 8,
+                   4, 8, 52, fix_alpha=2)
+
+
+def test_train_hybrid_powerlaw_graph(gp):
+    """BASELINE configs[4] in miniature: 2 stages x 2 graph partitions, GCNII, power-law graph."""
+    ref = golden("train_gcnii_powerlaw_hyb_s2g2")
+    ds = _powerlaw(gp)
+    part, _, _ = gp.partition_vertices(ds, 2, 1)
+    co = gp.make_chunks(ds, 4, 3)
+    assert np.array_equal(co, ref["chunk_of"])
+    opt = gp.TrainOptions(model=gp.ModelConfig(kind=2, layers=8, hidden=16), epochs=8, seed=51, fix_alpha=3)
+    res = gp.train_hybrid(ds, part, co, 2, opt)
+    met = ref["metrics"].reshape(8, 5)
+    assert np.max(np.abs(res.train_loss - met[:, 1]) / np.abs(met[:, 1])) < 1e-4, (res.train_loss, met[:, 1])
+    assert np.array_equal(res.comm.astype(np.uint64), ref["comm"].reshape(8, 3))
+    worst = max(float((np.abs(W.astype(np.float64) - ref[f"W{l}"]) / np.maximum(np.abs(ref[f"W{l}"]), 1e-3)).max())
+                for l, (W, _) in enumerate(res.params))
+    assert worst < 2e-3, worst

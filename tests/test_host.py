@@ -136,3 +136,14 @@ def test_invalid_arguments(gp, ds):
         gp.make_stage_assignment(4, 5)
     with pytest.raises(gp.InvalidArgument):
         gp.build_layer_specs(gp.ModelConfig(kind=gp.ModelKind.GCNII, layers=2), 4, 2)
+
+
+def test_powerlaw_dataset_chunk_plan_matches_reference():
+    """make_chunks on the committed power-law fixture (load_dataset of a save_dataset directory)
+    equals the reference's plan stored with its training goldens."""
+    import paper_2308_10087_b200 as gp
+    here = os.path.dirname(os.path.abspath(__file__))
+    ds = gp.Dataset.load(os.path.join(here, "golden", "powerlaw_2k"))
+    for name, K, seed in (("train_gcnii_powerlaw_hyb_s2g2", 4, 3), ("train_gcn_powerlaw_s2k8", 8, 4)):
+        ref = np.load(os.path.join(here, "golden", name + ".npz"))
+        assert np.array_equal(gp.make_chunks(ds, K, seed), ref["chunk_of"]), name
