@@ -63,3 +63,32 @@ def test_trace_structure_and_bubble(gp, tmp_path, model_kind, S, K):
     assert open(tmp_path / "metrics.csv").read().count("\n") == T + 1
     pipe = res.ledger[:, 0:2, :].sum()
     assert pipe == res.comm[:, 1].sum()
+
+
+@pytest.mark.parametrize("mode", ["sync", "hybrid"])
+def test_trace_sync_and_hybrid(gp, mode):
+    """Synchronous mode traces one whole-partition compute span per direction (chunk -1,
+    engines_impl.hpp:811, :867); hybrid workers trace like stages (G workers per stage)."""
+    ds = gp.Dataset.synthetic_er(*ER500)
+    model = gp.ModelConfig(kind=gp.ModelKind.GCNII, layers=5, hidden=16)
+    co = gp.make_chunks(ds, 4, 3)
+    T = 2
+    if mode == "sync":
+        res = gp.train_pipeline(ds, co, 2, gp.TrainOptions(model=model, epochs=T, seed=3, synchronous_mode=True,
+                                                           collect_trace=True))
+        W = 2
+    else:
+        part, _, _ = gp.partition_vertices(ds, 2, 1)
+        res = gp.train_hybrid(ds, part, co, 2, gp.TrainOptions(model=model, epochs=T, seed=3, fix_alpha=2,
+                                                                collect_trace=True))
+        W = 4
+    tr = res.trace
+    assert sorted(set(tr["worker"].tolist())) == list(range(W))
+    for w in range(W):
+        comp = tr[(tr["worker"] == w) & (tr["kind"] == 0)]
+        per_epoch = 3 if mode == "sync" else 2 * 4 + 1  # fwd, bwd, param step | per chunk + step
+        assert len(comp) == T * per_epoch, (w, len(comp))
+        c = np.sort(comp, order="t_start")
+        assert np.all(c["t_start"][1:] >= c["t_end"][:-1] - 1e-9)
+    b = gp.bubble_analysis(tr)
+    assert 0.0 <= b["measured_bubble"] < 1.0
