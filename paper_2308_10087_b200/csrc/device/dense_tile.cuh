@@ -171,7 +171,7 @@ __device__ __forceinline__ void tile_mac_fixed(float (&acc)[TR][8], const float*
     constexpr uint32_t kAms = kKp + 4, kMs = ws_col(kNcg - 1) + 8, kRa = kNrg * kAms;
     const float* a = As + size_t(rg) * kAms;
     const float* w = Ws + ws_col(cg);
-#pragma unroll 1
+#pragma unroll 1  // unrolling 2 or 5 k-groups measured within 2 %
     for (uint32_t i = 0; i < kKp; i += 4, a += 4, w += 4 * kMs) {
         float4 x[TR];
 #pragma unroll

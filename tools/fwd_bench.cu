@@ -366,6 +366,12 @@ int main(int argc, char** argv) {
         run("split dense k_fwd_dense8<1>", (const void*)k_fwd_dense8<true>, dsm, K);
         run("split dense k_fwd_tile<1,4>", (const void*)k_fwd_tile<true, 4>, tile_smem_bytes(H, H, 4), K);
         run("split dense k_fwd_tile<1,4,100>", (const void*)k_fwd_tile<true, 4, 100>, tile_smem_bytes(H, H, 4), K);
+        {  // cost of the next-layer dropout epilogue: same transform without gnext
+            float* keep = p.gnext;
+            p.gnext = nullptr;
+            run("  ... without next-layer dropout", (const void*)k_fwd_tile<true, 4, 100>, tile_smem_bytes(H, H, 4), K);
+            p.gnext = keep;
+        }
         run("split dense k_fwd_tile<1,2>", (const void*)k_fwd_tile<true, 2>, tile_smem_bytes(H, H, 2), K);
         run("split dense k_fwd_tile<1,1>", (const void*)k_fwd_tile<true, 1>, tile_smem_bytes(H, H, 1), K);
         run("k_fwd8 again", (const void*)k_fwd8<FWD_GCN2, 2>, wsm, K);
