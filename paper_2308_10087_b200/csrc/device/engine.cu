@@ -650,7 +650,7 @@ struct Stage {
     // gathers bypass L1 (no_allocate), so the unified carveout goes to shared memory.
     template <int NB>
     void setup_nb() {
-        const int smem_max = int(row_smem_bytes(kMaxWidth, kMaxWidth, kDenseRows));
+        const int smem_max = int(row_smem_bytes(kMaxWidth, kMaxWidth, 2));
         const void* fns[] = {(const void*)k_fwd8<FWD_DENSE, NB>,
                              (const void*)k_fwd8<FWD_GCN, NB>,
                              (const void*)k_fwd8<FWD_GCN2, NB>,
@@ -682,10 +682,7 @@ struct Stage {
                              (const void*)k_bwd8<PREV_AGG_HIST, OUT_LAYER, NB, true>,
                              (const void*)k_bwd8<PREV_AGG, OUT_DHIN, NB>,
                              (const void*)k_bwd8<PREV_AGG_HIST, OUT_DHIN, NB>,
-                             (const void*)k_bwd8<PREV_OWN, OUT_DHIN, NB>,
-                             (const void*)k_fwd_dense8<false>,
-                             (const void*)k_fwd_dense8<true>,
-                             (const void*)k_bwd_dense8};
+                             (const void*)k_bwd8<PREV_OWN, OUT_DHIN, NB>};
         for (const void* f : fns) {
             GP_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
             GP_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,

@@ -321,7 +321,7 @@ __device__ __forceinline__ void bwd_epilogue(const BwdParams& p, float (&g)[R][4
 // b + pre.W (the reference's exact-zero skip is an identity here: pre is never
 // -0 and x*W = +-0 leaves a non -0 accumulator unchanged) -> identity mix ->
 // ReLU -> h, and the next layer's dropped gather source. SPLIT: stop at pre
-// (k_fwd_dense8 does the transform).
+// (k_fwd_tile in dense_tile.cuh does the transform).
 // ---------------------------------------------------------------------------
 // Resident CTAs per SM the split (gather-only) kernels are compiled for: no
 // staged matrix, so registers alone bound their occupancy.
@@ -385,7 +385,7 @@ __global__ void __launch_bounds__(kBlock, MINB ? MINB : (SPLIT && NB == 2 ? GP_S
             }
         }
         if (has && in_act) st8_stream(p.pre + size_t(v) * p.prestride + 8 * hl, pre);
-        if (SPLIT) continue;  // transform + epilogue in k_fwd_dense8
+        if (SPLIT) continue;  // transform + epilogue in k_fwd_tile (dense_tile.cuh)
 
         stage_x2(xs, pre, hl, hb, in_act);
         float o[2][4];
@@ -398,50 +398,11 @@ __global__ void __launch_bounds__(kBlock, MINB ? MINB : (SPLIT && NB == 2 ? GP_S
 }
 
 // ---------------------------------------------------------------------------
-// Row transform + epilogue of a split forward (k_fwd8<KIND, NB, true> wrote pre),
-// 8 rows per warp: the gather kernel stays a pure latency-bound stream and this
-// one is a short FMA-issue-bound pass (pre is read back from L2).
-// ---------------------------------------------------------------------------
-constexpr int kDenseRows = 8;
-
-template <bool GCN2>
-__global__ void __launch_bounds__(kBlock, 3) k_fwd_dense8(FwdParams p) {
-    extern __shared__ float4 smem4[];
-    const uint32_t ms = mat_stride(p.dout);
-    float* Ms = reinterpret_cast<float*>(reinterpret_cast<char*>(smem4) + kEdgeSlotBytes);
-    float* bs = Ms + size_t(p.din) * ms + 32;
-    float* xs = bs + 128 + (threadIdx.x / 32) * 128 * kDenseRows;
-    stage_mat(Ms, p.W, p.din, p.dout, false, p.dout);
-    for (uint32_t c = threadIdx.x; c < 128; c += blockDim.x) bs[c] = (p.bias && c < p.dout) ? p.bias[c] : 0.f;
-    __syncthreads();
-    const uint64_t pol = evict_first_policy();
-    const int lane = threadIdx.x & 31;
-    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
-    for (uint32_t v0 = p.r0 + kDenseRows * ((blockIdx.x * blockDim.x + threadIdx.x) >> 5); v0 < p.r1;
-         v0 += kDenseRows * nw) {
-        // stage 8 pre rows as xs[i][8]
-        for (uint32_t idx = lane; idx < kDenseRows * p.din; idx += 32) {
-            const uint32_t r = idx / p.din, i = idx % p.din;
-            xs[i * kDenseRows + r] = v0 + r < p.r1 ? ld1_stream(p.pre + size_t(v0 + r) * p.prestride + i, pol) : 0.f;
-        }
-        __syncwarp();
-        float o[kDenseRows][4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-#pragma unroll
-            for (int r = 0; r < kDenseRows; ++r) o[r][k] = bs[(lane + 32 * k) & 127];
-        gemv_w<kDenseRows>(o, xs, Ms, p.din, ms, lane);
-        fwd_epilogue<kDenseRows, GCN2>(p, o, xs, v0, lane, pol);
-        __syncwarp();
-    }
-}
-
-// ---------------------------------------------------------------------------
 // Fused backward step (see k_bwd in kernels.cuh for the semantics): incoming
 // gradient of layer i (dtop | drop_{i+1}(A_hat . bg_{i+1}) over done chunks |
 // drop_{i+1}(bg_{i+1}[u])) (+ dh0 at global layer 0), then backward_out_row of
 // layer i (nn.hpp:202-218): dz, dagg = dz.W^T, GCNII mixes, dh0 += a*dagg, and
-// bg_i = (1-a)*dagg (Gcn2Conv) or dagg. SPLIT: stop at dz (k_bwd_dense8).
+// bg_i = (1-a)*dagg (Gcn2Conv) or dagg. SPLIT: stop at dz (k_bwd_tile does the rest).
 // ---------------------------------------------------------------------------
 template <int PREV, int OUT, int NB, bool SPLIT = false, int MINB = 0>
 __global__ void __launch_bounds__(kBlock, MINB ? MINB : (SPLIT && NB == 2 ? GP_SPLIT_MINB : (NB == 2 ? 4 : (NB == 4 ? 3 : 2))))
@@ -504,43 +465,13 @@ __global__ void __launch_bounds__(kBlock, MINB ? MINB : (SPLIT && NB == 2 ? GP_S
             for (int c = 0; c < 8; ++c) dz.v[c] = h.v[c] > 0.f ? dh.v[c] : 0.f;
         }
         if (has && dh_act) st8_stream(p.dz + size_t(u) * p.dzstride + 8 * hl, dz);
-        if (SPLIT || !p.need_dagg) continue;  // dz.W^T in k_bwd_dense8
+        if (SPLIT || !p.need_dagg) continue;  // dz.W^T in k_bwd_tile (dense_tile.cuh)
         stage_x2(xs, dz, hl, hb, dh_act);
         float g[2][4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) g[0][k] = g[1][k] = 0.f;
         gemv_w<2>(g, xs, Ms, p.dout, ms, lane);
         bwd_epilogue<2>(p, g, xs, base, lane, pol);
-        __syncwarp();
-    }
-}
-
-// Transform half of a split backward step (k_bwd8<PREV, OUT_LAYER, NB, true>
-// wrote dz), 8 rows per warp.
-__global__ void __launch_bounds__(kBlock, 3) k_bwd_dense8(BwdParams p) {
-    extern __shared__ float4 smem4[];
-    const uint32_t ms = mat_stride(p.din);
-    float* Ms = reinterpret_cast<float*>(reinterpret_cast<char*>(smem4) + kEdgeSlotBytes);
-    float* xs = Ms + size_t(p.dout) * ms + 32 + 128 + (threadIdx.x / 32) * 128 * kDenseRows;
-    stage_mat(Ms, p.W, p.dout, p.din, true, p.dout);  // Ms[j][c] = W[c][j]
-    __syncthreads();
-    const uint64_t pol = evict_first_policy();
-    const int lane = threadIdx.x & 31;
-    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
-    for (uint32_t u0 = p.r0 + kDenseRows * ((blockIdx.x * blockDim.x + threadIdx.x) >> 5); u0 < p.r1;
-         u0 += kDenseRows * nw) {
-        for (uint32_t idx = lane; idx < kDenseRows * p.dout; idx += 32) {
-            const uint32_t r = idx / p.dout, j = idx % p.dout;
-            xs[j * kDenseRows + r] = u0 + r < p.r1 ? ld1_stream(p.dz + size_t(u0 + r) * p.dzstride + j, pol) : 0.f;
-        }
-        __syncwarp();
-        float g[kDenseRows][4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-#pragma unroll
-            for (int r = 0; r < kDenseRows; ++r) g[r][k] = 0.f;
-        gemv_w<kDenseRows>(g, xs, Ms, p.dout, ms, lane);
-        bwd_epilogue<kDenseRows>(p, g, xs, u0, lane, pol);
         __syncwarp();
     }
 }

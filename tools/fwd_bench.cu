@@ -181,7 +181,7 @@ int main(int argc, char** argv) {
     cudaEvent_t a, b;
     CK(cudaEventCreate(&a));
     CK(cudaEventCreate(&b));
-    const size_t wsm = row_smem_bytes(H, H, 2), dsm = row_smem_bytes(H, H, kDenseRows);
+    const size_t wsm = row_smem_bytes(H, H, 2);
     auto run = [&](const char* name, const void* fn, size_t smem, int K) {
         CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         CK(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
@@ -309,7 +309,6 @@ int main(int argc, char** argv) {
             runb("k_bwd8<AGG,LAYER,4>", (const void*)k_bwd8<PREV_AGG, OUT_LAYER, 4>, done);
             runb("split k_bwd8<AGG,LAYER,2,1>", (const void*)k_bwd8<PREV_AGG, OUT_LAYER, 2, true>, done);
             runb("split k_bwd8<AGG,LAYER,4,1>", (const void*)k_bwd8<PREV_AGG, OUT_LAYER, 4, true>, done);
-            runb("split k_bwd_dense8", (const void*)k_bwd_dense8, done, dsm);
             runb("split k_bwd_tile<4>", (const void*)k_bwd_tile<4>, done, tile_smem_bytes(H, H, 4));
             runb("split k_bwd_tile<4,100>", (const void*)k_bwd_tile<4, 100>, done, tile_smem_bytes(H, H, 4));
         }
@@ -363,7 +362,6 @@ int main(int argc, char** argv) {
         run("k_fwd8<GCN2,4> (engine)", (const void*)k_fwd8<FWD_GCN2, 4>, wsm, K);
         run("split gather k_fwd8<GCN2,2,1>", (const void*)k_fwd8<FWD_GCN2, 2, true>, kEdgeSlotBytes, K);
         run("split gather k_fwd8<GCN2,4,1>", (const void*)k_fwd8<FWD_GCN2, 4, true>, kEdgeSlotBytes, K);
-        run("split dense k_fwd_dense8<1>", (const void*)k_fwd_dense8<true>, dsm, K);
         run("split dense k_fwd_tile<1,4>", (const void*)k_fwd_tile<true, 4>, tile_smem_bytes(H, H, 4), K);
         run("split dense k_fwd_tile<1,4,100>", (const void*)k_fwd_tile<true, 4, 100>, tile_smem_bytes(H, H, 4), K);
         {  // cost of the next-layer dropout epilogue: same transform without gnext
@@ -399,15 +397,9 @@ int main(int argc, char** argv) {
     }
     {
         full((const void*)k_fwd8<FWD_GCN2, 2, true>, kEdgeSlotBytes);
-        full((const void*)k_fwd_dense8<true>, dsm);
-        snap(got);
-        size_t bad = 0;
-        for (size_t i = 0; i < tab; ++i) bad += (reinterpret_cast<uint32_t&>(ref[i]) != reinterpret_cast<uint32_t&>(got[i]));
-        printf("split (gather + dense) vs fused: %zu differing floats\n", bad);
-        full((const void*)k_fwd8<FWD_GCN2, 2, true>, kEdgeSlotBytes);
         full((const void*)k_fwd_tile<true, 4, 100>, tile_smem_bytes(H, H, 4));
         snap(got);
-        bad = 0;
+        size_t bad = 0;
         for (size_t i = 0; i < tab; ++i) bad += (reinterpret_cast<uint32_t&>(ref[i]) != reinterpret_cast<uint32_t&>(got[i]));
         printf("split (gather + tile) vs fused: %zu differing floats\n", bad);
     }
