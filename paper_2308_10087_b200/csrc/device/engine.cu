@@ -741,6 +741,10 @@ struct Stage {
         if (const char* e = std::getenv("GP_SPLIT")) split_rows = std::string(e) != "0";
         if (const char* e = std::getenv("GP_IPC_SMCOPY")) ipc_smcopy = std::string(e) == "1";
         if (const char* e = std::getenv("GP_OCC5")) occ5_mode = std::atoi(e) ? 1 : 0;
+        if (const char* e = std::getenv("GP_TILE_TR")) {
+            const int v = std::atoi(e);
+            if (v == 1 || v == 2 || v == 4) tile_tr_env = v;
+        }
         setup_nb<2>();
         setup_nb<4>();
     }
@@ -793,8 +797,9 @@ struct Stage {
     int smem_optin = 227 * 1024;
     // rows per thread for a tile launch: by launch size, then down until the
     // staged matrix + double-buffered row tiles fit (SageConv's 2*din-wide transforms)
+    int tile_tr_env = 0;  // GP_TILE_TR=1/2/4 forces rows per thread (experiments)
     int tile_tr(uint32_t rows, uint32_t win, uint32_t wout) const {
-        int tr = tile_rows_per_thread(rows, wout, num_sms);
+        int tr = tile_tr_env ? tile_tr_env : tile_rows_per_thread(rows, wout, num_sms);
         // two resident CTAs (one stages rows while the other computes): H = 128 at 4 rows per
         // thread needs 139 KB and would run one CTA per SM
         while (tr > 1 && tile_smem_bytes(win, wout, uint32_t(tr)) > size_t(smem_optin) / 2) tr /= 2;
