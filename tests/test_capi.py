@@ -76,3 +76,13 @@ def test_libraries_do_not_interpose_torch():
     r = subprocess.run([sys.executable, "-c", code], cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                        capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
+
+
+def test_sass_contains_tcgen05_and_async_copies():
+    """The parameter-gradient GEMM issues tcgen05 MMAs (UTC*MMA) reading TMEM back (LDTM); the tiled
+    transforms stage rows with cp.async (LDGSTS)."""
+    dev = os.path.join(ROOT, "paper_2308_10087_b200", "lib", "libgpcuda.so")
+    sass = subprocess.run(["cuobjdump", "-sass", dev], capture_output=True, text=True).stdout
+    assert "UTCHMMA" in sass or "UTCMMA" in sass
+    assert "LDTM" in sass
+    assert "LDGSTS" in sass
