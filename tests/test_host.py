@@ -147,3 +147,29 @@ def test_powerlaw_dataset_chunk_plan_matches_reference():
     for name, K, seed in (("train_gcnii_powerlaw_hyb_s2g2", 4, 3), ("train_gcn_powerlaw_s2k8", 8, 4)):
         ref = np.load(os.path.join(here, "golden", name + ".npz"))
         assert np.array_equal(gp.make_chunks(ds, K, seed), ref["chunk_of"]), name
+
+
+def test_dataset_binary_csr_cache_round_trip(tmp_path):
+    """save_dataset writes graph.csr next to graph.txt (f2: binary CSR cache); load_dataset uses it
+    only while graph.txt is unchanged, and both paths give the same graph."""
+    import paper_2308_10087_b200 as gp
+    ds = gp.Dataset.synthetic_er(3000, 0.004, 9, 8, 3, 2)
+    d = tmp_path / "ds"
+    ds.save(str(d))
+    assert (d / "graph.csr").exists() and (d / "graph.txt").exists()
+    a = gp.Dataset.load(str(d))
+    for x, y in zip(a.graph(), ds.graph()):
+        assert np.array_equal(x, y)
+    # a stale cache is ignored: rewrite graph.txt with one edge removed
+    lines = (d / "graph.txt").read_text().splitlines()
+    n, m = (int(t) for t in lines[0].split())
+    (d / "graph.txt").write_text(f"{n} {m - 1}\n" + "\n".join(lines[2:]) + "\n")
+    meta = (d / "meta.json").read_text().replace(f'"num_edges": {m}', f'"num_edges": {m - 1}')
+    (d / "meta.json").write_text(meta)
+    b = gp.Dataset.load(str(d))
+    assert b.num_edges == m - 1
+    # the reference reads the same directory (graph.csr is an extra file it ignores)
+    (d / "graph.csr").unlink()
+    c = gp.Dataset.load(str(d))
+    for x, y in zip(b.graph(), c.graph()):
+        assert np.array_equal(x, y)
