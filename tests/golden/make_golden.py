@@ -38,6 +38,11 @@ SCENARIOS = {
                                           epoch=1)),
     "train_sage_wide_s2k4": ("train", dict(spec="er:300:0.03:11:200:7:2", model="sage", layers=3, hidden=16, S=2, K=4,
                                            chunk_seed=1, epochs=6, seed=50, fix_alpha=2)),
+    # BASELINE configs[1] in miniature, 20-epoch loss curve: arxiv-like density (avg degree ~14),
+    # 16-layer GCN, 2 stages, 8 chunks, default staleness (fix_alpha 10)
+    "train_gcn16_arxivlike_s2k8_20ep": ("train", dict(spec="er:20000:0.0007:21:128:40:5", model="gcn", layers=16,
+                                                      hidden=64, S=2, K=8, chunk_seed=6, epochs=20, seed=61,
+                                                      fix_alpha=10)),
     # BASELINE configs[4] in miniature: hybrid pipeline x graph parallel GCNII on a power-law graph
     # (tests/golden/powerlaw_2k, make_powerlaw.py; hubs of degree 822 next to degree-1 leaves)
     "train_gcnii_powerlaw_hyb_s2g2": ("train", dict(spec="dir:" + os.path.join(HERE, "powerlaw_2k"), model="gcnii",

@@ -137,7 +137,8 @@ def test_params_after_one_adam_step(gp):
         assert np.max(np.abs(W - want)) < 2e-6, f"W{l}"
 
 
-def _train_compare(gp, gname, ds, model, S, K, chunk_seed, epochs, seed, loss_tol=1e-4, **stal):
+def _train_compare(gp, gname, ds, model, S, K, chunk_seed, epochs, seed, loss_tol=1e-4, acc_tol=None,
+                   param_abs_tol=None, **stal):
     ref = golden(gname)
     chunk_of = np.zeros(ds.num_vertices, np.uint32) if K == 1 else gp.make_chunks(ds, K, chunk_seed)
     if K > 1 and ref["chunk_of"].size:
@@ -149,16 +150,20 @@ def _train_compare(gp, gname, ds, model, S, K, chunk_seed, epochs, seed, loss_to
     assert np.max(np.abs(res.train_loss - met[:, 1]) / np.abs(met[:, 1])) < loss_tol, (res.train_loss, met[:, 1])
     # accuracies: allow a couple of argmax flips on near-ties
     n = ds.num_vertices
-    assert np.max(np.abs(res.metrics[:, 2:5] - met[:, 2:5])) <= 3.0 / (0.2 * n)
+    assert np.max(np.abs(res.metrics[:, 2:5] - met[:, 2:5])) <= (acc_tol if acc_tol else 3.0 / (0.2 * n))
     comm = ref["comm"].reshape(epochs, 3)
     assert np.array_equal(res.comm.astype(np.uint64), comm), "ledger bytes differ"
-    worst, med = 0.0, []
+    worst, med, absmax = 0.0, [], 0.0
     for l, (W, b) in enumerate(res.params):
         rW = ref[f"W{l}"]
+        absmax = max(absmax, float(np.abs(W.astype(np.float64) - rW).max()))
         d = np.abs(W.astype(np.float64) - rW) / np.maximum(np.abs(rW), 1e-3)
         worst = max(worst, float(d.max()))
         med.append(float(np.median(d)))
-    assert worst < 2e-3 and max(med) < 1e-4, (worst, med)
+    if param_abs_tol is None:
+        assert worst < 2e-3 and max(med) < 1e-4, (worst, med)
+    else:  # long / deep runs: bounded in units of Adam steps (see the caller)
+        assert absmax <= param_abs_tol and max(med) < 1e-3, (absmax, med)
     return res
 
 
@@ -391,3 +396,20 @@ def test_train_hybrid_powerlaw_graph(gp):
     worst = max(float((np.abs(W.astype(np.float64) - ref[f"W{l}"]) / np.maximum(np.abs(ref[f"W{l}"]), 1e-3)).max())
                 for l, (W, _) in enumerate(res.params))
     assert worst < 2e-3, worst
+
+
+def test_train_gcn16_arxivlike_20_epoch_curve(gp):
+    """BASELINE configs[1] in miniature over 20 epochs (the north star's loss-curve horizon): 20 K
+    vertices at arxiv-like density, 16-layer GCN, 2 stages x 8 chunks, default staleness. Loss within
+    rel 1e-5 every epoch, parameters within the usual bars, ledger exact. The 16-layer GCN's logits stay
+    near-uniform for 20 epochs (loss ~ ln 40), so argmax ties flip on rounding: accuracies within 0.2 %.
+    Adam moves a weight by ~lr per step whatever the gradient's size, so gradient elements whose sign
+    sits at fp32 rounding level (vanishing gradients of the upper layers) can take a few opposite
+    steps: weights within 5 lr (5e-3) absolute, median relative 1e-3 (measured: 3.8e-3, <= 3.8e-4;
+    lower layers ~1e-5, tools/param_diff_probe.py). The engine against itself with only the
+    parameter-gradient summation order changed (GP_PGRAD=simt) differs by the same amounts (2.9e-3 at
+    layer 14), so this is fp32 amplification, not a semantic difference."""
+    ds = gp.Dataset.synthetic_er(20000, 0.0007, 21, 128, 40, 5)
+    res = _train_compare(gp, "train_gcn16_arxivlike_s2k8_20ep", ds, gp.ModelConfig(kind=0, layers=16, hidden=64),
+                         2, 8, 6, 20, 61, loss_tol=1e-5, acc_tol=2e-3, param_abs_tol=5e-3, fix_alpha=10)
+    assert res.metrics.shape[0] == 20
