@@ -95,3 +95,16 @@ def test_reddit_shape_epoch1_rows_bit_exact(gp):
     want = float(oma) * agg + float(a) * h0_gpu.astype(np.float64).sum(1)
     got = pre1_gpu.astype(np.float64).sum(1)
     assert np.max(np.abs(got - want)) <= 1e-5 * np.max(np.abs(want))
+
+
+def test_reddit_shape_64_layer_runs_are_deterministic(gp):
+    """The headline configuration (64-layer GCNII, K = 4, 4-stream wavefront, 5-CTA gathers, tcgen05
+    parameter gradients) trained twice for 3 epochs gives bit-identical losses and parameters."""
+    ds = gp.Dataset.synthetic_er(N, E2 / (N * (N - 1)), 1, F, C, 1)
+    model = gp.ModelConfig(kind=gp.ModelKind.GCNII, layers=64, hidden=H, dropout=0.5)
+    co = gp.make_chunks(ds, 4, 1)
+    runs = [gp.train_pipeline(ds, co, 1, gp.TrainOptions(model=model, epochs=3, seed=1)) for _ in range(2)]
+    assert np.array_equal(runs[0].train_loss, runs[1].train_loss)
+    assert np.all(np.isfinite(runs[0].train_loss))
+    for (Wa, ba), (Wb, bb) in zip(runs[0].params, runs[1].params):
+        assert np.array_equal(Wa.view(np.uint32), Wb.view(np.uint32))
