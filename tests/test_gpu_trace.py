@@ -92,3 +92,25 @@ def test_trace_sync_and_hybrid(gp, mode):
         assert np.all(c["t_start"][1:] >= c["t_end"][:-1] - 1e-9)
     b = gp.bubble_analysis(tr)
     assert 0.0 <= b["measured_bubble"] < 1.0
+
+
+def test_train_tool_writes_reference_run_outputs(gp, tmp_path):
+    """tools/gnnpipe_train.py: the reference CLI's run outputs from the engine, then a resumed run."""
+    import importlib.util
+    import os
+    spec = importlib.util.spec_from_file_location(
+        "gnnpipe_train", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools",
+                                      "gnnpipe_train.py"))
+    tool = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(tool)
+    out = tmp_path / "run"
+    args = ["--synthetic", "er:500:0.02:3:16:5:9", "--model", "gcnii", "--layers", "5", "--hidden", "16",
+            "--stages", "2", "--epochs", "3", "--trace", "--out", str(out)]
+    tool.main(args)
+    for name in ("metrics.csv", "trace.jsonl", "comm_report.csv", "stage_0.ckpt", "stage_1.ckpt", "state.ckpt"):
+        assert (out / name).exists(), name
+    assert open(out / "metrics.csv").read().count("\n") == 4
+    names = [n for n, _ in gp.load_checkpoint(str(out / "stage_1.ckpt"))]
+    assert names[0].startswith("layer") and names[0].endswith(".weight")
+    tool.main(args[:-2] + ["--resume", str(out / "state.ckpt"), "--out", str(tmp_path / "run2")])
+    assert open(tmp_path / "run2" / "metrics.csv").read().splitlines()[1].startswith("4,")
