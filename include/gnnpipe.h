@@ -227,7 +227,9 @@ gp_status gp_set_profiling(gp_ctx* ctx, int enable);
 /* Trace of a stage's epochs (replaces the simulated-clock trace of the fabric,
  * TraceEvent fabric.hpp, Fabric::trace fabric.cpp:256-264; collect_trace
  * fabric.cpp:222-227). Kinds follow TraceEvent::Kind. Times are the device's
- * %globaltimer in nanoseconds (one timebase for all stages of a node); a
+ * %globaltimer in nanoseconds (one timebase for all stages of a node, anchored
+ * once per epoch per stage by a one-thread stamp kernel: cross-stage times agree
+ * to a few microseconds); a
  * compute span covers one chunk's layers [layer_lo, layer_hi] of the stage
  * (chunk -1: the whole partition in synchronous mode, or the epoch-close
  * parameter step). Tracing runs chunks serially (no wavefront). */

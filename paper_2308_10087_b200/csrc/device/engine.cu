@@ -673,6 +673,10 @@ struct Stage {
                              (const void*)k_bwd8<PREV_SAGE, OUT_LAYER, NB, true>,
                              (const void*)k_bwd8<PREV_SAGE_HIST, OUT_LAYER, NB, true>,
                              (const void*)k_bwd8<PREV_SAGE, OUT_DHIN, NB>,
+                             (const void*)k_bwd8<PREV_AGG_ALL, OUT_LAYER, NB>,
+                             (const void*)k_bwd8<PREV_AGG_ALL, OUT_LAYER, NB, true>,
+                             (const void*)k_bwd8<PREV_AGG_ALL, OUT_LAYER, NB, true, 5>,
+                             (const void*)k_bwd8<PREV_AGG_ALL, OUT_DHIN, NB>,
                              (const void*)k_bwd8<PREV_SAGE_HIST, OUT_DHIN, NB>,
                              (const void*)k_bwd8<PREV_TOP, OUT_LAYER, NB>,
                              (const void*)k_bwd8<PREV_AGG, OUT_LAYER, NB>,
@@ -1537,7 +1541,7 @@ struct Stage {
                 p.sgap = nx.sgap;
                 e = double(rowptr_nnz(r0, r1));
             } else if (nx.agg) {
-                prev = hist ? PREV_AGG_HIST : PREV_AGG;
+                prev = hist ? PREV_AGG_HIST : (done == all_chunks() ? PREV_AGG_ALL : PREV_AGG);
                 e = double(rowptr_nnz(r0, r1));
             } else {
                 prev = PREV_OWN;
@@ -1570,7 +1574,8 @@ struct Stage {
                              (p.gcn2 ? double(rows) * d.din * 8.0 : 0.0);
         const double flops = 2.0 * e * d.dout + (p.need_dagg ? 2.0 * double(rows) * d.din * d.dout : 0.0);
         const double gather = e * double(pad8(d.dout)) * 4.0;
-        const int cls = prev == PREV_AGG || prev == PREV_AGG_HIST || prev == PREV_SAGE || prev == PREV_SAGE_HIST
+        const int cls = prev == PREV_AGG || prev == PREV_AGG_ALL || prev == PREV_AGG_HIST || prev == PREV_SAGE ||
+                                prev == PREV_SAGE_HIST
                             ? GP_K_BWD_AGG
                             : GP_K_BWD_DENSE;
         // SageConv layers (2*din-wide dagg) and SageConv neighbours always run split
@@ -1581,6 +1586,7 @@ struct Stage {
                 switch (prev) {
                     case PREV_TOP: bwd_nb<PREV_TOP, OUT_LAYER, true>(rows, kEdgeSlotBytes, p); break;
                     case PREV_AGG: bwd_nb<PREV_AGG, OUT_LAYER, true>(rows, kEdgeSlotBytes, p); break;
+                    case PREV_AGG_ALL: bwd_nb<PREV_AGG_ALL, OUT_LAYER, true>(rows, kEdgeSlotBytes, p); break;
                     case PREV_AGG_HIST: bwd_nb<PREV_AGG_HIST, OUT_LAYER, true>(rows, kEdgeSlotBytes, p); break;
                     case PREV_SAGE: bwd_nb<PREV_SAGE, OUT_LAYER, true>(rows, kEdgeSlotBytes, p); break;
                     case PREV_SAGE_HIST: bwd_nb<PREV_SAGE_HIST, OUT_LAYER, true>(rows, kEdgeSlotBytes, p); break;
@@ -1600,6 +1606,9 @@ struct Stage {
                 break;
             case PREV_AGG:
                 launch(cls, bytes, flops, gather, [&]() { bwd_nb<PREV_AGG, OUT_LAYER>(rows, smem, p); });
+                break;
+            case PREV_AGG_ALL:
+                launch(cls, bytes, flops, gather, [&]() { bwd_nb<PREV_AGG_ALL, OUT_LAYER>(rows, smem, p); });
                 break;
             case PREV_AGG_HIST:
                 launch(cls, bytes, flops, gather,
@@ -1646,10 +1655,15 @@ struct Stage {
         else if (hist)
             launch(GP_K_BWD_AGG, bytes, 2.0 * e * d.din, e * d.sin * 4.0,
                    [&]() { bwd_nb<PREV_AGG_HIST, OUT_DHIN>(rows, kEdgeSlotBytes, p); });
+        else if (done == all_chunks())
+            launch(GP_K_BWD_AGG, bytes, 2.0 * e * d.din, e * d.sin * 4.0,
+                   [&]() { bwd_nb<PREV_AGG_ALL, OUT_DHIN>(rows, kEdgeSlotBytes, p); });
         else
             launch(GP_K_BWD_AGG, bytes, 2.0 * e * d.din, e * d.sin * 4.0,
                    [&]() { bwd_nb<PREV_AGG, OUT_DHIN>(rows, kEdgeSlotBytes, p); });
     }
+
+    uint64_t all_chunks() const { return K == 64 ? ~0ull : ((1ull << K) - 1); }
 
     XentParams xent_params(uint32_t r0, uint32_t r1) {
         auto& d = L[len - 1];

@@ -21,7 +21,10 @@ constexpr int kBlock = kWarpsPerBlock * 32;
 constexpr unsigned kFull = 0xffffffffu;
 
 enum FwdKind { FWD_DENSE = 0, FWD_GCN = 1, FWD_GCN2 = 2, FWD_SAGE = 3 };
-enum PrevKind { PREV_TOP = 0, PREV_AGG = 1, PREV_AGG_HIST = 2, PREV_OWN = 3, PREV_SAGE = 4, PREV_SAGE_HIST = 5 };
+// PREV_AGG_ALL: PREV_AGG when every chunk is done (the last chunk of a backward pass,
+// synchronous mode): no done filter, so no per-batch compaction.
+enum PrevKind { PREV_TOP = 0, PREV_AGG = 1, PREV_AGG_HIST = 2, PREV_OWN = 3, PREV_SAGE = 4, PREV_SAGE_HIST = 5,
+                PREV_AGG_ALL = 6 };
 enum OutKind { OUT_LAYER = 0, OUT_DHIN = 1 };
 
 __device__ __forceinline__ float4 ld4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }

@@ -442,7 +442,8 @@ __global__ void __launch_bounds__(kBlock, MINB ? MINB : (SPLIT && NB == 2 ? GP_S
                     p.rowptr_m, p.edges_m, u, has, p.bgn + p.sgap, p.bgn_snap ? p.bgn_snap + p.sgap : nullptr,
                     p.bgnstride, p.done, lane, dh_act, reinterpret_cast<uint2*>(smem4) + (threadIdx.x / 32) * 32, own);
             } else {
-                s = gather_row8<true, PREV == PREV_AGG_HIST, NB>(p.rowptr, p.edges, u, has, p.bgn, p.bgn_snap, p.bgnstride,
+                s = gather_row8<PREV != PREV_AGG_ALL, PREV == PREV_AGG_HIST, NB>(p.rowptr, p.edges, u, has, p.bgn,
+                                                                              p.bgn_snap, p.bgnstride,
                                                              p.done, lane, dh_act,
                                                              reinterpret_cast<uint2*>(smem4) + (threadIdx.x / 32) * 32,
                                                              f8_zero());

@@ -47,12 +47,14 @@ def test_trace_structure_and_bubble(gp, tmp_path, model_kind, S, K):
         assert nsend == T * K * ((w < S - 1) + (w > 0))
         assert nrecv == nsend and (ev["kind"] == 3).sum() == nrecv
         assert sorted(set(comp["chunk"].tolist())) == [-1] + list(range(K))
-    # every forward message is received no earlier than it was sent
+    # every forward message is received no earlier than it was sent; each stage anchors its events to
+    # %globaltimer with one stamp kernel per epoch, so cross-stage times carry a few microseconds of
+    # anchor jitter (50 us tolerance)
     for w in range(1, S):
         sends = tr[(tr["worker"] == w - 1) & (tr["kind"] == 1)]
         recvs = tr[(tr["worker"] == w) & (tr["kind"] == 2)]
         for k in range(K):
-            assert recvs[recvs["chunk"] == k]["t_start"].min() >= sends[sends["chunk"] == k]["t_start"].min() - 1e-6
+            assert recvs[recvs["chunk"] == k]["t_start"].min() >= sends[sends["chunk"] == k]["t_start"].min() - 5e-5
     b = gp.bubble_analysis(tr)
     assert b["stages"] == S and b["chunks"] == K
     assert b["ideal_bubble"] == pytest.approx((S - 1) / (K + S - 1))
