@@ -341,17 +341,18 @@ def main():
     fa = prof["fwd_agg"]
     achieved = fa["alg_bytes"] / (fa["ms"] / 1e3) / 1e9 if fa["ms"] > 0 else None
     gather_rate = fa["gather_bytes"] / (fa["ms"] / 1e3) / 1e9 if fa["ms"] > 0 else None
-    traffic = None
+    traffic, traffic_src = None, None
     tp = os.path.join(ROOT, "profiles", "roofline_traffic.json")
     if os.path.exists(tp):
         try:
             t = json.load(open(tp)).get(args.workload)
             if t and L == WORKLOADS[args.workload][6]:
-                # ncu DRAM bytes per row x the average rows of one launch (one chunk)
-                traffic = {"value": t["dram_bytes_per_row"] * N / K / 1e9, "unit": "GB/launch",
-                           "source": t["source"]}
+                # ncu DRAM bytes per row x the average rows of one launch (one chunk), in bytes
+                traffic = t["dram_bytes_per_row"] * N / K
+                traffic_src = t["source"]
         except Exception:
             traffic = None
+    alg_per_launch = fa["alg_bytes"] / fa["launches"] if fa["launches"] else None
     agg_layers = sum(1 for s in specs if s.aggregates)
     edges_per_s = 2.0 * (E2) * agg_layers * 2 / (ms_step / 1e3)
     total_ms = sum(v["ms"] for v in prof.values())
@@ -369,7 +370,10 @@ def main():
         "edges_per_s": edges_per_s,
         "roofline": {"kernel": "k_fwd8<FWD_GCN2, split> (CSR SpMM gather + GCNII initial-residual mix -> pre; the transform runs in k_fwd_tile)",
                      "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                     "frac": (achieved / hbm) if achieved else None, "peak_source": src, "traffic": traffic,
+                     "frac": (achieved / hbm) if achieved else None, "peak_source": src,
+                     # DRAM read + write bytes per launch (ncu) next to the algorithmic bytes per launch
+                     "traffic": traffic, "traffic_unit": "bytes/launch", "traffic_source": traffic_src,
+                     "alg_bytes_per_launch": alg_per_launch,
                      "l2_gather_gbs": gather_rate,
                      # the binding roof of the gather: random 416-byte rows from the
                      # L2-resident table through LDG.256, measured by tools/tex_gather_bench.cu
