@@ -23,6 +23,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <deque>
+#include <functional>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -290,6 +291,14 @@ struct Stage {
     // streams in the chunk wavefront (GP_WAVE=1..4). Reddit shape, one B200:
     // 4 streams 0.440 vs 2 streams 0.466 s/epoch at K = 32 (0.435 vs 0.438 at K = 4).
     int wave_w = 4;
+    // GP_MERGED_G=1: one gather table per layer (G == Gs). A row of G holds the
+    // snapshot until its chunk rewrites it, so the forward gathers read a single
+    // table (half the L2 footprint); the wavefront then also orders "chunk j+1
+    // writes G_{i+1}" after "chunk j's layer i+1 gather" (wave_reads_done).
+    bool merged_g = false;
+    // forward wavefront hooks (merged_g): after the kernel gathering from G_i, and
+    // before the kernel writing rows of G_i
+    std::function<void(uint32_t)> on_gather_done, before_g_write;
     std::vector<LayerDev> L;
 
     // graph (renumbered chunk-contiguous)
@@ -527,6 +536,7 @@ struct Stage {
         GP_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, device));
         GP_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
         if (const char* e = std::getenv("GP_WAVE")) wave_w = std::max(1, std::min(kMaxWave, std::atoi(e)));
+        if (const char* e = std::getenv("GP_MERGED_G")) merged_g = std::atoi(e) != 0;
         for (int w = 1; w < wave_w; ++w) GP_CUDA(cudaStreamCreateWithFlags(&cs_side[w], cudaStreamNonBlocking));
         GP_CUDA(cudaEventCreate(&ev_start));
         GP_CUDA(cudaEventCreate(&ev_end));
@@ -593,7 +603,7 @@ struct Stage {
             if (d.agg) {
                 d.G = dalloc<float>(size_t(n + 1) * d.sin);
                 // stage 0's layer-0 input is x0 (cur == snap); sync mode never reads snapshots
-                d.Gs = (first && i == 0) || sync ? d.G : dalloc<float>(size_t(n + 1) * d.sin);
+                d.Gs = (first && i == 0) || sync || merged_g ? d.G : dalloc<float>(size_t(n + 1) * d.sin);
             }
             if (!sync && i + 1 < len && specs[lb + i + 1].kind != GP_DENSE)
                 d.hs = dalloc<float>(size_t(n) * d.sout);
@@ -1370,6 +1380,12 @@ struct Stage {
             nk = drop_key(t, d.l + 1, L[i + 1].din);
         }
         const float alpha = float(d.spec.alpha), beta = float(d.spec.beta);
+        auto gather_done = [&]() {
+            if (on_gather_done && d.agg) on_gather_done(i);
+        };
+        auto write_wait = [&]() {
+            if (before_g_write && gnext) before_g_write(i + 1);
+        };
         if (d.din <= kMaxWidth) {
             FwdParams p{};
             p.r0 = r0;
@@ -1424,6 +1440,8 @@ struct Stage {
                 const double db = double(rows) * (d.kw + d.dout + (gnext ? d.dout : 0)) * 4.0 +
                                   double(d.kw) * d.dout * 4.0;
                 launch(GP_K_FWD_AGG, eb, 2.0 * e * d.din, gather, [&]() { fwd_nb<FWD_SAGE, true>(rows, kEdgeSlotBytes, p); });
+                gather_done();
+                write_wait();
                 FwdParams q = p;
                 q.W = d.Wg;
                 q.din = d.kw;
@@ -1442,18 +1460,22 @@ struct Stage {
                     if (g2) fwd_nb<FWD_GCN2, true>(rows, kEdgeSlotBytes, p);
                     else fwd_nb<FWD_GCN, true>(rows, kEdgeSlotBytes, p);
                 });
+                gather_done();
+                write_wait();
                 launch(GP_K_FWD_DENSE, db, 2.0 * double(rows) * d.din * d.dout, 0, [&]() {
                     if (g2) fwd_dense_go<true>(rows, p);
                     else fwd_dense_go<false>(rows, p);
                 });
                 return;
             }
+            write_wait();
             if (d.spec.kind == GP_DENSE)
                 launch(cls, bytes, flops, 0, [&]() { fwd_nb<FWD_DENSE>(rows, smem, p); });
             else if (d.spec.kind == GP_GCNCONV)
                 launch(cls, bytes, flops, gather, [&]() { fwd_nb<FWD_GCN>(rows, smem, p); });
             else
                 launch(cls, bytes, flops, gather, [&]() { fwd_nb<FWD_GCN2>(rows, smem, p); });
+            gather_done();
             return;
         }
         // wide input (layer 0 with F > 128): pre first, then the tiled transform. SageConv:
@@ -1466,6 +1488,7 @@ struct Stage {
             launch(GP_K_FWD_AGG, e * 8.0 + double(n) * d.din * 4.0 + double(rows) * d.din * 4.0,
                    2.0 * e * d.din, e * d.sin * 4.0,
                    [&]() { k_spmm_pre<<<row_grid(rows, (const void*)k_spmm_pre, 0), kBlock, 0, cs>>>(sp); });
+            gather_done();
             if (d.sage) {
                 RemaskParams rp{r0, r1, d.din, cur_src(i), src_stride(i), d.pre, d.skw, orig, drop_key(t, d.l, d.din)};
                 launch(GP_K_FWD_DENSE, double(rows) * d.din * 8.0, 0, 0,
@@ -1493,6 +1516,7 @@ struct Stage {
         g.gnstride = gnstride;
         g.next_mask = nk;
         g.orig = orig;
+        write_wait();
         launch(GP_K_FWD_DENSE,
                double(rows) * (d.din + d.dout + (gnext ? d.dout : 0)) * 4.0 + double(d.din) * d.dout * 4.0,
                2.0 * double(rows) * d.din * d.dout, 0,
@@ -2522,9 +2546,24 @@ struct Stage {
             } restore{cs, main};
             // ev[j % W][i]: chunk j's input (i = 0) / layer i-1 output (i >= 1) is written
             std::vector<std::vector<cudaEvent_t>> ev(W, std::vector<cudaEvent_t>(len + 1, nullptr));
+            // merged_g: rd[j % W][i]: chunk j's gather from G_i has finished; chunk j+w
+            // overwrites its own (snapshot) rows of G_i only after that
+            std::vector<std::vector<cudaEvent_t>> rd(W, std::vector<cudaEvent_t>(len, nullptr));
+            uint32_t kk = 0;
+            struct Unhook {
+                Stage* st;
+                ~Unhook() { st->on_gather_done = nullptr, st->before_g_write = nullptr; }
+            } unhook{this};
+            if (merged_g && W > 1) {
+                on_gather_done = [&](uint32_t i) { rd[kk % W][i] = record_event(); };
+                before_g_write = [&](uint32_t i) {
+                    for (uint32_t w = 1; w < uint32_t(W) && w <= kk; ++w)
+                        if (cudaEvent_t e = rd[(kk - w) % W][i]) GP_CUDA(cudaStreamWaitEvent(cs, e, 0));
+                };
+            }
             wave_fork(W);
             uint64_t done = 0;
-            for (uint32_t kk = 0; kk < K; ++kk) {
+            for (; kk < K; ++kk) {
                 const uint32_t k = ord[kk];
                 const uint32_t r0 = row_begin(k), r1 = row_end(k);
                 done |= 1ull << k;  // "processed" includes the current chunk (:789)
@@ -2532,7 +2571,10 @@ struct Stage {
                 auto& mine = ev[kk % W];
                 if (!first) traced_recv(k, [&]() { recv_fwd(k); });
                 cudaEvent_t c0 = trace_mark();
-                if (!first && L[0].agg) remask(0, in_cur, r0, r1, drop_key(t, L[0].l, L[0].din));
+                if (!first && L[0].agg) {
+                    if (before_g_write) before_g_write(0);
+                    remask(0, in_cur, r0, r1, drop_key(t, L[0].l, L[0].din));
+                }
                 if (W > 1) mine[0] = record_event();
                 for (uint32_t i = 0; i < len; ++i) {
                     if (G > 1 && L[i].agg) halo_fwd(i, k, k + 1, t);  // exchange_rows (:792-794)
