@@ -108,3 +108,23 @@ def test_reddit_shape_64_layer_runs_are_deterministic(gp):
     assert np.all(np.isfinite(runs[0].train_loss))
     for (Wa, ba), (Wb, bb) in zip(runs[0].params, runs[1].params):
         assert np.array_equal(Wa.view(np.uint32), Wb.view(np.uint32))
+
+
+@pytest.mark.parametrize("env", [{}, {"GP_MERGED_G": "1"}], ids=["wavefront", "wavefront_merged_g"])
+def test_reddit_shape_wavefront_equals_serial_chunks(gp, env, monkeypatch):
+    """K = 32 (the 8-stage chunk count, where four chunks are in flight on the wavefront streams): the
+    wavefront, with split or merged gather tables, trains bit-identically to serial chunks (GP_WAVE=1),
+    so no chunk reads a gather row another stream is writing."""
+    ds = gp.Dataset.synthetic_er(N, E2 / (N * (N - 1)), 1, F, C, 1)
+    model = gp.ModelConfig(kind=gp.ModelKind.GCNII, layers=16, hidden=H, dropout=0.5)
+    co = gp.make_chunks(ds, 32, 1)
+    opt = gp.TrainOptions(model=model, epochs=3, seed=1)
+    monkeypatch.setenv("GP_WAVE", "1")
+    serial = gp.train_pipeline(ds, co, 1, opt)
+    monkeypatch.delenv("GP_WAVE")
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    wave = gp.train_pipeline(ds, co, 1, opt)
+    assert np.array_equal(wave.train_loss, serial.train_loss)
+    for (Wa, _), (Wb, _) in zip(wave.params, serial.params):
+        assert np.array_equal(Wa.view(np.uint32), Wb.view(np.uint32))

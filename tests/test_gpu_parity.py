@@ -176,8 +176,8 @@ def test_train_gcn_pipeline_stale_two_stages(gp):
                    fix_alpha=3)
 
 
-@pytest.mark.parametrize("env", [{}, {"GP_SPLIT": "0"}, {"GP_WAVE": "1"}, {"GP_OCC5": "1"}],
-                         ids=["default", "fused", "one_stream", "occ5"])
+@pytest.mark.parametrize("env", [{}, {"GP_SPLIT": "0"}, {"GP_WAVE": "1"}, {"GP_OCC5": "1"}, {"GP_MERGED_G": "1"}],
+                         ids=["default", "fused", "one_stream", "occ5", "merged_g"])
 def test_train_sage_pipeline_stale_two_stages(gp, env, monkeypatch):
     """GraphSAGE (SageConv: [own | mean] . W, nn.hpp:176-182, :234-243) over two stages, under every
     engine variant switch (SageConv layers always run split; the others follow GP_SPLIT)."""
@@ -210,8 +210,9 @@ def test_train_sage_wide_features_two_stages(gp):
                    gp.ModelConfig(kind=1, layers=3, hidden=16), 2, 4, 1, 6, 50, fix_alpha=2)
 
 
-@pytest.mark.parametrize("env", [{"GP_SPLIT": "0"}, {"GP_WAVE": "1"}, {"GP_OCC5": "1"}, {"GP_PGRAD": "simt"}],
-                         ids=["fused", "one_stream", "occ5", "simt_pgrad"])
+@pytest.mark.parametrize("env", [{"GP_SPLIT": "0"}, {"GP_WAVE": "1"}, {"GP_OCC5": "1"}, {"GP_PGRAD": "simt"},
+                                 {"GP_MERGED_G": "1"}, {"GP_MERGED_G": "1", "GP_SPLIT": "0"}],
+                         ids=["fused", "one_stream", "occ5", "simt_pgrad", "merged_g", "merged_g_fused"])
 def test_engine_variants_match_default_bitwise(gp, env, monkeypatch):
     """The engine's switches change scheduling and kernel shapes, never arithmetic order (except the
     pgrad reduction): losses and parameters equal the default run bit for bit."""
