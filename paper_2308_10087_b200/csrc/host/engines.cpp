@@ -274,7 +274,7 @@ TrainResult<float> run_hybrid_f32(const Dataset& ds, const Partition* part, cons
     std::vector<double> trace_bubble(T, -1.0);
     if (opt.fabric.collect_trace) {
         std::vector<std::vector<gp_trace_event>> ev(W);
-        double t0 = 0;
+        double ns0 = 0;
         bool any = false;
         for (uint32_t w = 0; w < W; ++w) {
             uint64_t cnt = 0;
@@ -282,7 +282,7 @@ TrainResult<float> run_hybrid_f32(const Dataset& ds, const Partition* part, cons
             ev[w].resize(cnt);
             gp_get_trace(ctx.v[w], ev[w].data(), cnt, &cnt);
             for (const auto& e : ev[w]) {
-                t0 = any ? std::min(t0, e.t_start_ns) : e.t_start_ns;
+                ns0 = any ? std::min(ns0, e.t_start_ns) : e.t_start_ns;
                 any = true;
             }
         }
@@ -292,8 +292,8 @@ TrainResult<float> run_hybrid_f32(const Dataset& ds, const Partition* part, cons
             for (const auto& e : ev[w]) {
                 TraceEvent te{};
                 te.worker = worker_id[w];
-                te.t_start = (e.t_start_ns - t0) * 1e-9;
-                te.t_end = (e.t_end_ns - t0) * 1e-9;
+                te.t_start = (e.t_start_ns - ns0) * 1e-9;
+                te.t_end = (e.t_end_ns - ns0) * 1e-9;
                 te.kind = TraceEvent::Kind(e.kind);
                 te.chunk = e.chunk;
                 te.layer_lo = e.layer_lo;

@@ -60,6 +60,8 @@ def test_trace_structure_and_bubble(gp, tmp_path, model_kind, S, K):
     assert b["ideal_bubble"] == pytest.approx((S - 1) / (K + S - 1))
     assert 0.0 <= b["measured_bubble"] < 1.0
     assert np.all((res.metrics[:, 6] >= 0) & (res.metrics[:, 6] < 1))
+    if S > 1:  # per-epoch measured idle fraction (engines_impl.hpp:887-891): stage 1 waits for chunk 0
+        assert np.all(res.metrics[:, 6] > 0)
     gp.write_run_outputs(res, str(tmp_path))
     assert sum(1 for _ in open(tmp_path / "trace.jsonl")) == len(tr)
     assert open(tmp_path / "metrics.csv").read().count("\n") == T + 1
