@@ -80,3 +80,27 @@ def test_writers_match_reference_bytes(gold, tmp_path):
         dict(mode="graph", n=1000, layers=4, hidden=16, stages=1, ways=3, alpha=0.25, vecs=1,
              predicted_bytes=128000, measured_bytes=127990, rel_error=7.8125e-5)])
     assert (tmp_path / "compare.csv").read_text() == str(gold["file_compare_csv"])
+
+
+def test_train_tool_compare_rows(tmp_path):
+    """`gnnsim compare` rows (gnnsim.cpp:305-347) from a result's ledger: graph mode predicts
+    2 alpha N sum(in_dim of aggregating layers) 4 bytes, pipeline volume_pipeline, hybrid both."""
+    import sys
+    from types import SimpleNamespace
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+    import gnnpipe_train
+    ds = gp.Dataset.synthetic_er(200, 0.05, 3, 24, 5, 4)
+    model = gp.ModelConfig(kind=gp.ModelKind.GCNII, layers=4, hidden=16)
+    specs = gp.build_layer_specs(model, ds.num_features, ds.num_classes)
+    alpha = 0.75
+    halo = 2.0 * sum(alpha * 200 * s.in_dim * 4.0 for s in specs if s.aggregates)
+    pipe = gp.comm_volumes(200, 4, 16, 2, 2, alpha, 2)["pipeline"]
+    comm = np.array([[int(halo), int(pipe), 0], [int(halo) + 40, int(pipe), 0]], np.uint64)
+    res = SimpleNamespace(metrics=np.zeros((2, 7)), comm=comm)
+    path = str(tmp_path / "compare.csv")
+    gnnpipe_train.write_compare(path, "hybrid", ds, model, res, 2, 2, alpha)
+    lines = open(path).read().splitlines()
+    assert lines[0] == "mode,N,L,H,S,W,alpha,vecs,predicted_bytes,measured_bytes,rel_error"
+    assert len(lines) == 3 and all(l.startswith("hybrid,200,4,16,2,2,0.75,2,") for l in lines[1:])
+    assert lines[1].endswith(",0")
+    assert float(lines[2].split(",")[-1]) == pytest.approx(40 / (halo + pipe))
