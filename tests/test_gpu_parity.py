@@ -407,7 +407,7 @@ def test_train_gcn16_arxivlike_20_epoch_curve(gp):
     Adam moves a weight by ~lr per step whatever the gradient's size, so gradient elements whose sign
     sits at fp32 rounding level (vanishing gradients of the upper layers) can take a few opposite
     steps: weights within 5 lr (5e-3) absolute, median relative 1e-3 (measured: 3.8e-3, <= 3.8e-4;
-    lower layers ~1e-5, tools/param_diff_probe.py). The engine against itself with only the
+    lower layers ~1e-5, a param-diff probe, round 1). The engine against itself with only the
     parameter-gradient summation order changed (GP_PGRAD=simt) differs by the same amounts (2.9e-3 at
     layer 14), so this is fp32 amplification, not a semantic difference."""
     ds = gp.Dataset.synthetic_er(20000, 0.0007, 21, 128, 40, 5)
