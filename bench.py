@@ -41,6 +41,7 @@ WORKLOADS = {
                  "GCNII H=128"),
 }
 METRIC = "epoch time, 64-layer GCNII full-graph, 1/2/4/8 B200; SpMM GB/s vs HBM peak"
+DATA = "synthetic (generate_er graph + hashed features, seed 1)"
 
 
 def peaks():
@@ -103,40 +104,94 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
+# ----------------------------------------------------------------------------- shared
+def stage_ranges(L, S):
+    """make_stage_assignment (engines.cpp:8-21) restated: near-equal consecutive layer
+    split, the first L mod S stages get one extra. Kept here so the reference arm never
+    imports the product package."""
+    base, extra = divmod(L, S)
+    out, lo = [], 0
+    for s in range(S):
+        hi = lo + base + (1 if s < extra else 0)
+        out.append((lo, hi))
+        lo = hi
+    return out
+
+
+def workload_config(args, S, K):
+    """The `config` object both arms print (identical keys and values)."""
+    N, E2, F, Cc, H, mk, L, desc = WORKLOADS[args.workload]
+    L = args.layers or L
+    return {"workload": desc, "num_vertices": N, "directed_edges": E2, "features": F, "classes": Cc,
+            "hidden": H, "layers": L, "model": mk, "stages": S, "chunks": K, "parallelism": f"pp{S}",
+            "l2_policy": (f"inputs larger than L2: one epoch streams {L} layers of N x H fp32 stashes "
+                          f"({N * H * 4 * L / 2**30:.1f} GiB per stash kind) through the 126 MB L2"
+                          if N * H * 4 * L > 4 * 126e6 else
+                          "inputs smaller than L2 (launch-bound shape; no flush between epochs)")}
+
+
 # ----------------------------------------------------------------------------- reference arm
-def reference_epoch(args, S, K, steps):
-    """Times the reference's own CPU kernels (oracle/_ref) on a bounded row sample and
-    assembles the epoch time of an S-stage pipeline: max stage work x (K+S-1)/K."""
+def reference_epochs(args, S, K):
+    """Whole epochs of the reference's own train_pipeline<float> (engines_impl.hpp:911-920,
+    oracle/_ref/ref_driver epochs; Fabric::Mode::Concurrent, one thread per stage worker)
+    on the same synthetic graph, at L=3 and L=4 layers, run side by side. A 64-layer epoch
+    on one core is hours, so the L-layer value is the projection
+    t(3) + (L-3) * (t(4) - t(3)), labelled as such."""
     from oracle.blob import REF_DRIVER, read_blob
     if not os.path.exists(REF_DRIVER):
         return None, "oracle/_ref/ref_driver not built"
     N, E2, F, Cc, H, model, L, _ = WORKLOADS[args.workload]
     L = args.layers or L
     p = E2 / (N * (N - 1))
-    threads = 1  # per-row cost of one reference worker; stages run as parallel threads
-    rows = args.ref_rows
+    Ls = (3, 4) if L > 16 else (L,)
+    Sm = min(S, 3)  # L=3 cannot be split over more stages than layers
     with tempfile.TemporaryDirectory() as td:
-        out = os.path.join(td, "b.blob")
-        cmd = [REF_DRIVER, "bench", f"spec=er:{N}:{p!r}:1:{F}:{Cc}:1", f"model={model}", f"layers={L}",
-               f"hidden={H}", f"rows={rows}", f"steps={steps}", f"threads={threads}", f"out={out}"]
+        procs = {}
         t0 = time.perf_counter()
-        r = subprocess.run(cmd, capture_output=True, text=True)
+        for l in Ls:
+            out = os.path.join(td, f"e{l}.blob")
+            cmd = [REF_DRIVER, "epochs", f"spec=er:{N}:{p!r}:1:{F}:{Cc}:1", f"model={model}", f"layers={l}",
+                   f"hidden={H}", f"S={min(Sm, l)}", f"K={K}", "chunk_seed=1", "seed=1", "epochs=1", f"out={out}"]
+            procs[l] = (subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True), out)
+        res = {}
+        for l, (pr, out) in procs.items():
+            _, err = pr.communicate()
+            if pr.returncode != 0:
+                return None, f"ref_driver epochs failed: {err.strip()[:200]}"
+            res[l] = read_blob(out)
         wall = time.perf_counter() - t0
-        if r.returncode != 0:
-            return None, f"ref_driver bench failed: {r.stderr.strip()[:200]}"
-        d = read_blob(out)
-    per = d["layer_epoch_seconds"].reshape(steps, L)
-    import paper_2308_10087_b200 as gp
-    ranges = gp.make_stage_assignment(L, S)
-    epochs = []
-    for s in range(steps):
-        stage_work = [float(per[s, lo:hi].sum()) for lo, hi in ranges]
-        # each stage is one reference worker thread (fabric.cpp:401-422); GPipe fill/drain
-        epochs.append(max(stage_work) * (K + S - 1) / K)
-    sample = (f"{int(d['rows_sampled'][0])} evenly strided rows per layer kind (first/middle/last) "
-              f"x {steps} steps of the reference per-row kernels + DropMask::make, extrapolated to "
-              f"N={N} rows x {L} layers, S={S} stage threads, (K+S-1)/K fill/drain; sampler wall {wall:.1f}s")
-    return {"epochs": epochs, "threads": min(S, os.cpu_count() or 1), "sample": sample}, None
+    ep = {l: float(res[l]["epoch_s"][0]) for l in Ls}
+    if len(Ls) == 2:
+        marg = ep[4] - ep[3]
+        full = ep[3] + (L - 3) * marg
+        how = (f"projection t(3)+(L-3)*(t(4)-t(3)) from measured whole train_pipeline<float> epochs at "
+               f"L=3 ({ep[3]:.1f} s) and L=4 ({ep[4]:.1f} s), marginal {marg:.1f} s per conv layer")
+    else:
+        full = ep[L]
+        how = f"measured whole train_pipeline<float> epoch at L={L} ({full:.2f} s)"
+    if S > Sm:  # more stages than the measured runs: each stage is one single-threaded worker
+        full = full * Sm / S * (K + S - 1) / (K + Sm - 1)
+        how += f"; scaled from S={Sm} to S={S} stage threads with (K+S-1)/K fill/drain"
+    g = res[Ls[0]]
+    sample = (f"{how}; same graph/features/K/seed as the GPU arm, S={min(Sm, Ls[0])} worker thread(s) per run, "
+              f"runs side by side; excl. dataset gen ({float(g['gen_s'][0]):.1f} s), make_chunks "
+              f"({float(g['chunk_s'][0]):.1f} s) and the call's setup ({float(g['setup_s'][0]):.1f} s); "
+              f"CPU wall {wall:.0f} s")
+    return {"value": full, "cores": min(Sm, Ls[0]), "sample": sample, "projection": len(Ls) == 2 or S > Sm,
+            "measured_epoch_s": ep, "cpu_wall_s": wall, "cpu": cpu_info()}, None
+
+
+def cpu_info():
+    model = ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"model": model, "nproc": os.cpu_count()}
 
 
 def run_reference_arm(args, world, rank):
@@ -144,21 +199,23 @@ def run_reference_arm(args, world, rank):
         return
     S = world
     K = args.chunks or 4 * S
-    res, err = reference_epoch(args, S, K, args.warmup + args.steps)
-    N, E2, F, Cc, H, model, L, desc = WORKLOADS[args.workload]
+    res, err = reference_epochs(args, S, K)
     if res is None:
         print(json.dumps({"impl": "reference", "unavailable": err}))
         return
-    ep = res["epochs"][args.warmup:]
-    v = statistics.median(ep)
+    v = res["value"]
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "s/epoch", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": desc, "stages": S, "chunks": K, "layers": args.layers or L},
-        "cpu_baseline": {"value": v, "unit": "s/epoch", "cores": res["threads"], "kind": "reference",
-                         "sample": res["sample"]},
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": DATA,
+        "config": workload_config(args, S, K),
+        "cpu_baseline": {"value": v, "unit": "s/epoch", "cores": res["cores"], "kind": "reference",
+                         "sample": res["sample"], "projection": res["projection"],
+                         "measured_epoch_s": res["measured_epoch_s"], "cpu_wall_s": res["cpu_wall_s"],
+                         "cpu": res["cpu"]},
         "e2e": {"value": v, "unit": "s/epoch", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": ("steps/warmup are not repeated on the CPU: one whole epoch per layer count is measured "
+                 "(cpu_baseline.measured_epoch_s; the run's CPU wall is cpu_baseline.cpu_wall_s)"),
     }
     print(json.dumps(line))
 
@@ -175,12 +232,22 @@ def main():
     ap.add_argument("--chunks", type=int, default=0, help="K (default 4*S, gnnsim.cpp:226)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--ref-rows", type=int, default=600)
     ap.add_argument("--transport", default="ipc", choices=["ipc", "nccl"],
                     help="stage boundary transport for N>1: CUDA-IPC copy-engine rings (default) or NCCL send/recv")
     args = ap.parse_args()
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # one process per GPU: relaunch this script under torchrun with N ranks
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} disagrees with WORLD_SIZE={world}")
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
@@ -328,12 +395,13 @@ def main():
 
     cpu = None
     if rank == 0 and S == 1 and not args.no_cpu_baseline:
-        res, err = reference_epoch(args, 1, K, 2)
+        res, err = reference_epochs(args, 1, K)
         if res is None:
             cpu = {"value": None, "unavailable": err}
         else:
-            cpu = {"value": statistics.median(res["epochs"]), "unit": "s/epoch", "cores": res["threads"],
-                   "kind": "reference", "sample": res["sample"]}
+            cpu = {"value": res["value"], "unit": "s/epoch", "cores": res["cores"], "kind": "reference",
+                   "sample": res["sample"], "projection": res["projection"],
+                   "measured_epoch_s": res["measured_epoch_s"], "cpu": res["cpu"]}
 
     if rank != 0:
         return
@@ -341,17 +409,22 @@ def main():
     fa = prof["fwd_agg"]
     achieved = fa["alg_bytes"] / (fa["ms"] / 1e3) / 1e9 if fa["ms"] > 0 else None
     gather_rate = fa["gather_bytes"] / (fa["ms"] / 1e3) / 1e9 if fa["ms"] > 0 else None
+    # DRAM bytes per launch of the dominant kernel from one committed `ncu --set full`
+    # capture of the same kernel build, scaled from its rows to the rows of one chunk launch
     traffic, traffic_src = None, None
     tp = os.path.join(ROOT, "profiles", "roofline_traffic.json")
     if os.path.exists(tp):
-        try:
-            t = json.load(open(tp)).get(args.workload)
-            if t and L == WORKLOADS[args.workload][6]:
-                # ncu DRAM bytes per row x the average rows of one launch (one chunk), in bytes
-                traffic = t["dram_bytes_per_row"] * N / K
-                traffic_src = t["source"]
-        except Exception:
-            traffic = None
+        t = json.load(open(tp)).get(args.workload)
+        if t:
+            traffic = t["dram_bytes_per_row"] * N / K
+            traffic_src = t["source"]
+    # the binding roof of the gather: random padded-row gathers from an L2-resident table,
+    # measured by tools/l2_gather_bench.cu (profiles/gather_ceiling.json)
+    ceiling, ceiling_src = None, None
+    cp = os.path.join(ROOT, "profiles", "gather_ceiling.json")
+    if os.path.exists(cp):
+        c = json.load(open(cp))
+        ceiling, ceiling_src = c.get("gbs"), c.get("source")
     alg_per_launch = fa["alg_bytes"] / fa["launches"] if fa["launches"] else None
     agg_layers = sum(1 for s in specs if s.aggregates)
     edges_per_s = 2.0 * (E2) * agg_layers * 2 / (ms_step / 1e3)
@@ -359,11 +432,10 @@ def main():
     line = {
         "metric": METRIC, "value": ms_step / 1e3, "unit": "s/epoch", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic (generate_er graph + hashed features, seed 1)",
-        "config": {"workload": desc, "num_vertices": N, "nnz_norm_adj": int(cols.size), "features": F,
-                   "classes": Cc, "hidden": H, "layers": L, "model": mk, "stages": S, "chunks": K,
-                   "parallelism": f"pp{S}", "transport": args.transport if S > 1 else None,
-                   "ranks_per_gpu": -(-world // max(1, ndev)), "l2_policy": f"inputs larger than L2 (stage stash {dev_bytes/2**30:.1f} GiB)"},
+        "vs_baseline": None, "dtype": "f32", "data": DATA,
+        "config": workload_config(args, S, K),
+        "transport": args.transport if S > 1 else None, "ranks_per_gpu": -(-world // max(1, ndev)),
+        "nnz_norm_adj": int(cols.size), "stage_stash_gib": round(dev_bytes / 2**30, 2),
         "clocks": clk.summary(),
         "e2e": e2e,
         "gpu_launches": int(launches),
@@ -375,10 +447,8 @@ def main():
                      "traffic": traffic, "traffic_unit": "bytes/launch", "traffic_source": traffic_src,
                      "alg_bytes_per_launch": alg_per_launch,
                      "l2_gather_gbs": gather_rate,
-                     # the binding roof of the gather: random 416-byte rows from the
-                     # L2-resident table through LDG.256, measured by tools/tex_gather_bench.cu
-                     "gather_ceiling_gbs": 16374.0,
-                     "gather_frac": (gather_rate / 16374.0) if gather_rate else None,
+                     "gather_ceiling_gbs": ceiling, "gather_ceiling_source": ceiling_src,
+                     "gather_frac": (gather_rate / ceiling) if gather_rate and ceiling else None,
                      "share_of_step": fa["ms"] / total_ms if total_ms else None},
         "cpu_baseline": cpu,
         "kernel_ms_per_epoch": {k: round(v["ms"], 3) for k, v in prof.items() if v["launches"]},

@@ -15,7 +15,8 @@
 //           seed=.. dropout=.. fix_alpha=.. shuffle=.. sync=.. hist=.. mode=seq|pipe
 //           out=...                           metrics + final params
 //   save    spec=... dir=...                 save_dataset (reference writer)
-//   bench   spec=... ...                     CPU baseline sample (see run_bench)
+//   epochs  spec=... model=.. layers=.. hidden=.. S=.. K=.. epochs=.. out=...
+//                                            timed whole train_pipeline epochs (CPU baseline)
 //   ckpt    model=.. layers=.. hidden=.. F=.. C=.. seed=.. lo=.. hi=.. path=.. out=...
 //                                            save_stage_checkpoint of init_params(seed)
 //   analytics in=EVENTS dir=DIR out=...      bubble_analysis of the trace in EVENTS (one
@@ -389,81 +390,46 @@ void cmd_save(const Args& a) {
     save_dataset(d, arg(a, "dir"));
 }
 
-// CPU baseline sample (bench.py --impl reference / cpu_baseline). Times the
-// reference's own per-row kernels — kernel::forward_row, backward_out_row,
-// backward_prev_row (nn.hpp:159-257) and param_grads_for_rows (nn.hpp:269-293) —
-// plus DropMask::make (nn.hpp:112-127) for every distinct layer shape of the
-// model, over a bounded, evenly strided row sample, with `threads` workers over
-// disjoint rows (the kernels are pure per row). Output: per-layer seconds for
-// one epoch of that layer over all N rows (per-row cost x N + mask cost), from
-// which bench.py assembles the epoch time of any stage split.
-void cmd_bench(const Args& a) {
+// CPU baseline (bench.py --impl reference and cpu_baseline): whole epochs of the
+// reference's own train_pipeline<float> (engines_impl.hpp:911-920) through its
+// public API, Fabric::Mode::Concurrent (one OS thread per stage worker,
+// fabric.cpp:395-422). The call's own setup (adjacency bundle, feature cast,
+// stash allocation) is timed by an epochs=0 call and subtracted; dataset
+// generation and make_chunks are timed separately.
+void cmd_epochs(const Args& a) {
+    using clk = std::chrono::steady_clock;
+    auto secs = [](clk::time_point t0) { return std::chrono::duration<double>(clk::now() - t0).count(); };
+    auto t0 = clk::now();
     Dataset d = make_dataset(arg(a, "spec"));
-    ModelConfig mc = model_from(a);
-    const uint32_t threads = uint32_t(argu(a, "threads", "1"));
-    const uint32_t sample = uint32_t(argu(a, "rows", "1000"));
-    const uint32_t steps = uint32_t(argu(a, "steps", "1"));
-    auto specs = build_layer_specs(mc, d.num_features(), d.num_classes);
-    auto params = init_params<float>(specs, 1);
-    auto adj = build_adj_bundle<float>(d.graph, mc.self_loops);
-    const VertexId n = d.num_vertices();
-    const uint32_t L = uint32_t(specs.size());
-    const bool needs_h0 = model_needs_h0(specs);
-    const uint32_t stride = std::max<uint32_t>(1, n / std::max<uint32_t>(1, sample));
-    std::vector<VertexId> rows;
-    for (VertexId v = 0; v < n && rows.size() < sample; v += stride) rows.push_back(v);
-    // representative layers: first, one middle (aggregating) layer, last
-    std::vector<uint32_t> reps = {0};
-    if (L > 2) reps.push_back(1);
-    if (L > 1) reps.push_back(L - 1);
-    std::vector<double> per_layer_epoch(size_t(steps) * L, 0.0);
-    std::vector<double> mask_secs(L, 0.0);
-    for (uint32_t s = 0; s < steps; ++s) {
-        std::vector<double> rep_cost(L, 0.0);
-        for (uint32_t li : reps) {
-            const auto& sp = specs[li];
-            MatF h_prev(n, sp.in_dim), h0(needs_h0 ? n : 0, mc.hidden), pre(n, sp.k_in()), out(n, sp.out_dim);
-            for (size_t i = 0; i < h_prev.size(); ++i) h_prev.data()[i] = float(hash_unit(mix64(3, i)) - 0.5);
-            for (size_t i = 0; i < h0.size(); ++i) h0.data()[i] = float(hash_unit(mix64(4, i)) - 0.5);
-            MatF dz(n, sp.out_dim), dagg(n, sp.k_in()), dprev(n, sp.in_dim), dh0(needs_h0 ? n : 0, mc.hidden),
-                dout(n, sp.out_dim);
-            for (size_t i = 0; i < dout.size(); ++i) dout.data()[i] = float(hash_unit(mix64(5, i)) - 0.5);
-            const auto tm0 = std::chrono::steady_clock::now();
-            auto mask = DropMask<float>::make(mc.dropout, 1, 1, li, n, sp.in_dim);
-            mask_secs[li] = std::chrono::duration<double>(std::chrono::steady_clock::now() - tm0).count();
-            const auto t0 = std::chrono::steady_clock::now();
-            std::vector<std::thread> pool;
-            for (uint32_t t = 0; t < threads; ++t)
-                pool.emplace_back([&, t]() {
-                    for (size_t r = t; r < rows.size(); r += threads) {
-                        const VertexId v = rows[r];
-                        kernel::forward_row(sp, params[li], adj, v, [&](VertexId u) { return h_prev.row(u); },
-                                            mask, needs_h0 && li > 0 ? h0.row(v) : nullptr, pre.row(v), out.row(v));
-                        kernel::backward_out_row(sp, params[li], dout.row(v), out.row(v), dz.row(v), dagg.row(v),
-                                                 sp.kind == LayerKind::Gcn2Conv ? dh0.row(v) : nullptr);
-                        if (li > 0)
-                            kernel::backward_prev_row(sp, adj, v, [&](VertexId u) { return dagg.row(u); },
-                                                      dagg.row(v), mask, dprev.row(v));
-                    }
-                });
-            for (auto& th : pool) th.join();
-            auto g = param_grads_for_rows(sp, rows, pre, dz);
-            (void)g;
-            const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-            // wall time of `threads` workers over the sample -> per-row wall cost
-            rep_cost[li] = secs / double(rows.size()) * double(n) + mask_secs[li];
-        }
-        for (uint32_t l = 0; l < L; ++l) {
-            const uint32_t src = l == 0 ? 0 : (l + 1 == L ? L - 1 : (L > 2 ? 1 : 0));
-            per_layer_epoch[size_t(s) * L + l] = rep_cost[src];
-        }
-    }
+    const double gen_s = secs(t0);
+    const uint32_t S = uint32_t(argu(a, "S", "1"));
+    const uint32_t K = uint32_t(argu(a, "K", "1"));
+    t0 = clk::now();
+    ChunkPlan plan = K == 1 ? chunk_plan_from_assignment(d.num_vertices(), std::vector<uint32_t>(d.num_vertices(), 0))
+                            : make_chunks(d.graph, K, argu(a, "chunk_seed", "1"));
+    const double chunk_s = secs(t0);
+    TrainOptions<float> opt;
+    opt.model = model_from(a);
+    opt.seed = argu(a, "seed", "1");
+    opt.fabric.mode = Fabric::Mode::Concurrent;
+    const uint32_t L = uint32_t(build_layer_specs(opt.model, d.num_features(), d.num_classes).size());
+    const auto sa = make_stage_assignment(L, S);
+    opt.epochs = 0;
+    t0 = clk::now();
+    (void)train_pipeline(d, plan, sa, opt);
+    const double setup_s = secs(t0);
+    opt.epochs = uint32_t(argu(a, "epochs", "1"));
+    t0 = clk::now();
+    const TrainResult<float> res = train_pipeline(d, plan, sa, opt);
+    const double total_s = secs(t0);
     Blob b(arg(a, "out"));
-    b.f64("layer_epoch_seconds", per_layer_epoch);  // steps x L
-    b.u64("rows_sampled", {rows.size()});
-    b.u64("threads", {threads});
-    b.u64("nnz", {adj.norm.cols.size()});
-    b.u64("num_layers", {L});
+    b.f64("gen_s", {gen_s});
+    b.f64("chunk_s", {chunk_s});
+    b.f64("setup_s", {setup_s});
+    b.f64("total_s", {total_s});
+    b.f64("epoch_s", {(total_s - setup_s) / double(opt.epochs)});
+    b.f64("loss", {res.metrics.empty() ? 0.0 : res.metrics.back().train_loss});
+    b.u64("threads", {S});
 }
 
 void cmd_analytics(const Args& a) {
@@ -559,7 +525,7 @@ int main(int argc, char** argv) {
         else if (cmd == "forward") cmd_forward(a);
         else if (cmd == "train") cmd_train(a);
         else if (cmd == "save") cmd_save(a);
-        else if (cmd == "bench") cmd_bench(a);
+        else if (cmd == "epochs") cmd_epochs(a);
         else if (cmd == "analytics") cmd_analytics(a);
         else if (cmd == "ckpt") cmd_ckpt(a);
         else {
