@@ -32,7 +32,7 @@ WORKLOADS = {
                "64-layer GCNII H=100, historical embeddings"),
     "arxiv": (169343, 2332486, 128, 40, 128, "gcn", 16,
               "ogbn-arxiv-shaped ER graph (169,343 vertices, 2.33M directed edges, 128 feat, 40 classes), 16-layer GCN"),
-    "er4k": (4096, 65520, 128, 16, 128, "gcn", 8,
+    "er4k": (4096, 65536, 128, 16, 128, "gcn", 8,
              "ER 4K vertices avg-deg 16, 128 feat, 16 classes, 8-layer GCN"),
     # 64 layers need ~560 GB of stashes at S=1 (70 GB per stage at S=8); on one GPU use --layers 8,
     # the work of one of the 8 stages

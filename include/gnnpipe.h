@@ -123,7 +123,14 @@ enum {
     GP_BUF_HSNAP = 5,    /* h_snap[i]                               (N x out) */
     GP_BUF_IN = 6,       /* in_cur (stage input)                    (N x in0) */
     GP_BUF_DH_IN = 7,    /* dh_in  (gradient sent upstream)         (N x in0) */
-    GP_BUF_GATHER = 8    /* masked gather source of layer i         (N x in)  */
+    GP_BUF_GATHER = 8,   /* masked gather source of layer i         (N x in)  */
+    /* historical-embedding state the next epoch reads stale rows from (resume):
+     * h_snap[i] / in_snap / dagg_snap[i] after the snapshot rule of
+     * engines_impl.hpp:671-679 (readable with gp_download, restorable with
+     * gp_upload_history) */
+    GP_BUF_HIST_H = 9,   /* (N x out)  */
+    GP_BUF_HIST_IN = 10, /* (N x in0)  */
+    GP_BUF_HIST_DAGG = 11 /* (N x k_in), historical-gradient ablation */
 };
 
 /* ---- lifecycle ---------------------------------------------------------- */
@@ -223,6 +230,18 @@ gp_status gp_run_epoch(gp_ctx* ctx, uint32_t t, const uint32_t* order, gp_epoch_
 gp_status gp_download(gp_ctx* ctx, uint32_t which, uint32_t local_layer, float* out,
                       uint64_t count);
 gp_status gp_set_profiling(gp_ctx* ctx, int enable);
+/* Device bytes gp_create + the uploads would allocate for this stage (the stash
+ * layout under the current GP_LEAN / GP_MERGED_G switches, graph with nnz_norm
+ * normalised entries, features of width num_features on stage 0, labels on the
+ * last stage). Needs no device: a memory plan for configurations larger than the
+ * GPUs at hand (reference: peak_buffer_bytes, engines_impl.hpp:891-896). */
+gp_status gp_stage_footprint(const gp_stage_config* cfg, uint64_t nnz_norm, uint32_t num_features,
+                             uint64_t* bytes);
+/* Restore one history buffer (GP_BUF_HIST_*, original vertex order, N x width)
+ * before resuming at epoch resume_epoch + 1. Extension: the reference has no
+ * resume path (its checkpoints are parameters only, nn.hpp:497-531). */
+gp_status gp_upload_history(gp_ctx* ctx, uint32_t which, uint32_t local_layer, const float* rows,
+                            uint64_t count, uint32_t resume_epoch);
 
 /* Trace of a stage's epochs (replaces the simulated-clock trace of the fabric,
  * TraceEvent fabric.hpp, Fabric::trace fabric.cpp:256-264; collect_trace
@@ -361,6 +380,8 @@ int gs_save_stage_checkpoint(const char* path, const gs_model_config* m, uint32_
                              const float* flat, uint32_t lo, uint32_t hi);
 int gs_load_checkpoint(const char* path, char* names, uint64_t names_cap, uint64_t* shapes, float* data,
                        uint64_t* n_tensors, uint64_t* n_floats);
+/* Bytes gs_load_checkpoint's newline-separated names need (incl. the NUL). */
+int gs_checkpoint_names_bytes(const char* path, uint64_t* bytes);
 /* Measured trace (collect_trace runs): copies up to cap events, *count = total. */
 int gs_result_trace(const gs_result* r, gs_trace_event* out, uint64_t cap, uint64_t* count);
 /* Communication ledger: T x 6 tags x 2 link classes (EpochComm::by_tag_link). */

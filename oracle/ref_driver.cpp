@@ -259,8 +259,10 @@ void cmd_forward(const Args& a) {
     const uint32_t L = uint32_t(specs.size());
     const VertexId n = d.num_vertices();
     const bool needs_h0 = model_needs_h0(specs);
+    // full=0: only the loss, parameter gradients and per-layer checksums (full-size graphs)
+    const bool full = argu(a, "full", "1") != 0;
     Blob b(arg(a, "out"));
-    dump_params(b, "init_", params);
+    if (full) dump_params(b, "init_", params);
     std::vector<ForwardCache<float>> caches;
     std::vector<DropMask<float>> masks;
     for (uint32_t l = 0; l < L; ++l) {
@@ -268,14 +270,16 @@ void cmd_forward(const Args& a) {
         const MatF& src = l == 0 ? d.features : caches[l - 1].out;
         const MatF* h0 = needs_h0 && l > 0 ? &caches[0].out : nullptr;
         caches.push_back(layer_forward(specs[l], params[l], adj, src, h0, masks[l]));
-        b.mat("pre" + std::to_string(l), caches[l].pre);
-        b.mat("h" + std::to_string(l), caches[l].out);
+        if (full) {
+            b.mat("pre" + std::to_string(l), caches[l].pre);
+            b.mat("h" + std::to_string(l), caches[l].out);
+        }
     }
     // Loss head on the training rows, as train_sequential does.
     std::vector<uint8_t> train_mask = d.mask(Split::Train);
     auto loss = softmax_xent(caches[L - 1].out, d.labels, train_mask);
     b.f64("loss", {loss.loss});
-    b.mat("grad_logits", loss.grad_logits);
+    if (full) b.mat("grad_logits", loss.grad_logits);
     // Backward: reproduce train_sequential's loop (engines_impl.hpp:250-277),
     // dumping dz/dagg/grad_in per layer and param grads.
     std::vector<MatF> dz(L), dagg(L), dh(L);
@@ -306,14 +310,27 @@ void cmd_forward(const Args& a) {
     auto rows = std::vector<VertexId>(n);
     for (VertexId v = 0; v < n; ++v) rows[v] = v;
     for (uint32_t l = 0; l < L; ++l) {
-        b.mat("dz" + std::to_string(l), dz[l]);
-        if (l > 0) b.mat("dagg" + std::to_string(l), dagg[l]);
-        b.mat("dh" + std::to_string(l), dh[l]);
+        if (full) {
+            b.mat("dz" + std::to_string(l), dz[l]);
+            if (l > 0) b.mat("dagg" + std::to_string(l), dagg[l]);
+            b.mat("dh" + std::to_string(l), dh[l]);
+        } else {
+            // fp64 column sums of the activations and gradients (size-independent checks)
+            auto colsum = [](const MatF& m) {
+                std::vector<double> s(m.cols(), 0.0);
+                for (size_t r = 0; r < m.rows(); ++r)
+                    for (size_t c = 0; c < m.cols(); ++c) s[c] += double(m.at(r, c));
+                return s;
+            };
+            b.f64("sum_h" + std::to_string(l), colsum(caches[l].out));
+            b.f64("sum_pre" + std::to_string(l), colsum(caches[l].pre));
+            b.f64("sum_dz" + std::to_string(l), colsum(dz[l]));
+        }
         auto g = param_grads_for_rows(specs[l], rows, caches[l].pre, dz[l]);
         b.mat("gW" + std::to_string(l), g.weight);
         b.f32("gb" + std::to_string(l), g.bias);
     }
-    if (needs_h0) b.mat("dh0", dh0);
+    if (needs_h0 && full) b.mat("dh0", dh0);
 }
 
 void cmd_train(const Args& a) {

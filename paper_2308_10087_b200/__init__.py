@@ -22,7 +22,7 @@ import numpy as np
 __all__ = [
     "GP_OK", "GP_EINVAL", "GP_ENUMERIC", "GP_EFABRIC", "GP_ECUDA", "GP_ERUNTIME",
     "GnnsimError", "InvalidArgument", "NumericError", "FabricError", "GpuEngineError",
-    "LayerKind", "ModelKind", "ModelConfig", "TrainOptions", "TrainResult", "LayerSpec",
+    "LayerKind", "ModelKind", "stage_footprint", "ModelConfig", "TrainOptions", "TrainResult", "LayerSpec",
     "Dataset", "make_chunks", "partition_vertices", "shuffle_chunk_order", "make_stage_assignment",
     "build_layer_specs", "init_params", "train_pipeline", "train_sequential", "train_hybrid", "StageEngine",
     "nccl_unique_id", "device_count", "lib_paths", "PROFILE_CLASSES",
@@ -40,7 +40,8 @@ os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
 GP_OK, GP_EINVAL, GP_ENUMERIC, GP_EFABRIC, GP_ECUDA, GP_ERUNTIME = 0, 1, 2, 3, 4, 5
 PROFILE_CLASSES = ["remask", "fwd_agg", "fwd_dense", "bwd_agg", "bwd_dense", "xent", "pgrad", "optim", "xfer"]
 IPC_BLOB_BYTES = 256  # GP_IPC_BLOB_BYTES
-GP_BUF = {"h": 0, "pre": 1, "dz": 2, "dagg": 3, "dh0": 4, "hsnap": 5, "in": 6, "dh_in": 7, "gather": 8}
+GP_BUF = {"h": 0, "pre": 1, "dz": 2, "dagg": 3, "dh0": 4, "hsnap": 5, "in": 6, "dh_in": 7, "gather": 8,
+          "hist_h": 9, "hist_in": 10, "hist_dagg": 11}
 
 
 class GnnsimError(RuntimeError):
@@ -175,6 +176,7 @@ def _L():
         "gs_num_layers": (C.c_int, [P(gs_model_config), u32p]),
         "gs_build_layer_specs": (C.c_int, [P(gs_model_config), C.c_uint32, C.c_uint32, P(gp_layer_spec)]),
         "gs_init_params": (C.c_int, [P(gs_model_config), C.c_uint32, C.c_uint32, C.c_uint64, f32p]),
+        "gs_checkpoint_names_bytes": (C.c_int, [C.c_char_p, P(C.c_uint64)]),
         "gs_train_pipeline": (C.c_int, [vp, u32p, C.c_uint32, C.c_uint32, P(gs_train_options), P(vp)]),
         "gs_train_sequential": (C.c_int, [vp, P(gs_train_options), P(vp)]),
         "gs_train_hybrid": (C.c_int, [vp, u32p, u32p, C.c_uint32, C.c_uint32, P(gs_train_options), P(vp)]),
@@ -226,6 +228,8 @@ def _L():
         "gp_abort": (None, [vp]),
         "gp_run_epoch": (C.c_int, [vp, C.c_uint32, u32p, P(gp_epoch_stats)]),
         "gp_download": (C.c_int, [vp, C.c_uint32, C.c_uint32, f32p, C.c_uint64]),
+        "gp_upload_history": (C.c_int, [vp, C.c_uint32, C.c_uint32, f32p, C.c_uint64, C.c_uint32]),
+        "gp_stage_footprint": (C.c_int, [P(gp_stage_config), C.c_uint64, C.c_uint32, u64p]),
         "gp_set_profiling": (C.c_int, [vp, C.c_int]),
         "gp_get_profile": (C.c_int, [vp, P(gp_profile)]),
         "gp_reset_profile": (C.c_int, [vp]),
@@ -519,7 +523,9 @@ def load_checkpoint(path: str):
     _gs(lib.gs_load_checkpoint(path.encode(), None, 0, None, None, C.byref(nt), C.byref(nf)))
     shapes = np.zeros(2 * nt.value, np.uint64)
     data = np.zeros(nf.value, np.float32)
-    names = C.create_string_buffer(64 * nt.value + 64)
+    nb = C.c_uint64()
+    _gs(lib.gs_checkpoint_names_bytes(path.encode(), C.byref(nb)))
+    names = C.create_string_buffer(int(nb.value))
     _gs(lib.gs_load_checkpoint(path.encode(), names, len(names), _ptr(shapes, C.c_uint64), _ptr(data, C.c_float),
                                C.byref(nt), C.byref(nf)))
     out, at = [], 0
@@ -656,6 +662,50 @@ def nccl_unique_id() -> bytes:
     return bytes(buf)
 
 
+def _stage_config(specs_c, *, num_vertices, num_chunks, specs, stage, num_stages, layer_range, hidden,
+                  num_classes, dropout, seed, lr=1e-3, optimizer="adam", fix_alpha=10, historical_gradients=False,
+                  synchronous_mode=False, device=0, beta1=0.9, beta2=0.999, eps=1e-8, group_size=1, group_rank=0):
+    cfg = gp_stage_config()
+    cfg.device = device
+    cfg.num_vertices = num_vertices
+    cfg.num_chunks = num_chunks
+    cfg.num_stages = num_stages
+    cfg.stage = stage
+    cfg.layer_begin, cfg.layer_end = layer_range
+    cfg.num_layers = len(specs)
+    cfg.specs = specs_c
+    cfg.hidden = hidden
+    cfg.num_classes = num_classes
+    cfg.dropout = dropout
+    cfg.seed = seed
+    cfg.optimizer = 1 if optimizer == "sgd" else 0
+    cfg.lr, cfg.beta1, cfg.beta2, cfg.eps = lr, beta1, beta2, eps
+    cfg.fix_alpha = fix_alpha
+    cfg.historical_gradients = int(historical_gradients)
+    cfg.synchronous_mode = int(synchronous_mode)
+    cfg.group_size = group_size
+    cfg.group_rank = group_rank
+    return cfg
+
+
+def _specs_c(specs):
+    return (gp_layer_spec * len(specs))(*[gp_layer_spec(s.kind, s.in_dim, s.out_dim, int(s.relu), s.alpha, s.beta)
+                                          for s in specs])
+
+
+def stage_footprint(*, nnz_norm: int, num_features: int = 0, **stage_kw) -> int:
+    """Device bytes one stage (or hybrid worker) would allocate: gp_stage_footprint, the
+    engine's own stash layout pass plus graph / features / labels. Needs no GPU. Takes the
+    StageEngine keyword arguments (specs, num_vertices, num_chunks, stage, ...)."""
+    sc = _specs_c(stage_kw["specs"])
+    cfg = _stage_config(sc, **stage_kw)
+    out = C.c_uint64()
+    rc = _L().gp_stage_footprint(C.byref(cfg), nnz_norm, num_features, C.byref(out))
+    if rc != GP_OK:
+        raise _ERR.get(rc, GnnsimError)((_L().gp_last_error(None) or b"").decode())
+    return int(out.value)
+
+
 class StageEngine:
     """One pipeline stage on one GPU, driven directly through the gp_* C-ABI."""
 
@@ -666,8 +716,7 @@ class StageEngine:
                  beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8, group_size: int = 1,
                  group_rank: int = 0):
         self.specs = list(specs)
-        self._specs_c = (gp_layer_spec * len(specs))(*[
-            gp_layer_spec(s.kind, s.in_dim, s.out_dim, int(s.relu), s.alpha, s.beta) for s in specs])
+        self._specs_c = _specs_c(specs)
         cfg = gp_stage_config()
         cfg.device = device
         cfg.num_vertices = num_vertices

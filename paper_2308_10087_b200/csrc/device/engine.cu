@@ -295,7 +295,18 @@ struct Stage {
     // snapshot until its chunk rewrites it, so the forward gathers read a single
     // table (half the L2 footprint); the wavefront then also orders "chunk j+1
     // writes G_{i+1}" after "chunk j's layer i+1 gather" (wave_reads_done).
-    bool merged_g = false;
+    bool merged_g = true;
+    // GP_LEAN=1 (default): four N x H buffers per layer instead of seven. dz is written
+    // in place over the layer's output h (the backward reads h[v] only for its own
+    // ReLU mask, in the same lane, right before writing dz[v]); the backward gather
+    // table bg_i lives in the forward gather table G_i (dead once the stage's forward
+    // is complete, rebuilt at the next epoch start); snapshots are copies taken at
+    // the end of epoch t when epoch t+1 refreshes (engines_impl.hpp:671-679), since
+    // h no longer survives the backward. GP_LEAN=0 keeps h, dz, G and bg apart and
+    // snapshots by pointer swap (the round-1 layout; tests that read activations
+    // after an epoch use it).
+    bool lean = true;
+    bool state_restored = false;  // gp_set_history: the snapshot rows were loaded
     // forward wavefront hooks (merged_g): after the kernel gathering from G_i, and
     // before the kernel writing rows of G_i
     std::function<void(uint32_t)> on_gather_done, before_g_write;
@@ -423,6 +434,7 @@ struct Stage {
     }
 
     ~Stage() {
+        if (plan_only) return;  // gp_stage_footprint: nothing was created
         if (device >= 0) cudaSetDevice(device);
         if (tr.ipc_up.linked() || tr.ipc_down.linked() || tr.ipcg.linked) {
             // a dead peer leaves in-stream waits pending: bounded wait, then leak
@@ -527,6 +539,9 @@ struct Stage {
                 throw Error(GP_EINVAL, "Gcn2Conv needs in_dim == out_dim");
         }
         if (needs_h0 && (H == 0 || H > kMaxWidth)) throw Error(GP_EINVAL, "bad hidden width");
+        if (const char* e = std::getenv("GP_MERGED_G")) merged_g = std::atoi(e) != 0;
+        if (const char* e = std::getenv("GP_LEAN")) lean = std::atoi(e) != 0;
+        if (plan_only) return;
         device = c.device;
         int ndev = 0;
         if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
@@ -536,12 +551,37 @@ struct Stage {
         GP_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, device));
         GP_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
         if (const char* e = std::getenv("GP_WAVE")) wave_w = std::max(1, std::min(kMaxWave, std::atoi(e)));
-        if (const char* e = std::getenv("GP_MERGED_G")) merged_g = std::atoi(e) != 0;
         for (int w = 1; w < wave_w; ++w) GP_CUDA(cudaStreamCreateWithFlags(&cs_side[w], cudaStreamNonBlocking));
         GP_CUDA(cudaEventCreate(&ev_start));
         GP_CUDA(cudaEventCreate(&ev_end));
         alloc();
         setup_kernels();
+    }
+
+    // Device footprint of this configuration without a device: the stash layout pass
+    // (alloc_layout in sizing mode) plus the graph, features and labels the uploads
+    // allocate (CSR: u64 row pointers + 8-byte packed entries; SageConv mean CSRs).
+    bool plan_only = false;
+    uint64_t plan_bytes(const gp_stage_config& c, uint64_t nnz_norm, uint32_t F_in) {
+        plan_only = true;
+        init(c);
+        arena_sizing = true;
+        arena_need = 0;
+        alloc_layout();
+        arena_sizing = false;
+        uint64_t b = arena_need;
+        auto add = [&](uint64_t bytes) { b += (std::max<uint64_t>(bytes, 16) + 255) & ~uint64_t(255); };
+        add(8ull * (n + 1));                                  // rowptr
+        add(8ull * nnz_norm);                                 // packed {col | chunk, weight}
+        add(4ull * n);                                        // new -> original id
+        if (has_sage) {
+            const uint64_t nnz_m = nnz_norm >= n ? nnz_norm - n : nnz_norm;  // no self loops
+            add(8ull * (n + 1));
+            add(2 * 8ull * nnz_m);
+        }
+        if (first) add(4ull * n * pad8(F_in ? F_in : specs[0].in_dim));  // x0
+        if (last) add(5ull * n);                              // labels + split
+        return b;
     }
 
     void alloc() {
@@ -598,7 +638,7 @@ struct Stage {
             }
             d.h = dalloc<float>(size_t(n) * d.sout);
             d.pre = dalloc<float>(size_t(n) * d.skw);
-            d.dz = dalloc<float>(size_t(n) * d.sout);
+            d.dz = lean ? d.h : dalloc<float>(size_t(n) * d.sout);
             // gather tables carry one extra all-zero row (row n, see gather_row)
             if (d.agg) {
                 d.G = dalloc<float>(size_t(n + 1) * d.sin);
@@ -608,7 +648,10 @@ struct Stage {
             if (!sync && i + 1 < len && specs[lb + i + 1].kind != GP_DENSE)
                 d.hs = dalloc<float>(size_t(n) * d.sout);
             if (d.l > 0) {
-                d.bg = dalloc<float>(size_t(n + 1) * d.skw);
+                // lean: bg_i in G_i's rows (same width for non-SageConv layers; the
+                // historical-gradient ablation swaps bg with its snapshot, so it keeps its own)
+                d.bg = lean && d.agg && !d.sage && !hist && d.skw == d.sin ? d.G
+                                                                        : dalloc<float>(size_t(n + 1) * d.skw);
                 if (hist && d.agg) d.bgs = dalloc<float>(size_t(n + 1) * d.skw);
             }
         }
@@ -619,7 +662,9 @@ struct Stage {
             if (needs_h0) h0 = dalloc<float>(size_t(n) * pad8(H));
         }
         if (needs_h0) dh0 = dalloc<float>(size_t(n) * pad8(H));
-        dtop = dalloc<float>(size_t(n) * L[len - 1].sout);
+        // lean: a chunk's incoming gradient (dtop, read first in its backward) and its
+        // outgoing one (dh_in, written last) share rows when their strides agree
+        dtop = lean && dh_in && L[len - 1].sout == sin0 ? dh_in : dalloc<float>(size_t(n) * L[len - 1].sout);
         // pgrad workspace: ~2 waves of CTAs
         splits = std::max<uint32_t>(1, std::min<uint32_t>(2 * num_sms, (n + 63) / 64));
         size_t wmax = 1;
@@ -632,7 +677,7 @@ struct Stage {
         red_loss = dalloc<double>(1);
         red_correct = dalloc<unsigned long long>(3);
         tickets = dalloc<uint32_t>(kTickets);
-        GP_CUDA(cudaDeviceSynchronize());
+        if (!arena_sizing) GP_CUDA(cudaDeviceSynchronize());
     }
 
     // Work counters of the dynamically scheduled row kernels (one per launch).
@@ -2485,6 +2530,22 @@ struct Stage {
         }
     }
 
+    // Lean layout: snap := cur for every stash the next epoch reads stale rows from
+    // (all n rows: hybrid halo rows pulled into cur are part of the snapshot, like the
+    // reference's whole-matrix copy). backward = true: the historical dagg tables.
+    void copy_snapshots(bool backward) {
+        auto copy = [&](float* dst, const float* src, size_t floats) {
+            if (!dst || !src || dst == src) return;
+            GP_CUDA(cudaMemcpyAsync(dst, src, floats * 4, cudaMemcpyDeviceToDevice, cs));
+        };
+        if (backward) {
+            for (auto& d : L) copy(d.bgs, d.bg, size_t(n) * d.skw);
+            return;
+        }
+        copy(in_snap, in_cur, size_t(n) * sin0);
+        for (auto& d : L) copy(d.hs, d.h, size_t(n) * d.sout);
+    }
+
     void run_epoch(uint32_t t, const uint32_t* order, gp_epoch_stats* out) {
         GP_CUDA(cudaSetDevice(device));
         if (!graph_ready) throw Error(GP_EINVAL, "graph not uploaded");
@@ -2512,12 +2573,20 @@ struct Stage {
         // rewritten before it is read again, so a pointer swap is exact.
         const uint32_t fix_alpha = std::max<uint32_t>(1, cfg.fix_alpha);
         if (!sync && (t - 1) % fix_alpha == 0) {
-            if (in_snap) std::swap(in_snap, in_cur);
-            for (auto& d : L) {
-                if (d.hs) std::swap(d.hs, d.h);
-                if (d.bgs) std::swap(d.bgs, d.bg);
+            if (!lean) {
+                if (in_snap) std::swap(in_snap, in_cur);
+                for (auto& d : L) {
+                    if (d.hs) std::swap(d.hs, d.h);
+                    if (d.bgs) std::swap(d.bgs, d.bg);
+                }
+            } else if (!(t == 1 && last_epoch == 0) && last_epoch != t - 1 && !state_restored) {
+                // lean snapshots are copied at the end of epoch t-1 (copy_snapshots)
+                throw Error(GP_EINVAL, "lean stash layout: epoch " + std::to_string(t) +
+                                           " refreshes the snapshot but epoch " + std::to_string(t - 1) +
+                                           " did not run here (restore it with gp_set_history, or GP_LEAN=0)");
             }
         }
+        state_restored = false;
         // Masked gather sources start from the snapshot rows (stale reads).
         for (uint32_t i = 0; i < len; ++i) {
             if (!L[i].agg) continue;
@@ -2601,6 +2670,10 @@ struct Stage {
             if (!last)
                 for (uint32_t kk = 0; kk < K; ++kk) traced_send(ord[kk], [&]() { send_fwd(ord[kk]); });
         }
+
+        // lean layout: the next epoch's snapshot (snap := cur at t+1) is taken now, before
+        // the backward overwrites h with dz
+        if (lean && !sync && t % fix_alpha == 0) copy_snapshots(false);
 
         // ---- metrics (last stage) ---------------------------------------------------
         if (last) {
@@ -2686,6 +2759,7 @@ struct Stage {
                 for (uint32_t kk = K; kk-- > 0;) traced_send(ord[kk], [&]() { send_bwd(ord[kk]); });
         }
 
+        if (lean && hist && t % fix_alpha == 0) copy_snapshots(true);
         {
             cudaEvent_t c0 = trace_mark();
             param_step();
@@ -2736,6 +2810,51 @@ struct Stage {
         if (out) *out = st;
     }
 
+    // ---- historical-embedding state (resume) -------------------------------------
+    // The rows the next epoch reads stale values from: h_snap / in_snap / dagg_snap
+    // after epoch last_epoch's snapshot rule (engines_impl.hpp:671-679). Lean layout:
+    // the snapshot buffer itself (copies are taken at the end of the epoch). Swap
+    // layout: the current buffer when the next epoch refreshes, else the snapshot.
+    struct HistBuf {
+        float *next, *snap, *cur;
+        uint32_t width, stride;
+    };
+    HistBuf history(uint32_t which, uint32_t i) {
+        if (sync) throw Error(GP_EINVAL, "synchronous mode keeps no historical embeddings");
+        const uint32_t fix_alpha = std::max<uint32_t>(1, cfg.fix_alpha);
+        const bool refresh_next = last_epoch % fix_alpha == 0;
+        HistBuf b{};
+        if (which == GP_BUF_HIST_IN) {
+            b = {nullptr, in_snap, in_cur, in0, sin0};
+        } else {
+            if (i >= len) throw Error(GP_EINVAL, "local layer out of range");
+            auto& d = L[i];
+            if (which == GP_BUF_HIST_H) b = {nullptr, d.hs, d.h, d.dout, d.sout};
+            else b = {nullptr, d.bgs, d.bg, d.kw, d.skw};  // SageConv: both (gapped) halves
+        }
+        if (!b.snap) throw Error(GP_EINVAL, "no historical rows for this buffer on this stage");
+        b.next = lean || !refresh_next ? b.snap : b.cur;
+        return b;
+    }
+
+    // Restore the historical rows (original vertex order, N x width) before resuming
+    // at epoch last_epoch + 1 = t: the next run_epoch reads them as the snapshot.
+    void upload_history(uint32_t which, uint32_t i, const float* in, uint64_t count, uint32_t resume_epoch) {
+        GP_CUDA(cudaSetDevice(device));
+        if (!graph_ready) throw Error(GP_EINVAL, "graph not uploaded");
+        if (which != GP_BUF_HIST_H && which != GP_BUF_HIST_IN && which != GP_BUF_HIST_DAGG)
+            throw Error(GP_EINVAL, "gp_upload_history: not a history buffer");
+        last_epoch = resume_epoch;
+        const HistBuf hb = history(which, i);
+        if (count != uint64_t(n) * hb.width) throw Error(GP_EINVAL, "count != N * width");
+        std::vector<float> tmp(size_t(n) * hb.stride, 0.f);
+        for (uint32_t r = 0; r < n; ++r) std::memcpy(&tmp[size_t(r) * hb.stride], in + size_t(inv[r]) * hb.width, size_t(hb.width) * 4);
+        // swap layout: both halves, so whichever the next epoch's rule picks holds them
+        for (float* dst : {hb.snap, lean ? nullptr : hb.cur})
+            if (dst) GP_CUDA(cudaMemcpy(dst, tmp.data(), tmp.size() * 4, cudaMemcpyHostToDevice));
+        state_restored = true;
+    }
+
     void download(uint32_t which, uint32_t i, float* out, uint64_t count) {
         GP_CUDA(cudaSetDevice(device));
         GP_CUDA(cudaStreamSynchronize(cs));
@@ -2747,15 +2866,32 @@ struct Stage {
             return L[i];
         };
         switch (which) {
-            case GP_BUF_H: { auto& d = need_layer(); src = d.h; width = d.dout; stride = d.sout; break; }
+            case GP_BUF_H: {
+                auto& d = need_layer();
+                if (lean && last_epoch) throw Error(GP_EINVAL, "lean stash layout: h holds dz after the backward (GP_LEAN=0 keeps activations)");
+                src = d.h; width = d.dout; stride = d.sout; break;
+            }
             case GP_BUF_PRE: { auto& d = need_layer(); src = d.pre; width = d.din; stride = d.skw; gap = d.sgap; break; }
             case GP_BUF_DZ: { auto& d = need_layer(); src = d.dz; width = d.dout; stride = d.sout; break; }
             case GP_BUF_DAGG: { auto& d = need_layer(); src = d.bg; width = d.din; stride = d.skw; gap = d.sgap; break; }
             case GP_BUF_HSNAP: { auto& d = need_layer(); src = d.hs; width = d.dout; stride = d.sout; break; }
-            case GP_BUF_GATHER: { auto& d = need_layer(); src = d.G; width = d.din; stride = d.sin; break; }
+            case GP_BUF_GATHER: {
+                auto& d = need_layer();
+                if (lean && last_epoch && d.bg == d.G) throw Error(GP_EINVAL, "lean stash layout: the gather table holds dagg after the backward (GP_LEAN=0)");
+                src = d.G; width = d.din; stride = d.sin; break;
+            }
             case GP_BUF_DH0: src = dh0; width = H; stride = pad8(H); break;
             case GP_BUF_IN: src = in_cur; width = in0; stride = sin0; break;
             case GP_BUF_DH_IN: src = dh_in; width = in0; stride = sin0; break;
+            case GP_BUF_HIST_H:
+            case GP_BUF_HIST_IN:
+            case GP_BUF_HIST_DAGG: {
+                const HistBuf hb = history(which, i);
+                src = hb.next;
+                width = hb.width;
+                stride = hb.stride;
+                break;
+            }
             default: throw Error(GP_EINVAL, "unknown buffer");
         }
         if (!src) throw Error(GP_EINVAL, "buffer not allocated on this stage");
@@ -3001,6 +3137,18 @@ gp_status gp_run_epoch(gp_ctx* ctx, uint32_t t, const uint32_t* order, gp_epoch_
 
 gp_status gp_download(gp_ctx* ctx, uint32_t which, uint32_t local_layer, float* out, uint64_t count) {
     return gp::guard(&ctx->st, [&]() { ctx->st.download(which, local_layer, out, count); });
+}
+
+gp_status gp_stage_footprint(const gp_stage_config* cfg, uint64_t nnz_norm, uint32_t num_features, uint64_t* bytes) {
+    if (!cfg || !bytes) return GP_EINVAL;
+    gp::Stage st;
+    return gp::guard(nullptr, [&]() { *bytes = st.plan_bytes(*cfg, nnz_norm, num_features); });
+}
+
+gp_status gp_upload_history(gp_ctx* ctx, uint32_t which, uint32_t local_layer, const float* rows, uint64_t count,
+                            uint32_t resume_epoch) {
+    if (!ctx || !rows) return GP_EINVAL;
+    return gp::guard(&ctx->st, [&]() { ctx->st.upload_history(which, local_layer, rows, count, resume_epoch); });
 }
 
 gp_status gp_set_profiling(gp_ctx* ctx, int enable) {

@@ -86,6 +86,7 @@ TrainOptions<float> options_of(const gs_train_options* o) {
 // options + the resume state named by o->resume_path (shapes from the dataset)
 TrainOptions<float> options_for(const gs_train_options* o, const Dataset& d) {
     TrainOptions<float> t = options_of(o);
+    t.keep_history = o->save_state_path && *o->save_state_path;  // a saved state resumes exactly
     if (o->resume_path && *o->resume_path)
         t.resume = std::make_shared<TrainState>(
             load_train_state(o->resume_path, build_layer_specs(t.model, d.num_features(), d.num_classes)));
@@ -523,10 +524,21 @@ int gs_load_checkpoint(const char* path, char* names, uint64_t names_cap, uint64
         if (n_tensors) *n_tensors = ts.size();
         if (n_floats) *n_floats = floats;
         if (names && names_cap) {
-            const size_t k = std::min<size_t>(names_cap - 1, all.size());
-            std::memcpy(names, all.data(), k);
-            names[k] = 0;
+            if (all.size() + 1 > names_cap)
+                throw std::invalid_argument("gs_load_checkpoint: names buffer needs " + std::to_string(all.size() + 1) +
+                                            " bytes (gs_checkpoint_names_bytes)");
+            std::memcpy(names, all.data(), all.size());
+            names[all.size()] = 0;
         }
+    });
+}
+
+int gs_checkpoint_names_bytes(const char* path, uint64_t* bytes) {
+    return guarded([&]() {
+        if (!path || !bytes) throw std::invalid_argument("null argument");
+        uint64_t b = 1;
+        for (const auto& t : load_checkpoint(path)) b += t.name.size() + 1;
+        *bytes = b;
     });
 }
 

@@ -3,6 +3,7 @@
 // written exactly as the reference's JSON library dumps it (compact, keys in
 // sorted order), so files are byte-compatible in both directions.
 #include <cctype>
+#include <cstdio>
 #include <cstring>
 #include <fstream>
 #include <map>
@@ -20,6 +21,10 @@ std::string json_escape(const std::string& s) {
         if (c == '"' || c == '\\') {
             o += '\\';
             o += c;
+        } else if (c == '\b' || c == '\f' || c == '\n' || c == '\r' || c == '\t') {
+            // nlohmann::json dump: the short escapes for these five, \u00XX for the rest
+            o += '\\';
+            o += c == '\b' ? 'b' : c == '\f' ? 'f' : c == '\n' ? 'n' : c == '\r' ? 'r' : 't';
         } else if (static_cast<unsigned char>(c) < 0x20) {
             char buf[8];
             std::snprintf(buf, sizeof buf, "\\u%04x", unsigned(static_cast<unsigned char>(c)));
@@ -57,10 +62,37 @@ struct HeaderReader {
                 if (++i >= s.size()) fail();
                 if (s[i] == 'u') {
                     if (i + 4 >= s.size()) fail();
-                    o += char(std::stoul(s.substr(i + 1, 4), nullptr, 16));
+                    uint32_t cp = uint32_t(std::stoul(s.substr(i + 1, 4), nullptr, 16));
                     i += 5;
+                    // surrogate pair -> one code point; then UTF-8 (as nlohmann parses it)
+                    if (cp >= 0xD800 && cp < 0xDC00 && i + 5 < s.size() && s[i] == '\\' && s[i + 1] == 'u') {
+                        const uint32_t lo = uint32_t(std::stoul(s.substr(i + 2, 4), nullptr, 16));
+                        if (lo >= 0xDC00 && lo < 0xE000) {
+                            cp = 0x10000 + ((cp - 0xD800) << 10) + (lo - 0xDC00);
+                            i += 6;
+                        }
+                    }
+                    if (cp < 0x80) {
+                        o += char(cp);
+                    } else if (cp < 0x800) {
+                        o += char(0xC0 | (cp >> 6));
+                        o += char(0x80 | (cp & 0x3F));
+                    } else if (cp < 0x10000) {
+                        o += char(0xE0 | (cp >> 12));
+                        o += char(0x80 | ((cp >> 6) & 0x3F));
+                        o += char(0x80 | (cp & 0x3F));
+                    } else {
+                        o += char(0xF0 | (cp >> 18));
+                        o += char(0x80 | ((cp >> 12) & 0x3F));
+                        o += char(0x80 | ((cp >> 6) & 0x3F));
+                        o += char(0x80 | (cp & 0x3F));
+                    }
                     continue;
                 }
+                const char e = s[i];
+                o += e == 'b' ? '\b' : e == 'f' ? '\f' : e == 'n' ? '\n' : e == 'r' ? '\r' : e == 't' ? '\t' : e;
+                ++i;
+                continue;
             }
             o += s[i++];
         }
@@ -180,6 +212,12 @@ void save_train_state(const std::string& path, const TrainState& st) {
             }
         }
     }
+    for (const auto& h : st.history) {
+        names.push_back("history.w" + std::to_string(h.worker) + ".k" + std::to_string(h.which) + ".l" +
+                        std::to_string(h.layer));
+        data.push_back(h.rows.data());
+        shapes.push_back({h.width ? h.rows.size() / h.width : 0, h.width});
+    }
     save_checkpoint(path, names, data, shapes);
 }
 
@@ -209,6 +247,19 @@ TrainState load_train_state(const std::string& path, const std::vector<LayerSpec
             if (specs[l].has_bias()) p.bias = take(n + ".bias" + sfx, 1, o);
             (which == 0 ? st.params : (which == 1 ? st.adam_m : st.adam_v)).push_back(std::move(p));
         }
+    }
+    for (auto& [name, t] : by) {  // history.wW.kK.lL (sorted by name: a stable order)
+        unsigned w = 0, k = 0, l = 0;
+        if (name.rfind("history.", 0) != 0) continue;
+        if (std::sscanf(name.c_str(), "history.w%u.k%u.l%u", &w, &k, &l) != 3)
+            throw std::invalid_argument("train state " + path + ": bad history tensor name " + name);
+        TrainState::HistoryRows h;
+        h.worker = w;
+        h.which = k;
+        h.layer = l;
+        h.width = uint32_t(t.cols);
+        h.rows = std::move(t.data);
+        st.history.push_back(std::move(h));
     }
     return st;
 }

@@ -155,6 +155,10 @@ TrainResult<float> run_hybrid_f32(const Dataset& ds, const Partition* part, cons
                     p->bias.size() != (specs[l].has_bias() ? specs[l].out_dim : 0u))
                     throw std::invalid_argument("resume: layer " + std::to_string(l) + " has the wrong shape");
         params = rs.params;
+        if (!opt.staleness.synchronous_mode && rs.epoch > 0 && rs.history.empty())
+            throw std::invalid_argument(
+                "resume: stale-mode training reads historical embeddings the state does not hold "
+                "(save it with TrainOptions::keep_history, or resume in synchronous mode)");
     }
     timer.mark("init_params");
 
@@ -217,6 +221,12 @@ TrainResult<float> run_hybrid_f32(const Dataset& ds, const Partition* part, cons
                                              v.bias.empty() ? nullptr : v.bias.data(), opt.resume->optimizer_step),
                       g, "gp_set_optimizer_state");
             }
+        if (opt.resume && !opt.staleness.synchronous_mode)
+            for (const auto& h : opt.resume->history)
+                if (h.worker == w) {
+                    const uint32_t li = h.which == GP_BUF_HIST_IN ? 0 : h.layer - sa.begin(s);
+                    check(gp_upload_history(g, h.which, li, h.rows.data(), h.rows.size(), t0), g, "gp_upload_history");
+                }
         if (opt.profile) gp_set_profiling(g, 1);
         if (opt.fabric.collect_trace) gp_set_trace(g, 1);
         if (s > 0) check(gp_link_local(ctx.v[w - G], g), g, "gp_link_local");  // same rank, previous stage
@@ -238,6 +248,10 @@ TrainResult<float> run_hybrid_f32(const Dataset& ds, const Partition* part, cons
                 for (uint32_t k = 0; k < K; ++k) order[k] = k;
                 if (opt.staleness.shuffle_chunks) order = shuffle_chunk_order(plan, t, opt.seed);
                 check(gp_run_epoch(ctx.v[w], t, order.data(), &stats[w][t - t0 - 1]), ctx.v[w], "gp_run_epoch");
+                // fill_quality_metrics (engines_impl.hpp:164-171) throws inside the epoch that
+                // produced a non-finite loss; a partial sum over this rank's rows suffices
+                if (stats[w][t - t0 - 1].has_quality && !std::isfinite(stats[w][t - t0 - 1].loss_sum))
+                    throw NumericError("non-finite training loss at epoch " + std::to_string(t));
             }
         } catch (...) {
             errs[w] = std::current_exception();
@@ -330,7 +344,7 @@ TrainResult<float> run_hybrid_f32(const Dataset& ds, const Partition* part, cons
             for (int i = 0; i < 3; ++i) cor[i] += q.correct[i];
         }
         m.train_loss = split_count[0] ? loss / double(split_count[0]) : 0.0;  // :164-171
-        if (!std::isfinite(m.train_loss)) throw NumericError("non-finite training loss at epoch " + std::to_string(t + 1));
+        if (!std::isfinite(m.train_loss)) throw NumericError("non-finite training loss at epoch " + std::to_string(m.epoch));
         m.train_acc = split_count[0] ? double(cor[0]) / double(split_count[0]) : 0.0;
         m.val_acc = split_count[1] ? double(cor[1]) / double(split_count[1]) : 0.0;
         m.test_acc = split_count[2] ? double(cor[2]) / double(split_count[2]) : 0.0;
@@ -376,6 +390,32 @@ TrainResult<float> run_hybrid_f32(const Dataset& ds, const Partition* part, cons
                                          V.bias.empty() ? nullptr : V.bias.data(), &step),
                   g, "gp_get_optimizer_state");
             res.final_state.optimizer_step = step;
+        }
+    }
+    if (opt.keep_history && !opt.staleness.synchronous_mode) {
+        const bool hist = opt.staleness.historical_gradients;
+        auto fetch = [&](uint32_t w, uint32_t which, uint32_t layer, uint32_t li, uint32_t width) {
+            TrainState::HistoryRows h;
+            h.worker = w;
+            h.which = which;
+            h.layer = layer;
+            h.width = width;
+            h.rows.resize(size_t(n) * width);
+            check(gp_download(ctx.v[w], which, li, h.rows.data(), h.rows.size()), ctx.v[w], "gp_download(history)");
+            res.final_state.history.push_back(std::move(h));
+        };
+        for (uint32_t w = 0; w < W; ++w) {
+            const uint32_t s = w / G, lb = sa.begin(s), le = sa.end(s);
+            if (s > 0 && specs[lb].kind != LayerKind::Dense) fetch(w, GP_BUF_HIST_IN, lb, 0, specs[lb].in_dim);
+            for (uint32_t l = lb; l < le; ++l) {
+                if (l + 1 < le && specs[l + 1].kind != LayerKind::Dense)
+                    fetch(w, GP_BUF_HIST_H, l, l - lb, specs[l].out_dim);
+                if (hist && l > 0 && specs[l].kind != LayerKind::Dense) {
+                    const uint32_t din = specs[l].in_dim;
+                    fetch(w, GP_BUF_HIST_DAGG, l, l - lb,
+                          specs[l].kind == LayerKind::SageConv ? ((din + 7u) & ~7u) + din : din);
+                }
+            }
         }
     }
     res.worker_params.resize(W);

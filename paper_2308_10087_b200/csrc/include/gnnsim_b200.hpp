@@ -330,13 +330,22 @@ struct WorkerParams {
 // Resumable training state (extension: the reference's checkpoints are
 // parameters only and there is no resume path). epoch = last completed epoch;
 // adam_m / adam_v mirror params (Optimizer m_/v_, nn.hpp:431-495).
+// history: the historical-embedding rows the next epoch reads stale values from
+// (h_snap / in_snap / dagg_snap after the snapshot rule, engines_impl.hpp:671-679),
+// one entry per worker and buffer, original vertex order; empty in synchronous mode.
 struct TrainState {
     uint32_t epoch = 0;
     uint64_t optimizer_step = 0;
     std::vector<LayerParams<float>> params, adam_m, adam_v;
+    struct HistoryRows {
+        uint32_t worker = 0, which = 0, layer = 0, width = 0;  // which: GP_BUF_HIST_*; layer: global
+        std::vector<float> rows;                                // N x width
+    };
+    std::vector<HistoryRows> history;
 };
 // Stored in the checkpoint format: layerL.weight/.bias (as save_stage_checkpoint),
-// layerL.{weight,bias}.adam_{m,v}, and train.state = [epoch, optimizer_step].
+// layerL.{weight,bias}.adam_{m,v}, train.state = [epoch, optimizer_step], and
+// history.wW.kK.lL (N x width) for each history entry.
 void save_train_state(const std::string& path, const TrainState& st);
 TrainState load_train_state(const std::string& path, const std::vector<LayerSpec>& specs);
 
@@ -362,11 +371,14 @@ struct TrainOptions {
     FabricOptions fabric;
     int device = 0;        // first CUDA device (stages round-robin over visible GPUs)
     bool profile = false;  // per-kernel device timing
-    // Continue from a saved state: parameters and optimizer moments are restored
-    // and epochs run from resume->epoch + 1 (dropout keys, chunk order and the
-    // snapshot schedule continue). The historical-embedding stashes restart empty,
-    // so a resumed run equals an uninterrupted one exactly in synchronous mode.
+    // Continue from a saved state: parameters, optimizer moments and (stale mode) the
+    // historical-embedding rows are restored and epochs run from resume->epoch + 1
+    // (dropout keys, chunk order and the snapshot schedule continue), so a resumed run
+    // equals an uninterrupted one. Stale-mode resume without history is rejected.
     std::shared_ptr<const TrainState> resume;
+    // Put the historical-embedding rows into final_state.history (N x H per stashed
+    // layer and worker, read back from the device after the last epoch).
+    bool keep_history = false;
 };
 
 template <typename T>

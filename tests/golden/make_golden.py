@@ -19,6 +19,27 @@ from oracle.blob import run_ref  # noqa: E402
 ER500 = "er:500:0.02:3:16:5:9"
 ER300W = "er:300:0.03:11:40:7:2"  # F=40 > nothing special; used for GCN first layer width != H
 
+# BASELINE.json configs at their own shapes (bench.py WORKLOADS; p = directed entries / (N (N-1)))
+CFG0 = "er:4096:" + repr(65536 / (4096 * 4095)) + ":1:128:16:1"
+CFG1 = "er:169343:" + repr(2332486 / (169343 * 169342)) + ":1:128:40:1"
+CFG2 = "er:232965:" + repr(114615892 / (232965 * 232964)) + ":1:602:41:1"
+BIG = {  # full-size scenarios: chunk_of is stored as its sha256, the forward dump is compact
+    # configs[0] exactly: ER-4K, F=H=128, C=16, 8-layer GCN, K=4, S=1, 20 epochs
+    "cfg0_er4k_gcn8_s1k4_20ep": ("train", dict(spec=CFG0, model="gcn", layers=8, hidden=128, S=1, K=4, chunk_seed=1,
+                                               epochs=20, seed=1)),
+    # configs[1] at the real ogbn-arxiv shape: 16-layer GCN, 2 stages x 8 chunks and 4 x 16
+    "cfg1_arxiv_gcn16_s2k8_3ep": ("train", dict(spec=CFG1, model="gcn", layers=16, hidden=128, S=2, K=8,
+                                                chunk_seed=1, epochs=3, seed=1, fabric="conc")),
+    "cfg1_arxiv_gcn16_s4k16_3ep": ("train", dict(spec=CFG1, model="gcn", layers=16, hidden=128, S=4, K=16,
+                                                 chunk_seed=1, epochs=3, seed=1, fabric="conc")),
+    # configs[2] at the full Reddit shape with 4 layers (Dense 602->100, 2 Gcn2Conv, Dense 100->41):
+    # whole-graph epoch-1 loss and every parameter gradient; 2 pipeline epochs at K=4 (params after Adam)
+    "cfg2_reddit_gcnii4_forward": ("forward", dict(spec=CFG2, model="gcnii", layers=4, hidden=100, seed=1, epoch=1,
+                                                   full=0)),
+    "cfg2_reddit_gcnii4_s1k4_2ep": ("train", dict(spec=CFG2, model="gcnii", layers=4, hidden=100, S=1, K=4,
+                                                  chunk_seed=1, epochs=2, seed=1)),
+}
+
 SCENARIOS = {
     # name: (cmd, kwargs)
     "graph_er500": ("graph", dict(spec=ER500)),
@@ -140,10 +161,34 @@ def golden_checkpoints(td):
     print("checkpoints", sorted(out))
 
 
+def make_big(name, td):
+    import hashlib
+    cmd, kw = BIG[name]
+    d = run_ref(cmd, os.path.join(td, name + ".blob"), timeout=7200, **kw)
+    if "chunk_of" in d:
+        d["chunk_of_sha256"] = np.array(hashlib.sha256(d.pop("chunk_of").astype("<u4").tobytes()).hexdigest())
+    meta = {"cmd": cmd, **{k: str(v) for k, v in kw.items()}}
+    np.savez_compressed(os.path.join(HERE, name + ".npz"), __meta__=np.array(repr(meta)), **d)
+    print(name, sorted(d)[:6], "...")
+
+
 def main():
+    names = sys.argv[1:]
     with tempfile.TemporaryDirectory() as td:
+        if names:  # only the named scenarios (the full-size ones take minutes each on one core)
+            for n in names:
+                if n in BIG:
+                    make_big(n, td)
+                else:
+                    cmd, kw = SCENARIOS[n]
+                    d = run_ref(cmd, os.path.join(td, n + ".blob"), **kw)
+                    np.savez_compressed(os.path.join(HERE, n + ".npz"),
+                                        __meta__=np.array(repr({"cmd": cmd, **{k: str(v) for k, v in kw.items()}})), **d)
+            return
         golden_analytics(td)
         golden_checkpoints(td)
+        for name in BIG:
+            make_big(name, td)
         for name, (cmd, kw) in SCENARIOS.items():
             d = run_ref(cmd, os.path.join(td, name + ".blob"), **kw)
             meta = {"cmd": cmd, **{k: str(v) for k, v in kw.items()}}

@@ -49,3 +49,20 @@ def test_truncated_checkpoint_raises(gold, tmp_path):
     gold["ckpt_gcnii"][:-5].tofile(path)
     with pytest.raises(gp.GnnsimError):
         gp.load_checkpoint(path)
+
+
+def test_header_escapes_decode_like_the_reference(gp, tmp_path):
+    """The header is JSON (nlohmann::json, nn.cpp:104-124): short escapes (\\t, \\b, ...) and
+    \\uXXXX code points, incl. surrogate pairs, decode to the same UTF-8 names."""
+    import json
+    import struct
+
+    import numpy as np
+    names = ["tab\there", "café", "smile\U0001F600", "bs\bff\f"]
+    header = json.dumps({"tensors": [{"cols": 1, "name": n, "rows": 1} for n in names]},
+                        separators=(",", ":"), ensure_ascii=True).encode()
+    p = tmp_path / "esc.ckpt"
+    p.write_bytes(struct.pack("<Q", len(header)) + header + np.arange(4, dtype=np.float32).tobytes())
+    got = gp.load_checkpoint(str(p))
+    assert [n for n, _ in got] == names
+    assert [float(a[0, 0]) for _, a in got] == [0.0, 1.0, 2.0, 3.0]

@@ -1,0 +1,137 @@
+"""Parity at the BASELINE.json configurations themselves (not miniatures), against fixtures the
+unmodified reference wrote (tests/golden/make_golden.py, BIG scenarios; oracle/_ref/ref_driver):
+
+  * configs[0] exactly: ER-4K (avg degree 16), F = H = 128, C = 16, 8-layer GCN, K = 4, S = 1,
+    a 20-epoch loss curve and the final parameters (train_pipeline<float>, engines_impl.hpp:911-920);
+  * configs[1] at the real ogbn-arxiv shape (169,343 vertices, 2.33 M directed edges), 16-layer
+    GCN, 2 stages x 8 chunks and 4 stages x 16 chunks, 3 epochs: losses, ledger, parameters;
+  * configs[2] at the full Reddit shape (232,965 vertices, 114.6 M directed edges, F = 602) with a
+    4-layer GCNII: the whole-graph epoch-1 loss, every layer's parameter gradient, the
+    parameters after the first Adam step, per-column checksums of every activation and dz;
+    and 2 pipeline epochs at K = 4.
+
+Graphs are regenerated here by the product's own generate_er / make_chunks (bit-exact: the
+chunk plan is compared through its sha256). Bars as in test_gpu_parity.py."""
+import hashlib
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+CFG0 = (4096, 65536 / (4096 * 4095), 1, 128, 16, 1)
+CFG1 = (169343, 2332486 / (169343 * 169342), 1, 128, 40, 1)
+CFG2 = (232965, 114615892 / (232965 * 232964), 1, 602, 41, 1)
+
+
+@pytest.fixture(scope="module", autouse=True)
+def need_gpu(gp):
+    if gp.device_count() == 0:
+        pytest.fail("no CUDA device visible: GPU tests must run on the B200 box")
+
+
+def golden(name):
+    return dict(np.load(os.path.join(GOLD, name + ".npz")))
+
+
+def rel(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-30))
+
+
+def sha(co):
+    return hashlib.sha256(np.ascontiguousarray(co, "<u4").tobytes()).hexdigest()
+
+
+def compare_training(gp, name, ds, model, S, K, epochs, loss_tol=1e-4, param_abs_tol=None):
+    ref = golden(name)
+    co = gp.make_chunks(ds, K, 1)
+    assert sha(co) == str(ref["chunk_of_sha256"]), "chunk plan not bit-exact"
+    res = gp.train_pipeline(ds, co, S, gp.TrainOptions(model=model, epochs=epochs, seed=1))
+    met = ref["metrics"].reshape(epochs, 5)
+    assert np.array_equal(res.metrics[:, 0], met[:, 0])
+    lrel = np.abs(res.train_loss - met[:, 1]) / np.abs(met[:, 1])
+    assert lrel.max() < loss_tol, (res.train_loss, met[:, 1])
+    # accuracies: a few argmax flips on near-ties (logits stay near-uniform in deep GCNs)
+    assert np.max(np.abs(res.metrics[:, 2:5] - met[:, 2:5])) <= max(2e-3, 5.0 / (0.2 * ds.num_vertices))
+    assert np.array_equal(res.comm.astype(np.uint64), ref["comm"].reshape(epochs, 3)), "ledger bytes differ"
+    worst, med, absmax = 0.0, [], 0.0
+    for l, (W, b) in enumerate(res.params):
+        rW = ref[f"W{l}"].astype(np.float64)
+        absmax = max(absmax, float(np.abs(W - rW).max()))
+        d = np.abs(W - rW) / np.maximum(np.abs(rW), 1e-3)
+        worst = max(worst, float(d.max()))
+        med.append(float(np.median(d)))
+    if param_abs_tol is None:
+        assert worst < 2e-3 and max(med) < 1e-4, (worst, med)
+    else:  # long runs: Adam moves a weight by ~lr per step whatever the gradient's size
+        assert absmax <= param_abs_tol and max(med) < 1e-3, (absmax, med)
+    return res, lrel
+
+
+def test_cfg0_er4k_gcn8_20_epoch_curve(gp):
+    """configs[0] exactly: the one BASELINE config the CPU reference runs whole (1.4-1.9 s/epoch)."""
+    ds = gp.Dataset.synthetic_er(*CFG0)
+    model = gp.ModelConfig(kind=gp.ModelKind.GCN, layers=8, hidden=128)
+    res, lrel = compare_training(gp, "cfg0_er4k_gcn8_s1k4_20ep", ds, model, 1, 4, 20, loss_tol=1e-5,
+                                 param_abs_tol=5e-3)
+    assert res.metrics.shape[0] == 20
+
+
+@pytest.mark.parametrize("S,K", [(2, 8), (4, 16)])
+def test_cfg1_arxiv_shape_gcn16(gp, S, K):
+    ds = gp.Dataset.synthetic_er(*CFG1)
+    model = gp.ModelConfig(kind=gp.ModelKind.GCN, layers=16, hidden=128)
+    compare_training(gp, f"cfg1_arxiv_gcn16_s{S}k{K}_3ep", ds, model, S, K, 3, loss_tol=1e-5)
+
+
+@pytest.fixture(scope="module")
+def reddit(gp):
+    return gp.Dataset.synthetic_er(*CFG2)
+
+
+def test_cfg2_reddit_shape_gcnii4_loss_and_every_gradient(gp, reddit, monkeypatch):
+    """Whole-graph epoch 1 (train_sequential's first epoch == S = 1, K = 1 pipeline,
+    test_engines.cpp:103-113) at the full Reddit shape: loss (rel 1e-6), every parameter gradient
+    (rel 1e-4), the parameters after the first Adam step, and fp64 column sums of every layer's
+    pre / h (from bit-exact rows) and dz."""
+    monkeypatch.setenv("GP_LEAN", "0")  # read h back after the epoch
+    ref = golden("cfg2_reddit_gcnii4_forward")
+    ds = reddit
+    model = gp.ModelConfig(kind=gp.ModelKind.GCNII, layers=4, hidden=100)
+    specs = gp.build_layer_specs(model, ds.num_features, ds.num_classes)
+    init = gp.init_params(model, ds.num_features, ds.num_classes, 1)
+    eng = gp.StageEngine(num_vertices=ds.num_vertices, num_chunks=1, specs=specs, stage=0, num_stages=1,
+                         layer_range=(0, 4), hidden=100, num_classes=ds.num_classes, dropout=0.5, seed=1)
+    off, cols, vals = ds.normalize_adjacency(True)
+    eng.upload_graph(off, cols, vals, np.zeros(ds.num_vertices, np.uint32))
+    x, lab, sp = ds.arrays()
+    eng.upload_features(x)
+    eng.upload_labels(lab, sp)
+    for l, (W, b) in enumerate(init):
+        eng.set_params(l, W, b)
+    st = eng.run_epoch(1, [0])
+    ntrain = int((sp == 1).sum())
+    assert abs(st.loss_sum / ntrain - float(ref["loss"][0])) <= 1e-6 * abs(float(ref["loss"][0]))
+    for l in range(4):
+        gW, gb = eng.get_grads(l)
+        assert rel(gW, ref[f"gW{l}"]) < 1e-4, (l, rel(gW, ref[f"gW{l}"]))
+        if gb.size:
+            assert rel(gb, ref[f"gb{l}"]) < 1e-4, l
+        for name, tol in (("h", 1e-9), ("pre", 1e-9), ("dz", 1e-4)):
+            s = eng.download(name, l).astype(np.float64).sum(0)
+            want = ref[f"sum_{name}{l}"]
+            assert rel(s, want) < tol, (name, l, rel(s, want))
+        W, _ = eng.get_params(l)
+        g = ref[f"gW{l}"].astype(np.float64)
+        want = init[l][0].astype(np.float64) - 1e-3 * g / (np.abs(g) + 1e-8)  # first Adam step
+        assert np.max(np.abs(W - want)) < 2e-6, l
+    eng.close()
+
+
+def test_cfg2_reddit_shape_gcnii4_pipeline_two_epochs(gp, reddit):
+    model = gp.ModelConfig(kind=gp.ModelKind.GCNII, layers=4, hidden=100)
+    compare_training(gp, "cfg2_reddit_gcnii4_s1k4_2ep", reddit, model, 1, 4, 2, loss_tol=1e-5)

@@ -36,7 +36,8 @@ def _dense_rows(x, W, b):
     return y
 
 
-def test_reddit_shape_epoch1_rows_bit_exact(gp):
+def test_reddit_shape_epoch1_rows_bit_exact(gp, monkeypatch):
+    monkeypatch.setenv("GP_LEAN", "0")  # activations and gather tables kept apart from dz / dagg
     from oracle import oracle as O
     ds = gp.Dataset.synthetic_er(N, E2 / (N * (N - 1)), 1, F, C, 1)
     model = gp.ModelConfig(kind=gp.ModelKind.GCNII, layers=4, hidden=H, dropout=0.5)

@@ -67,7 +67,8 @@ def single_stage(gp, ds, model, seed, K=1, chunk_of=None, **kw):
 
 
 @pytest.mark.parametrize("name,kind,layers", [("forward_gcn", 0, 3), ("forward_gcnii", 2, 5), ("forward_sage", 1, 3)])
-def test_epoch1_forward_bitexact_and_backward_close(gp, name, kind, layers):
+def test_epoch1_forward_bitexact_and_backward_close(gp, name, kind, layers, monkeypatch):
+    monkeypatch.setenv("GP_LEAN", "0")  # keep h apart from dz so the activations can be read back
     ref = golden(name)
     ds = er500(gp)
     model = gp.ModelConfig(kind=kind, layers=layers, hidden=16)
@@ -176,8 +177,9 @@ def test_train_gcn_pipeline_stale_two_stages(gp):
                    fix_alpha=3)
 
 
-@pytest.mark.parametrize("env", [{}, {"GP_SPLIT": "0"}, {"GP_WAVE": "1"}, {"GP_OCC5": "1"}, {"GP_MERGED_G": "1"}],
-                         ids=["default", "fused", "one_stream", "occ5", "merged_g"])
+@pytest.mark.parametrize("env", [{}, {"GP_SPLIT": "0"}, {"GP_WAVE": "1"}, {"GP_OCC5": "1"}, {"GP_MERGED_G": "0"},
+                                 {"GP_LEAN": "0"}],
+                         ids=["default", "fused", "one_stream", "occ5", "split_g", "swap_layout"])
 def test_train_sage_pipeline_stale_two_stages(gp, env, monkeypatch):
     """GraphSAGE (SageConv: [own | mean] . W, nn.hpp:176-182, :234-243) over two stages, under every
     engine variant switch (SageConv layers always run split; the others follow GP_SPLIT)."""
@@ -187,9 +189,10 @@ def test_train_sage_pipeline_stale_two_stages(gp, env, monkeypatch):
                    fix_alpha=3)
 
 
-def test_sage_wide_features_forward_bitexact(gp):
+def test_sage_wide_features_forward_bitexact(gp, monkeypatch):
     """SageConv layer 0 over F = 200 features (> 128): mean aggregate + own row through the wide
     path (k_spmm_pre, k_remask, k_dense_gemm with the gapped weights), bit-exact."""
+    monkeypatch.setenv("GP_LEAN", "0")
     ref = golden("forward_sage_wide")
     ds = gp.Dataset.synthetic_er(300, 0.03, 11, 200, 7, 2)
     model = gp.ModelConfig(kind=1, layers=3, hidden=16)
@@ -210,19 +213,36 @@ def test_train_sage_wide_features_two_stages(gp):
                    gp.ModelConfig(kind=1, layers=3, hidden=16), 2, 4, 1, 6, 50, fix_alpha=2)
 
 
-@pytest.mark.parametrize("env", [{"GP_SPLIT": "0"}, {"GP_WAVE": "1"}, {"GP_OCC5": "1"}, {"GP_PGRAD": "simt"},
-                                 {"GP_MERGED_G": "1"}, {"GP_MERGED_G": "1", "GP_SPLIT": "0"}],
-                         ids=["fused", "one_stream", "occ5", "simt_pgrad", "merged_g", "merged_g_fused"])
-def test_engine_variants_match_default_bitwise(gp, env, monkeypatch):
-    """The engine's switches change scheduling and kernel shapes, never arithmetic order (except the
-    pgrad reduction): losses and parameters equal the default run bit for bit."""
+VARIANTS = [{"GP_SPLIT": "0"}, {"GP_WAVE": "1"}, {"GP_OCC5": "1"}, {"GP_PGRAD": "simt"}, {"GP_MERGED_G": "0"},
+            {"GP_MERGED_G": "0", "GP_SPLIT": "0"}, {"GP_LEAN": "0"}, {"GP_LEAN": "0", "GP_MERGED_G": "0"},
+            {"GP_LEAN": "0", "GP_SPLIT": "0"}]
+VARIANT_IDS = ["fused", "one_stream", "occ5", "simt_pgrad", "split_g", "split_g_fused", "swap_layout",
+               "swap_layout_split_g", "swap_layout_fused"]
+
+
+@pytest.mark.parametrize("hist", [False, True], ids=["stale", "hist"])
+@pytest.mark.parametrize("G", [1, 2], ids=["pipeline", "hybrid"])
+@pytest.mark.parametrize("env", VARIANTS, ids=VARIANT_IDS)
+def test_engine_variants_match_default_bitwise(gp, env, G, hist, monkeypatch):
+    """The engine's switches change scheduling, kernel shapes and the stash layout (lean
+    in-place dz / bg-in-G with snapshot copies vs separate buffers with pointer swaps), never
+    arithmetic order (except the pgrad reduction): losses and parameters equal the default run
+    bit for bit, in pipeline and hybrid runs, with and without historical gradients."""
     ds = er500(gp)
     model = gp.ModelConfig(kind=2, layers=6, hidden=16)
     co = gp.make_chunks(ds, 4, 3)
-    base = gp.train_pipeline(ds, co, 2, gp.TrainOptions(model=model, epochs=4, seed=9, fix_alpha=2))
+    part, _, _ = gp.partition_vertices(ds, 2, 2)
+
+    def run():
+        opt = gp.TrainOptions(model=model, epochs=4, seed=9, fix_alpha=2, historical_gradients=hist)
+        if G == 1:
+            return gp.train_pipeline(ds, co, 2, opt)
+        return gp.train_hybrid(ds, part, co, 2, opt)
+
+    base = run()
     for k, v in env.items():
         monkeypatch.setenv(k, v)
-    res = gp.train_pipeline(ds, co, 2, gp.TrainOptions(model=model, epochs=4, seed=9, fix_alpha=2))
+    res = run()
     if "GP_PGRAD" in env:  # different parameter-gradient summation order: tolerance
         np.testing.assert_allclose(res.train_loss, base.train_loss, rtol=1e-4)
         return
