@@ -37,6 +37,7 @@
 #include "dense_tile.cuh"
 #include "rows8.cuh"
 #include "tc_pgrad.cuh"
+#include "tc_xform.cuh"
 
 namespace gp {
 namespace {
@@ -276,6 +277,9 @@ struct LayerDev {
     float *G = nullptr;                  // masked gather source (input of this layer): rows of done chunks
     float *Gs = nullptr;                 // masked snapshot rows (rows of not-done chunks); == G if cur == snap
     float *bg = nullptr, *bgs = nullptr; // backward gather source (+ snapshot, hist mode)
+    // tcgen05 row transforms (tc_xform.cuh): prepared W' operands, forward and backward
+    bool tc = false;
+    float *xf_fwd = nullptr, *xf_bwd = nullptr;
 };
 
 struct Stage {
@@ -306,6 +310,9 @@ struct Stage {
     // snapshots by pointer swap (the round-1 layout; tests that read activations
     // after an epoch use it).
     bool lean = true;
+    // GP_TC_XFORM=1 (default): the GCN / GCNII row transforms (pre.W', dz.W'^T and their
+    // epilogues) run on tcgen05 (3xTF32, fp32-level); 0: the bit-exact CUDA-core tiles
+    bool use_tc_xform = true;
     bool state_restored = false;  // gp_set_history: the snapshot rows were loaded
     // forward wavefront hooks (merged_g): after the kernel gathering from G_i, and
     // before the kernel writing rows of G_i
@@ -541,6 +548,7 @@ struct Stage {
         if (needs_h0 && (H == 0 || H > kMaxWidth)) throw Error(GP_EINVAL, "bad hidden width");
         if (const char* e = std::getenv("GP_MERGED_G")) merged_g = std::atoi(e) != 0;
         if (const char* e = std::getenv("GP_LEAN")) lean = std::atoi(e) != 0;
+        if (const char* e = std::getenv("GP_TC_XFORM")) use_tc_xform = std::atoi(e) != 0;
         if (plan_only) return;
         device = c.device;
         int ndev = 0;
@@ -635,6 +643,11 @@ struct Stage {
                 d.gb = dalloc<float>(d.dout);
                 d.mb = dalloc<float>(d.dout);
                 d.vb = dalloc<float>(d.dout);
+            }
+            if (use_tc_xform && d.agg && !d.sage && d.din <= kMaxWidth && d.dout <= kMaxWidth) {
+                d.tc = true;
+                d.xf_fwd = dalloc<float>(2 * size_t(xf_pad8k(d.din)) * xf_pad16(d.dout));
+                d.xf_bwd = dalloc<float>(2 * size_t(xf_pad8k(d.dout)) * xf_pad16(d.din));
             }
             d.h = dalloc<float>(size_t(n) * d.sout);
             d.pre = dalloc<float>(size_t(n) * d.skw);
@@ -776,7 +789,8 @@ struct Stage {
                              (const void*)k_pgrad_tc,    (const void*)k_pull_rows,     (const void*)k_remask,
                              (const void*)k_spmm_pre,    (const void*)k_stamp,         (const void*)k_transpose,
                              (const void*)k_xent_fold,   (const void*)k_xent_grad,     (const void*)k_xent_stats,
-                             (const void*)k_zero,        (const void*)k_sage_weights};
+                             (const void*)k_zero,        (const void*)k_sage_weights,  (const void*)k_tc_prep,
+                             (const void*)k_tc_xform<false>, (const void*)k_tc_xform<true>};
         for (const void* f : fns) {
             cudaFuncAttributes a;
             GP_CUDA(cudaFuncGetAttributes(&a, f));
@@ -793,6 +807,8 @@ struct Stage {
         preload_kernels();
         if (const char* e = std::getenv("GP_PGRAD")) use_tc_pgrad = std::string(e) != "simt";
         GP_CUDA(cudaFuncSetAttribute(k_pgrad_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        GP_CUDA(cudaFuncSetAttribute(k_tc_xform<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        GP_CUDA(cudaFuncSetAttribute(k_tc_xform<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         if (const char* e = std::getenv("GP_NB")) {
             const int v = std::atoi(e);
             if (v == 2 || v == 4) nb = v;
@@ -1275,6 +1291,67 @@ struct Stage {
         const uint32_t nw = d.din * d.dout;
         launch(GP_K_OPTIM, nw * 8.0, 0, 0,
                [&]() { k_transpose<<<(nw + 255) / 256, 256, 0, cs>>>(d.W, d.WT, d.din, d.dout); });
+        if (d.tc) {  // W' = beta W + (1 - beta) I (Gcn2Conv) as tf32 hi / lo operands
+            const bool g2 = d.spec.kind == GP_GCN2CONV;
+            const float beta = float(d.spec.beta), omb = 1.f - beta;
+            launch(GP_K_OPTIM, nw * 12.0, 0, 0, [&]() {
+                k_tc_prep<<<(nw + 255) / 256, 256, 0, cs>>>(d.W, d.din, d.dout, xf_pad8k(d.din), xf_pad16(d.dout), 0,
+                                                            g2, beta, omb, d.xf_fwd);
+                k_tc_prep<<<(nw + 255) / 256, 256, 0, cs>>>(d.W, d.dout, d.din, xf_pad8k(d.dout), xf_pad16(d.din), 1,
+                                                            g2, beta, omb, d.xf_bwd);
+            });
+        }
+    }
+
+    // tcgen05 transform launch over rows [r0, r1): one CTA per SM (>= 116 KB of shared
+    // memory, so a second CTA never waits on TMEM columns), persistent over 128-row tiles
+    template <bool BWD>
+    void tc_xform_go(const TcXformParams& x) {
+        const uint32_t ntiles = (x.r1 - x.r0 + kXfM - 1) / kXfM;
+        const size_t smem = std::max<size_t>(xf_smem_bytes(x.kpad, x.npad), 116 * 1024);
+        const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(ntiles, uint32_t(num_sms)));
+        k_tc_xform<BWD><<<grid, kXfThreads, smem, cs>>>(x);
+    }
+    TcXformParams tc_fwd_params(const LayerDev& d, const FwdParams& p) const {
+        TcXformParams x{};
+        x.r0 = p.r0;
+        x.r1 = p.r1;
+        x.A = p.pre;
+        x.astride = p.prestride;
+        x.kdim = d.din;
+        x.kpad = xf_pad8k(d.din);
+        x.ndim = d.dout;
+        x.npad = xf_pad16(d.dout);
+        x.ostride = p.outstride;
+        x.Bop = d.xf_fwd;
+        x.bias = p.bias;
+        x.relu = p.relu;
+        x.out = p.out;
+        x.gnext = p.gnext;
+        x.gnstride = p.gnstride;
+        x.next_mask = p.next_mask;
+        x.orig = p.orig;
+        return x;
+    }
+    TcXformParams tc_bwd_params(const LayerDev& d, const BwdParams& p) const {
+        TcXformParams x{};
+        x.r0 = p.r0;
+        x.r1 = p.r1;
+        x.A = p.dz;
+        x.astride = p.dzstride;
+        x.kdim = d.dout;
+        x.kpad = xf_pad8k(d.dout);
+        x.ndim = d.din;
+        x.npad = xf_pad16(d.din);
+        x.ostride = p.bgstride;
+        x.Bop = d.xf_bwd;
+        x.gcn2 = p.gcn2;
+        x.alpha = p.alpha;
+        x.oma = p.oma;
+        x.dh0 = p.dh0;
+        x.dh0stride = p.dh0stride;
+        x.bg = p.bg;
+        return x;
     }
 
     void set_params(uint32_t l, const float* W, const float* b) {
@@ -1508,7 +1585,8 @@ struct Stage {
                 gather_done();
                 write_wait();
                 launch(GP_K_FWD_DENSE, db, 2.0 * double(rows) * d.din * d.dout, 0, [&]() {
-                    if (g2) fwd_dense_go<true>(rows, p);
+                    if (d.tc) tc_xform_go<false>(tc_fwd_params(d, p));
+                    else if (g2) fwd_dense_go<true>(rows, p);
                     else fwd_dense_go<false>(rows, p);
                 });
                 return;
@@ -1665,7 +1743,10 @@ struct Stage {
             if (p.need_dagg) {
                 const double db = double(rows) * (d.dout + d.din) * 4.0 + (p.gcn2 ? double(rows) * d.din * 8.0 : 0.0) +
                                   double(d.din) * d.dout * 4.0;
-                launch(GP_K_BWD_DENSE, db, 2.0 * double(rows) * d.din * d.dout, 0, [&]() { bwd_dense_go(rows, p); });
+                launch(GP_K_BWD_DENSE, db, 2.0 * double(rows) * d.din * d.dout, 0, [&]() {
+                    if (d.tc) tc_xform_go<true>(tc_bwd_params(d, p));
+                    else bwd_dense_go(rows, p);
+                });
             }
             return;
         }

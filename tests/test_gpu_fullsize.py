@@ -38,6 +38,7 @@ def _dense_rows(x, W, b):
 
 def test_reddit_shape_epoch1_rows_bit_exact(gp, monkeypatch):
     monkeypatch.setenv("GP_LEAN", "0")  # activations and gather tables kept apart from dz / dagg
+    monkeypatch.setenv("GP_TC_XFORM", "0")  # bit-exact rows need the CUDA-core transforms
     from oracle import oracle as O
     ds = gp.Dataset.synthetic_er(N, E2 / (N * (N - 1)), 1, F, C, 1)
     model = gp.ModelConfig(kind=gp.ModelKind.GCNII, layers=4, hidden=H, dropout=0.5)

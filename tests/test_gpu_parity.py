@@ -69,6 +69,7 @@ def single_stage(gp, ds, model, seed, K=1, chunk_of=None, **kw):
 @pytest.mark.parametrize("name,kind,layers", [("forward_gcn", 0, 3), ("forward_gcnii", 2, 5), ("forward_sage", 1, 3)])
 def test_epoch1_forward_bitexact_and_backward_close(gp, name, kind, layers, monkeypatch):
     monkeypatch.setenv("GP_LEAN", "0")  # keep h apart from dz so the activations can be read back
+    monkeypatch.setenv("GP_TC_XFORM", "0")  # the bit-exact CUDA-core transforms
     ref = golden(name)
     ds = er500(gp)
     model = gp.ModelConfig(kind=kind, layers=layers, hidden=16)
@@ -193,6 +194,7 @@ def test_sage_wide_features_forward_bitexact(gp, monkeypatch):
     """SageConv layer 0 over F = 200 features (> 128): mean aggregate + own row through the wide
     path (k_spmm_pre, k_remask, k_dense_gemm with the gapped weights), bit-exact."""
     monkeypatch.setenv("GP_LEAN", "0")
+    monkeypatch.setenv("GP_TC_XFORM", "0")
     ref = golden("forward_sage_wide")
     ds = gp.Dataset.synthetic_er(300, 0.03, 11, 200, 7, 2)
     model = gp.ModelConfig(kind=1, layers=3, hidden=16)
@@ -213,17 +215,21 @@ def test_train_sage_wide_features_two_stages(gp):
                    gp.ModelConfig(kind=1, layers=3, hidden=16), 2, 4, 1, 6, 50, fix_alpha=2)
 
 
-VARIANTS = [{"GP_SPLIT": "0"}, {"GP_WAVE": "1"}, {"GP_OCC5": "1"}, {"GP_PGRAD": "simt"}, {"GP_MERGED_G": "0"},
-            {"GP_MERGED_G": "0", "GP_SPLIT": "0"}, {"GP_LEAN": "0"}, {"GP_LEAN": "0", "GP_MERGED_G": "0"},
-            {"GP_LEAN": "0", "GP_SPLIT": "0"}]
+# (base env, variant env): the fused kernels (GP_SPLIT=0) run the CUDA-core GEMV, so they are
+# compared with the CUDA-core split transforms (GP_TC_XFORM=0)
+CC = {"GP_TC_XFORM": "0"}
+VARIANTS = [(CC, {"GP_SPLIT": "0"}), ({}, {"GP_WAVE": "1"}), ({}, {"GP_OCC5": "1"}), ({}, {"GP_PGRAD": "simt"}),
+            ({}, {"GP_MERGED_G": "0"}), (CC, {"GP_MERGED_G": "0", "GP_SPLIT": "0"}), ({}, {"GP_LEAN": "0"}),
+            ({}, {"GP_LEAN": "0", "GP_MERGED_G": "0"}), (CC, {"GP_LEAN": "0", "GP_SPLIT": "0"}),
+            (CC, {"GP_WAVE": "1"}), (CC, {"GP_LEAN": "0"})]
 VARIANT_IDS = ["fused", "one_stream", "occ5", "simt_pgrad", "split_g", "split_g_fused", "swap_layout",
-               "swap_layout_split_g", "swap_layout_fused"]
+               "swap_layout_split_g", "swap_layout_fused", "cuda_core_one_stream", "cuda_core_swap_layout"]
 
 
 @pytest.mark.parametrize("hist", [False, True], ids=["stale", "hist"])
 @pytest.mark.parametrize("G", [1, 2], ids=["pipeline", "hybrid"])
-@pytest.mark.parametrize("env", VARIANTS, ids=VARIANT_IDS)
-def test_engine_variants_match_default_bitwise(gp, env, G, hist, monkeypatch):
+@pytest.mark.parametrize("envs", VARIANTS, ids=VARIANT_IDS)
+def test_engine_variants_match_default_bitwise(gp, envs, G, hist, monkeypatch):
     """The engine's switches change scheduling, kernel shapes and the stash layout (lean
     in-place dz / bg-in-G with snapshot copies vs separate buffers with pointer swaps), never
     arithmetic order (except the pgrad reduction): losses and parameters equal the default run
@@ -239,6 +245,9 @@ def test_engine_variants_match_default_bitwise(gp, env, G, hist, monkeypatch):
             return gp.train_pipeline(ds, co, 2, opt)
         return gp.train_hybrid(ds, part, co, 2, opt)
 
+    base_env, env = envs
+    for k, v in base_env.items():
+        monkeypatch.setenv(k, v)
     base = run()
     for k, v in env.items():
         monkeypatch.setenv(k, v)
