@@ -331,6 +331,7 @@ struct Stage {
     uint2* edges_m = nullptr;
     uint2* edges_mt = nullptr;
     uint32_t* orig = nullptr;          // new -> original id (device)
+    uint32_t* id_rows = nullptr;       // own rows in ascending original id (reductions)
     std::vector<uint32_t> perm;        // original -> new (host)
     std::vector<uint32_t> inv;         // new -> original (host)
     uint64_t nnz = 0;
@@ -1179,7 +1180,24 @@ struct Stage {
         if (G == 1) hg->col.clear();  // only hybrid needs the host columns
         bstart = hg->bstart;
         build_halo();
+        build_id_rows();
         graph_ready = true;
+    }
+
+    // Own rows in ascending original vertex id: the order param_grads_for_rows and the
+    // loss sum visit rows in (nn.hpp:269-293, engines_impl.hpp:725-734, :873-876). Reducing
+    // in this order, with split boundaries fixed by the row count alone, makes parameter
+    // gradients and the loss independent of the chunk plan (a synchronous pipeline then
+    // equals the sequential trainer bit for bit, test_engines.cpp:115-126).
+    void build_id_rows() {
+        std::vector<uint32_t> rows;
+        rows.reserve(own_end() - own_begin());
+        for (uint32_t v = 0; v < n; ++v) {
+            const uint32_t r = perm[v];
+            if (r >= own_begin() && r < own_end()) rows.push_back(r);
+        }
+        if (!id_rows) id_rows = dalloc<uint32_t>(std::max<size_t>(rows.size(), 1), false);
+        GP_CUDA(cudaMemcpy(id_rows, rows.data(), rows.size() * 4, cudaMemcpyHostToDevice));
     }
 
     // Halo lists (chunk_push_sets, engines_impl.hpp:488-499): peer r2 pushes, in
@@ -1231,6 +1249,7 @@ struct Stage {
         bstart = o.bstart;
         nnz = o.nnz;
         build_halo();
+        build_id_rows();
         graph_ready = true;
     }
 
@@ -1862,14 +1881,14 @@ struct Stage {
             if (use_tc_pgrad) {
                 // tcgen05 (3xTF32) split-K GEMM, one CTA per SM (TMEM accumulator, ~120 KB smem)
                 used_splits = std::min<uint32_t>(splits, uint32_t(num_sms));
-                TcPgradParams tp{re, (nown + used_splits - 1) / used_splits, rb, pre, d.skw, d.dz, d.sout, d.din,
-                                 d.dout, (d.dout + 15) / 16 * 16, ws, gb ? wsb : nullptr};
+                TcPgradParams tp{nown, (nown + used_splits - 1) / used_splits, 0, pre, d.skw, d.dz, d.sout, d.din,
+                                 d.dout, (d.dout + 15) / 16 * 16, ws, gb ? wsb : nullptr, id_rows};
                 const size_t smem = 2 * (2 * size_t(kTcM) * kTcKt * 4 + 2 * size_t(tp.npad) * kTcKt * 4);
                 dim3 grid(used_splits, ti, 1);
                 launch(GP_K_PGRAD, pg_bytes, pg_flops, 0, [&]() { k_pgrad_tc<<<grid, kTcThreads, smem, cs>>>(tp); });
             } else {
                 const uint32_t rps = (nown + splits - 1) / splits;
-                PgradParams pp{re, rps, rb, pre, d.skw, d.dz, d.sout, d.din, d.dout, ws, gb ? wsb : nullptr};
+                PgradParams pp{nown, rps, 0, pre, d.skw, d.dz, d.sout, d.din, d.dout, ws, gb ? wsb : nullptr, id_rows};
                 dim3 grid(splits, ti, 1);
                 launch(GP_K_PGRAD, pg_bytes, pg_flops, 0, [&]() { k_pgrad_partial<<<grid, 256, 0, cs>>>(pp); });
             }
@@ -2758,7 +2777,8 @@ struct Stage {
 
         // ---- metrics (last stage) ---------------------------------------------------
         if (last) {
-            XentParams p = xent_params(own_begin(), own_end());
+            XentParams p = xent_params(0, own_end() - own_begin());
+            p.rows = id_rows;
             launch(GP_K_XENT, double(own_end() - own_begin()) * L[len - 1].dout * 4.0, 0, 0,
                    [&]() { k_xent_stats<<<xent_blocks, kBlock, 0, cs>>>(p); });
             launch(GP_K_XENT, 0, 0, 0, [&]() {

@@ -429,6 +429,9 @@ struct XentParams {
     uint32_t gstride;
     double* part_loss;
     unsigned long long* part_correct;  // 3 per block
+    // k_xent_stats: row i of [r0, r1) is stash row rows[i] (ascending original id), so
+    // the loss partials do not depend on the chunking; null: row i
+    const uint32_t* rows;
 };
 
 struct RowSoftmax {
@@ -470,7 +473,8 @@ __global__ void __launch_bounds__(kBlock) k_xent_stats(XentParams p) {
     double loss = 0.0;
     unsigned long long corr[3] = {0, 0, 0};
     const uint32_t nw = gridDim.x * kWarpsPerBlock;
-    for (uint32_t v = p.r0 + blockIdx.x * kWarpsPerBlock + warp; v < p.r1; v += nw) {
+    for (uint32_t i = p.r0 + blockIdx.x * kWarpsPerBlock + warp; i < p.r1; i += nw) {
+        const uint32_t v = p.rows ? p.rows[i] : i;
         const uint8_t s = p.split[v];
         if (s == 0 || s > 3) continue;
         const float4 l = uint32_t(4 * lane) < p.classes
@@ -562,6 +566,7 @@ struct PgradParams {
     uint32_t din, dout;
     float* ws;   // splits x din x dout
     float* wsb;  // splits x dout
+    const uint32_t* rows;  // reduction row i -> stash row rows[i] (ascending original id); null: i
 };
 
 // CTA tile 128 (k_in) x 128 (out): each row of pre/dz is read once per CTA.
@@ -590,12 +595,13 @@ __global__ void __launch_bounds__(256, 2) k_pgrad_partial(PgradParams p) {
     auto fetch = [&](uint32_t r0) {
         const uint32_t row = r0 + lr;
         const bool ok = row < rend;
+        const uint32_t srow = ok && p.rows ? p.rows[row] : row;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const uint32_t ci = i0 + lc + 4 * h, cj = lc + 4 * h;
-            rp[h] = (ok && ci < p.din) ? *reinterpret_cast<const float4*>(p.pre + size_t(row) * p.prestride + ci)
+            rp[h] = (ok && ci < p.din) ? *reinterpret_cast<const float4*>(p.pre + size_t(srow) * p.prestride + ci)
                                        : f4_zero();
-            rd[h] = (ok && cj < p.dout) ? *reinterpret_cast<const float4*>(p.dz + size_t(row) * p.dzstride + cj)
+            rd[h] = (ok && cj < p.dout) ? *reinterpret_cast<const float4*>(p.dz + size_t(srow) * p.dzstride + cj)
                                         : f4_zero();
         }
     };

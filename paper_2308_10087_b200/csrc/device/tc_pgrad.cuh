@@ -39,6 +39,10 @@ struct TcPgradParams {
     uint32_t npad;  // dout rounded up to 16 (MMA N)
     float* ws;      // splits x din x dout
     float* wsb;     // splits x dout (bias partials) or null
+    // row i of the reduction is stash row rows[i] (the own rows in ascending original
+    // id, param_grads_for_rows' order, nn.hpp:269-293), so the sum order and the split
+    // boundaries do not depend on the chunking; null: row i
+    const uint32_t* rows;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -118,12 +122,13 @@ struct TcItem {
 };
 
 __device__ __forceinline__ void tc_load(TcItem& it, const float* src, uint32_t stride, uint32_t col0,
-                                        uint32_t cols_valid, uint32_t row0, uint32_t rend) {
+                                        uint32_t cols_valid, uint32_t row0, uint32_t rend,
+                                        const uint32_t* rows = nullptr) {
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
         const uint32_t row = row0 + e;
         if (row < rend && col0 < cols_valid)
-            it.v[e] = *reinterpret_cast<const float4*>(src + size_t(row) * stride + col0);
+            it.v[e] = *reinterpret_cast<const float4*>(src + size_t(rows ? rows[row] : row) * stride + col0);
         else
             it.v[e] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
@@ -196,8 +201,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_pgrad_tc(TcPgradParams p) {
     const uint32_t nst = (rend > rbeg) ? (rend - rbeg + kTcKt - 1) / kTcKt : 0;
     TcItem ia, ib;
     if (nst > 0) {
-        tc_load(ia, p.pre, p.prestride, i0 + 4 * a_q, p.din, rbeg + 4 * a_c, rend);
-        if (has_b) tc_load(ib, p.dz, p.dzstride, 4 * b_q, p.dout, rbeg + 4 * b_c, rend);
+        tc_load(ia, p.pre, p.prestride, i0 + 4 * a_q, p.din, rbeg + 4 * a_c, rend, p.rows);
+        if (has_b) tc_load(ib, p.dz, p.dzstride, 4 * b_q, p.dout, rbeg + 4 * b_c, rend, p.rows);
     }
     uint32_t uses[2] = {0, 0};
     for (uint32_t it = 0; it < nst; ++it) {
@@ -212,8 +217,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_pgrad_tc(TcPgradParams p) {
         if (has_b) tc_store(ib, b_hi, b_lo, b_lbo, b_c, b_q, p.dout, 4 * b_q, do_bias ? bcol : nullptr);
         if (it + 1 < nst) {  // prefetch the next stage while this one is multiplied
             const uint32_t r1 = rbeg + (it + 1) * kTcKt;
-            tc_load(ia, p.pre, p.prestride, i0 + 4 * a_q, p.din, r1 + 4 * a_c, rend);
-            if (has_b) tc_load(ib, p.dz, p.dzstride, 4 * b_q, p.dout, r1 + 4 * b_c, rend);
+            tc_load(ia, p.pre, p.prestride, i0 + 4 * a_q, p.din, r1 + 4 * a_c, rend, p.rows);
+            if (has_b) tc_load(ib, p.dz, p.dzstride, 4 * b_q, p.dout, r1 + 4 * b_c, rend, p.rows);
         }
         // generic-proxy smem writes -> visible to the tensor-core (async) proxy
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

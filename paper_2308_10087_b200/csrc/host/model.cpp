@@ -71,6 +71,13 @@ StageAssignment make_stage_assignment(uint32_t layers, uint32_t stages) {
     return sa;
 }
 
+uint32_t GroupMap::spanning_groups() const {
+    uint32_t count = 0;
+    for (const auto& g : groups)
+        if (std::any_of(g.begin(), g.end(), [&](uint32_t w) { return node_of[w] != node_of[g.front()]; })) ++count;
+    return count;
+}
+
 GroupMap assign_groups(uint32_t num_workers, uint32_t workers_per_node, uint32_t num_stages, uint32_t group_size) {
     if (workers_per_node == 0) throw std::invalid_argument("assign_groups: workers_per_node == 0");
     if (num_stages * group_size != num_workers)

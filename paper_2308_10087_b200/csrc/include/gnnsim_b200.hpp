@@ -119,6 +119,10 @@ void save_dataset(const Dataset& d, const std::string& dir);
 // Synthetic shapes of BASELINE.json: generate_er graph plus
 // x[v,j] = 2*hash_unit(mix64(fseed, v*F+j)) - 1, label = mix64(fseed,0x4C42,v) % C,
 // split by mix64(fseed,0x5350,v) % 10 (60/20/20).
+// Stochastic block model dataset (dataset.cpp:147-191): blocks of block_size vertices,
+// edge probability p_in inside a block and p_out across; one-hot-plus-noise features,
+// label = block, 60/20/20 split by position in the block.
+Dataset generate_sbm(uint32_t num_blocks, uint32_t block_size, double p_in, double p_out, uint64_t seed);
 Dataset synthetic_er_dataset(VertexId n, double p, uint64_t graph_seed, uint32_t F, uint32_t C,
                              uint64_t feature_seed);
 
@@ -133,6 +137,8 @@ struct Partition {
 };
 Partition partition_vertices(const Graph& g, uint32_t num_parts, uint64_t seed);
 Partition partition_from_assignment(const Graph& g, std::vector<uint32_t> assignment);
+// E|B_i| for an ER(n, p) graph cut into m equal parts (partition.cpp:206-211)
+double expected_boundary(double n, double m, double p);
 
 struct ChunkPlan {
     uint32_t num_chunks = 0;
@@ -252,6 +258,7 @@ struct GroupMap {
     std::vector<uint32_t> node_of, group_of, rank_in_group;
     std::vector<std::vector<uint32_t>> groups;
     uint32_t num_groups() const { return uint32_t(groups.size()); }
+    uint32_t spanning_groups() const;  // groups whose workers sit on more than one node
 };
 GroupMap assign_groups(uint32_t num_workers, uint32_t workers_per_node, uint32_t num_stages,
                        uint32_t group_size);
@@ -284,6 +291,14 @@ struct FabricOptions {
     std::vector<uint32_t> node_of;
     double watchdog_seconds = 600.0;
     bool collect_trace = false;
+};
+// Fabric (fabric.hpp:150-160) is the reference's simulated worker substrate; here only
+// its option types remain, so callers' `opt.fabric.mode = Fabric::Mode::Concurrent`
+// compiles. Both modes produce identical results in the reference too (fabric.hpp:146-149).
+class Fabric {
+  public:
+    using Mode = FabricOptions::Mode;
+    using Options = FabricOptions;
 };
 
 // ---------------------------------------------------------------- engines
