@@ -349,6 +349,10 @@ int gs_partition_vertices(const gs_dataset* d, uint32_t parts, uint64_t seed,
                           uint32_t* assignment, uint64_t* edge_cut, uint64_t* boundary_total);
 int gs_shuffle_chunk_order(uint32_t K, uint64_t epoch, uint64_t seed, uint32_t* order);
 int gs_make_stage_assignment(uint32_t layers, uint32_t stages, uint32_t* ranges /* 2*S */);
+/* chunks.txt / parts.txt (save_assignment / load_assignment, partition.cpp:250-269);
+ * load: call with assignment = NULL for the count n, then with a buffer of cap >= n. */
+int gs_save_assignment(const char* path, uint32_t num_parts, const uint32_t* assignment, uint64_t n);
+int gs_load_assignment(const char* path, uint32_t* num_parts, uint32_t* assignment, uint64_t cap, uint64_t* n);
 
 /* Model (nn.cpp:28-71, nn.hpp:60-72). */
 int gs_num_layers(const gs_model_config* m, uint32_t* L);

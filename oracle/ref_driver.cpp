@@ -402,6 +402,19 @@ void cmd_ckpt(const Args& a) {
     b.u64("num_layers", {specs.size()});
 }
 
+// save_assignment of make_chunks(K) and partition_vertices(K) (partition.cpp:250-256)
+void cmd_assign(const Args& a) {
+    Dataset d = make_dataset(arg(a, "spec"));
+    const uint32_t K = uint32_t(argu(a, "K"));
+    const uint64_t seed = argu(a, "seed");
+    ChunkPlan plan = make_chunks(d.graph, K, seed);
+    save_assignment(arg(a, "dir") + "/chunks.txt", plan.num_chunks, plan.chunk_of);
+    Partition p = partition_vertices(d.graph, K, seed);
+    save_assignment(arg(a, "dir") + "/parts.txt", p.num_parts, p.assignment);
+    Blob b(arg(a, "out"));
+    b.u32("chunk_of", plan.chunk_of);
+}
+
 void cmd_save(const Args& a) {
     Dataset d = make_dataset(arg(a, "spec"));
     save_dataset(d, arg(a, "dir"));
@@ -542,6 +555,7 @@ int main(int argc, char** argv) {
         else if (cmd == "forward") cmd_forward(a);
         else if (cmd == "train") cmd_train(a);
         else if (cmd == "save") cmd_save(a);
+        else if (cmd == "assign") cmd_assign(a);
         else if (cmd == "epochs") cmd_epochs(a);
         else if (cmd == "analytics") cmd_analytics(a);
         else if (cmd == "ckpt") cmd_ckpt(a);

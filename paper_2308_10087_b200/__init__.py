@@ -24,6 +24,7 @@ __all__ = [
     "GnnsimError", "InvalidArgument", "NumericError", "FabricError", "GpuEngineError",
     "LayerKind", "ModelKind", "stage_footprint", "ModelConfig", "TrainOptions", "TrainResult", "LayerSpec",
     "Dataset", "make_chunks", "partition_vertices", "shuffle_chunk_order", "make_stage_assignment",
+    "save_assignment", "load_assignment",
     "build_layer_specs", "init_params", "train_pipeline", "train_sequential", "train_hybrid", "StageEngine",
     "nccl_unique_id", "device_count", "lib_paths", "PROFILE_CLASSES",
 ]
@@ -172,6 +173,8 @@ def _L():
         "gs_make_chunks": (C.c_int, [vp, C.c_uint32, C.c_uint64, u32p]),
         "gs_partition_vertices": (C.c_int, [vp, C.c_uint32, C.c_uint64, u32p, u64p, u64p]),
         "gs_shuffle_chunk_order": (C.c_int, [C.c_uint32, C.c_uint64, C.c_uint64, u32p]),
+        "gs_save_assignment": (C.c_int, [C.c_char_p, C.c_uint32, u32p, C.c_uint64]),
+        "gs_load_assignment": (C.c_int, [C.c_char_p, P(C.c_uint32), u32p, C.c_uint64, P(C.c_uint64)]),
         "gs_make_stage_assignment": (C.c_int, [C.c_uint32, C.c_uint32, u32p]),
         "gs_num_layers": (C.c_int, [P(gs_model_config), u32p]),
         "gs_build_layer_specs": (C.c_int, [P(gs_model_config), C.c_uint32, C.c_uint32, P(gp_layer_spec)]),
@@ -463,6 +466,21 @@ def shuffle_chunk_order(num_chunks: int, epoch: int, seed: int) -> np.ndarray:
     out = np.zeros(num_chunks, np.uint32)
     _gs(_L().gs_shuffle_chunk_order(num_chunks, epoch, seed, _ptr(out, C.c_uint32)))
     return out
+
+
+def save_assignment(path: str, num_parts: int, assignment) -> None:
+    """save_assignment (partition.cpp:250-256): chunks.txt / parts.txt."""
+    a = np.ascontiguousarray(assignment, np.uint32)
+    _gs(_L().gs_save_assignment(path.encode(), num_parts, _ptr(a, C.c_uint32), a.size))
+
+
+def load_assignment(path: str):
+    """load_assignment (partition.cpp:258-267): (num_parts, assignment)."""
+    parts, n = C.c_uint32(), C.c_uint64()
+    _gs(_L().gs_load_assignment(path.encode(), C.byref(parts), None, 0, C.byref(n)))
+    a = np.zeros(n.value, np.uint32)
+    _gs(_L().gs_load_assignment(path.encode(), C.byref(parts), _ptr(a, C.c_uint32), a.size, C.byref(n)))
+    return int(parts.value), a
 
 
 def make_stage_assignment(layers: int, stages: int):

@@ -19,11 +19,13 @@
 //     SWIZZLE_NONE core-matrix layout, <= 128 KB) lands in shared memory once, by two
 //     cp.async.bulk copies completing on an mbarrier (TMA engine, no thread involved);
 //   * A streams in K-chunks of 32 columns: coalesced 16-byte global loads (8 threads
-//     per row), hi/lo split in registers, stored into the core-matrix layout; two
-//     stage buffers, the loads of chunk g+1 in flight while chunk g is multiplied;
+//     per row, L2 evict-first), hi/lo split in registers, stored into the core-matrix
+//     layout; two stage buffers, the loads of chunks g+1 and g+2 in flight (32 KB per
+//     SM) while chunk g is multiplied;
 //   * one elected thread issues the MMAs; two TMEM accumulators (2 x npad columns), so
 //     the epilogue of tile j-1 (8 warps: TMEM lane quarter = warp % 4, column half =
-//     warp / 4) overlaps the MMAs of tile j.
+//     warp / 4) overlaps the MMAs of tile j; each epilogue pass issues its dh0 loads
+//     and four tcgen05.ld before one wait.
 #pragma once
 
 #include "tc_pgrad.cuh"
@@ -101,14 +103,20 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                  : "memory");
 }
 
-__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
-    uint32_t r[8];
+// 8 columns of this warp's 32 TMEM lanes; completes at tmem_ld_wait()
+__device__ __forceinline__ void tmem_ld8_async(uint32_t taddr, uint32_t (&r)[8]) {
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                  : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
                  : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+__device__ __forceinline__ float4 ld4_ef(const float* p, uint64_t pol) {
+    float4 a;
+    asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w)
+                 : "l"(p), "l"(pol));
+    return a;
 }
 
 __device__ __forceinline__ void st_v4_ef(float* p, float a, float b, float c, float d, uint64_t pol) {
@@ -157,25 +165,30 @@ __global__ void __launch_bounds__(kXfThreads, 1) k_tc_xform(TcXformParams p) {
     const uint64_t pol = evict_first_policy();
 
     // A staging: thread handles float4 items idx = tid + 256 e (e < 4): row m = idx / 8,
-    // k-core kc = idx % 8 of the chunk (8 threads read one row's 128 contiguous bytes)
-    float4 reg[4];
-    auto load_chunk = [&](uint32_t tile, uint32_t c) {
+    // k-core kc = idx % 8 of the chunk (8 threads read one row's 128 contiguous bytes).
+    // Chunks are numbered g = j * nchunks + c over this CTA's tiles; two chunks are in
+    // flight in registers (32 KB per SM) while the current one is split and multiplied.
+    float4 reg[2][4];
+    const uint32_t total_chunks = my_tiles * nchunks;
+    auto load_chunk = [&](uint32_t gg, float4 (&r)[4]) {
+        if (gg >= total_chunks) return;
+        const uint32_t tile = blockIdx.x + (gg / nchunks) * gridDim.x, c = gg % nchunks;
         const uint32_t row0 = p.r0 + tile * kXfM, k0 = c * kXfKc;
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
             const uint32_t idx = tid + kXfThreads * e, m = idx >> 3, kc = idx & 7;
             const uint32_t v = row0 + m, k = k0 + 4 * kc;
-            reg[e] = (v < p.r1 && k < p.kdim) ? *reinterpret_cast<const float4*>(p.A + size_t(v) * p.astride + k)
-                                              : make_float4(0.f, 0.f, 0.f, 0.f);
+            r[e] = (v < p.r1 && k < p.kdim) ? ld4_ef(p.A + size_t(v) * p.astride + k, pol)
+                                            : make_float4(0.f, 0.f, 0.f, 0.f);
         }
     };
-    auto store_chunk = [&](uint32_t st) {
+    auto store_chunk = [&](uint32_t st, const float4 (&r)[4]) {
         uint8_t* hi = a_base + st * 2 * a_bytes;
         uint8_t* lo = hi + a_bytes;
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
             const uint32_t idx = tid + kXfThreads * e, m = idx >> 3, kc = idx & 7;
-            const float x[4] = {reg[e].x, reg[e].y, reg[e].z, reg[e].w};
+            const float x[4] = {r[e].x, r[e].y, r[e].z, r[e].w};
             float h[4], l[4];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
@@ -189,7 +202,8 @@ __global__ void __launch_bounds__(kXfThreads, 1) k_tc_xform(TcXformParams p) {
     };
 
     // epilogue of local tile j (accumulator j & 1): TMEM lanes 32 (warp % 4) .. +31 are
-    // rows, columns [half * npad / 2, (half + 1) * npad / 2) in groups of 8
+    // rows, columns [half * npad / 2, (half + 1) * npad / 2) in passes of up to 4 groups of
+    // 8: the pass's global loads (dh0) and TMEM loads are all issued before one wait
     auto epilogue = [&](uint32_t j) {
         const uint32_t acc = j & 1;
         mbar_wait(&bars[2 + acc], (j >> 1) & 1);
@@ -199,69 +213,91 @@ __global__ void __launch_bounds__(kXfThreads, 1) k_tc_xform(TcXformParams p) {
         const uint32_t row = 32 * q + lane, v = p.r0 + tile * kXfM + row;
         const bool valid = v < p.r1;
         const uint32_t vo = (!BWD && p.gnext && valid) ? p.orig[v] : 0u;
-        const uint32_t cw = npad / 2;
-        for (uint32_t c0 = half * cw; c0 < (half + 1) * cw; c0 += 8) {
-            float a[8];
-            tmem_ld8(tmem + ((32u * q) << 16) + acc * npad + c0, a);
-            if (!valid || c0 >= p.ostride) continue;
-            float o[8];
-            if (!BWD) {
-                float g[8];
+        const uint32_t cw = npad / 2, cbeg = half * cw, cend = min(cbeg + cw, p.ostride);
+        const uint32_t taddr = tmem + ((32u * q) << 16) + acc * npad;
+        for (uint32_t c1 = cbeg; c1 < half * cw + cw; c1 += 32) {
+            uint32_t a[4][8];
+            float4 d0[4][2];
 #pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    const uint32_t c = c0 + i;
-                    float val = 0.f;
-                    if (c < p.ndim) {
-                        val = __fadd_rn(a[i], bias_sh[c]);
-                        if (p.relu && val < 0.f) val = 0.f;
-                    }
-                    o[i] = val;
-                    g[i] = (p.gnext && c < p.ndim) ? drop_apply(p.next_mask, vo, c, val) : 0.f;
+            for (int gi = 0; gi < 4; ++gi) {
+                const uint32_t c0 = c1 + 8 * gi;
+                if (BWD && p.gcn2 && valid && c0 < cend) {
+                    const float* src = p.dh0 + size_t(v) * p.dh0stride + c0;
+                    d0[gi][0] = ld4_ef(src, pol);
+                    d0[gi][1] = ld4_ef(src + 4, pol);
                 }
-                float* dst = p.out + size_t(v) * p.ostride + c0;
-                st_v4_ef(dst, o[0], o[1], o[2], o[3], pol);
-                st_v4_ef(dst + 4, o[4], o[5], o[6], o[7], pol);
-                if (p.gnext) {
-                    float* gd = p.gnext + size_t(v) * p.gnstride + c0;
-                    st_v4_ef(gd, g[0], g[1], g[2], g[3], pol);
-                    st_v4_ef(gd + 4, g[4], g[5], g[6], g[7], pol);
-                }
-            } else {
-                if (p.gcn2) {
-                    float* d0 = p.dh0 + size_t(v) * p.dh0stride + c0;
-                    float4 x0 = *reinterpret_cast<const float4*>(d0), x1 = *reinterpret_cast<const float4*>(d0 + 4);
-                    float d[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+                if (c0 < half * cw + cw) tmem_ld8_async(taddr + c0, a[gi]);  // warp-uniform
+            }
+            tmem_ld_wait();
+            if (!valid) continue;
+#pragma unroll
+            for (int gi = 0; gi < 4; ++gi) {
+                const uint32_t c0 = c1 + 8 * gi;
+                if (c0 >= cend) break;
+                float o[8];
+                if (!BWD) {
+                    float gn[8];
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
-                        const bool in = c0 + i < p.ndim;
-                        d[i] = in ? __fadd_rn(d[i], __fmul_rn(p.alpha, a[i])) : d[i];
-                        o[i] = in ? __fmul_rn(p.oma, a[i]) : 0.f;
+                        const uint32_t c = c0 + i;
+                        float val = 0.f;
+                        if (c < p.ndim) {
+                            val = __fadd_rn(__uint_as_float(a[gi][i]), bias_sh[c]);
+                            if (p.relu && val < 0.f) val = 0.f;
+                        }
+                        o[i] = val;
+                        gn[i] = (p.gnext && c < p.ndim) ? drop_apply(p.next_mask, vo, c, val) : 0.f;
                     }
-                    st_v4_ef(d0, d[0], d[1], d[2], d[3], pol);
-                    st_v4_ef(d0 + 4, d[4], d[5], d[6], d[7], pol);
+                    float* dst = p.out + size_t(v) * p.ostride + c0;
+                    st_v4_ef(dst, o[0], o[1], o[2], o[3], pol);
+                    st_v4_ef(dst + 4, o[4], o[5], o[6], o[7], pol);
+                    if (p.gnext) {
+                        float* gd = p.gnext + size_t(v) * p.gnstride + c0;
+                        st_v4_ef(gd, gn[0], gn[1], gn[2], gn[3], pol);
+                        st_v4_ef(gd + 4, gn[4], gn[5], gn[6], gn[7], pol);
+                    }
                 } else {
+                    if (p.gcn2) {
+                        float d[8] = {d0[gi][0].x, d0[gi][0].y, d0[gi][0].z, d0[gi][0].w,
+                                      d0[gi][1].x, d0[gi][1].y, d0[gi][1].z, d0[gi][1].w};
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) o[i] = c0 + i < p.ndim ? a[i] : 0.f;
+                        for (int i = 0; i < 8; ++i) {
+                            const bool in = c0 + i < p.ndim;
+                            const float av = __uint_as_float(a[gi][i]);
+                            d[i] = in ? __fadd_rn(d[i], __fmul_rn(p.alpha, av)) : d[i];
+                            o[i] = in ? __fmul_rn(p.oma, av) : 0.f;
+                        }
+                        float* dd = p.dh0 + size_t(v) * p.dh0stride + c0;
+                        st_v4_ef(dd, d[0], d[1], d[2], d[3], pol);
+                        st_v4_ef(dd + 4, d[4], d[5], d[6], d[7], pol);
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) o[i] = c0 + i < p.ndim ? __uint_as_float(a[gi][i]) : 0.f;
+                    }
+                    float* dst = p.bg + size_t(v) * p.ostride + c0;
+                    st_v4_ef(dst, o[0], o[1], o[2], o[3], pol);
+                    st_v4_ef(dst + 4, o[4], o[5], o[6], o[7], pol);
                 }
-                float* dst = p.bg + size_t(v) * p.ostride + c0;
-                st_v4_ef(dst, o[0], o[1], o[2], o[3], pol);
-                st_v4_ef(dst + 4, o[4], o[5], o[6], o[7], pol);
             }
         }
         asm volatile("tcgen05.fence::before_thread_sync;");
     };
 
     uint32_t g = 0;  // A chunks staged so far (stage = g & 1)
-    if (my_tiles > 0) load_chunk(blockIdx.x, 0);
+    load_chunk(0, reg[0]);
+    load_chunk(1, reg[1]);
     for (uint32_t j = 0; j < my_tiles; ++j) {
-        const uint32_t tile = blockIdx.x + j * gridDim.x, acc = j & 1;
+        const uint32_t acc = j & 1;
         for (uint32_t c = 0; c < nchunks; ++c, ++g) {
             const uint32_t st = g & 1;
             if (g >= 2) mbar_wait(&bars[st], ((g >> 1) - 1) & 1);  // the MMAs that read this stage are done
-            store_chunk(st);
-            // issue the next chunk's loads (this tile's next chunk or the next tile's first)
-            if (c + 1 < nchunks) load_chunk(tile, c + 1);
-            else if (j + 1 < my_tiles) load_chunk(tile + gridDim.x, 0);
+            if (st == 0) {  // register sets alternate with g (the indices must be compile-time)
+                store_chunk(0, reg[0]);
+                load_chunk(g + 2, reg[0]);
+            } else {
+                store_chunk(1, reg[1]);
+                load_chunk(g + 2, reg[1]);
+            }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncthreads();
             if (tid == 0) {

@@ -219,6 +219,26 @@ int gs_shuffle_chunk_order(uint32_t K, uint64_t epoch, uint64_t seed, uint32_t* 
     });
 }
 
+int gs_save_assignment(const char* path, uint32_t num_parts, const uint32_t* assignment, uint64_t n) {
+    return guarded([&]() {
+        if (!path || (n && !assignment)) throw std::invalid_argument("null argument");
+        save_assignment(path, num_parts, std::vector<uint32_t>(assignment, assignment + n));
+    });
+}
+
+int gs_load_assignment(const char* path, uint32_t* num_parts, uint32_t* assignment, uint64_t cap, uint64_t* n) {
+    return guarded([&]() {
+        if (!path) throw std::invalid_argument("null path");
+        auto [parts, a] = load_assignment(path);
+        if (num_parts) *num_parts = parts;
+        if (n) *n = a.size();
+        if (assignment) {
+            if (cap < a.size()) throw std::invalid_argument("gs_load_assignment: buffer too small");
+            std::memcpy(assignment, a.data(), a.size() * 4);
+        }
+    });
+}
+
 int gs_make_stage_assignment(uint32_t layers, uint32_t stages, uint32_t* ranges) {
     return guarded([&]() {
         auto sa = make_stage_assignment(layers, stages);

@@ -149,6 +149,10 @@ struct ChunkPlan {
 ChunkPlan make_chunks(const Graph& g, uint32_t num_chunks, uint64_t seed);
 ChunkPlan chunk_plan_from_assignment(VertexId n, std::vector<uint32_t> chunk_of);
 std::vector<uint32_t> shuffle_chunk_order(const ChunkPlan& plan, uint64_t epoch, uint64_t seed);
+// chunks.txt / parts.txt (partition.cpp:250-269): the part count on the first line, then
+// one part id per vertex line; load returns {parts, assignment}
+void save_assignment(const std::string& path, uint32_t num_parts, const std::vector<uint32_t>& assignment);
+std::pair<uint32_t, std::vector<uint32_t>> load_assignment(const std::string& path);
 
 // ---------------------------------------------------------------- model
 enum class ModelKind { GCN, Sage, GCNII };

@@ -172,12 +172,25 @@ def make_big(name, td):
     print(name, sorted(d)[:6], "...")
 
 
+def golden_assignments(td):
+    """chunks.txt / parts.txt written by the reference's save_assignment (partition.cpp:250-256)."""
+    d = run_ref("assign", os.path.join(td, "assign.blob"), spec=ER500, K=4, seed=5, dir=td)
+    files = {}
+    for name in ("chunks.txt", "parts.txt"):
+        with open(os.path.join(td, name)) as f:
+            files["file_" + name.replace(".", "_")] = np.array(f.read())
+    np.savez_compressed(os.path.join(HERE, "assign_er500_k4.npz"), **files, chunk_of=d["chunk_of"])
+    print("assignments", sorted(files))
+
+
 def main():
     names = sys.argv[1:]
     with tempfile.TemporaryDirectory() as td:
         if names:  # only the named scenarios (the full-size ones take minutes each on one core)
             for n in names:
-                if n in BIG:
+                if n == "assignments":
+                    golden_assignments(td)
+                elif n in BIG:
                     make_big(n, td)
                 else:
                     cmd, kw = SCENARIOS[n]
@@ -187,6 +200,7 @@ def main():
             return
         golden_analytics(td)
         golden_checkpoints(td)
+        golden_assignments(td)
         for name in BIG:
             make_big(name, td)
         for name, (cmd, kw) in SCENARIOS.items():

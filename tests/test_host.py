@@ -173,3 +173,29 @@ def test_dataset_binary_csr_cache_round_trip(tmp_path):
     c = gp.Dataset.load(str(d))
     for x, y in zip(b.graph(), c.graph()):
         assert np.array_equal(x, y)
+
+
+def test_assignment_files_match_reference_bytes(gp, tmp_path):
+    """save_assignment / load_assignment (partition.cpp:250-269): chunks.txt and parts.txt byte-equal
+    to the reference writer's, and loading either gives back the plan."""
+    import os
+
+    import numpy as np
+    ref = dict(np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "assign_er500_k4.npz")))
+    ds = gp.Dataset.synthetic_er(500, 0.02, 3, 16, 5, 9)
+    co = gp.make_chunks(ds, 4, 5)
+    part, _, _ = gp.partition_vertices(ds, 4, 5)
+    for name, arr in (("chunks.txt", co), ("parts.txt", part)):
+        path = str(tmp_path / name)
+        gp.save_assignment(path, 4, arr)
+        assert open(path).read() == str(ref["file_" + name.replace(".", "_")]), name
+        parts, back = gp.load_assignment(path)
+        assert parts == 4 and np.array_equal(back, arr)
+    ref_path = tmp_path / "ref_chunks.txt"
+    ref_path.write_text(str(ref["file_chunks_txt"]))
+    parts, back = gp.load_assignment(str(ref_path))
+    assert parts == 4 and np.array_equal(back, ref["chunk_of"])
+    bad = tmp_path / "bad.txt"
+    bad.write_text("x\n")
+    with pytest.raises(gp.GnnsimError):
+        gp.load_assignment(str(bad))
