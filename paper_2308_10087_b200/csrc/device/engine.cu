@@ -808,8 +808,8 @@ struct Stage {
         preload_kernels();
         if (const char* e = std::getenv("GP_PGRAD")) use_tc_pgrad = std::string(e) != "simt";
         GP_CUDA(cudaFuncSetAttribute(k_pgrad_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        GP_CUDA(cudaFuncSetAttribute(k_tc_xform<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        GP_CUDA(cudaFuncSetAttribute(k_tc_xform<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        GP_CUDA(cudaFuncSetAttribute(k_tc_xform<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kXfSmemMax)));
+        GP_CUDA(cudaFuncSetAttribute(k_tc_xform<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kXfSmemMax)));
         if (const char* e = std::getenv("GP_NB")) {
             const int v = std::atoi(e);
             if (v == 2 || v == 4) nb = v;
@@ -1744,8 +1744,11 @@ struct Stage {
                                 prev == PREV_SAGE_HIST
                             ? GP_K_BWD_AGG
                             : GP_K_BWD_DENSE;
-        // SageConv layers (2*din-wide dagg) and SageConv neighbours always run split
-        if ((split_rows && cls == GP_K_BWD_AGG) || d.sage || prev == PREV_SAGE || prev == PREV_SAGE_HIST) {
+        // SageConv layers (2*din-wide dagg) and SageConv neighbours always run split; so do
+        // tcgen05 layers whatever feeds their gradient (a stage's last layer, PREV_TOP, too),
+        // so a layer's arithmetic never depends on where the stage boundaries fall
+        if ((split_rows && (cls == GP_K_BWD_AGG || (d.tc && p.need_dagg))) || d.sage || prev == PREV_SAGE ||
+            prev == PREV_SAGE_HIST) {
             // gather (+ mask, dh0 term, ReLU) -> dz, then dz.W^T + mixes -> bg, dh0
             const double ab = e * 8.0 + double(n) * d.dout * 4.0 + double(rows) * d.dout * 8.0;
             launch(cls, ab, 2.0 * e * d.dout, gather, [&]() {
