@@ -411,20 +411,23 @@ def main():
     gather_rate = fa["gather_bytes"] / (fa["ms"] / 1e3) / 1e9 if fa["ms"] > 0 else None
     # DRAM bytes per launch of the dominant kernel from one committed `ncu --set full`
     # capture of the same kernel build, scaled from its rows to the rows of one chunk launch
+    # DRAM bytes per launch of the dominant kernel from a committed `ncu --set full` capture
+    # of the same build at this workload (tools/roofline_capture.py); K = 4 chunk launches
     traffic, traffic_src = None, None
     tp = os.path.join(ROOT, "profiles", "roofline_traffic.json")
     if os.path.exists(tp):
         t = json.load(open(tp)).get(args.workload)
-        if t:
-            traffic = t["dram_bytes_per_row"] * N / K
+        if t and "dram_bytes_per_launch" in t:
+            traffic = t["dram_bytes_per_launch"] * 4.0 / K
             traffic_src = t["source"]
-    # the binding roof of the gather: random padded-row gathers from an L2-resident table,
-    # measured by tools/l2_gather_bench.cu (profiles/gather_ceiling.json)
+    # the binding roof of the gather: uniformly random padded-row gathers from a table of
+    # this workload's shape, measured by tools/gather_ceiling.cu (profiles/gather_ceiling.json)
     ceiling, ceiling_src = None, None
     cp = os.path.join(ROOT, "profiles", "gather_ceiling.json")
     if os.path.exists(cp):
-        c = json.load(open(cp))
-        ceiling, ceiling_src = c.get("gbs"), c.get("source")
+        c = json.load(open(cp)).get(args.workload)
+        if c:
+            ceiling, ceiling_src = c.get("gbs"), c.get("source")
     alg_per_launch = fa["alg_bytes"] / fa["launches"] if fa["launches"] else None
     agg_layers = sum(1 for s in specs if s.aggregates)
     edges_per_s = 2.0 * (E2) * agg_layers * 2 / (ms_step / 1e3)
@@ -440,7 +443,8 @@ def main():
         "e2e": e2e,
         "gpu_launches": int(launches),
         "edges_per_s": edges_per_s,
-        "roofline": {"kernel": "k_fwd8<FWD_GCN2, split> (CSR SpMM gather + GCNII initial-residual mix -> pre; the transform runs in k_fwd_tile)",
+        "roofline": {"kernel": "k_fwd8<FWD_GCN|FWD_GCN2, 2, split> (CSR SpMM gather [+ GCNII initial-residual mix] -> pre; "
+                               "the transform runs in k_tc_xform on tcgen05)",
                      "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": (achieved / hbm) if achieved else None, "peak_source": src,
                      # DRAM read + write bytes per launch (ncu) next to the algorithmic bytes per launch
