@@ -12,6 +12,7 @@
 //   stage messages    :690-724  -> Transport (local D2D, CUDA-IPC peer rings, or NCCL)
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <nccl.h>  // types and the config initializer only; libnccl.so.2 is dlopen'ed
 #include <dlfcn.h>
 #include <unistd.h>
 
@@ -76,6 +77,14 @@ struct NcclApi {
     void* recv = nullptr;
     Group group_start = nullptr, group_end = nullptr;
     ErrStr err = nullptr;
+    // non-blocking communicators: init with a watchdog instead of blocking forever on
+    // a peer that never joins (NCCL >= 2.14)
+    typedef int (*CommInitRankConfig)(void**, int, ncclUniqueId, int, ncclConfig_t*);
+    typedef int (*CommGetAsyncError)(void*, int*);
+    typedef int (*CommAbort)(void*);
+    CommInitRankConfig init_config = nullptr;
+    CommGetAsyncError async_error = nullptr;
+    CommAbort abort_comm = nullptr;
     bool load() {
         if (h) return true;
         h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
@@ -88,6 +97,9 @@ struct NcclApi {
         group_start = (Group)dlsym(h, "ncclGroupStart");
         group_end = (Group)dlsym(h, "ncclGroupEnd");
         err = (ErrStr)dlsym(h, "ncclGetErrorString");
+        init_config = (CommInitRankConfig)dlsym(h, "ncclCommInitRankConfig");
+        async_error = (CommGetAsyncError)dlsym(h, "ncclCommGetAsyncError");
+        abort_comm = (CommAbort)dlsym(h, "ncclCommAbort");
         return get_unique_id && comm_init_rank && comm_destroy && send && recv && group_start &&
                group_end;
     }
@@ -102,8 +114,57 @@ typedef int (*NcclRecvFn)(void*, size_t, int, int, void*, cudaStream_t);
 constexpr int kNcclFloat = 7;  // ncclFloat32
 
 void nccl_check(int r, const char* what) {
-    if (r != 0)
+    if (r != 0 && r != ncclInProgress)
         throw Error(GP_ECUDA, std::string(what) + ": " + (g_nccl.err ? g_nccl.err(r) : "nccl error"));
+}
+
+// Seconds a non-blocking NCCL operation may stay in progress (GP_NCCL_TIMEOUT, default 120).
+double nccl_timeout() {
+    const char* e = std::getenv("GP_NCCL_TIMEOUT");
+    return e ? std::atof(e) : 120.0;
+}
+
+// Poll a non-blocking communicator until its pending operation (init, or the enqueue of a
+// grouped send/recv) leaves ncclInProgress; abort it and raise GP_EFABRIC on a timeout (a
+// peer that never joins) and GP_ECUDA on an NCCL error (e.g. two ranks on one device).
+void nccl_wait(void*& comm, const char* what) {
+    const auto t0 = std::chrono::steady_clock::now();
+    for (;;) {
+        int state = 0;
+        const int r = g_nccl.async_error(comm, &state);
+        if (r != 0) state = r;
+        if (state == 0) return;
+        if (state != ncclInProgress) {
+            g_nccl.abort_comm(comm);
+            comm = nullptr;
+            throw Error(GP_ECUDA, std::string(what) + ": " + (g_nccl.err ? g_nccl.err(state) : "nccl error"));
+        }
+        if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > nccl_timeout()) {
+            g_nccl.abort_comm(comm);
+            comm = nullptr;
+            throw Error(GP_EFABRIC, std::string(what) + ": timed out after " + std::to_string(nccl_timeout()) +
+                                        " s (GP_NCCL_TIMEOUT; the peer rank never joined)");
+        }
+        std::this_thread::sleep_for(std::chrono::milliseconds(1));
+    }
+}
+
+// One 2-rank communicator per stage boundary, created non-blocking.
+void* nccl_comm_init(const uint8_t* id_bytes, int rank, const char* what) {
+    if (!g_nccl.init_config || !g_nccl.async_error || !g_nccl.abort_comm)
+        throw Error(GP_ECUDA, "libnccl.so.2 lacks the non-blocking communicator API (NCCL >= 2.14)");
+    ncclUniqueId id;
+    std::memcpy(&id, id_bytes, sizeof(id));
+    ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+    cfg.blocking = 0;
+    void* comm = nullptr;
+    const int r = g_nccl.init_config(&comm, 2, id, rank, &cfg);
+    if (r != 0 && r != ncclInProgress) {
+        if (comm) g_nccl.abort_comm(comm);
+        throw Error(GP_ECUDA, std::string(what) + ": " + (g_nccl.err ? g_nccl.err(r) : "nccl error"));
+    }
+    nccl_wait(comm, what);
+    return comm;
 }
 
 // ------------------------------------------------------------------ stream memory ops
@@ -2028,6 +2089,7 @@ struct Stage {
                 nccl_check(((NcclRecvFn)g_nccl.recv)(p.ptr, p.floats, kNcclFloat, peer, comm, st), "ncclRecv");
         }
         nccl_check(g_nccl.group_end(), "ncclGroupEnd");
+        nccl_wait(comm, send ? "ncclSend" : "ncclRecv");  // non-blocking comm: enqueued
         cudaEvent_t done = pool_event();
         GP_CUDA(cudaEventRecord(done, st));
         GP_CUDA(cudaStreamWaitEvent(cs, done, 0));
@@ -3180,17 +3242,13 @@ gp_status gp_link_nccl(gp_ctx* ctx, const uint8_t* up_id, const uint8_t* down_id
         auto& st = ctx->st;
         if (!gp::g_nccl.load()) throw gp::Error(GP_ECUDA, "libnccl.so.2 not loadable");
         GP_CUDA(cudaSetDevice(st.device));
-        auto init = (gp::NcclInitFn)gp::g_nccl.comm_init_rank;
+        if (st.S < 2) throw gp::Error(GP_EINVAL, "gp_link_nccl: a single-stage pipeline has no boundary");
         if (up_id && !st.first) {
-            gp::NcclId id;
-            std::memcpy(id.b, up_id, 128);
-            gp::nccl_check(init(&st.tr.up_comm, 2, id, 1), "ncclCommInitRank(up)");
+            st.tr.up_comm = gp::nccl_comm_init(up_id, 1, "ncclCommInitRankConfig(up)");
             GP_CUDA(cudaStreamCreateWithFlags(&st.tr.up_stream, cudaStreamNonBlocking));
         }
         if (down_id && !st.last) {
-            gp::NcclId id;
-            std::memcpy(id.b, down_id, 128);
-            gp::nccl_check(init(&st.tr.down_comm, 2, id, 0), "ncclCommInitRank(down)");
+            st.tr.down_comm = gp::nccl_comm_init(down_id, 0, "ncclCommInitRankConfig(down)");
             GP_CUDA(cudaStreamCreateWithFlags(&st.tr.down_stream, cudaStreamNonBlocking));
         }
     });
