@@ -23,6 +23,12 @@ from paper_2308_10087_b200 import distributed as D  # noqa: E402
 ER500 = (500, 0.02, 3, 16, 5, 9)
 
 
+def dataset(case):
+    if case.get("data") == "powerlaw":  # tests/golden/powerlaw_2k (Chung-Lu, max degree 822)
+        return gp.Dataset.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "powerlaw_2k"))
+    return gp.Dataset.synthetic_er(*ER500)
+
+
 def main():
     out, case = sys.argv[1], json.loads(sys.argv[2])
     kind, L, H, S, G, K = case["kind"], case["L"], case["H"], case["S"], case["G"], case["K"]
@@ -32,7 +38,7 @@ def main():
     w, W = dist.get_rank(), dist.get_world_size()
     assert W == S * G
     s, r = w // G, w % G
-    ds = gp.Dataset.synthetic_er(*ER500)
+    ds = dataset(case)
     part, _, _ = gp.partition_vertices(ds, G, case["ps"])
     chunk_of = gp.make_chunks(ds, K, case["cs"])
     model = gp.ModelConfig(kind=kind, layers=L, hidden=H)

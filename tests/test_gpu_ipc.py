@@ -112,11 +112,14 @@ HYB_IPC = [
     dict(kind=2, L=5, H=16, S=1, G=3, K=3, cs=5, ps=3, epochs=4, seed=44, sync=True),
     dict(kind=0, L=6, H=12, S=2, G=2, K=6, cs=7, ps=4, epochs=4, seed=45, fix_alpha=2, hist=True),
     dict(kind=1, L=4, H=16, S=2, G=2, K=4, cs=3, ps=1, epochs=4, seed=48, fix_alpha=3),
+    # BASELINE configs[4]'s shape in miniature: 4 stages x 2 graph partitions (8 worker
+    # processes), GCNII, K = 16, power-law graph
+    dict(kind=2, L=8, H=16, S=4, G=2, K=16, cs=3, ps=1, epochs=4, seed=51, fix_alpha=3, data="powerlaw"),
 ]
 
 
 @pytest.mark.parametrize("case", HYB_IPC, ids=[f"k{c['kind']}_s{c['S']}g{c['G']}{'_hist' if c.get('hist') else ''}"
-                                               for c in HYB_IPC])
+                                               f"{'_' + c['data'] if c.get('data') else ''}" for c in HYB_IPC])
 def test_ipc_hybrid_processes_match_in_process_hybrid(gp, tmp_path, case):
     """S x G worker processes (gp_link_group_ipc + gp_link_ipc) == train_hybrid in one
     process (gp_link_group + gp_link_local), bit for bit."""
@@ -129,7 +132,8 @@ def test_ipc_hybrid_processes_match_in_process_hybrid(gp, tmp_path, case):
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     z = np.load(out)
-    ds = gp.Dataset.synthetic_er(500, 0.02, 3, 16, 5, 9)
+    import ipc_hybrid_worker as HW
+    ds = HW.dataset(case)
     part, _, _ = gp.partition_vertices(ds, case["G"], case["ps"])
     co = gp.make_chunks(ds, case["K"], case["cs"])
     kw = {}

@@ -34,7 +34,9 @@ def main():
     ap.add_argument("--tag", default="r2")
     a = ap.parse_args()
     out = os.path.join(ROOT, "gpurun_out", f"{a.tag}_ncu_fwd_{a.workload}")
-    cmd = ["ncu", "--set", "full", "--clock-control", "none", "--import-source", "on", "-k", "regex:k_fwd8",
+    # the aggregating layers' gather (k_fwd8<FWD_GCN = 1 | FWD_GCN2 = 2, ...>), not the Dense layers'
+    cmd = ["ncu", "--set", "full", "--clock-control", "none", "--kernel-name-base", "demangled",
+           "-k", "regex:k_fwd8<[^,]*[12],",
            "--launch-skip", str(a.skip), "-c", "8", "-f", "-o", out, sys.executable, "bench.py", "--workload",
            a.workload, "--steps", "1", "--warmup", "1", "--no-e2e", "--no-cpu-baseline"]
     if a.layers:
@@ -42,20 +44,28 @@ def main():
     subprocess.run(cmd, cwd=ROOT, check=True, stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
     raw = subprocess.run(["ncu", "-i", out + ".ncu-rep", "--page", "raw", "--csv"], capture_output=True, text=True,
                          check=True).stdout
+    details = subprocess.run(["ncu", "-i", out + ".ncu-rep", "--page", "details", "--csv"], capture_output=True,
+                             text=True, check=True).stdout
+    with open(out + "_details.csv", "w") as f:  # the text summary travels back; the report is large
+        f.write(details)
+    os.remove(out + ".ncu-rep")
     r = csv.reader(io.StringIO(raw))
     head = next(r)
-    next(r)  # units
+    units = dict(zip(head, next(r)))
     rows = [dict(zip(head, x)) for x in r]
-    f = lambda d, k: float(d[k].replace(",", ""))
-    tot = [f(d, "dram__bytes_read.sum") + f(d, "dram__bytes_write.sum") for d in rows]
-    dur = [f(d, "gpu__time_duration.sum") for d in rows]
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1.0, "usecond": 1e3,
+             "msecond": 1e6, "second": 1e9, "ns": 1.0, "us": 1e3, "ms": 1e6, "s": 1e9, "%": 1.0}
+    f = lambda d, k: float(d[k].replace(",", "")) * scale.get(units.get(k, ""), 1.0)
+    tot = [f(d, "dram__bytes_read.sum") + f(d, "dram__bytes_write.sum") for d in rows]  # bytes
+    dur = [f(d, "gpu__time_duration.sum") for d in rows]  # ns
     hit = [f(d, "lts__t_sector_hit_rate.pct") for d in rows]
     N, stride = SHAPES[a.workload]
     entry = {"kernel": rows[0]["Kernel Name"], "launches": len(rows),
-             "dram_bytes_per_launch": sum(tot) / len(tot), "ncu_duration_us_mean": sum(dur) / len(dur) / 1e3,
+             "dram_bytes_per_launch": sum(tot) / len(tot), "ncu_duration_ms_mean": sum(dur) / len(dur) / 1e6,
              "l2_hit_pct_mean": sum(hit) / len(hit),
-             "source": f"{os.path.relpath(out, ROOT)}.ncu-rep (ncu --set full --clock-control none, launches "
-                       f"{a.skip + 1}-{a.skip + 8} of k_fwd8 = 8 layers of one chunk; K = 4 chunks)"}
+             "source": f"profiles/{os.path.basename(out)}_details.csv (ncu --set full --clock-control none, launches "
+                       f"{a.skip + 1}-{a.skip + 8} of the aggregating k_fwd8 = consecutive layers of one chunk; "
+                       f"K = 4 chunks)"}
     update(os.path.join(ROOT, "profiles", "roofline_traffic.json"), a.workload, entry)
     print(json.dumps({a.workload: entry}))
     g = subprocess.run([os.path.join(ROOT, "tools", "gather_ceiling"), a.workload, str(N + 1), str(stride)],
