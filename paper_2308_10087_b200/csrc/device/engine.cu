@@ -712,7 +712,7 @@ struct Stage {
                 d.xf_bwd = dalloc<float>(2 * size_t(xf_pad8k(d.dout)) * xf_pad16(d.din));
             }
             d.h = dalloc<float>(size_t(n) * d.sout);
-            d.pre = dalloc<float>(size_t(n) * d.skw);
+            if (G == 1 || arena_sizing) d.pre = own_rows_alloc(d.skw);  // G > 1: at graph upload
             d.dz = lean ? d.h : dalloc<float>(size_t(n) * d.sout);
             // gather tables carry one extra all-zero row (row n, see gather_row)
             if (d.agg) {
@@ -733,13 +733,8 @@ struct Stage {
         if (!first) {
             in_cur = dalloc<float>(size_t(n) * sin0);
             if (!sync && L[0].agg) in_snap = dalloc<float>(size_t(n) * sin0);
-            dh_in = dalloc<float>(size_t(n) * sin0);
-            if (needs_h0) h0 = dalloc<float>(size_t(n) * pad8(H));
         }
-        if (needs_h0) dh0 = dalloc<float>(size_t(n) * pad8(H));
-        // lean: a chunk's incoming gradient (dtop, read first in its backward) and its
-        // outgoing one (dh_in, written last) share rows when their strides agree
-        dtop = lean && dh_in && L[len - 1].sout == sin0 ? dh_in : dalloc<float>(size_t(n) * L[len - 1].sout);
+        if (G == 1 || arena_sizing) alloc_own_stage_rows();  // G > 1: at graph upload
         // pgrad workspace: ~2 waves of CTAs
         splits = std::max<uint32_t>(1, std::min<uint32_t>(2 * num_sms, (n + 63) / 64));
         size_t wmax = 1;
@@ -753,6 +748,48 @@ struct Stage {
         red_correct = dalloc<unsigned long long>(3);
         tickets = dalloc<uint32_t>(kTickets);
         if (!arena_sizing) GP_CUDA(cudaDeviceSynchronize());
+    }
+
+    // ---- owner-row buffers ---------------------------------------------------
+    // pre, the received h0, dh0 and the incoming / outgoing chunk gradients are only ever
+    // touched at this worker's own rows. A hybrid worker (G > 1) allocates them for its own
+    // rows [own_begin, own_end) only, once the partition is known (graph upload), and keeps
+    // a base pointer offset by own_begin rows, so every kernel indexes them by global row as
+    // before. The layout pass (gp_stage_footprint) sizes them at the partitioner's balance
+    // cap max(ceil(N/G), floor(1.05 N/G)) (partition.cpp:183-187).
+    uint32_t own_rows_planned() const {
+        if (G == 1) return n;
+        if (graph_ready || !bstart.empty()) return own_end() - own_begin();
+        return std::min<uint32_t>(n, std::max<uint32_t>((n + G - 1) / G, uint32_t(1.05 * double(n) / G)));
+    }
+    float* own_rows_alloc(uint32_t stride) {
+        const uint32_t rows = own_rows_planned();
+        float* base = dalloc<float>(size_t(rows) * stride);
+        if (arena_sizing || G == 1) return base;
+        return base - size_t(own_begin()) * stride;
+    }
+    void alloc_own_stage_rows() {
+        if (!first) {
+            dh_in = own_rows_alloc(sin0);
+            if (needs_h0) h0 = own_rows_alloc(pad8(H));
+        }
+        if (needs_h0) dh0 = own_rows_alloc(pad8(H));
+        // lean: a chunk's incoming gradient (dtop, read first in its backward) and its
+        // outgoing one (dh_in, written last) share rows when their strides agree
+        dtop = lean && dh_in && L[len - 1].sout == sin0 ? dh_in : own_rows_alloc(L[len - 1].sout);
+    }
+    // G > 1, after the partition renumbering: the owner-row buffers
+    void ensure_own_buffers() {
+        if (G == 1 || dtop) return;
+        for (auto& d : L) d.pre = own_rows_alloc(d.skw);
+        alloc_own_stage_rows();
+    }
+    bool own_only(const float* p) const {
+        if (G == 1 || !p) return false;
+        if (p == dh0 || p == h0 || p == dh_in || p == dtop) return true;
+        for (const auto& d : L)
+            if (p == d.pre) return true;
+        return false;
     }
 
     // Work counters of the dynamically scheduled row kernels (one per launch).
@@ -1242,6 +1279,7 @@ struct Stage {
         bstart = hg->bstart;
         build_halo();
         build_id_rows();
+        ensure_own_buffers();
         graph_ready = true;
     }
 
@@ -1311,6 +1349,7 @@ struct Stage {
         nnz = o.nnz;
         build_halo();
         build_id_rows();
+        ensure_own_buffers();
         graph_ready = true;
     }
 
@@ -2849,7 +2888,9 @@ struct Stage {
             launch(GP_K_XENT, 0, 0, 0, [&]() {
                 k_xent_fold<<<1, 32, 0, cs>>>(part_loss, part_correct, xent_blocks, red_loss, red_correct);
             });
-            if (needs_h0) zero_words(reinterpret_cast<uint32_t*>(dh0), size_t(n) * pad8(H));
+            if (needs_h0)
+                zero_words(reinterpret_cast<uint32_t*>(dh0 + size_t(own_begin()) * pad8(H)),
+                           size_t(own_end() - own_begin()) * pad8(H));
         }
 
         // ---- backward ---------------------------------------------------------------
@@ -3064,8 +3105,12 @@ struct Stage {
         // SageConv pre / dagg: k_in = 2 din columns, halves at 0 and gap
         const uint32_t ow = gap ? 2 * width : width;
         if (count != uint64_t(n) * ow) throw Error(GP_EINVAL, "count != N * width");
-        std::vector<float> tmp(size_t(n) * stride);
-        GP_CUDA(cudaMemcpy(tmp.data(), src, tmp.size() * 4, cudaMemcpyDeviceToHost));
+        std::vector<float> tmp(size_t(n) * stride, 0.f);
+        if (own_only(src))  // a hybrid worker's owner-row buffer: other rows read as zero
+            GP_CUDA(cudaMemcpy(tmp.data() + size_t(own_begin()) * stride, src + size_t(own_begin()) * stride,
+                               size_t(own_end() - own_begin()) * stride * 4, cudaMemcpyDeviceToHost));
+        else
+            GP_CUDA(cudaMemcpy(tmp.data(), src, tmp.size() * 4, cudaMemcpyDeviceToHost));
         for (uint32_t r = 0; r < n; ++r) {
             std::memcpy(out + size_t(inv[r]) * ow, &tmp[size_t(r) * stride], size_t(width) * 4);
             if (gap) std::memcpy(out + size_t(inv[r]) * ow + width, &tmp[size_t(r) * stride + gap], size_t(width) * 4);
