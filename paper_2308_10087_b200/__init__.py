@@ -234,6 +234,7 @@ def _L():
         "gp_upload_history": (C.c_int, [vp, C.c_uint32, C.c_uint32, f32p, C.c_uint64, C.c_uint32]),
         "gp_stage_footprint": (C.c_int, [P(gp_stage_config), C.c_uint64, C.c_uint32, u64p]),
         "gp_set_profiling": (C.c_int, [vp, C.c_int]),
+        "gp_set_live_timing": (C.c_int, [vp, C.c_int]),
         "gp_get_profile": (C.c_int, [vp, P(gp_profile)]),
         "gp_reset_profile": (C.c_int, [vp]),
         "gp_device_bytes": (C.c_int, [vp, u64p]),
@@ -894,6 +895,11 @@ class StageEngine:
 
     def set_profiling(self, on: bool = True):
         _L().gp_set_profiling(self._h, int(on))
+
+    def set_live_timing(self, kernel_class: Optional[str]):
+        """Events around every launch of one kernel class during normal epochs (None = off)."""
+        cls = -1 if kernel_class is None else PROFILE_CLASSES.index(kernel_class)
+        _gp(_L().gp_set_live_timing(self._h, cls), self._h)
 
     def reset_profile(self):
         _L().gp_reset_profile(self._h)

@@ -439,6 +439,9 @@ struct Stage {
     Transport tr;
     // profiling
     bool profiling = false;
+    // gp_set_live_timing: CUDA events around every launch of one kernel class during normal
+    // (wavefront) epochs, accumulated like the profiling epoch's; -1 = off
+    int live_cls = -1;
 
     // ---- trace (FabricOptions::collect_trace, fabric.cpp:222-227, :256-264) ----
     // Per epoch: one anchor (event + %globaltimer stamp) and a pair of timing
@@ -1544,7 +1547,7 @@ struct Stage {
     template <typename F>
     void launch(int cls, double bytes, double flops, double gather, F&& fn) {
         ++launches;
-        if (!profiling) {
+        if (!profiling && cls != live_cls) {
             fn();
             GP_CUDA(cudaGetLastError());
             return;
@@ -3356,6 +3359,12 @@ gp_status gp_upload_history(gp_ctx* ctx, uint32_t which, uint32_t local_layer, c
                             uint32_t resume_epoch) {
     if (!ctx || !rows) return GP_EINVAL;
     return gp::guard(&ctx->st, [&]() { ctx->st.upload_history(which, local_layer, rows, count, resume_epoch); });
+}
+
+gp_status gp_set_live_timing(gp_ctx* ctx, int kernel_class) {
+    if (!ctx || kernel_class < -1 || kernel_class >= GP_K_NUM) return GP_EINVAL;
+    ctx->st.live_cls = kernel_class;
+    return GP_OK;
 }
 
 gp_status gp_set_profiling(gp_ctx* ctx, int enable) {

@@ -362,6 +362,14 @@ int main(int argc, char** argv) {
         run("k_fwd8<GCN2,4> (engine)", (const void*)k_fwd8<FWD_GCN2, 4>, wsm, K);
         run("split gather k_fwd8<GCN2,2,1>", (const void*)k_fwd8<FWD_GCN2, 2, true>, kEdgeSlotBytes, K);
         run("split gather k_fwd8<GCN2,4,1>", (const void*)k_fwd8<FWD_GCN2, 4, true>, kEdgeSlotBytes, K);
+        // gathers in flight vs resident CTAs (MINB = minimum CTAs per SM for the register cap)
+        run("split gather k_fwd8<GCN2,2,1,5> (engine)", (const void*)k_fwd8<FWD_GCN2, 2, true, 5>, kEdgeSlotBytes, K);
+        run("split gather k_fwd8<GCN2,2,1,6>", (const void*)k_fwd8<FWD_GCN2, 2, true, 6>, kEdgeSlotBytes, K);
+        run("split gather k_fwd8<GCN2,4,1,4>", (const void*)k_fwd8<FWD_GCN2, 4, true, 4>, kEdgeSlotBytes, K);
+        run("split gather k_fwd8<GCN2,4,1,3>", (const void*)k_fwd8<FWD_GCN2, 4, true, 3>, kEdgeSlotBytes, K);
+        run("split gather k_fwd8<GCN2,8,1,3>", (const void*)k_fwd8<FWD_GCN2, 8, true, 3>, kEdgeSlotBytes, K);
+        run("split gather k_fwd8<GCN2,8,1,2>", (const void*)k_fwd8<FWD_GCN2, 8, true, 2>, kEdgeSlotBytes, K);
+        run("split gather k_fwd8<GCN2,16,1,2>", (const void*)k_fwd8<FWD_GCN2, 16, true, 2>, kEdgeSlotBytes, K);
         run("split dense k_fwd_tile<1,4>", (const void*)k_fwd_tile<true, 4>, tile_smem_bytes(H, H, 4), K);
         run("split dense k_fwd_tile<1,4,100>", (const void*)k_fwd_tile<true, 4, 100>, tile_smem_bytes(H, H, 4), K);
         {  // cost of the next-layer dropout epilogue: same transform without gnext
