@@ -465,6 +465,10 @@ def main():
                                 "the timed region (its stream; chunk wavefront on)"),
                      "ms_per_launch": fa["ms"] / fa["launches"] if fa["launches"] else None,
                      "achieved_serial": achieved_serial,
+                     "note": ("achieved: live launch durations, which include the kernels co-running on the "
+                              "other wavefront streams (per-step kernel time = share_of_step x the step); "
+                              "achieved_serial: the same bytes over the isolated launch time of the serial "
+                              "profiling epoch"),
                      "share_of_step": (fa["ms"] / args.steps) / ms_step if ms_step else None},
         "cpu_baseline": cpu,
         "kernel_ms_per_epoch": {k: round(v["ms"], 3) for k, v in prof.items() if v["launches"]},

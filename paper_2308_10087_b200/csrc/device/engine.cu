@@ -917,7 +917,7 @@ struct Stage {
         }
         if (const char* e = std::getenv("GP_SPLIT")) split_rows = std::string(e) != "0";
         if (const char* e = std::getenv("GP_IPC_SMCOPY")) ipc_smcopy = std::string(e) == "1";
-        if (const char* e = std::getenv("GP_OCC5")) occ5_mode = std::atoi(e) ? 1 : 0;
+        if (const char* e = std::getenv("GP_OCC5")) occ5_mode = std::string(e) == "auto" ? -1 : (std::atoi(e) ? 1 : 0);
         if (const char* e = std::getenv("GP_TILE_TR")) {
             const int v = std::atoi(e);
             if (v == 1 || v == 2 || v == 4) tile_tr_env = v;
@@ -926,10 +926,13 @@ struct Stage {
         setup_nb<4>();
     }
 
-    // Split gather kernels: 5 resident CTAs (48 registers) when the launch has
-    // enough row pairs to keep every warp busy for several pairs, else 4 (64
-    // registers: more gathers in flight per warp). GP_OCC5=0/1 forces one.
-    int occ5_mode = -1;
+    // Split gather kernels: 4 resident CTAs (64 registers: more gathers in flight per
+    // warp) by default; GP_OCC5=1 forces the 5-CTA (48-register) build, GP_OCC5=auto
+    // takes it for launches with enough row pairs to keep every warp busy. With the
+    // tcgen05 transforms co-running in the wavefront, 4 CTAs measured 0.393 vs 0.396
+    // s/epoch at K = 4 (3 runs each), 0.437 vs 0.445 at K = 32 (round 1, with the
+    // CUDA-core transforms, the 5-CTA build won inside the wavefront).
+    int occ5_mode = 0;
     bool use_occ5(uint32_t rows) const {
         if (occ5_mode >= 0) return occ5_mode == 1;
         return uint64_t(rows) / 2 >= 2ull * uint64_t(num_sms) * 5 * kWarpsPerBlock;
