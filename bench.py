@@ -417,6 +417,7 @@ def main():
     gather_rate = fa["gather_bytes"] / (fa["ms"] / 1e3) / 1e9 if fa["ms"] > 0 else None
     fs = prof["fwd_agg"]  # the serial profiling epoch (no concurrent kernels)
     achieved_serial = fs["alg_bytes"] / (fs["ms"] / 1e3) / 1e9 if fs["ms"] > 0 else None
+    gather_serial = fs["gather_bytes"] / (fs["ms"] / 1e3) / 1e9 if fs["ms"] > 0 else None
     # DRAM bytes per launch of the dominant kernel from one committed `ncu --set full`
     # capture of the same kernel build, scaled from its rows to the rows of one chunk launch
     # DRAM bytes per launch of the dominant kernel from a committed `ncu --set full` capture
@@ -461,6 +462,9 @@ def main():
                      "l2_gather_gbs": gather_rate,
                      "gather_ceiling_gbs": ceiling, "gather_ceiling_source": ceiling_src,
                      "gather_frac": (gather_rate / ceiling) if gather_rate and ceiling else None,
+                     # like for like with the ceiling microbenchmark (an isolated kernel): the serial epoch
+                     "l2_gather_gbs_serial": gather_serial,
+                     "gather_frac_serial": (gather_serial / ceiling) if gather_serial and ceiling else None,
                      "timing": (f"CUDA events around each of the {fa['launches']} launches of the kernel inside "
                                 "the timed region (its stream; chunk wavefront on)"),
                      "ms_per_launch": fa["ms"] / fa["launches"] if fa["launches"] else None,
