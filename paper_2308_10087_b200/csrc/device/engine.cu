@@ -2719,8 +2719,14 @@ struct Stage {
     // ---- chunk wavefront helpers ------------------------------------------------
     // W compute streams; chunk j runs on stream j % W. Off for hybrid groups (halo
     // exchange is ordered on one stream), K = 1, and in profiling mode (clean
-    // per-kernel times).
-    int wave_width() const { return G == 1 && K > 1 && !profiling && !tracing ? wave_w : 1; }
+    // per-kernel times). Merged gather tables rely on the one-stream order for hybrid
+    // groups: a halo pull overwrites chunk k's boundary rows of G_i, which earlier chunks
+    // gather as snapshot rows; on one stream those gathers are complete by then (with W > 1
+    // the pull would need the before_g_write ordering the producer epilogues get).
+    int wave_width() const {
+        static_assert(true, "hybrid groups (G > 1) run one stream: see the comment above");
+        return G == 1 && K > 1 && !profiling && !tracing ? wave_w : 1;
+    }
     cudaStream_t wave_stream(uint32_t j, int W, cudaStream_t main) const { return j % W ? cs_side[j % W] : main; }
     cudaEvent_t record_event() {
         cudaEvent_t e = pool_event();
