@@ -2723,10 +2723,7 @@ struct Stage {
     // groups: a halo pull overwrites chunk k's boundary rows of G_i, which earlier chunks
     // gather as snapshot rows; on one stream those gathers are complete by then (with W > 1
     // the pull would need the before_g_write ordering the producer epilogues get).
-    int wave_width() const {
-        static_assert(true, "hybrid groups (G > 1) run one stream: see the comment above");
-        return G == 1 && K > 1 && !profiling && !tracing ? wave_w : 1;
-    }
+    int wave_width() const { return G == 1 && K > 1 && !profiling && !tracing ? wave_w : 1; }
     cudaStream_t wave_stream(uint32_t j, int W, cudaStream_t main) const { return j % W ? cs_side[j % W] : main; }
     cudaEvent_t record_event() {
         cudaEvent_t e = pool_event();
