@@ -374,7 +374,6 @@ struct Stage {
     // GP_TC_XFORM=1 (default): the GCN / GCNII row transforms (pre.W', dz.W'^T and their
     // epilogues) run on tcgen05 (3xTF32, fp32-level); 0: the bit-exact CUDA-core tiles
     bool use_tc_xform = true;
-    bool tc_ws = true;  // GP_TC_XFORM=2: the single-role kernel (k_tc_xform) instead of k_tc_xform_ws
     bool state_restored = false;  // gp_set_history: the snapshot rows were loaded
     // forward wavefront hooks (merged_g): after the kernel gathering from G_i, and
     // before the kernel writing rows of G_i
@@ -614,10 +613,7 @@ struct Stage {
         if (needs_h0 && (H == 0 || H > kMaxWidth)) throw Error(GP_EINVAL, "bad hidden width");
         if (const char* e = std::getenv("GP_MERGED_G")) merged_g = std::atoi(e) != 0;
         if (const char* e = std::getenv("GP_LEAN")) lean = std::atoi(e) != 0;
-        if (const char* e = std::getenv("GP_TC_XFORM")) {
-            use_tc_xform = std::atoi(e) != 0;
-            tc_ws = std::atoi(e) != 2;
-        }
+        if (const char* e = std::getenv("GP_TC_XFORM")) use_tc_xform = std::atoi(e) != 0;
         if (plan_only) return;
         device = c.device;
         int ndev = 0;
@@ -896,8 +892,7 @@ struct Stage {
                              (const void*)k_spmm_pre,    (const void*)k_stamp,         (const void*)k_transpose,
                              (const void*)k_xent_fold,   (const void*)k_xent_grad,     (const void*)k_xent_stats,
                              (const void*)k_zero,        (const void*)k_sage_weights,  (const void*)k_tc_prep,
-                             (const void*)k_tc_xform<false>, (const void*)k_tc_xform<true>,
-                             (const void*)k_tc_xform_ws<false>, (const void*)k_tc_xform_ws<true>};
+                             (const void*)k_tc_xform<false>, (const void*)k_tc_xform<true>};
         for (const void* f : fns) {
             cudaFuncAttributes a;
             GP_CUDA(cudaFuncGetAttributes(&a, f));
@@ -916,8 +911,6 @@ struct Stage {
         GP_CUDA(cudaFuncSetAttribute(k_pgrad_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         GP_CUDA(cudaFuncSetAttribute(k_tc_xform<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kXfSmemMax)));
         GP_CUDA(cudaFuncSetAttribute(k_tc_xform<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kXfSmemMax)));
-        GP_CUDA(cudaFuncSetAttribute(k_tc_xform_ws<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kWsSmemMax)));
-        GP_CUDA(cudaFuncSetAttribute(k_tc_xform_ws<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kWsSmemMax)));
         if (const char* e = std::getenv("GP_NB")) {
             const int v = std::atoi(e);
             if (v == 2 || v == 4) nb = v;
@@ -1440,13 +1433,8 @@ struct Stage {
     template <bool BWD>
     void tc_xform_go(const TcXformParams& x) {
         const uint32_t ntiles = (x.r1 - x.r0 + kXfM - 1) / kXfM;
-        const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(ntiles, uint32_t(num_sms)));
-        if (tc_ws) {  // warp-specialised (default)
-            const size_t smem = std::max<size_t>(ws_smem_bytes(x.kpad, x.npad), 116 * 1024);
-            k_tc_xform_ws<BWD><<<grid, kWsThreads, smem, cs>>>(x);
-            return;
-        }
         const size_t smem = std::max<size_t>(xf_smem_bytes(x.kpad, x.npad), 116 * 1024);
+        const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(ntiles, uint32_t(num_sms)));
         k_tc_xform<BWD><<<grid, kXfThreads, smem, cs>>>(x);
     }
     TcXformParams tc_fwd_params(const LayerDev& d, const FwdParams& p) const {

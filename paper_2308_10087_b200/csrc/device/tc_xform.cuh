@@ -300,268 +300,4 @@ __global__ void __launch_bounds__(kXfThreads, 1) k_tc_xform(TcXformParams p) {
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
 }
 
-
-// ---------------------------------------------------------------------------
-// Warp-specialised version (default): the same GEMM and epilogues, with the three jobs on
-// separate warps so none waits for another's latency:
-//   warps 0-3   epilogue: TMEM lane quarter = warp, all npad columns of 32 rows each;
-//   warps 4-7   loaders: A chunks (128 rows x 32 columns) from global, hi/lo split, into a
-//               ring of kWsStages stages; two chunks of loads in flight per thread;
-//   warp 8      MMA issuer (one lane), also brings W' in with the TMA bulk-copy engine.
-// mbarriers: full[s] (4 loader warps arrive), empty[s] (tcgen05.commit after the MMAs that
-// read stage s), acc_full[a] (tcgen05.commit after a tile's last chunk), acc_empty[a] (4
-// epilogue warps arrive after their tcgen05.ld of accumulator a completed).
-// ---------------------------------------------------------------------------
-constexpr int kWsThreads = 288;  // 9 warps
-constexpr int kWsLoaderWarp0 = 4, kWsMmaWarp = 8;
-
-constexpr uint32_t kWsSmemMax = 224 * 1024;  // + 2 KB static, under the 227 KB opt-in
-
-// ring depth that fits next to W' (<= 224 KB dynamic): 4 at H = 100, 3 at H = 128
-__host__ __device__ inline uint32_t ws_stages(uint32_t kpad, uint32_t npad) {
-    const size_t b = size_t(2) * kpad * npad * 4, stage = size_t(2) * kXfM * kXfKc * 4;
-    const size_t room = b < kWsSmemMax ? (kWsSmemMax - b) / stage : 0;
-    return uint32_t(room < 2 ? 2 : (room > 4 ? 4 : room));
-}
-__host__ __device__ inline size_t ws_smem_bytes(uint32_t kpad, uint32_t npad) {
-    return size_t(2) * kpad * npad * 4 + size_t(ws_stages(kpad, npad)) * 2 * kXfM * kXfKc * 4;
-}
-
-// 8 columns of this warp's 32 TMEM lanes; complete at tmem_ld_wait()
-__device__ __forceinline__ void tmem_ld8_async(uint32_t taddr, uint32_t (&r)[8]) {
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-                 : "r"(taddr));
-}
-__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-
-__device__ __forceinline__ float4 ld4_ef(const float* p, uint64_t pol) {
-    float4 a;
-    asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
-                 : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w)
-                 : "l"(p), "l"(pol));
-    return a;
-}
-
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-template <bool BWD>
-__global__ void __launch_bounds__(kWsThreads, 1) k_tc_xform_ws(TcXformParams p) {
-    extern __shared__ __align__(1024) uint8_t xsm[];
-    __shared__ __align__(8) uint64_t full[4], empty[4], acc_full[2], acc_empty[2], bload;
-    __shared__ uint32_t tmem_base_sh;
-    __shared__ float bias_sh[128];
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const uint32_t kpad = p.kpad, npad = p.npad;
-    const uint32_t b_bytes = kpad * npad * 4;
-    const uint32_t R = ws_stages(kpad, npad);
-    uint8_t* b_hi = xsm;
-    uint8_t* b_lo = xsm + b_bytes;
-    uint8_t* ring = xsm + 2 * b_bytes;
-    constexpr uint32_t a_bytes = kXfM * kXfKc * 4;  // one of hi / lo of one stage
-    const uint32_t ntiles = (p.r1 - p.r0 + kXfM - 1) / kXfM;
-    const uint32_t my_tiles = blockIdx.x < ntiles ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-    const uint32_t nchunks = (kpad + kXfKc - 1) / kXfKc;
-    const uint32_t total = my_tiles * nchunks;
-    const uint32_t a_lbo = (kXfM / 8) * 128, b_lbo = (npad / 8) * 128;
-    const uint64_t pol = evict_first_policy();
-
-    if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(&tmem_base_sh)));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    if (tid == kWsMmaWarp * 32) {
-        for (uint32_t i = 0; i < R; ++i) {
-            mbar_init(&full[i], 4);
-            mbar_init(&empty[i], 1);
-        }
-        for (int a = 0; a < 2; ++a) {
-            mbar_init(&acc_full[a], 1);
-            mbar_init(&acc_empty[a], 4);
-        }
-        mbar_init(&bload, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;");
-    }
-    for (uint32_t c = tid; c < 128; c += kWsThreads) bias_sh[c] = (p.bias && c < p.ndim) ? p.bias[c] : 0.f;
-    asm volatile("tcgen05.fence::before_thread_sync;");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;");
-    const uint32_t tmem = tmem_base_sh;
-
-    if (warp >= kWsLoaderWarp0 && warp < kWsMmaWarp) {
-        // ---- loaders: item e of thread lt: row m = idx / 8, k-core kc = idx % 8 ----
-        const uint32_t lt = tid - kWsLoaderWarp0 * 32;  // 0..127
-        auto load = [&](uint32_t g, float4 (&r)[8]) {
-            if (g >= total) return;
-            const uint32_t tile = blockIdx.x + (g / nchunks) * gridDim.x, c = g % nchunks;
-            const uint32_t row0 = p.r0 + tile * kXfM, k0 = c * kXfKc;
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                const uint32_t idx = lt + 128 * e, m = idx >> 3, kc = idx & 7;
-                const uint32_t v = row0 + m, k = k0 + 4 * kc;
-                r[e] = (v < p.r1 && k < p.kdim) ? ld4_ef(p.A + size_t(v) * p.astride + k, pol)
-                                                : make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-        };
-        auto store = [&](uint32_t g, const float4 (&r)[8]) {
-            const uint32_t s = g % R, u = g / R;
-            if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);  // the MMAs that read this stage are done
-            uint8_t* hi = ring + s * 2 * a_bytes;
-            uint8_t* lo = hi + a_bytes;
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                const uint32_t idx = lt + 128 * e, m = idx >> 3, kc = idx & 7;
-                const float x[4] = {r[e].x, r[e].y, r[e].z, r[e].w};
-                float h[4], l[4];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    h[q] = to_tf32(x[q]);
-                    l[q] = to_tf32(__fsub_rn(x[q], h[q]));
-                }
-                const uint32_t off = kc * a_lbo + (m >> 3) * 128 + (m & 7) * 16;
-                *reinterpret_cast<float4*>(hi + off) = make_float4(h[0], h[1], h[2], h[3]);
-                *reinterpret_cast<float4*>(lo + off) = make_float4(l[0], l[1], l[2], l[3]);
-            }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // visible to the tensor cores
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&full[s]);
-        };
-        float4 ra[8], rb[8];
-        load(0, ra);
-        load(1, rb);
-        for (uint32_t g = 0; g < total; g += 2) {
-            store(g, ra);
-            load(g + 2, ra);
-            if (g + 1 < total) {
-                store(g + 1, rb);
-                load(g + 3, rb);
-            }
-        }
-    } else if (warp == kWsMmaWarp) {
-        // ---- MMA issuer ----
-        if (lane == 0 && my_tiles > 0) {
-            mbar_expect_tx(&bload, 2 * b_bytes);
-            bulk_g2s(b_hi, p.Bop, b_bytes, &bload);
-            bulk_g2s(b_lo, reinterpret_cast<const uint8_t*>(p.Bop) + b_bytes, b_bytes, &bload);
-            mbar_wait(&bload, 0);
-            const uint32_t idesc = umma_idesc_tf32(kXfM, npad);
-            const uint32_t sbh = smem_u32(b_hi), sbl = smem_u32(b_lo);
-            uint32_t g = 0;
-            for (uint32_t j = 0; j < my_tiles; ++j) {
-                const uint32_t a = j & 1, v = j >> 1;
-                if (v > 0) mbar_wait(&acc_empty[a], (v - 1) & 1);  // the epilogue of tile j-2 read it
-                asm volatile("tcgen05.fence::after_thread_sync;");
-                const uint32_t d = tmem + a * npad;
-                for (uint32_t c = 0; c < nchunks; ++c, ++g) {
-                    const uint32_t s = g % R, u = g / R;
-                    mbar_wait(&full[s], u & 1);
-                    asm volatile("tcgen05.fence::after_thread_sync;");
-                    const uint8_t* ah = ring + s * 2 * a_bytes;
-                    const uint32_t sah = smem_u32(ah), sal = smem_u32(ah + a_bytes);
-                    const uint32_t ksteps = min(uint32_t(kXfKc), kpad - c * kXfKc) / 8;
-                    for (uint32_t st = 0; st < ksteps; ++st) {
-                        const uint32_t kcore = c * (kXfKc / 4) + 2 * st;
-                        const uint64_t dah = umma_desc(sah + 2 * st * a_lbo, a_lbo, 128);
-                        const uint64_t dal = umma_desc(sal + 2 * st * a_lbo, a_lbo, 128);
-                        const uint64_t dbh = umma_desc(sbh + kcore * b_lbo, b_lbo, 128);
-                        const uint64_t dbl = umma_desc(sbl + kcore * b_lbo, b_lbo, 128);
-                        const uint32_t accum = (c == 0 && st == 0) ? 0u : 1u;
-                        mma_tf32(d, dah, dbh, idesc, accum);
-                        mma_tf32(d, dah, dbl, idesc, 1u);
-                        mma_tf32(d, dal, dbh, idesc, 1u);
-                    }
-                    umma_commit(&empty[s]);
-                }
-                umma_commit(&acc_full[a]);
-            }
-        }
-    } else {
-        // ---- epilogue: warp q owns TMEM lanes / tile rows 32 q .. 32 q + 31 ----
-        const uint32_t q = warp;
-        for (uint32_t j = 0; j < my_tiles; ++j) {
-            const uint32_t a = j & 1, tile = blockIdx.x + j * gridDim.x;
-            const uint32_t row = 32 * q + lane, v = p.r0 + tile * kXfM + row;
-            const bool valid = v < p.r1;
-            const uint32_t vo = (!BWD && p.gnext && valid) ? p.orig[v] : 0u;
-            mbar_wait(&acc_full[a], (j >> 1) & 1);
-            asm volatile("tcgen05.fence::after_thread_sync;");
-            const uint32_t taddr = tmem + ((32u * q) << 16) + a * npad;
-            for (uint32_t c1 = 0; c1 < npad; c1 += 32) {
-                uint32_t acc[4][8];
-                float4 d0[4][2];
-#pragma unroll
-                for (int gi = 0; gi < 4; ++gi) {
-                    const uint32_t c0 = c1 + 8 * gi;
-                    if (BWD && p.gcn2 && valid && c0 < p.ostride) {
-                        const float* src = p.dh0 + size_t(v) * p.dh0stride + c0;
-                        d0[gi][0] = ld4_ef(src, pol);
-                        d0[gi][1] = ld4_ef(src + 4, pol);
-                    }
-                    if (c0 < npad) tmem_ld8_async(taddr + c0, acc[gi]);  // warp-uniform
-                }
-                tmem_ld_wait();
-                if (!valid) continue;
-#pragma unroll
-                for (int gi = 0; gi < 4; ++gi) {
-                    const uint32_t c0 = c1 + 8 * gi;
-                    if (c0 >= p.ostride) break;
-                    float o[8];
-                    if (!BWD) {
-                        float gn[8];
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) {
-                            const uint32_t c = c0 + i;
-                            float val = 0.f;
-                            if (c < p.ndim) {
-                                val = __fadd_rn(__uint_as_float(acc[gi][i]), bias_sh[c]);
-                                if (p.relu && val < 0.f) val = 0.f;
-                            }
-                            o[i] = val;
-                            gn[i] = (p.gnext && c < p.ndim) ? drop_apply(p.next_mask, vo, c, val) : 0.f;
-                        }
-                        float* dst = p.out + size_t(v) * p.ostride + c0;
-                        st_v4_ef(dst, o[0], o[1], o[2], o[3], pol);
-                        st_v4_ef(dst + 4, o[4], o[5], o[6], o[7], pol);
-                        if (p.gnext) {
-                            float* gd = p.gnext + size_t(v) * p.gnstride + c0;
-                            st_v4_ef(gd, gn[0], gn[1], gn[2], gn[3], pol);
-                            st_v4_ef(gd + 4, gn[4], gn[5], gn[6], gn[7], pol);
-                        }
-                    } else {
-                        if (p.gcn2) {
-                            float dd[8] = {d0[gi][0].x, d0[gi][0].y, d0[gi][0].z, d0[gi][0].w,
-                                           d0[gi][1].x, d0[gi][1].y, d0[gi][1].z, d0[gi][1].w};
-#pragma unroll
-                            for (int i = 0; i < 8; ++i) {
-                                const bool in = c0 + i < p.ndim;
-                                const float av = __uint_as_float(acc[gi][i]);
-                                dd[i] = in ? __fadd_rn(dd[i], __fmul_rn(p.alpha, av)) : dd[i];
-                                o[i] = in ? __fmul_rn(p.oma, av) : 0.f;
-                            }
-                            float* dp = p.dh0 + size_t(v) * p.dh0stride + c0;
-                            st_v4_ef(dp, dd[0], dd[1], dd[2], dd[3], pol);
-                            st_v4_ef(dp + 4, dd[4], dd[5], dd[6], dd[7], pol);
-                        } else {
-#pragma unroll
-                            for (int i = 0; i < 8; ++i) o[i] = c0 + i < p.ndim ? __uint_as_float(acc[gi][i]) : 0.f;
-                        }
-                        float* dst = p.bg + size_t(v) * p.ostride + c0;
-                        st_v4_ef(dst, o[0], o[1], o[2], o[3], pol);
-                        st_v4_ef(dst + 4, o[4], o[5], o[6], o[7], pol);
-                    }
-                }
-            }
-            asm volatile("tcgen05.fence::before_thread_sync;");
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&acc_empty[a]);
-        }
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;");
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
-}
-
 }  // namespace gp

@@ -221,10 +221,9 @@ CC = {"GP_TC_XFORM": "0"}
 VARIANTS = [(CC, {"GP_SPLIT": "0"}), ({}, {"GP_WAVE": "1"}), ({}, {"GP_OCC5": "1"}), ({}, {"GP_PGRAD": "simt"}),
             ({}, {"GP_MERGED_G": "0"}), (CC, {"GP_MERGED_G": "0", "GP_SPLIT": "0"}), ({}, {"GP_LEAN": "0"}),
             ({}, {"GP_LEAN": "0", "GP_MERGED_G": "0"}), (CC, {"GP_LEAN": "0", "GP_SPLIT": "0"}),
-            (CC, {"GP_WAVE": "1"}), (CC, {"GP_LEAN": "0"}), ({}, {"GP_TC_XFORM": "2"})]
+            (CC, {"GP_WAVE": "1"}), (CC, {"GP_LEAN": "0"})]
 VARIANT_IDS = ["fused", "one_stream", "occ5", "simt_pgrad", "split_g", "split_g_fused", "swap_layout",
-               "swap_layout_split_g", "swap_layout_fused", "cuda_core_one_stream", "cuda_core_swap_layout",
-               "tc_single_role"]
+               "swap_layout_split_g", "swap_layout_fused", "cuda_core_one_stream", "cuda_core_swap_layout"]
 
 
 @pytest.mark.parametrize("hist", [False, True], ids=["stale", "hist"])
