@@ -1071,6 +1071,12 @@ struct Stage {
     void stage_rows_h2d(T* dst, const std::vector<uint64_t>& rp, unsigned nth, Fill&& fill) {
         const uint32_t rows = uint32_t(rp.size() - 1);
         if (rp[rows] == 0) return;
+        if (rp[rows] * sizeof(T) < (size_t(4) << 20)) {  // small graphs: no pinned staging (its
+            std::vector<T> tmp(rp[rows]);                  // allocation costs more than the copy)
+            for (uint32_t r = 0; r < rows; ++r) fill(r, tmp.data() + rp[r]);
+            GP_CUDA(cudaMemcpy(dst, tmp.data(), tmp.size() * sizeof(T), cudaMemcpyHostToDevice));
+            return;
+        }
         for (int i = 0; i < 2; ++i) {
             if (!h2d_stage[i]) GP_CUDA(cudaMallocHost(&h2d_stage[i], kStageChunk));
             if (!h2d_done[i]) GP_CUDA(cudaEventCreateWithFlags(&h2d_done[i], cudaEventDisableTiming));
