@@ -129,7 +129,7 @@ double nccl_timeout() {
 // peer that never joins) and GP_ECUDA on an NCCL error (e.g. two ranks on one device).
 void nccl_wait(void*& comm, const char* what) {
     const auto t0 = std::chrono::steady_clock::now();
-    for (;;) {
+    for (uint32_t spin = 0;; ++spin) {
         int state = 0;
         const int r = g_nccl.async_error(comm, &state);
         if (r != 0) state = r;
@@ -145,7 +145,9 @@ void nccl_wait(void*& comm, const char* what) {
             throw Error(GP_EFABRIC, std::string(what) + ": timed out after " + std::to_string(nccl_timeout()) +
                                         " s (GP_NCCL_TIMEOUT; the peer rank never joined)");
         }
-        std::this_thread::sleep_for(std::chrono::milliseconds(1));
+        // an enqueue normally completes within microseconds: spin first, then back off
+        if (spin < 1000) std::this_thread::yield();
+        else std::this_thread::sleep_for(std::chrono::microseconds(200));
     }
 }
 
