@@ -1649,7 +1649,8 @@ struct Stage {
             p.rowptr = rowptr;
             p.edges = edges;
             p.gsrc = d.G;
-            p.gsnap = d.agg ? d.Gs : nullptr;
+            // one table (merged, synchronous, or stage 0's features): plain gather, no per-entry choice
+            p.gsnap = d.agg && d.Gs != d.G ? d.Gs : nullptr;
             p.done = done;
             p.gstride = d.sin;
             p.zrow = n;

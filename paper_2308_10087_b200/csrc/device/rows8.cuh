@@ -363,19 +363,24 @@ __global__ void __launch_bounds__(kBlock, MINB ? MINB : (SPLIT && NB == 2 ? GP_S
             // pre = [drop(x_v) | mean over neighbours of drop(x_u)] (nn.hpp:176-182); the own row
             // is the current gather-table row (v's chunk is done), the mean half starts at sgap
             const F8 own = (has && in_act) ? ld8_stream(p.gsrc + size_t(v) * p.gstride + 8 * hl) : f8_zero();
-            const F8 z = gather_row8<false, true, NB>(p.rowptr_m, p.edges_m, v, has, p.gsrc, p.gsnap, p.gstride, p.done,
-                                                  lane, in_act, reinterpret_cast<uint2*>(smem4) + (threadIdx.x / 32) * 32,
-                                                  f8_zero());
+            uint2* es = reinterpret_cast<uint2*>(smem4) + (threadIdx.x / 32) * 32;
+            const F8 z = p.gsnap ? gather_row8<false, true, NB>(p.rowptr_m, p.edges_m, v, has, p.gsrc, p.gsnap,
+                                                                p.gstride, p.done, lane, in_act, es, f8_zero())
+                                 : gather_row8<false, false, NB>(p.rowptr_m, p.edges_m, v, has, p.gsrc, nullptr,
+                                                                 p.gstride, p.done, lane, in_act, es, f8_zero());
             if (has && in_act) {
                 st8_stream(p.pre + size_t(v) * p.prestride + 8 * hl, own);
                 st8_stream(p.pre + size_t(v) * p.prestride + p.sgap + 8 * hl, z);
             }
             continue;  // SageConv runs split: transform in k_fwd_tile (gapped weights)
         } else {
-            // "cur if the neighbour's chunk is done, else snapshot" (engines_impl.hpp:740-744)
-            const F8 z = gather_row8<false, true, NB>(p.rowptr, p.edges, v, has, p.gsrc, p.gsnap, p.gstride, p.done, lane,
-                                                  in_act, reinterpret_cast<uint2*>(smem4) + (threadIdx.x / 32) * 32,
-                                                  f8_zero());
+            // "cur if the neighbour's chunk is done, else snapshot" (engines_impl.hpp:740-744); with
+            // one (merged) table, gsnap == null and the per-entry table choice is skipped
+            uint2* es = reinterpret_cast<uint2*>(smem4) + (threadIdx.x / 32) * 32;
+            const F8 z = p.gsnap ? gather_row8<false, true, NB>(p.rowptr, p.edges, v, has, p.gsrc, p.gsnap, p.gstride,
+                                                                p.done, lane, in_act, es, f8_zero())
+                                 : gather_row8<false, false, NB>(p.rowptr, p.edges, v, has, p.gsrc, nullptr, p.gstride,
+                                                                 p.done, lane, in_act, es, f8_zero());
             if (KIND == FWD_GCN2) {
                 const F8 h = (has && in_act) ? ld8_stream(p.h0 + size_t(v) * p.h0stride + 8 * hl) : f8_zero();
 #pragma unroll

@@ -370,6 +370,15 @@ int main(int argc, char** argv) {
         run("split gather k_fwd8<GCN2,8,1,3>", (const void*)k_fwd8<FWD_GCN2, 8, true, 3>, kEdgeSlotBytes, K);
         run("split gather k_fwd8<GCN2,8,1,2>", (const void*)k_fwd8<FWD_GCN2, 8, true, 2>, kEdgeSlotBytes, K);
         run("split gather k_fwd8<GCN2,16,1,2>", (const void*)k_fwd8<FWD_GCN2, 16, true, 2>, kEdgeSlotBytes, K);
+        {  // one gather table (gsnap = null): no per-entry cur/snapshot choice
+            const float* keep = p.gsnap;
+            p.gsnap = nullptr;
+            run("one-table split gather k_fwd8<GCN2,2,1>", (const void*)k_fwd8<FWD_GCN2, 2, true>, kEdgeSlotBytes, K);
+            run("one-table split gather k_fwd8<GCN2,2,1,5>", (const void*)k_fwd8<FWD_GCN2, 2, true, 5>, kEdgeSlotBytes, K);
+            run("one-table split gather k_fwd8<GCN2,4,1,4>", (const void*)k_fwd8<FWD_GCN2, 4, true, 4>, kEdgeSlotBytes, K);
+            run("one-table split gather k_fwd8<GCN2,4,1,3>", (const void*)k_fwd8<FWD_GCN2, 4, true, 3>, kEdgeSlotBytes, K);
+            p.gsnap = keep;
+        }
         run("split dense k_fwd_tile<1,4>", (const void*)k_fwd_tile<true, 4>, tile_smem_bytes(H, H, 4), K);
         run("split dense k_fwd_tile<1,4,100>", (const void*)k_fwd_tile<true, 4, 100>, tile_smem_bytes(H, H, 4), K);
         {  // cost of the next-layer dropout epilogue: same transform without gnext
