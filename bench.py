@@ -438,6 +438,7 @@ def main():
         if c:
             ceiling, ceiling_src = c.get("gbs"), c.get("source")
     alg_per_launch = fa["alg_bytes"] / fa["launches"] if fa["launches"] else None
+    gathered = prof["fwd_agg"]["gather_bytes"] + prof["bwd_agg"]["gather_bytes"]  # one (profiling) epoch
     agg_layers = sum(1 for s in specs if s.aggregates)
     edges_per_s = 2.0 * (E2) * agg_layers * 2 / (ms_step / 1e3)
     total_ms = sum(v["ms"] for v in prof.values())
@@ -474,6 +475,11 @@ def main():
                               "achieved_serial: the same bytes over the isolated launch time of the serial "
                               "profiling epoch"),
                      "share_of_step": (fa["ms"] / args.steps) / ms_step if ms_step else None},
+        # epoch-level bound: every byte the forward and backward SpMMs gather per epoch, at the
+        # measured random-row gather ceiling of this shape, is a lower bound on the epoch time
+        "epoch_gather_bound": ({
+            "gathered_bytes": gathered, "ceiling_gbs": ceiling, "bound_s": gathered / (ceiling * 1e9),
+            "frac": gathered / (ceiling * 1e9) / (ms_step / 1e3)} if ceiling else None),
         "cpu_baseline": cpu,
         "kernel_ms_per_epoch": {k: round(v["ms"], 3) for k, v in prof.items() if v["launches"]},
         "host_prep_s": round(prep_s, 2),
