@@ -347,6 +347,8 @@ void cmd_train(const Args& a) {
     opt.staleness.synchronous_mode = argu(a, "sync", "0") != 0;
     opt.fabric.mode = arg(a, "fabric", "det") == "conc" ? Fabric::Mode::Concurrent
                                                         : Fabric::Mode::Deterministic;
+    // full-size pipelines fill for minutes before the last stage's first message arrives
+    opt.fabric.watchdog_seconds = argd(a, "watchdog", "60");
     const std::string mode = arg(a, "mode", "pipe");
     TrainResult<float> res;
     std::vector<uint32_t> chunk_of;

@@ -38,6 +38,13 @@ BIG = {  # full-size scenarios: chunk_of is stored as its sha256, the forward du
                                                    full=0)),
     "cfg2_reddit_gcnii4_s1k4_2ep": ("train", dict(spec=CFG2, model="gcnii", layers=4, hidden=100, S=1, K=4,
                                                   chunk_seed=1, epochs=2, seed=1)),
+    # configs[2] itself: the headline 64-layer GCNII at the Reddit shape, 8 stages x 32 chunks (the
+    # reference runs one worker thread per stage), 2 epochs
+    "cfg2_reddit_gcnii64_s8k32_2ep": ("train", dict(spec=CFG2, model="gcnii", layers=64, hidden=100, S=8, K=32,
+                                                    chunk_seed=1, epochs=2, seed=1, fabric="conc", watchdog=36000)),
+    # configs[1] over the north star's 20-epoch loss-curve horizon at the real arxiv shape
+    "cfg1_arxiv_gcn16_s2k8_20ep": ("train", dict(spec=CFG1, model="gcn", layers=16, hidden=128, S=2, K=8,
+                                                 chunk_seed=1, epochs=20, seed=1, fabric="conc", watchdog=36000)),
 }
 
 SCENARIOS = {
@@ -164,7 +171,7 @@ def golden_checkpoints(td):
 def make_big(name, td):
     import hashlib
     cmd, kw = BIG[name]
-    d = run_ref(cmd, os.path.join(td, name + ".blob"), timeout=7200, **kw)
+    d = run_ref(cmd, os.path.join(td, name + ".blob"), timeout=14400, **kw)
     if "chunk_of" in d:
         d["chunk_of_sha256"] = np.array(hashlib.sha256(d.pop("chunk_of").astype("<u4").tobytes()).hexdigest())
     meta = {"cmd": cmd, **{k: str(v) for k, v in kw.items()}}

@@ -40,10 +40,26 @@ def _worker(rank, world, port, sync, q):
         allc = [None] * world
         dist.all_gather_object(allc, chunk_of.tobytes())
         assert all(c == allc[0] for c in allc)
-        ids = D.exchange_unique_ids(dist, rank, world, lambda: os.urandom(128))
+        # NCCL stage-boundary ids: the engine's own gp_nccl_unique_id on rank 0 (works without a GPU)
+        ids = D.exchange_unique_ids(dist, rank, world, gp.nccl_unique_id)
+        assert len(ids) == world - 1 and all(len(i) == 128 and any(i) for i in ids)
         up, down = D.boundary_ids(ids, rank, world)
         if rank > 0:
             assert up == ids[rank - 1]
+        if rank < world - 1:
+            assert down == ids[rank]
+        # CUDA-IPC link setup: every stage's (up, down) export blobs meet their neighbours'
+        blob = lambda tag: bytes([rank, tag]) + bytes(gp.IPC_BLOB_BYTES - 2)
+        mine = (blob(1) if rank > 0 else None, blob(2) if rank < world - 1 else None)
+        up_peer, down_peer = D.exchange_ipc_blobs(dist, rank, world, mine)
+        assert (up_peer[:2] == bytes([rank - 1, 2])) if rank > 0 else up_peer is None
+        assert (down_peer[:2] == bytes([rank + 1, 1])) if rank < world - 1 else down_peer is None
+        # hybrid group link setup: 2 groups of world/2 workers exchange their group blobs
+        if world % 2 == 0:
+            G = world // 2
+            st, gr = rank // G, rank % G
+            peers = D.exchange_group_blobs(dist, st, gr, G, bytes([st, gr]) * 8)
+            assert all(peers[r] == bytes([st, r]) * 8 for r in range(G))  # group-rank order, own included
         # schedule agreement with neighbours, for 3 epochs of shuffled orders
         L = 8
         model = gp.ModelConfig(kind=gp.ModelKind.GCNII, layers=L, hidden=H)
@@ -70,6 +86,13 @@ def _worker(rank, world, port, sync, q):
         want = 3 * 2 * (S - 1) * ds.num_vertices * H * 4 * 2
         assert t_all == want, (t_all, want)
         assert D.max_over_ranks(dist, float(rank)) == float(world - 1)
+        # every rank plans its stage's device memory with the engine's layout pass (no GPU)
+        plan = gp.stage_footprint(nnz_norm=1 << 20, num_features=12, specs=specs, num_vertices=ds.num_vertices,
+                                  num_chunks=K, stage=rank, num_stages=S, layer_range=(lo, hi), hidden=H,
+                                  num_classes=5, dropout=0.5, seed=1)
+        allp = [None] * world
+        dist.all_gather_object(allp, plan)
+        assert all(x > 0 for x in allp) and (world < 3 or len(set(allp[1:-1])) == 1)
         q.put((rank, "ok"))
     except Exception as e:  # pragma: no cover - reported to the parent
         q.put((rank, repr(e)))
@@ -101,3 +124,22 @@ def test_pipeline_plumbing_gloo(world, sync):
 def test_schedule_single_stage_has_no_messages():
     from paper_2308_10087_b200 import distributed as D
     assert D.message_schedule([2, 0, 1], 0, 1) == []
+
+
+def test_bench_self_launches_ranks_on_cpu():
+    """bench.py --gpus 2 without WORLD_SIZE relaunches itself under torchrun with 2 ranks; on the
+    reference arm rank 0 alone prints the line (S = 2 stage threads) and rank 1 exits 0."""
+    import json
+    import subprocess
+    import sys
+    from oracle.blob import have_ref
+    if not have_ref():
+        pytest.skip("oracle/_ref/ref_driver not built")
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--impl", "reference", "--workload", "er4k",
+                        "--steps", "2", "--warmup", "1"], cwd=ROOT, capture_output=True, text=True, timeout=600,
+                       env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1 and lines[0]["n_gpus"] == 2 and lines[0]["config"]["stages"] == 2
+    assert lines[0]["config"]["chunks"] == 8

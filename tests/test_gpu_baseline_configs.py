@@ -145,3 +145,13 @@ def test_cfg2_reddit_shape_gcnii4_loss_and_every_gradient(gp, reddit, monkeypatc
 def test_cfg2_reddit_shape_gcnii4_pipeline_two_epochs(gp, reddit):
     model = gp.ModelConfig(kind=gp.ModelKind.GCNII, layers=4, hidden=100)
     compare_training(gp, "cfg2_reddit_gcnii4_s1k4_2ep", reddit, model, 1, 4, 2, loss_tol=1e-5)
+
+
+def test_cfg2_reddit_headline_gcnii64_eight_stages(gp, reddit):
+    """configs[2] itself: the 64-layer GCNII at the full Reddit shape, 8 pipeline stages x 32 chunks
+    (as 8 in-process stages on the one GPU), 2 epochs against the reference's own train_pipeline run
+    with 8 worker threads: loss curve, ledger (2.43 GiB per epoch, the paper's figure) and every
+    layer's parameters."""
+    model = gp.ModelConfig(kind=gp.ModelKind.GCNII, layers=64, hidden=100)
+    res, _ = compare_training(gp, "cfg2_reddit_gcnii64_s8k32_2ep", reddit, model, 8, 32, 2, loss_tol=1e-5)
+    assert all(int(c[1]) == 2 * 7 * 232965 * 100 * 2 * 4 for c in res.comm)
