@@ -377,6 +377,12 @@ struct Stage {
     // epilogues) run on tcgen05 (3xTF32, fp32-level); 0: the bit-exact CUDA-core tiles
     bool use_tc_xform = true;
     bool state_restored = false;  // gp_set_history: the snapshot rows were loaded
+    // lean layout, epoch t with t % fix_alpha == 0 (the next epoch refreshes the snapshot):
+    // tcgen05 forward epilogues write each row of h into hs as well (dual_done[i] marks the
+    // layers), so copy_snapshots only copies the rest (single-process stages: hybrid halo rows
+    // land in h outside the epilogue)
+    bool dual_snap = false;
+    std::vector<uint8_t> dual_done;
     // forward wavefront hooks (merged_g): after the kernel gathering from G_i, and
     // before the kernel writing rows of G_i
     std::function<void(uint32_t)> on_gather_done, before_g_write;
@@ -1460,6 +1466,8 @@ struct Stage {
         x.bias = p.bias;
         x.relu = p.relu;
         x.out = p.out;
+        // lean layout, epoch before a snapshot refresh: the epilogue writes h into the snapshot too
+        x.out2 = dual_snap && d.hs ? d.hs : nullptr;
         x.gnext = p.gnext;
         x.gnstride = p.gnstride;
         x.next_mask = p.next_mask;
@@ -1718,6 +1726,7 @@ struct Stage {
                 });
                 gather_done();
                 write_wait();
+                if (d.tc && dual_snap && d.hs) dual_done[i] = 1;
                 launch(GP_K_FWD_DENSE, db, 2.0 * double(rows) * d.din * d.dout, 0, [&]() {
                     if (d.tc) tc_xform_go<false>(tc_fwd_params(d, p));
                     else if (g2) fwd_dense_go<true>(rows, p);
@@ -2756,16 +2765,18 @@ struct Stage {
     // (all n rows: hybrid halo rows pulled into cur are part of the snapshot, like the
     // reference's whole-matrix copy). backward = true: the historical dagg tables.
     void copy_snapshots(bool backward) {
-        auto copy = [&](float* dst, const float* src, size_t floats) {
+        auto copy = [&](float* dst, const float* src, size_t floats) {  // SM copy at HBM rate
             if (!dst || !src || dst == src) return;
-            GP_CUDA(cudaMemcpyAsync(dst, src, floats * 4, cudaMemcpyDeviceToDevice, cs));
+            const uint32_t blocks = uint32_t(std::min<size_t>(size_t(num_sms) * 8, (floats / 4 + 255) / 256 + 1));
+            launch(GP_K_REMASK, double(floats) * 8.0, 0, 0, [&]() { k_copy<<<blocks, 256, 0, cs>>>(dst, src, floats); });
         };
         if (backward) {
             for (auto& d : L) copy(d.bgs, d.bg, size_t(n) * d.skw);
             return;
         }
         copy(in_snap, in_cur, size_t(n) * sin0);
-        for (auto& d : L) copy(d.hs, d.h, size_t(n) * d.sout);
+        for (uint32_t i = 0; i < len; ++i)
+            if (!(i < dual_done.size() && dual_done[i])) copy(L[i].hs, L[i].h, size_t(n) * L[i].sout);
     }
 
     void run_epoch(uint32_t t, const uint32_t* order, gp_epoch_stats* out) {
@@ -2809,6 +2820,8 @@ struct Stage {
             }
         }
         state_restored = false;
+        dual_snap = lean && !sync && G == 1 && t % fix_alpha == 0;
+        dual_done.assign(len, 0);
         // Masked gather sources start from the snapshot rows (stale reads).
         for (uint32_t i = 0; i < len; ++i) {
             if (!L[i].agg) continue;

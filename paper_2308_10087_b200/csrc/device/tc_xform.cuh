@@ -47,6 +47,7 @@ struct TcXformParams {
     uint32_t relu;
     // forward epilogue
     float* out;
+    float* out2;  // optional second copy of out (the next epoch's snapshot, lean layout) or null
     float* gnext;
     uint32_t gnstride;
     DropKey next_mask;
@@ -226,6 +227,11 @@ __global__ void __launch_bounds__(kXfThreads, 1) k_tc_xform(TcXformParams p) {
                 float* dst = p.out + size_t(v) * p.ostride + c0;
                 st_v4_ef(dst, o[0], o[1], o[2], o[3], pol);
                 st_v4_ef(dst + 4, o[4], o[5], o[6], o[7], pol);
+                if (p.out2) {
+                    float* d2 = p.out2 + size_t(v) * p.ostride + c0;
+                    st_v4_ef(d2, o[0], o[1], o[2], o[3], pol);
+                    st_v4_ef(d2 + 4, o[4], o[5], o[6], o[7], pol);
+                }
                 if (p.gnext) {
                     float* gd = p.gnext + size_t(v) * p.gnstride + c0;
                     st_v4_ef(gd, g[0], g[1], g[2], g[3], pol);
