@@ -717,7 +717,7 @@ struct Stage {
                 d.mb = dalloc<float>(d.dout);
                 d.vb = dalloc<float>(d.dout);
             }
-            if (use_tc_xform && d.agg && !d.sage && d.din <= kMaxWidth && d.dout <= kMaxWidth) {
+            if (use_tc_xform && !d.sage && d.din <= kMaxWidth && d.dout <= kMaxWidth) {
                 d.tc = true;
                 d.xf_fwd = dalloc<float>(2 * size_t(xf_pad8k(d.din)) * xf_pad16(d.dout));
                 d.xf_bwd = dalloc<float>(2 * size_t(xf_pad8k(d.dout)) * xf_pad16(d.din));
@@ -1711,6 +1711,18 @@ struct Stage {
                 q.din = d.kw;
                 launch(GP_K_FWD_DENSE, db, 2.0 * double(rows) * d.kin * d.dout, 0,
                        [&]() { fwd_dense_go<false>(rows, q); });
+                return;
+            }
+            if (!d.agg && d.tc && split_rows) {
+                // Dense on tcgen05: pre = drop(x) (the reference's dropped input row), then b + pre.W'
+                RemaskParams rp{r0, r1, d.din, cur_src(i), src_stride(i), d.pre, d.skw, orig, drop_key(t, d.l, d.din)};
+                launch(GP_K_FWD_DENSE, double(rows) * d.din * 8.0, 0, 0,
+                       [&]() { k_remask<<<row_grid(rows, (const void*)k_remask, 0), kBlock, 0, cs>>>(rp); });
+                write_wait();
+                if (dual_snap && d.hs) dual_done[i] = 1;
+                const double db = double(rows) * (d.din + d.dout + (gnext ? d.dout : 0)) * 4.0 + double(d.din) * d.dout * 4.0;
+                launch(GP_K_FWD_DENSE, db, 2.0 * double(rows) * d.din * d.dout, 0,
+                       [&]() { tc_xform_go<false>(tc_fwd_params(d, p)); });
                 return;
             }
             if (d.agg && split_rows) {

@@ -155,3 +155,13 @@ def test_cfg2_reddit_headline_gcnii64_eight_stages(gp, reddit):
     model = gp.ModelConfig(kind=gp.ModelKind.GCNII, layers=64, hidden=100)
     res, _ = compare_training(gp, "cfg2_reddit_gcnii64_s8k32_2ep", reddit, model, 8, 32, 2, loss_tol=1e-5)
     assert all(int(c[1]) == 2 * 7 * 232965 * 100 * 2 * 4 for c in res.comm)
+
+
+def test_cfg1_arxiv_shape_gcn16_20_epoch_curve(gp):
+    """configs[1] at the real ogbn-arxiv shape over the north star's 20-epoch horizon (2 stages x 8
+    chunks, default staleness: two snapshot refreshes)."""
+    ds = gp.Dataset.synthetic_er(*CFG1)
+    model = gp.ModelConfig(kind=gp.ModelKind.GCN, layers=16, hidden=128)
+    res, lrel = compare_training(gp, "cfg1_arxiv_gcn16_s2k8_20ep", ds, model, 2, 8, 20, loss_tol=1e-5,
+                                 param_abs_tol=2e-2)
+    assert res.metrics.shape[0] == 20
