@@ -238,6 +238,7 @@ struct GroupLink {
 // Host copy of the renumbered graph, shared by the contexts that share the
 // device graph (needed to derive each rank's halo lists).
 struct HostGraph {
+    std::vector<uint64_t> blk_nnz;  // (G*K row blocks) x (K column chunks) CSR entry counts
     std::vector<uint64_t> rp;       // renumbered row pointers
     std::vector<uint32_t> col;      // renumbered columns
     std::vector<uint32_t> part;     // new id -> partition
@@ -1245,18 +1246,28 @@ struct Stage {
         const unsigned nth = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
         std::atomic<bool> bad{false};
         edges = dalloc<uint2>(std::max<uint64_t>(nz, 1), false);
+        // CSR entries per (row block (rank, chunk), column chunk): the entries a done-filtered
+        // backward gather actually fetches, for the byte / flop accounting
+        std::vector<std::atomic<uint64_t>> blk_nnz(size_t(G) * K * K);
         stage_rows_h2d(edges, h->rp, nth, [&](uint32_t r, uint2* out) {
             const uint32_t v = inv[r];
             uint64_t w = 0;
+            uint32_t per_chunk[kMaxChunks] = {};
             const bool ok = src.row(v, n, [&](uint32_t u, float val) {
                 uint32_t bits;
                 std::memcpy(&bits, &val, 4);
                 out[w] = make_uint2(perm[u] | (chunk_of[u] << kColBits), bits);
                 if (G > 1) h->col[h->rp[r] + w] = perm[u];
+                ++per_chunk[chunk_of[u] < K ? chunk_of[u] : 0];
                 ++w;
             });
+            const size_t blk = (size_t(h->part[r]) * K + h->chunk[r]) * K;
+            for (uint32_t c = 0; c < K; ++c)
+                if (per_chunk[c]) blk_nnz[blk + c].fetch_add(per_chunk[c], std::memory_order_relaxed);
             if (!ok) bad = true;
         });
+        h->blk_nnz.resize(blk_nnz.size());
+        for (size_t i = 0; i < blk_nnz.size(); ++i) h->blk_nnz[i] = blk_nnz[i].load();
         if (bad) throw Error(GP_EINVAL, "CSR column out of range (or a self loop in the graph)");
         if (has_sage) {
             // mean / mean_t (graph.cpp:100-112, nn.hpp:85-98): the normalised rows
@@ -1801,6 +1812,20 @@ struct Stage {
                [&]() { k_dense_gemm<<<(rows + 63) / 64, kBlock, 0, cs>>>(g); });
     }
 
+    // CSR entries of rows [r0, r1) whose column chunk is in `done` (what a done-filtered
+    // gather fetches); the whole count when [r0, r1) is not one (rank, chunk) block
+    double done_nnz(uint32_t r0, uint32_t r1, uint64_t done) {
+        if (done == all_chunks() || !hg || hg->blk_nnz.empty()) return double(rowptr_nnz(r0, r1));
+        for (uint32_t k = 0; k < K; ++k)
+            if (row_begin(k) == r0 && row_end(k) == r1) {
+                const size_t blk = (size_t(grank) * K + k) * K;
+                uint64_t e = 0;
+                for (uint32_t c = 0; c < K; ++c)
+                    if ((done >> c) & 1ull) e += hg->blk_nnz[blk + c];
+                return double(e);
+            }
+        return double(rowptr_nnz(r0, r1));
+    }
     std::vector<uint64_t> h_rowptr;  // host copy for byte accounting
     uint64_t rowptr_nnz(uint32_t r0, uint32_t r1) {
         if (h_rowptr.empty()) {
@@ -1844,7 +1869,7 @@ struct Stage {
                 e = double(rowptr_nnz(r0, r1));
             } else if (nx.agg) {
                 prev = hist ? PREV_AGG_HIST : (done == all_chunks() ? PREV_AGG_ALL : PREV_AGG);
-                e = double(rowptr_nnz(r0, r1));
+                e = hist ? double(rowptr_nnz(r0, r1)) : done_nnz(r0, r1, done);  // entries gathered
             } else {
                 prev = PREV_OWN;
             }
@@ -1951,7 +1976,7 @@ struct Stage {
         p.rowptr_m = rowptr_m;
         p.edges_m = edges_mt;
         p.sgap = d.sgap;
-        const double e = d.agg ? double(rowptr_nnz(r0, r1)) : 0.0;
+        const double e = d.agg ? (hist ? double(rowptr_nnz(r0, r1)) : done_nnz(r0, r1, done)) : 0.0;
         const double bytes = e * 8.0 + (d.agg ? double(n) : double(rows)) * d.din * 4.0 + double(rows) * d.din * 4.0;
         if (d.sage)
             launch(GP_K_BWD_AGG, bytes, 2.0 * e * d.din, e * d.sin * 4.0, [&]() {
