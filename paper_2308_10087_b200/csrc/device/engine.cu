@@ -377,6 +377,7 @@ struct Stage {
     // GP_TC_XFORM=1 (default): the GCN / GCNII row transforms (pre.W', dz.W'^T and their
     // epilogues) run on tcgen05 (3xTF32, fp32-level); 0: the bit-exact CUDA-core tiles
     bool use_tc_xform = true;
+    bool tc_dense = true;  // GP_TC_DENSE=0: Dense layers keep the fused CUDA-core GEMV kernels
     bool state_restored = false;  // gp_set_history: the snapshot rows were loaded
     // lean layout, epoch t with t % fix_alpha == 0 (the next epoch refreshes the snapshot):
     // tcgen05 forward epilogues write each row of h into hs as well (dual_done[i] marks the
@@ -547,7 +548,7 @@ struct Stage {
         if (ev_start) cudaEventDestroy(ev_start);
         if (trace_origin) cudaEventDestroy(trace_origin);
         for (int i = 0; i < 2; ++i) {
-            if (h2d_stage[i]) cudaFreeHost(h2d_stage[i]);
+
             if (h2d_done[i]) cudaEventDestroy(h2d_done[i]);
         }
         if (trace_stamp) cudaFreeHost(trace_stamp);
@@ -623,6 +624,7 @@ struct Stage {
         if (const char* e = std::getenv("GP_MERGED_G")) merged_g = std::atoi(e) != 0;
         if (const char* e = std::getenv("GP_LEAN")) lean = std::atoi(e) != 0;
         if (const char* e = std::getenv("GP_TC_XFORM")) use_tc_xform = std::atoi(e) != 0;
+        if (const char* e = std::getenv("GP_TC_DENSE")) tc_dense = std::atoi(e) != 0;
         if (plan_only) return;
         device = c.device;
         int ndev = 0;
@@ -718,7 +720,7 @@ struct Stage {
                 d.mb = dalloc<float>(d.dout);
                 d.vb = dalloc<float>(d.dout);
             }
-            if (use_tc_xform && !d.sage && d.din <= kMaxWidth && d.dout <= kMaxWidth) {
+            if (use_tc_xform && (d.agg || tc_dense) && !d.sage && d.din <= kMaxWidth && d.dout <= kMaxWidth) {
                 d.tc = true;
                 d.xf_fwd = dalloc<float>(2 * size_t(xf_pad8k(d.din)) * xf_pad16(d.dout));
                 d.xf_bwd = dalloc<float>(2 * size_t(xf_pad8k(d.dout)) * xf_pad16(d.din));
@@ -1046,17 +1048,36 @@ struct Stage {
     // of one chunk overlaps the DMA of the previous one): pageable cudaMemcpy runs at
     // ~1.5 GB/s here, the staged path at PCIe rate. Synchronous on return.
     static constexpr size_t kStageChunk = size_t(32) << 20;
-    char* h2d_stage[2] = {nullptr, nullptr};
+    // The two pinned buffers are process-wide (allocating 64 MB of pinned memory costs tens
+    // of ms per engine); an upload holds them through a StagingLease.
+    struct StagingPool {
+        std::mutex mu;
+        char* buf[2] = {nullptr, nullptr};
+    };
+    static StagingPool& staging_pool() {
+        static StagingPool* pool = new StagingPool;  // never freed: lives until process exit
+        return *pool;
+    }
+    struct StagingLease {
+        std::unique_lock<std::mutex> lk;
+        char* buf[2];
+        StagingLease() : lk(staging_pool().mu) {
+            for (int i = 0; i < 2; ++i) {
+                if (!staging_pool().buf[i]) GP_CUDA(cudaMallocHost(&staging_pool().buf[i], kStageChunk));
+                buf[i] = staging_pool().buf[i];
+            }
+        }
+    };
     cudaEvent_t h2d_done[2] = {nullptr, nullptr};
     void h2d(void* dst, const void* src, size_t bytes) {
         if (bytes < (size_t(4) << 20)) {
             GP_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice));
             return;
         }
-        for (int i = 0; i < 2; ++i) {
-            if (!h2d_stage[i]) GP_CUDA(cudaMallocHost(&h2d_stage[i], kStageChunk));
+        StagingLease lease;
+        char* const* h2d_stage = lease.buf;
+        for (int i = 0; i < 2; ++i)
             if (!h2d_done[i]) GP_CUDA(cudaEventCreateWithFlags(&h2d_done[i], cudaEventDisableTiming));
-        }
         const char* s8 = static_cast<const char*>(src);
         char* d8 = static_cast<char*>(dst);
         bool used[2] = {false, false};
@@ -1086,10 +1107,10 @@ struct Stage {
             GP_CUDA(cudaMemcpy(dst, tmp.data(), tmp.size() * sizeof(T), cudaMemcpyHostToDevice));
             return;
         }
-        for (int i = 0; i < 2; ++i) {
-            if (!h2d_stage[i]) GP_CUDA(cudaMallocHost(&h2d_stage[i], kStageChunk));
+        StagingLease lease;
+        char* const* h2d_stage = lease.buf;
+        for (int i = 0; i < 2; ++i)
             if (!h2d_done[i]) GP_CUDA(cudaEventCreateWithFlags(&h2d_done[i], cudaEventDisableTiming));
-        }
         const uint64_t cap = kStageChunk / sizeof(T);
         bool used[2] = {false, false};
         uint32_t r0 = 0;
