@@ -937,13 +937,12 @@ struct Stage {
         setup_nb<4>();
     }
 
-    // Split gather kernels: 4 resident CTAs (64 registers: more gathers in flight per
-    // warp) by default; GP_OCC5=1 forces the 5-CTA (48-register) build, GP_OCC5=auto
-    // takes it for launches with enough row pairs to keep every warp busy. With the
-    // tcgen05 transforms co-running in the wavefront, 4 CTAs measured 0.393 vs 0.396
-    // s/epoch at K = 4 (3 runs each), 0.437 vs 0.445 at K = 32 (round 1, with the
-    // CUDA-core transforms, the 5-CTA build won inside the wavefront).
-    int occ5_mode = 0;
+    // Split gather kernels: 5 resident CTAs (48 registers) by default; GP_OCC5=0 forces the
+    // 4-CTA (64-register) build, GP_OCC5=auto takes 5 CTAs for launches with enough row pairs
+    // to keep every warp busy. With the single-table gather and tcgen05 transforms (Dense
+    // layers too) co-running in the wavefront: 5 CTAs 0.371 vs 0.374 s/epoch at K = 4 (3 runs
+    // each), 0.448 vs 0.466 at K = 32.
+    int occ5_mode = 1;
     bool use_occ5(uint32_t rows) const {
         if (occ5_mode >= 0) return occ5_mode == 1;
         return uint64_t(rows) / 2 >= 2ull * uint64_t(num_sms) * 5 * kWarpsPerBlock;
