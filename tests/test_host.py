@@ -199,3 +199,15 @@ def test_assignment_files_match_reference_bytes(gp, tmp_path):
     bad.write_text("x\n")
     with pytest.raises(gp.GnnsimError):
         gp.load_assignment(str(bad))
+
+
+def test_train_tool_partition_files_roundtrip(gp):
+    """tools/gnnpipe_train.py --parts-file: the boundary total computed from a loaded parts.txt equals
+    partition_vertices' own (partition.cpp:28-50)."""
+    import numpy as np
+    ds = gp.Dataset.synthetic_er(500, 0.02, 3, 16, 5, 9)
+    part, _, bt = gp.partition_vertices(ds, 3, 4)
+    off, cols, _ = ds.normalize_adjacency(True)
+    rows = np.repeat(np.arange(ds.num_vertices, dtype=np.int64), np.diff(off).astype(np.int64))
+    cross = part[rows] != part[cols]
+    assert int(np.unique(rows[cross] * 3 + part[cols[cross]]).size) == bt

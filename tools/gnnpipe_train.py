@@ -9,10 +9,16 @@ trainer as `gnnsim train --mode` does (gnnsim.cpp:187-239, :284-302); `--compare
         --hidden 64 --stages 2 --chunks 8 --epochs 20 --out runs/er4k
     python tools/gnnpipe_train.py --dataset DIR ...          # a save_dataset directory
     python tools/gnnpipe_train.py --synthetic ... --mode graph --workers 4 --compare --out runs/g4
+    python tools/gnnpipe_train.py ... --chunks-file runs/a/chunks.txt --parts-file runs/a/parts.txt ...
+
+The chunk plan and partition a run used are written to OUT/chunks.txt and OUT/parts.txt (the
+reference CLI's save_assignment format, partition.cpp:250-256).
 """
 import argparse
 import os
 import sys
+
+import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
@@ -61,6 +67,9 @@ def main(argv=None):
     ap.add_argument("--sync", action="store_true")
     ap.add_argument("--trace", action="store_true", help="collect the measured trace (chunks run serially)")
     ap.add_argument("--resume", default="", help="state.ckpt of an earlier run")
+    ap.add_argument("--chunks-file", default="",
+                    help="chunks.txt to train with (load_assignment); the plan used is written to OUT/chunks.txt")
+    ap.add_argument("--parts-file", default="", help="parts.txt (hybrid / graph mode partition); written to OUT")
     ap.add_argument("--out", required=True)
     a = ap.parse_args(argv)
 
@@ -77,21 +86,47 @@ def main(argv=None):
                           synchronous_mode=a.sync, collect_trace=a.trace, resume_path=a.resume,
                           save_state_path=os.path.join(a.out, "state.ckpt"))
     stages, ways, alpha = a.stages, 1, 0.0
+
+    def chunk_plan():  # make_chunks, or a chunks.txt (partition.cpp:250-269); saved next to the outputs
+        if a.chunks_file:
+            k, co = gp.load_assignment(a.chunks_file)
+            if co.size != ds.num_vertices:
+                raise SystemExit(f"{a.chunks_file}: {co.size} vertices, dataset has {ds.num_vertices}")
+        else:
+            k, co = K, gp.make_chunks(ds, K, a.seed)
+        gp.save_assignment(os.path.join(a.out, "chunks.txt"), k, co)
+        return co
+
+    def partition(parts):
+        if a.parts_file:
+            g, part = gp.load_assignment(a.parts_file)
+            if part.size != ds.num_vertices:
+                raise SystemExit(f"{a.parts_file}: {part.size} vertices, dataset has {ds.num_vertices}")
+            # boundary total sum_i |B_i| (partition.cpp:28-50): vertices outside part i with a neighbour in it
+            off, cols, _ = ds.normalize_adjacency(True)
+            rows = np.repeat(np.arange(ds.num_vertices, dtype=np.int64), np.diff(off).astype(np.int64))
+            cross = part[rows] != part[cols]
+            bt = int(np.unique(rows[cross] * g + part[cols[cross]]).size)
+        else:
+            part, _, bt = gp.partition_vertices(ds, parts, a.seed)
+            g = parts
+        gp.save_assignment(os.path.join(a.out, "parts.txt"), g, part)
+        return part, bt
     if mode == "sequential":
         stages = 1
         res = gp.train_sequential(ds, opt)
     elif mode == "graph":
         stages = 1  # compare.csv's ways column is the group size (1) in graph mode (gnnsim.cpp:314)
-        part, _, bt = gp.partition_vertices(ds, a.workers or 2, a.seed)
+        part, bt = partition(a.workers or 2)
         alpha = bt / ds.num_vertices  # replication_factor (partition.cpp:200-204)
         res = gp.train_graph_parallel(ds, part, opt)
     elif mode == "hybrid":
         ways = a.parts
-        part, _, bt = gp.partition_vertices(ds, ways, a.seed)
+        part, bt = partition(ways)
         alpha = bt / ds.num_vertices
-        res = gp.train_hybrid(ds, part, gp.make_chunks(ds, K, a.seed), a.stages, opt)
+        res = gp.train_hybrid(ds, part, chunk_plan(), a.stages, opt)
     else:
-        res = gp.train_pipeline(ds, gp.make_chunks(ds, K, a.seed), a.stages, opt)
+        res = gp.train_pipeline(ds, chunk_plan(), a.stages, opt)
     if a.compare:
         write_compare(os.path.join(a.out, "compare.csv"), mode, ds, model, res, stages, ways, alpha)
     gp.write_run_outputs(res, a.out)
