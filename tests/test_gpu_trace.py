@@ -111,10 +111,16 @@ def test_train_tool_writes_reference_run_outputs(gp, tmp_path):
     args = ["--synthetic", "er:500:0.02:3:16:5:9", "--model", "gcnii", "--layers", "5", "--hidden", "16",
             "--stages", "2", "--epochs", "3", "--trace", "--out", str(out)]
     tool.main(args)
-    for name in ("metrics.csv", "trace.jsonl", "comm_report.csv", "stage_0.ckpt", "stage_1.ckpt", "state.ckpt"):
+    for name in ("metrics.csv", "trace.jsonl", "comm_report.csv", "stage_0.ckpt", "stage_1.ckpt", "state.ckpt",
+                 "chunks.txt"):
         assert (out / name).exists(), name
+    k, co = gp.load_assignment(str(out / "chunks.txt"))
+    ds = gp.Dataset.synthetic_er(500, 0.02, 3, 16, 5, 9)
+    assert k == 8 and np.array_equal(co, gp.make_chunks(ds, 8, 1))
     assert open(out / "metrics.csv").read().count("\n") == 4
     names = [n for n, _ in gp.load_checkpoint(str(out / "stage_1.ckpt"))]
     assert names[0].startswith("layer") and names[0].endswith(".weight")
-    tool.main(args[:-2] + ["--resume", str(out / "state.ckpt"), "--out", str(tmp_path / "run2")])
+    tool.main(args[:-2] + ["--resume", str(out / "state.ckpt"), "--chunks-file", str(out / "chunks.txt"),
+                           "--out", str(tmp_path / "run2")])
     assert open(tmp_path / "run2" / "metrics.csv").read().splitlines()[1].startswith("4,")
+    assert open(tmp_path / "run2" / "chunks.txt").read() == open(out / "chunks.txt").read()
