@@ -83,6 +83,11 @@ __device__ __forceinline__ F8 shfl8(const F8& x, int src) {
 // entries; a batch of 16 is gathered as soon as either half's queue is full, so
 // sparse done-sets do not pay for padded slots. HIST (historical-gradient
 // ablation) keeps every entry and reads not-done chunks from `snap`.
+// GP_TAIL_SKIP: the last (partial) batch of a row pair gathers only the groups of NB slots
+// that hold an entry in either half (padding slots past both halves' ends are not loaded)
+#ifndef GP_TAIL_SKIP
+#define GP_TAIL_SKIP 1
+#endif
 #ifndef GP_SMEM_EDGES
 #define GP_SMEM_EDGES 1
 #endif
@@ -114,7 +119,8 @@ __device__ __forceinline__ F8 gather_row8(const uint64_t* __restrict__ rowptr, c
     const uint2 pad = make_uint2(has_row ? v : 0u, 0u);
     F8 acc = init;  // +0 (SpMM) or the own-row term SageConv's backward starts from (nn.hpp:234-243)
     uint2* es = eslot + (hb ? 16 : 0);
-    auto batch16 = [&](const uint2 my) {
+    // lim: slots [lim, 16) are padding in both halves (warp-uniform), so their groups are skipped
+    auto batch16 = [&](const uint2 my, const uint32_t lim) {
         if (kSmemEdges) {
             __syncwarp();
             es[hl] = my;
@@ -122,6 +128,7 @@ __device__ __forceinline__ F8 gather_row8(const uint64_t* __restrict__ rowptr, c
         }
 #pragma unroll
         for (int t = 0; t < 16; t += NB) {
+            if (GP_TAIL_SKIP && uint32_t(t) >= lim) break;
             float w[NB];
             F8 x[NB];
 #pragma unroll
@@ -150,7 +157,10 @@ __device__ __forceinline__ F8 gather_row8(const uint64_t* __restrict__ rowptr, c
         for (uint32_t off = 0; off < n_max; off += 16) {
             const uint2 my = nxt;
             nxt = off + 16 + hl < n_my ? ld_edge(edges + e0 + off + 16 + hl) : pad;
-            batch16(my);
+            if (off + 16 <= n_max)
+                batch16(my, 16u);  // full batch: no group test in the hot loop
+            else
+                batch16(my, n_max - off);
         }
         return acc;
     }
@@ -174,7 +184,7 @@ __device__ __forceinline__ F8 gather_row8(const uint64_t* __restrict__ rowptr, c
         const uint2 cur = j < 0 ? carry : (j < cnt ? make_uint2(ax, ay) : pad);
         const int tmax = max(tot, __shfl_xor_sync(kFull, tot, 16));
         if (tmax >= 16) {
-            batch16(cur);
+            batch16(cur, 16u);
             // entries of the new batch beyond this 16-slot batch stay queued
             const int k = 16 - nq + hl;
             const uint32_t rx = __shfl_sync(kFull, e.x, hb + (k < 16 ? k : 15));
@@ -186,7 +196,8 @@ __device__ __forceinline__ F8 gather_row8(const uint64_t* __restrict__ rowptr, c
             nq = tot;
         }
     }
-    if (__shfl_xor_sync(kFull, nq, 16) + nq > 0) batch16(carry);
+    const int nq_max = max(nq, __shfl_xor_sync(kFull, nq, 16));
+    if (nq_max > 0) batch16(carry, uint32_t(nq_max));
     return acc;
 }
 
