@@ -178,9 +178,9 @@ def test_train_gcn_pipeline_stale_two_stages(gp):
                    fix_alpha=3)
 
 
-@pytest.mark.parametrize("env", [{}, {"GP_SPLIT": "0"}, {"GP_WAVE": "1"}, {"GP_OCC5": "1"}, {"GP_MERGED_G": "0"},
+@pytest.mark.parametrize("env", [{}, {"GP_SPLIT": "0"}, {"GP_WAVE": "1"}, {"GP_OCC5": "0"}, {"GP_MERGED_G": "0"},
                                  {"GP_LEAN": "0"}],
-                         ids=["default", "fused", "one_stream", "occ5", "split_g", "swap_layout"])
+                         ids=["default", "fused", "one_stream", "occ4", "split_g", "swap_layout"])
 def test_train_sage_pipeline_stale_two_stages(gp, env, monkeypatch):
     """GraphSAGE (SageConv: [own | mean] . W, nn.hpp:176-182, :234-243) over two stages, under every
     engine variant switch (SageConv layers always run split; the others follow GP_SPLIT)."""
@@ -218,11 +218,11 @@ def test_train_sage_wide_features_two_stages(gp):
 # (base env, variant env): the fused kernels (GP_SPLIT=0) run the CUDA-core GEMV, so they are
 # compared with the CUDA-core split transforms (GP_TC_XFORM=0)
 CC = {"GP_TC_XFORM": "0"}
-VARIANTS = [(CC, {"GP_SPLIT": "0"}), ({}, {"GP_WAVE": "1"}), ({}, {"GP_OCC5": "1"}), ({}, {"GP_PGRAD": "simt"}),
+VARIANTS = [(CC, {"GP_SPLIT": "0"}), ({}, {"GP_WAVE": "1"}), ({}, {"GP_OCC5": "0"}), ({}, {"GP_PGRAD": "simt"}),
             ({}, {"GP_MERGED_G": "0"}), (CC, {"GP_MERGED_G": "0", "GP_SPLIT": "0"}), ({}, {"GP_LEAN": "0"}),
             ({}, {"GP_LEAN": "0", "GP_MERGED_G": "0"}), (CC, {"GP_LEAN": "0", "GP_SPLIT": "0"}),
             (CC, {"GP_WAVE": "1"}), (CC, {"GP_LEAN": "0"})]
-VARIANT_IDS = ["fused", "one_stream", "occ5", "simt_pgrad", "split_g", "split_g_fused", "swap_layout",
+VARIANT_IDS = ["fused", "one_stream", "occ4", "simt_pgrad", "split_g", "split_g_fused", "swap_layout",
                "swap_layout_split_g", "swap_layout_fused", "cuda_core_one_stream", "cuda_core_swap_layout"]
 
 
