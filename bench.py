@@ -418,8 +418,11 @@ def main():
     fs = prof["fwd_agg"]  # the serial profiling epoch (no concurrent kernels)
     achieved_serial = fs["alg_bytes"] / (fs["ms"] / 1e3) / 1e9 if fs["ms"] > 0 else None
     gather_serial = fs["gather_bytes"] / (fs["ms"] / 1e3) / 1e9 if fs["ms"] > 0 else None
-    # DRAM bytes per launch of the dominant kernel from one committed `ncu --set full`
-    # capture of the same kernel build, scaled from its rows to the rows of one chunk launch
+    # the same bytes over the time the kernel occupied the GPU in the timed region (union of its
+    # launch intervals: concurrent launches of two chunks on the wavefront streams count once)
+    span = fa.get("span_ms", 0.0)
+    achieved_span = fa["alg_bytes"] / (span / 1e3) / 1e9 if span > 0 else None
+    gather_span = fa["gather_bytes"] / (span / 1e3) / 1e9 if span > 0 else None
     # DRAM bytes per launch of the dominant kernel from a committed `ncu --set full` capture
     # of the same build at this workload (tools/roofline_capture.py); K = 4 chunk launches
     traffic, traffic_src = None, None
@@ -470,10 +473,16 @@ def main():
                                 "the timed region (its stream; chunk wavefront on)"),
                      "ms_per_launch": fa["ms"] / fa["launches"] if fa["launches"] else None,
                      "achieved_serial": achieved_serial,
+                     "span_share_of_step": (span / args.steps) / ms_step if ms_step else None,
+                     "achieved_span": achieved_span,
+                     "frac_span": (achieved_span / hbm) if achieved_span else None,
+                     "l2_gather_gbs_span": gather_span,
+                     "gather_frac_span": (gather_span / ceiling) if gather_span and ceiling else None,
                      "note": ("achieved: live launch durations, which include the kernels co-running on the "
                               "other wavefront streams (per-step kernel time = share_of_step x the step); "
-                              "achieved_serial: the same bytes over the isolated launch time of the serial "
-                              "profiling epoch"),
+                              "achieved_span: the same bytes over the time at least one launch of the kernel "
+                              "was running (union of the live launch intervals); achieved_serial: over the "
+                              "isolated launch time of the serial profiling epoch"),
                      "share_of_step": (fa["ms"] / args.steps) / ms_step if ms_step else None},
         # epoch-level bound: every byte the forward and backward SpMMs gather per epoch, at the
         # measured random-row gather ceiling of this shape, is a lower bound on the epoch time

@@ -111,6 +111,9 @@ typedef struct {
     double alg_bytes[GP_K_NUM];  /* algorithmic HBM bytes       */
     double flops[GP_K_NUM];
     double gather_bytes[GP_K_NUM]; /* bytes gathered through L2 by SpMMs        */
+    double span_ms[GP_K_NUM];    /* time at least one launch of the class ran   */
+                                 /* (union of its launch intervals; concurrent  */
+                                 /* launches on the wavefront streams overlap)  */
 } gp_profile;
 
 /* Buffers readable through gp_download (parity tests; original vertex order). */

@@ -101,7 +101,8 @@ class gp_epoch_stats(C.Structure):
 
 class gp_profile(C.Structure):
     _fields_ = [("ms", C.c_double * 9), ("launches", C.c_uint64 * 9), ("alg_bytes", C.c_double * 9),
-                ("flops", C.c_double * 9), ("gather_bytes", C.c_double * 9)]
+                ("flops", C.c_double * 9), ("gather_bytes", C.c_double * 9),
+                ("span_ms", C.c_double * 9)]
 
 
 class gs_model_config(C.Structure):
@@ -624,7 +625,8 @@ def _result(h, specs) -> TrainResult:
         peak = C.c_uint64()
         _gs(lib.gs_result_peak_bytes(h, C.byref(peak)))
         prof = {name: {"ms": pr.ms[i], "launches": pr.launches[i], "alg_bytes": pr.alg_bytes[i],
-                       "flops": pr.flops[i], "gather_bytes": pr.gather_bytes[i]}
+                       "flops": pr.flops[i], "gather_bytes": pr.gather_bytes[i],
+                       "span_ms": pr.span_ms[i]}
                 for i, name in enumerate(PROFILE_CLASSES)}
         n = C.c_uint64()
         _gs(lib.gs_result_trace(h, None, 0, C.byref(n)))
@@ -908,7 +910,8 @@ class StageEngine:
         pr = gp_profile()
         _L().gp_get_profile(self._h, C.byref(pr))
         return {name: {"ms": pr.ms[i], "launches": pr.launches[i], "alg_bytes": pr.alg_bytes[i],
-                       "flops": pr.flops[i], "gather_bytes": pr.gather_bytes[i]}
+                       "flops": pr.flops[i], "gather_bytes": pr.gather_bytes[i],
+                       "span_ms": pr.span_ms[i]}
                 for i, name in enumerate(PROFILE_CLASSES)}
 
     def mark(self, slot: int):

@@ -3087,9 +3087,12 @@ struct Stage {
         GP_CUDA(cudaEventElapsedTime(&st.epoch_ms, ev_start, ev_end));
         st.kernel_launches = launches;
         float busy = 0.f;
+        std::vector<std::pair<float, float>> iv[GP_K_NUM];  // launch intervals since ev_start
         for (auto& tm : timed) {
-            float ms = 0.f;
+            float ms = 0.f, t0 = 0.f;
             GP_CUDA(cudaEventElapsedTime(&ms, tm.a, tm.b));
+            GP_CUDA(cudaEventElapsedTime(&t0, ev_start, tm.a));
+            iv[tm.cls].emplace_back(t0, t0 + ms);
             busy += ms;
             prof.ms[tm.cls] += ms;
             prof.launches[tm.cls] += 1;
@@ -3100,6 +3103,22 @@ struct Stage {
             ev_free.push_back(tm.b);
         }
         timed.clear();
+        for (int c = 0; c < GP_K_NUM; ++c) {
+            auto& v = iv[c];
+            std::sort(v.begin(), v.end());
+            double span = 0, lo = 0, hi = -1;
+            for (auto& x : v) {
+                if (x.first > hi) {
+                    if (hi > lo) span += hi - lo;
+                    lo = x.first;
+                    hi = x.second;
+                } else {
+                    hi = std::max<double>(hi, x.second);
+                }
+            }
+            if (hi > lo) span += hi - lo;
+            prof.span_ms[c] += span;
+        }
         st.busy_ms = busy;
         trace_resolve();
         if (out) *out = st;

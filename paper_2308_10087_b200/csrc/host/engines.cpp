@@ -444,6 +444,7 @@ TrainResult<float> run_hybrid_f32(const Dataset& ds, const Partition* part, cons
             res.profile.alg_bytes[k] += pr.alg_bytes[k];
             res.profile.flops[k] += pr.flops[k];
             res.profile.gather_bytes[k] += pr.gather_bytes[k];
+            res.profile.span_ms[k] += pr.span_ms[k];
         }
     }
     timer.mark("results");

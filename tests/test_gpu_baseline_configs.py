@@ -46,7 +46,7 @@ def sha(co):
     return hashlib.sha256(np.ascontiguousarray(co, "<u4").tobytes()).hexdigest()
 
 
-def compare_training(gp, name, ds, model, S, K, epochs, loss_tol=1e-4, param_abs_tol=None):
+def compare_training(gp, name, ds, model, S, K, epochs, loss_tol=1e-4, param_abs_tol=None, med_tol=None):
     ref = golden(name)
     co = gp.make_chunks(ds, K, 1)
     assert sha(co) == str(ref["chunk_of_sha256"]), "chunk plan not bit-exact"
@@ -71,7 +71,9 @@ def compare_training(gp, name, ds, model, S, K, epochs, loss_tol=1e-4, param_abs
     # against itself with another pgrad summation order shows the same, test_gpu_parity.py)
     if param_abs_tol is None:
         param_abs_tol = 2e-3 * epochs
-    assert absmax <= param_abs_tol and max(med) < (1e-4 if epochs <= 3 else 1e-3), (absmax, worst, med)
+    if med_tol is None:
+        med_tol = 1e-4 if epochs <= 3 else 1e-3
+    assert absmax <= param_abs_tol and max(med) < med_tol, (absmax, worst, med)
     return res, lrel
 
 
@@ -157,11 +159,18 @@ def test_cfg2_reddit_headline_gcnii64_eight_stages(gp, reddit):
     assert all(int(c[1]) == 2 * 7 * 232965 * 100 * 2 * 4 for c in res.comm)
 
 
-def test_cfg1_arxiv_shape_gcn16_20_epoch_curve(gp):
+@pytest.mark.parametrize("tc", ["1", "0"], ids=["tcgen05", "cuda_core"])
+def test_cfg1_arxiv_shape_gcn16_20_epoch_curve(gp, monkeypatch, tc):
     """configs[1] at the real ogbn-arxiv shape over the north star's 20-epoch horizon (2 stages x 8
-    chunks, default staleness: two snapshot refreshes)."""
+    chunks, default staleness): the loss curve within rel 1e-5 at every epoch, the ledger exact, and
+    the parameters. The last layers of a 16-layer GCN drift under Adam by what the arithmetic of the
+    transforms leaves: the bit-exact fp32 CUDA-core transforms end within a per-layer median rel
+    2.4e-4 of the reference, the tcgen05 3xTF32 transforms (disclosed TF32 inputs) within 1.3e-3,
+    the same distance as between the engine's two paths (1.4e-3; tools/param_control.py).
+    Layers 0-10 stay within 1e-5 either way."""
+    monkeypatch.setenv("GP_TC_XFORM", tc)
     ds = gp.Dataset.synthetic_er(*CFG1)
     model = gp.ModelConfig(kind=gp.ModelKind.GCN, layers=16, hidden=128)
     res, lrel = compare_training(gp, "cfg1_arxiv_gcn16_s2k8_20ep", ds, model, 2, 8, 20, loss_tol=1e-5,
-                                 param_abs_tol=2e-2)
+                                 param_abs_tol=2e-2, med_tol=2e-3 if tc == "1" else 5e-4)
     assert res.metrics.shape[0] == 20
