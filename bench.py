@@ -358,6 +358,16 @@ def main():
         losses = box[0]
     ms_step = ms / args.steps
 
+    # occupied time per kernel class inside normal (wavefront) epochs: events around every
+    # launch for two extra untimed epochs, reduced to the union of each class's launch intervals
+    eng.reset_profile()
+    eng.set_live_timing("all")
+    for _ in range(2):
+        t += 1
+        eng.run_epoch(t, order(t))
+    eng.synchronize()
+    live_all = eng.profile()
+    eng.set_live_timing(None)
     # per-kernel device times from one extra, untimed profiling epoch
     eng.set_profiling(True)
     eng.reset_profile()
@@ -491,6 +501,12 @@ def main():
             "frac": gathered / (ceiling * 1e9) / (ms_step / 1e3)} if ceiling else None),
         "cpu_baseline": cpu,
         "kernel_ms_per_epoch": {k: round(v["ms"], 3) for k, v in prof.items() if v["launches"]},
+        # wavefront epochs: ms per epoch during which at least one launch of the class ran, and the
+        # gather rate over that time as a fraction of the gather ceiling
+        "kernel_span_ms_per_epoch": {k: round(v["span_ms"] / 2, 3) for k, v in live_all.items() if v["launches"]},
+        "gather_frac_span": {k: round(v["gather_bytes"] / (v["span_ms"] / 1e3) / 1e9 / ceiling, 3)
+                             for k, v in live_all.items()
+                             if v["launches"] and v["gather_bytes"] and v["span_ms"] and ceiling},
         "host_prep_s": round(prep_s, 2),
         "loss_last": (losses[-1] / float((sp == 1).sum())) if losses else None,
     }

@@ -234,8 +234,8 @@ gp_status gp_download(gp_ctx* ctx, uint32_t which, uint32_t local_layer, float* 
                       uint64_t count);
 gp_status gp_set_profiling(gp_ctx* ctx, int enable);
 /* CUDA events around every launch of one kernel class (GP_K_*) in normal epochs (the
- * chunk wavefront stays on), accumulated into gp_get_profile; -1 turns it off. Used by
- * bench.py to time the dominant kernel inside the timed region. */
+ * chunk wavefront stays on), accumulated into gp_get_profile; GP_K_NUM times every class,
+ * -1 turns it off. Used by bench.py to time the dominant kernel inside the timed region. */
 gp_status gp_set_live_timing(gp_ctx* ctx, int kernel_class);
 /* Device bytes gp_create + the uploads would allocate for this stage (the stash
  * layout under the current GP_LEAN / GP_MERGED_G switches, graph with nnz_norm

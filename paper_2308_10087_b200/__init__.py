@@ -899,8 +899,10 @@ class StageEngine:
         _L().gp_set_profiling(self._h, int(on))
 
     def set_live_timing(self, kernel_class: Optional[str]):
-        """Events around every launch of one kernel class during normal epochs (None = off)."""
-        cls = -1 if kernel_class is None else PROFILE_CLASSES.index(kernel_class)
+        """Events around every launch of one kernel class during normal epochs ("all": every
+        class, None = off)."""
+        cls = -1 if kernel_class is None else (len(PROFILE_CLASSES) if kernel_class == "all"
+                                                else PROFILE_CLASSES.index(kernel_class))
         _gp(_L().gp_set_live_timing(self._h, cls), self._h)
 
     def reset_profile(self):

@@ -1597,7 +1597,7 @@ struct Stage {
     template <typename F>
     void launch(int cls, double bytes, double flops, double gather, F&& fn) {
         ++launches;
-        if (!profiling && cls != live_cls) {
+        if (!profiling && cls != live_cls && live_cls != GP_K_NUM) {
             fn();
             GP_CUDA(cudaGetLastError());
             return;
@@ -3466,7 +3466,7 @@ gp_status gp_upload_history(gp_ctx* ctx, uint32_t which, uint32_t local_layer, c
 }
 
 gp_status gp_set_live_timing(gp_ctx* ctx, int kernel_class) {
-    if (!ctx || kernel_class < -1 || kernel_class >= GP_K_NUM) return GP_EINVAL;
+    if (!ctx || kernel_class < -1 || kernel_class > GP_K_NUM) return GP_EINVAL;
     ctx->st.live_cls = kernel_class;
     return GP_OK;
 }
