@@ -354,12 +354,12 @@ struct Stage {
     int device = 0;
     std::string err;
     cudaStream_t cs = nullptr;       // compute stream (the current one: see the backward wavefront)
-    static constexpr int kMaxWave = 8;
+    static constexpr int kMaxWave = 16;
     cudaStream_t cs_side[kMaxWave] = {};  // extra compute streams of the chunk wavefront
-    // streams in the chunk wavefront (GP_WAVE=1..8; default 8 from K = 16 on, else 4).
-    // Reddit shape, one B200: K = 32: 8 streams 0.433, 6: 0.443, 4: 0.449, 3: 0.457 s/epoch
-    // (2: 0.466 in round 1); K = 16: 8: 0.404, 6: 0.405, 4: 0.419; K = 8: 4 streams 0.376
-    // vs 6: 0.388; K = 4: 4 = 6.
+    // streams in the chunk wavefront (GP_WAVE=1..16; default 12 from K = 32 on, 8 from 16, else
+    // 4). Reddit shape, one B200: K = 32: 16 streams 0.428, 12: 0.429, 8: 0.433, 6: 0.443, 4:
+    // 0.449, 3: 0.457 s/epoch (2: 0.466 in round 1); K = 16: 12: 0.407, 8: 0.404, 6: 0.405, 4:
+    // 0.419; K = 8: 4 streams 0.376 vs 6: 0.388; K = 4: 4 = 6.
     int wave_w = 4;
     // GP_MERGED_G=1: one gather table per layer (G == Gs). A row of G holds the
     // snapshot until its chunk rewrites it, so the forward gathers read a single
@@ -636,7 +636,7 @@ struct Stage {
         GP_CUDA(cudaSetDevice(device));
         GP_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, device));
         GP_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-        wave_w = K >= 16 ? 8 : 4;
+        wave_w = K >= 32 ? 12 : (K >= 16 ? 8 : 4);
         if (const char* e = std::getenv("GP_WAVE")) wave_w = std::max(1, std::min(kMaxWave, std::atoi(e)));
         for (int w = 1; w < wave_w; ++w) GP_CUDA(cudaStreamCreateWithFlags(&cs_side[w], cudaStreamNonBlocking));
         GP_CUDA(cudaEventCreate(&ev_start));
