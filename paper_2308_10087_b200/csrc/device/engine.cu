@@ -366,6 +366,10 @@ struct Stage {
     // table (half the L2 footprint); the wavefront then also orders "chunk j+1
     // writes G_{i+1}" after "chunk j's layer i+1 gather" (wave_reads_done).
     bool merged_g = true;
+    // GP_TC_MIX=1: Gcn2Conv identity mix in the tcgen05 epilogue from the unsplit input row
+    // (forward h error vs fp64 3-8x lower: median 3-9e-8 vs 2e-7 of max|row|; 1.5 % slower
+    // epoch: 0.366 vs 0.360 s at K = 4); 0 (default): folded into W' = beta W + (1 - beta) I
+    bool tc_mix_epi = false;
     // GP_LEAN=1 (default): four N x H buffers per layer instead of seven. dz is written
     // in place over the layer's output h (the backward reads h[v] only for its own
     // ReLU mask, in the same lane, right before writing dz[v]); the backward gather
@@ -624,6 +628,7 @@ struct Stage {
         }
         if (needs_h0 && (H == 0 || H > kMaxWidth)) throw Error(GP_EINVAL, "bad hidden width");
         if (const char* e = std::getenv("GP_MERGED_G")) merged_g = std::atoi(e) != 0;
+        if (const char* e = std::getenv("GP_TC_MIX")) tc_mix_epi = std::atoi(e) != 0;
         if (const char* e = std::getenv("GP_LEAN")) lean = std::atoi(e) != 0;
         if (const char* e = std::getenv("GP_TC_XFORM")) use_tc_xform = std::atoi(e) != 0;
         if (const char* e = std::getenv("GP_TC_DENSE")) tc_dense = std::atoi(e) != 0;
@@ -1464,8 +1469,8 @@ struct Stage {
         const uint32_t nw = d.din * d.dout;
         launch(GP_K_OPTIM, nw * 8.0, 0, 0,
                [&]() { k_transpose<<<(nw + 255) / 256, 256, 0, cs>>>(d.W, d.WT, d.din, d.dout); });
-        if (d.tc) {  // W' = beta W + (1 - beta) I (Gcn2Conv) as tf32 hi / lo operands
-            const bool g2 = d.spec.kind == GP_GCN2CONV;
+        if (d.tc) {  // W (or, GP_TC_MIX=0, W' = beta W + (1 - beta) I for Gcn2Conv) as tf32 hi / lo
+            const bool g2 = d.spec.kind == GP_GCN2CONV && !tc_mix_epi;
             const float beta = float(d.spec.beta), omb = 1.f - beta;
             launch(GP_K_OPTIM, nw * 12.0, 0, 0, [&]() {
                 k_tc_prep<<<(nw + 255) / 256, 256, 0, cs>>>(d.W, d.din, d.dout, xf_pad8k(d.din), xf_pad16(d.dout), 0,
@@ -1506,7 +1511,16 @@ struct Stage {
         x.gnstride = p.gnstride;
         x.next_mask = p.next_mask;
         x.orig = p.orig;
+        tc_mix(d, x);
         return x;
+    }
+    // Gcn2Conv identity mix in the transform epilogue (GP_TC_MIX=1) or folded into the
+    // prepared operand (GP_TC_MIX=0, default)
+    void tc_mix(const LayerDev& d, TcXformParams& x) const {
+        if (d.spec.kind != GP_GCN2CONV || !tc_mix_epi) return;
+        x.mix = 1;
+        x.mbeta = float(d.spec.beta);
+        x.momb = 1.f - x.mbeta;
     }
     TcXformParams tc_bwd_params(const LayerDev& d, const BwdParams& p) const {
         TcXformParams x{};
@@ -1526,6 +1540,7 @@ struct Stage {
         x.dh0 = p.dh0;
         x.dh0stride = p.dh0stride;
         x.bg = p.bg;
+        tc_mix(d, x);
         return x;
     }
 

@@ -4,6 +4,7 @@
 // forward  (kernel::forward_row, nn.hpp:183-196):  out = act(pre . W' + b), then h and
 //          the next layer's dropped gather row; Gcn2Conv folds its identity mix into the
 //          operand, W' = beta W + (1 - beta) I, so out = (1-beta) pre + beta pre.W in one GEMM
+//          (mix = 1: B = W and the epilogue mixes from the unsplit pre row instead)
 // backward (kernel::backward_out_row, nn.hpp:202-218): D = dz . W'^T with the same fold
 //          (dagg = (1-beta) dz + beta dz.W^T); Gcn2Conv: dh0 += alpha D, bg = (1-alpha) D;
 //          otherwise bg = D
@@ -58,6 +59,12 @@ struct TcXformParams {
     float* dh0;
     uint32_t dh0stride;
     float* bg;
+    // mix = 1 (Gcn2Conv, GP_TC_MIX=1): B holds W itself and the epilogue applies the identity
+    // mix in fp32 from the unsplit input row, out = omb * A + beta * (A.W) (the reference's own
+    // expression, nn.hpp:188-190 / :207-209), so only the small beta term carries the TF32
+    // split error; mix = 0 (default): the mix is folded into B (W' = beta W + (1 - beta) I)
+    uint32_t mix;
+    float mbeta, momb;
 };
 
 __host__ __device__ constexpr uint32_t xf_pad16(uint32_t x) { return (x + 15u) & ~15u; }
@@ -211,6 +218,15 @@ __global__ void __launch_bounds__(kXfThreads, 1) k_tc_xform(TcXformParams p) {
             tmem_ld8(tmem + ((32u * q) << 16) + acc * npad + c0, a);
             if (!valid || c0 >= p.ostride) continue;
             float o[8];
+            float x[8];  // mix: the unsplit input row (pre / dz) at these columns (square layer)
+            if (p.mix) {
+                const float* xr = p.A + size_t(v) * p.astride + c0;
+                const float4 x0 = *reinterpret_cast<const float4*>(xr), x1 = *reinterpret_cast<const float4*>(xr + 4);
+                x[0] = x0.x, x[1] = x0.y, x[2] = x0.z, x[3] = x0.w, x[4] = x1.x, x[5] = x1.y, x[6] = x1.z, x[7] = x1.w;
+                if (BWD)
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) a[i] = __fadd_rn(__fmul_rn(p.momb, x[i]), __fmul_rn(p.mbeta, a[i]));
+            }
             if (!BWD) {
                 float g[8];
 #pragma unroll
@@ -219,6 +235,7 @@ __global__ void __launch_bounds__(kXfThreads, 1) k_tc_xform(TcXformParams p) {
                     float val = 0.f;
                     if (c < p.ndim) {
                         val = __fadd_rn(a[i], bias_sh[c]);
+                        if (p.mix) val = __fadd_rn(__fmul_rn(p.momb, x[i]), __fmul_rn(p.mbeta, val));
                         if (p.relu && val < 0.f) val = 0.f;
                     }
                     o[i] = val;

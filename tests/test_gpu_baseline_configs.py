@@ -98,7 +98,7 @@ def reddit(gp):
     return gp.Dataset.synthetic_er(*CFG2)
 
 
-@pytest.mark.parametrize("tc", ["1", "0"], ids=["tcgen05", "cuda_core"])
+@pytest.mark.parametrize("tc", ["1", "0", "mix"], ids=["tcgen05", "cuda_core", "tcgen05_epilogue_mix"])
 def test_cfg2_reddit_shape_gcnii4_loss_and_every_gradient(gp, reddit, monkeypatch, tc):
     """Whole-graph epoch 1 (train_sequential's first epoch == S = 1, K = 1 pipeline,
     test_engines.cpp:103-113) at the full Reddit shape: loss, every parameter gradient (rel 1e-4),
@@ -106,7 +106,9 @@ def test_cfg2_reddit_shape_gcnii4_loss_and_every_gradient(gp, reddit, monkeypatc
     CUDA-core transforms: pre / h rows are bit-exact (sums to 1e-9), loss rel 1e-6. tcgen05
     (3xTF32) transforms: fp32-level rows (sums rel 1e-5), loss rel 1e-5."""
     monkeypatch.setenv("GP_LEAN", "0")  # read h back after the epoch
-    monkeypatch.setenv("GP_TC_XFORM", tc)
+    monkeypatch.setenv("GP_TC_XFORM", "0" if tc == "0" else "1")
+    if tc == "mix":  # GCNII identity mix in the tcgen05 epilogue instead of folded into W'
+        monkeypatch.setenv("GP_TC_MIX", "1")
     exact = tc == "0"
     ref = golden("cfg2_reddit_gcnii4_forward")
     ds = reddit

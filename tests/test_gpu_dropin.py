@@ -27,6 +27,12 @@ def run(name, timeout):
     exe = os.path.join(BIN, name)
     if not os.path.exists(exe):
         pytest.fail(f"{exe} not built (tests/cpp/build_dropin.py runs in build() next to /root/reference)")
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "cpp"))
+    from build_dropin import header_digest
+    stamp = os.path.join(BIN, "headers.sha256")
+    if not os.path.exists(stamp) or open(stamp).read().strip() != header_digest():
+        pytest.fail("drop-in binaries were compiled against other API headers: rerun tests/cpp/build_dropin.py")
     r = subprocess.run([exe], capture_output=True, text=True, timeout=timeout)
     return r.returncode, r.stdout + r.stderr
 

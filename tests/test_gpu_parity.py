@@ -265,7 +265,11 @@ def test_train_sage_historical_gradients(gp):
                    fix_alpha=2, historical_gradients=True)
 
 
-def test_train_gcnii_pipeline_stale_two_stages(gp):
+@pytest.mark.parametrize("mix", ["0", "1"], ids=["folded_mix", "epilogue_mix"])
+def test_train_gcnii_pipeline_stale_two_stages(gp, mix, monkeypatch):
+    """GCNII over two stages, 10 epochs; with the identity mix folded into the tcgen05 operand
+    (default) and applied in the transform epilogue (GP_TC_MIX=1)."""
+    monkeypatch.setenv("GP_TC_MIX", mix)
     _train_compare(gp, "train_gcnii_s2k4", er500(gp), gp.ModelConfig(kind=2, layers=6, hidden=16), 2, 4, 3, 10, 43,
                    fix_alpha=3)
 
