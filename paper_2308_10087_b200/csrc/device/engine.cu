@@ -366,6 +366,7 @@ struct Stage {
     // table (half the L2 footprint); the wavefront then also orders "chunk j+1
     // writes G_{i+1}" after "chunk j's layer i+1 gather" (wave_reads_done).
     bool merged_g = true;
+    bool host_timing = false;  // GP_HOST_TIMING=1: per-epoch enqueue vs device time on stderr
     // GP_TC_MIX=1: Gcn2Conv identity mix in the tcgen05 epilogue from the unsplit input row
     // (forward h error vs fp64 3-8x lower: median 3-9e-8 vs 2e-7 of max|row|; 1.5 % slower
     // epoch: 0.366 vs 0.360 s at K = 4); 0 (default): folded into W' = beta W + (1 - beta) I
@@ -628,6 +629,7 @@ struct Stage {
         }
         if (needs_h0 && (H == 0 || H > kMaxWidth)) throw Error(GP_EINVAL, "bad hidden width");
         if (const char* e = std::getenv("GP_MERGED_G")) merged_g = std::atoi(e) != 0;
+        if (const char* e = std::getenv("GP_HOST_TIMING")) host_timing = std::atoi(e) != 0;
         if (const char* e = std::getenv("GP_TC_MIX")) tc_mix_epi = std::atoi(e) != 0;
         if (const char* e = std::getenv("GP_LEAN")) lean = std::atoi(e) != 0;
         if (const char* e = std::getenv("GP_TC_XFORM")) use_tc_xform = std::atoi(e) != 0;
@@ -2868,6 +2870,7 @@ struct Stage {
                 seen[k] = 1;
             }
         }
+        const auto h_start = std::chrono::steady_clock::now();
         std::fill(bytes_sent, bytes_sent + 6, 0);
         std::fill(msgs_sent, msgs_sent + 6, 0);
         launches = 0;
@@ -3079,6 +3082,8 @@ struct Stage {
             trace_add(GP_TRACE_COMPUTE, -1, c0, trace_mark());  // epoch-close parameter step
         }
         GP_CUDA(cudaEventRecord(ev_end, cs));
+        const double enqueue_ms =
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h_start).count();
         if (tr.ipc_up.linked() || tr.ipc_down.linked() || tr.ipcg.linked) {
             sync_watchdog(cs, 600.0);
             for (cudaStream_t st : {tr.ipc_up.stream, tr.ipc_down.stream, tr.ipc_up.rstream, tr.ipc_down.rstream})
@@ -3103,6 +3108,9 @@ struct Stage {
             st.msgs_sent[i] = msgs_sent[i];
         }
         GP_CUDA(cudaEventElapsedTime(&st.epoch_ms, ev_start, ev_end));
+        if (host_timing)  // host-side enqueue time of the epoch next to its device time
+            std::fprintf(stderr, "[gp epoch] stage %u t=%u enqueue %.1f ms device %.1f ms launches %llu\n", s, t,
+                         enqueue_ms, double(st.epoch_ms), (unsigned long long)launches);
         st.kernel_launches = launches;
         float busy = 0.f;
         std::vector<std::pair<float, float>> iv[GP_K_NUM];  // launch intervals since ev_start
