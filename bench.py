@@ -134,24 +134,27 @@ def workload_config(args, S, K):
 def reference_epochs(args, S, K):
     """Whole epochs of the reference's own train_pipeline<float> (engines_impl.hpp:911-920,
     oracle/_ref/ref_driver epochs; Fabric::Mode::Concurrent, one thread per stage worker)
-    on the same synthetic graph, at L=3 and L=4 layers, run side by side. A 64-layer epoch
-    on one core is hours, so the L-layer value is the projection
-    t(3) + (L-3) * (t(4) - t(3)), labelled as such."""
+    on the same synthetic graph and the same S stages, at two layer counts La and Lb = La + S
+    (one more layer on every stage), run side by side: La = 3 at S = 1, else the smallest
+    multiple of S that is >= 3. A 64-layer epoch on the host is hours, so the L-layer value is
+    the projection t(La) + (L - La) * (t(Lb) - t(La)) / S, labelled as
+    such."""
     from oracle.blob import REF_DRIVER, read_blob
     if not os.path.exists(REF_DRIVER):
         return None, "oracle/_ref/ref_driver not built"
     N, E2, F, Cc, H, model, L, _ = WORKLOADS[args.workload]
     L = args.layers or L
     p = E2 / (N * (N - 1))
-    Ls = (3, 4) if L > 16 else (L,)
-    Sm = min(S, 3)  # L=3 cannot be split over more stages than layers
+    La = S * -(-max(3, S) // S)
+    Lb = La + S
+    Ls = (La, Lb) if L > 16 and L > Lb else (L,)  # up to 16 layers: the whole model is measured
     with tempfile.TemporaryDirectory() as td:
         procs = {}
         t0 = time.perf_counter()
         for l in Ls:
             out = os.path.join(td, f"e{l}.blob")
             cmd = [REF_DRIVER, "epochs", f"spec=er:{N}:{p!r}:1:{F}:{Cc}:1", f"model={model}", f"layers={l}",
-                   f"hidden={H}", f"S={min(Sm, l)}", f"K={K}", "chunk_seed=1", "seed=1", "epochs=1", f"out={out}"]
+                   f"hidden={H}", f"S={min(S, l)}", f"K={K}", "chunk_seed=1", "seed=1", "epochs=1", f"out={out}"]
             procs[l] = (subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True), out)
         res = {}
         for l, (pr, out) in procs.items():
@@ -162,22 +165,20 @@ def reference_epochs(args, S, K):
         wall = time.perf_counter() - t0
     ep = {l: float(res[l]["epoch_s"][0]) for l in Ls}
     if len(Ls) == 2:
-        marg = ep[4] - ep[3]
-        full = ep[3] + (L - 3) * marg
-        how = (f"projection t(3)+(L-3)*(t(4)-t(3)) from measured whole train_pipeline<float> epochs at "
-               f"L=3 ({ep[3]:.1f} s) and L=4 ({ep[4]:.1f} s), marginal {marg:.1f} s per conv layer")
+        marg = (ep[Lb] - ep[La]) / S
+        full = ep[La] + (L - La) * marg
+        how = (f"projection t({La})+(L-{La})*(t({Lb})-t({La}))/S from measured whole train_pipeline<float> epochs "
+               f"at L={La} ({ep[La]:.1f} s) and L={Lb} ({ep[Lb]:.1f} s) over S={S} stages, marginal {marg:.1f} s "
+               f"per layer")
     else:
         full = ep[L]
         how = f"measured whole train_pipeline<float> epoch at L={L} ({full:.2f} s)"
-    if S > Sm:  # more stages than the measured runs: each stage is one single-threaded worker
-        full = full * Sm / S * (K + S - 1) / (K + Sm - 1)
-        how += f"; scaled from S={Sm} to S={S} stage threads with (K+S-1)/K fill/drain"
     g = res[Ls[0]]
-    sample = (f"{how}; same graph/features/K/seed as the GPU arm, S={min(Sm, Ls[0])} worker thread(s) per run, "
+    sample = (f"{how}; same graph/features/K/seed as the GPU arm, S={S} worker thread(s) per run, "
               f"runs side by side; excl. dataset gen ({float(g['gen_s'][0]):.1f} s), make_chunks "
               f"({float(g['chunk_s'][0]):.1f} s) and the call's setup ({float(g['setup_s'][0]):.1f} s); "
               f"CPU wall {wall:.0f} s")
-    return {"value": full, "cores": min(Sm, Ls[0]), "sample": sample, "projection": len(Ls) == 2 or S > Sm,
+    return {"value": full, "cores": S, "sample": sample, "projection": len(Ls) == 2,
             "measured_epoch_s": ep, "cpu_wall_s": wall, "cpu": cpu_info()}, None
 
 
