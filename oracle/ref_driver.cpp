@@ -444,6 +444,9 @@ void cmd_epochs(const Args& a) {
     opt.model = model_from(a);
     opt.seed = argu(a, "seed", "1");
     opt.fabric.mode = Fabric::Mode::Concurrent;
+    // a deep stage's first message can take minutes at full size: the reference's 60 s fabric
+    // watchdog would abort the timing run
+    opt.fabric.watchdog_seconds = argd(a, "watchdog", "36000");
     const uint32_t L = uint32_t(build_layer_specs(opt.model, d.num_features(), d.num_classes).size());
     const auto sa = make_stage_assignment(L, S);
     opt.epochs = 0;
