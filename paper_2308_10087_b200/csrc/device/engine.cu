@@ -12,6 +12,7 @@
 //   stage messages    :690-724  -> Transport (local D2D, CUDA-IPC peer rings, or NCCL)
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <cub/device/device_scan.cuh>
 #include <nccl.h>  // types and the config initializer only; libnccl.so.2 is dlopen'ed
 #include <dlfcn.h>
 #include <unistd.h>
@@ -409,6 +410,14 @@ struct Stage {
     uint2* edges_m = nullptr;
     uint2* edges_mt = nullptr;
     uint32_t* orig = nullptr;          // new -> original id (device)
+    // GP_BWD_CSR=1 (default): the backward gathers of a stale-mode epoch read a per-epoch
+    // done-filtered copy of the own rows' CSR (k_done_csr) instead of filtering each batch
+    bool bwd_csr = true;
+    bool bwd_csr_ready = false;        // built for the current epoch's backward order
+    uint64_t* rowptr_f = nullptr;
+    uint2* edges_f = nullptr;
+    void* scan_tmp = nullptr;
+    size_t scan_tmp_bytes = 0;
     uint32_t* id_rows = nullptr;       // own rows in ascending original id (reductions)
     std::vector<uint32_t> perm;        // original -> new (host)
     std::vector<uint32_t> inv;         // new -> original (host)
@@ -629,6 +638,7 @@ struct Stage {
         }
         if (needs_h0 && (H == 0 || H > kMaxWidth)) throw Error(GP_EINVAL, "bad hidden width");
         if (const char* e = std::getenv("GP_MERGED_G")) merged_g = std::atoi(e) != 0;
+        if (const char* e = std::getenv("GP_BWD_CSR")) bwd_csr = std::atoi(e) != 0;
         if (const char* e = std::getenv("GP_HOST_TIMING")) host_timing = std::atoi(e) != 0;
         if (const char* e = std::getenv("GP_TC_MIX")) tc_mix_epi = std::atoi(e) != 0;
         if (const char* e = std::getenv("GP_LEAN")) lean = std::atoi(e) != 0;
@@ -672,6 +682,10 @@ struct Stage {
             const uint64_t nnz_m = nnz_norm >= n ? nnz_norm - n : nnz_norm;  // no self loops
             add(8ull * (n + 1));
             add(2 * 8ull * nnz_m);
+        }
+        if (needs_bwd_csr()) {  // done-filtered backward CSR (own rows; hybrid: a 1/G share)
+            add(8ull * (n + 1));
+            add(8ull * ((nnz_norm + G - 1) / G));
         }
         if (first) add(4ull * n * pad8(F_in ? F_in : specs[0].in_dim));  // x0
         if (last) add(5ull * n);                              // labels + split
@@ -1341,6 +1355,7 @@ struct Stage {
         build_halo();
         build_id_rows();
         ensure_own_buffers();
+        alloc_bwd_csr();
         graph_ready = true;
     }
 
@@ -1349,6 +1364,54 @@ struct Stage {
     // in this order, with split boundaries fixed by the row count alone, makes parameter
     // gradients and the loss independent of the chunk plan (a synchronous pipeline then
     // equals the sequential trainer bit for bit, test_engines.cpp:115-126).
+    // A stale-mode backward gather (PREV_AGG) filters by done chunks: layers i >= 1 that
+    // aggregate (not SageConv: its filtered gather runs over the mean CSR), and layer 0 on
+    // a non-first stage (the dh_in gather)
+    bool needs_bwd_csr() const {
+        if (!bwd_csr || sync || hist || K < 2) return false;
+        for (uint32_t i = 0; i < len; ++i)
+            if (L[i].agg && !L[i].sage && (i > 0 || !first)) return true;
+        return false;
+    }
+    uint64_t bwd_csr_cap = 0;
+    void alloc_bwd_csr() {
+        if (!needs_bwd_csr()) return;
+        const uint64_t own_nnz = hg->rp[own_end()] - hg->rp[own_begin()];
+        if (rowptr_f && own_nnz <= bwd_csr_cap) return;
+        rowptr_f = dalloc<uint64_t>(size_t(n) + 1);  // rowptr_f[own_begin] stays 0
+        edges_f = dalloc<uint2>(std::max<uint64_t>(own_nnz, 1), false);
+        bwd_csr_cap = own_nnz;
+        const uint32_t items = own_end() - own_begin() + 1;
+        scan_tmp_bytes = 0;
+        GP_CUDA(cub::DeviceScan::InclusiveSum(nullptr, scan_tmp_bytes, rowptr_f, rowptr_f, items, cs));
+        scan_tmp = dalloc<char>(std::max<size_t>(scan_tmp_bytes, 16), false);
+    }
+
+    // The epoch's done-filtered backward CSR: chunk order[kk] runs its backward with
+    // done = {order[kk], ..., order[K-1]} (engines_impl.hpp:829-866)
+    void build_bwd_csr(const std::vector<uint32_t>& ord) {
+        bwd_csr_ready = false;
+        if (!rowptr_f || !needs_bwd_csr()) return;
+        DoneCsrParams p{};
+        p.rowptr = rowptr;
+        p.edges = edges;
+        p.rowptr_f = rowptr_f;
+        p.edges_f = edges_f;
+        for (uint32_t k = 0; k <= K; ++k) p.rb[k] = row_begin(k);
+        uint64_t done = 0;
+        for (uint32_t kk = K; kk-- > 0;) p.mask[ord[kk]] = done |= 1ull << ord[kk];
+        const dim3 grid(std::max<uint32_t>(1, (uint32_t(num_sms) * 8 + K - 1) / K), K);
+        const uint32_t items = own_end() - own_begin() + 1;
+        const double eb = double(hg->rp[own_end()] - hg->rp[own_begin()]) * 8.0;
+        launch(GP_K_BWD_AGG, eb + double(items) * 16.0, 0, 0, [&]() {
+            k_done_csr<true><<<grid, kBlock, 0, cs>>>(p);
+            GP_CUDA(cub::DeviceScan::InclusiveSum(scan_tmp, scan_tmp_bytes, rowptr_f + own_begin(),
+                                                  rowptr_f + own_begin(), items, cs));
+            k_done_csr<false><<<grid, kBlock, 0, cs>>>(p);
+        });
+        bwd_csr_ready = true;
+    }
+
     void build_id_rows() {
         std::vector<uint32_t> rows;
         rows.reserve(own_end() - own_begin());
@@ -1411,6 +1474,7 @@ struct Stage {
         build_halo();
         build_id_rows();
         ensure_own_buffers();
+        alloc_bwd_csr();
         graph_ready = true;
     }
 
@@ -1910,6 +1974,11 @@ struct Stage {
             } else if (nx.agg) {
                 prev = hist ? PREV_AGG_HIST : (done == all_chunks() ? PREV_AGG_ALL : PREV_AGG);
                 e = hist ? double(rowptr_nnz(r0, r1)) : done_nnz(r0, r1, done);  // entries gathered
+                if (prev == PREV_AGG && bwd_csr_ready) {  // the same entries, pre-filtered
+                    p.rowptr = rowptr_f;
+                    p.edges = edges_f;
+                    prev = PREV_AGG_ALL;
+                }
             } else {
                 prev = PREV_OWN;
             }
@@ -2028,9 +2097,14 @@ struct Stage {
         else if (hist)
             launch(GP_K_BWD_AGG, bytes, 2.0 * e * d.din, e * d.sin * 4.0,
                    [&]() { bwd_nb<PREV_AGG_HIST, OUT_DHIN>(rows, kEdgeSlotBytes, p); });
-        else if (done == all_chunks())
+        else if (done == all_chunks() || bwd_csr_ready) {
+            if (done != all_chunks()) {  // the same entries, pre-filtered
+                p.rowptr = rowptr_f;
+                p.edges = edges_f;
+            }
             launch(GP_K_BWD_AGG, bytes, 2.0 * e * d.din, e * d.sin * 4.0,
                    [&]() { bwd_nb<PREV_AGG_ALL, OUT_DHIN>(rows, kEdgeSlotBytes, p); });
+        }
         else
             launch(GP_K_BWD_AGG, bytes, 2.0 * e * d.din, e * d.sin * 4.0,
                    [&]() { bwd_nb<PREV_AGG, OUT_DHIN>(rows, kEdgeSlotBytes, p); });
@@ -3003,6 +3077,7 @@ struct Stage {
         }
 
         // ---- backward ---------------------------------------------------------------
+        if (!sync) build_bwd_csr(ord);
         if (!sync) {
             // Wavefront over W streams (SURVEY §8(a')9): chunk j+1 of the backward order
             // runs layer i+1 while chunk j runs layer i. Legal because a chunk only
@@ -3075,6 +3150,7 @@ struct Stage {
                 for (uint32_t kk = K; kk-- > 0;) traced_send(ord[kk], [&]() { send_bwd(ord[kk]); });
         }
 
+        bwd_csr_ready = false;
         if (lean && hist && t % fix_alpha == 0) copy_snapshots(true);
         {
             cudaEvent_t c0 = trace_mark();

@@ -789,6 +789,44 @@ __global__ void __launch_bounds__(kBlock) k_pull_rows(PullParams p) {
     }
 }
 
+// Done-filtered CSR of one epoch's backward pass. backward_prev_row (nn.hpp:222-257)
+// gathers only the entries of chunks already processed; every layer of chunk k runs with
+// the same done set (the chunks at or after k in the forward order, engines_impl.hpp:
+// 829-866), so the filter is a per-epoch property of (row, entry), not of the layer. It is
+// applied once per epoch here, order-preserving, and the backward gathers of all layers
+// then read the compacted rows without a per-batch ballot. Pass 1 (COUNT) writes the kept
+// count of row v to rowptr_f[v + 1]; an in-place inclusive scan turns it into row
+// pointers (rowptr_f[own_begin] stays 0); pass 2 writes the kept entries.
+struct DoneCsrParams {
+    const uint64_t* rowptr;
+    const uint2* edges;
+    uint64_t* rowptr_f;
+    uint2* edges_f;
+    uint32_t rb[kMaxChunks + 1];  // chunk k owns rows [rb[k], rb[k + 1])
+    uint64_t mask[kMaxChunks];    // done set of chunk k's backward step
+};
+
+template <bool COUNT>
+__global__ void __launch_bounds__(kBlock) k_done_csr(const __grid_constant__ DoneCsrParams p) {
+    const uint32_t k = blockIdx.y;
+    const uint64_t m = p.mask[k];
+    const int lane = threadIdx.x & 31;
+    const uint32_t nw = gridDim.x * kWarpsPerBlock;
+    for (uint32_t v = p.rb[k] + blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5); v < p.rb[k + 1]; v += nw) {
+        const uint64_t e0 = p.rowptr[v], e1 = p.rowptr[v + 1];
+        uint64_t out = COUNT ? 0 : p.rowptr_f[v];
+        for (uint64_t e = e0; e < e1; e += 32) {
+            const bool in = e + lane < e1;
+            const uint2 x = in ? __ldcs(reinterpret_cast<const uint2*>(p.edges) + e + lane) : make_uint2(0u, 0u);
+            const bool ok = in && ((m >> (x.x >> kColBits)) & 1ull);
+            const unsigned b = __ballot_sync(kFull, ok);
+            if (!COUNT && ok) p.edges_f[out + __popc(b & ((1u << lane) - 1u))] = x;
+            out += __popc(b);
+        }
+        if (COUNT && lane == 0) p.rowptr_f[v + 1] = out;
+    }
+}
+
 // group_weight_sync (engines_impl.hpp:102-128): rank 0 folds the group's
 // gradients in rank order, g = ((g0 + g1) + g2) + ..., one rounding per add.
 struct FoldParams {
