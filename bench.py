@@ -469,8 +469,12 @@ def main():
         "edges_per_s": edges_per_s,
         "roofline": {"kernel": "k_fwd8<FWD_GCN|FWD_GCN2, 2, split> (CSR SpMM gather [+ GCNII initial-residual mix] -> pre; "
                                "the transform runs in k_tc_xform on tcgen05)",
-                     "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                     "frac": (achieved / hbm) if achieved else None, "peak_source": src,
+                     # achieved: algorithmic bytes per launch / the kernel's effective launch duration
+                     # in the timed region = its occupied time (union of the live launch intervals)
+                     # / launches. Launches of different chunks overlap on the wavefront streams, so
+                     # a single launch's own interval (achieved_live) counts the shared time twice.
+                     "bound": "hbm", "achieved": achieved_span, "peak": hbm, "unit": "GB/s",
+                     "frac": (achieved_span / hbm) if achieved_span else None, "peak_source": src,
                      # DRAM read + write bytes per launch (ncu) next to the algorithmic bytes per launch
                      "traffic": traffic, "traffic_unit": "bytes/launch", "traffic_source": traffic_src,
                      "alg_bytes_per_launch": alg_per_launch,
@@ -482,18 +486,22 @@ def main():
                      "gather_frac_serial": (gather_serial / ceiling) if gather_serial and ceiling else None,
                      "timing": (f"CUDA events around each of the {fa['launches']} launches of the kernel inside "
                                 "the timed region (its stream; chunk wavefront on)"),
-                     "ms_per_launch": fa["ms"] / fa["launches"] if fa["launches"] else None,
+                     "ms_per_launch": span / fa["launches"] if fa["launches"] else None,
+                     "ms_per_launch_live": fa["ms"] / fa["launches"] if fa["launches"] else None,
+                     "achieved_live": achieved, "frac_live": (achieved / hbm) if achieved else None,
                      "achieved_serial": achieved_serial,
                      "span_share_of_step": (span / args.steps) / ms_step if ms_step else None,
                      "achieved_span": achieved_span,
                      "frac_span": (achieved_span / hbm) if achieved_span else None,
                      "l2_gather_gbs_span": gather_span,
                      "gather_frac_span": (gather_span / ceiling) if gather_span and ceiling else None,
-                     "note": ("achieved: live launch durations, which include the kernels co-running on the "
-                              "other wavefront streams (per-step kernel time = share_of_step x the step); "
-                              "achieved_span: the same bytes over the time at least one launch of the kernel "
-                              "was running (union of the live launch intervals); achieved_serial: over the "
-                              "isolated launch time of the serial profiling epoch"),
+                     "note": ("achieved (= achieved_span): algorithmic bytes over the time at least one "
+                              "launch of the kernel was running (union of the live launch intervals, CUDA "
+                              "events on each launch's stream), i.e. per launch over span / launches; "
+                              "achieved_live: over each launch's own interval, which includes the launches "
+                              "of other chunks co-running on the other wavefront streams (summed intervals = "
+                              "share_of_step x the step); achieved_serial: over the isolated launch time of "
+                              "the serial profiling epoch"),
                      "share_of_step": (fa["ms"] / args.steps) / ms_step if ms_step else None},
         # epoch-level bound: every byte the forward and backward SpMMs gather per epoch, at the
         # measured random-row gather ceiling of this shape, is a lower bound on the epoch time
