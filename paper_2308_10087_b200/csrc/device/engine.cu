@@ -362,6 +362,11 @@ struct Stage {
     // 0.449, 3: 0.457 s/epoch (2: 0.466 in round 1); K = 16: 12: 0.407, 8: 0.404, 6: 0.405, 4:
     // 0.419; K = 8: 4 streams 0.376 vs 6: 0.388; K = 4: 4 = 6.
     int wave_w = 4;
+    // GP_REMASK_OVERLAP=1 (default): the epoch-start snapshot remasks of layers >= 1 run on
+    // their own stream, each waited for only by the kernels that write or read that layer's
+    // gather table, so they overlap the first chunk's first layers instead of preceding them
+    bool remask_overlap = true;
+    cudaStream_t cs_prep = nullptr;
     // GP_MERGED_G=1: one gather table per layer (G == Gs). A row of G holds the
     // snapshot until its chunk rewrites it, so the forward gathers read a single
     // table (half the L2 footprint); the wavefront then also orders "chunk j+1
@@ -583,6 +588,7 @@ struct Stage {
         if (cs) cudaStreamDestroy(cs);
         for (auto st : cs_side)
             if (st) cudaStreamDestroy(st);
+        if (cs_prep) cudaStreamDestroy(cs_prep);
     }
 
     // ---- configuration ------------------------------------------------------
@@ -656,6 +662,8 @@ struct Stage {
         wave_w = K >= 32 ? 12 : (K >= 16 ? 8 : 4);
         if (const char* e = std::getenv("GP_WAVE")) wave_w = std::max(1, std::min(kMaxWave, std::atoi(e)));
         for (int w = 1; w < wave_w; ++w) GP_CUDA(cudaStreamCreateWithFlags(&cs_side[w], cudaStreamNonBlocking));
+        if (const char* e = std::getenv("GP_REMASK_OVERLAP")) remask_overlap = std::atoi(e) != 0;
+        if (remask_overlap) GP_CUDA(cudaStreamCreateWithFlags(&cs_prep, cudaStreamNonBlocking));
         GP_CUDA(cudaEventCreate(&ev_start));
         GP_CUDA(cudaEventCreate(&ev_end));
         alloc();
@@ -2974,15 +2982,31 @@ struct Stage {
         state_restored = false;
         dual_snap = lean && !sync && G == 1 && t % fix_alpha == 0;
         dual_done.assign(len, 0);
-        // Masked gather sources start from the snapshot rows (stale reads).
+        // Masked gather sources start from the snapshot rows (stale reads). With
+        // remask_overlap, layers >= 1 are remasked on cs_prep; rm_ev[i] orders every chunk's
+        // first write of G_i (the layer i-1 epilogue) and read of it after the remask.
+        std::vector<cudaEvent_t> rm_ev(len, nullptr);
+        const bool ovl = remask_overlap && cs_prep && !sync;
+        if (ovl) GP_CUDA(cudaStreamWaitEvent(cs_prep, record_event(), 0));
         for (uint32_t i = 0; i < len; ++i) {
             if (!L[i].agg) continue;
             if (i == 0 && first) {
                 remask(0, x0, 0, n, drop_key(t, L[0].l, L[0].din));  // cur == snap == x0
             } else if (!sync) {
-                remask(i, snap_src(i), 0, n, drop_key(t, L[i].l, L[i].din), true);
+                if (ovl && i > 0) {
+                    cudaStream_t main = cs;
+                    cs = cs_prep;
+                    remask(i, snap_src(i), 0, n, drop_key(t, L[i].l, L[i].din), true);
+                    rm_ev[i] = record_event();
+                    cs = main;
+                } else {
+                    remask(i, snap_src(i), 0, n, drop_key(t, L[i].l, L[i].din), true);
+                }
             }
         }
+        auto wait_remask = [&](uint32_t i) {  // before a kernel that writes or reads G_i
+            if (i < len && rm_ev[i]) GP_CUDA(cudaStreamWaitEvent(cs, rm_ev[i], 0));
+        };
 
         // ---- forward -----------------------------------------------------------
         const uint64_t all_done = K == 64 ? ~0ull : ((1ull << K) - 1);
@@ -3037,6 +3061,8 @@ struct Stage {
                     if (L[i].agg)  // G_i rows of the W-1 previous chunks (other streams)
                         for (uint32_t w = 1; w < uint32_t(W) && w <= kk; ++w)
                             GP_CUDA(cudaStreamWaitEvent(cs, ev[(kk - w) % W][i], 0));
+                    if (kk == 0) wait_remask(i);  // chunk 0 reads G_i (later chunks follow it)
+                    wait_remask(i + 1);           // the epilogue writes this chunk's rows of G_{i+1}
                     forward_layer(i, r0, r1, t, done);
                     if (W > 1) mine[i + 1] = record_event();
                 }
@@ -3044,6 +3070,7 @@ struct Stage {
                 if (!last) traced_send(k, [&]() { send_fwd(k); });
             }
             wave_join(W, main);
+            for (uint32_t i = 0; i < len; ++i) wait_remask(i);
         } else {
             if (!first)
                 for (uint32_t kk = 0; kk < K; ++kk) traced_recv(ord[kk], [&]() { recv_fwd(ord[kk]); });

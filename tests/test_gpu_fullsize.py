@@ -112,7 +112,8 @@ def test_reddit_shape_64_layer_runs_are_deterministic(gp):
         assert np.array_equal(Wa.view(np.uint32), Wb.view(np.uint32))
 
 
-@pytest.mark.parametrize("env", [{}, {"GP_MERGED_G": "1"}], ids=["wavefront", "wavefront_merged_g"])
+@pytest.mark.parametrize("env", [{}, {"GP_MERGED_G": "0"}, {"GP_REMASK_OVERLAP": "0"}],
+                         ids=["wavefront", "wavefront_split_g", "wavefront_remask_in_order"])
 def test_reddit_shape_wavefront_equals_serial_chunks(gp, env, monkeypatch):
     """K = 32 (the 8-stage chunk count, where four chunks are in flight on the wavefront streams): the
     wavefront, with split or merged gather tables, trains bit-identically to serial chunks (GP_WAVE=1),
