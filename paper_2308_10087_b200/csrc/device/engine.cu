@@ -390,6 +390,9 @@ struct Stage {
     // GP_TC_XFORM=1 (default): the GCN / GCNII row transforms (pre.W', dz.W'^T and their
     // epilogues) run on tcgen05 (3xTF32, fp32-level); 0: the bit-exact CUDA-core tiles
     bool use_tc_xform = true;
+    // GP_XF_PAD: launches of at least this many rows stage A with the padded k-core stride
+    // (tc_xform.cuh; 1 = always, 0 = never; default 16384: K = 4 chunks yes, K = 32 no)
+    uint32_t xf_pad_rows = 16384;
     bool tc_dense = true;  // GP_TC_DENSE=0: Dense layers keep the fused CUDA-core GEMV kernels
     bool state_restored = false;  // gp_set_history: the snapshot rows were loaded
     // lean layout, epoch t with t % fix_alpha == 0 (the next epoch refreshes the snapshot):
@@ -663,6 +666,10 @@ struct Stage {
         if (const char* e = std::getenv("GP_WAVE")) wave_w = std::max(1, std::min(kMaxWave, std::atoi(e)));
         for (int w = 1; w < wave_w; ++w) GP_CUDA(cudaStreamCreateWithFlags(&cs_side[w], cudaStreamNonBlocking));
         if (const char* e = std::getenv("GP_REMASK_OVERLAP")) remask_overlap = std::atoi(e) != 0;
+        if (const char* e = std::getenv("GP_XF_PAD")) {
+            const long v = std::atol(e);
+            xf_pad_rows = v == 0 ? UINT32_MAX : v == 1 ? 0u : uint32_t(v);
+        }
         if (remask_overlap) GP_CUDA(cudaStreamCreateWithFlags(&cs_prep, cudaStreamNonBlocking));
         GP_CUDA(cudaEventCreate(&ev_start));
         GP_CUDA(cudaEventCreate(&ev_end));
@@ -1558,7 +1565,8 @@ struct Stage {
     // tcgen05 transform launch over rows [r0, r1): one CTA per SM (>= 116 KB of shared
     // memory, so a second CTA never waits on TMEM columns), persistent over 128-row tiles
     template <bool BWD>
-    void tc_xform_go(const TcXformParams& x) {
+    void tc_xform_go(TcXformParams x) {
+        x.a_lbo = x.r1 - x.r0 >= xf_pad_rows ? kXfLboPad : kXfLboDense;
         const uint32_t ntiles = (x.r1 - x.r0 + kXfM - 1) / kXfM;
         const size_t smem = std::max<size_t>(xf_smem_bytes(x.kpad, x.npad), 116 * 1024);
         const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(ntiles, uint32_t(num_sms)));

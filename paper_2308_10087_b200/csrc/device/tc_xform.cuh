@@ -65,6 +65,7 @@ struct TcXformParams {
     // split error; mix = 0 (default): the mix is folded into B (W' = beta W + (1 - beta) I)
     uint32_t mix;
     float mbeta, momb;
+    uint32_t a_lbo;  // A stage k-core stride in bytes: kXfLboDense or kXfLboPad
 };
 
 __host__ __device__ constexpr uint32_t xf_pad16(uint32_t x) { return (x + 15u) & ~15u; }
@@ -76,8 +77,18 @@ constexpr uint32_t kXfSmemMax = 200 * 1024;  // H = 128: 128 + 64 KB
 // (measured alternatives, Reddit shape, per K = 4 backward launch: this version 59 us;
 // two chunks of A in flight in registers, 59 us; a 2-6 deep cp.async raw ring with the
 // epilogue's dh0 rows prefetched across the chunk loop, 88 us)
+// A stage k-core stride (p.a_lbo): the dense 16 row groups (kXfLboDense), or + 64 bytes
+// (kXfLboPad) so k-cores kc and kc + 1 start in opposite halves of the 128-byte bank space
+// and a warp's 32 stores (4 rows x 8 k-cores) spread over all 8 bank groups (dense: an 8-way
+// conflict on every store). The padded stride is measured faster for large launches (K = 4:
+// 17.3 vs 19.2 ms forward, 13.1 vs 15.0 ms backward per epoch, epoch -0.8 %) but the K = 32
+// wavefront epoch is ~1 % slower with it despite faster kernels, so the engine picks it by
+// launch size (GP_XF_PAD)
+constexpr uint32_t kXfLboDense = (kXfM / 8) * 128;
+constexpr uint32_t kXfLboPad = kXfLboDense + 64;
+constexpr uint32_t kXfAbytes = kXfLboPad * (kXfKc / 4);  // stage buffer of one of hi / lo (max)
 __host__ __device__ inline size_t xf_smem_bytes(uint32_t kpad, uint32_t npad) {
-    return size_t(2) * kpad * npad * 4 + size_t(2) * 2 * kXfM * kXfKc * 4 + 128 * 4;
+    return size_t(2) * kpad * npad * 4 + size_t(2) * 2 * kXfAbytes + 128 * 4;
 }
 
 // Prepared operand of W' (B[n][k], K-major core matrices): element (n, k) of the hi
@@ -141,7 +152,7 @@ __global__ void __launch_bounds__(kXfThreads, 1) k_tc_xform(TcXformParams p) {
     uint8_t* b_hi = xsm;
     uint8_t* b_lo = xsm + b_bytes;
     uint8_t* a_base = xsm + 2 * b_bytes;
-    constexpr uint32_t a_bytes = kXfM * kXfKc * 4;  // one of hi / lo of one stage
+    const uint32_t a_lbo = p.a_lbo, a_bytes = a_lbo * (kXfKc / 4);
     float* bias_sh = reinterpret_cast<float*>(a_base + 4 * a_bytes);
     const uint32_t ntiles = (p.r1 - p.r0 + kXfM - 1) / kXfM;
     const uint32_t my_tiles = blockIdx.x < ntiles ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
@@ -166,7 +177,7 @@ __global__ void __launch_bounds__(kXfThreads, 1) k_tc_xform(TcXformParams p) {
         bulk_g2s(b_lo, reinterpret_cast<const uint8_t*>(p.Bop) + b_bytes, b_bytes, &bars[4]);
     }
     const uint32_t idesc = umma_idesc_tf32(kXfM, npad);
-    const uint32_t a_lbo = (kXfM / 8) * 128, b_lbo = (npad / 8) * 128;
+    const uint32_t b_lbo = (npad / 8) * 128;
     const uint64_t pol = evict_first_policy();
 
     // A staging: thread handles float4 items idx = tid + 256 e (e < 4): row m = idx / 8,
