@@ -24,11 +24,16 @@ POWERLAW10M = dict(N=10_000_000, nnz=400_000_000 + 10_000_000, F=128, C=64, H=12
 
 
 def test_reddit_headline_footprint(gp, monkeypatch):
-    # the round-1 swap layout measured 41.7 GiB on the device (bench.py stage_stash_gib)
+    # the round-1 swap layout measured 41.7 GiB on the device (bench.py stage_stash_gib), without
+    # the per-epoch done-filtered backward CSR (8 B per entry, 0.86 GiB here) it did not have
+    monkeypatch.setenv("GP_BWD_CSR", "0")
     swap = _worst(gp, monkeypatch, "0", S=1, K=4, **REDDIT)
     assert abs(swap / 2**30 - 41.7) < 0.1
+    monkeypatch.delenv("GP_BWD_CSR")
     lean = _worst(gp, monkeypatch, "1", S=1, K=4, **REDDIT)
     assert lean < 0.62 * swap
+    monkeypatch.setenv("GP_BWD_CSR", "0")
+    assert 0.8 * 2**30 < lean - _worst(gp, monkeypatch, "1", S=1, K=4, **REDDIT) < 0.9 * 2**30
 
 
 @pytest.mark.parametrize("S", [2, 4, 8])
