@@ -2177,7 +2177,7 @@ struct Stage {
                 used_splits = std::min<uint32_t>(splits, uint32_t(num_sms));
                 TcPgradParams tp{nown, (nown + used_splits - 1) / used_splits, 0, pre, d.skw, d.dz, d.sout, d.din,
                                  d.dout, (d.dout + 15) / 16 * 16, ws, gb ? wsb : nullptr, id_rows};
-                const size_t smem = 2 * (2 * size_t(kTcM) * kTcKt * 4 + 2 * size_t(tp.npad) * kTcKt * 4);
+                const size_t smem = tc_pgrad_smem(tp.npad);
                 dim3 grid(used_splits, ti, 1);
                 launch(GP_K_PGRAD, pg_bytes, pg_flops, 0, [&]() { k_pgrad_tc<<<grid, kTcThreads, smem, cs>>>(tp); });
             } else {

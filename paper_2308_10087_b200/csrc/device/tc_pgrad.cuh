@@ -27,6 +27,15 @@ namespace gp {
 constexpr int kTcThreads = 256;  // 8 warps stage operands; warps 0-3 read TMEM; one thread issues MMAs
 constexpr int kTcKt = 32;        // rows (K) per pipeline stage
 constexpr int kTcM = 128;        // M tile (rows of dW)
+// Stage layout strides: 8-row core-matrix groups every kTcSbo = 144 bytes (128 + 16), so the
+// 8 lanes of a quarter-warp, which write index quads q = 0..7 (indices 4q + j: group q / 2,
+// row 4 (q & 1) + j), start in 8 different 16-byte bank groups: conflict-free 128-bit stores
+// (with SBO = 128 they fell into 2 groups, a 4-way conflict on every stage store)
+constexpr uint32_t kTcSbo = 144;
+__host__ __device__ constexpr uint32_t tc_lbo(uint32_t rows) { return (rows / 8) * kTcSbo; }
+__host__ __device__ constexpr size_t tc_pgrad_smem(uint32_t npad) {
+    return size_t(2) * (2 * tc_lbo(kTcM) + 2 * tc_lbo(npad)) * (kTcKt / 4);
+}
 
 struct TcPgradParams {
     uint32_t n, rows_per_split;  // n = end row (exclusive); rows start at row0
@@ -152,7 +161,7 @@ __device__ __forceinline__ void tc_store(const TcItem& it, uint8_t* hi, uint8_t*
             h[e] = to_tf32(x);
             l[e] = to_tf32(x - h[e]);
         }
-        const uint32_t off = c * lbo + (m >> 3) * 128 + (m & 7) * 16;
+        const uint32_t off = c * lbo + (m >> 3) * kTcSbo + (m & 7) * 16;
         *reinterpret_cast<float4*>(hi + off) = make_float4(h[0], h[1], h[2], h[3]);
         *reinterpret_cast<float4*>(lo + off) = make_float4(l[0], l[1], l[2], l[3]);
     }
@@ -171,9 +180,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_pgrad_tc(TcPgradParams p) {
     const uint32_t rbeg = p.row0 + split * p.rows_per_split;
     const uint32_t rend = min(p.n, rbeg + p.rows_per_split);
     const uint32_t npad = p.npad;
-    const uint32_t a_bytes = kTcM * kTcKt * 4, b_bytes = npad * kTcKt * 4;
+    const uint32_t a_lbo = tc_lbo(kTcM), b_lbo = tc_lbo(npad);
+    const uint32_t a_bytes = a_lbo * (kTcKt / 4), b_bytes = b_lbo * (kTcKt / 4);
     const uint32_t stage_bytes = 2 * a_bytes + 2 * b_bytes;
-    const uint32_t a_lbo = (kTcM / 8) * 128, b_lbo = (npad / 8) * 128;
     // work items: A has 32 q x 8 c = 256 (one per thread); B has npad/4 q x 8 c
     const uint32_t a_q = tid & 31, a_c = tid >> 5;
     const uint32_t b_items = (npad / 4) * (kTcKt / 4);
@@ -228,10 +237,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_pgrad_tc(TcPgradParams p) {
             const uint32_t ah = smem_u32(a_hi), al = smem_u32(a_lo), bh = smem_u32(b_hi), bl = smem_u32(b_lo);
 #pragma unroll
             for (uint32_t s = 0; s < kTcKt / 8; ++s) {
-                const uint64_t dah = umma_desc(ah + 2 * s * a_lbo, a_lbo, 128);
-                const uint64_t dal = umma_desc(al + 2 * s * a_lbo, a_lbo, 128);
-                const uint64_t dbh = umma_desc(bh + 2 * s * b_lbo, b_lbo, 128);
-                const uint64_t dbl = umma_desc(bl + 2 * s * b_lbo, b_lbo, 128);
+                const uint64_t dah = umma_desc(ah + 2 * s * a_lbo, a_lbo, kTcSbo);
+                const uint64_t dal = umma_desc(al + 2 * s * a_lbo, a_lbo, kTcSbo);
+                const uint64_t dbh = umma_desc(bh + 2 * s * b_lbo, b_lbo, kTcSbo);
+                const uint64_t dbl = umma_desc(bl + 2 * s * b_lbo, b_lbo, kTcSbo);
                 const uint32_t first = (it == 0 && s == 0) ? 0u : 1u;
                 mma_tf32(tmem, dah, dbh, idesc, first);
                 mma_tf32(tmem, dah, dbl, idesc, 1u);

@@ -77,15 +77,14 @@ constexpr uint32_t kXfSmemMax = 200 * 1024;  // H = 128: 128 + 64 KB
 // (measured alternatives, Reddit shape, per K = 4 backward launch: this version 59 us;
 // two chunks of A in flight in registers, 59 us; a 2-6 deep cp.async raw ring with the
 // epilogue's dh0 rows prefetched across the chunk loop, 88 us)
-// A stage k-core stride (p.a_lbo): the dense 16 row groups (kXfLboDense), or + 64 bytes
-// (kXfLboPad) so k-cores kc and kc + 1 start in opposite halves of the 128-byte bank space
-// and a warp's 32 stores (4 rows x 8 k-cores) spread over all 8 bank groups (dense: an 8-way
-// conflict on every store). The padded stride is measured faster for large launches (K = 4:
-// 17.3 vs 19.2 ms forward, 13.1 vs 15.0 ms backward per epoch, epoch -0.8 %) but the K = 32
-// wavefront epoch is ~1 % slower with it despite faster kernels, so the engine picks it by
-// launch size (GP_XF_PAD)
+// A stage k-core stride (p.a_lbo): the dense 16 row groups (kXfLboDense), or + 16 bytes
+// (kXfLboPad). A 128-bit shared store is served a quarter-warp at a time; the 8 lanes of a
+// quarter hold one row's 8 k-cores, which with the dense stride all start in the same 16-byte
+// bank group (8-way conflict, 32 wavefronts per warp store). An odd multiple of 16 bytes per
+// k-core puts them in 8 different groups (4 wavefronts, the minimum for 512 bytes). The
+// engine picks the padded stride by launch size (GP_XF_PAD).
 constexpr uint32_t kXfLboDense = (kXfM / 8) * 128;
-constexpr uint32_t kXfLboPad = kXfLboDense + 64;
+constexpr uint32_t kXfLboPad = kXfLboDense + 16;
 constexpr uint32_t kXfAbytes = kXfLboPad * (kXfKc / 4);  // stage buffer of one of hi / lo (max)
 __host__ __device__ inline size_t xf_smem_bytes(uint32_t kpad, uint32_t npad) {
     return size_t(2) * kpad * npad * 4 + size_t(2) * 2 * kXfAbytes + 128 * 4;
