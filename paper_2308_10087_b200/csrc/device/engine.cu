@@ -390,9 +390,9 @@ struct Stage {
     // GP_TC_XFORM=1 (default): the GCN / GCNII row transforms (pre.W', dz.W'^T and their
     // epilogues) run on tcgen05 (3xTF32, fp32-level); 0: the bit-exact CUDA-core tiles
     bool use_tc_xform = true;
-    // GP_XF_PAD: launches of at least this many rows stage A with the padded k-core stride
-    // (tc_xform.cuh; 1 = always, 0 = never; default 16384: K = 4 chunks yes, K = 32 no)
-    uint32_t xf_pad_rows = 16384;
+    // GP_XF_PAD: launches of at least this many rows stage A with the padded (conflict-free)
+    // k-core stride (tc_xform.cuh); 1 (default) = always, 0 = never (the dense stride)
+    uint32_t xf_pad_rows = 0;
     bool tc_dense = true;  // GP_TC_DENSE=0: Dense layers keep the fused CUDA-core GEMV kernels
     bool state_restored = false;  // gp_set_history: the snapshot rows were loaded
     // lean layout, epoch t with t % fix_alpha == 0 (the next epoch refreshes the snapshot):
