@@ -389,7 +389,10 @@ def main():
             t0 = time.perf_counter()
             res = gp.train_pipeline(ds, chunk_of, 1, opt)
             e2e_s = time.perf_counter() - t0
-            h2d = (off.nbytes + cols.nbytes + vals.nbytes + chunk_of.nbytes + x.nbytes + lab.nbytes + sp.nbytes +
+            # train_pipeline ships the raw neighbour lists (u64 offsets, u32 neighbours); the
+            # normalised, renumbered CSR is built on the device from them (k_build_edges)
+            raw_graph = 8 * off.size + 4 * (cols.size - N)  # neighbours = normalised entries - self loops
+            h2d = (raw_graph + chunk_of.nbytes + x.nbytes + lab.nbytes + sp.nbytes +
                    sum(w.nbytes + b.nbytes for w, b in params))
             d2h = sum(w.nbytes + b.nbytes for w, b in res.params) + res.metrics.nbytes
         else:

@@ -216,6 +216,7 @@ def _L():
         "gp_destroy": (None, [vp]),
         "gp_last_error": (C.c_char_p, [vp]),
         "gp_upload_graph": (C.c_int, [vp, u64p, u32p, f32p, C.c_uint64, u32p]),
+        "gp_upload_graph_raw": (C.c_int, [vp, u64p, u32p, C.c_uint64, C.c_int, u32p]),
         "gp_share_graph": (C.c_int, [vp, vp]),
         "gp_upload_features": (C.c_int, [vp, f32p, C.c_uint32]),
         "gp_upload_labels": (C.c_int, [vp, u32p, u8p]),
@@ -809,6 +810,15 @@ class StageEngine:
         co = np.ascontiguousarray(chunk_of, np.uint32)
         _gp(_L().gp_upload_graph(self._h, _ptr(off, C.c_uint64), _ptr(c, C.c_uint32), _ptr(v, C.c_float),
                                  c.size, _ptr(co, C.c_uint32)), self._h)
+
+    def upload_graph_raw(self, offsets, neighbors, chunk_of, self_loops: bool = True):
+        """gp_upload_graph_raw: the graph's own CSR (Dataset.graph()); normalize_adjacency<float>
+        is applied while the packed CSR is built (on the device for large graphs)."""
+        off = np.ascontiguousarray(offsets, np.uint64)
+        nb = np.ascontiguousarray(neighbors, np.uint32)
+        co = np.ascontiguousarray(chunk_of, np.uint32)
+        _gp(_L().gp_upload_graph_raw(self._h, _ptr(off, C.c_uint64), _ptr(nb, C.c_uint32), nb.size,
+                                     int(self_loops), _ptr(co, C.c_uint32)), self._h)
 
     def share_graph(self, owner: "StageEngine"):
         _gp(_L().gp_share_graph(self._h, owner._h), self._h)

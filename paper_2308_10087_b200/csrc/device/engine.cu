@@ -393,6 +393,10 @@ struct Stage {
     // GP_XF_PAD: launches of at least this many rows stage A with the padded (conflict-free)
     // k-core stride (tc_xform.cuh); 1 (default) = always, 0 = never (the dense stride)
     uint32_t xf_pad_rows = 0;
+    // GP_GRAPH_BUILD: where a single-partition upload of raw neighbour lists packs the
+    // normalised CSR: "device" (k_build_edges), "host" (the builder hybrid groups and
+    // precomputed values always use), default: the device from 64 MB of packed entries
+    int graph_build = 0;  // 0 auto, 1 device, 2 host
     bool tc_dense = true;  // GP_TC_DENSE=0: Dense layers keep the fused CUDA-core GEMV kernels
     bool state_restored = false;  // gp_set_history: the snapshot rows were loaded
     // lean layout, epoch t with t % fix_alpha == 0 (the next epoch refreshes the snapshot):
@@ -666,6 +670,8 @@ struct Stage {
         if (const char* e = std::getenv("GP_WAVE")) wave_w = std::max(1, std::min(kMaxWave, std::atoi(e)));
         for (int w = 1; w < wave_w; ++w) GP_CUDA(cudaStreamCreateWithFlags(&cs_side[w], cudaStreamNonBlocking));
         if (const char* e = std::getenv("GP_REMASK_OVERLAP")) remask_overlap = std::atoi(e) != 0;
+        if (const char* e = std::getenv("GP_GRAPH_BUILD"))
+            graph_build = std::string(e) == "device" ? 1 : std::string(e) == "host" ? 2 : 0;
         if (const char* e = std::getenv("GP_XF_PAD")) {
             const long v = std::atol(e);
             xf_pad_rows = v == 0 ? UINT32_MAX : v == 1 ? 0u : uint32_t(v);
@@ -1250,8 +1256,103 @@ struct Stage {
         upload_graph_src(RawGraph{off, nbr, loops}, m2 + (loops ? n : 0), chunk_of);
     }
 
+    // Raw neighbour lists -> normalised, renumbered, packed CSR on the device (k_build_edges):
+    // the host only ships the raw lists (4 bytes per entry instead of 8, no per-entry host
+    // arithmetic); the renumbering and row pointers come from the host builder. Sets edges and
+    // hg->blk_nnz; throws like the host builder on a bad neighbour.
+    void build_edges_device(const RawGraph& src, HostGraph& h, const uint32_t* chunk_of, unsigned nth) {
+        const uint64_t m2 = src.off[n];
+        auto t_prev = std::chrono::steady_clock::now();
+        auto phase = [&](const char* what) {
+            if (!host_timing) return;
+            const auto now = std::chrono::steady_clock::now();
+            std::fprintf(stderr, "[gp graph] %-12s %.1f ms\n", what,
+                         std::chrono::duration<double, std::milli>(now - t_prev).count());
+            t_prev = now;
+        };
+        auto tmp = [&](size_t bytes) {
+            void* p = nullptr;
+            GP_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 16)));
+            return p;
+        };
+        struct Free {
+            std::vector<void*> v;
+            ~Free() {
+                for (void* p : v) cudaFree(p);
+            }
+        } fr;
+        auto* d_off = static_cast<uint64_t*>(tmp((size_t(n) + 1) * 8));
+        auto* d_nbr = static_cast<uint32_t*>(tmp(m2 * 4));
+        auto* d_inv = static_cast<uint32_t*>(tmp(size_t(n) * 4));
+        auto* d_perm = static_cast<uint32_t*>(tmp(size_t(n) * 4));
+        auto* d_chunk = static_cast<uint32_t*>(tmp(size_t(n) * 4));
+        auto* d_rp = static_cast<uint64_t*>(tmp((size_t(n) + 1) * 8));
+        auto* d_blk = static_cast<unsigned long long*>(tmp(size_t(K) * K * 8));
+        auto* d_bad = static_cast<uint32_t*>(tmp(4));
+        fr.v = {d_off, d_nbr, d_inv, d_perm, d_chunk, d_rp, d_blk, d_bad};
+        phase("alloc");
+        h2d_mt(d_nbr, src.nbr, m2 * 4, nth);
+        phase("h2d nbr");
+        GP_CUDA(cudaMemcpy(d_off, src.off, (size_t(n) + 1) * 8, cudaMemcpyHostToDevice));
+        GP_CUDA(cudaMemcpy(d_inv, inv.data(), size_t(n) * 4, cudaMemcpyHostToDevice));
+        GP_CUDA(cudaMemcpy(d_perm, perm.data(), size_t(n) * 4, cudaMemcpyHostToDevice));
+        GP_CUDA(cudaMemcpy(d_chunk, chunk_of, size_t(n) * 4, cudaMemcpyHostToDevice));
+        GP_CUDA(cudaMemcpy(d_rp, h.rp.data(), (size_t(n) + 1) * 8, cudaMemcpyHostToDevice));
+        GP_CUDA(cudaMemset(d_blk, 0, size_t(K) * K * 8));
+        GP_CUDA(cudaMemset(d_bad, 0, 4));
+        BuildEdgesParams p{d_off, d_nbr, d_inv, d_perm, d_chunk, d_rp, edges, d_blk, d_bad, n, K, src.loops ? 1u : 0u};
+        const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>((n + kWarpsPerBlock - 1) / kWarpsPerBlock,
+                                                                    uint32_t(num_sms) * 8));
+        k_build_edges<<<grid, kBlock, size_t(K) * K * 4, cs>>>(p);
+        GP_CUDA(cudaGetLastError());
+        uint32_t bad = 0;
+        std::vector<uint64_t> blk(size_t(K) * K);
+        GP_CUDA(cudaMemcpyAsync(&bad, d_bad, 4, cudaMemcpyDeviceToHost, cs));
+        GP_CUDA(cudaMemcpyAsync(blk.data(), d_blk, blk.size() * 8, cudaMemcpyDeviceToHost, cs));
+        GP_CUDA(cudaStreamSynchronize(cs));
+        phase("build");
+        if (bad) throw Error(GP_EINVAL, "CSR column out of range (or a self loop in the graph)");
+        h.blk_nnz = std::move(blk);
+    }
+
+    // h2d with the staging copies split over nth threads (large raw arrays)
+    void h2d_mt(void* dst, const void* src, size_t bytes, unsigned nth) {
+        if (bytes < (size_t(4) << 20) || nth < 2) return h2d(dst, src, bytes);
+        StagingLease lease;
+        char* const* h2d_stage = lease.buf;
+        for (int i = 0; i < 2; ++i)
+            if (!h2d_done[i]) GP_CUDA(cudaEventCreateWithFlags(&h2d_done[i], cudaEventDisableTiming));
+        const char* s8 = static_cast<const char*>(src);
+        char* d8 = static_cast<char*>(dst);
+        bool used[2] = {false, false};
+        for (size_t off = 0, j = 0; off < bytes; off += kStageChunk, ++j) {
+            const int b = int(j & 1);
+            const size_t len = std::min(kStageChunk, bytes - off);
+            if (used[b]) GP_CUDA(cudaEventSynchronize(h2d_done[b]));
+            const size_t part = (len / nth + 63) & ~size_t(63);
+            std::vector<std::thread> pool;
+            for (unsigned t = 0; t < nth; ++t) {
+                const size_t a = std::min(len, t * part), z = std::min(len, a + part);
+                if (a < z) pool.emplace_back([=]() { std::memcpy(h2d_stage[b] + a, s8 + off + a, z - a); });
+            }
+            for (auto& th : pool) th.join();
+            GP_CUDA(cudaMemcpyAsync(d8 + off, h2d_stage[b], len, cudaMemcpyHostToDevice, cs));
+            GP_CUDA(cudaEventRecord(h2d_done[b], cs));
+            used[b] = true;
+        }
+        GP_CUDA(cudaStreamSynchronize(cs));
+    }
+
     template <class Src>
     void upload_graph_src(const Src& src, uint64_t nz, const uint32_t* chunk_of) {
+        auto t_prev = std::chrono::steady_clock::now();
+        auto phase = [&](const char* what) {
+            if (!host_timing) return;
+            const auto now = std::chrono::steady_clock::now();
+            std::fprintf(stderr, "[gp upload] %-12s %.1f ms\n", what,
+                         std::chrono::duration<double, std::milli>(now - t_prev).count());
+            t_prev = now;
+        };
         if (G > 1 && part_host.size() != n) throw Error(GP_EINVAL, "hybrid: upload the partition first");
         auto partof = [&](uint32_t v) -> uint32_t { return G > 1 ? part_host[v] : 0u; };
         auto h = std::make_shared<HostGraph>();
@@ -1308,7 +1409,14 @@ struct Stage {
         // CSR entries per (row block (rank, chunk), column chunk): the entries a done-filtered
         // backward gather actually fetches, for the byte / flop accounting
         std::vector<std::atomic<uint64_t>> blk_nnz(size_t(G) * K * K);
-        stage_rows_h2d(edges, h->rp, nth, [&](uint32_t r, uint2* out) {
+        phase("renumber");
+        bool built = false;
+        if constexpr (std::is_same<Src, RawGraph>::value)
+            if (G == 1 && (graph_build == 1 || (graph_build == 0 && nz * 8 >= (size_t(64) << 20)))) {
+                build_edges_device(src, *h, chunk_of, nth);
+                built = true;
+            }
+        if (!built) stage_rows_h2d(edges, h->rp, nth, [&](uint32_t r, uint2* out) {
             const uint32_t v = inv[r];
             uint64_t w = 0;
             uint32_t per_chunk[kMaxChunks] = {};
@@ -1325,9 +1433,12 @@ struct Stage {
                 if (per_chunk[c]) blk_nnz[blk + c].fetch_add(per_chunk[c], std::memory_order_relaxed);
             if (!ok) bad = true;
         });
-        h->blk_nnz.resize(blk_nnz.size());
-        for (size_t i = 0; i < blk_nnz.size(); ++i) h->blk_nnz[i] = blk_nnz[i].load();
+        if (!built) {
+            h->blk_nnz.resize(blk_nnz.size());
+            for (size_t i = 0; i < blk_nnz.size(); ++i) h->blk_nnz[i] = blk_nnz[i].load();
+        }
         if (bad) throw Error(GP_EINVAL, "CSR column out of range (or a self loop in the graph)");
+        phase("entries");
         if (has_sage) {
             // mean / mean_t (graph.cpp:100-112, nn.hpp:85-98): the normalised rows
             // without the self loop, same renumbering and chunk bits
@@ -1369,8 +1480,10 @@ struct Stage {
         bstart = hg->bstart;
         build_halo();
         build_id_rows();
+        phase("rows");
         ensure_own_buffers();
         alloc_bwd_csr();
+        phase("buffers");
         graph_ready = true;
     }
 

@@ -827,6 +827,76 @@ __global__ void __launch_bounds__(kBlock) k_done_csr(const __grid_constant__ Don
     }
 }
 
+// Normalised adjacency of the renumbered graph built on the device from the raw neighbour
+// lists (normalize_adjacency<float> graph.cpp:68-98: w_vu = float(1 / sqrt(d_v d_u)) in double,
+// d = degree + 1 with the self loop, which goes before the first neighbour u > v; the
+// adjacency bundle nn.hpp:85-98). One warp per renumbered row r (v = inv[r]), 32 entries per
+// step: the same entries, order and bits as the host builder (upload_graph_src), which
+// remains the path for hybrid groups and precomputed values. Also counts the entries per
+// (row chunk, column chunk) for the done-filtered accounting, and flags a neighbour out of
+// range or equal to its row.
+struct BuildEdgesParams {
+    const uint64_t* off;    // raw offsets (original ids)
+    const uint32_t* nbr;    // raw neighbours
+    const uint32_t* inv;    // renumbered row -> original id
+    const uint32_t* perm;   // original id -> renumbered row
+    const uint32_t* chunk;  // original id -> chunk
+    const uint64_t* rp;     // renumbered row pointers (self loops included)
+    uint2* edges;
+    unsigned long long* blk;  // K x K entry counts
+    uint32_t* bad;
+    uint32_t n, K, loops;
+};
+
+__global__ void __launch_bounds__(kBlock) k_build_edges(BuildEdgesParams p) {
+    extern __shared__ unsigned int hist[];  // K x K per CTA
+    for (uint32_t i = threadIdx.x; i < p.K * p.K; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const uint32_t nw = gridDim.x * kWarpsPerBlock;
+    const double extra = p.loops ? 1.0 : 0.0;
+    for (uint32_t r = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5); r < p.n; r += nw) {
+        const uint32_t v = p.inv[r];
+        const uint64_t e0 = p.off[v], e1 = p.off[v + 1];
+        const double dv = double(e1 - e0) + extra;
+        const uint32_t cr = p.chunk[v];
+        const uint64_t base = p.rp[r];
+        bool placed = !p.loops;  // warp-uniform: the self loop is written
+        const uint2 self = make_uint2(r | (cr << kColBits), __float_as_uint(float(1.0 / sqrt(dv * dv))));
+        for (uint64_t b = e0; b < e1; b += 32) {
+            const uint64_t i = b + lane;
+            const bool in = i < e1;
+            const uint32_t u = in ? p.nbr[i] : 0u;
+            const bool ok = in && u < p.n && u != v;
+            if (__any_sync(kFull, in && !ok) && lane == 0) atomicOr(p.bad, 1u);
+            uint32_t shift = placed ? (p.loops ? 1u : 0u) : 0u;
+            if (!placed) {
+                const unsigned gt = __ballot_sync(kFull, ok && u > v);
+                if (gt) {
+                    const int first = __ffs(gt) - 1;
+                    if (lane == first) p.edges[base + (b - e0) + first] = self;
+                    shift = lane >= first ? 1u : 0u;
+                    placed = true;
+                }
+            }
+            uint32_t cu = 0xffffffffu;
+            if (ok) {
+                cu = p.chunk[u];
+                const double du = double(p.off[u + 1] - p.off[u]) + extra;
+                p.edges[base + (i - e0) + shift] =
+                    make_uint2(p.perm[u] | (cu << kColBits), __float_as_uint(float(1.0 / sqrt(dv * du))));
+            }
+            const unsigned grp = __match_any_sync(kFull, cu);
+            if (ok && lane == __ffs(grp) - 1) atomicAdd(&hist[cr * p.K + cu], __popc(grp));
+        }
+        if (!placed && lane == 0) p.edges[base + (e1 - e0)] = self;
+        if (p.loops && lane == 0) atomicAdd(&hist[cr * p.K + cr], 1u);
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < p.K * p.K; i += blockDim.x)
+        if (hist[i]) atomicAdd(&p.blk[i], (unsigned long long)hist[i]);
+}
+
 // group_weight_sync (engines_impl.hpp:102-128): rank 0 folds the group's
 // gradients in rank order, g = ((g0 + g1) + g2) + ..., one rounding per add.
 struct FoldParams {

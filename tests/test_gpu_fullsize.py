@@ -148,3 +148,37 @@ def test_reddit_shape_filtered_csr_equals_batch_filter(gp, K, monkeypatch):
     assert np.array_equal(base.train_loss, batch.train_loss)
     for (Wa, _), (Wb, _) in zip(base.params, batch.params):
         assert np.array_equal(Wa.view(np.uint32), Wb.view(np.uint32))
+
+
+def test_reddit_shape_device_graph_build_equals_host(gp, monkeypatch):
+    """train_pipeline ships the raw neighbour lists and k_build_edges normalises, renumbers and
+    packs them on the device (default for large graphs); the host builder (GP_GRAPH_BUILD=host)
+    gives the same entries, order and weights: bit-identical training at the Reddit shape."""
+    ds = gp.Dataset.synthetic_er(N, E2 / (N * (N - 1)), 1, F, C, 1)
+    model = gp.ModelConfig(kind=gp.ModelKind.GCNII, layers=4, hidden=H, dropout=0.5)
+    co = gp.make_chunks(ds, 4, 1)
+    opt = gp.TrainOptions(model=model, epochs=2, seed=1)
+    dev = gp.train_pipeline(ds, co, 1, opt)
+    monkeypatch.setenv("GP_GRAPH_BUILD", "host")
+    host = gp.train_pipeline(ds, co, 1, opt)
+    assert np.array_equal(dev.train_loss, host.train_loss)
+    for (Wa, _), (Wb, _) in zip(dev.params, host.params):
+        assert np.array_equal(Wa.view(np.uint32), Wb.view(np.uint32))
+
+
+@pytest.mark.parametrize("mode", ["device", "host"])
+def test_raw_graph_with_self_loop_is_rejected(gp, mode, monkeypatch):
+    """A self loop (or an out-of-range neighbour) in the raw lists is rejected by both builders,
+    like normalize_adjacency's input check."""
+    monkeypatch.setenv("GP_GRAPH_BUILD", mode)
+    ds = gp.Dataset.synthetic_er(300, 0.05, 1, 8, 3, 1)
+    off, nb, _ = ds.graph()
+    nb = nb.copy()
+    nb[int(off[5])] = 5  # vertex 5 lists itself
+    co = gp.make_chunks(ds, 2, 1)
+    specs = gp.build_layer_specs(gp.ModelConfig(kind=gp.ModelKind.GCN, layers=2, hidden=8), 8, 3)
+    eng = gp.StageEngine(specs=specs, num_vertices=300, num_chunks=2, stage=0, num_stages=1,
+                         layer_range=(0, 2), hidden=8, num_classes=3, dropout=0.5, seed=1)
+    with pytest.raises(gp.InvalidArgument):
+        eng.upload_graph_raw(off, nb, co, self_loops=True)
+    eng.close()

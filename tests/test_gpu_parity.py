@@ -223,11 +223,12 @@ VARIANTS = [(CC, {"GP_SPLIT": "0"}), ({}, {"GP_WAVE": "1"}), ({}, {"GP_OCC5": "0
             ({}, {"GP_LEAN": "0", "GP_MERGED_G": "0"}), (CC, {"GP_LEAN": "0", "GP_SPLIT": "0"}),
             (CC, {"GP_WAVE": "1"}), (CC, {"GP_LEAN": "0"}), ({}, {"GP_BWD_CSR": "0"}),
             (CC, {"GP_BWD_CSR": "0", "GP_SPLIT": "0"}), ({}, {"GP_REMASK_OVERLAP": "0"}),
-            ({}, {"GP_REMASK_OVERLAP": "0", "GP_WAVE": "1"}), ({}, {"GP_XF_PAD": "0"})]
+            ({}, {"GP_REMASK_OVERLAP": "0", "GP_WAVE": "1"}), ({}, {"GP_XF_PAD": "0"}),
+            ({}, {"GP_GRAPH_BUILD": "device"})]
 VARIANT_IDS = ["fused", "one_stream", "occ4", "simt_pgrad", "split_g", "split_g_fused", "swap_layout",
                "swap_layout_split_g", "swap_layout_fused", "cuda_core_one_stream", "cuda_core_swap_layout",
                "batch_filter", "batch_filter_fused", "remask_in_order", "remask_in_order_one_stream",
-               "xf_dense_stride"]
+               "xf_dense_stride", "device_graph_build"]
 
 
 @pytest.mark.parametrize("hist", [False, True], ids=["stale", "hist"])
