@@ -3107,7 +3107,7 @@ struct Stage {
         // remask_overlap, layers >= 1 are remasked on cs_prep; rm_ev[i] orders every chunk's
         // first write of G_i (the layer i-1 epilogue) and read of it after the remask.
         std::vector<cudaEvent_t> rm_ev(len, nullptr);
-        const bool ovl = remask_overlap && cs_prep && !sync;
+        const bool ovl = remask_overlap && cs_prep && !sync && !profiling;  // profiling: one launch at a time
         if (ovl) GP_CUDA(cudaStreamWaitEvent(cs_prep, record_event(), 0));
         for (uint32_t i = 0; i < len; ++i) {
             if (!L[i].agg) continue;
