@@ -452,3 +452,24 @@ def test_train_gcn16_arxivlike_20_epoch_curve(gp):
     res = _train_compare(gp, "train_gcn16_arxivlike_s2k8_20ep", ds, gp.ModelConfig(kind=0, layers=16, hidden=64),
                          2, 8, 6, 20, 61, loss_tol=1e-5, acc_tol=2e-3, param_abs_tol=5e-3, fix_alpha=10)
     assert res.metrics.shape[0] == 20
+
+
+@pytest.mark.parametrize("loops", [True, False], ids=["self_loops", "no_self_loops"])
+@pytest.mark.parametrize("K", [3, 64])
+def test_device_graph_build_equals_host_builder(gp, loops, K, monkeypatch):
+    """k_build_edges (GP_GRAPH_BUILD=device) against the host builder on a sparse graph with
+    isolated vertices (rows holding only the self loop, or nothing), self loops on and off, and
+    64 chunks (the largest done-set / per-chunk histogram): bit-identical training."""
+    ds = gp.Dataset.synthetic_er(700, 0.003, 5, 12, 4, 2)
+    off, _, _ = ds.graph()
+    assert (np.diff(off) == 0).any()  # isolated vertices present
+    co = gp.make_chunks(ds, K, 1)
+    model = gp.ModelConfig(kind=gp.ModelKind.GCNII, layers=4, hidden=16, self_loops=loops)
+    opt = gp.TrainOptions(model=model, epochs=4, seed=3, fix_alpha=2)
+    runs = {}
+    for mode in ("device", "host"):
+        monkeypatch.setenv("GP_GRAPH_BUILD", mode)
+        runs[mode] = gp.train_pipeline(ds, co, 2, opt)
+    np.testing.assert_array_equal(runs["device"].train_loss, runs["host"].train_loss)
+    for (Wa, _), (Wb, _) in zip(runs["device"].params, runs["host"].params):
+        assert np.array_equal(Wa.view(np.uint32), Wb.view(np.uint32))
