@@ -154,7 +154,8 @@ gp_status gp_upload_graph(gp_ctx* ctx, const uint64_t* offsets, const uint32_t* 
  * strictly ascending neighbours, no self loops): normalize_adjacency<float>
  * (graph.cpp:68-98) is applied row by row while the packed CSR is built, with the
  * same double-precision expression, so the uploaded matrix is bit-identical and no
- * N-sized host copy of it is made. num_neighbors = 2E. */
+ * N-sized host copy of it is made. Single-partition stages ship the raw lists and
+ * build the packed CSR on the device (GP_GRAPH_BUILD). num_neighbors = 2E. */
 gp_status gp_upload_graph_raw(gp_ctx* ctx, const uint64_t* offsets, const uint32_t* neighbors,
                               uint64_t num_neighbors, int self_loops, const uint32_t* chunk_of);
 /* Hybrid (train_hybrid, engines_impl.hpp:515-909, G > 1): the vertex partition
