@@ -32,6 +32,10 @@ constexpr int kTcM = 128;        // M tile (rows of dW)
 // row 4 (q & 1) + j), start in 8 different 16-byte bank groups: conflict-free 128-bit stores
 // (with SBO = 128 they fell into 2 groups, a 4-way conflict on every stage store)
 constexpr uint32_t kTcSbo = 144;
+#ifndef GP_PGRAD_PF
+#define GP_PGRAD_PF 2
+#endif
+constexpr int kTcPf = GP_PGRAD_PF;  // stages of operand loads in flight per thread
 __host__ __device__ constexpr uint32_t tc_lbo(uint32_t rows) { return (rows / 8) * kTcSbo; }
 __host__ __device__ constexpr size_t tc_pgrad_smem(uint32_t npad) {
     return size_t(2) * (2 * tc_lbo(kTcM) + 2 * tc_lbo(npad)) * (kTcKt / 4);
@@ -208,47 +212,59 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_pgrad_tc(TcPgradParams p) {
 
     float bcol[4] = {0.f, 0.f, 0.f, 0.f};
     const uint32_t nst = (rend > rbeg) ? (rend - rbeg + kTcKt - 1) / kTcKt : 0;
-    TcItem ia, ib;
-    if (nst > 0) {
-        tc_load(ia, p.pre, p.prestride, i0 + 4 * a_q, p.din, rbeg + 4 * a_c, rend, p.rows);
-        if (has_b) tc_load(ib, p.dz, p.dzstride, 4 * b_q, p.dout, rbeg + 4 * b_c, rend, p.rows);
-    }
-    uint32_t uses[2] = {0, 0};
-    for (uint32_t it = 0; it < nst; ++it) {
-        const uint32_t st = it & 1;
-        if (uses[st] > 0) mbar_wait(&bars[st], (uses[st] - 1) & 1);  // MMAs that read this stage are done
-        uint8_t* base = tsm + st * stage_bytes;
-        uint8_t* a_hi = base;
-        uint8_t* a_lo = base + a_bytes;
-        uint8_t* b_hi = base + 2 * a_bytes;
-        uint8_t* b_lo = base + 2 * a_bytes + b_bytes;
-        tc_store(ia, a_hi, a_lo, a_lbo, a_c, a_q, i0 + mvalid, i0 + 4 * a_q, nullptr);
-        if (has_b) tc_store(ib, b_hi, b_lo, b_lbo, b_c, b_q, p.dout, 4 * b_q, do_bias ? bcol : nullptr);
-        if (it + 1 < nst) {  // prefetch the next stage while this one is multiplied
-            const uint32_t r1 = rbeg + (it + 1) * kTcKt;
-            tc_load(ia, p.pre, p.prestride, i0 + 4 * a_q, p.din, r1 + 4 * a_c, rend, p.rows);
-            if (has_b) tc_load(ib, p.dz, p.dzstride, 4 * b_q, p.dout, r1 + 4 * b_c, rend, p.rows);
-        }
-        // generic-proxy smem writes -> visible to the tensor-core (async) proxy
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncthreads();
-        if (tid == 0) {
-            asm volatile("tcgen05.fence::after_thread_sync;");
-            const uint32_t ah = smem_u32(a_hi), al = smem_u32(a_lo), bh = smem_u32(b_hi), bl = smem_u32(b_lo);
+    // kTcPf stages of row loads in flight per thread (a register ring, statically indexed by
+    // unrolling the stage loop kTcPf times): the id-ordered rows are random 512-byte reads and
+    // the loop is bound by their latency (ncu: long-scoreboard stalls first, DRAM at 1.9 TB/s).
+    // Per Reddit epoch: 1 stage 8.14 ms, 2 stages 7.57, 4 stages 8.06 (244 registers)
+    TcItem ia[kTcPf], ib[kTcPf];
 #pragma unroll
-            for (uint32_t s = 0; s < kTcKt / 8; ++s) {
-                const uint64_t dah = umma_desc(ah + 2 * s * a_lbo, a_lbo, kTcSbo);
-                const uint64_t dal = umma_desc(al + 2 * s * a_lbo, a_lbo, kTcSbo);
-                const uint64_t dbh = umma_desc(bh + 2 * s * b_lbo, b_lbo, kTcSbo);
-                const uint64_t dbl = umma_desc(bl + 2 * s * b_lbo, b_lbo, kTcSbo);
-                const uint32_t first = (it == 0 && s == 0) ? 0u : 1u;
-                mma_tf32(tmem, dah, dbh, idesc, first);
-                mma_tf32(tmem, dah, dbl, idesc, 1u);
-                mma_tf32(tmem, dal, dbh, idesc, 1u);
-            }
-            umma_commit(&bars[st]);
+    for (int u = 0; u < kTcPf; ++u)
+        if (uint32_t(u) < nst) {
+            const uint32_t r1 = rbeg + u * kTcKt;
+            tc_load(ia[u], p.pre, p.prestride, i0 + 4 * a_q, p.din, r1 + 4 * a_c, rend, p.rows);
+            if (has_b) tc_load(ib[u], p.dz, p.dzstride, 4 * b_q, p.dout, r1 + 4 * b_c, rend, p.rows);
         }
-        ++uses[st];
+    uint32_t uses[2] = {0, 0};
+    for (uint32_t it0 = 0; it0 < nst; it0 += kTcPf) {
+#pragma unroll
+        for (int u = 0; u < kTcPf; ++u) {
+            const uint32_t it = it0 + u;
+            if (it >= nst) break;
+            const uint32_t st = it & 1;
+            if (uses[st] > 0) mbar_wait(&bars[st], (uses[st] - 1) & 1);  // MMAs that read this stage are done
+            uint8_t* base = tsm + st * stage_bytes;
+            uint8_t* a_hi = base;
+            uint8_t* a_lo = base + a_bytes;
+            uint8_t* b_hi = base + 2 * a_bytes;
+            uint8_t* b_lo = base + 2 * a_bytes + b_bytes;
+            tc_store(ia[u], a_hi, a_lo, a_lbo, a_c, a_q, i0 + mvalid, i0 + 4 * a_q, nullptr);
+            if (has_b) tc_store(ib[u], b_hi, b_lo, b_lbo, b_c, b_q, p.dout, 4 * b_q, do_bias ? bcol : nullptr);
+            if (it + kTcPf < nst) {  // refill the slot kTcPf stages ahead
+                const uint32_t r1 = rbeg + (it + kTcPf) * kTcKt;
+                tc_load(ia[u], p.pre, p.prestride, i0 + 4 * a_q, p.din, r1 + 4 * a_c, rend, p.rows);
+                if (has_b) tc_load(ib[u], p.dz, p.dzstride, 4 * b_q, p.dout, r1 + 4 * b_c, rend, p.rows);
+            }
+            // generic-proxy smem writes -> visible to the tensor-core (async) proxy
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncthreads();
+            if (tid == 0) {
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                const uint32_t ah = smem_u32(a_hi), al = smem_u32(a_lo), bh = smem_u32(b_hi), bl = smem_u32(b_lo);
+#pragma unroll
+                for (uint32_t s = 0; s < kTcKt / 8; ++s) {
+                    const uint64_t dah = umma_desc(ah + 2 * s * a_lbo, a_lbo, kTcSbo);
+                    const uint64_t dal = umma_desc(al + 2 * s * a_lbo, a_lbo, kTcSbo);
+                    const uint64_t dbh = umma_desc(bh + 2 * s * b_lbo, b_lbo, kTcSbo);
+                    const uint64_t dbl = umma_desc(bl + 2 * s * b_lbo, b_lbo, kTcSbo);
+                    const uint32_t first = (it == 0 && s == 0) ? 0u : 1u;
+                    mma_tf32(tmem, dah, dbh, idesc, first);
+                    mma_tf32(tmem, dah, dbl, idesc, 1u);
+                    mma_tf32(tmem, dal, dbh, idesc, 1u);
+                }
+                umma_commit(&bars[st]);
+            }
+            ++uses[st];
+        }
     }
     // bias partials: thread (b_q, b_c) summed columns 4b_q..+3 over its rows; fold the 8 k-cores
     if (do_bias) {
