@@ -71,7 +71,13 @@ struct TcXformParams {
 __host__ __device__ constexpr uint32_t xf_pad16(uint32_t x) { return (x + 15u) & ~15u; }
 __host__ __device__ constexpr uint32_t xf_pad8k(uint32_t x) { return (x + 7u) & ~7u; }
 
-constexpr uint32_t kXfSmemMax = 200 * 1024;  // H = 128: 128 + 64 KB
+constexpr uint32_t kXfSmemMax = 200 * 1024;
+#ifndef GP_XF_PF
+#define GP_XF_PF 3
+#endif
+// A chunks in flight per thread (K = 32 epoch: 3 -> 0.397-0.400 s, 2 -> 0.400-0.406, 1 -> 0.414-0.420;
+// no difference at K = 4; profiles/r2b_xform_prefetch_ab.txt)
+constexpr int kXfPf = GP_XF_PF;  // H = 128: 128 + 64 KB
 
 // shared memory: B hi/lo + 2 stages x (A hi, A lo) of 128 x 32 tf32 + bias
 // (measured alternatives, Reddit shape, per K = 4 backward launch: this version 59 us;
@@ -182,8 +188,10 @@ __global__ void __launch_bounds__(kXfThreads, 1) k_tc_xform(TcXformParams p) {
 
     // A staging: thread handles float4 items idx = tid + 256 e (e < 4): row m = idx / 8,
     // k-core kc = idx % 8 of the chunk (8 threads read one row's 128 contiguous bytes)
-    float4 reg[4];
-    auto load_chunk = [&](uint32_t tile, uint32_t c) {
+    // kXfPf A chunks in flight per thread: a register ring over the flattened (tile, chunk)
+    // sequence, statically indexed by unrolling the chunk loop kXfPf times
+    float4 ring[kXfPf][4];
+    auto load_chunk = [&](float4 (&reg)[4], uint32_t tile, uint32_t c) {
         const uint32_t row0 = p.r0 + tile * kXfM, k0 = c * kXfKc;
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
@@ -193,7 +201,7 @@ __global__ void __launch_bounds__(kXfThreads, 1) k_tc_xform(TcXformParams p) {
                                               : make_float4(0.f, 0.f, 0.f, 0.f);
         }
     };
-    auto store_chunk = [&](uint32_t st) {
+    auto store_chunk = [&](const float4 (&reg)[4], uint32_t st) {
         uint8_t* hi = a_base + st * 2 * a_bytes;
         uint8_t* lo = hi + a_bytes;
 #pragma unroll
@@ -290,17 +298,21 @@ __global__ void __launch_bounds__(kXfThreads, 1) k_tc_xform(TcXformParams p) {
         asm volatile("tcgen05.fence::before_thread_sync;");
     };
 
-    uint32_t g = 0;  // A chunks staged so far (stage = g & 1)
-    if (my_tiles > 0) load_chunk(blockIdx.x, 0);
-    for (uint32_t j = 0; j < my_tiles; ++j) {
-        const uint32_t tile = blockIdx.x + j * gridDim.x, acc = j & 1;
-        for (uint32_t c = 0; c < nchunks; ++c, ++g) {
+    const uint32_t total = my_tiles * nchunks;  // A chunks this CTA stages (stage = g & 1)
+    auto chunk_at = [&](float4 (&reg)[4], uint32_t g) { load_chunk(reg, blockIdx.x + (g / nchunks) * gridDim.x, g % nchunks); };
+#pragma unroll
+    for (int u = 0; u < kXfPf; ++u)
+        if (uint32_t(u) < total) chunk_at(ring[u], u);
+    for (uint32_t g0 = 0; g0 < total; g0 += kXfPf) {
+#pragma unroll
+        for (int u = 0; u < kXfPf; ++u) {
+            const uint32_t g = g0 + u;
+            if (g >= total) break;
+            const uint32_t j = g / nchunks, c = g % nchunks, acc = j & 1;
             const uint32_t st = g & 1;
             if (g >= 2) mbar_wait(&bars[st], ((g >> 1) - 1) & 1);  // the MMAs that read this stage are done
-            store_chunk(st);
-            // issue the next chunk's loads (this tile's next chunk or the next tile's first)
-            if (c + 1 < nchunks) load_chunk(tile, c + 1);
-            else if (j + 1 < my_tiles) load_chunk(tile + gridDim.x, 0);
+            store_chunk(ring[u], st);
+            if (g + kXfPf < total) chunk_at(ring[u], g + kXfPf);  // refill the slot kXfPf chunks ahead
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncthreads();
             if (tid == 0) {
@@ -325,8 +337,8 @@ __global__ void __launch_bounds__(kXfThreads, 1) k_tc_xform(TcXformParams p) {
                 umma_commit(&bars[st]);
                 if (c + 1 == nchunks) umma_commit(&bars[2 + acc]);  // tile j's accumulator is complete
             }
+            if (c + 1 == nchunks && j > 0) epilogue(j - 1);  // overlaps tile j's MMAs
         }
-        if (j > 0) epilogue(j - 1);  // overlaps tile j's MMAs
     }
     if (my_tiles > 0) epilogue(my_tiles - 1);
     __syncthreads();
