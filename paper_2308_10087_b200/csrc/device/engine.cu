@@ -670,6 +670,7 @@ struct Stage {
         if (const char* e = std::getenv("GP_WAVE")) wave_w = std::max(1, std::min(kMaxWave, std::atoi(e)));
         for (int w = 1; w < wave_w; ++w) GP_CUDA(cudaStreamCreateWithFlags(&cs_side[w], cudaStreamNonBlocking));
         if (const char* e = std::getenv("GP_REMASK_OVERLAP")) remask_overlap = std::atoi(e) != 0;
+        if (const char* e = std::getenv("GP_FUSED_STEP")) fused_step = std::atoi(e) != 0;
         if (const char* e = std::getenv("GP_GRAPH_BUILD"))
             graph_build = std::string(e) == "device" ? 1 : std::string(e) == "host" ? 2 : 0;
         if (const char* e = std::getenv("GP_XF_PAD")) {
@@ -1298,8 +1299,9 @@ struct Stage {
         GP_CUDA(cudaMemcpy(d_perm, perm.data(), size_t(n) * 4, cudaMemcpyHostToDevice));
         GP_CUDA(cudaMemcpy(d_chunk, chunk_of, size_t(n) * 4, cudaMemcpyHostToDevice));
         GP_CUDA(cudaMemcpy(d_rp, h.rp.data(), (size_t(n) + 1) * 8, cudaMemcpyHostToDevice));
-        GP_CUDA(cudaMemset(d_blk, 0, size_t(K) * K * 8));
-        GP_CUDA(cudaMemset(d_bad, 0, 4));
+        GP_CUDA(cudaMemsetAsync(d_blk, 0, size_t(K) * K * 8, cs));
+        GP_CUDA(cudaMemsetAsync(d_bad, 0, 4, cs));
+        settle_uploads();  // the small copies above went through the legacy stream
         BuildEdgesParams p{d_off, d_nbr, d_inv, d_perm, d_chunk, d_rp, edges, d_blk, d_bad, n, K, src.loops ? 1u : 0u};
         const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>((n + kWarpsPerBlock - 1) / kWarpsPerBlock,
                                                                     uint32_t(num_sms) * 8));
@@ -1483,6 +1485,7 @@ struct Stage {
         phase("rows");
         ensure_own_buffers();
         alloc_bwd_csr();
+        settle_uploads();
         phase("buffers");
         graph_ready = true;
     }
@@ -1603,6 +1606,7 @@ struct Stage {
         build_id_rows();
         ensure_own_buffers();
         alloc_bwd_csr();
+        settle_uploads();
         graph_ready = true;
     }
 
@@ -1622,6 +1626,7 @@ struct Stage {
             std::memcpy(out, x + size_t(inv[r]) * f, size_t(f) * 4);
             std::memset(out + f, 0, size_t(sx - f) * 4);
         });
+        settle_uploads();
         x_ready = true;
     }
 
@@ -1644,6 +1649,7 @@ struct Stage {
         if (!split) split = dalloc<uint8_t>(n, false);
         GP_CUDA(cudaMemcpy(labels, hl.data(), size_t(n) * 4, cudaMemcpyHostToDevice));
         GP_CUDA(cudaMemcpy(split, hs.data(), n, cudaMemcpyHostToDevice));
+        settle_uploads();
         labels_ready = true;
     }
 
@@ -1739,16 +1745,22 @@ struct Stage {
         return x;
     }
 
+    // A cudaMemcpy from pageable host memory may return before its DMA has landed, and the
+    // engine's streams are non-blocking (not ordered after the legacy stream): every upload
+    // entry point waits for its legacy-stream copies before returning, so no kernel can read a
+    // buffer whose upload is still in flight.
+    void settle_uploads() { GP_CUDA(cudaStreamSynchronize(cudaStreamLegacy)); }
+
     void set_params(uint32_t l, const float* W, const float* b) {
         GP_CUDA(cudaSetDevice(device));
         auto& d = layer(l);
+        if (d.b && !b) throw Error(GP_EINVAL, "layer has a bias");
+        GP_CUDA(cudaStreamSynchronize(cs));
         GP_CUDA(cudaMemcpy(d.W, W, size_t(d.kin) * d.dout * 4, cudaMemcpyHostToDevice));
+        if (d.b) GP_CUDA(cudaMemcpy(d.b, b, size_t(d.dout) * 4, cudaMemcpyHostToDevice));
+        settle_uploads();  // transpose_w reads W on cs
         transpose_w(d);
         GP_CUDA(cudaStreamSynchronize(cs));
-        if (d.b) {
-            if (!b) throw Error(GP_EINVAL, "layer has a bias");
-            GP_CUDA(cudaMemcpy(d.b, b, size_t(d.dout) * 4, cudaMemcpyHostToDevice));
-        }
     }
 
     void get_grads(uint32_t l, float* W, float* b) {
@@ -1784,6 +1796,7 @@ struct Stage {
             GP_CUDA(cudaMemcpy(d.mb, mb, size_t(d.dout) * 4, cudaMemcpyHostToDevice));
             GP_CUDA(cudaMemcpy(d.vb, vb, size_t(d.dout) * 4, cudaMemcpyHostToDevice));
         }
+        settle_uploads();
         step = t;
     }
 
@@ -2308,7 +2321,49 @@ struct Stage {
         }
     }
 
+    // GP_FUSED_STEP=1 (default): the optimizer step and the derived weight copies of all
+    // non-SageConv layers in one k_param_step launch (was 4-5 launches per layer)
+    bool fused_step = true;
+    StepLayer* step_table = nullptr;
+    uint32_t step_max = 0;
+    // the per-layer descriptor table of k_param_step, built at engine setup (gp_create), not
+    // inside an epoch
+    void build_step_table() {
+        if (step_table || len == 0) return;
+        std::vector<StepLayer> t(len);
+        for (uint32_t i = 0; i < len; ++i) {
+            auto& d = L[i];
+            const bool g2 = d.spec.kind == GP_GCN2CONV && !tc_mix_epi;
+            t[i] = StepLayer{d.W, d.gW, d.mW, d.vW, d.WT, d.b, d.gb, d.mb, d.vb, d.tc ? d.xf_fwd : nullptr,
+                             d.tc ? d.xf_bwd : nullptr, d.din, d.dout, g2 ? 1u : 0u, float(d.spec.beta),
+                             1.f - float(d.spec.beta)};
+            step_max = std::max(step_max, d.din * d.dout + (d.b ? d.dout : 0u));
+        }
+        step_table = dalloc<StepLayer>(len, false);
+        GP_CUDA(cudaMemcpyAsync(step_table, t.data(), t.size() * sizeof(StepLayer), cudaMemcpyHostToDevice, cs));
+        GP_CUDA(cudaStreamSynchronize(cs));  // t is a host temporary
+    }
     void adam_all(double c1d, double c2d) {
+        bool any_sage = false;
+        for (auto& d : L) any_sage |= d.sage;
+        if (fused_step && !any_sage && len > 0 && len <= 65535) {
+            if (!step_table) build_step_table();
+            AdamParams a{};
+            a.sgd = cfg.optimizer == 1;
+            a.lr = float(cfg.lr);
+            a.b1 = float(cfg.beta1);
+            a.b2 = float(cfg.beta2);
+            a.omb1 = 1.f - a.b1;
+            a.omb2 = 1.f - a.b2;
+            a.eps = float(cfg.eps);
+            a.c1 = float(c1d);
+            a.c2 = float(c2d);
+            double elems = 0;
+            for (auto& d : L) elems += double(d.din) * d.dout + (d.b ? d.dout : 0);
+            const dim3 grid(std::min<uint32_t>((step_max + 255) / 256, 1024u), len);
+            launch(GP_K_OPTIM, elems * 36.0, 0, 0, [&]() { k_param_step<<<grid, 256, 0, cs>>>(step_table, a); });
+            return;
+        }
         for (uint32_t i = 0; i < len; ++i) {
             auto& d = L[i];
             AdamParams a{};
@@ -3416,6 +3471,7 @@ struct Stage {
         // swap layout: both halves, so whichever the next epoch's rule picks holds them
         for (float* dst : {hb.snap, lean ? nullptr : hb.cur})
             if (dst) GP_CUDA(cudaMemcpy(dst, tmp.data(), tmp.size() * 4, cudaMemcpyHostToDevice));
+        settle_uploads();
         state_restored = true;
     }
 

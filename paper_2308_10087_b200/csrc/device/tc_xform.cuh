@@ -346,4 +346,60 @@ __global__ void __launch_bounds__(kXfThreads, 1) k_tc_xform(TcXformParams p) {
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
 }
 
+// The whole optimizer step of a stage's GCN / GCNII / Dense layers in one launch
+// (Optimizer::step nn.hpp:456-467 per parameter, then the derived copies the next epoch
+// reads): per weight element the same Adam (or SGD) arithmetic as k_adam, then W^T
+// (k_transpose) and, for tcgen05 layers, the element's hi / lo entries of the prepared
+// forward and backward operands (k_tc_prep; their zero padding was written by the first
+// k_tc_prep and never changes). blockIdx.y = layer; bias elements follow the weights.
+struct StepLayer {
+    float *W, *gW, *mW, *vW, *WT;
+    float *b, *gb, *mb, *vb;
+    float *xf_fwd, *xf_bwd;  // null: not a tcgen05 layer
+    uint32_t din, dout, g2;
+    float beta, omb;
+};
+
+__global__ void __launch_bounds__(256) k_param_step(const StepLayer* __restrict__ layers, AdamParams a) {
+    const StepLayer L = layers[blockIdx.y];
+    const uint32_t nw = L.din * L.dout, nb = L.b ? L.dout : 0u;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nw + nb; i += gridDim.x * blockDim.x) {
+        const bool isw = i < nw;
+        const uint32_t e = isw ? i : i - nw;
+        float* P = isw ? L.W : L.b;
+        const float g = (isw ? L.gW : L.gb)[e];
+        float w;
+        if (a.sgd) {
+            w = __fsub_rn(P[e], __fmul_rn(a.lr, g));
+        } else {
+            float* M = isw ? L.mW : L.mb;
+            float* V = isw ? L.vW : L.vb;
+            const float m = __fadd_rn(__fmul_rn(a.b1, M[e]), __fmul_rn(a.omb1, g));
+            const float v = __fadd_rn(__fmul_rn(a.b2, V[e]), __fmul_rn(__fmul_rn(a.omb2, g), g));
+            M[e] = m;
+            V[e] = v;
+            const float mhat = __fdiv_rn(m, a.c1);
+            const float vhat = __fdiv_rn(v, a.c2);
+            w = __fsub_rn(P[e], __fdiv_rn(__fmul_rn(a.lr, mhat), __fadd_rn(__fsqrt_rn(vhat), a.eps)));
+        }
+        P[e] = w;
+        if (!isw) continue;
+        const uint32_t r = e / L.dout, c = e % L.dout;  // W[r][c], r < din, c < dout
+        L.WT[size_t(c) * L.din + r] = w;
+        if (!L.xf_fwd) continue;
+        // forward operand: B[n = c][k = r] = W'[r][c] (kpad = pad8(din), npad = pad16(dout));
+        // backward: B[n = r][k = c] = W'[r][c] (kpad = pad8(dout), npad = pad16(din))
+        const float wp = L.g2 ? __fadd_rn(__fmul_rn(L.beta, w), r == c ? L.omb : 0.f) : w;
+        const float hi = to_tf32(wp), lo = to_tf32(__fsub_rn(wp, hi));
+        const uint32_t kpf = xf_pad8k(L.din), npf = xf_pad16(L.dout);
+        const size_t of = size_t(r >> 2) * npf * 4 + (c >> 3) * 32 + (c & 7) * 4 + (r & 3);
+        L.xf_fwd[of] = hi;
+        L.xf_fwd[size_t(kpf) * npf + of] = lo;
+        const uint32_t kpb = xf_pad8k(L.dout), npb = xf_pad16(L.din);
+        const size_t ob = size_t(c >> 2) * npb * 4 + (r >> 3) * 32 + (r & 7) * 4 + (c & 3);
+        L.xf_bwd[ob] = hi;
+        L.xf_bwd[size_t(kpb) * npb + ob] = lo;
+    }
+}
+
 }  // namespace gp

@@ -224,11 +224,11 @@ VARIANTS = [(CC, {"GP_SPLIT": "0"}), ({}, {"GP_WAVE": "1"}), ({}, {"GP_OCC5": "0
             (CC, {"GP_WAVE": "1"}), (CC, {"GP_LEAN": "0"}), ({}, {"GP_BWD_CSR": "0"}),
             (CC, {"GP_BWD_CSR": "0", "GP_SPLIT": "0"}), ({}, {"GP_REMASK_OVERLAP": "0"}),
             ({}, {"GP_REMASK_OVERLAP": "0", "GP_WAVE": "1"}), ({}, {"GP_XF_PAD": "0"}),
-            ({}, {"GP_GRAPH_BUILD": "device"})]
+            ({}, {"GP_GRAPH_BUILD": "device"}), ({}, {"GP_FUSED_STEP": "0"})]
 VARIANT_IDS = ["fused", "one_stream", "occ4", "simt_pgrad", "split_g", "split_g_fused", "swap_layout",
                "swap_layout_split_g", "swap_layout_fused", "cuda_core_one_stream", "cuda_core_swap_layout",
                "batch_filter", "batch_filter_fused", "remask_in_order", "remask_in_order_one_stream",
-               "xf_dense_stride", "device_graph_build"]
+               "xf_dense_stride", "device_graph_build", "per_layer_step"]
 
 
 @pytest.mark.parametrize("hist", [False, True], ids=["stale", "hist"])
@@ -473,3 +473,25 @@ def test_device_graph_build_equals_host_builder(gp, loops, K, monkeypatch):
     np.testing.assert_array_equal(runs["device"].train_loss, runs["host"].train_loss)
     for (Wa, _), (Wb, _) in zip(runs["device"].params, runs["host"].params):
         assert np.array_equal(Wa.view(np.uint32), Wb.view(np.uint32))
+
+
+@pytest.mark.parametrize("optimizer", ["adam", "sgd"])
+@pytest.mark.parametrize("kind", [0, 2], ids=["gcn", "gcnii"])
+def test_fused_optimizer_step_equals_per_layer_kernels(gp, optimizer, kind, monkeypatch):
+    """k_param_step (one launch: Adam / SGD, W^T, tcgen05 operand preparation for every layer)
+    against the per-layer k_adam / k_transpose / k_tc_prep sequence (GP_FUSED_STEP=0), with the
+    CUDA-core transforms too (they read W^T): bit-identical training."""
+    ds = er500(gp)
+    co = gp.make_chunks(ds, 4, 3)
+    opt = gp.TrainOptions(model=gp.ModelConfig(kind=kind, layers=5, hidden=16), epochs=5, seed=4, fix_alpha=2,
+                          optimizer=optimizer, lr=0.01)
+    for tc in ("1", "0"):
+        monkeypatch.setenv("GP_TC_XFORM", tc)
+        monkeypatch.delenv("GP_FUSED_STEP", raising=False)
+        fused = gp.train_pipeline(ds, co, 2, opt)
+        monkeypatch.setenv("GP_FUSED_STEP", "0")
+        loop = gp.train_pipeline(ds, co, 2, opt)
+        np.testing.assert_array_equal(fused.train_loss, loop.train_loss)
+        for (Wa, ba), (Wb, bb) in zip(fused.params, loop.params):
+            assert np.array_equal(Wa.view(np.uint32), Wb.view(np.uint32))
+            assert np.array_equal(ba.view(np.uint32), bb.view(np.uint32))
