@@ -12,7 +12,6 @@
 //   stage messages    :690-724  -> Transport (local D2D, CUDA-IPC peer rings, or NCCL)
 #include <cuda.h>
 #include <cuda_runtime.h>
-#include <cub/device/device_scan.cuh>
 #include <nccl.h>  // types and the config initializer only; libnccl.so.2 is dlopen'ed
 #include <dlfcn.h>
 #include <unistd.h>
@@ -428,8 +427,8 @@ struct Stage {
     bool bwd_csr_ready = false;        // built for the current epoch's backward order
     uint64_t* rowptr_f = nullptr;
     uint2* edges_f = nullptr;
-    void* scan_tmp = nullptr;
-    size_t scan_tmp_bytes = 0;
+    unsigned long long* scan_tmp = nullptr;  // per-tile totals of the row-count scan
+    uint32_t scan_tiles = 0;
     uint32_t* id_rows = nullptr;       // own rows in ascending original id (reductions)
     std::vector<uint32_t> perm;        // original -> new (host)
     std::vector<uint32_t> inv;         // new -> original (host)
@@ -1513,9 +1512,8 @@ struct Stage {
         edges_f = dalloc<uint2>(std::max<uint64_t>(own_nnz, 1), false);
         bwd_csr_cap = own_nnz;
         const uint32_t items = own_end() - own_begin() + 1;
-        scan_tmp_bytes = 0;
-        GP_CUDA(cub::DeviceScan::InclusiveSum(nullptr, scan_tmp_bytes, rowptr_f, rowptr_f, items, cs));
-        scan_tmp = dalloc<char>(std::max<size_t>(scan_tmp_bytes, 16), false);
+        scan_tiles = (items + kScanTile - 1) / kScanTile;
+        scan_tmp = dalloc<unsigned long long>(scan_tiles, false);
     }
 
     // The epoch's done-filtered backward CSR: chunk order[kk] runs its backward with
@@ -1536,8 +1534,10 @@ struct Stage {
         const double eb = double(hg->rp[own_end()] - hg->rp[own_begin()]) * 8.0;
         launch(GP_K_BWD_AGG, eb + double(items) * 16.0, 0, 0, [&]() {
             k_done_csr<true><<<grid, kBlock, 0, cs>>>(p);
-            GP_CUDA(cub::DeviceScan::InclusiveSum(scan_tmp, scan_tmp_bytes, rowptr_f + own_begin(),
-                                                  rowptr_f + own_begin(), items, cs));
+            auto* v = reinterpret_cast<unsigned long long*>(rowptr_f + own_begin());
+            k_scan_tiles<<<scan_tiles, kScanThreads, 0, cs>>>(v, items, scan_tmp);
+            k_scan_totals<<<1, kScanThreads, 0, cs>>>(scan_tmp, scan_tiles);
+            k_scan_add<<<scan_tiles, kScanThreads, 0, cs>>>(v, items, scan_tmp);
             k_done_csr<false><<<grid, kBlock, 0, cs>>>(p);
         });
         bwd_csr_ready = true;

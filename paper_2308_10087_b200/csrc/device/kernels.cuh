@@ -827,6 +827,82 @@ __global__ void __launch_bounds__(kBlock) k_done_csr(const __grid_constant__ Don
     }
 }
 
+// In-place inclusive scan of u64 values (the filtered CSR's row counts -> row pointers):
+// k_scan_tiles scans tiles of kScanTile values per CTA and records each tile's total,
+// k_scan_totals turns the totals into exclusive tile offsets (one CTA, sequential over
+// chunks of 1024), k_scan_add adds them. Integer sums: the result is exact and order-free.
+constexpr uint32_t kScanThreads = 1024, kScanPer = 4, kScanTile = kScanThreads * kScanPer;
+
+__device__ __forceinline__ unsigned long long block_incl_scan(unsigned long long x, unsigned long long* warp_tot) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(kFull, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        unsigned long long t = lane < int(blockDim.x >> 5) ? warp_tot[lane] : 0ull;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long y = __shfl_up_sync(kFull, t, o);
+            if (lane >= o) t += y;
+        }
+        warp_tot[lane] = t;  // inclusive over warps
+    }
+    __syncthreads();
+    const unsigned long long r = x + (w > 0 ? warp_tot[w - 1] : 0ull);
+    __syncthreads();  // warp_tot is reused by the caller's next scan
+    return r;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_tiles(unsigned long long* v, uint32_t n,
+                                                             unsigned long long* totals) {
+    __shared__ unsigned long long wt[32];
+    const uint64_t base = uint64_t(blockIdx.x) * kScanTile + uint64_t(threadIdx.x) * kScanPer;
+    unsigned long long a[kScanPer], sum = 0;
+#pragma unroll
+    for (int q = 0; q < int(kScanPer); ++q) {
+        a[q] = base + q < n ? v[base + q] : 0ull;
+        sum += a[q];
+    }
+    const unsigned long long incl = block_incl_scan(sum, wt);
+    unsigned long long run = incl - sum;
+#pragma unroll
+    for (int q = 0; q < int(kScanPer); ++q) {
+        run += a[q];
+        if (base + q < n) v[base + q] = run;
+    }
+    if (threadIdx.x == blockDim.x - 1) totals[blockIdx.x] = incl;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_totals(unsigned long long* totals, uint32_t tiles) {
+    __shared__ unsigned long long wt[32];
+    unsigned long long carry = 0;
+    for (uint32_t c = 0; c < tiles; c += kScanThreads) {
+        const uint32_t i = c + threadIdx.x;
+        const unsigned long long x = i < tiles ? totals[i] : 0ull;
+        const unsigned long long incl = block_incl_scan(x, wt);
+        if (i < tiles) totals[i] = carry + incl - x;  // exclusive offset of tile i
+        __shared__ unsigned long long last;
+        if (threadIdx.x == kScanThreads - 1) last = incl;
+        __syncthreads();
+        carry += last;
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_add(unsigned long long* v, uint32_t n,
+                                                           const unsigned long long* offsets) {
+    if (blockIdx.x == 0) return;
+    const unsigned long long off = offsets[blockIdx.x];
+    const uint64_t base = uint64_t(blockIdx.x) * kScanTile + uint64_t(threadIdx.x) * kScanPer;
+#pragma unroll
+    for (int q = 0; q < int(kScanPer); ++q)
+        if (base + q < n) v[base + q] += off;
+}
+
 // Normalised adjacency of the renumbered graph built on the device from the raw neighbour
 // lists (normalize_adjacency<float> graph.cpp:68-98: w_vu = float(1 / sqrt(d_v d_u)) in double,
 // d = degree + 1 with the self loop, which goes before the first neighbour u > v; the
