@@ -179,9 +179,34 @@ struct RemaskParams {
     DropKey mask;
 };
 
+// Rows up to 128 wide: each warp handles kRemaskRows rows per step with all their loads
+// issued before the stores (4.35 vs 4.5-4.6 ms per Reddit epoch; the per-element dropout
+// hash, not the copy, bounds this kernel).
+constexpr uint32_t kRemaskRows = 4;
 __global__ void __launch_bounds__(kBlock) k_remask(RemaskParams p) {
     const int lane = threadIdx.x & 31;
     const uint32_t nw = gridDim.x * kWarpsPerBlock;
+    if (p.width <= 128) {
+        const uint32_t c0 = 4 * lane;
+        const bool act = c0 < p.width;
+        for (uint32_t v0 = p.r0 + (blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5)) * kRemaskRows; v0 < p.r1;
+             v0 += nw * kRemaskRows) {
+            float4 x[kRemaskRows];
+            uint32_t vo[kRemaskRows];
+#pragma unroll
+            for (uint32_t q = 0; q < kRemaskRows; ++q) {
+                const uint32_t v = v0 + q;
+                const bool in = act && v < p.r1;
+                vo[q] = v < p.r1 ? p.orig[v] : 0u;
+                x[q] = in ? ld4_rw(p.src + size_t(v) * p.sstride + c0) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (uint32_t q = 0; q < kRemaskRows; ++q)
+                if (act && v0 + q < p.r1)
+                    st4(p.dst + size_t(v0 + q) * p.dstride + c0, drop4(p.mask, vo[q], c0, p.width, x[q]));
+        }
+        return;
+    }
     for (uint32_t v = p.r0 + blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5); v < p.r1; v += nw) {
         const uint32_t vo = p.orig[v];
         for (uint32_t c0 = 4 * lane; c0 < p.width; c0 += 128) {
